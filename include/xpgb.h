@@ -1,0 +1,205 @@
+/*
+ * xpgb.h — C ABI of the B200-native expert-paging MoE layer (libxpgb.so).
+ *
+ * Drop-in boundary for the hot path of the reference package `xpg` 0.1.0
+ * (/root/reference/pkg/src/xpg).  The reference has no FFI: its boundary is
+ * duck-typed Python.  Every entry point below names the reference interface
+ * it replaces (file:line); the Python host layer `paper_2604_02715_b200`
+ * binds these with ctypes and re-exposes the reference's names.
+ *
+ * Conventions
+ *   - Plain C types only: pointers, sizes, ints.  Device pointers are
+ *     `void*`/`float*` into CUDA global memory of the context's device;
+ *     streams are `cudaStream_t` passed as `void*` (NULL = legacy stream).
+ *   - Every function returns an xpgb_status; on failure a message is
+ *     available from xpgb_last_error() (thread-local).
+ *   - Ids follow the reference: layer in [1, N], expert in [1, L],
+ *     kind 1 = GATE_UP (2F x H), kind 2 = DOWN (H x F), token index 0-based,
+ *     block ids 1-based per kind.
+ *   - One context per device; no hidden globals besides the error string.
+ */
+#ifndef XPGB_H_
+#define XPGB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define XPGB_ABI_VERSION 1
+
+/* Status codes map 1:1 onto the reference exception tree (errors.py:4-74). */
+typedef enum xpgb_status {
+  XPGB_OK = 0,
+  XPGB_ERR = 1,                    /* XpgError                */
+  XPGB_ERR_OUT_OF_RANGE = 2,       /* OutOfRangeError         */
+  XPGB_ERR_CONTAINER_FORMAT = 3,   /* ContainerFormatError    */
+  XPGB_ERR_DOUBLE_MAP = 4,         /* DoubleMapError          */
+  XPGB_ERR_POOL_EXHAUSTED = 5,     /* PoolExhaustedError      */
+  XPGB_ERR_NOT_MAPPED = 6,         /* NotMappedError          */
+  XPGB_ERR_PAGE_FAULT = 7,         /* PageFaultError          */
+  XPGB_ERR_CAPACITY_EXCEEDED = 8,  /* CapacityExceededError   */
+  XPGB_ERR_BACKEND_MISS = 9,       /* BackendMissError        */
+  XPGB_ERR_INFEASIBLE_CONFIG = 10, /* InfeasibleConfigError   */
+  XPGB_ERR_CONFIG = 11,            /* ConfigError             */
+  XPGB_ERR_DEADLOCK = 12,          /* DeadlockError           */
+  XPGB_ERR_CUDA = 13               /* CUDA failure -> XpgError */
+} xpgb_status;
+
+/* Page states (paging.py:41-45). */
+enum { XPGB_PAGE_UNMAPPED = 0, XPGB_PAGE_LOADING = 1, XPGB_PAGE_RESIDENT = 2, XPGB_PAGE_EVICTING = 3 };
+
+/* Pool geometry of a context. */
+enum {
+  XPGB_POOL_RING = 0,     /* reference PageTable: 2 x L blocks per kind (paging.py:115-122) */
+  XPGB_POOL_RESIDENT = 1  /* every tensor owns a block: resident_baseline (pipeline.py:216-230) */
+};
+
+/* ModelSpec (model.py:35-86).  H and F must be multiples of 8 (16-byte rows for TMA). */
+typedef struct xpgb_spec {
+  int32_t num_layers;        /* N >= 2 */
+  int32_t experts_per_layer; /* L >= 1 */
+  int32_t hidden_dim;        /* H */
+  int32_t intermediate_dim;  /* F */
+} xpgb_spec;
+
+typedef struct xpgb_ctx xpgb_ctx;
+
+/* Ordering-log record (pipeline.py:82-91); event codes below. */
+enum {
+  XPGB_EV_RECYCLE = 0,
+  XPGB_EV_LOAD_START = 1,
+  XPGB_EV_LOAD_DONE = 2,
+  XPGB_EV_COMPUTE_START = 3,
+  XPGB_EV_COMPUTE_DONE = 4,
+  XPGB_EV_RUN_BEGIN = 5
+};
+typedef struct xpgb_record {
+  int32_t t;                /* global order, from a device-side atomic counter */
+  int32_t event;            /* XPGB_EV_* */
+  int32_t iteration;
+  int32_t layer;
+  int32_t kind;             /* 1/2 for loads and recycles, -1 otherwise */
+  int32_t target_iteration; /* recycle only, else -1 */
+  int32_t target_layer;     /* recycle only, else -1 */
+  int32_t pad;
+  int64_t wall_ns;          /* %globaltimer when the record was written */
+} xpgb_record;
+
+/* StreamedRunner.run options (pipeline.py:307-331, 403-483). */
+typedef struct xpgb_run_opts {
+  int32_t iterations;        /* >= 1 */
+  int32_t tokens;            /* T (ForwardSpec.tokens_per_step) */
+  int32_t top_k;             /* ForwardSpec.top_k */
+  int32_t sequential;        /* 1: host-synchronous twin of mode="sequential"; 0: async streams ("threaded") */
+  uint64_t router_seed;      /* ForwardSpec.router_seed reduced mod 2^64 */
+  int32_t sabotage_iteration;/* (iteration, layer) whose RAW wait is skipped; 0 = none */
+  int32_t sabotage_layer;
+  const float* fetch_delay_s;   /* optional [N][L][2] seconds per tensor (delay_fn hook), host memory */
+  const float* compute_delay_s; /* optional [iterations][N] seconds (compute_delay_fn hook), host memory */
+  int32_t log_enable;        /* record the ordering log (default on) */
+  int32_t reserved;
+} xpgb_run_opts;
+
+typedef struct xpgb_report {
+  int64_t stall_ns;          /* compute stream blocked on RAW (RunReport.stall_seconds) */
+  int64_t war_wait_ns;       /* copy streams blocked on WAR (RunReport.war_wait_seconds) */
+  int64_t elapsed_ns;        /* first to last log record */
+  int64_t arena_peak_bytes;  /* PageTable.arena_peak_bytes */
+  int64_t h2d_bytes;         /* bytes paged in from the pinned host pool */
+  int64_t d2d_bytes;         /* bytes paged in from the device tier */
+  int64_t copy_busy_ns[2];   /* per copy stream: sum of load-start..load-done spans */
+  int32_t page_fault;        /* 1 if a compute read a non-resident page */
+  int32_t n_records;
+} xpgb_report;
+
+/* ---------------------------------------------------------------- basics */
+int xpgb_abi_version(void);
+const char* xpgb_last_error(void);
+/* Number of kernels this library launched since load (evidence counter). */
+int64_t xpgb_kernel_launches(void);
+
+/* Create a context on `device`.  pool = XPGB_POOL_RING (PageTable, paging.py:97-130)
+ * or XPGB_POOL_RESIDENT (resident_baseline).  max_tokens sizes workspaces (grows lazily). */
+int xpgb_create(const xpgb_spec* spec, int32_t device, int32_t pool, int32_t max_tokens, xpgb_ctx** out);
+int xpgb_destroy(xpgb_ctx* ctx);
+int xpgb_sync(xpgb_ctx* ctx);
+
+/* ---------------------------------------------------------------- storage
+ * WeightContainer payload (model.py:142-202) lives in a pinned host pool in
+ * container order; StorageHierarchy.fetch (storage.py:228-243) copies from it. */
+/* Allocate a pinned host pool of total_bytes; *host_ptr receives it for filling. */
+int xpgb_host_pool_alloc(xpgb_ctx* ctx, void** host_ptr, uint64_t* bytes);
+/* Use caller memory (cudaHostRegister'd here) as the host pool. */
+int xpgb_host_pool_register(xpgb_ctx* ctx, void* host_ptr, uint64_t bytes);
+/* Placement (plan_placement, storage.py:92-168): backend_of[((layer-1)*L + expert-1)*2 + kind-1]
+ * = 0 host tier, 1 device tier.  Device-tier tensors are staged into HBM once, here. */
+int xpgb_set_placement(xpgb_ctx* ctx, const uint8_t* backend_of);
+/* StorageHierarchy.fetch: copy the exact sigma bytes of a tensor into dst (device memory) on stream. */
+int xpgb_fetch(xpgb_ctx* ctx, int32_t layer, int32_t expert, int32_t kind, void* dst, uint64_t dst_bytes,
+               void* stream);
+
+/* ---------------------------------------------------------------- page table (paging.py:97-271) */
+int xpgb_pt_map(xpgb_ctx* ctx, int32_t layer, int32_t expert, int32_t kind, int32_t* block_id);
+int xpgb_pt_mark_resident(xpgb_ctx* ctx, int32_t layer, int32_t expert, int32_t kind);
+int xpgb_pt_unmap(xpgb_ctx* ctx, int32_t layer, int32_t expert, int32_t kind);
+int xpgb_pt_state(xpgb_ctx* ctx, int32_t layer, int32_t expert, int32_t kind, int32_t* state);
+int xpgb_pt_block(xpgb_ctx* ctx, int32_t layer, int32_t expert, int32_t kind, int32_t* block_id);
+int xpgb_pt_block_ptr(xpgb_ctx* ctx, int32_t kind, int32_t block_id, void** dptr, uint64_t* bytes);
+int xpgb_pt_loading_view(xpgb_ctx* ctx, int32_t layer, int32_t expert, int32_t kind, void** dptr,
+                         uint64_t* bytes);
+/* read_page: copy a resident page's bytes to host memory (PageFault otherwise). */
+int xpgb_pt_read(xpgb_ctx* ctx, int32_t layer, int32_t expert, int32_t kind, void* host_dst, uint64_t bytes);
+int xpgb_pt_peak_bytes(xpgb_ctx* ctx, uint64_t* peak);
+int xpgb_pt_pool_bytes(xpgb_ctx* ctx, uint64_t* bytes);
+int xpgb_pt_check_consistency(xpgb_ctx* ctx);
+/* Trace sink (paging.py:137-146): enable, then fetch newline-separated lines. */
+int xpgb_pt_trace_enable(xpgb_ctx* ctx, int32_t enable);
+int xpgb_pt_trace_get(xpgb_ctx* ctx, char* buf, uint64_t cap, uint64_t* needed);
+/* Map + fetch + mark_resident every tensor of the model (resident pools). */
+int xpgb_make_resident(xpgb_ctx* ctx);
+
+/* ---------------------------------------------------------------- compute */
+/* routed_experts (pipeline.py:154-170) for layers [layer_first, layer_first+layer_count):
+ * out_dev int32 [layer_count][T][min(top_k, L)], ascending 1-based ids. Stateless. */
+int xpgb_route(uint64_t seed, int32_t layer_first, int32_t layer_count, int32_t tokens, int32_t num_experts,
+               int32_t top_k, int32_t* out_dev, void* stream);
+/* layer_forward (pipeline.py:192-208) through the device page table: every
+ * routed expert of `layer` must be RESIDENT (else a page fault is recorded). */
+int xpgb_layer_forward(xpgb_ctx* ctx, int32_t layer, const float* x_dev, float* y_dev, int32_t tokens,
+                       int32_t top_k, uint64_t router_seed, void* stream);
+/* Device fault word: 0 = clean; fills a message like PageFaultError's. */
+int xpgb_fault_get(xpgb_ctx* ctx, int32_t* faulted, char* msg, uint64_t cap);
+int xpgb_fault_clear(xpgb_ctx* ctx);
+
+/* ---------------------------------------------------------------- schedule (pipeline.py:299-483) */
+/* StreamedRunner.run: x_dev/y_dev are [T][H] fp32 device buffers (y may alias x). */
+int xpgb_run(xpgb_ctx* ctx, const xpgb_run_opts* opts, const float* x_dev, float* y_dev, xpgb_report* rep);
+/* Ordering log of the last run (OrderingLog.records, pipeline.py:94-116). */
+int xpgb_log_get(xpgb_ctx* ctx, xpgb_record* out, int32_t cap, int32_t* n);
+
+/* ---------------------------------------------------------------- expert-parallel building blocks
+ * (no reference counterpart).  A context may own a contiguous expert
+ * shard [expert_first, expert_first+expert_count) of every layer. */
+int xpgb_set_expert_shard(xpgb_ctx* ctx, int32_t expert_first, int32_t expert_count);
+/* Grouped SwiGLU over rows already grouped by local expert:
+ * rows_dev bf16 [n_rows][H], offsets_dev int32 [expert_count+1] device row ranges,
+ * out_dev fp32 [n_rows][H] (expert output, unscaled).  Pages must be resident. */
+int xpgb_experts_forward(xpgb_ctx* ctx, int32_t layer, const void* rows_dev, const int32_t* offsets_dev,
+                         int32_t n_rows, float* out_dev, void* stream);
+
+/* Per-kernel device timing of the last layer_forward/run (ns, CUDA events). */
+typedef struct xpgb_kernel_times {
+  double route_ns, plan_ns, gather_ns, gate_up_ns, down_ns, combine_ns;
+  int64_t gate_up_bytes, down_bytes;  /* algorithmic bytes of the last launch */
+  int32_t down_splits, n_units_gate_up, n_units_down;
+} xpgb_kernel_times;
+int xpgb_profile_layer(xpgb_ctx* ctx, int32_t layer, const float* x_dev, float* y_dev, int32_t tokens,
+                       int32_t top_k, uint64_t router_seed, int32_t reps, xpgb_kernel_times* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XPGB_H_ */

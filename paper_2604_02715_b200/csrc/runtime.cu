@@ -1,0 +1,1192 @@
+// Runtime behind the C ABI (include/xpgb.h): context, pinned host pool,
+// device tier, PagedTensor (host bookkeeping + device slot table), page-in
+// engine on two copy streams with RAW/WAR event ordering, ordering log,
+// and the MoE forward pipeline.
+//
+// Reference mapping (xpg 0.1.0):
+//   PageTable            paging.py:97-271      -> PageTableHost + d_pt (device slot table)
+//   StorageHierarchy     storage.py:214-243    -> host pool (pinned) + device tier, fetch()
+//   StreamedRunner       pipeline.py:299-483   -> run(): copy streams = loaders, compute stream
+//   OrderingLog          pipeline.py:94-116    -> device log written by stream-ordered kernels
+//   layer_forward        pipeline.py:192-208   -> enqueue_forward(): route/plan/gather/GEMMs/combine
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <exception>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../../include/xpgb.h"
+#include "launch_count.h"
+#include "moe_kernels.cuh"
+#include "ptx_sm100.cuh"
+
+namespace xpgb {
+
+static std::atomic<long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+static thread_local std::string g_err;
+
+struct Err {
+  int code;
+  std::string msg;
+};
+
+static std::string fmt(const char* f, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, f);
+  vsnprintf(buf, sizeof(buf), f, ap);
+  va_end(ap);
+  return buf;
+}
+
+#define XFAIL(code, ...) throw Err{code, fmt(__VA_ARGS__)}
+#define CK(x)                                                                                  \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess) throw Err{XPGB_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+#define CKLAUNCH() CK(cudaGetLastError())
+
+template <class Fn>
+static int guard(Fn&& fn) {
+  try {
+    fn();
+    return XPGB_OK;
+  } catch (const Err& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return XPGB_ERR;
+  }
+}
+
+// --------------------------------------------------------------------------- tensor maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) XFAIL(XPGB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+// Row-major bf16 [rows][cols] -> box {64 cols, box_rows}, 128-B swizzle.
+static CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)kBK, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) XFAIL(XPGB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) rows=%llu cols=%llu", (int)r,
+                               (unsigned long long)rows, (unsigned long long)cols);
+  return m;
+}
+
+// --------------------------------------------------------------------------- small kernels
+
+struct PtOp {
+  int32_t* unmap_row;
+  int32_t unmap_n;
+  int32_t set_n;
+  int32_t* set_row;
+  xpgb_record* log;
+  int32_t* log_count;
+  int32_t log_cap;
+  int32_t n_rec;
+  int32_t rec[2][6];  // event, it, layer, kind, target_it, target_layer
+  int32_t vals[448];
+};
+static_assert(sizeof(PtOp) < 4000, "kernel parameter block too large");
+
+__device__ void write_record(xpgb_record* log, int32_t* count, int cap, const int32_t* r) {
+  const int t = atomicAdd(count, 1);
+  if (t < cap) {
+    xpgb_record rec;
+    rec.t = t;
+    rec.event = r[0];
+    rec.iteration = r[1];
+    rec.layer = r[2];
+    rec.kind = r[3];
+    rec.target_iteration = r[4];
+    rec.target_layer = r[5];
+    rec.pad = 0;
+    rec.wall_ns = (int64_t)globaltimer_ns();
+    log[t] = rec;
+    __threadfence();
+  }
+}
+
+// Stream-ordered page-table update + ordering-log append (copy streams and compute stream).
+__global__ void k_pt_op(PtOp op) {
+  if (threadIdx.x == 0 && op.log && op.n_rec > 0) write_record(op.log, op.log_count, op.log_cap, op.rec[0]);
+  __syncthreads();
+  for (int i = threadIdx.x; i < op.unmap_n; i += blockDim.x) op.unmap_row[i] = -1;
+  for (int i = threadIdx.x; i < op.set_n; i += blockDim.x) op.set_row[i] = op.vals[i];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0 && op.log && op.n_rec > 1) write_record(op.log, op.log_count, op.log_cap, op.rec[1]);
+}
+
+__global__ void k_sleep(uint64_t ns) {
+  const uint64_t t0 = globaltimer_ns();
+  while (globaltimer_ns() - t0 < ns) __nanosleep(20000);
+}
+
+// --------------------------------------------------------------------------- context
+
+static const char* state_name(int s) {
+  switch (s) {
+    case XPGB_PAGE_LOADING: return "loading";
+    case XPGB_PAGE_RESIDENT: return "resident";
+    case XPGB_PAGE_EVICTING: return "evicting";
+    default: return "unmapped";
+  }
+}
+
+struct Ctx {
+  int N, L, H, F;
+  int device;
+  int pool;
+  int e_first = 0, E = 0;  // expert shard
+  uint64_t s1, s2;         // sigma per kind
+  int num_sms = 148;
+
+  // device pool (arena): kind-1 blocks then kind-2 blocks (paging.py:115-122)
+  int blocks = 0;
+  uint8_t* arena = nullptr;
+  CUtensorMap map_gu{}, map_dn{};
+
+  // host pool (shard-local container order)
+  uint8_t* host = nullptr;
+  uint64_t host_bytes = 0;
+  bool host_owned = false, host_registered = false;
+
+  // device tier
+  std::vector<uint8_t> backend;  // [N*E][2] 0 host, 1 device
+  uint8_t* dev_tier = nullptr;
+  std::vector<int64_t> dev_off;  // [N*E][2] offset of the tensor in dev_tier or -1
+
+  // page table (host bookkeeping)
+  std::vector<int8_t> st[2];
+  std::vector<int32_t> blk[2];  // 1-based block or 0
+  std::vector<int32_t> owner[2];  // block -> page index or -1
+  std::set<int32_t> free_ids[2];
+  uint64_t bound = 0, peak = 0;
+  long long step = 0;
+  bool trace_on = false;
+  std::string trace;
+  int32_t* d_pt = nullptr;  // [2][N*E] device slot table
+
+  // streams / events
+  cudaStream_t s_copy[2] = {nullptr, nullptr};
+  cudaStream_t s_comp = nullptr;
+  cudaEvent_t ev_load[2][4], ev_comp[4], ev_begin, ev_end;
+
+  // workspace
+  int cap_T = 0, cap_kk = 0, cap_rows = 0, cap_splits = 8;
+  LayerWork work{};
+  int32_t* topk_single = nullptr;
+  int32_t* topk_all = nullptr;
+  int topk_all_cap = 0;
+  CUtensorMap map_xp{}, map_h{};
+  long long* d_fault = nullptr;
+
+  // log
+  xpgb_record* d_log = nullptr;
+  int32_t* d_log_count = nullptr;
+  int log_cap = 0;
+  std::vector<xpgb_record> last_log;
+
+  // profiling
+  bool prof = false;
+  cudaEvent_t pev[7];
+  xpgb_kernel_times last_times{};
+};
+
+static int page_index(Ctx* c, int layer, int expert, int kind) {
+  if (layer < 1 || layer > c->N) XFAIL(XPGB_ERR_OUT_OF_RANGE, "layer %d outside [1, %d]", layer, c->N);
+  if (expert < 1 || expert > c->L) XFAIL(XPGB_ERR_OUT_OF_RANGE, "expert %d outside [1, %d]", expert, c->L);
+  if (kind != 1 && kind != 2) XFAIL(XPGB_ERR_OUT_OF_RANGE, "unknown tensor kind %d", kind);
+  const int el = expert - 1 - c->e_first;
+  if (el < 0 || el >= c->E)
+    XFAIL(XPGB_ERR_OUT_OF_RANGE, "expert %d outside this shard [%d, %d]", expert, c->e_first + 1,
+          c->e_first + c->E);
+  return (layer - 1) * c->E + el;
+}
+
+static std::string tid_str(int layer, int expert, int kind) { return fmt("L%dE%dK%d", layer, expert, kind); }
+
+static uint64_t sigma_of(Ctx* c, int kind) { return kind == 1 ? c->s1 : c->s2; }
+
+static uint8_t* block_ptr(Ctx* c, int kind, int block1) {
+  return kind == 1 ? c->arena + (uint64_t)(block1 - 1) * c->s1
+                   : c->arena + (uint64_t)c->blocks * c->s1 + (uint64_t)(block1 - 1) * c->s2;
+}
+
+static void emit(Ctx* c, const char* ev, int layer, int expert, int kind, int block, const char* extra) {
+  if (!c->trace_on) return;
+  c->trace += fmt("event=%s layer=%d expert=%d kind=%d block=%d t=%lld", ev, layer, expert, kind, block, c->step);
+  if (extra && *extra) {
+    c->trace += " ";
+    c->trace += extra;
+  }
+  c->trace += "\n";
+}
+
+static void free_pools(Ctx* c) {
+  if (c->arena) cudaFree(c->arena);
+  if (c->d_pt) cudaFree(c->d_pt);
+  if (c->dev_tier) cudaFree(c->dev_tier);
+  c->arena = nullptr;
+  c->d_pt = nullptr;
+  c->dev_tier = nullptr;
+}
+
+static void init_pools(Ctx* c) {
+  free_pools(c);
+  c->blocks = (c->pool == XPGB_POOL_RING) ? 2 * c->E : c->N * c->E;
+  const uint64_t bytes = (uint64_t)c->blocks * (c->s1 + c->s2);
+  CK(cudaMalloc(&c->arena, bytes));
+  CK(cudaMemset(c->arena, 0, bytes));
+  const size_t pages = (size_t)c->N * c->E;
+  CK(cudaMalloc(&c->d_pt, 2 * pages * sizeof(int32_t)));
+  CK(cudaMemset(c->d_pt, 0xFF, 2 * pages * sizeof(int32_t)));
+  for (int k = 0; k < 2; ++k) {
+    c->st[k].assign(pages, XPGB_PAGE_UNMAPPED);
+    c->blk[k].assign(pages, 0);
+    c->owner[k].assign(c->blocks + 1, -1);
+    c->free_ids[k].clear();
+    for (int b = 1; b <= c->blocks; ++b) c->free_ids[k].insert(b);
+  }
+  c->bound = c->peak = 0;
+  c->step = 0;
+  c->backend.assign(pages * 2, 0);
+  c->dev_off.assign(pages * 2, -1);
+  c->map_gu = make_map(c->arena, (uint64_t)c->blocks * 2 * c->F, c->H, kBM);
+  c->map_dn = make_map(c->arena + (uint64_t)c->blocks * c->s1, (uint64_t)c->blocks * c->H, c->F, kBM);
+}
+
+static void ensure_log(Ctx* c, int cap) {
+  if (cap <= c->log_cap) {
+    CK(cudaMemset(c->d_log_count, 0, sizeof(int32_t)));
+    return;
+  }
+  if (c->d_log) cudaFree(c->d_log);
+  CK(cudaMalloc(&c->d_log, (size_t)cap * sizeof(xpgb_record)));
+  c->log_cap = cap;
+  CK(cudaMemset(c->d_log_count, 0, sizeof(int32_t)));
+}
+
+static void ensure_work(Ctx* c, int T, int kk) {
+  if (kk > kMaxTopK) XFAIL(XPGB_ERR_OUT_OF_RANGE, "top_k %d above the kernel limit %d", kk, kMaxTopK);
+  if (T <= c->cap_T && kk <= c->cap_kk && c->work.xp) return;
+  const int nT = std::max(T, std::max(c->cap_T, 16));
+  const int nkk = std::max(kk, c->cap_kk);
+  const int rows = nT * nkk;
+  LayerWork& w = c->work;
+  auto fr = [](void* p) { if (p) cudaFree(p); };
+  fr(w.pos); fr(w.offsets); fr(w.slot_gu); fr(w.slot_dn); fr(w.units1); fr(w.units2); fr(w.counters);
+  fr(w.xp); fr(w.hbuf); fr(w.part); fr(c->topk_single);
+  const int E = c->E;
+  const long long mt1 = (c->F + kBM - 1) / kBM, mt2 = (c->H + kBM - 1) / kBM;
+  const long long max_units1 = (E + rows / 32 + 1) * mt1;
+  const long long max_units2 = (E + rows / 32 + 1) * mt2 * c->cap_splits;
+  CK(cudaMalloc(&w.pos, (size_t)rows * 4));
+  CK(cudaMalloc(&w.offsets, (size_t)(E + 1) * 4));
+  CK(cudaMalloc(&w.slot_gu, (size_t)E * 4));
+  CK(cudaMalloc(&w.slot_dn, (size_t)E * 4));
+  CK(cudaMalloc(&w.units1, (size_t)max_units1 * sizeof(GemmUnit)));
+  CK(cudaMalloc(&w.units2, (size_t)max_units2 * sizeof(GemmUnit)));
+  CK(cudaMalloc(&w.counters, 16));
+  CK(cudaMalloc(&w.xp, (size_t)rows * c->H * 2));
+  CK(cudaMemset(w.xp, 0, (size_t)rows * c->H * 2));
+  CK(cudaMalloc(&w.hbuf, (size_t)rows * c->F * 2));
+  CK(cudaMemset(w.hbuf, 0, (size_t)rows * c->F * 2));
+  CK(cudaMalloc(&w.part, (size_t)c->cap_splits * rows * c->H * 4));
+  CK(cudaMalloc(&c->topk_single, (size_t)rows * 4));
+  w.fault = c->d_fault;
+  c->cap_T = nT;
+  c->cap_kk = nkk;
+  c->cap_rows = rows;
+  c->map_xp = make_map(w.xp, rows, c->H, kBoxRowsB);
+  c->map_h = make_map(w.hbuf, rows, c->F, kBoxRowsB);
+}
+
+static int pick_bn(int T) { return T <= 32 ? 32 : (T <= 64 ? 64 : 128); }
+
+// Split-K factor for the down projection: balance (units x splits) over the SMs.
+static int pick_splits(Ctx* c, int T, int kk, int bn) {
+  const int KB = (c->F + kBK - 1) / kBK;
+  const long long active = std::min<long long>(c->E, (long long)T * kk);
+  if (active <= 0) return 1;
+  const long long rows_per = std::max<long long>(1, ((long long)T * kk + active - 1) / active);
+  const long long tiles = active * ((c->H + kBM - 1) / kBM) * ((rows_per + bn - 1) / bn);
+  int best = 1;
+  double best_eff = -1;
+  for (int s = 1; s <= c->cap_splits; ++s) {
+    if (KB / s < 4) break;
+    const double work = (double)tiles * s / c->num_sms;
+    const double eff = work / std::ceil(work) * std::min(1.0, work);  // wave quantisation x fill
+    if (eff > best_eff + 0.02) { best_eff = eff; best = s; }
+  }
+  return best;
+}
+
+static void prof_rec(Ctx* c, int i, cudaStream_t s) {
+  if (c->prof) CK(cudaEventRecord(c->pev[i], s));
+}
+
+// layer_forward (pipeline.py:192-208) on `s`: y may alias x.
+static void enqueue_forward(Ctx* c, int layer, const float* x, float* y, int T, int top_k, uint64_t seed,
+                            const int32_t* topk, cudaStream_t s) {
+  const int kk = std::min(top_k, c->L);
+  ensure_work(c, T, kk);
+  if (T == 0) return;
+  LayerWork w = c->work;
+  prof_rec(c, 0, s);
+  if (topk == nullptr) {
+    launch_route(seed, layer, 1, T, c->L, top_k, c->topk_single, s);
+    CKLAUNCH();
+    topk = c->topk_single;
+  }
+  w.topk = const_cast<int32_t*>(topk);
+  const int bn = pick_bn(T);
+  const int splits = pick_splits(c, T, kk, bn);
+  const size_t pages = (size_t)c->N * c->E;
+  prof_rec(c, 1, s);
+  launch_plan(w, c->d_pt, c->d_pt + pages, layer, T, kk, c->e_first, c->E, c->F, c->H, bn, bn, splits, s);
+  CKLAUNCH();
+  prof_rec(c, 2, s);
+  launch_gather(w, x, T, kk, c->H, s);
+  CKLAUNCH();
+  prof_rec(c, 3, s);
+  launch_gate_up(c->map_gu, c->map_xp, w, c->F, c->H, bn, c->num_sms, s);
+  CKLAUNCH();
+  prof_rec(c, 4, s);
+  launch_down(c->map_dn, c->map_h, w, c->F, c->H, bn, splits, c->cap_rows, c->num_sms, s);
+  CKLAUNCH();
+  prof_rec(c, 5, s);
+  launch_combine(w, y, T, kk, c->H, splits, c->cap_rows, (float)(1.0 / top_k), s);
+  CKLAUNCH();
+  prof_rec(c, 6, s);
+  c->last_times.down_splits = splits;
+}
+
+// --------------------------------------------------------------------------- page table ops
+
+static int pt_map(Ctx* c, int layer, int expert, int kind) {
+  const int pi = page_index(c, layer, expert, kind);
+  const int k = kind - 1;
+  if (c->st[k][pi] != XPGB_PAGE_UNMAPPED || c->blk[k][pi] != 0)
+    XFAIL(XPGB_ERR_DOUBLE_MAP, "%s is already mapped (%s)", tid_str(layer, expert, kind).c_str(),
+          state_name(c->st[k][pi]));
+  if (c->free_ids[k].empty())
+    XFAIL(XPGB_ERR_POOL_EXHAUSTED, "no free kind-%d block for %s; protocol bug", kind,
+          tid_str(layer, expert, kind).c_str());
+  const int b = *c->free_ids[k].begin();  // lowest id first (paging.py:160-161)
+  c->free_ids[k].erase(c->free_ids[k].begin());
+  c->blk[k][pi] = b;
+  c->owner[k][b] = pi;
+  c->st[k][pi] = XPGB_PAGE_LOADING;
+  c->bound += sigma_of(c, kind);
+  c->peak = std::max(c->peak, c->bound);
+  c->step += 1;
+  emit(c, "map", layer, expert, kind, b, "");
+  return b;
+}
+
+static void pt_mark_resident(Ctx* c, int layer, int expert, int kind) {
+  const int pi = page_index(c, layer, expert, kind);
+  const int k = kind - 1;
+  if (c->st[k][pi] != XPGB_PAGE_LOADING)
+    XFAIL(XPGB_ERR_NOT_MAPPED, "%s is %s, expected loading", tid_str(layer, expert, kind).c_str(),
+          state_name(c->st[k][pi]));
+  c->st[k][pi] = XPGB_PAGE_RESIDENT;
+  c->step += 1;
+  emit(c, "state", layer, expert, kind, c->blk[k][pi], "state=resident");
+}
+
+static void pt_unmap(Ctx* c, int layer, int expert, int kind) {
+  const int pi = page_index(c, layer, expert, kind);
+  const int k = kind - 1;
+  const int b = c->blk[k][pi];
+  if (b == 0 || (c->st[k][pi] != XPGB_PAGE_RESIDENT && c->st[k][pi] != XPGB_PAGE_EVICTING))
+    XFAIL(XPGB_ERR_NOT_MAPPED, "%s is %s; nothing to unmap", tid_str(layer, expert, kind).c_str(),
+          state_name(c->st[k][pi]));
+  c->st[k][pi] = XPGB_PAGE_EVICTING;
+  c->step += 1;
+  emit(c, "state", layer, expert, kind, b, "state=evicting");
+  c->blk[k][pi] = 0;
+  c->owner[k][b] = -1;
+  c->free_ids[k].insert(b);
+  c->st[k][pi] = XPGB_PAGE_UNMAPPED;
+  c->bound -= sigma_of(c, kind);
+  c->step += 1;
+  emit(c, "unmap", layer, expert, kind, b, "");
+}
+
+static void pt_sync_entry(Ctx* c, int layer, int expert, int kind) {
+  const int pi = page_index(c, layer, expert, kind);
+  const int k = kind - 1;
+  const int32_t v = c->st[k][pi] == XPGB_PAGE_UNMAPPED ? -1 : pt_entry(c->blk[k][pi] - 1, c->st[k][pi]);
+  CK(cudaMemcpy(c->d_pt + (size_t)k * c->N * c->E + pi, &v, 4, cudaMemcpyHostToDevice));
+}
+
+// StorageHierarchy.fetch (storage.py:228-243): exact bytes into dst on stream.
+static uint64_t fetch(Ctx* c, int layer, int expert, int kind, void* dst, uint64_t dst_bytes, cudaStream_t s,
+                      bool* from_host) {
+  const int pi = page_index(c, layer, expert, kind);
+  const uint64_t sz = sigma_of(c, kind);
+  if (dst_bytes != sz)
+    XFAIL(XPGB_ERR_BACKEND_MISS, "%s: fetched %llu bytes into a %llu-byte block",
+          tid_str(layer, expert, kind).c_str(), (unsigned long long)sz, (unsigned long long)dst_bytes);
+  const uint64_t within = (kind == 2) ? c->s1 : 0;
+  const size_t ti = (size_t)pi * 2 + (kind - 1);
+  if (c->backend[ti] == 1) {
+    if (c->dev_off[ti] < 0) XFAIL(XPGB_ERR_BACKEND_MISS, "%s is not staged on the device tier",
+                                  tid_str(layer, expert, kind).c_str());
+    CK(cudaMemcpyAsync(dst, c->dev_tier + c->dev_off[ti], sz, cudaMemcpyDeviceToDevice, s));
+    if (from_host) *from_host = false;
+  } else {
+    if (!c->host) XFAIL(XPGB_ERR_BACKEND_MISS, "%s: no host pool attached", tid_str(layer, expert, kind).c_str());
+    const uint64_t off = (uint64_t)pi * (c->s1 + c->s2) + within;
+    CK(cudaMemcpyAsync(dst, c->host + off, sz, cudaMemcpyHostToDevice, s));
+    if (from_host) *from_host = true;
+  }
+  return sz;
+}
+
+// --------------------------------------------------------------------------- run (StreamedRunner)
+
+struct RunState {
+  Ctx* c;
+  const xpgb_run_opts* o;
+  float* acts;
+  long long h2d = 0, d2d = 0;
+  bool log;
+};
+
+static void set_rec(PtOp& op, int idx, int ev, int it, int layer, int kind, int tit, int tl) {
+  op.rec[idx][0] = ev;
+  op.rec[idx][1] = it;
+  op.rec[idx][2] = layer;
+  op.rec[idx][3] = kind;
+  op.rec[idx][4] = tit;
+  op.rec[idx][5] = tl;
+  op.n_rec = idx + 1;
+}
+
+static PtOp blank_op(Ctx* c, bool log) {
+  PtOp op;
+  memset(&op, 0, sizeof(op));
+  if (log) {
+    op.log = c->d_log;
+    op.log_count = c->d_log_count;
+    op.log_cap = c->log_cap;
+  }
+  return op;
+}
+
+static void launch_op(const PtOp& op, cudaStream_t s) {
+  k_pt_op<<<1, 128, 0, s>>>(op);
+  note_launch();
+  CKLAUNCH();
+}
+
+static void log_only(Ctx* c, bool log, cudaStream_t s, int ev, int it, int layer) {
+  if (!log) return;
+  PtOp op = blank_op(c, true);
+  set_rec(op, 0, ev, it, layer, -1, -1, -1);
+  launch_op(op, s);
+}
+
+// Alg. 1 MaterializeLayer (pipeline.py:335-360) for one kind, enqueued on copy stream `kind`.
+static void materialize(RunState& rs, int g, int it, int layer, int kind) {
+  Ctx* c = rs.c;
+  const int N = c->N, E = c->E, k = kind - 1;
+  cudaStream_t s = c->s_copy[k];
+  const bool seq = rs.o->sequential != 0;
+  PtOp op = blank_op(c, rs.log);
+  int nrec = 0;
+  if (it > 1 || layer > 2) {
+    const int tgt = ((layer - 3 + N) % N) + 1;
+    const int tgt_it = layer > 2 ? it : it - 1;
+    const int gt = (tgt_it - 1) * N + (tgt - 1);
+    CK(cudaStreamWaitEvent(s, c->ev_comp[gt & 3], 0));  // WAR
+    for (int e = 0; e < E; ++e) pt_unmap(c, tgt, c->e_first + e + 1, kind);
+    op.unmap_row = c->d_pt + (size_t)k * N * E + (size_t)(tgt - 1) * E;
+    op.unmap_n = E;
+    if (rs.log) set_rec(op, nrec++, XPGB_EV_RECYCLE, it, layer, kind, tgt_it, tgt);
+  }
+  // map every expert of the layer (lowest free block first) -> LOADING entries
+  std::vector<int> blocks(E);
+  for (int e = 0; e < E; ++e) blocks[e] = pt_map(c, layer, c->e_first + e + 1, kind);
+  if (rs.log) set_rec(op, nrec++, XPGB_EV_LOAD_START, it, layer, kind, -1, -1);
+  int32_t* row = c->d_pt + (size_t)k * N * E + (size_t)(layer - 1) * E;
+  const int chunk = (int)(sizeof(op.vals) / sizeof(int32_t));
+  for (int e0 = 0; e0 < E; e0 += chunk) {
+    PtOp o2 = (e0 == 0) ? op : blank_op(c, false);
+    if (e0 > 0) { o2.unmap_n = 0; o2.n_rec = 0; }
+    o2.set_row = row + e0;
+    o2.set_n = std::min(chunk, E - e0);
+    for (int i = 0; i < o2.set_n; ++i) o2.vals[i] = pt_entry(blocks[e0 + i] - 1, XPGB_PAGE_LOADING);
+    launch_op(o2, s);
+  }
+  const float* delays = rs.o->fetch_delay_s;
+  for (int e = 0; e < E; ++e) {
+    const int pi = (layer - 1) * E + e;
+    if (delays) {
+      const float d = delays[((size_t)(layer - 1) * c->L + (c->e_first + e)) * 2 + k];
+      if (d > 0) {
+        k_sleep<<<1, 1, 0, s>>>((uint64_t)(d * 1e9));
+        note_launch();
+        CKLAUNCH();
+      }
+    }
+    bool from_host = true;
+    const uint64_t n = fetch(c, layer, c->e_first + e + 1, kind, block_ptr(c, kind, blocks[e]), sigma_of(c, kind), s,
+                             &from_host);
+    (from_host ? rs.h2d : rs.d2d) += n;
+    (void)pi;
+  }
+  for (int e = 0; e < E; ++e) pt_mark_resident(c, layer, c->e_first + e + 1, kind);
+  for (int e0 = 0; e0 < E; e0 += chunk) {
+    PtOp o3 = blank_op(c, rs.log && e0 + chunk >= E);
+    o3.set_row = row + e0;
+    o3.set_n = std::min(chunk, E - e0);
+    for (int i = 0; i < o3.set_n; ++i) o3.vals[i] = pt_entry(blocks[e0 + i] - 1, XPGB_PAGE_RESIDENT);
+    if (o3.log) set_rec(o3, 0, XPGB_EV_LOAD_DONE, it, layer, kind, -1, -1);
+    launch_op(o3, s);
+  }
+  CK(cudaEventRecord(c->ev_load[k][g & 3], s));
+  if (seq) CK(cudaStreamSynchronize(s));
+}
+
+// Alg. 1 ForwardPass (pipeline.py:368-384) on the compute stream.
+static void forward_step(RunState& rs, int g, int it, int layer) {
+  Ctx* c = rs.c;
+  cudaStream_t s = c->s_comp;
+  const xpgb_run_opts* o = rs.o;
+  const bool paged = c->pool == XPGB_POOL_RING;
+  const bool skip = (o->sabotage_iteration == it && o->sabotage_layer == layer);
+  if (paged && !skip) {
+    CK(cudaStreamWaitEvent(s, c->ev_load[0][g & 3], 0));  // RAW
+    CK(cudaStreamWaitEvent(s, c->ev_load[1][g & 3], 0));
+  }
+  log_only(c, rs.log, s, XPGB_EV_COMPUTE_START, it, layer);
+  if (o->compute_delay_s) {
+    const float d = o->compute_delay_s[(size_t)(it - 1) * c->N + (layer - 1)];
+    if (d > 0) {
+      k_sleep<<<1, 1, 0, s>>>((uint64_t)(d * 1e9));
+      note_launch();
+      CKLAUNCH();
+    }
+  }
+  const int kk = std::min(o->top_k, c->L);
+  const int32_t* topk = c->topk_all + (size_t)(layer - 1) * o->tokens * kk;
+  enqueue_forward(c, layer, rs.acts, rs.acts, o->tokens, o->top_k, o->router_seed, topk, s);
+  log_only(c, rs.log, s, XPGB_EV_COMPUTE_DONE, it, layer);
+  CK(cudaEventRecord(c->ev_comp[g & 3], s));
+  if (o->sequential) CK(cudaStreamSynchronize(s));
+}
+
+static void run_impl(Ctx* c, const xpgb_run_opts* o, const float* x, float* y, xpgb_report* rep) {
+  if (o->iterations < 1) XFAIL(XPGB_ERR, "need at least one iteration");
+  if (o->tokens < 0 || o->top_k < 1) XFAIL(XPGB_ERR_OUT_OF_RANGE, "bad ForwardSpec (T=%d, top_k=%d)", o->tokens,
+                                           o->top_k);
+  const int N = c->N;
+  const int steps = o->iterations * N;
+  const int kk = std::min(o->top_k, c->L);
+  ensure_work(c, o->tokens, kk);
+  if (c->topk_all_cap < N * o->tokens * kk) {
+    if (c->topk_all) cudaFree(c->topk_all);
+    c->topk_all_cap = std::max(N * o->tokens * kk, 1);
+    CK(cudaMalloc(&c->topk_all, (size_t)c->topk_all_cap * 4));
+  }
+  const bool log = o->log_enable != 0;
+  ensure_log(c, steps * 8 + 16);
+  CK(cudaMemset(c->d_fault, 0, sizeof(long long)));
+  const bool paged = c->pool == XPGB_POOL_RING;
+  if (paged) {
+    // a run starts from an empty ring, like a fresh PageTable (pipeline.py:325)
+    for (int k = 0; k < 2; ++k)
+      for (size_t pi = 0; pi < c->st[k].size(); ++pi)
+        if (c->st[k][pi] != XPGB_PAGE_UNMAPPED)
+          XFAIL(XPGB_ERR_DOUBLE_MAP, "run() needs an empty page table; page %zu kind %d is mapped", pi, k + 1);
+    c->bound = 0;
+    c->peak = 0;
+  }
+  RunState rs{c, o, y, 0, 0, log};
+  cudaStream_t s = c->s_comp;
+  CK(cudaDeviceSynchronize());  // inputs written by other streams are complete
+  if (y != x) CK(cudaMemcpyAsync(y, x, (size_t)o->tokens * c->H * 4, cudaMemcpyDeviceToDevice, s));
+  // routing is a pure function of (seed, t, layer): one launch covers all N layers
+  if (o->tokens > 0) {
+    launch_route(o->router_seed, 1, N, o->tokens, c->L, o->top_k, c->topk_all, s);
+    CKLAUNCH();
+  }
+  log_only(c, log, s, XPGB_EV_RUN_BEGIN, 0, 0);
+  CK(cudaEventRecord(c->ev_begin, s));
+  CK(cudaStreamWaitEvent(c->s_copy[0], c->ev_begin, 0));
+  CK(cudaStreamWaitEvent(c->s_copy[1], c->ev_begin, 0));
+  if (o->sequential) CK(cudaStreamSynchronize(s));
+
+  auto step_of = [&](int g, int* it, int* layer) {
+    *it = g / N + 1;
+    *layer = g % N + 1;
+  };
+  int it, ly;
+  if (paged) {
+    // inline order: mat(0), mat(1), then fwd(g) | mat(g+2) (pipeline.py:412-424); the
+    // async mode enqueues the same order so every waited event is already recorded.
+    for (int kind = 1; kind <= 2; ++kind) { step_of(0, &it, &ly); materialize(rs, 0, it, ly, kind); }
+    if (steps > 1)
+      for (int kind = 1; kind <= 2; ++kind) { step_of(1, &it, &ly); materialize(rs, 1, it, ly, kind); }
+  }
+  for (int g = 0; g < steps; ++g) {
+    step_of(g, &it, &ly);
+    forward_step(rs, g, it, ly);
+    if (paged && g + 2 < steps) {
+      int it2, ly2;
+      step_of(g + 2, &it2, &ly2);
+      for (int kind = 1; kind <= 2; ++kind) materialize(rs, g + 2, it2, ly2, kind);
+    }
+  }
+  CK(cudaEventRecord(c->ev_end, s));
+  CK(cudaStreamSynchronize(c->s_copy[0]));
+  CK(cudaStreamSynchronize(c->s_copy[1]));
+  CK(cudaStreamSynchronize(s));
+
+  // collect the log
+  int32_t n = 0;
+  CK(cudaMemcpy(&n, c->d_log_count, 4, cudaMemcpyDeviceToHost));
+  n = std::min(n, c->log_cap);
+  c->last_log.resize(n);
+  if (n) CK(cudaMemcpy(c->last_log.data(), c->d_log, (size_t)n * sizeof(xpgb_record), cudaMemcpyDeviceToHost));
+  std::sort(c->last_log.begin(), c->last_log.end(),
+            [](const xpgb_record& a, const xpgb_record& b) { return a.t < b.t; });
+
+  memset(rep, 0, sizeof(*rep));
+  // stall = compute stream idle before each compute-start (since the previous
+  // compute-done / run begin); war wait = copy stream idle before each recycle.
+  int64_t prev_comp = -1, prev_copy[2] = {-1, -1}, load_start[2] = {0, 0};
+  int64_t first = 0, last = 0;
+  for (size_t i = 0; i < c->last_log.size(); ++i) {
+    const xpgb_record& r = c->last_log[i];
+    if (i == 0) first = r.wall_ns;
+    last = std::max<int64_t>(last, r.wall_ns);
+    switch (r.event) {
+      case XPGB_EV_RUN_BEGIN:
+        prev_comp = r.wall_ns;
+        prev_copy[0] = prev_copy[1] = r.wall_ns;
+        break;
+      case XPGB_EV_COMPUTE_START:
+        if (prev_comp >= 0) rep->stall_ns += std::max<int64_t>(0, r.wall_ns - prev_comp);
+        break;
+      case XPGB_EV_COMPUTE_DONE: prev_comp = r.wall_ns; break;
+      case XPGB_EV_RECYCLE:
+        if (r.kind >= 1 && prev_copy[r.kind - 1] >= 0)
+          rep->war_wait_ns += std::max<int64_t>(0, r.wall_ns - prev_copy[r.kind - 1]);
+        break;
+      case XPGB_EV_LOAD_START:
+        if (r.kind >= 1) load_start[r.kind - 1] = r.wall_ns;
+        break;
+      case XPGB_EV_LOAD_DONE:
+        if (r.kind >= 1) {
+          rep->copy_busy_ns[r.kind - 1] += r.wall_ns - load_start[r.kind - 1];
+          prev_copy[r.kind - 1] = r.wall_ns;
+        }
+        break;
+    }
+  }
+  rep->elapsed_ns = last - first;
+  rep->arena_peak_bytes = (int64_t)c->peak;
+  rep->h2d_bytes = rs.h2d;
+  rep->d2d_bytes = rs.d2d;
+  rep->n_records = (int32_t)c->last_log.size();
+  long long fw = 0;
+  CK(cudaMemcpy(&fw, c->d_fault, sizeof(fw), cudaMemcpyDeviceToHost));
+  rep->page_fault = fw != 0;
+
+  if (paged) {
+    // drain: the last two layers are still bound; release them like a finished
+    // runner would drop its table (the reference keeps them until GC).
+    for (int k = 0; k < 2; ++k)
+      for (size_t pi = 0; pi < c->st[k].size(); ++pi)
+        if (c->st[k][pi] == XPGB_PAGE_RESIDENT) {
+          const int layer = (int)(pi / c->E) + 1, e = (int)(pi % c->E);
+          pt_unmap(c, layer, c->e_first + e + 1, k + 1);
+        }
+    CK(cudaMemset(c->d_pt, 0xFF, 2 * (size_t)c->N * c->E * sizeof(int32_t)));
+  }
+}
+
+static void stage_device_tier(Ctx* c) {
+  if (c->dev_tier) {
+    cudaFree(c->dev_tier);
+    c->dev_tier = nullptr;
+  }
+  const size_t pages = (size_t)c->N * c->E;
+  uint64_t n = 0;
+  for (size_t pi = 0; pi < pages; ++pi)
+    for (int k = 0; k < 2; ++k) n += (c->backend[pi * 2 + k] ? (k ? c->s2 : c->s1) : 0);
+  std::fill(c->dev_off.begin(), c->dev_off.end(), -1);
+  if (n == 0) return;
+  if (!c->host) XFAIL(XPGB_ERR_BACKEND_MISS, "device-tier staging needs the host pool");
+  CK(cudaMalloc(&c->dev_tier, n));
+  uint64_t at = 0;
+  for (size_t pi = 0; pi < pages; ++pi)
+    for (int k = 0; k < 2; ++k) {
+      if (!c->backend[pi * 2 + k]) continue;
+      const uint64_t sz = k ? c->s2 : c->s1;
+      c->dev_off[pi * 2 + k] = (int64_t)at;
+      CK(cudaMemcpy(c->dev_tier + at, c->host + pi * (c->s1 + c->s2) + (k ? c->s1 : 0), sz, cudaMemcpyHostToDevice));
+      at += sz;
+    }
+}
+
+}  // namespace xpgb
+
+using namespace xpgb;
+
+struct xpgb_ctx {
+  Ctx c;
+};
+
+// =========================================================================== C ABI
+
+extern "C" {
+
+int xpgb_abi_version(void) { return XPGB_ABI_VERSION; }
+const char* xpgb_last_error(void) { return g_err.c_str(); }
+int64_t xpgb_kernel_launches(void) { return g_launches.load(); }
+
+int xpgb_create(const xpgb_spec* spec, int32_t device, int32_t pool, int32_t max_tokens, xpgb_ctx** out) {
+  return guard([&] {
+    if (!spec || !out) XFAIL(XPGB_ERR, "null argument");
+    if (spec->num_layers < 2) XFAIL(XPGB_ERR_OUT_OF_RANGE, "num_layers must be >= 2, got %d", spec->num_layers);
+    if (spec->experts_per_layer < 1)
+      XFAIL(XPGB_ERR_OUT_OF_RANGE, "experts_per_layer must be >= 1, got %d", spec->experts_per_layer);
+    if (spec->hidden_dim < 1 || spec->intermediate_dim < 1)
+      XFAIL(XPGB_ERR_OUT_OF_RANGE, "hidden_dim and intermediate_dim must be >= 1");
+    if (spec->hidden_dim % 8 || spec->intermediate_dim % 8)
+      XFAIL(XPGB_ERR_OUT_OF_RANGE, "B200 kernels need hidden_dim and intermediate_dim multiples of 8 (got %d, %d)",
+            spec->hidden_dim, spec->intermediate_dim);
+    if (spec->experts_per_layer > kMaxExperts)
+      XFAIL(XPGB_ERR_OUT_OF_RANGE, "experts_per_layer above %d", kMaxExperts);
+    if (pool != XPGB_POOL_RING && pool != XPGB_POOL_RESIDENT) XFAIL(XPGB_ERR_CONFIG, "unknown pool kind %d", pool);
+    CK(cudaSetDevice(device));
+    int major = 0;
+    CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    if (major != 10) XFAIL(XPGB_ERR_CUDA, "libxpgb is built for sm_100a; device %d has compute capability %d.x",
+                           device, major);
+    auto* h = new xpgb_ctx();
+    Ctx* c = &h->c;
+    c->N = spec->num_layers;
+    c->L = spec->experts_per_layer;
+    c->H = spec->hidden_dim;
+    c->F = spec->intermediate_dim;
+    c->device = device;
+    c->pool = pool;
+    c->E = c->L;
+    c->s1 = 2ull * c->H * 2 * c->F;
+    c->s2 = 2ull * c->F * c->H;
+    CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    set_gemm_attrs();
+    for (int k = 0; k < 2; ++k) CK(cudaStreamCreateWithFlags(&c->s_copy[k], cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k)
+      for (int i = 0; i < 4; ++i) CK(cudaEventCreateWithFlags(&c->ev_load[k][i], cudaEventDisableTiming));
+    for (int i = 0; i < 4; ++i) CK(cudaEventCreateWithFlags(&c->ev_comp[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_begin, cudaEventDisableTiming));
+    CK(cudaEventCreate(&c->ev_end));
+    for (int i = 0; i < 7; ++i) CK(cudaEventCreate(&c->pev[i]));
+    CK(cudaMalloc(&c->d_fault, sizeof(long long)));
+    CK(cudaMemset(c->d_fault, 0, sizeof(long long)));
+    CK(cudaMalloc(&c->d_log_count, sizeof(int32_t)));
+    CK(cudaMemset(c->d_log_count, 0, sizeof(int32_t)));
+    init_pools(c);
+    ensure_work(c, std::max(1, max_tokens), std::min(c->L, 8));
+    *out = h;
+  });
+}
+
+int xpgb_destroy(xpgb_ctx* h) {
+  return guard([&] {
+    if (!h) return;
+    Ctx* c = &h->c;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    free_pools(c);
+    LayerWork& w = c->work;
+    void* ptrs[] = {w.pos, w.offsets, w.slot_gu, w.slot_dn, w.units1, w.units2, w.counters, w.xp, w.hbuf, w.part,
+                    c->topk_single, c->topk_all, c->d_fault, c->d_log, c->d_log_count};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    if (c->host && c->host_owned) cudaFreeHost(c->host);
+    if (c->host && c->host_registered) cudaHostUnregister(c->host);
+    for (int k = 0; k < 2; ++k) {
+      cudaStreamDestroy(c->s_copy[k]);
+      for (int i = 0; i < 4; ++i) cudaEventDestroy(c->ev_load[k][i]);
+    }
+    for (int i = 0; i < 4; ++i) cudaEventDestroy(c->ev_comp[i]);
+    cudaEventDestroy(c->ev_begin);
+    cudaEventDestroy(c->ev_end);
+    for (int i = 0; i < 7; ++i) cudaEventDestroy(c->pev[i]);
+    cudaStreamDestroy(c->s_comp);
+    delete h;
+  });
+}
+
+int xpgb_sync(xpgb_ctx* h) {
+  return guard([&] { CK(cudaDeviceSynchronize()); (void)h; });
+}
+
+int xpgb_host_pool_alloc(xpgb_ctx* h, void** host_ptr, uint64_t* bytes) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    const uint64_t need = (uint64_t)c->N * c->E * (c->s1 + c->s2);
+    if (c->host && c->host_owned && c->host_bytes == need) {
+      *host_ptr = c->host;
+      if (bytes) *bytes = need;
+      return;
+    }
+    if (c->host && c->host_owned) cudaFreeHost(c->host);
+    if (c->host && c->host_registered) cudaHostUnregister(c->host);
+    c->host = nullptr;
+    c->host_owned = c->host_registered = false;
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&c->host), need, cudaHostAllocPortable));
+    c->host_owned = true;
+    c->host_bytes = need;
+    *host_ptr = c->host;
+    if (bytes) *bytes = need;
+  });
+}
+
+int xpgb_host_pool_register(xpgb_ctx* h, void* host_ptr, uint64_t bytes) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    const uint64_t need = (uint64_t)c->N * c->E * (c->s1 + c->s2);
+    if (bytes != need)
+      XFAIL(XPGB_ERR_CONTAINER_FORMAT, "payload is %llu bytes, expected %llu", (unsigned long long)bytes,
+            (unsigned long long)need);
+    if (c->host && c->host_owned) cudaFreeHost(c->host);
+    if (c->host && c->host_registered) cudaHostUnregister(c->host);
+    c->host = static_cast<uint8_t*>(host_ptr);
+    c->host_owned = false;
+    c->host_registered = false;
+    cudaError_t e = cudaHostRegister(host_ptr, bytes, cudaHostRegisterPortable);
+    if (e == cudaSuccess) {
+      c->host_registered = true;
+    } else if (e == cudaErrorHostMemoryAlreadyRegistered) {
+      cudaGetLastError();
+    } else {
+      c->host = nullptr;
+      CK(e);
+    }
+    c->host_bytes = bytes;
+  });
+}
+
+int xpgb_set_placement(xpgb_ctx* h, const uint8_t* backend_of) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    for (int layer = 0; layer < c->N; ++layer)
+      for (int e = 0; e < c->E; ++e)
+        for (int k = 0; k < 2; ++k)
+          c->backend[((size_t)layer * c->E + e) * 2 + k] =
+              backend_of ? (backend_of[((size_t)layer * c->L + c->e_first + e) * 2 + k] ? 1 : 0) : 0;
+    stage_device_tier(c);
+  });
+}
+
+int xpgb_fetch(xpgb_ctx* h, int32_t layer, int32_t expert, int32_t kind, void* dst, uint64_t dst_bytes,
+               void* stream) {
+  return guard([&] { fetch(&h->c, layer, expert, kind, dst, dst_bytes, (cudaStream_t)stream, nullptr); });
+}
+
+int xpgb_pt_map(xpgb_ctx* h, int32_t layer, int32_t expert, int32_t kind, int32_t* block_id) {
+  return guard([&] {
+    const int b = pt_map(&h->c, layer, expert, kind);
+    pt_sync_entry(&h->c, layer, expert, kind);
+    if (block_id) *block_id = b;
+  });
+}
+int xpgb_pt_mark_resident(xpgb_ctx* h, int32_t layer, int32_t expert, int32_t kind) {
+  return guard([&] {
+    pt_mark_resident(&h->c, layer, expert, kind);
+    pt_sync_entry(&h->c, layer, expert, kind);
+  });
+}
+int xpgb_pt_unmap(xpgb_ctx* h, int32_t layer, int32_t expert, int32_t kind) {
+  return guard([&] {
+    pt_unmap(&h->c, layer, expert, kind);
+    pt_sync_entry(&h->c, layer, expert, kind);
+  });
+}
+int xpgb_pt_state(xpgb_ctx* h, int32_t layer, int32_t expert, int32_t kind, int32_t* state) {
+  return guard([&] { *state = h->c.st[kind - 1][page_index(&h->c, layer, expert, kind)]; });
+}
+int xpgb_pt_block(xpgb_ctx* h, int32_t layer, int32_t expert, int32_t kind, int32_t* block_id) {
+  return guard([&] { *block_id = h->c.blk[kind - 1][page_index(&h->c, layer, expert, kind)]; });
+}
+int xpgb_pt_block_ptr(xpgb_ctx* h, int32_t kind, int32_t block_id, void** dptr, uint64_t* bytes) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    if (kind != 1 && kind != 2) XFAIL(XPGB_ERR_OUT_OF_RANGE, "unknown tensor kind %d", kind);
+    if (block_id < 1 || block_id > c->blocks)
+      XFAIL(XPGB_ERR_OUT_OF_RANGE, "block %d outside [1, %d]", block_id, c->blocks);
+    *dptr = block_ptr(c, kind, block_id);
+    if (bytes) *bytes = sigma_of(c, kind);
+  });
+}
+int xpgb_pt_loading_view(xpgb_ctx* h, int32_t layer, int32_t expert, int32_t kind, void** dptr, uint64_t* bytes) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    const int pi = page_index(c, layer, expert, kind);
+    if (c->st[kind - 1][pi] != XPGB_PAGE_LOADING)
+      XFAIL(XPGB_ERR_PAGE_FAULT, "write through %s while %s", tid_str(layer, expert, kind).c_str(),
+            state_name(c->st[kind - 1][pi]));
+    *dptr = block_ptr(c, kind, c->blk[kind - 1][pi]);
+    if (bytes) *bytes = sigma_of(c, kind);
+  });
+}
+int xpgb_pt_read(xpgb_ctx* h, int32_t layer, int32_t expert, int32_t kind, void* host_dst, uint64_t bytes) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    const int pi = page_index(c, layer, expert, kind);
+    if (c->st[kind - 1][pi] != XPGB_PAGE_RESIDENT)
+      XFAIL(XPGB_ERR_PAGE_FAULT, "read through %s while %s", tid_str(layer, expert, kind).c_str(),
+            state_name(c->st[kind - 1][pi]));
+    const uint64_t sz = sigma_of(c, kind);
+    if (bytes < sz) XFAIL(XPGB_ERR_OUT_OF_RANGE, "destination holds %llu bytes, page has %llu",
+                          (unsigned long long)bytes, (unsigned long long)sz);
+    CK(cudaMemcpy(host_dst, block_ptr(c, kind, c->blk[kind - 1][pi]), sz, cudaMemcpyDeviceToHost));
+  });
+}
+int xpgb_pt_peak_bytes(xpgb_ctx* h, uint64_t* peak) {
+  return guard([&] { *peak = h->c.peak; });
+}
+int xpgb_pt_pool_bytes(xpgb_ctx* h, uint64_t* bytes) {
+  return guard([&] { *bytes = (uint64_t)h->c.blocks * (h->c.s1 + h->c.s2); });
+}
+int xpgb_pt_check_consistency(xpgb_ctx* h) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    for (int k = 0; k < 2; ++k) {
+      size_t bound = 0;
+      for (size_t pi = 0; pi < c->blk[k].size(); ++pi) {
+        const int b = c->blk[k][pi];
+        if (b) {
+          ++bound;
+          if (c->owner[k][b] != (int)pi) XFAIL(XPGB_ERR, "forward/reverse maps disagree at block %d", b);
+          if (c->free_ids[k].count(b)) XFAIL(XPGB_ERR, "block %d both bound and free", b);
+        }
+      }
+      if (bound + c->free_ids[k].size() != (size_t)c->blocks) XFAIL(XPGB_ERR, "block accounting broken");
+    }
+  });
+}
+int xpgb_pt_trace_enable(xpgb_ctx* h, int32_t enable) {
+  return guard([&] {
+    h->c.trace_on = enable != 0;
+    h->c.trace.clear();
+  });
+}
+int xpgb_pt_trace_get(xpgb_ctx* h, char* buf, uint64_t cap, uint64_t* needed) {
+  return guard([&] {
+    const std::string& t = h->c.trace;
+    if (needed) *needed = t.size() + 1;
+    if (buf && cap > 0) {
+      const size_t n = std::min<size_t>(t.size(), cap - 1);
+      memcpy(buf, t.data(), n);
+      buf[n] = 0;
+    }
+  });
+}
+int xpgb_make_resident(xpgb_ctx* h) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    cudaStream_t s = c->s_copy[0];
+    for (int layer = 1; layer <= c->N; ++layer)
+      for (int e = 0; e < c->E; ++e)
+        for (int kind = 1; kind <= 2; ++kind) {
+          const int ex = c->e_first + e + 1;
+          const int pi = page_index(c, layer, ex, kind);
+          if (c->st[kind - 1][pi] == XPGB_PAGE_RESIDENT) continue;
+          const int b = pt_map(c, layer, ex, kind);
+          fetch(c, layer, ex, kind, block_ptr(c, kind, b), sigma_of(c, kind), s, nullptr);
+          pt_mark_resident(c, layer, ex, kind);
+        }
+    CK(cudaStreamSynchronize(s));
+    // bulk device-table upload
+    const size_t pages = (size_t)c->N * c->E;
+    std::vector<int32_t> tab(2 * pages);
+    for (int k = 0; k < 2; ++k)
+      for (size_t pi = 0; pi < pages; ++pi)
+        tab[k * pages + pi] = c->st[k][pi] == XPGB_PAGE_UNMAPPED ? -1 : pt_entry(c->blk[k][pi] - 1, c->st[k][pi]);
+    CK(cudaMemcpy(c->d_pt, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
+  });
+}
+
+int xpgb_route(uint64_t seed, int32_t layer_first, int32_t layer_count, int32_t tokens, int32_t num_experts,
+               int32_t top_k, int32_t* out_dev, void* stream) {
+  return guard([&] {
+    if (num_experts < 1 || num_experts > kMaxExperts)
+      XFAIL(XPGB_ERR_OUT_OF_RANGE, "num_experts %d outside [1, %d]", num_experts, kMaxExperts);
+    if (top_k < 1 || std::min(top_k, num_experts) > kMaxTopK)
+      XFAIL(XPGB_ERR_OUT_OF_RANGE, "top_k %d outside [1, %d]", top_k, kMaxTopK);
+    launch_route(seed, layer_first, layer_count, tokens, num_experts, top_k, out_dev, (cudaStream_t)stream);
+    CKLAUNCH();
+  });
+}
+
+int xpgb_layer_forward(xpgb_ctx* h, int32_t layer, const float* x_dev, float* y_dev, int32_t tokens, int32_t top_k,
+                       uint64_t router_seed, void* stream) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    if (layer < 1 || layer > c->N) XFAIL(XPGB_ERR_OUT_OF_RANGE, "layer %d outside [1, %d]", layer, c->N);
+    if (top_k < 1) XFAIL(XPGB_ERR_OUT_OF_RANGE, "top_k must be >= 1");
+    enqueue_forward(c, layer, x_dev, y_dev, tokens, top_k, router_seed, nullptr, (cudaStream_t)stream);
+  });
+}
+
+int xpgb_fault_get(xpgb_ctx* h, int32_t* faulted, char* msg, uint64_t cap) {
+  return guard([&] {
+    long long fw = 0;
+    CK(cudaMemcpy(&fw, h->c.d_fault, sizeof(fw), cudaMemcpyDeviceToHost));
+    *faulted = fw != 0;
+    if (msg && cap) {
+      std::string m;
+      if (fw) {
+        const int kind = (int)((fw >> 1) & 3), state = (int)((fw >> 3) & 7), expert = (int)((fw >> 8) & 0xFFFFFF),
+                  layer = (int)(fw >> 32);
+        m = fmt("read through %s while %s", tid_str(layer, expert, kind).c_str(), state_name(state));
+      }
+      const size_t n = std::min<size_t>(m.size(), cap - 1);
+      memcpy(msg, m.data(), n);
+      msg[n] = 0;
+    }
+  });
+}
+int xpgb_fault_clear(xpgb_ctx* h) {
+  return guard([&] { CK(cudaMemset(h->c.d_fault, 0, sizeof(long long))); });
+}
+
+int xpgb_run(xpgb_ctx* h, const xpgb_run_opts* opts, const float* x_dev, float* y_dev, xpgb_report* rep) {
+  return guard([&] {
+    if (!opts || !rep) XFAIL(XPGB_ERR, "null argument");
+    run_impl(&h->c, opts, x_dev, y_dev, rep);
+  });
+}
+
+int xpgb_log_get(xpgb_ctx* h, xpgb_record* out, int32_t cap, int32_t* n) {
+  return guard([&] {
+    const auto& l = h->c.last_log;
+    *n = (int32_t)l.size();
+    if (out) memcpy(out, l.data(), std::min<size_t>(cap, l.size()) * sizeof(xpgb_record));
+  });
+}
+
+int xpgb_set_expert_shard(xpgb_ctx* h, int32_t expert_first, int32_t expert_count) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    if (expert_first < 0 || expert_count < 1 || expert_first + expert_count > c->L)
+      XFAIL(XPGB_ERR_OUT_OF_RANGE, "shard [%d, %d) outside [0, %d)", expert_first, expert_first + expert_count, c->L);
+    CK(cudaDeviceSynchronize());
+    if (c->host && c->host_owned) cudaFreeHost(c->host);
+    if (c->host && c->host_registered) cudaHostUnregister(c->host);
+    c->host = nullptr;
+    c->host_owned = c->host_registered = false;
+    c->e_first = expert_first;
+    c->E = expert_count;
+    c->cap_T = 0;  // force workspace re-creation with the new expert count
+    init_pools(c);
+    ensure_work(c, 16, std::min(c->L, 8));
+  });
+}
+
+int xpgb_experts_forward(xpgb_ctx* h, int32_t layer, const void* rows_dev, const int32_t* offsets_dev,
+                         int32_t n_rows, float* out_dev, void* stream) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    if (layer < 1 || layer > c->N) XFAIL(XPGB_ERR_OUT_OF_RANGE, "layer %d outside [1, %d]", layer, c->N);
+    cudaStream_t s = (cudaStream_t)stream;
+    ensure_work(c, std::max(n_rows, 1), 1);
+    if (n_rows == 0) return;
+    LayerWork w = c->work;
+    CK(cudaMemcpyAsync(w.xp, rows_dev, (size_t)n_rows * c->H * 2, cudaMemcpyDeviceToDevice, s));
+    const int bn = pick_bn(n_rows);
+    const int splits = pick_splits(c, n_rows, 1, bn);
+    const size_t pages = (size_t)c->N * c->E;
+    launch_plan_rows(w, offsets_dev, c->d_pt, c->d_pt + pages, layer, c->e_first, c->E, c->F, c->H, bn, bn, splits, s);
+    CKLAUNCH();
+    launch_gate_up(c->map_gu, c->map_xp, w, c->F, c->H, bn, c->num_sms, s);
+    CKLAUNCH();
+    launch_down(c->map_dn, c->map_h, w, c->F, c->H, bn, splits, c->cap_rows, c->num_sms, s);
+    CKLAUNCH();
+    launch_reduce_rows(w, out_dev, n_rows, c->H, splits, c->cap_rows, s);
+    CKLAUNCH();
+  });
+}
+
+int xpgb_profile_layer(xpgb_ctx* h, int32_t layer, const float* x_dev, float* y_dev, int32_t tokens, int32_t top_k,
+                       uint64_t router_seed, int32_t reps, xpgb_kernel_times* out) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    cudaStream_t s = c->s_comp;
+    xpgb_kernel_times acc{};
+    const int kk = std::min(top_k, c->L);
+    c->prof = true;
+    for (int r = 0; r < std::max(1, reps); ++r) {
+      enqueue_forward(c, layer, x_dev, y_dev, tokens, top_k, router_seed, nullptr, s);
+      CK(cudaStreamSynchronize(s));
+      float ms[6];
+      for (int i = 0; i < 6; ++i) CK(cudaEventElapsedTime(&ms[i], c->pev[i], c->pev[i + 1]));
+      acc.route_ns += ms[0] * 1e6;
+      acc.plan_ns += ms[1] * 1e6;
+      acc.gather_ns += ms[2] * 1e6;
+      acc.gate_up_ns += ms[3] * 1e6;
+      acc.down_ns += ms[4] * 1e6;
+      acc.combine_ns += ms[5] * 1e6;
+    }
+    c->prof = false;
+    const double inv = 1.0 / std::max(1, reps);
+    acc.route_ns *= inv; acc.plan_ns *= inv; acc.gather_ns *= inv;
+    acc.gate_up_ns *= inv; acc.down_ns *= inv; acc.combine_ns *= inv;
+    int counters[3];
+    CK(cudaMemcpy(counters, c->work.counters, 12, cudaMemcpyDeviceToHost));
+    std::vector<int32_t> offs(c->E + 1);
+    CK(cudaMemcpy(offs.data(), c->work.offsets, (c->E + 1) * 4, cudaMemcpyDeviceToHost));
+    long long active = 0;
+    for (int e = 0; e < c->E; ++e) active += (offs[e + 1] > offs[e]);
+    const long long pairs = (long long)tokens * kk;
+    acc.gate_up_bytes = active * (long long)c->s1 + pairs * c->H * 2 + pairs * c->F * 2;
+    acc.down_bytes = active * (long long)c->s2 + pairs * c->F * 2 + pairs * c->H * 4 * c->last_times.down_splits;
+    acc.n_units_gate_up = counters[0];
+    acc.n_units_down = counters[1];
+    acc.down_splits = c->last_times.down_splits;
+    c->last_times = acc;
+    *out = acc;
+  });
+}
+
+}  // extern "C"

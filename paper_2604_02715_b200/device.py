@@ -1,0 +1,135 @@
+"""Thin owner of one ``xpgb_ctx`` (one device, one pool) plus tensor plumbing.
+
+PyTorch is used only for device/pinned memory and the current CUDA stream;
+every computation is a libxpgb kernel launched through the C ABI.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import call, lib
+from .errors import OutOfRangeError, XpgError
+from .geometry import ModelSpec
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise XpgError("no CUDA device: the B200 expert-paging path has no CPU fallback")
+    return torch
+
+
+def current_stream_ptr(device: int = 0) -> int:
+    torch = _torch()
+    return int(torch.cuda.current_stream(device).cuda_stream)
+
+
+def as_device_f32(acts, device: int, rows: int, cols: int):
+    """(tensor, was_numpy): a contiguous float32 CUDA tensor holding acts."""
+    torch = _torch()
+    if isinstance(acts, torch.Tensor):
+        t = acts
+        if t.device.type != "cuda":
+            t = t.to(f"cuda:{device}", non_blocking=False)
+        t = t.to(torch.float32).contiguous()
+        was_numpy = False
+    else:
+        arr = np.ascontiguousarray(np.asarray(acts, dtype=np.float32))
+        t = torch.from_numpy(arr).to(f"cuda:{device}")
+        was_numpy = True
+    if tuple(t.shape) != (rows, cols):
+        raise OutOfRangeError(f"activations have shape {tuple(t.shape)}, expected {(rows, cols)}")
+    return t, was_numpy
+
+
+class Context:
+    """One libxpgb context: pools, page table, streams, workspaces."""
+
+    def __init__(self, spec: ModelSpec, pool: int = _lib.POOL_RING, device: int = 0, max_tokens: int = 16):
+        _torch()
+        self.spec = spec
+        self.device = device
+        self.pool = pool
+        self.expert_first = 0
+        self.expert_count = spec.experts_per_layer
+        s = _lib.Spec(spec.num_layers, spec.experts_per_layer, spec.hidden_dim, spec.intermediate_dim)
+        h = C.c_void_p()
+        call("xpgb_create", C.byref(s), device, pool, max(1, int(max_tokens)), C.byref(h))
+        self._h = h
+        self._host_ref = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib().xpgb_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):  # pragma: no cover - GC timing
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- storage
+    def attach_host_pool(self, pinned_u8) -> None:
+        """Use a (pinned) torch uint8 tensor holding this shard's payload as the host pool."""
+        call("xpgb_host_pool_register", self._h, C.c_void_p(pinned_u8.data_ptr()), C.c_uint64(pinned_u8.numel()))
+        self._host_ref = pinned_u8
+
+    def set_placement(self, backend_of: np.ndarray) -> None:
+        arr = np.ascontiguousarray(backend_of, dtype=np.uint8)
+        call("xpgb_set_placement", self._h, arr.ctypes.data_as(C.POINTER(C.c_uint8)))
+
+    def set_expert_shard(self, first: int, count: int) -> None:
+        call("xpgb_set_expert_shard", self._h, first, count)
+        self.expert_first, self.expert_count = first, count
+
+    def make_resident(self) -> None:
+        call("xpgb_make_resident", self._h)
+
+    # ---- compute
+    def layer_forward(self, layer: int, x, y, tokens: int, top_k: int, seed: int, stream: int | None = None):
+        st = current_stream_ptr(self.device) if stream is None else stream
+        call("xpgb_layer_forward", self._h, layer, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), tokens,
+             top_k, C.c_uint64(int(seed) & 0xFFFFFFFFFFFFFFFF), C.c_void_p(st))
+
+    def fault(self):
+        f = C.c_int32()
+        buf = C.create_string_buffer(512)
+        call("xpgb_fault_get", self._h, C.byref(f), buf, 512)
+        return (buf.value.decode() if f.value else None)
+
+    def clear_fault(self):
+        call("xpgb_fault_clear", self._h)
+
+    def profile_layer(self, layer: int, x, y, tokens: int, top_k: int, seed: int, reps: int = 5):
+        kt = _lib.KernelTimes()
+        call("xpgb_profile_layer", self._h, layer, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), tokens,
+             top_k, C.c_uint64(int(seed) & 0xFFFFFFFFFFFFFFFF), reps, C.byref(kt))
+        return {name: getattr(kt, name) for name, _ in _lib.KernelTimes._fields_}
+
+    def sync(self):
+        call("xpgb_sync", self._h)
+
+
+def kernel_launches() -> int:
+    return int(lib().xpgb_kernel_launches())
+
+
+def route_table(seed: int, tokens: int, num_layers: int, num_experts: int, top_k: int, device: int = 0,
+                layer_first: int = 1):
+    """Routing of layers [layer_first, layer_first+num_layers) as an int32 CUDA tensor [n, T, min(k, L)]."""
+    torch = _torch()
+    kk = min(top_k, num_experts)
+    out = torch.empty((num_layers, tokens, kk), dtype=torch.int32, device=f"cuda:{device}")
+    call("xpgb_route", C.c_uint64(int(seed) & 0xFFFFFFFFFFFFFFFF), layer_first, num_layers, tokens, num_experts,
+         top_k, C.c_void_p(out.data_ptr()), C.c_void_p(current_stream_ptr(device)))
+    return out

@@ -1,0 +1,345 @@
+"""Streamed execution of the paged MoE stack on a B200 (reference pipeline.py:1-483).
+
+Alg. 1 of the paper on CUDA streams instead of threads:
+
+* loader(kind) threads  -> two copy streams (GATE_UP, DOWN), fed by the C++ schedule;
+* compute thread        -> one compute stream running route/plan/gather/GEMM/combine;
+* threading.Event       -> cudaEvent: RAW = compute waits on both load events of its
+  step, WAR = the copy stream waits on the compute event of the layer it recycles;
+* OrderingLog           -> device log appended by stream-ordered kernels with a global
+  atomic counter, so the record order is the causal order the GPU executed.
+
+``mode="sequential"`` enqueues the same task order but synchronises the host
+after every task, the deterministic twin of the reference's inline mode.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import hashlib
+import json
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import call
+from .device import Context, _torch, as_device_f32, route_table
+from .errors import XpgError
+from .geometry import ExpertTensorId, ModelSpec, TensorKind, WeightContainer, initial_activations, iter_tensor_ids
+from .pagetable import PageTable
+from .tiers import StorageHierarchy
+
+ROLE_LOAD = {TensorKind.GATE_UP: "load1", TensorKind.DOWN: "load2"}
+ROLE_COMPUTE = "comp"
+
+
+@dataclass(frozen=True)
+class ForwardSpec:
+    tokens_per_step: int = 4
+    top_k: int = 2
+    router_seed: int = 0
+
+
+@dataclass(frozen=True)
+class OrderingRecord:
+    t: int
+    event: str
+    iteration: int
+    layer: int
+    kind: int | None = None
+    target_iteration: int | None = None
+    target_layer: int | None = None
+    wall: float = 0.0
+
+
+def validate_ordering(records) -> list:
+    """RAW/WAR replay of an ordering log (pipeline.py:119-147): one message per violation."""
+    first = {}
+    for r in records:
+        first.setdefault((r.event, r.iteration, r.layer, r.kind), r.t)
+
+    def before(event, it, layer, kind, t):
+        at = first.get((event, it, layer, kind))
+        return at is not None and at < t
+
+    problems = []
+    for r in records:
+        if r.event == "compute-start":
+            problems += [
+                f"RAW: compute-start iter={r.iteration} layer={r.layer} before load-done kind={k}"
+                for k in (1, 2) if not before("load-done", r.iteration, r.layer, k, r.t)
+            ]
+        elif r.event == "recycle" and not before("compute-done", r.target_iteration, r.target_layer, None, r.t):
+            problems.append(
+                f"WAR: recycle of iter={r.target_iteration} layer={r.target_layer} kind={r.kind} before its compute-done")
+    return problems
+
+
+def _intervals(records) -> dict:
+    spans, opened = {}, {}
+    for r in records:
+        phase, _, edge = r.event.partition("-")
+        if edge == "start":
+            opened[(phase, r.iteration, r.layer, r.kind)] = r.wall
+        elif edge == "done":
+            t0 = opened.get((phase, r.iteration, r.layer, r.kind))
+            if t0 is not None:
+                name = f"load{r.kind}" if phase == "load" else "compute"
+                spans.setdefault((r.iteration, r.layer), {})[name] = (t0, r.wall)
+    return spans
+
+
+@dataclass
+class RunReport:
+    final_activations: object
+    arena_peak_bytes: int
+    stall_seconds: float
+    war_wait_seconds: float
+    violations: list
+    records: list
+    intervals: dict = field(default_factory=dict)
+    page_fault: str | None = None
+    # B200 additions
+    h2d_bytes: int = 0
+    d2d_bytes: int = 0
+    copy_busy_seconds: tuple = (0.0, 0.0)
+    elapsed_seconds: float = 0.0
+
+    @property
+    def checksum(self) -> str:
+        a = self.final_activations
+        if hasattr(a, "detach"):
+            a = a.detach().cpu().numpy()
+        return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+    @property
+    def page_in_gbps(self) -> float:
+        busy = max(self.copy_busy_seconds) if self.copy_busy_seconds else 0.0
+        return (self.h2d_bytes + self.d2d_bytes) / self.elapsed_seconds / 1e9 if self.elapsed_seconds > 0 else 0.0
+
+    @property
+    def exposed_fraction(self) -> float:
+        return self.stall_seconds / self.elapsed_seconds if self.elapsed_seconds > 0 else 0.0
+
+    def to_json(self) -> str:
+        return json.dumps({
+            "activation_checksum": self.checksum,
+            "stall_ms": self.stall_seconds * 1e3,
+            "war_wait_ms": self.war_wait_seconds * 1e3,
+            "arena_peak_bytes": self.arena_peak_bytes,
+            "violation_count": len(self.violations),
+            "violations": self.violations,
+            "page_fault": self.page_fault,
+            "layer_intervals": {f"iter{it}.layer{ly}": v for (it, ly), v in sorted(self.intervals.items())},
+            "h2d_bytes": self.h2d_bytes,
+            "d2d_bytes": self.d2d_bytes,
+            "elapsed_ms": self.elapsed_seconds * 1e3,
+        }, indent=2)
+
+
+def _records_from_log(ctx: Context):
+    n = C.c_int32()
+    call("xpgb_log_get", ctx.handle, None, 0, C.byref(n))
+    arr = (_lib.Record * max(n.value, 1))()
+    call("xpgb_log_get", ctx.handle, arr, n.value, C.byref(n))
+    out = []
+    t = 0
+    base = None
+    for i in range(n.value):
+        r = arr[i]
+        if r.event == _lib.EV_RUN_BEGIN:
+            base = r.wall_ns
+            continue
+        if base is None:
+            base = r.wall_ns
+        kind = r.kind if r.kind > 0 else None
+        out.append(OrderingRecord(
+            t=t, event=_lib.EVENT_NAMES[r.event], iteration=r.iteration, layer=r.layer, kind=kind,
+            target_iteration=r.target_iteration if r.target_iteration > 0 else None,
+            target_layer=r.target_layer if r.target_layer > 0 else None,
+            wall=(r.wall_ns - base) * 1e-9))
+        t += 1
+    return out
+
+
+def _run_context(ctx: Context, spec: ModelSpec, fwd: ForwardSpec, iterations: int, acts, sequential: bool,
+                 fetch_delay=None, compute_delay=None, sabotage=None, log: bool = True):
+    torch = _torch()
+    x, was_numpy = as_device_f32(acts, ctx.device, fwd.tokens_per_step, spec.hidden_dim)
+    y = torch.empty_like(x)
+    opts = _lib.RunOpts()
+    opts.iterations = iterations
+    opts.tokens = fwd.tokens_per_step
+    opts.top_k = fwd.top_k
+    opts.sequential = 1 if sequential else 0
+    opts.router_seed = int(fwd.router_seed) & 0xFFFFFFFFFFFFFFFF
+    opts.sabotage_iteration, opts.sabotage_layer = sabotage if sabotage else (0, 0)
+    keep = []
+    if fetch_delay is not None:
+        fd = np.ascontiguousarray(fetch_delay, dtype=np.float32)
+        keep.append(fd)
+        opts.fetch_delay_s = fd.ctypes.data_as(C.POINTER(C.c_float))
+    if compute_delay is not None:
+        cd = np.ascontiguousarray(compute_delay, dtype=np.float32)
+        keep.append(cd)
+        opts.compute_delay_s = cd.ctypes.data_as(C.POINTER(C.c_float))
+    opts.log_enable = 1 if log else 0
+    rep = _lib.Report()
+    torch.cuda.current_stream(ctx.device).synchronize()
+    call("xpgb_run", ctx.handle, C.byref(opts), C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), C.byref(rep))
+    out = y.cpu().numpy() if was_numpy else y
+    return out, rep
+
+
+class StreamedRunner:
+    """Paged pipeline for n iterations over N layers on one B200."""
+
+    def __init__(self, spec: ModelSpec, hierarchy: StorageHierarchy, fwd: ForwardSpec, mode: str = "threaded",
+                 compute_delay_fn=None, sabotage_skip_raw=None, trace=None, device: int = 0):
+        if mode not in ("threaded", "sequential"):
+            raise XpgError(f"unknown mode {mode!r}")
+        self.spec = spec
+        self.hierarchy = hierarchy
+        self.fwd = fwd
+        self.mode = mode
+        self.compute_delay_fn = compute_delay_fn
+        self.sabotage_skip_raw = sabotage_skip_raw
+        self.ctx = Context(spec, _lib.POOL_RING, device, max_tokens=fwd.tokens_per_step)
+        self.ctx.attach_host_pool(hierarchy.container.pinned)
+        self.ctx.set_placement(hierarchy.backend_map())
+        self.table = PageTable(spec, trace=trace, context=self.ctx)
+        self.stall_seconds = 0.0
+        self.war_wait_seconds = 0.0
+
+    def run(self, iterations: int, acts=None) -> RunReport:
+        if iterations < 1:
+            raise XpgError("need at least one iteration")
+        if acts is None:
+            acts = initial_activations(self.spec, self.fwd, 0)
+        cd = None
+        if self.compute_delay_fn is not None:
+            cd = np.array([[self.compute_delay_fn(it, ly) for ly in range(1, self.spec.num_layers + 1)]
+                           for it in range(1, iterations + 1)], dtype=np.float32)
+        out, rep = _run_context(self.ctx, self.spec, self.fwd, iterations, acts, self.mode == "sequential",
+                                fetch_delay=self.hierarchy.delay_table(), compute_delay=cd,
+                                sabotage=self.sabotage_skip_raw)
+        self.table.sync_trace()
+        records = _records_from_log(self.ctx)
+        self.stall_seconds = rep.stall_ns * 1e-9
+        self.war_wait_seconds = rep.war_wait_ns * 1e-9
+        return RunReport(
+            final_activations=out,
+            arena_peak_bytes=int(rep.arena_peak_bytes),
+            stall_seconds=self.stall_seconds,
+            war_wait_seconds=self.war_wait_seconds,
+            violations=validate_ordering(records),
+            records=records,
+            intervals=_intervals(records),
+            page_fault=self.ctx.fault() if rep.page_fault else None,
+            h2d_bytes=int(rep.h2d_bytes),
+            d2d_bytes=int(rep.d2d_bytes),
+            copy_busy_seconds=(rep.copy_busy_ns[0] * 1e-9, rep.copy_busy_ns[1] * 1e-9),
+            elapsed_seconds=rep.elapsed_ns * 1e-9,
+        )
+
+
+def run_iterations(iterations: int, spec: ModelSpec, hierarchy: StorageHierarchy, fwd: ForwardSpec,
+                   mode: str = "threaded", acts=None, **runner_kwargs) -> RunReport:
+    return StreamedRunner(spec, hierarchy, fwd, mode=mode, **runner_kwargs).run(iterations, acts=acts)
+
+
+class ResidentModel:
+    """Every expert tensor of a container resident in HBM (one block per tensor).
+
+    The fully-resident comparator: the same kernels read the same device slot
+    table, which simply never changes (pipeline.py:216-230).
+    """
+
+    def __init__(self, spec: ModelSpec, container: WeightContainer, device: int = 0, max_tokens: int = 16):
+        self.spec = spec
+        self.container = container
+        self.ctx = Context(spec, _lib.POOL_RESIDENT, device, max_tokens=max_tokens)
+        self.ctx.attach_host_pool(container.pinned)
+        self.ctx.make_resident()
+
+    def forward(self, layer: int, acts, fwd: ForwardSpec):
+        torch = _torch()
+        x, was_numpy = as_device_f32(acts, self.ctx.device, acts.shape[0], self.spec.hidden_dim)
+        y = torch.empty_like(x)
+        self.ctx.clear_fault()
+        self.ctx.layer_forward(layer, x, y, x.shape[0], fwd.top_k, fwd.router_seed)
+        fault = self.ctx.fault()
+        if fault:
+            from .errors import PageFaultError
+
+            raise PageFaultError(fault)
+        return y.cpu().numpy() if was_numpy else y
+
+    def run(self, iterations: int, fwd: ForwardSpec, acts, log: bool = False):
+        return _run_context(self.ctx, self.spec, fwd, iterations, acts, sequential=False, log=log)
+
+
+_RESIDENT_CACHE: dict = {}
+
+
+def _resident_for(spec: ModelSpec, weights_of) -> ResidentModel:
+    if isinstance(weights_of, ResidentModel):
+        return weights_of
+    owner = getattr(weights_of, "__self__", None)
+    if isinstance(owner, WeightContainer):
+        key = id(owner)
+        hit = _RESIDENT_CACHE.get(key)
+        if hit is None or hit[0] is not owner:
+            hit = (owner, ResidentModel(spec, owner))
+            _RESIDENT_CACHE.clear()
+            _RESIDENT_CACHE[key] = hit
+        return hit[1]
+    # generic callable: materialise bf16 words of every tensor (exact for bf16-valued weights)
+    from .geometry import float32_to_bf16, tensor_offset
+
+    words = np.zeros(spec.total_bytes // 2, dtype=np.uint16)
+    for tid in iter_tensor_ids(spec):
+        w = np.asarray(weights_of(tid), dtype=np.float32).reshape(-1)
+        off = tensor_offset(tid, spec) // 2
+        words[off:off + w.size] = float32_to_bf16(w)
+    return ResidentModel(spec, WeightContainer(spec, words))
+
+
+def layer_forward(weights_of, spec: ModelSpec, fwd: ForwardSpec, layer: int, acts):
+    """One MoE layer (pipeline.py:192-208) on the GPU.
+
+    ``weights_of`` may be a ``ResidentModel``, a ``PageTable`` whose layer
+    pages are RESIDENT, ``WeightContainer.tensor_f32`` (as in the reference's
+    ``resident_baseline``), or any tid -> float32 matrix callable.
+    """
+    if isinstance(weights_of, PageTable):
+        torch = _torch()
+        ctx = weights_of.ctx
+        x, was_numpy = as_device_f32(acts, ctx.device, np.shape(acts)[0], spec.hidden_dim)
+        y = torch.empty_like(x)
+        ctx.clear_fault()
+        ctx.layer_forward(layer, x, y, x.shape[0], fwd.top_k, fwd.router_seed)
+        fault = ctx.fault()
+        if fault:
+            from .errors import PageFaultError
+
+            raise PageFaultError(fault)
+        return y.cpu().numpy() if was_numpy else y
+    model = _resident_for(spec, weights_of)
+    return model.forward(layer, acts, fwd)
+
+
+def resident_baseline(iterations: int, spec: ModelSpec, container, fwd: ForwardSpec, acts=None):
+    """Fully-resident oracle path on the GPU: same kernels, every page resident."""
+    if acts is None:
+        acts = initial_activations(spec, fwd, 0)
+    model = container if isinstance(container, ResidentModel) else _resident_for(spec, container.tensor_f32)
+    out, _ = model.run(iterations, fwd, acts)
+    return out
+
+
+def routed_experts(seed: int, token: int, layer: int, num_experts: int, top_k: int, device: int = 0):
+    """Experts of one token (ascending, 1-based) from the GPU router kernel."""
+    tab = route_table(seed, token + 1, 1, num_experts, top_k, device=device, layer_first=layer)
+    return [int(v) for v in tab[0, token].tolist()]

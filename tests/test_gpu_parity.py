@@ -1,0 +1,224 @@
+"""Parity of the CUDA path (through the C ABI) with the reference oracle.  Needs a B200.
+
+Bars (north star): routing and slot ids bit-exact; layer outputs within
+rel-L2 <= 1e-2 of the reference (bf16 tensor-core inputs, fp32 accumulate);
+GPU-streamed == GPU-resident bit-identical.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-2  # north-star bf16 tolerance, relative L2
+
+
+@pytest.fixture(scope="module")
+def X():
+    import paper_2604_02715_b200 as X
+
+    return X
+
+
+@pytest.fixture(scope="module")
+def O():
+    from oracle import xpg_oracle as O
+
+    return O
+
+
+def test_router_bit_exact_golden(X, golden):
+    from paper_2604_02715_b200.device import route_table
+
+    arrays, meta = golden
+    for key, c in meta["cases"].items():
+        if not key.startswith("route_"):
+            continue
+        got = route_table(int(c["seed"]), c["T"], c["N"], c["L"], c["k"]).cpu().numpy()
+        np.testing.assert_array_equal(got, arrays[key], err_msg=key)
+
+
+@pytest.mark.parametrize("L,k,T,N", [(8, 2, 256, 8), (128, 8, 256, 4), (256, 8, 256, 8), (1024, 32, 64, 2), (33, 5, 77, 3)])
+def test_router_bit_exact_oracle_full_sizes(X, O, L, k, T, N):
+    from paper_2604_02715_b200.device import route_table
+
+    for seed in (7, 0, 2**64 - 1, -12345):
+        got = route_table(seed, T, N, L, k).cpu().numpy()
+        want = O.route_all(seed, T, N, L, k)
+        np.testing.assert_array_equal(got, want)
+
+
+def test_routed_experts_single_token(X):
+    assert X.routed_experts(7, 0, 1, 8, 2) == [2, 6]
+    assert X.routed_experts(0, 0, 1, 1, 2) == [1]
+    assert X.routed_experts(2**64 + 7, 3, 1, 8, 2) == X.routed_experts(7, 3, 1, 8, 2)
+
+
+@pytest.mark.parametrize("ci", range(8))
+def test_layer_forward_golden(X, O, golden, ci):
+    arrays, meta = golden
+    c = meta["cases"][f"fwd_{ci}"]
+    spec = X.ModelSpec(c["N"], c["L"], c["H"], c["F"])
+    container = X.generate_synthetic_model(spec, c["wseed"])
+    fwd = X.ForwardSpec(c["T"], c["k"], int(c["rseed"]))
+    y = X.layer_forward(container.tensor_f32, spec, fwd, c["layer"], arrays[f"fwd_x_{ci}"])
+    err = O.rel_l2(y, arrays[f"fwd_y_{ci}"])
+    assert err <= TOL, err
+
+
+@pytest.mark.parametrize("ci", range(2))
+def test_resident_stack_golden(X, O, golden, ci):
+    arrays, meta = golden
+    c = meta["cases"][f"stack_{ci}"]
+    spec = X.ModelSpec(c["N"], c["L"], c["H"], c["F"])
+    container = X.generate_synthetic_model(spec, c["wseed"])
+    fwd = X.ForwardSpec(c["T"], c["k"], c["wseed"])
+    y = X.resident_baseline(c["iterations"], spec, container, fwd, acts=arrays[f"stack_x_{ci}"])
+    assert O.rel_l2(y, arrays[f"stack_y_{ci}"]) <= TOL * c["N"] * c["iterations"]
+
+
+def _hier(X, spec, seed=1, alpha=None, delay_fn=None):
+    container = X.generate_synthetic_model(spec, seed)
+    if alpha is None:
+        backends = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 30e9, 1 << 40)]
+    else:
+        backends = [X.Backend(1, X.BackendKind.COMPRESSED_DEVICE, 300e9, 1 << 40),
+                    X.Backend(2, X.BackendKind.HOST_OFFLOAD, 30e9, 1 << 40)]
+    plan = X.plan_placement(spec, backends, alpha=alpha)
+    return container, X.StorageHierarchy(container, None, plan, backends, delay_fn)
+
+
+@pytest.mark.parametrize("mode", ["sequential", "threaded"])
+@pytest.mark.parametrize("alpha", [None, 0.5])
+def test_streamed_equals_resident_bit_exact(X, mode, alpha):
+    spec = X.ModelSpec(4, 8, 256, 512)
+    fwd = X.ForwardSpec(16, 2, 7)
+    container, hier = _hier(X, spec, seed=7, alpha=alpha)
+    x = X.initial_activations(spec, fwd, 7)
+    rep = X.run_iterations(3, spec, hier, fwd, mode=mode, acts=x.copy())
+    base = X.resident_baseline(3, spec, container, fwd, acts=x.copy())
+    assert rep.page_fault is None
+    assert rep.violations == []
+    assert rep.final_activations.tobytes() == base.tobytes()
+    assert rep.arena_peak_bytes == 2 * spec.experts_per_layer * spec.expert_bytes
+
+
+def test_streamed_parity_with_oracle_per_layer(X, O, golden):
+    """A 1-iteration streamed run layer by layer against the oracle on fresh inputs."""
+    spec = X.ModelSpec(2, 8, 256, 512)
+    fwd = X.ForwardSpec(64, 2, 3)
+    container, hier = _hier(X, spec, seed=7)
+    pool = O.WordPool(2, 8, 256, 512, container.words)
+    x = np.random.default_rng(5).standard_normal((64, 256), dtype=np.float32)
+    rep = X.run_iterations(1, spec, hier, fwd, mode="threaded", acts=x)
+    want = O.resident_stack(pool, x, 2, 3, 1)
+    assert O.rel_l2(rep.final_activations, want) <= 2 * TOL
+
+
+@pytest.mark.parametrize("N,L", [(2, 1), (2, 3), (3, 1), (4, 2), (5, 3), (6, 2), (8, 4), (4, 8), (3, 5)])
+def test_slot_ids_and_log_match_reference(X, O, golden, N, L):
+    arrays, meta = golden
+    ci = next(k.split("_")[1] for k, c in meta["cases"].items()
+              if k.startswith("slots_") and c["N"] == N and c["L"] == L)
+    spec = X.ModelSpec(N, L, 16, 16)
+    _, hier = _hier(X, spec, seed=1)
+    trace = []
+    runner = X.StreamedRunner(spec, hier, X.ForwardSpec(2, 2, 1), mode="sequential", trace=trace)
+    rep = runner.run(3)
+    maps = []
+    for line in trace:
+        f = dict(kv.split("=") for kv in line.split())
+        if f["event"] == "map":
+            maps.append((int(f["layer"]), int(f["expert"]), int(f["kind"]), int(f["block"])))
+    assert maps == [tuple(r) for r in arrays[f"slots_{ci}"].tolist()]
+    ev = {0: "recycle", 1: "load-start", 2: "load-done", 3: "compute-start", 4: "compute-done"}
+    want = [(ev[r[0]], r[1], r[2], None if r[3] < 0 else r[3], None if r[4] < 0 else r[4], None if r[5] < 0 else r[5])
+            for r in arrays[f"order_{ci}"].tolist()]
+    got = [(r.event, r.iteration, r.layer, r.kind, r.target_iteration, r.target_layer) for r in rep.records]
+    assert got == want
+    assert rep.violations == []
+
+
+def test_threaded_log_is_clean_and_overlaps(X):
+    spec = X.ModelSpec(6, 2, 64, 64)
+    _, hier = _hier(X, spec, seed=5, alpha=0.5, delay_fn=lambda tid: 0.002)
+    runner = X.StreamedRunner(spec, hier, X.ForwardSpec(3, 2, 5), mode="threaded",
+                              compute_delay_fn=lambda it, ly: 0.004)
+    rep = runner.run(2)
+    assert rep.violations == []
+    overlaps = 0
+    for (it, ly), spans in rep.intervals.items():
+        nxt = (it, ly + 1) if ly < spec.num_layers else (it + 1, 1)
+        ns = rep.intervals.get(nxt)
+        if ns and "load1" in ns and "compute" in spans and ns["load1"][0] < spans["compute"][1]:
+            overlaps += 1
+    assert overlaps > 0
+    kind_overlaps = sum(1 for s in rep.intervals.values()
+                        if "load1" in s and "load2" in s and s["load1"][0] < s["load2"][1] and s["load2"][0] < s["load1"][1])
+    assert kind_overlaps > 0
+
+
+def test_injected_delays_stall_but_stay_exact(X):
+    spec = X.ModelSpec(4, 2, 64, 128)
+    fwd = X.ForwardSpec(3, 2, 5)
+    container, hier = _hier(X, spec, seed=3, alpha=0.5, delay_fn=lambda tid: 0.001)
+    x = X.initial_activations(spec, fwd, 3)
+    rep = X.run_iterations(2, spec, hier, fwd, mode="threaded", acts=x.copy())
+    base = X.resident_baseline(2, spec, container, fwd, acts=x.copy())
+    assert rep.final_activations.tobytes() == base.tobytes()
+    assert rep.violations == []
+    assert rep.stall_seconds > 0
+
+
+def test_sabotage_reports_raw_violation_and_page_fault(X):
+    spec = X.ModelSpec(4, 2, 64, 128)
+    _, hier = _hier(X, spec, seed=2, alpha=0.5, delay_fn=lambda tid: 0.03 if tid.layer == 3 else 0.0)
+    runner = X.StreamedRunner(spec, hier, X.ForwardSpec(3, 2, 5), mode="threaded", sabotage_skip_raw=(1, 3))
+    rep = runner.run(2)
+    assert rep.page_fault is not None
+    assert any(v.startswith("RAW") for v in rep.violations)
+
+
+def test_cold_start_and_war_targets(X):
+    spec = X.ModelSpec(4, 2, 64, 128)
+    _, hier = _hier(X, spec, seed=2)
+    rep = X.run_iterations(2, spec, hier, X.ForwardSpec(3, 2, 5), mode="threaded")
+    rec = [r for r in rep.records if r.event == "recycle"]
+    assert [r for r in rec if r.iteration == 1 and r.layer <= 2] == []
+    assert {(r.target_iteration, r.target_layer) for r in rec if r.iteration == 1 and r.layer == 3} == {(1, 1)}
+    assert {(r.target_iteration, r.target_layer) for r in rec if r.iteration == 2 and r.layer == 1} == {(1, 3)}
+
+
+def test_per_kind_window_never_exceeds_two_layers(X):
+    spec = X.ModelSpec(6, 2, 16, 32)
+    trace = []
+    _, hier = _hier(X, spec, seed=4, alpha=0.5)
+    X.StreamedRunner(spec, hier, X.ForwardSpec(3, 2, 5), mode="threaded", trace=trace).run(3)
+    mapped = {1: set(), 2: set()}
+    for line in trace:
+        f = dict(kv.split("=") for kv in line.split())
+        kind, layer = int(f["kind"]), int(f["layer"])
+        if f["event"] == "map":
+            mapped[kind].add(layer)
+        elif f["event"] == "unmap":
+            mapped[kind].discard(layer)
+        assert len(mapped[kind]) <= 2, line
+
+
+def test_zero_input_stays_zero(X):
+    spec = X.ModelSpec(4, 2, 64, 128)
+    _, hier = _hier(X, spec, seed=2)
+    zeros = np.zeros((3, 64), dtype=np.float32)
+    rep = X.run_iterations(1, spec, hier, X.ForwardSpec(3, 2, 5), mode="sequential", acts=zeros)
+    assert not rep.final_activations.any()
+
+
+def test_report_json_fields(X):
+    import json
+
+    spec = X.ModelSpec(4, 2, 64, 128)
+    _, hier = _hier(X, spec, seed=2)
+    doc = json.loads(X.run_iterations(1, spec, hier, X.ForwardSpec(3, 2, 5)).to_json())
+    for key in ("activation_checksum", "stall_ms", "arena_peak_bytes", "violation_count", "layer_intervals"):
+        assert key in doc
+    assert doc["violation_count"] == 0

@@ -1,0 +1,154 @@
+"""Host-side logic of the B200 package (no GPU): geometry, ids, placement, ordering."""
+
+import numpy as np
+import pytest
+
+import paper_2604_02715_b200 as X
+from paper_2604_02715_b200.errors import STATUS_CLASSES, raise_for_status
+from oracle import xpg_oracle as O
+
+TINY = X.ModelSpec(2, 2, 4, 8)
+
+
+def test_sigma_and_sizes():
+    assert TINY.sigma_gate_up == 2 * 4 * 16 == 128
+    assert TINY.sigma_down == 2 * 8 * 4 == 64
+    assert TINY.layer_bytes == 2 * (128 + 64)
+    assert TINY.total_bytes == 768
+    assert TINY.tensor_shape(X.TensorKind.GATE_UP) == (16, 4)
+    assert TINY.tensor_shape(X.TensorKind.DOWN) == (4, 8)
+
+
+def test_spec_validation():
+    for bad in [(1, 2, 4, 8), (2, 0, 4, 8), (2, 2, 0, 8)]:
+        with pytest.raises(X.OutOfRangeError):
+            X.ModelSpec(*bad)
+
+
+def test_tensor_offsets_match_oracle_and_tile_payload():
+    spec = X.ModelSpec(3, 5, 16, 24)
+    spans = []
+    for tid in X.iter_tensor_ids(spec):
+        off = X.tensor_offset(tid, spec)
+        assert off == O.tensor_offset(3, 5, 16, 24, tid.layer, tid.expert, int(tid.kind))
+        spans.append((off, off + spec.sigma(tid.kind)))
+    spans.sort()
+    assert spans[0][0] == 0 and spans[-1][1] == spec.total_bytes
+    assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+    with pytest.raises(X.OutOfRangeError):
+        X.tensor_offset(X.ExpertTensorId(4, 1, X.TensorKind.GATE_UP), spec)
+
+
+def test_generator_bit_identical_to_reference(golden):
+    _, meta = golden
+    for key, digest in meta["cases"].items():
+        if key.startswith("gen_"):
+            _, N, L, H, F, seed = key.split("_")
+            c = X.generate_synthetic_model(X.ModelSpec(int(N), int(L), int(H), int(F)), int(seed),
+                                           chunk_values=1000)
+            import hashlib
+
+            assert hashlib.sha256(c.payload).hexdigest() == digest, key
+
+
+def test_container_roundtrip_and_errors():
+    c = X.generate_synthetic_model(TINY, 5)
+    raw = c.to_bytes()
+    again = X.WeightContainer.from_bytes(raw)
+    assert again.spec == TINY and again.payload == c.payload
+    rebuilt = b"".join(c.tensor_bytes(t) for t in X.iter_tensor_ids(TINY))
+    assert rebuilt == c.payload
+    with pytest.raises(X.ContainerFormatError):
+        X.WeightContainer.from_bytes(b"NOPE" + raw[4:])
+    with pytest.raises(X.ContainerFormatError):
+        X.WeightContainer.from_bytes(raw[:-1])
+
+
+def test_bf16_conversions(golden):
+    arrays, _ = golden
+    np.testing.assert_array_equal(X.float32_to_bf16(arrays["bf16_in"]), arrays["bf16_out"])
+    assert X.float32_to_bf16(np.array([1.0], np.float32))[0] == 0x3F80
+
+
+@pytest.mark.parametrize("i,n,want", [(2, 48, 48), (3, 48, 1), (5, 48, 3), (1, 8, 7), (2, 8, 8), (1, 2, 1), (2, 2, 2)])
+def test_target_layer(i, n, want):
+    assert X.target_layer(i, n) == want == O.target_layer(i, n)
+
+
+def test_target_layer_range():
+    with pytest.raises(X.OutOfRangeError):
+        X.target_layer(3, 2)
+    with pytest.raises(X.OutOfRangeError):
+        X.target_layer(1, 1)
+
+
+def test_vaddr():
+    spec = X.ModelSpec(4, 3, 8, 16)
+    space = X.AddressSpace.for_spec(spec)
+    assert X.page_vaddr(X.ExpertTensorId(1, 1, X.TensorKind.GATE_UP), space) == space.base_gate_up
+    last = X.ExpertTensorId(4, 3, X.TensorKind.DOWN)
+    assert X.page_vaddr(last, space) == space.base_down + space.extent(X.TensorKind.DOWN) - spec.sigma_down
+    assert space.base_gate_up + space.extent(X.TensorKind.GATE_UP) <= space.base_down
+    sp2 = X.AddressSpace(X.ModelSpec(4, 8, 5, 5), 0, 10**9)
+    assert X.page_vaddr(X.ExpertTensorId(2, 3, X.TensorKind.GATE_UP), sp2) == 10 * sp2.spec.sigma_gate_up
+
+
+def test_placement_matches_reference(golden):
+    arrays, meta = golden
+    n = 0
+    for key, case in meta["cases"].items():
+        if not key.startswith("place_"):
+            continue
+        spec = X.ModelSpec(*case["spec"])
+        backends = [X.Backend(b[0], X.BackendKind(b[1]), b[2], b[3]) for b in case["backends"]]
+        plan = X.plan_placement(spec, backends, alpha=case["alpha"])
+        tab = np.zeros((spec.num_layers, spec.experts_per_layer, 2), dtype=np.int32)
+        for tid, bid in plan.assignment.items():
+            tab[tid.layer - 1, tid.expert - 1, int(tid.kind) - 1] = bid
+        np.testing.assert_array_equal(tab, arrays[key], err_msg=key)
+        for bid, frac in case["fractions"].items():
+            assert plan.fractions[int(bid)] == pytest.approx(frac)
+        assert X.estimate_load(plan, backends, spec).tau_load == pytest.approx(case["tau_load"])
+        n += 1
+    assert n == 12
+
+
+def test_placement_errors():
+    with pytest.raises(X.OutOfRangeError):
+        X.plan_placement(TINY, [])
+    b = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 1e9, 10)]
+    with pytest.raises(X.CapacityExceededError):
+        X.plan_placement(TINY, b)
+    with pytest.raises(X.OutOfRangeError):
+        X.Backend(1, X.BackendKind.HOST_OFFLOAD, 0, 1)
+
+
+def test_validate_ordering_constructed_logs():
+    R = X.OrderingRecord
+    war = [R(0, "load-done", 1, 1, 1), R(1, "load-done", 1, 1, 2), R(2, "compute-start", 1, 1),
+           R(3, "recycle", 1, 3, 1, 1, 1), R(4, "compute-done", 1, 1)]
+    v = X.validate_ordering(war)
+    assert len(v) == 1 and v[0].startswith("WAR")
+    raw = [R(0, "compute-start", 1, 1), R(1, "load-done", 1, 1, 1), R(2, "load-done", 1, 1, 2)]
+    v = X.validate_ordering(raw)
+    assert len(v) == 2 and all(s.startswith("RAW") for s in v)
+
+
+def test_status_codes_map_onto_reference_errors():
+    assert STATUS_CLASSES[4] is X.DoubleMapError and STATUS_CLASSES[7] is X.PageFaultError
+    with pytest.raises(X.PoolExhaustedError):
+        raise_for_status(5, "x")
+    raise_for_status(0, "")
+
+
+def test_storage_fetch_host_dest():
+    c = X.generate_synthetic_model(TINY, 3)
+    backends = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 1e9, 1 << 40)]
+    h = X.StorageHierarchy(c, None, X.plan_placement(TINY, backends), backends)
+    tid = X.ExpertTensorId(2, 1, X.TensorKind.DOWN)
+    dest = bytearray(TINY.sigma_down)
+    h.fetch(tid, memoryview(dest))
+    assert bytes(dest) == c.tensor_bytes(tid)
+    with pytest.raises(X.BackendMissError):
+        h.fetch(tid, memoryview(bytearray(3)))
+    assert h.backend_map().sum() == 0
