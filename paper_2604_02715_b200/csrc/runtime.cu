@@ -893,14 +893,20 @@ int xpgb_host_pool_register(xpgb_ctx* h, void* host_ptr, uint64_t bytes) {
     c->host = static_cast<uint8_t*>(host_ptr);
     c->host_owned = false;
     c->host_registered = false;
-    cudaError_t e = cudaHostRegister(host_ptr, bytes, cudaHostRegisterPortable);
-    if (e == cudaSuccess) {
-      c->host_registered = true;
-    } else if (e == cudaErrorHostMemoryAlreadyRegistered) {
-      cudaGetLastError();
-    } else {
-      c->host = nullptr;
-      CK(e);
+    cudaPointerAttributes attr;
+    cudaError_t q = cudaPointerGetAttributes(&attr, host_ptr);
+    const bool pinned = (q == cudaSuccess && attr.type == cudaMemoryTypeHost);
+    if (q != cudaSuccess) cudaGetLastError();
+    if (!pinned) {
+      cudaError_t e = cudaHostRegister(host_ptr, bytes, cudaHostRegisterPortable);
+      if (e == cudaSuccess) {
+        c->host_registered = true;
+      } else if (e == cudaErrorHostMemoryAlreadyRegistered) {
+        cudaGetLastError();
+      } else {
+        c->host = nullptr;
+        throw Err{XPGB_ERR_CUDA, std::string("cudaHostRegister: ") + cudaGetErrorString(e)};
+      }
     }
     c->host_bytes = bytes;
   });
