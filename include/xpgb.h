@@ -100,7 +100,7 @@ typedef struct xpgb_run_opts {
   const float* fetch_delay_s;   /* optional [N][L][2] seconds per tensor (delay_fn hook), host memory */
   const float* compute_delay_s; /* optional [iterations][N] seconds (compute_delay_fn hook), host memory */
   int32_t log_enable;        /* record the ordering log (default on) */
-  int32_t reserved;
+  int32_t profile;           /* time every MoE kernel launch with CUDA events (report.kern_*) */
 } xpgb_run_opts;
 
 typedef struct xpgb_report {
@@ -113,6 +113,14 @@ typedef struct xpgb_report {
   int64_t copy_busy_ns[2];   /* per copy stream: sum of load-start..load-done spans */
   int32_t page_fault;        /* 1 if a compute read a non-resident page */
   int32_t n_records;
+  /* opts.profile: mean device time per launch over the run (CUDA events on the compute stream) */
+  double kern_gate_up_ns;
+  double kern_down_ns;
+  double kern_aux_ns;        /* plan + gather + combine per layer */
+  int64_t gate_up_bytes;     /* mean algorithmic bytes per gate/up launch (weights of routed experts + rows) */
+  int64_t down_bytes;
+  int32_t down_splits;
+  int32_t active_experts;    /* routed experts summed over the N layers of one iteration */
 } xpgb_report;
 
 /* ---------------------------------------------------------------- basics */
@@ -130,6 +138,9 @@ int xpgb_sync(xpgb_ctx* ctx);
 /* ---------------------------------------------------------------- storage
  * WeightContainer payload (model.py:142-202) lives in a pinned host pool in
  * container order; StorageHierarchy.fetch (storage.py:228-243) copies from it. */
+/* Exact-size pinned (page-locked, portable) host allocation, no context needed. */
+int xpgb_pinned_alloc(uint64_t bytes, void** out);
+int xpgb_pinned_free(void* ptr);
 /* Allocate a pinned host pool of total_bytes; *host_ptr receives it for filling. */
 int xpgb_host_pool_alloc(xpgb_ctx* ctx, void** host_ptr, uint64_t* bytes);
 /* Use caller memory (cudaHostRegister'd here) as the host pool. */

@@ -44,13 +44,16 @@ class RunOpts(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("tokens", C.c_int32), ("top_k", C.c_int32), ("sequential", C.c_int32),
                 ("router_seed", C.c_uint64), ("sabotage_iteration", C.c_int32), ("sabotage_layer", C.c_int32),
                 ("fetch_delay_s", C.POINTER(C.c_float)), ("compute_delay_s", C.POINTER(C.c_float)),
-                ("log_enable", C.c_int32), ("reserved", C.c_int32)]
+                ("log_enable", C.c_int32), ("profile", C.c_int32)]
 
 
 class Report(C.Structure):
     _fields_ = [("stall_ns", C.c_int64), ("war_wait_ns", C.c_int64), ("elapsed_ns", C.c_int64),
                 ("arena_peak_bytes", C.c_int64), ("h2d_bytes", C.c_int64), ("d2d_bytes", C.c_int64),
-                ("copy_busy_ns", C.c_int64 * 2), ("page_fault", C.c_int32), ("n_records", C.c_int32)]
+                ("copy_busy_ns", C.c_int64 * 2), ("page_fault", C.c_int32), ("n_records", C.c_int32),
+                ("kern_gate_up_ns", C.c_double), ("kern_down_ns", C.c_double), ("kern_aux_ns", C.c_double),
+                ("gate_up_bytes", C.c_int64), ("down_bytes", C.c_int64), ("down_splits", C.c_int32),
+                ("active_experts", C.c_int32)]
 
 
 class KernelTimes(C.Structure):
@@ -71,6 +74,8 @@ _SIGS = {
     "xpgb_create": [C.POINTER(Spec), _I, _I, _I, C.POINTER(_P)],
     "xpgb_destroy": [_P],
     "xpgb_sync": [_P],
+    "xpgb_pinned_alloc": [_U64, C.POINTER(_P)],
+    "xpgb_pinned_free": [_P],
     "xpgb_host_pool_alloc": [_P, C.POINTER(_P), C.POINTER(_U64)],
     "xpgb_host_pool_register": [_P, _P, _U64],
     "xpgb_set_placement": [_P, C.POINTER(C.c_uint8)],

@@ -218,6 +218,8 @@ struct Ctx {
   // profiling
   bool prof = false;
   cudaEvent_t pev[7];
+  cudaEvent_t* cur_ev = nullptr;          // 7 events bracketing the next enqueue_forward
+  std::vector<cudaEvent_t> run_ev;        // per-step event sets for opts.profile
   xpgb_kernel_times last_times{};
 };
 
@@ -351,7 +353,8 @@ static int pick_splits(Ctx* c, int T, int kk, int bn) {
 }
 
 static void prof_rec(Ctx* c, int i, cudaStream_t s) {
-  if (c->prof) CK(cudaEventRecord(c->pev[i], s));
+  if (c->cur_ev) CK(cudaEventRecord(c->cur_ev[i], s));
+  else if (c->prof) CK(cudaEventRecord(c->pev[i], s));
 }
 
 // layer_forward (pipeline.py:192-208) on `s`: y may alias x.
@@ -602,7 +605,9 @@ static void forward_step(RunState& rs, int g, int it, int layer) {
   }
   const int kk = std::min(o->top_k, c->L);
   const int32_t* topk = c->topk_all + (size_t)(layer - 1) * o->tokens * kk;
+  c->cur_ev = o->profile ? &c->run_ev[(size_t)g * 7] : nullptr;
   enqueue_forward(c, layer, rs.acts, rs.acts, o->tokens, o->top_k, o->router_seed, topk, s);
+  c->cur_ev = nullptr;
   log_only(c, rs.log, s, XPGB_EV_COMPUTE_DONE, it, layer);
   CK(cudaEventRecord(c->ev_comp[g & 3], s));
   if (o->sequential) CK(cudaStreamSynchronize(s));
@@ -623,6 +628,13 @@ static void run_impl(Ctx* c, const xpgb_run_opts* o, const float* x, float* y, x
   }
   const bool log = o->log_enable != 0;
   ensure_log(c, steps * 8 + 16);
+  if (o->profile) {
+    while (c->run_ev.size() < (size_t)steps * 7) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      c->run_ev.push_back(e);
+    }
+  }
   CK(cudaMemset(c->d_fault, 0, sizeof(long long)));
   const bool paged = c->pool == XPGB_POOL_RING;
   if (paged) {
@@ -725,6 +737,40 @@ static void run_impl(Ctx* c, const xpgb_run_opts* o, const float* x, float* y, x
   long long fw = 0;
   CK(cudaMemcpy(&fw, c->d_fault, sizeof(fw), cudaMemcpyDeviceToHost));
   rep->page_fault = fw != 0;
+
+  // routed experts per layer (routing is iteration-invariant) -> algorithmic bytes
+  if (o->tokens > 0) {
+    std::vector<int32_t> tk((size_t)N * o->tokens * kk);
+    CK(cudaMemcpy(tk.data(), c->topk_all, tk.size() * 4, cudaMemcpyDeviceToHost));
+    long long active = 0;
+    for (int l = 0; l < N; ++l) {
+      std::vector<char> seen(c->L + 1, 0);
+      for (size_t i = 0; i < (size_t)o->tokens * kk; ++i) {
+        const int e = tk[(size_t)l * o->tokens * kk + i];
+        const int el = e - 1 - c->e_first;
+        if (el >= 0 && el < c->E && !seen[e]) { seen[e] = 1; ++active; }
+      }
+    }
+    const long long pairs = (long long)o->tokens * kk;
+    rep->active_experts = (int32_t)active;
+    rep->down_splits = c->last_times.down_splits;
+    rep->gate_up_bytes = (long long)((double)active / N * c->s1) + pairs * c->H * 2 + pairs * c->F * 2;
+    rep->down_bytes = (long long)((double)active / N * c->s2) + pairs * c->F * 2 +
+                      pairs * (long long)c->H * 4 * std::max(1, rep->down_splits);
+  }
+  if (o->profile && steps > 0) {
+    double gu = 0, dn = 0, aux = 0;
+    for (int g = 0; g < steps; ++g) {
+      float ms[6];
+      for (int i = 0; i < 6; ++i) CK(cudaEventElapsedTime(&ms[i], c->run_ev[(size_t)g * 7 + i], c->run_ev[(size_t)g * 7 + i + 1]));
+      gu += ms[3];
+      dn += ms[4];
+      aux += ms[1] + ms[2] + ms[5];
+    }
+    rep->kern_gate_up_ns = gu * 1e6 / steps;
+    rep->kern_down_ns = dn * 1e6 / steps;
+    rep->kern_aux_ns = aux * 1e6 / steps;
+  }
 
   if (paged) {
     // drain: the last two layers are still bound; release them like a finished
@@ -851,6 +897,7 @@ int xpgb_destroy(xpgb_ctx* h) {
     cudaEventDestroy(c->ev_begin);
     cudaEventDestroy(c->ev_end);
     for (int i = 0; i < 7; ++i) cudaEventDestroy(c->pev[i]);
+    for (cudaEvent_t e : c->run_ev) cudaEventDestroy(e);
     cudaStreamDestroy(c->s_comp);
     delete h;
   });
@@ -858,6 +905,18 @@ int xpgb_destroy(xpgb_ctx* h) {
 
 int xpgb_sync(xpgb_ctx* h) {
   return guard([&] { CK(cudaDeviceSynchronize()); (void)h; });
+}
+
+int xpgb_pinned_alloc(uint64_t bytes, void** out) {
+  return guard([&] {
+    *out = nullptr;
+    CK(cudaHostAlloc(out, std::max<uint64_t>(bytes, 1), cudaHostAllocPortable));
+  });
+}
+int xpgb_pinned_free(void* ptr) {
+  return guard([&] {
+    if (ptr) CK(cudaFreeHost(ptr));
+  });
 }
 
 int xpgb_host_pool_alloc(xpgb_ctx* h, void** host_ptr, uint64_t* bytes) {

@@ -105,6 +105,7 @@ class RunReport:
     d2d_bytes: int = 0
     copy_busy_seconds: tuple = (0.0, 0.0)
     elapsed_seconds: float = 0.0
+    kernels: dict = field(default_factory=dict)
 
     @property
     def checksum(self) -> str:
@@ -164,7 +165,7 @@ def _records_from_log(ctx: Context):
 
 
 def _run_context(ctx: Context, spec: ModelSpec, fwd: ForwardSpec, iterations: int, acts, sequential: bool,
-                 fetch_delay=None, compute_delay=None, sabotage=None, log: bool = True):
+                 fetch_delay=None, compute_delay=None, sabotage=None, log: bool = True, profile: bool = False):
     torch = _torch()
     x, was_numpy = as_device_f32(acts, ctx.device, fwd.tokens_per_step, spec.hidden_dim)
     y = torch.empty_like(x)
@@ -185,6 +186,7 @@ def _run_context(ctx: Context, spec: ModelSpec, fwd: ForwardSpec, iterations: in
         keep.append(cd)
         opts.compute_delay_s = cd.ctypes.data_as(C.POINTER(C.c_float))
     opts.log_enable = 1 if log else 0
+    opts.profile = 1 if profile else 0
     rep = _lib.Report()
     torch.cuda.current_stream(ctx.device).synchronize()
     call("xpgb_run", ctx.handle, C.byref(opts), C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), C.byref(rep))
@@ -212,7 +214,7 @@ class StreamedRunner:
         self.stall_seconds = 0.0
         self.war_wait_seconds = 0.0
 
-    def run(self, iterations: int, acts=None) -> RunReport:
+    def run(self, iterations: int, acts=None, profile: bool = False) -> RunReport:
         if iterations < 1:
             raise XpgError("need at least one iteration")
         if acts is None:
@@ -223,7 +225,7 @@ class StreamedRunner:
                            for it in range(1, iterations + 1)], dtype=np.float32)
         out, rep = _run_context(self.ctx, self.spec, self.fwd, iterations, acts, self.mode == "sequential",
                                 fetch_delay=self.hierarchy.delay_table(), compute_delay=cd,
-                                sabotage=self.sabotage_skip_raw)
+                                sabotage=self.sabotage_skip_raw, profile=profile)
         self.table.sync_trace()
         records = _records_from_log(self.ctx)
         self.stall_seconds = rep.stall_ns * 1e-9
@@ -241,7 +243,16 @@ class StreamedRunner:
             d2d_bytes=int(rep.d2d_bytes),
             copy_busy_seconds=(rep.copy_busy_ns[0] * 1e-9, rep.copy_busy_ns[1] * 1e-9),
             elapsed_seconds=rep.elapsed_ns * 1e-9,
+            kernels=_kernel_stats(rep),
         )
+
+
+def _kernel_stats(rep) -> dict:
+    return {
+        "gate_up_ns": rep.kern_gate_up_ns, "down_ns": rep.kern_down_ns, "aux_ns": rep.kern_aux_ns,
+        "gate_up_bytes": int(rep.gate_up_bytes), "down_bytes": int(rep.down_bytes),
+        "down_splits": int(rep.down_splits), "active_experts": int(rep.active_experts),
+    }
 
 
 def run_iterations(iterations: int, spec: ModelSpec, hierarchy: StorageHierarchy, fwd: ForwardSpec,
@@ -276,8 +287,8 @@ class ResidentModel:
             raise PageFaultError(fault)
         return y.cpu().numpy() if was_numpy else y
 
-    def run(self, iterations: int, fwd: ForwardSpec, acts, log: bool = False):
-        return _run_context(self.ctx, self.spec, fwd, iterations, acts, sequential=False, log=log)
+    def run(self, iterations: int, fwd: ForwardSpec, acts, log: bool = False, profile: bool = False):
+        return _run_context(self.ctx, self.spec, fwd, iterations, acts, sequential=False, log=log, profile=profile)
 
 
 _RESIDENT_CACHE: dict = {}
