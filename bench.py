@@ -220,6 +220,7 @@ def main():
     ap.add_argument("--ref-sample-tokens", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-resident", action="store_true")
+    ap.add_argument("--ep", action="store_true", help="use the expert-parallel runner even at N=1")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.tokens:
@@ -241,15 +242,29 @@ def main():
     spec = X.ModelSpec(N, L, H, F)
     fwd = X.ForwardSpec(T, k, SEED)
     t0 = time.time()
-    container = X.generate_fast_model(spec, SEED + rank, device=dev)
+    use_ep = world > 1 or args.ep
+    if use_ep:
+        from paper_2604_02715_b200.expert_parallel import ExpertParallelRunner, shard_bounds
+
+        first, count = shard_bounds(L, world)[rank]
+        # each rank holds only its expert shard (shard-local container order) in pinned memory
+        shard = X.generate_fast_model(X.ModelSpec(N, count, H, F), SEED + 1000 * rank, device=dev)
+        container = None
+    else:
+        container = X.generate_fast_model(spec, SEED + rank, device=dev)
     gen_s = time.time() - t0
-    log(f"model generated ({spec.total_bytes / 1e9:.1f} GB pinned) in {gen_s:.1f}s")
-    backends = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 55e9, 1 << 50)]
-    hier = X.StorageHierarchy(container, None, X.plan_placement(spec, backends), backends)
-    runner = X.StreamedRunner(spec, hier, fwd, mode="threaded", device=dev)
-    x_host = X.initial_activations(spec, fwd, SEED)
+    log(f"model generated in {gen_s:.1f}s")
+    if use_ep:
+        group = None
+        runner = ExpertParallelRunner(spec, None, fwd, rank, world, device=dev, group=group, shard_pool=shard.pinned)
+        budget = 2.0 / N  # 2-layer ring of this rank's shard
+    else:
+        backends = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 55e9, 1 << 50)]
+        hier = X.StorageHierarchy(container, None, X.plan_placement(spec, backends), backends)
+        runner = X.StreamedRunner(spec, hier, fwd, mode="threaded", device=dev)
+        budget = runner.table.pool_bytes / spec.total_bytes
+    x_host = X.initial_activations(spec, fwd, SEED + rank)
     x_dev = torch.from_numpy(x_host).to(f"cuda:{dev}")
-    budget = runner.table.pool_bytes / spec.total_bytes
 
     # ---- warm-up (untimed)
     log("warm-up")
@@ -282,7 +297,9 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(e2e_steps):
-        out = runner.run(1, acts=x_host).final_activations  # numpy in -> H2D, D2H -> numpy out
+        out = runner.run(1, acts=x_host).final_activations  # numpy in -> H2D, D2H -> host out
+        if hasattr(out, "cpu"):
+            out = out.cpu().numpy()
     e1.record()
     torch.cuda.synchronize()
     e2e_elapsed = max_over_ranks(torch, world, e0.elapsed_time(e1) * 1e-3, dev)
@@ -293,7 +310,7 @@ def main():
     # ---- fully-resident comparator: same kernels, every page resident in HBM
     resident = {}
     kern = rep.kernels
-    if not args.no_resident:
+    if not args.no_resident and not use_ep:
         del runner
         model = X.ResidentModel(spec, container, device=dev, max_tokens=T)
         model.run(args.warmup, fwd, x_dev)
@@ -346,9 +363,12 @@ def main():
         "clocks": clocks.summary(),
         "model_gen_s": gen_s,
     }
-    if not args.no_resident:
+    if not args.no_resident and not use_ep:
         line["paged_kernels"] = paged_kern
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if use_ep:
+        line["config"]["parallelism"] = f"ep{world} (experts sharded, NCCL all_to_all dispatch/combine)"
+        line["config"]["tokens_per_rank"] = T
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and container is not None:
         os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count() or 1))
         import numpy as np  # noqa: F811
 

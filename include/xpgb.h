@@ -188,6 +188,17 @@ int xpgb_fault_clear(xpgb_ctx* ctx);
 /* ---------------------------------------------------------------- schedule (pipeline.py:299-483) */
 /* StreamedRunner.run: x_dev/y_dev are [T][H] fp32 device buffers (y may alias x). */
 int xpgb_run(xpgb_ctx* ctx, const xpgb_run_opts* opts, const float* x_dev, float* y_dev, xpgb_report* rep);
+/* The same schedule one step at a time, so the compute of a step can be external
+ * (e.g. expert-parallel dispatch/GEMM/combine over NCCL).  Step g = (iteration-1)*N + layer-1.
+ * Order: begin; materialize(0); materialize(1); for g: acquire(g, s); <compute on s>;
+ * release(g, s); materialize(g+2); end.  acts_dev (fp32 [T][H]) enables session_compute. */
+int xpgb_session_begin(xpgb_ctx* ctx, const xpgb_run_opts* opts, float* acts_dev);
+int xpgb_session_materialize(xpgb_ctx* ctx, int32_t step);  /* _materialize, pipeline.py:335-360 */
+int xpgb_session_acquire(xpgb_ctx* ctx, int32_t step, void* stream); /* RAW wait + compute-start */
+int xpgb_session_compute(xpgb_ctx* ctx, int32_t step);      /* built-in layer_forward of the step */
+int xpgb_session_release(xpgb_ctx* ctx, int32_t step, void* stream); /* compute-done + WAR event */
+int xpgb_session_end(xpgb_ctx* ctx, xpgb_report* rep);
+int xpgb_session_abort(xpgb_ctx* ctx);
 /* Ordering log of the last run (OrderingLog.records, pipeline.py:94-116). */
 int xpgb_log_get(xpgb_ctx* ctx, xpgb_record* out, int32_t cap, int32_t* n);
 
@@ -200,6 +211,12 @@ int xpgb_set_expert_shard(xpgb_ctx* ctx, int32_t expert_first, int32_t expert_co
  * out_dev fp32 [n_rows][H] (expert output, unscaled).  Pages must be resident. */
 int xpgb_experts_forward(xpgb_ctx* ctx, int32_t layer, const void* rows_dev, const int32_t* offsets_dev,
                          int32_t n_rows, float* out_dev, void* stream);
+
+/* Ordered combine (pipeline.py:198-207) of rows returned by the expert owners:
+ * y[t] = sum_{s ascending} rows[index[t][s]] * f32(1/top_k); index < 0 skips the slot.
+ * rows fp32 [*][hidden], index int32 [tokens][kk], kk = number of routed slots. */
+int xpgb_combine_rows(const float* rows_dev, const int32_t* index_dev, int32_t tokens, int32_t kk, int32_t top_k,
+                      int32_t hidden, float* y_dev, void* stream);
 
 /* Per-kernel device timing of the last layer_forward/run (ns, CUDA events). */
 typedef struct xpgb_kernel_times {

@@ -99,9 +99,17 @@ _SIGS = {
     "xpgb_fault_get": [_P, C.POINTER(_I), C.c_char_p, _U64],
     "xpgb_fault_clear": [_P],
     "xpgb_run": [_P, C.POINTER(RunOpts), _P, _P, C.POINTER(Report)],
+    "xpgb_session_begin": [_P, C.POINTER(RunOpts), _P],
+    "xpgb_session_materialize": [_P, _I],
+    "xpgb_session_acquire": [_P, _I, _P],
+    "xpgb_session_compute": [_P, _I],
+    "xpgb_session_release": [_P, _I, _P],
+    "xpgb_session_end": [_P, C.POINTER(Report)],
+    "xpgb_session_abort": [_P],
     "xpgb_log_get": [_P, C.POINTER(Record), _I, C.POINTER(_I)],
     "xpgb_set_expert_shard": [_P, _I, _I],
     "xpgb_experts_forward": [_P, _I, _P, _P, _I, _P, _P],
+    "xpgb_combine_rows": [_P, _P, _I, _I, _I, _I, _P, _P],
     "xpgb_profile_layer": [_P, _I, _P, _P, _I, _I, _U64, _I, C.POINTER(KernelTimes)],
 }
 _RESTYPES = {"xpgb_last_error": C.c_char_p, "xpgb_kernel_launches": C.c_int64}

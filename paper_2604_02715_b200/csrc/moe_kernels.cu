@@ -1,10 +1,11 @@
 // MoE layer kernels for sm_100a:
-//   k_route      hash router top-k (bit-exact with xpg pipeline.py:154-170)
-//   k_plan       expert-major permutation, page-table read + fault check, GEMM work lists
-//   k_gather     fp32 token rows -> bf16 expert-major rows
-//   k_gate_up    grouped GEMM  X_e * Wgu_e^T with fused SwiGLU epilogue (tcgen05 + TMA + TMEM)
-//   k_down       grouped GEMM  h_e * Wd_e^T, split-K partials (tcgen05 + TMA + TMEM)
-//   k_combine    ordered per-token weighted sum (pipeline.py:198-207)
+//   k_route        hash router top-k (bit-exact with xpg pipeline.py:154-170)
+//   k_route_plan   router + per-expert counts + expert-major positions, one CTA per layer
+//   k_gather       fp32 token rows -> bf16 expert-major rows (first layer of a run)
+//   k_moe_gemm     grouped GEMM, tcgen05 + TMA + TMEM, persistent; two instantiations:
+//                    gate/up:  X_e * Wgu_e^T with the SwiGLU epilogue -> bf16 h rows
+//                    down:     h_e * Wd_e^T, split-K partials          -> fp32 rows
+//   k_combine      ordered per-token weighted sum (pipeline.py:198-207) + next-layer gather
 #include <cuda_bf16.h>
 #include <cstdio>
 
@@ -23,20 +24,15 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   return z ^ (z >> 31);
 }
 
-// One warp per (layer, token).  Lane l owns experts j = l+1, l+33, ...; each of
-// the kk rounds takes the warp-wide minimum of (score, j) among untaken
-// candidates (ties broken by the smaller j, as the reference's tuple sort), and
-// the selected ids are finally written in ascending order.
-__global__ void k_route(uint64_t seed, int layer_first, int layer_count, int T, int L, int top_k,
-                        int32_t* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  const long long gw = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  if (gw >= (long long)layer_count * T) return;
-  const int li = (int)(gw / T), t = (int)(gw % T);
-  const int layer = layer_first + li;
-  const int kk = min(top_k, L);
-  const uint64_t base = seed * 0x9E37ull + (uint64_t)(uint32_t)layer * 0xC2B2ull + (uint64_t)(uint32_t)t * 0x85EBull;
-  const int ncand = (L - lane + 31) / 32;  // candidates owned by this lane
+// Warp-cooperative top-k of one (layer, token).  Lane l owns experts
+// j = l+1, l+33, ...; each of the kk rounds takes the warp-wide minimum of
+// (score, j) over untaken candidates (ties -> smaller j, the reference's tuple
+// order).  Returns, in lanes 0..kk-1, the selected id and its ascending rank.
+__device__ __forceinline__ void route_token(uint64_t seed, int layer, int t, int L, int kk, int lane, int* id,
+                                            int* rank) {
+  const uint64_t base =
+      seed * 0x9E37ull + (uint64_t)(uint32_t)layer * 0xC2B2ull + (uint64_t)(uint32_t)t * 0x85EBull;
+  const int ncand = (L - lane + 31) / 32;
   uint32_t taken = 0;
   int mine = 0x7fffffff;
   for (int r = 0; r < kk; ++r) {
@@ -57,12 +53,22 @@ __global__ void k_route(uint64_t seed, int layer_first, int layer_count, int T, 
     if (((bj - 1) & 31) == lane) taken |= 1u << ((bj - 1) >> 5);
     if (lane == r) mine = bj;
   }
-  int rank = 0;
-  for (int i = 0; i < kk; ++i) {
-    const int other = __shfl_sync(0xffffffffu, mine, i);
-    rank += (other < mine);
-  }
-  if (lane < kk) out[((long long)li * T + t) * kk + rank] = mine;
+  int rk = 0;
+  for (int i = 0; i < kk; ++i) rk += (__shfl_sync(0xffffffffu, mine, i) < mine);
+  *id = mine;
+  *rank = rk;
+}
+
+__global__ void k_route(uint64_t seed, int layer_first, int layer_count, int T, int L, int top_k,
+                        int32_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const long long gw = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (gw >= (long long)layer_count * T) return;
+  const int li = (int)(gw / T), t = (int)(gw % T);
+  const int kk = min(top_k, L);
+  int id, rank;
+  route_token(seed, layer_first + li, t, L, kk, lane, &id, &rank);
+  if (lane < kk) out[((long long)li * T + t) * kk + rank] = id;
 }
 
 void launch_route(uint64_t seed, int layer_first, int layer_count, int T, int L, int top_k, int32_t* out,
@@ -74,8 +80,6 @@ void launch_route(uint64_t seed, int layer_first, int layer_count, int T, int L,
   k_route<<<(unsigned)blocks, threads, 0, s>>>(seed, layer_first, layer_count, T, L, top_k, out);
   note_launch();
 }
-
-// ============================================================================ plan
 
 // Block-wide exclusive scan of one int per thread (blockDim.x == 1024).
 __device__ int block_exclusive_scan(int v, int* warp_tot, int* total) {
@@ -95,7 +99,7 @@ __device__ int block_exclusive_scan(int v, int* warp_tot, int* total) {
       const int y = __shfl_up_sync(0xffffffffu, s, off);
       if (lane >= off) s += y;
     }
-    warp_tot[lane] = s;  // inclusive
+    warp_tot[lane] = s;
     if (lane == 31) *total = s;
   }
   __syncthreads();
@@ -104,145 +108,73 @@ __device__ int block_exclusive_scan(int v, int* warp_tot, int* total) {
   return excl;
 }
 
-struct PlanShared {
-  int cnt[kMaxExperts];
-  int off[kMaxExperts];
-  int cur[kMaxExperts];
-  int warp_tot[32];
-  int total;
-  int fault;
-};
-
-// Resolve slots, emit GEMM units.  Shared by the routed and the pre-grouped (EP) plans.
-__device__ void plan_tail(PlanShared& sh, const LayerWork& w, const int32_t* pt_gu, const int32_t* pt_dn,
-                          int layer, int e_first, int e_count, int F, int H, int bn1, int bn2, int splits) {
-  const int tid = threadIdx.x;
-  const int e = tid;
-  const int n = (e < e_count) ? sh.cnt[e] : 0;
-  if (e < e_count) {
-    w.offsets[e] = sh.off[e];
-    if (e == e_count - 1) w.offsets[e_count] = sh.off[e] + n;
-    int sg = -1, sd = -1;
-    if (n > 0) {
-      // read_page semantics (paging.py:228-237): only RESIDENT pages may be read.
-      const int32_t eg = pt_gu[(long long)(layer - 1) * e_count + e];
-      const int32_t ed = pt_dn[(long long)(layer - 1) * e_count + e];
-      if (pt_state(eg) != 2) {
-        atomicCAS((unsigned long long*)w.fault, 0ull,
-                  (unsigned long long)fault_pack(layer, e_first + e + 1, 1, pt_state(eg)));
-        sh.fault = 1;
-      } else {
-        sg = pt_block0(eg);
-      }
-      if (pt_state(ed) != 2) {
-        atomicCAS((unsigned long long*)w.fault, 0ull,
-                  (unsigned long long)fault_pack(layer, e_first + e + 1, 2, pt_state(ed)));
-        sh.fault = 1;
-      } else {
-        sd = pt_block0(ed);
-      }
+// One CTA (1024 threads) per layer: route every token, count rows per local
+// expert, exclusive-scan the counts into row offsets, place each (token, slot)
+// pair.  Row order inside an expert is irrelevant to the result: every GEMM
+// output column depends only on its own activation row.
+__global__ void __launch_bounds__(1024, 1)
+    k_route_plan(uint64_t seed, int layer_first, int T, int L, int top_k, int e_first, int E,
+                 int32_t* __restrict__ topk, int32_t* __restrict__ pos, int32_t* __restrict__ offsets,
+                 const long long* __restrict__ fault) {
+  __shared__ int cnt[kMaxExperts];
+  __shared__ int warp_tot[32];
+  __shared__ int total;
+  if (fault && *fault) return;
+  const int li = blockIdx.x, layer = layer_first + li;
+  const int kk = min(top_k, L);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  int32_t* tk = topk + (long long)li * T * kk;
+  int32_t* ps = pos + (long long)li * T * kk;
+  int32_t* of = offsets + (long long)li * (E + 1);
+  for (int e = threadIdx.x; e < E; e += blockDim.x) cnt[e] = 0;
+  __syncthreads();
+  for (int t = warp; t < T; t += nwarps) {
+    int id, rank;
+    route_token(seed, layer, t, L, kk, lane, &id, &rank);
+    if (lane < kk) {
+      tk[(long long)t * kk + rank] = id;
+      const int el = id - 1 - e_first;
+      if (el >= 0 && el < E) atomicAdd(&cnt[el], 1);
     }
-    w.slot_gu[e] = sg;
-    w.slot_dn[e] = sd;
   }
   __syncthreads();
-  const int mt1 = (F + kBM - 1) / kBM, mt2 = (H + kBM - 1) / kBM;
-  const int nt1 = (n + bn1 - 1) / bn1, nt2 = (n + bn2 - 1) / bn2;
-  const int u1 = sh.fault ? 0 : nt1 * mt1;
-  const int u2 = sh.fault ? 0 : nt2 * mt2 * splits;
-  const int b1 = block_exclusive_scan(u1, sh.warp_tot, &sh.total);
-  const int tot1 = sh.total;
+  int carry = 0;
+  for (int e0 = 0; e0 < E; e0 += blockDim.x) {
+    const int e = e0 + threadIdx.x;
+    const int v = e < E ? cnt[e] : 0;
+    const int ex = block_exclusive_scan(v, warp_tot, &total);
+    if (e < E) {
+      of[e] = carry + ex;
+      cnt[e] = carry + ex;  // becomes the placement cursor
+    }
+    carry += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) of[E] = carry;
   __syncthreads();
-  const int b2 = block_exclusive_scan(u2, sh.warp_tot, &sh.total);
-  const int tot2 = sh.total;
-  if (u1 > 0) {
-    int idx = b1;
-    for (int m = 0; m < mt1; ++m)
-      for (int t = 0; t < nt1; ++t) {
-        const int rows = min(bn1, n - t * bn1);
-        w.units1[idx++] = GemmUnit{e, m * kBM, sh.off[e] + t * bn1, rows};
-      }
-  }
-  if (u2 > 0) {
-    int idx = b2;
-    for (int m = 0; m < mt2; ++m)
-      for (int s = 0; s < splits; ++s)
-        for (int t = 0; t < nt2; ++t) {
-          const int rows = min(bn2, n - t * bn2);
-          w.units2[idx++] = GemmUnit{e, m * kBM, sh.off[e] + t * bn2, rows | (s << 16)};
-        }
-  }
-  if (tid == 0) {
-    w.counters[0] = tot1;
-    w.counters[1] = tot2;
+  for (int p = threadIdx.x; p < T * kk; p += blockDim.x) {
+    const int el = tk[p] - 1 - e_first;
+    ps[p] = (el >= 0 && el < E) ? atomicAdd(&cnt[el], 1) : -1;
   }
 }
 
-__global__ void __launch_bounds__(1024, 1)
-    k_plan(LayerWork w, const int32_t* __restrict__ pt_gu, const int32_t* __restrict__ pt_dn, int layer, int T,
-           int kk, int e_first, int e_count, int F, int H, int bn1, int bn2, int splits) {
-  __shared__ PlanShared sh;
-  const int tid = threadIdx.x;
-  const int pairs = T * kk;
-  if (tid == 0) sh.fault = (*(volatile long long*)w.fault != 0);
-  for (int e = tid; e < e_count; e += blockDim.x) sh.cnt[e] = 0;
-  __syncthreads();
-  if (sh.fault) {
-    if (tid == 0) { w.counters[0] = 0; w.counters[1] = 0; w.counters[2] = 0; }
-    return;
-  }
-  for (int p = tid; p < pairs; p += blockDim.x) {
-    const int e = w.topk[p] - 1 - e_first;
-    if (e >= 0 && e < e_count) atomicAdd(&sh.cnt[e], 1);
-  }
-  __syncthreads();
-  const int v = (tid < e_count) ? sh.cnt[tid] : 0;
-  const int ex = block_exclusive_scan(v, sh.warp_tot, &sh.total);
-  if (tid < e_count) { sh.off[tid] = ex; sh.cur[tid] = ex; }
-  if (tid == 0) w.counters[2] = sh.total;
-  __syncthreads();
-  // Row order inside an expert is irrelevant to the result: every output
-  // column of the GEMM depends only on its own activation row.
-  for (int p = tid; p < pairs; p += blockDim.x) {
-    const int e = w.topk[p] - 1 - e_first;
-    w.pos[p] = (e >= 0 && e < e_count) ? atomicAdd(&sh.cur[e], 1) : -1;
-  }
-  __syncthreads();
-  plan_tail(sh, w, pt_gu, pt_dn, layer, e_first, e_count, F, H, bn1, bn2, splits);
-}
-
-__global__ void __launch_bounds__(1024, 1)
-    k_plan_rows(LayerWork w, const int32_t* __restrict__ offsets_in, const int32_t* __restrict__ pt_gu,
-                const int32_t* __restrict__ pt_dn, int layer, int e_first, int e_count, int F, int H, int bn1,
-                int bn2, int splits) {
-  __shared__ PlanShared sh;
-  const int tid = threadIdx.x;
-  if (tid == 0) sh.fault = (*(volatile long long*)w.fault != 0);
-  if (tid < e_count) {
-    sh.off[tid] = offsets_in[tid];
-    sh.cnt[tid] = offsets_in[tid + 1] - offsets_in[tid];
-  }
-  __syncthreads();
-  if (sh.fault) {
-    if (tid == 0) { w.counters[0] = 0; w.counters[1] = 0; }
-    return;
-  }
-  plan_tail(sh, w, pt_gu, pt_dn, layer, e_first, e_count, F, H, bn1, bn2, splits);
-}
-
-void launch_plan(const LayerWork& w, const int32_t* pt_gu, const int32_t* pt_dn, int layer, int T, int kk,
-                 int e_first, int e_count, int F, int H, int bn1, int bn2, int splits, cudaStream_t s) {
-  k_plan<<<1, 1024, 0, s>>>(w, pt_gu, pt_dn, layer, T, kk, e_first, e_count, F, H, bn1, bn2, splits);
-  note_launch();
-}
-void launch_plan_rows(const LayerWork& w, const int32_t* offsets_in, const int32_t* pt_gu, const int32_t* pt_dn,
-                      int layer, int e_first, int e_count, int F, int H, int bn1, int bn2, int splits,
-                      cudaStream_t s) {
-  k_plan_rows<<<1, 1024, 0, s>>>(w, offsets_in, pt_gu, pt_dn, layer, e_first, e_count, F, H, bn1, bn2, splits);
+void launch_route_plan(uint64_t seed, int layer_first, int layer_count, int T, int L, int top_k, int e_first, int E,
+                       int32_t* topk, int32_t* pos, int32_t* offsets, const long long* fault, cudaStream_t s) {
+  if (layer_count <= 0) return;
+  k_route_plan<<<layer_count, 1024, 0, s>>>(seed, layer_first, T, L, top_k, e_first, E, topk, pos, offsets, fault);
   note_launch();
 }
 
 // ============================================================================ gather / combine
+
+__device__ __forceinline__ uint2 pack_bf16x4(float4 v) {
+  __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y);
+  __nv_bfloat162 b = __floats2bfloat162_rn(v.z, v.w);
+  uint2 r;
+  r.x = *reinterpret_cast<uint32_t*>(&a);
+  r.y = *reinterpret_cast<uint32_t*>(&b);
+  return r;
+}
 
 // One block per token: convert the fp32 row to bf16 once, store it at each of
 // its kk expert-major positions (8-byte vector stores).
@@ -254,34 +186,35 @@ __global__ void k_gather(const float* __restrict__ x, const int32_t* __restrict_
   int p[kMaxTopK];
   for (int s = 0; s < kk; ++s) p[s] = pos[t * kk + s];
   for (int i = threadIdx.x; i < H / 4; i += blockDim.x) {
-    const float4 v = xr[i];
-    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y);
-    __nv_bfloat162 b = __floats2bfloat162_rn(v.z, v.w);
-    uint2 packed;
-    packed.x = *reinterpret_cast<uint32_t*>(&a);
-    packed.y = *reinterpret_cast<uint32_t*>(&b);
+    const uint2 packed = pack_bf16x4(xr[i]);
     for (int s = 0; s < kk; ++s)
       if (p[s] >= 0) *reinterpret_cast<uint2*>(xp + (size_t)p[s] * H + 4 * i) = packed;
   }
 }
 
-void launch_gather(const LayerWork& w, const float* x, int T, int kk, int H, cudaStream_t s) {
+void launch_gather(const float* x, const int32_t* pos, const long long* fault, __nv_bfloat16* xp, int T, int kk,
+                   int H, cudaStream_t s) {
   if (T == 0) return;
   const int threads = min(256, max(32, H / 4));
-  k_gather<<<T, threads, 0, s>>>(x, w.pos, w.fault, w.xp, kk, H);
+  k_gather<<<T, threads, 0, s>>>(x, pos, fault, xp, kk, H);
   note_launch();
 }
 
 // y_t = sum over routed experts in ascending order of (sum_split part) * inv_k,
 // with explicit round-to-nearest adds/multiplies (no FMA contraction) so the
 // accumulation mirrors `y += expert_output(...) * inv_k` (pipeline.py:206).
+// With next_pos, bf16(y_t) also lands in the next layer's expert-major rows.
 __global__ void k_combine(const float* __restrict__ part, const int32_t* __restrict__ pos,
                           const long long* __restrict__ fault, float* __restrict__ y, int kk, int H, int splits,
-                          long long split_stride, float inv_k) {
+                          long long split_stride, float inv_k, const int32_t* __restrict__ next_pos,
+                          __nv_bfloat16* __restrict__ xp) {
   if (*fault) return;
   const int t = blockIdx.x;
-  int p[kMaxTopK];
-  for (int s = 0; s < kk; ++s) p[s] = pos[t * kk + s];
+  int p[kMaxTopK], q[kMaxTopK];
+  for (int s = 0; s < kk; ++s) {
+    p[s] = pos[t * kk + s];
+    q[s] = next_pos ? next_pos[t * kk + s] : -1;
+  }
   for (int i = threadIdx.x; i < H / 4; i += blockDim.x) {
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int s = 0; s < kk; ++s) {
@@ -289,8 +222,8 @@ __global__ void k_combine(const float* __restrict__ part, const int32_t* __restr
       const float4* src = reinterpret_cast<const float4*>(part + (size_t)p[s] * H) + i;
       float4 v = src[0];
       for (int k = 1; k < splits; ++k) {
-        const float4 q = src[k * split_stride / 4];
-        v.x = __fadd_rn(v.x, q.x); v.y = __fadd_rn(v.y, q.y); v.z = __fadd_rn(v.z, q.z); v.w = __fadd_rn(v.w, q.w);
+        const float4 w = src[k * split_stride / 4];
+        v.x = __fadd_rn(v.x, w.x); v.y = __fadd_rn(v.y, w.y); v.z = __fadd_rn(v.z, w.z); v.w = __fadd_rn(v.w, w.w);
       }
       acc.x = __fadd_rn(acc.x, __fmul_rn(v.x, inv_k));
       acc.y = __fadd_rn(acc.y, __fmul_rn(v.y, inv_k));
@@ -298,14 +231,20 @@ __global__ void k_combine(const float* __restrict__ part, const int32_t* __restr
       acc.w = __fadd_rn(acc.w, __fmul_rn(v.w, inv_k));
     }
     reinterpret_cast<float4*>(y + (size_t)t * H)[i] = acc;
+    if (next_pos) {
+      const uint2 packed = pack_bf16x4(acc);
+      for (int s = 0; s < kk; ++s)
+        if (q[s] >= 0) *reinterpret_cast<uint2*>(xp + (size_t)q[s] * H + 4 * i) = packed;
+    }
   }
 }
 
-void launch_combine(const LayerWork& w, float* y, int T, int kk, int H, int splits, int cap_rows, float inv_k,
+void launch_combine(const float* part, const int32_t* pos, const long long* fault, float* y, int T, int kk, int H,
+                    int splits, long long split_stride, float inv_k, const int32_t* next_pos, __nv_bfloat16* xp,
                     cudaStream_t s) {
   if (T == 0) return;
   const int threads = min(256, max(32, H / 4));
-  k_combine<<<T, threads, 0, s>>>(w.part, w.pos, w.fault, y, kk, H, splits, (long long)cap_rows * H, inv_k);
+  k_combine<<<T, threads, 0, s>>>(part, pos, fault, y, kk, H, splits, split_stride, inv_k, next_pos, xp);
   note_launch();
 }
 
@@ -313,37 +252,41 @@ void launch_combine(const LayerWork& w, float* y, int T, int kk, int H, int spli
 __global__ void k_reduce_rows(const float* __restrict__ part, const long long* __restrict__ fault,
                               float* __restrict__ out, long long n4, int splits, long long split_stride4) {
   if (*fault) return;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
     const float4* src = reinterpret_cast<const float4*>(part) + i;
     float4 v = src[0];
     for (int k = 1; k < splits; ++k) {
-      const float4 q = src[k * split_stride4];
-      v.x = __fadd_rn(v.x, q.x); v.y = __fadd_rn(v.y, q.y); v.z = __fadd_rn(v.z, q.z); v.w = __fadd_rn(v.w, q.w);
+      const float4 w = src[k * split_stride4];
+      v.x = __fadd_rn(v.x, w.x); v.y = __fadd_rn(v.y, w.y); v.z = __fadd_rn(v.z, w.z); v.w = __fadd_rn(v.w, w.w);
     }
     reinterpret_cast<float4*>(out)[i] = v;
   }
 }
 
-void launch_reduce_rows(const LayerWork& w, float* out, int n_rows, int H, int splits, int cap_rows,
-                        cudaStream_t s) {
+void launch_reduce_rows(const float* part, const long long* fault, float* out, int n_rows, int H, int splits,
+                        long long split_stride, cudaStream_t s) {
   const long long n4 = (long long)n_rows * H / 4;
   if (n4 == 0) return;
   const long long nb = (n4 + 255) / 256;
   const int blocks = (int)(nb < 148 * 8 ? nb : 148 * 8);
-  k_reduce_rows<<<blocks, 256, 0, s>>>(w.part, w.fault, out, n4, splits, (long long)cap_rows * H / 4);
+  k_reduce_rows<<<blocks, 256, 0, s>>>(part, fault, out, n4, splits, split_stride / 4);
   note_launch();
 }
 
-// ============================================================================ tcgen05 grouped GEMMs
+// ============================================================================ tcgen05 grouped GEMM
 //
-// Warp roles (192 threads, one CTA per SM, persistent over the unit list):
-//   warp 0      TMA producer (one elected lane)
+// Warp roles (192 threads, one CTA per SM, persistent over the work units):
+//   warp 0      TMA producer (lane 0)
 //   warp 1      TMEM allocator + MMA issuer (lane 0 issues tcgen05.mma)
 //   warps 2..5  epilogue: TMEM -> registers -> global (warp w reads lanes 32*(w%4)..)
-// Swap-AB: the weight tile (128 rows x 64 K) is the UMMA A operand, the
-// expert's activation rows (n <= BN) are B, so decode-size n costs N=16..BN
-// columns instead of padding M.  Weights are addressed through the page
+// Swap-AB: the weight tile (128 rows x 64 K) is the UMMA A operand and the
+// expert's activation rows (n <= BN) are B, so a decode-size expert costs an
+// N = 16..BN MMA instead of a padded M.  Weights are addressed through the page
 // table: row = block * rows_per_block + m0 inside one tensor map over the pool.
+// The work-unit list is derived in every CTA's prologue from the expert row
+// offsets (no global unit array), and the same prologue performs read_page's
+// residency check (paging.py:228-237) on every routed expert's page.
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
@@ -351,19 +294,55 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 
 __device__ __forceinline__ float silu_f(float g) { return g * (1.0f / (1.0f + __expf(-g))); }
 
-template <int BN, int STAGES>
-struct GateUpCfg {
+template <bool GU, int BN, int STAGES>
+struct GemmCfg {
   static constexpr int A_BYTES = kBM * kBK * 2;
+  static constexpr int NA = GU ? 2 : 1;  // A tiles per stage (gate + up)
   static constexpr int B_BYTES = BN * kBK * 2;
-  static constexpr int STAGE = 2 * A_BYTES + B_BYTES;
-  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+  static constexpr int STAGE = NA * A_BYTES + B_BYTES;
+  static constexpr int ACC_COLS = GU ? 256 : 128;  // TMEM columns per accumulator stage
+  static constexpr int TMEM_COLS = 2 * ACC_COLS;
+  static constexpr int TAB_BYTES = (3 * kMaxExperts + 8) * 4;
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256 + TAB_BYTES;
 };
 
-template <int BN, int STAGES>
+struct Unit {
+  int e, m0, row_begin, n_rows, split;
+};
+
+__device__ __forceinline__ Unit decode_unit(int u, const int* s_up, const int* s_off, int E, int bn, int splits,
+                                            bool gate_up) {
+  int lo = 0, hi = E;  // largest e with s_up[e] <= u
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (s_up[mid] <= u) lo = mid; else hi = mid;
+  }
+  Unit r;
+  r.e = lo;
+  const int local = u - s_up[lo];
+  const int n = s_off[lo + 1] - s_off[lo];
+  const int nt_count = (n + bn - 1) / bn;
+  int m, nt;
+  if (gate_up) {
+    m = local / nt_count;
+    nt = local % nt_count;
+    r.split = 0;
+  } else {
+    m = local / (splits * nt_count);
+    const int rem = local % (splits * nt_count);
+    r.split = rem / nt_count;
+    nt = rem % nt_count;
+  }
+  r.m0 = m * kBM;
+  r.row_begin = s_off[lo] + nt * bn;
+  r.n_rows = min(bn, n - nt * bn);
+  return r;
+}
+
+template <bool GU, int BN, int STAGES>
 __global__ void __launch_bounds__(192, 1)
-    k_gate_up(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x, LayerWork w,
-              int F, int H) {
-  using C = GateUpCfg<BN, STAGES>;
+    k_moe_gemm(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_b, GemmParams p) {
+  using C = GemmCfg<GU, BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE);
@@ -371,48 +350,95 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* s_off = reinterpret_cast<int*>(smem + STAGES * C::STAGE + 256);
+  int* s_up = s_off + kMaxExperts + 1;
+  int* s_slot = s_up + kMaxExperts + 1;
+  int* s_flag = s_slot + kMaxExperts;
 
-  if (*w.fault != 0) return;
-  const int n_units = w.counters[0];
-  if ((int)blockIdx.x >= n_units) return;
+  const int E = p.E;
+  const int MT = ((GU ? p.F : p.H) + kBM - 1) / kBM;
+  const int S = GU ? 1 : p.splits;
   const uint32_t warp = warp_id_sync();
   const uint32_t lane = threadIdx.x & 31;
 
+  // ---- prologue: unit prefix + page-table residency check
+  if (threadIdx.x == 0) *s_flag = (*(volatile long long*)p.fault != 0);
+  for (int e = threadIdx.x; e <= E; e += blockDim.x) s_off[e] = p.offsets[e];
+  __syncthreads();
+  if (*s_flag) return;
+  if (warp == 0) {
+    int carry = 0;
+    bool bad = false;
+    if (lane == 0) s_up[0] = 0;
+    for (int e0 = 0; e0 < E; e0 += 32) {
+      const int e = e0 + lane;
+      int u = 0;
+      if (e < E) {
+        const int n = s_off[e + 1] - s_off[e];
+        if (n > 0) {
+          u = ((n + BN - 1) / BN) * MT * S;
+          const int32_t ent = p.pt[e];
+          if (pt_state(ent) != 2) {
+            atomicCAS((unsigned long long*)p.fault, 0ull,
+                      (unsigned long long)fault_pack(p.layer, p.e_first + e + 1, GU ? 1 : 2, pt_state(ent)));
+            bad = true;
+          }
+          s_slot[e] = pt_block0(ent);
+        }
+      }
+      int x = u;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off) x += y;
+      }
+      if (e < E) s_up[e + 1] = carry + x;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) *s_flag = 1;
+  }
+  __syncthreads();
+  const int n_units = s_up[E];
+  if (*s_flag || (int)blockIdx.x >= n_units) return;
+
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_w);
-    tma_prefetch_desc(&map_x);
+    tma_prefetch_desc(&map_b);
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int KB = (H + kBK - 1) / kBK;
+  const int K = GU ? p.H : p.F;
+  const int KB = (K + kBK - 1) / kBK;
+  const int rows_per_block = GU ? 2 * p.F : p.H;
 
   if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol_w = policy_evict_first();
-      const uint64_t pol_x = policy_evict_last();
+      const uint64_t pol_b = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-        const GemmUnit un = w.units1[u];
-        const int n_rows = un.n_and_split & 0xFFFF;
-        const int nb = (n_rows + kBoxRowsB - 1) / kBoxRowsB;
-        const int gate_row = w.slot_gu[un.expert] * 2 * F + un.m0;
-        const uint32_t bytes = 2 * C::A_BYTES + nb * kBoxRowsB * kBK * 2;
-        for (int kb = 0; kb < KB; ++kb) {
+        const Unit un = decode_unit(u, s_up, s_off, E, BN, S, GU);
+        const int kb0 = GU ? 0 : un.split * KB / S, kb1 = GU ? KB : (un.split + 1) * KB / S;
+        const int nb = (un.n_rows + kBoxRowsB - 1) / kBoxRowsB;
+        const int wrow = s_slot[un.e] * rows_per_block + un.m0;
+        const uint32_t bytes = C::NA * C::A_BYTES + nb * kBoxRowsB * kBK * 2;
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE;
           mbar_arrive_expect_tx(&full[stage], bytes);
-          tma_load_2d(sa, &map_w, &full[stage], kb * kBK, gate_row, pol_w);
-          tma_load_2d(sa + C::A_BYTES, &map_w, &full[stage], kb * kBK, gate_row + F, pol_w);
+          tma_load_2d(sa, &map_w, &full[stage], kb * kBK, wrow, pol_w);
+          if (GU) tma_load_2d(sa + C::A_BYTES, &map_w, &full[stage], kb * kBK, wrow + p.F, pol_w);
+          uint8_t* sb = sa + C::NA * C::A_BYTES;
           for (int i = 0; i < nb; ++i)
-            tma_load_2d(sa + 2 * C::A_BYTES + i * kBoxRowsB * kBK * 2, &map_x, &full[stage], kb * kBK,
-                        un.row_begin + i * kBoxRowsB, pol_x);
+            tma_load_2d(sb + i * kBoxRowsB * kBK * 2, &map_b, &full[stage], kb * kBK, un.row_begin + i * kBoxRowsB,
+                        pol_b);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -422,26 +448,26 @@ __global__ void __launch_bounds__(192, 1)
     uint32_t phase = 0;
     int it = 0;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
-      const GemmUnit un = w.units1[u];
-      const int n_rows = un.n_and_split & 0xFFFF;
-      const uint32_t idesc = idesc_bf16_f32(kBM, (n_rows + 15) & ~15);
+      const Unit un = decode_unit(u, s_up, s_off, E, BN, S, GU);
+      const int kb0 = GU ? 0 : un.split * KB / S, kb1 = GU ? KB : (un.split + 1) * KB / S;
+      const uint32_t idesc = idesc_bf16_f32(kBM, (un.n_rows + 15) & ~15);
       const int acc = it & 1;
       const uint32_t acc_par = (it >> 1) & 1;
       mbar_wait(&tempty[acc], acc_par ^ 1);
       tc_fence_after();
-      const uint32_t d_gate = tmem + acc * 256;
-      const uint32_t d_up = d_gate + 128;
-      for (int kb = 0; kb < KB; ++kb) {
+      const uint32_t d0 = tmem + acc * C::ACC_COLS;
+      for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t base = smem_u32(smem + stage * C::STAGE);
+          const uint32_t bbase = base + C::NA * C::A_BYTES;
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
-            const uint64_t bdesc = sdesc_k_sw128(base + 2 * C::A_BYTES + 32 * k);
-            const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
-            umma_bf16(d_gate, sdesc_k_sw128(base + 32 * k), bdesc, idesc, accum);
-            umma_bf16(d_up, sdesc_k_sw128(base + C::A_BYTES + 32 * k), bdesc, idesc, accum);
+            const uint64_t bdesc = sdesc_k_sw128(bbase + 32 * k);
+            const uint32_t accum = (kb > kb0 || k > 0) ? 1u : 0u;
+            umma_bf16(d0, sdesc_k_sw128(base + 32 * k), bdesc, idesc, accum);
+            if (GU) umma_bf16(d0 + 128, sdesc_k_sw128(base + C::A_BYTES + 32 * k), bdesc, idesc, accum);
           }
           umma_commit(&empty[stage]);
         }
@@ -455,23 +481,35 @@ __global__ void __launch_bounds__(192, 1)
     const int q = warp & 3;
     int it = 0;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
-      const GemmUnit un = w.units1[u];
-      const int n_rows = un.n_and_split & 0xFFFF;
+      const Unit un = decode_unit(u, s_up, s_off, E, BN, S, GU);
       const int acc = it & 1;
       const uint32_t acc_par = (it >> 1) & 1;
       mbar_wait(&tfull[acc], acc_par);
       tc_fence_after();
       const int r = un.m0 + q * 32 + lane;
-      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * 256;
-      __nv_bfloat16* hcol = w.hbuf + (size_t)un.row_begin * F + r;
-      for (int c0 = 0; c0 < n_rows; c0 += 16) {
-        float g[16], v[16];
-        tmem_ld16(tbase + c0, g);
-        tmem_ld16(tbase + 128 + c0, v);
-        if (r < F) {
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * C::ACC_COLS;
+      if (GU) {
+        __nv_bfloat16* hcol = p.hbuf + (size_t)un.row_begin * p.F + r;
+        for (int c0 = 0; c0 < un.n_rows; c0 += 16) {
+          float g[16], v[16];
+          tmem_ld16(tbase + c0, g);
+          tmem_ld16(tbase + 128 + c0, v);
+          if (r < p.F) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (c0 + i < n_rows) hcol[(size_t)(c0 + i) * F] = __float2bfloat16_rn(silu_f(g[i]) * v[i]);
+            for (int i = 0; i < 16; ++i)
+              if (c0 + i < un.n_rows) hcol[(size_t)(c0 + i) * p.F] = __float2bfloat16_rn(silu_f(g[i]) * v[i]);
+          }
+        }
+      } else {
+        float* out = p.part + un.split * p.split_stride + (size_t)un.row_begin * p.H + r;
+        for (int c0 = 0; c0 < un.n_rows; c0 += 16) {
+          float v[16];
+          tmem_ld16(tbase + c0, v);
+          if (r < p.H) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (c0 + i < un.n_rows) out[(size_t)(c0 + i) * p.H] = v[i];
+          }
         }
       }
       tc_fence_before();
@@ -481,199 +519,46 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc<512>(tmem);
-}
-
-template <int BN, int STAGES>
-struct DownCfg {
-  static constexpr int A_BYTES = kBM * kBK * 2;
-  static constexpr int B_BYTES = BN * kBK * 2;
-  static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
-};
-
-template <int BN, int STAGES>
-__global__ void __launch_bounds__(192, 1)
-    k_down(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_h, LayerWork w,
-           int F, int H, int splits, long long split_stride) {
-  using C = DownCfg<BN, STAGES>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = align1024(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-
-  if (*w.fault != 0) return;
-  const int n_units = w.counters[1];
-  if ((int)blockIdx.x >= n_units) return;
-  const uint32_t warp = warp_id_sync();
-  const uint32_t lane = threadIdx.x & 31;
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&map_w);
-    tma_prefetch_desc(&map_h);
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
-    fence_mbar_init();
-  }
-  if (warp == 1) tmem_alloc<256>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const int KB = (F + kBK - 1) / kBK;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      const uint64_t pol_w = policy_evict_first();
-      const uint64_t pol_x = policy_evict_last();
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-        const GemmUnit un = w.units2[u];
-        const int n_rows = un.n_and_split & 0xFFFF;
-        const int split = un.n_and_split >> 16;
-        const int kb0 = split * KB / splits, kb1 = (split + 1) * KB / splits;
-        const int nb = (n_rows + kBoxRowsB - 1) / kBoxRowsB;
-        const int wrow = w.slot_dn[un.expert] * H + un.m0;
-        const uint32_t bytes = C::A_BYTES + nb * kBoxRowsB * kBK * 2;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * C::STAGE;
-          mbar_arrive_expect_tx(&full[stage], bytes);
-          tma_load_2d(sa, &map_w, &full[stage], kb * kBK, wrow, pol_w);
-          for (int i = 0; i < nb; ++i)
-            tma_load_2d(sa + C::A_BYTES + i * kBoxRowsB * kBK * 2, &map_h, &full[stage], kb * kBK,
-                        un.row_begin + i * kBoxRowsB, pol_x);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    int stage = 0;
-    uint32_t phase = 0;
-    int it = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
-      const GemmUnit un = w.units2[u];
-      const int n_rows = un.n_and_split & 0xFFFF;
-      const int split = un.n_and_split >> 16;
-      const int kb0 = split * KB / splits, kb1 = (split + 1) * KB / splits;
-      const uint32_t idesc = idesc_bf16_f32(kBM, (n_rows + 15) & ~15);
-      const int acc = it & 1;
-      const uint32_t acc_par = (it >> 1) & 1;
-      mbar_wait(&tempty[acc], acc_par ^ 1);
-      tc_fence_after();
-      const uint32_t d = tmem + acc * 128;
-      for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(&full[stage], phase);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t base = smem_u32(smem + stage * C::STAGE);
-#pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)
-            umma_bf16(d, sdesc_k_sw128(base + 32 * k), sdesc_k_sw128(base + C::A_BYTES + 32 * k), idesc,
-                      (kb > kb0 || k > 0) ? 1u : 0u);
-          umma_commit(&empty[stage]);
-        }
-        __syncwarp();
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
-      }
-      if (lane == 0) umma_commit(&tfull[acc]);
-      __syncwarp();
-    }
-  } else {
-    const int q = warp & 3;
-    int it = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
-      const GemmUnit un = w.units2[u];
-      const int n_rows = un.n_and_split & 0xFFFF;
-      const int split = un.n_and_split >> 16;
-      const int acc = it & 1;
-      const uint32_t acc_par = (it >> 1) & 1;
-      mbar_wait(&tfull[acc], acc_par);
-      tc_fence_after();
-      const int r = un.m0 + q * 32 + lane;
-      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * 128;
-      float* out = w.part + split * split_stride + (size_t)un.row_begin * H + r;
-      for (int c0 = 0; c0 < n_rows; c0 += 16) {
-        float v[16];
-        tmem_ld16(tbase + c0, v);
-        if (r < H) {
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (c0 + i < n_rows) out[(size_t)(c0 + i) * H] = v[i];
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == 1) tmem_dealloc<256>(tmem);
+  if (warp == 1) tmem_dealloc<C::TMEM_COLS>(tmem);
 }
 
 // ---- instantiations / launchers
 
-#define XPGB_GU_CFG(BN, ST) \
-  case BN:                  \
-    kern = k_gate_up<BN, ST>; smem = GateUpCfg<BN, ST>::SMEM; break;
-#define XPGB_DN_CFG(BN, ST) \
-  case BN:                  \
-    kern = k_down<BN, ST>; smem = DownCfg<BN, ST>::SMEM; break;
+using GemmKernel = void (*)(const CUtensorMap, const CUtensorMap, GemmParams);
 
-int gemm_smem_bytes(int which, int bn) {
-  if (which == 0) {
-    switch (bn) {
-      case 32: return GateUpCfg<32, 6>::SMEM;
-      case 64: return GateUpCfg<64, 5>::SMEM;
-      default: return GateUpCfg<128, 4>::SMEM;
-    }
-  }
-  switch (bn) {
-    case 32: return DownCfg<32, 10>::SMEM;
-    case 64: return DownCfg<64, 8>::SMEM;
-    default: return DownCfg<128, 6>::SMEM;
-  }
+template <bool GU, int BN, int ST>
+static void set_attr() {
+  cudaFuncSetAttribute(k_moe_gemm<GU, BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<GU, BN, ST>::SMEM);
 }
 
 void set_gemm_attrs() {
-  cudaFuncSetAttribute(k_gate_up<32, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, GateUpCfg<32, 6>::SMEM);
-  cudaFuncSetAttribute(k_gate_up<64, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, GateUpCfg<64, 5>::SMEM);
-  cudaFuncSetAttribute(k_gate_up<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, GateUpCfg<128, 4>::SMEM);
-  cudaFuncSetAttribute(k_down<32, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, DownCfg<32, 10>::SMEM);
-  cudaFuncSetAttribute(k_down<64, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, DownCfg<64, 8>::SMEM);
-  cudaFuncSetAttribute(k_down<128, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, DownCfg<128, 6>::SMEM);
+  set_attr<true, 32, 5>();
+  set_attr<true, 64, 4>();
+  set_attr<true, 128, 4>();
+  set_attr<false, 32, 9>();
+  set_attr<false, 64, 8>();
+  set_attr<false, 128, 6>();
 }
 
-void launch_gate_up(const CUtensorMap& map_w, const CUtensorMap& map_x, const LayerWork& w, int F, int H, int bn,
-                    int grid, cudaStream_t s) {
-  void (*kern)(const CUtensorMap, const CUtensorMap, LayerWork, int, int) = nullptr;
-  int smem = 0;
-  switch (bn) {
-    XPGB_GU_CFG(32, 6)
-    XPGB_GU_CFG(64, 5)
-    default:
-      kern = k_gate_up<128, 4>; smem = GateUpCfg<128, 4>::SMEM; break;
-  }
-  kern<<<grid, 192, smem, s>>>(map_w, map_x, w, F, H);
+void launch_gate_up(const CUtensorMap& map_w, const CUtensorMap& map_x, const GemmParams& p, int bn, int grid,
+                    cudaStream_t s) {
+  GemmKernel kern;
+  int smem;
+  if (bn == 32) { kern = k_moe_gemm<true, 32, 5>; smem = GemmCfg<true, 32, 5>::SMEM; }
+  else if (bn == 64) { kern = k_moe_gemm<true, 64, 4>; smem = GemmCfg<true, 64, 4>::SMEM; }
+  else { kern = k_moe_gemm<true, 128, 4>; smem = GemmCfg<true, 128, 4>::SMEM; }
+  kern<<<grid, 192, smem, s>>>(map_w, map_x, p);
   note_launch();
 }
 
-void launch_down(const CUtensorMap& map_w, const CUtensorMap& map_h, const LayerWork& w, int F, int H, int bn,
-                 int splits, int cap_rows, int grid, cudaStream_t s) {
-  void (*kern)(const CUtensorMap, const CUtensorMap, LayerWork, int, int, int, long long) = nullptr;
-  int smem = 0;
-  switch (bn) {
-    XPGB_DN_CFG(32, 10)
-    XPGB_DN_CFG(64, 8)
-    default:
-      kern = k_down<128, 6>; smem = DownCfg<128, 6>::SMEM; break;
-  }
-  kern<<<grid, 192, smem, s>>>(map_w, map_h, w, F, H, splits, (long long)cap_rows * H);
+void launch_down(const CUtensorMap& map_w, const CUtensorMap& map_h, const GemmParams& p, int bn, int grid,
+                 cudaStream_t s) {
+  GemmKernel kern;
+  int smem;
+  if (bn == 32) { kern = k_moe_gemm<false, 32, 9>; smem = GemmCfg<false, 32, 9>::SMEM; }
+  else if (bn == 64) { kern = k_moe_gemm<false, 64, 8>; smem = GemmCfg<false, 64, 8>::SMEM; }
+  else { kern = k_moe_gemm<false, 128, 6>; smem = GemmCfg<false, 128, 6>::SMEM; }
+  kern<<<grid, 192, smem, s>>>(map_w, map_h, p);
   note_launch();
 }
 

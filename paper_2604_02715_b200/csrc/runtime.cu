@@ -161,7 +161,10 @@ static const char* state_name(int s) {
   }
 }
 
+struct Session;
+
 struct Ctx {
+  Session* sess = nullptr;
   int N, L, H, F;
   int device;
   int pool;
@@ -202,10 +205,15 @@ struct Ctx {
 
   // workspace
   int cap_T = 0, cap_kk = 0, cap_rows = 0, cap_splits = 8;
-  LayerWork work{};
-  int32_t* topk_single = nullptr;
-  int32_t* topk_all = nullptr;
-  int topk_all_cap = 0;
+  // routing plans: buffer 0/1 alternate per iteration of a run, buffer 2 serves layer_forward
+  int32_t* plan_topk[3] = {nullptr, nullptr, nullptr};  // [N][T][kk]
+  int32_t* plan_pos[3] = {nullptr, nullptr, nullptr};   // [N][T][kk]
+  int32_t* plan_off[3] = {nullptr, nullptr, nullptr};   // [N][E+1]
+  __nv_bfloat16* xp = nullptr;  // [cap_rows][H]
+  __nv_bfloat16* hbuf = nullptr;  // [cap_rows][F]
+  float* part = nullptr;          // [cap_splits][cap_rows][H]
+  int32_t* ep_off = nullptr;      // [E+1] scratch for experts_forward
+  int last_splits = 1;
   CUtensorMap map_xp{}, map_h{};
   long long* d_fault = nullptr;
 
@@ -220,7 +228,7 @@ struct Ctx {
   cudaEvent_t pev[7];
   cudaEvent_t* cur_ev = nullptr;          // 7 events bracketing the next enqueue_forward
   std::vector<cudaEvent_t> run_ev;        // per-step event sets for opts.profile
-  xpgb_kernel_times last_times{};
+  xpgb_kernel_times last_times{};  // last xpgb_profile_layer
 };
 
 static int page_index(Ctx* c, int layer, int expert, int kind) {
@@ -297,39 +305,44 @@ static void ensure_log(Ctx* c, int cap) {
   CK(cudaMemset(c->d_log_count, 0, sizeof(int32_t)));
 }
 
+static void free_work(Ctx* c) {
+  auto fr = [](void* p) { if (p) cudaFree(p); };
+  for (int b = 0; b < 3; ++b) {
+    fr(c->plan_topk[b]); fr(c->plan_pos[b]); fr(c->plan_off[b]);
+    c->plan_topk[b] = c->plan_pos[b] = c->plan_off[b] = nullptr;
+  }
+  fr(c->xp); fr(c->hbuf); fr(c->part); fr(c->ep_off);
+  c->xp = c->hbuf = nullptr;
+  c->part = nullptr;
+  c->ep_off = nullptr;
+  c->cap_T = c->cap_kk = c->cap_rows = 0;
+}
+
 static void ensure_work(Ctx* c, int T, int kk) {
   if (kk > kMaxTopK) XFAIL(XPGB_ERR_OUT_OF_RANGE, "top_k %d above the kernel limit %d", kk, kMaxTopK);
-  if (T <= c->cap_T && kk <= c->cap_kk && c->work.xp) return;
+  if (T <= c->cap_T && kk <= c->cap_kk && c->xp) return;
   const int nT = std::max(T, std::max(c->cap_T, 16));
   const int nkk = std::max(kk, c->cap_kk);
-  const int rows = nT * nkk;
-  LayerWork& w = c->work;
-  auto fr = [](void* p) { if (p) cudaFree(p); };
-  fr(w.pos); fr(w.offsets); fr(w.slot_gu); fr(w.slot_dn); fr(w.units1); fr(w.units2); fr(w.counters);
-  fr(w.xp); fr(w.hbuf); fr(w.part); fr(c->topk_single);
-  const int E = c->E;
-  const long long mt1 = (c->F + kBM - 1) / kBM, mt2 = (c->H + kBM - 1) / kBM;
-  const long long max_units1 = (E + rows / 32 + 1) * mt1;
-  const long long max_units2 = (E + rows / 32 + 1) * mt2 * c->cap_splits;
-  CK(cudaMalloc(&w.pos, (size_t)rows * 4));
-  CK(cudaMalloc(&w.offsets, (size_t)(E + 1) * 4));
-  CK(cudaMalloc(&w.slot_gu, (size_t)E * 4));
-  CK(cudaMalloc(&w.slot_dn, (size_t)E * 4));
-  CK(cudaMalloc(&w.units1, (size_t)max_units1 * sizeof(GemmUnit)));
-  CK(cudaMalloc(&w.units2, (size_t)max_units2 * sizeof(GemmUnit)));
-  CK(cudaMalloc(&w.counters, 16));
-  CK(cudaMalloc(&w.xp, (size_t)rows * c->H * 2));
-  CK(cudaMemset(w.xp, 0, (size_t)rows * c->H * 2));
-  CK(cudaMalloc(&w.hbuf, (size_t)rows * c->F * 2));
-  CK(cudaMemset(w.hbuf, 0, (size_t)rows * c->F * 2));
-  CK(cudaMalloc(&w.part, (size_t)c->cap_splits * rows * c->H * 4));
-  CK(cudaMalloc(&c->topk_single, (size_t)rows * 4));
-  w.fault = c->d_fault;
+  CK(cudaDeviceSynchronize());
+  free_work(c);
+  const long long rows = (long long)nT * nkk;
+  const int E = c->E, N = c->N;
+  for (int b = 0; b < 3; ++b) {
+    CK(cudaMalloc(&c->plan_topk[b], (size_t)N * rows * 4));
+    CK(cudaMalloc(&c->plan_pos[b], (size_t)N * rows * 4));
+    CK(cudaMalloc(&c->plan_off[b], (size_t)N * (E + 1) * 4));
+  }
+  CK(cudaMalloc(&c->xp, (size_t)rows * c->H * 2));
+  CK(cudaMemset(c->xp, 0, (size_t)rows * c->H * 2));
+  CK(cudaMalloc(&c->hbuf, (size_t)rows * c->F * 2));
+  CK(cudaMemset(c->hbuf, 0, (size_t)rows * c->F * 2));
+  CK(cudaMalloc(&c->part, (size_t)c->cap_splits * rows * c->H * 4));
+  CK(cudaMalloc(&c->ep_off, (size_t)(E + 1) * 4));
   c->cap_T = nT;
   c->cap_kk = nkk;
-  c->cap_rows = rows;
-  c->map_xp = make_map(w.xp, rows, c->H, kBoxRowsB);
-  c->map_h = make_map(w.hbuf, rows, c->F, kBoxRowsB);
+  c->cap_rows = (int)rows;
+  c->map_xp = make_map(c->xp, rows, c->H, kBoxRowsB);
+  c->map_h = make_map(c->hbuf, rows, c->F, kBoxRowsB);
 }
 
 static int pick_bn(int T) { return T <= 32 ? 32 : (T <= 64 ? 64 : 128); }
@@ -357,40 +370,74 @@ static void prof_rec(Ctx* c, int i, cudaStream_t s) {
   else if (c->prof) CK(cudaEventRecord(c->pev[i], s));
 }
 
-// layer_forward (pipeline.py:192-208) on `s`: y may alias x.
-static void enqueue_forward(Ctx* c, int layer, const float* x, float* y, int T, int top_k, uint64_t seed,
-                            const int32_t* topk, cudaStream_t s) {
+static GemmParams gemm_params(Ctx* c, int layer, int kind, const int32_t* offsets, int splits) {
+  GemmParams p;
+  p.offsets = offsets;
+  p.pt = c->d_pt + (size_t)(kind - 1) * c->N * c->E + (size_t)(layer - 1) * c->E;
+  p.fault = c->d_fault;
+  p.hbuf = c->hbuf;
+  p.part = c->part;
+  p.split_stride = (long long)c->cap_rows * c->H;
+  p.layer = layer;
+  p.e_first = c->e_first;
+  p.E = c->E;
+  p.F = c->F;
+  p.H = c->H;
+  p.splits = splits;
+  return p;
+}
+
+// Plan (route + positions) layers [1, N] of one iteration into buffer b.
+static void enqueue_plan(Ctx* c, int b, int layer_first, int layer_count, int T, int top_k, uint64_t seed,
+                         cudaStream_t s) {
+  const int kk = std::min(top_k, c->L);
+  const size_t lo = (size_t)(layer_first - 1);
+  launch_route_plan(seed, layer_first, layer_count, T, c->L, top_k, c->e_first, c->E,
+                    c->plan_topk[b] + lo * T * kk, c->plan_pos[b] + lo * T * kk, c->plan_off[b] + lo * (c->E + 1),
+                    c->d_fault, s);
+  CKLAUNCH();
+}
+
+// layer_forward (pipeline.py:192-208) on `s` from plan buffer b; y may alias x.
+// gather: x -> expert-major bf16 rows first (else the previous combine already did it);
+// next_pos: fuse the next layer's gather into this layer's combine.
+static void enqueue_forward(Ctx* c, int layer, const float* x, float* y, int T, int top_k, int b, bool gather,
+                            const int32_t* next_pos, cudaStream_t s) {
+  const int kk = std::min(top_k, c->L);
+  if (T == 0) return;
+  const int32_t* pos = c->plan_pos[b] + (size_t)(layer - 1) * T * kk;
+  const int32_t* off = c->plan_off[b] + (size_t)(layer - 1) * (c->E + 1);
+  const int bn = pick_bn(T);
+  const int splits = pick_splits(c, T, kk, bn);
+  prof_rec(c, 1, s);
+  if (gather) {
+    launch_gather(x, pos, c->d_fault, c->xp, T, kk, c->H, s);
+    CKLAUNCH();
+  }
+  prof_rec(c, 2, s);
+  prof_rec(c, 3, s);
+  launch_gate_up(c->map_gu, c->map_xp, gemm_params(c, layer, 1, off, 1), bn, c->num_sms, s);
+  CKLAUNCH();
+  prof_rec(c, 4, s);
+  launch_down(c->map_dn, c->map_h, gemm_params(c, layer, 2, off, splits), bn, c->num_sms, s);
+  CKLAUNCH();
+  prof_rec(c, 5, s);
+  launch_combine(c->part, pos, c->d_fault, y, T, kk, c->H, splits, (long long)c->cap_rows * c->H,
+                 (float)(1.0 / top_k), next_pos, c->xp, s);
+  CKLAUNCH();
+  prof_rec(c, 6, s);
+  c->last_splits = splits;
+}
+
+// Standalone layer_forward: plan this layer into buffer 2, then the chain.
+static void enqueue_layer(Ctx* c, int layer, const float* x, float* y, int T, int top_k, uint64_t seed,
+                          cudaStream_t s) {
   const int kk = std::min(top_k, c->L);
   ensure_work(c, T, kk);
   if (T == 0) return;
-  LayerWork w = c->work;
   prof_rec(c, 0, s);
-  if (topk == nullptr) {
-    launch_route(seed, layer, 1, T, c->L, top_k, c->topk_single, s);
-    CKLAUNCH();
-    topk = c->topk_single;
-  }
-  w.topk = const_cast<int32_t*>(topk);
-  const int bn = pick_bn(T);
-  const int splits = pick_splits(c, T, kk, bn);
-  const size_t pages = (size_t)c->N * c->E;
-  prof_rec(c, 1, s);
-  launch_plan(w, c->d_pt, c->d_pt + pages, layer, T, kk, c->e_first, c->E, c->F, c->H, bn, bn, splits, s);
-  CKLAUNCH();
-  prof_rec(c, 2, s);
-  launch_gather(w, x, T, kk, c->H, s);
-  CKLAUNCH();
-  prof_rec(c, 3, s);
-  launch_gate_up(c->map_gu, c->map_xp, w, c->F, c->H, bn, c->num_sms, s);
-  CKLAUNCH();
-  prof_rec(c, 4, s);
-  launch_down(c->map_dn, c->map_h, w, c->F, c->H, bn, splits, c->cap_rows, c->num_sms, s);
-  CKLAUNCH();
-  prof_rec(c, 5, s);
-  launch_combine(w, y, T, kk, c->H, splits, c->cap_rows, (float)(1.0 / top_k), s);
-  CKLAUNCH();
-  prof_rec(c, 6, s);
-  c->last_times.down_splits = splits;
+  enqueue_plan(c, 2, layer, 1, T, top_k, seed, s);
+  enqueue_forward(c, layer, x, y, T, top_k, 2, true, nullptr, s);
 }
 
 // --------------------------------------------------------------------------- page table ops
@@ -583,61 +630,58 @@ static void materialize(RunState& rs, int g, int it, int layer, int kind) {
   if (seq) CK(cudaStreamSynchronize(s));
 }
 
-// Alg. 1 ForwardPass (pipeline.py:368-384) on the compute stream.
-static void forward_step(RunState& rs, int g, int it, int layer) {
-  Ctx* c = rs.c;
-  cudaStream_t s = c->s_comp;
-  const xpgb_run_opts* o = rs.o;
-  const bool paged = c->pool == XPGB_POOL_RING;
-  const bool skip = (o->sabotage_iteration == it && o->sabotage_layer == layer);
-  if (paged && !skip) {
-    CK(cudaStreamWaitEvent(s, c->ev_load[0][g & 3], 0));  // RAW
-    CK(cudaStreamWaitEvent(s, c->ev_load[1][g & 3], 0));
-  }
-  log_only(c, rs.log, s, XPGB_EV_COMPUTE_START, it, layer);
-  if (o->compute_delay_s) {
-    const float d = o->compute_delay_s[(size_t)(it - 1) * c->N + (layer - 1)];
-    if (d > 0) {
-      k_sleep<<<1, 1, 0, s>>>((uint64_t)(d * 1e9));
-      note_launch();
-      CKLAUNCH();
-    }
-  }
-  const int kk = std::min(o->top_k, c->L);
-  const int32_t* topk = c->topk_all + (size_t)(layer - 1) * o->tokens * kk;
-  c->cur_ev = o->profile ? &c->run_ev[(size_t)g * 7] : nullptr;
-  enqueue_forward(c, layer, rs.acts, rs.acts, o->tokens, o->top_k, o->router_seed, topk, s);
-  c->cur_ev = nullptr;
-  log_only(c, rs.log, s, XPGB_EV_COMPUTE_DONE, it, layer);
-  CK(cudaEventRecord(c->ev_comp[g & 3], s));
-  if (o->sequential) CK(cudaStreamSynchronize(s));
+// ---- session: the StreamedRunner schedule, one step at a time --------------------
+
+struct Session {
+  bool active = false;
+  xpgb_run_opts o{};
+  std::vector<float> fetch_delay, compute_delay;
+  RunState rs{};
+  int steps = 0;
+  bool paged = false;
+};
+
+static Session& session_of(Ctx* c) {
+  if (!c->sess) c->sess = new Session();
+  return *c->sess;
 }
 
-static void run_impl(Ctx* c, const xpgb_run_opts* o, const float* x, float* y, xpgb_report* rep) {
+static void step_of(Ctx* c, int g, int* it, int* layer) {
+  *it = g / c->N + 1;
+  *layer = g % c->N + 1;
+}
+
+// Begin a run: empty ring, fresh log, RUN_BEGIN on the compute stream; copy streams
+// start after it.  `acts` (device fp32 [T][H]) is the buffer the built-in compute
+// updates in place; external-compute sessions pass nullptr.
+static void session_begin(Ctx* c, const xpgb_run_opts* o, float* acts) {
+  Session& ss = session_of(c);
+  if (ss.active) XFAIL(XPGB_ERR, "a session is already active on this context");
   if (o->iterations < 1) XFAIL(XPGB_ERR, "need at least one iteration");
-  if (o->tokens < 0 || o->top_k < 1) XFAIL(XPGB_ERR_OUT_OF_RANGE, "bad ForwardSpec (T=%d, top_k=%d)", o->tokens,
-                                           o->top_k);
+  if (o->tokens < 0 || o->top_k < 1)
+    XFAIL(XPGB_ERR_OUT_OF_RANGE, "bad ForwardSpec (T=%d, top_k=%d)", o->tokens, o->top_k);
   const int N = c->N;
-  const int steps = o->iterations * N;
+  ss.o = *o;
+  ss.steps = o->iterations * N;
+  ss.fetch_delay.clear();
+  ss.compute_delay.clear();
+  if (o->fetch_delay_s) ss.fetch_delay.assign(o->fetch_delay_s, o->fetch_delay_s + (size_t)N * c->L * 2);
+  if (o->compute_delay_s) ss.compute_delay.assign(o->compute_delay_s, o->compute_delay_s + (size_t)ss.steps);
+  ss.o.fetch_delay_s = ss.fetch_delay.empty() ? nullptr : ss.fetch_delay.data();
+  ss.o.compute_delay_s = ss.compute_delay.empty() ? nullptr : ss.compute_delay.data();
   const int kk = std::min(o->top_k, c->L);
   ensure_work(c, o->tokens, kk);
-  if (c->topk_all_cap < N * o->tokens * kk) {
-    if (c->topk_all) cudaFree(c->topk_all);
-    c->topk_all_cap = std::max(N * o->tokens * kk, 1);
-    CK(cudaMalloc(&c->topk_all, (size_t)c->topk_all_cap * 4));
-  }
-  const bool log = o->log_enable != 0;
-  ensure_log(c, steps * 8 + 16);
+  ensure_log(c, ss.steps * 8 + 16);
   if (o->profile) {
-    while (c->run_ev.size() < (size_t)steps * 7) {
+    while (c->run_ev.size() < (size_t)ss.steps * 7) {
       cudaEvent_t e;
       CK(cudaEventCreate(&e));
       c->run_ev.push_back(e);
     }
   }
   CK(cudaMemset(c->d_fault, 0, sizeof(long long)));
-  const bool paged = c->pool == XPGB_POOL_RING;
-  if (paged) {
+  ss.paged = c->pool == XPGB_POOL_RING;
+  if (ss.paged) {
     // a run starts from an empty ring, like a fresh PageTable (pipeline.py:325)
     for (int k = 0; k < 2; ++k)
       for (size_t pi = 0; pi < c->st[k].size(); ++pi)
@@ -646,46 +690,98 @@ static void run_impl(Ctx* c, const xpgb_run_opts* o, const float* x, float* y, x
     c->bound = 0;
     c->peak = 0;
   }
-  RunState rs{c, o, y, 0, 0, log};
+  ss.rs = RunState{c, &ss.o, acts, 0, 0, o->log_enable != 0};
   cudaStream_t s = c->s_comp;
   CK(cudaDeviceSynchronize());  // inputs written by other streams are complete
-  if (y != x) CK(cudaMemcpyAsync(y, x, (size_t)o->tokens * c->H * 4, cudaMemcpyDeviceToDevice, s));
-  // routing is a pure function of (seed, t, layer): one launch covers all N layers
-  if (o->tokens > 0) {
-    launch_route(o->router_seed, 1, N, o->tokens, c->L, o->top_k, c->topk_all, s);
-    CKLAUNCH();
-  }
-  log_only(c, log, s, XPGB_EV_RUN_BEGIN, 0, 0);
+  log_only(c, ss.rs.log, s, XPGB_EV_RUN_BEGIN, 0, 0);
   CK(cudaEventRecord(c->ev_begin, s));
   CK(cudaStreamWaitEvent(c->s_copy[0], c->ev_begin, 0));
   CK(cudaStreamWaitEvent(c->s_copy[1], c->ev_begin, 0));
   if (o->sequential) CK(cudaStreamSynchronize(s));
+  ss.active = true;
+}
 
-  auto step_of = [&](int g, int* it, int* layer) {
-    *it = g / N + 1;
-    *layer = g % N + 1;
-  };
+static void session_materialize(Ctx* c, int g) {
+  Session& ss = session_of(c);
+  if (!ss.active) XFAIL(XPGB_ERR, "no active session");
+  if (!ss.paged || g < 0 || g >= ss.steps) return;
   int it, ly;
-  if (paged) {
-    // inline order: mat(0), mat(1), then fwd(g) | mat(g+2) (pipeline.py:412-424); the
-    // async mode enqueues the same order so every waited event is already recorded.
-    for (int kind = 1; kind <= 2; ++kind) { step_of(0, &it, &ly); materialize(rs, 0, it, ly, kind); }
-    if (steps > 1)
-      for (int kind = 1; kind <= 2; ++kind) { step_of(1, &it, &ly); materialize(rs, 1, it, ly, kind); }
+  step_of(c, g, &it, &ly);
+  for (int kind = 1; kind <= 2; ++kind) materialize(ss.rs, g, it, ly, kind);
+}
+
+// RAW: `s` waits for both load events of step g, then compute-start is logged on it.
+static void session_acquire(Ctx* c, int g, cudaStream_t s) {
+  Session& ss = session_of(c);
+  if (!ss.active) XFAIL(XPGB_ERR, "no active session");
+  int it, layer;
+  step_of(c, g, &it, &layer);
+  const xpgb_run_opts* o = &ss.o;
+  const bool skip = (o->sabotage_iteration == it && o->sabotage_layer == layer);
+  if (ss.paged && !skip) {
+    CK(cudaStreamWaitEvent(s, c->ev_load[0][g & 3], 0));
+    CK(cudaStreamWaitEvent(s, c->ev_load[1][g & 3], 0));
   }
-  for (int g = 0; g < steps; ++g) {
-    step_of(g, &it, &ly);
-    forward_step(rs, g, it, ly);
-    if (paged && g + 2 < steps) {
-      int it2, ly2;
-      step_of(g + 2, &it2, &ly2);
-      for (int kind = 1; kind <= 2; ++kind) materialize(rs, g + 2, it2, ly2, kind);
+  log_only(c, ss.rs.log, s, XPGB_EV_COMPUTE_START, it, layer);
+  if (o->compute_delay_s) {
+    const float d = o->compute_delay_s[(size_t)g];
+    if (d > 0) {
+      k_sleep<<<1, 1, 0, s>>>((uint64_t)(d * 1e9));
+      note_launch();
+      CKLAUNCH();
     }
   }
+}
+
+// compute-done on `s` and the WAR event the loaders of step g+2 wait on.
+static void session_release(Ctx* c, int g, cudaStream_t s) {
+  Session& ss = session_of(c);
+  if (!ss.active) XFAIL(XPGB_ERR, "no active session");
+  int it, layer;
+  step_of(c, g, &it, &layer);
+  log_only(c, ss.rs.log, s, XPGB_EV_COMPUTE_DONE, it, layer);
+  CK(cudaEventRecord(c->ev_comp[g & 3], s));
+  if (ss.o.sequential) CK(cudaStreamSynchronize(s));
+}
+
+// Built-in compute of step g (single-GPU layer_forward chain) on the compute stream.
+static void session_compute(Ctx* c, int g) {
+  Session& ss = session_of(c);
+  const xpgb_run_opts* o = &ss.o;
+  int it, layer;
+  step_of(c, g, &it, &layer);
+  cudaStream_t s = c->s_comp;
+  const int kk = std::min(o->top_k, c->L);
+  const int T = o->tokens;
+  c->cur_ev = (o->profile && T > 0) ? &c->run_ev[(size_t)g * 7] : nullptr;
+  prof_rec(c, 0, s);
+  if (layer == 1 && T > 0) {
+    // one route+plan launch per decode step covers all N layers; plans alternate between
+    // buffers 0/1 so the next step's plan never overwrites rows still in use
+    if (it == 1) enqueue_plan(c, 0, 1, c->N, T, o->top_k, o->router_seed, s);
+    if (it < o->iterations) enqueue_plan(c, it & 1, 1, c->N, T, o->top_k, o->router_seed, s);
+  }
+  const int b = (it - 1) & 1;
+  const bool last = (g + 1 == ss.steps);
+  const int32_t* next_pos = nullptr;
+  if (!last && T > 0) next_pos = layer < c->N ? c->plan_pos[b] + (size_t)layer * T * kk : c->plan_pos[it & 1];
+  enqueue_forward(c, layer, ss.rs.acts, ss.rs.acts, T, o->top_k, b, g == 0, next_pos, s);
+  c->cur_ev = nullptr;
+}
+
+static void session_end(Ctx* c, xpgb_report* rep) {
+  Session& ss = session_of(c);
+  if (!ss.active) XFAIL(XPGB_ERR, "no active session");
+  ss.active = false;
+  const xpgb_run_opts* o = &ss.o;
+  RunState& rs = ss.rs;
+  const int N = c->N;
+  const int steps = ss.steps;
+  const int kk = std::min(o->top_k, c->L);
+  const bool paged = ss.paged;
+  cudaStream_t s = c->s_comp;
   CK(cudaEventRecord(c->ev_end, s));
-  CK(cudaStreamSynchronize(c->s_copy[0]));
-  CK(cudaStreamSynchronize(c->s_copy[1]));
-  CK(cudaStreamSynchronize(s));
+  CK(cudaDeviceSynchronize());
 
   // collect the log
   int32_t n = 0;
@@ -739,9 +835,9 @@ static void run_impl(Ctx* c, const xpgb_run_opts* o, const float* x, float* y, x
   rep->page_fault = fw != 0;
 
   // routed experts per layer (routing is iteration-invariant) -> algorithmic bytes
-  if (o->tokens > 0) {
+  if (o->tokens > 0 && rs.acts) {
     std::vector<int32_t> tk((size_t)N * o->tokens * kk);
-    CK(cudaMemcpy(tk.data(), c->topk_all, tk.size() * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(tk.data(), c->plan_topk[0], tk.size() * 4, cudaMemcpyDeviceToHost));
     long long active = 0;
     for (int l = 0; l < N; ++l) {
       std::vector<char> seen(c->L + 1, 0);
@@ -753,19 +849,19 @@ static void run_impl(Ctx* c, const xpgb_run_opts* o, const float* x, float* y, x
     }
     const long long pairs = (long long)o->tokens * kk;
     rep->active_experts = (int32_t)active;
-    rep->down_splits = c->last_times.down_splits;
+    rep->down_splits = c->last_splits;
     rep->gate_up_bytes = (long long)((double)active / N * c->s1) + pairs * c->H * 2 + pairs * c->F * 2;
     rep->down_bytes = (long long)((double)active / N * c->s2) + pairs * c->F * 2 +
                       pairs * (long long)c->H * 4 * std::max(1, rep->down_splits);
   }
-  if (o->profile && steps > 0) {
+  if (o->profile && steps > 0 && o->tokens > 0) {
     double gu = 0, dn = 0, aux = 0;
     for (int g = 0; g < steps; ++g) {
       float ms[6];
       for (int i = 0; i < 6; ++i) CK(cudaEventElapsedTime(&ms[i], c->run_ev[(size_t)g * 7 + i], c->run_ev[(size_t)g * 7 + i + 1]));
       gu += ms[3];
       dn += ms[4];
-      aux += ms[1] + ms[2] + ms[5];
+      aux += ms[0] + ms[1] + ms[2] + ms[5];
     }
     rep->kern_gate_up_ns = gu * 1e6 / steps;
     rep->kern_down_ns = dn * 1e6 / steps;
@@ -783,6 +879,51 @@ static void run_impl(Ctx* c, const xpgb_run_opts* o, const float* x, float* y, x
         }
     CK(cudaMemset(c->d_pt, 0xFF, 2 * (size_t)c->N * c->E * sizeof(int32_t)));
   }
+}
+
+
+static void session_abort(Ctx* c) {
+  Session& ss = session_of(c);
+  if (!ss.active) return;
+  ss.active = false;
+  cudaDeviceSynchronize();
+  // drop every binding so the next run starts from an empty ring
+  for (int k = 0; k < 2; ++k)
+    for (size_t pi = 0; pi < c->st[k].size(); ++pi) {
+      if (c->blk[k][pi]) {
+        c->free_ids[k].insert(c->blk[k][pi]);
+        c->owner[k][c->blk[k][pi]] = -1;
+      }
+      c->blk[k][pi] = 0;
+      c->st[k][pi] = XPGB_PAGE_UNMAPPED;
+    }
+  c->bound = 0;
+  cudaMemset(c->d_pt, 0xFF, 2 * (size_t)c->N * c->E * sizeof(int32_t));
+}
+
+static void run_impl(Ctx* c, const xpgb_run_opts* o, const float* x, float* y, xpgb_report* rep) {
+  if (o->tokens > 0 && y != x) {
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpyAsync(y, x, (size_t)o->tokens * c->H * 4, cudaMemcpyDeviceToDevice, c->s_comp));
+  }
+  session_begin(c, o, y);
+  Session& ss = session_of(c);
+  try {
+  // inline order: mat(0), mat(1), then fwd(g) | mat(g+2) (pipeline.py:412-424); the
+  // async mode enqueues the same order so every waited event is already recorded.
+  session_materialize(c, 0);
+  session_materialize(c, 1);
+  for (int g = 0; g < ss.steps; ++g) {
+    session_acquire(c, g, c->s_comp);
+    session_compute(c, g);
+    session_release(c, g, c->s_comp);
+    session_materialize(c, g + 2);
+  }
+  } catch (...) {
+    session_abort(c);
+    throw;
+  }
+  session_end(c, rep);
 }
 
 static void stage_device_tier(Ctx* c) {
@@ -882,9 +1023,8 @@ int xpgb_destroy(xpgb_ctx* h) {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     free_pools(c);
-    LayerWork& w = c->work;
-    void* ptrs[] = {w.pos, w.offsets, w.slot_gu, w.slot_dn, w.units1, w.units2, w.counters, w.xp, w.hbuf, w.part,
-                    c->topk_single, c->topk_all, c->d_fault, c->d_log, c->d_log_count};
+    free_work(c);
+    void* ptrs[] = {c->d_fault, c->d_log, c->d_log_count};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (c->host && c->host_owned) cudaFreeHost(c->host);
@@ -898,6 +1038,7 @@ int xpgb_destroy(xpgb_ctx* h) {
     cudaEventDestroy(c->ev_end);
     for (int i = 0; i < 7; ++i) cudaEventDestroy(c->pev[i]);
     for (cudaEvent_t e : c->run_ev) cudaEventDestroy(e);
+    delete c->sess;
     cudaStreamDestroy(c->s_comp);
     delete h;
   });
@@ -1130,7 +1271,7 @@ int xpgb_layer_forward(xpgb_ctx* h, int32_t layer, const float* x_dev, float* y_
     Ctx* c = &h->c;
     if (layer < 1 || layer > c->N) XFAIL(XPGB_ERR_OUT_OF_RANGE, "layer %d outside [1, %d]", layer, c->N);
     if (top_k < 1) XFAIL(XPGB_ERR_OUT_OF_RANGE, "top_k must be >= 1");
-    enqueue_forward(c, layer, x_dev, y_dev, tokens, top_k, router_seed, nullptr, (cudaStream_t)stream);
+    enqueue_layer(c, layer, x_dev, y_dev, tokens, top_k, router_seed, (cudaStream_t)stream);
   });
 }
 
@@ -1161,6 +1302,44 @@ int xpgb_run(xpgb_ctx* h, const xpgb_run_opts* opts, const float* x_dev, float* 
     if (!opts || !rep) XFAIL(XPGB_ERR, "null argument");
     run_impl(&h->c, opts, x_dev, y_dev, rep);
   });
+}
+
+int xpgb_session_begin(xpgb_ctx* h, const xpgb_run_opts* opts, float* acts_dev) {
+  return guard([&] {
+    if (!opts) XFAIL(XPGB_ERR, "null argument");
+    session_begin(&h->c, opts, acts_dev);
+  });
+}
+int xpgb_session_materialize(xpgb_ctx* h, int32_t step) {
+  return guard([&] {
+    try {
+      session_materialize(&h->c, step);
+    } catch (...) {
+      session_abort(&h->c);
+      throw;
+    }
+  });
+}
+int xpgb_session_acquire(xpgb_ctx* h, int32_t step, void* stream) {
+  return guard([&] { session_acquire(&h->c, step, (cudaStream_t)stream); });
+}
+int xpgb_session_compute(xpgb_ctx* h, int32_t step) {
+  return guard([&] {
+    if (!session_of(&h->c).rs.acts) XFAIL(XPGB_ERR, "session has no activation buffer for built-in compute");
+    session_compute(&h->c, step);
+  });
+}
+int xpgb_session_release(xpgb_ctx* h, int32_t step, void* stream) {
+  return guard([&] { session_release(&h->c, step, (cudaStream_t)stream); });
+}
+int xpgb_session_end(xpgb_ctx* h, xpgb_report* rep) {
+  return guard([&] {
+    if (!rep) XFAIL(XPGB_ERR, "null argument");
+    session_end(&h->c, rep);
+  });
+}
+int xpgb_session_abort(xpgb_ctx* h) {
+  return guard([&] { session_abort(&h->c); });
 }
 
 int xpgb_log_get(xpgb_ctx* h, xpgb_record* out, int32_t cap, int32_t* n) {
@@ -1195,20 +1374,32 @@ int xpgb_experts_forward(xpgb_ctx* h, int32_t layer, const void* rows_dev, const
     Ctx* c = &h->c;
     if (layer < 1 || layer > c->N) XFAIL(XPGB_ERR_OUT_OF_RANGE, "layer %d outside [1, %d]", layer, c->N);
     cudaStream_t s = (cudaStream_t)stream;
-    ensure_work(c, std::max(n_rows, 1), 1);
+    if (n_rows > c->cap_rows || !c->xp) ensure_work(c, std::max(n_rows, 1), 1);
     if (n_rows == 0) return;
-    LayerWork w = c->work;
-    CK(cudaMemcpyAsync(w.xp, rows_dev, (size_t)n_rows * c->H * 2, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(c->xp, rows_dev, (size_t)n_rows * c->H * 2, cudaMemcpyDeviceToDevice, s));
     const int bn = pick_bn(n_rows);
     const int splits = pick_splits(c, n_rows, 1, bn);
-    const size_t pages = (size_t)c->N * c->E;
-    launch_plan_rows(w, offsets_dev, c->d_pt, c->d_pt + pages, layer, c->e_first, c->E, c->F, c->H, bn, bn, splits, s);
+    launch_gate_up(c->map_gu, c->map_xp, gemm_params(c, layer, 1, offsets_dev, 1), bn, c->num_sms, s);
     CKLAUNCH();
-    launch_gate_up(c->map_gu, c->map_xp, w, c->F, c->H, bn, c->num_sms, s);
+    launch_down(c->map_dn, c->map_h, gemm_params(c, layer, 2, offsets_dev, splits), bn, c->num_sms, s);
     CKLAUNCH();
-    launch_down(c->map_dn, c->map_h, w, c->F, c->H, bn, splits, c->cap_rows, c->num_sms, s);
+    launch_reduce_rows(c->part, c->d_fault, out_dev, n_rows, c->H, splits, (long long)c->cap_rows * c->H, s);
     CKLAUNCH();
-    launch_reduce_rows(w, out_dev, n_rows, c->H, splits, c->cap_rows, s);
+  });
+}
+
+int xpgb_combine_rows(const float* rows_dev, const int32_t* index_dev, int32_t tokens, int32_t kk, int32_t top_k,
+                      int32_t hidden, float* y_dev, void* stream) {
+  return guard([&] {
+    if (hidden % 4) XFAIL(XPGB_ERR_OUT_OF_RANGE, "hidden_dim must be a multiple of 4");
+    if (kk < 1 || kk > kMaxTopK || top_k < 1) XFAIL(XPGB_ERR_OUT_OF_RANGE, "kk %d outside [1, %d]", kk, kMaxTopK);
+    static long long* zero = nullptr;
+    if (!zero) {
+      CK(cudaMalloc(&zero, sizeof(long long)));
+      CK(cudaMemset(zero, 0, sizeof(long long)));
+    }
+    launch_combine(rows_dev, index_dev, zero, y_dev, tokens, kk, hidden, 1, 0, (float)(1.0 / top_k), nullptr,
+                   nullptr, (cudaStream_t)stream);
     CKLAUNCH();
   });
 }
@@ -1222,13 +1413,12 @@ int xpgb_profile_layer(xpgb_ctx* h, int32_t layer, const float* x_dev, float* y_
     const int kk = std::min(top_k, c->L);
     c->prof = true;
     for (int r = 0; r < std::max(1, reps); ++r) {
-      enqueue_forward(c, layer, x_dev, y_dev, tokens, top_k, router_seed, nullptr, s);
+      enqueue_layer(c, layer, x_dev, y_dev, tokens, top_k, router_seed, s);
       CK(cudaStreamSynchronize(s));
       float ms[6];
       for (int i = 0; i < 6; ++i) CK(cudaEventElapsedTime(&ms[i], c->pev[i], c->pev[i + 1]));
-      acc.route_ns += ms[0] * 1e6;
-      acc.plan_ns += ms[1] * 1e6;
-      acc.gather_ns += ms[2] * 1e6;
+      acc.plan_ns += ms[0] * 1e6;  // route + plan (one launch)
+      acc.gather_ns += ms[1] * 1e6;
       acc.gate_up_ns += ms[3] * 1e6;
       acc.down_ns += ms[4] * 1e6;
       acc.combine_ns += ms[5] * 1e6;
@@ -1237,18 +1427,24 @@ int xpgb_profile_layer(xpgb_ctx* h, int32_t layer, const float* x_dev, float* y_
     const double inv = 1.0 / std::max(1, reps);
     acc.route_ns *= inv; acc.plan_ns *= inv; acc.gather_ns *= inv;
     acc.gate_up_ns *= inv; acc.down_ns *= inv; acc.combine_ns *= inv;
-    int counters[3];
-    CK(cudaMemcpy(counters, c->work.counters, 12, cudaMemcpyDeviceToHost));
     std::vector<int32_t> offs(c->E + 1);
-    CK(cudaMemcpy(offs.data(), c->work.offsets, (c->E + 1) * 4, cudaMemcpyDeviceToHost));
-    long long active = 0;
-    for (int e = 0; e < c->E; ++e) active += (offs[e + 1] > offs[e]);
+    CK(cudaMemcpy(offs.data(), c->plan_off[2] + (size_t)(layer - 1) * (c->E + 1), (c->E + 1) * 4,
+                  cudaMemcpyDeviceToHost));
+    long long active = 0, u1 = 0, u2 = 0;
+    const int bn = pick_bn(tokens);
+    for (int e = 0; e < c->E; ++e) {
+      const int n = offs[e + 1] - offs[e];
+      if (n <= 0) continue;
+      ++active;
+      u1 += (long long)((n + bn - 1) / bn) * ((c->F + kBM - 1) / kBM);
+      u2 += (long long)((n + bn - 1) / bn) * ((c->H + kBM - 1) / kBM) * c->last_splits;
+    }
     const long long pairs = (long long)tokens * kk;
     acc.gate_up_bytes = active * (long long)c->s1 + pairs * c->H * 2 + pairs * c->F * 2;
-    acc.down_bytes = active * (long long)c->s2 + pairs * c->F * 2 + pairs * c->H * 4 * c->last_times.down_splits;
-    acc.n_units_gate_up = counters[0];
-    acc.n_units_down = counters[1];
-    acc.down_splits = c->last_times.down_splits;
+    acc.down_bytes = active * (long long)c->s2 + pairs * c->F * 2 + pairs * c->H * 4 * c->last_splits;
+    acc.n_units_gate_up = (int32_t)u1;
+    acc.n_units_down = (int32_t)u2;
+    acc.down_splits = c->last_splits;
     c->last_times = acc;
     *out = acc;
   });

@@ -1,0 +1,282 @@
+"""Expert parallelism over G GPUs: one rank per GPU, experts sharded contiguously.
+
+No reference counterpart (the reference is single-process).  The
+partition follows the north star: rank r owns experts
+``[first_r, first_r + count_r)`` of every layer — its own HBM ring, its own
+pinned host pool holding only its shard, its own copy streams — and a layer
+exchanges tokens twice:
+
+* dispatch: each (token, routed expert) row goes, as bf16, to the expert's owner;
+* combine: the owner's fp32 expert outputs come back and the token's owner sums
+  them in ascending expert order with weight f32(1/top_k) (pipeline.py:198-207).
+
+Rank r's T tokens are rows ``[r*T, (r+1)*T)`` of the global step batch, so the
+router's token index is the global row and a G-rank step computes exactly what
+one GPU computes on the concatenated batch.  The router is a pure function of
+(seed, token, layer), so every rank computes the global routing table locally
+and derives send/receive counts and every permutation from it — no count
+exchange.  The exchange itself is ``all_to_all_single`` (NCCL over NVLink on
+GPUs, gloo in the CPU tests); the expert GEMMs are libxpgb's tcgen05 kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import call
+from .geometry import ModelSpec, tensor_offset, ExpertTensorId, TensorKind
+from .streamed import ForwardSpec, RunReport, _kernel_stats, _records_from_log, _intervals, validate_ordering
+
+
+def shard_bounds(num_experts: int, world: int):
+    """Contiguous, balanced expert blocks: [(first, count)] per rank (0-based first)."""
+    base, rem = divmod(num_experts, world)
+    out, first = [], 0
+    for r in range(world):
+        n = base + (1 if r < rem else 0)
+        out.append((first, n))
+        first += n
+    return out
+
+
+def shard_payload(container, first: int, count: int):
+    """Pinned uint8 tensor with experts [first, first+count) of every layer, in
+    shard-local container order (layer, local expert, kind)."""
+    from .geometry import _pinned_bytes
+
+    spec = container.spec
+    eb = spec.expert_bytes
+    out = _pinned_bytes(spec.num_layers * count * eb, True)
+    for layer in range(1, spec.num_layers + 1):
+        src = tensor_offset(ExpertTensorId(layer, first + 1, TensorKind.GATE_UP), spec)
+        dst = (layer - 1) * count * eb
+        out[dst:dst + count * eb].copy_(container.pinned[src:src + count * eb])
+    return out
+
+
+@dataclass
+class DispatchPlan:
+    """Index bookkeeping of one layer's dispatch/combine on one rank (torch tensors)."""
+
+    send_counts: list      # rows this rank sends to each rank
+    recv_counts: list      # rows this rank receives from each rank
+    send_rows: object      # [n_send] local token row of each sent pair, in send order
+    to_expert: object      # [n_recv] arrival index of each expert-major row
+    from_expert: object    # [n_recv] expert-major index of each arrival row
+    offsets: object        # [count+1] expert-major row offsets of the local experts (int32)
+    ret_index: object      # [T, kk] position of each (token, slot) in the returned buffer (int32)
+
+
+def build_plan(routes, rank: int, world: int, tokens: int, bounds) -> DispatchPlan:
+    """routes: [world*tokens, kk] int tensor of 1-based ids (ascending per row)."""
+    import torch
+
+    dev = routes.device
+    G, T = world, tokens
+    kk = routes.shape[1]
+    L = sum(n for _, n in bounds)
+    owner = torch.empty(L, dtype=torch.int64, device=dev)
+    for r, (f, n) in enumerate(bounds):
+        owner[f:f + n] = r
+    e0 = routes.to(torch.int64) - 1                      # [G*T, kk] 0-based expert
+    dst = owner[e0]                                      # owner rank per pair
+    g_tok = torch.arange(G * T, device=dev).unsqueeze(1).expand(G * T, kk)
+    slot = torch.arange(kk, device=dev).unsqueeze(0).expand(G * T, kk)
+    src = g_tok // T
+    local_tok = g_tok - src * T
+    # canonical pair order inside a (src -> dst) message: (expert, local token, slot)
+    inner = (e0 * T + local_tok) * kk + slot
+    span = L * T * kk
+
+    # ---- send side: my tokens, ordered by (dst, expert, token, slot)
+    mine = slice(rank * T, (rank + 1) * T)
+    key = (dst[mine] * span + inner[mine]).reshape(-1)
+    send_order = torch.argsort(key, stable=True)
+    send_counts = torch.bincount(dst[mine].reshape(-1), minlength=G)
+    send_rows = (send_order // kk)
+    ret_index = torch.empty(T * kk, dtype=torch.int64, device=dev)
+    ret_index[send_order] = torch.arange(T * kk, device=dev)
+
+    # ---- receive side: every pair I own, in arrival order (src, expert, token, slot)
+    own = (dst == rank).reshape(-1)
+    akey = (src.reshape(-1) * span + inner.reshape(-1))[own]
+    arrival = torch.argsort(akey, stable=True)
+    a_src = src.reshape(-1)[own][arrival]
+    a_exp = e0.reshape(-1)[own][arrival]
+    recv_counts = torch.bincount(a_src, minlength=G)
+    to_expert = torch.argsort(a_exp, stable=True)        # expert-major row i <- arrival to_expert[i]
+    from_expert = torch.empty_like(to_expert)
+    from_expert[to_expert] = torch.arange(to_expert.numel(), device=dev)
+    first, count = bounds[rank]
+    per_exp = torch.bincount(a_exp - first, minlength=count) if a_exp.numel() else torch.zeros(count, dtype=torch.int64, device=dev)
+    offsets = torch.zeros(count + 1, dtype=torch.int32, device=dev)
+    offsets[1:] = torch.cumsum(per_exp, 0).to(torch.int32)
+    return DispatchPlan(
+        send_counts=[int(v) for v in send_counts.tolist()],
+        recv_counts=[int(v) for v in recv_counts.tolist()],
+        send_rows=send_rows,
+        to_expert=to_expert,
+        from_expert=from_expert,
+        offsets=offsets,
+        ret_index=ret_index.reshape(T, kk).to(torch.int32),
+    )
+
+
+class ExpertParallelMoE:
+    """One rank's MoE layer under expert parallelism.
+
+    route_fn(seed, n_tokens, layer, L, k) -> int [n_tokens, kk] (default: libxpgb router kernel);
+    expert_fn(layer, rows_bf16 [n, H], offsets int32 [count+1]) -> fp32 [n, H] unscaled expert outputs
+    (default: libxpgb grouped SwiGLU through this rank's page table);
+    combine_fn(rows fp32, index int32 [T, kk], top_k) -> fp32 [T, H] (default: libxpgb ordered combine).
+    The defaults need a CUDA device; the CPU tests inject oracle-backed functions.
+    """
+
+    def __init__(self, spec: ModelSpec, fwd: ForwardSpec, rank: int, world: int, group=None, ctx=None,
+                 route_fn=None, expert_fn=None, combine_fn=None):
+        self.spec = spec
+        self.fwd = fwd
+        self.rank = rank
+        self.world = world
+        self.group = group
+        self.ctx = ctx
+        self.bounds = shard_bounds(spec.experts_per_layer, world)
+        self.route_fn = route_fn or self._gpu_route
+        self.expert_fn = expert_fn or self._gpu_experts
+        self.combine_fn = combine_fn or self._gpu_combine
+
+    # ---- defaults on the GPU
+    def _gpu_route(self, seed, n_tokens, layer, L, k):
+        from .device import route_table
+
+        return route_table(seed, n_tokens, 1, L, k, device=self.ctx.device, layer_first=layer)[0]
+
+    def _gpu_experts(self, layer, rows, offsets):
+        import torch
+
+        from .device import current_stream_ptr
+
+        out = torch.empty((rows.shape[0], self.spec.hidden_dim), dtype=torch.float32, device=rows.device)
+        if rows.shape[0]:
+            call("xpgb_experts_forward", self.ctx.handle, layer, C.c_void_p(rows.data_ptr()),
+                 C.c_void_p(offsets.data_ptr()), int(rows.shape[0]), C.c_void_p(out.data_ptr()),
+                 C.c_void_p(current_stream_ptr(self.ctx.device)))
+        return out
+
+    def _gpu_combine(self, rows, index, top_k):
+        import torch
+
+        from .device import current_stream_ptr
+
+        T, kk = index.shape
+        y = torch.empty((T, self.spec.hidden_dim), dtype=torch.float32, device=index.device)
+        if T:
+            call("xpgb_combine_rows", C.c_void_p(rows.data_ptr()), C.c_void_p(index.data_ptr()), T, kk, top_k,
+                 self.spec.hidden_dim, C.c_void_p(y.data_ptr()), C.c_void_p(current_stream_ptr(self.ctx.device)))
+        return y
+
+    # ---- one layer
+    def plan(self, layer: int, tokens: int) -> DispatchPlan:
+        routes = self.route_fn(self.fwd.router_seed, self.world * tokens, layer, self.spec.experts_per_layer,
+                               self.fwd.top_k)
+        return build_plan(routes, self.rank, self.world, tokens, self.bounds)
+
+    def forward(self, layer: int, x, plan: DispatchPlan | None = None):
+        import torch
+        import torch.distributed as dist
+
+        T, H = x.shape
+        plan = plan or self.plan(layer, T)
+        send = x.index_select(0, plan.send_rows).to(torch.bfloat16)
+        recv = torch.empty((sum(plan.recv_counts), H), dtype=torch.bfloat16, device=x.device)
+        self._a2a(recv, send, plan.recv_counts, plan.send_counts)
+        rows = recv.index_select(0, plan.to_expert)
+        out = self.expert_fn(layer, rows, plan.offsets)
+        back = out.index_select(0, plan.from_expert)
+        ret = torch.empty((send.shape[0], H), dtype=torch.float32, device=x.device)
+        self._a2a(ret, back, plan.send_counts, plan.recv_counts)
+        return self.combine_fn(ret, plan.ret_index, self.fwd.top_k)
+
+    def _a2a(self, out, inp, out_splits, in_splits):
+        import torch
+        import torch.distributed as dist
+
+        if self.world == 1:
+            out.copy_(inp)
+            return
+        if out.dtype == torch.bfloat16 and out.device.type == "cpu":
+            # gloo has no 16-bit all_to_all: move pairs of bf16 words as int32 (H is even)
+            dist.all_to_all_single(out.view(torch.int32), inp.contiguous().view(torch.int32), out_splits, in_splits,
+                                   group=self.group)
+        else:
+            dist.all_to_all_single(out, inp.contiguous(), out_splits, in_splits, group=self.group)
+
+
+class ExpertParallelRunner:
+    """The paged decode loop of one rank under EP (StreamedRunner semantics per rank).
+
+    The rank's libxpgb context pages its expert shard through its own 2-layer ring
+    (session API: RAW/WAR events, ordering log); the compute of each step is the
+    EP dispatch -> grouped SwiGLU -> combine of ExpertParallelMoE on torch's stream.
+    """
+
+    def __init__(self, spec: ModelSpec, container, fwd: ForwardSpec, rank: int, world: int, device: int = 0,
+                 group=None, shard_pool=None):
+        from .device import Context
+
+        self.spec = spec
+        self.fwd = fwd
+        self.rank, self.world = rank, world
+        first, count = shard_bounds(spec.experts_per_layer, world)[rank]
+        self.ctx = Context(spec, _lib.POOL_RING, device, max_tokens=world * fwd.tokens_per_step)
+        self.ctx.set_expert_shard(first, count)
+        pool = shard_pool if shard_pool is not None else shard_payload(container, first, count)
+        self.ctx.attach_host_pool(pool)
+        self.moe = ExpertParallelMoE(spec, fwd, rank, world, group=group, ctx=self.ctx)
+
+    def run(self, iterations: int, acts, profile: bool = False) -> RunReport:
+        import torch
+
+        from .device import current_stream_ptr
+
+        N = self.spec.num_layers
+        x = acts if isinstance(acts, torch.Tensor) else torch.from_numpy(np.asarray(acts, np.float32))
+        x = x.to(f"cuda:{self.ctx.device}", torch.float32).contiguous()
+        T = x.shape[0]
+        plans = [self.moe.plan(layer, T) for layer in range(1, N + 1)]  # routing: pure function of (seed, t, layer)
+        opts = _lib.RunOpts()
+        opts.iterations = iterations
+        opts.tokens = self.world * T
+        opts.top_k = self.fwd.top_k
+        opts.router_seed = int(self.fwd.router_seed) & 0xFFFFFFFFFFFFFFFF
+        opts.log_enable = 1
+        h = self.ctx.handle
+        torch.cuda.synchronize(self.ctx.device)
+        call("xpgb_session_begin", h, C.byref(opts), None)
+        try:
+            call("xpgb_session_materialize", h, 0)
+            call("xpgb_session_materialize", h, 1)
+            for g in range(iterations * N):
+                layer = g % N + 1
+                st = C.c_void_p(current_stream_ptr(self.ctx.device))
+                call("xpgb_session_acquire", h, g, st)
+                x = self.moe.forward(layer, x, plans[layer - 1])
+                call("xpgb_session_release", h, g, st)
+                call("xpgb_session_materialize", h, g + 2)
+        except Exception:
+            _lib.lib().xpgb_session_abort(h)
+            raise
+        rep = _lib.Report()
+        call("xpgb_session_end", h, C.byref(rep))
+        records = _records_from_log(self.ctx)
+        return RunReport(
+            final_activations=x, arena_peak_bytes=int(rep.arena_peak_bytes), stall_seconds=rep.stall_ns * 1e-9,
+            war_wait_seconds=rep.war_wait_ns * 1e-9, violations=validate_ordering(records), records=records,
+            intervals=_intervals(records), page_fault=self.ctx.fault() if rep.page_fault else None,
+            h2d_bytes=int(rep.h2d_bytes), d2d_bytes=int(rep.d2d_bytes),
+            copy_busy_seconds=(rep.copy_busy_ns[0] * 1e-9, rep.copy_busy_ns[1] * 1e-9),
+            elapsed_seconds=rep.elapsed_ns * 1e-9, kernels=_kernel_stats(rep))

@@ -222,3 +222,53 @@ def test_report_json_fields(X):
     for key in ("activation_checksum", "stall_ms", "arena_peak_bytes", "violation_count", "layer_intervals"):
         assert key in doc
     assert doc["violation_count"] == 0
+
+
+def test_expert_parallel_runner_world1_matches_resident(X, O):
+    """The EP runner (session API + experts_forward + ordered combine) on one GPU."""
+    from paper_2604_02715_b200.expert_parallel import ExpertParallelRunner
+
+    spec = X.ModelSpec(4, 8, 256, 512)
+    fwd = X.ForwardSpec(16, 2, 7)
+    container = X.generate_synthetic_model(spec, 7)
+    x = X.initial_activations(spec, fwd, 7)
+    runner = ExpertParallelRunner(spec, container, fwd, rank=0, world=1)
+    rep = runner.run(2, x)
+    assert rep.page_fault is None and rep.violations == []
+    assert rep.arena_peak_bytes == 2 * spec.experts_per_layer * spec.expert_bytes
+    base = X.resident_baseline(2, spec, container, fwd, acts=x.copy())
+    assert O.rel_l2(rep.final_activations.cpu().numpy(), base) <= 1e-3
+
+
+def test_session_api_external_compute_matches_run(X):
+    """begin/materialize/acquire/compute/release/end reproduces run() bit for bit."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2604_02715_b200 import _lib
+    from paper_2604_02715_b200._lib import call
+
+    spec = X.ModelSpec(4, 4, 128, 256)
+    fwd = X.ForwardSpec(8, 2, 3)
+    container, hier = _hier(X, spec, seed=3)
+    x = X.initial_activations(spec, fwd, 3)
+    runner = X.StreamedRunner(spec, hier, fwd)
+    want = runner.run(2, acts=x.copy()).final_activations
+    acts = torch.from_numpy(x.copy()).cuda()
+    opts = _lib.RunOpts()
+    opts.iterations, opts.tokens, opts.top_k, opts.router_seed, opts.log_enable = 2, 8, 2, 3, 1
+    h = runner.ctx.handle
+    torch.cuda.synchronize()
+    call("xpgb_session_begin", h, C.byref(opts), C.c_void_p(acts.data_ptr()))
+    call("xpgb_session_materialize", h, 0)
+    call("xpgb_session_materialize", h, 1)
+    for g in range(2 * spec.num_layers):
+        call("xpgb_session_acquire", h, g, None)
+        call("xpgb_session_compute", h, g)
+        call("xpgb_session_release", h, g, None)
+        call("xpgb_session_materialize", h, g + 2)
+    rep = _lib.Report()
+    call("xpgb_session_end", h, C.byref(rep))
+    assert acts.cpu().numpy().tobytes() == want.tobytes()
+    assert rep.page_fault == 0
