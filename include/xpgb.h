@@ -45,7 +45,12 @@ typedef enum xpgb_status {
   XPGB_ERR_INFEASIBLE_CONFIG = 10, /* InfeasibleConfigError   */
   XPGB_ERR_CONFIG = 11,            /* ConfigError             */
   XPGB_ERR_DEADLOCK = 12,          /* DeadlockError           */
-  XPGB_ERR_CUDA = 13               /* CUDA failure -> XpgError */
+  XPGB_ERR_CUDA = 13,              /* CUDA failure -> XpgError */
+  XPGB_ERR_ODD_LENGTH = 14,        /* OddLengthError          */
+  XPGB_ERR_EMPTY_HISTOGRAM = 15,   /* EmptyHistogramError     */
+  XPGB_ERR_SYMBOL_NOT_IN_TABLE = 16, /* SymbolNotInTableError */
+  XPGB_ERR_TRUNCATED_STREAM = 17,  /* TruncatedStreamError    */
+  XPGB_ERR_INVALID_CODE = 18       /* InvalidCodeError        */
 } xpgb_status;
 
 /* Page states (paging.py:41-45). */
@@ -108,8 +113,8 @@ typedef struct xpgb_report {
   int64_t war_wait_ns;       /* copy streams blocked on WAR (RunReport.war_wait_seconds) */
   int64_t elapsed_ns;        /* first to last log record */
   int64_t arena_peak_bytes;  /* PageTable.arena_peak_bytes */
-  int64_t h2d_bytes;         /* bytes paged in from the pinned host pool */
-  int64_t d2d_bytes;         /* bytes paged in from the device tier */
+  int64_t h2d_bytes;         /* bytes paged in from the pinned host pool (wire bytes) */
+  int64_t d2d_bytes;         /* raw bytes paged in from the device tier */
   int64_t copy_busy_ns[2];   /* per copy stream: sum of load-start..load-done spans */
   int32_t page_fault;        /* 1 if a compute read a non-resident page */
   int32_t n_records;
@@ -121,6 +126,7 @@ typedef struct xpgb_report {
   int64_t down_bytes;
   int32_t down_splits;
   int32_t active_experts;    /* routed experts summed over the N layers of one iteration */
+  int64_t decoded_bytes;     /* bf16 bytes produced by the GPU exponent decoder */
 } xpgb_report;
 
 /* ---------------------------------------------------------------- basics */
@@ -171,6 +177,38 @@ int xpgb_pt_trace_enable(xpgb_ctx* ctx, int32_t enable);
 int xpgb_pt_trace_get(xpgb_ctx* ctx, char* buf, uint64_t cap, uint64_t* needed);
 /* Map + fetch + mark_resident every tensor of the model (resident pools). */
 int xpgb_make_resident(xpgb_ctx* ctx);
+
+/* ---------------------------------------------------------------- exponent codec (codec.py:48-330)
+ * Stream bytes are bit-identical to xpg's compress(); the chunk index (bit offset of every
+ * `chunk`-value block) is B200 side metadata that lets the GPU decode one stream in parallel.
+ * Packed record layout (all parts 16-byte aligned):
+ *   [sign/mantissa plane: n][exponent stream: bits_len + 8 zero bytes][index: ceil(n/chunk) u32] */
+int xpgb_codec_histogram(const void* data, uint64_t bytes, uint64_t* counts256, int32_t threads);
+/* compress() of one tensor into caller buffers (host). */
+int xpgb_codec_encode(const void* data, uint64_t bytes, const uint8_t* lengths256, void* sm_out, void* bits_out,
+                      uint64_t bits_cap, uint64_t* bits_len, uint64_t* bit_count, uint32_t* index_out,
+                      int32_t chunk);
+/* Compress n_tensors consecutive tensors of a payload into packed records (multi-threaded,
+ * host only).  out == NULL computes the layout only (pool_bytes, rec_offsets, bits_lens,
+ * bit_counts: [n_tensors]); otherwise out (>= pool_bytes) receives the records. */
+int xpgb_codec_pack(const void* payload, int32_t n_tensors, const uint64_t* value_counts, const uint8_t* lengths256,
+                    int32_t chunk, int32_t threads, void* out, uint64_t out_cap, uint64_t* pool_bytes,
+                    uint64_t* rec_offsets, uint64_t* bits_lens, uint64_t* bit_counts);
+/* Byte size of a packed record. */
+uint64_t xpgb_codec_record_bytes(uint64_t n, uint64_t bits_len, int32_t chunk);
+/* Rebuild the chunk index of a stream on the host, validating it like decompress():
+ * TruncatedStreamError / InvalidCodeError statuses (codec.py:304-327). */
+int xpgb_codec_index(const void* bits, uint64_t bits_len, uint64_t n, const uint8_t* lengths256, int32_t chunk,
+                     uint32_t* index_out);
+/* decompress() on the GPU: packed record in device memory -> n bf16 words at out_dev. */
+int xpgb_codec_decode(const void* record_dev, uint64_t n, uint64_t bits_len, int32_t chunk,
+                      const uint8_t* lengths256, void* out_dev, void* stream);
+/* Attach a packed model (records in container order, tensors of this context's shard) to the
+ * context.  Device-tier tensors are then held compressed in HBM and decoded into ring blocks
+ * (the reference's compressed device tier, storage.py:235-238); with host_compressed = 1 the
+ * host tier also ships compressed records over PCIe and decodes them on the GPU. */
+int xpgb_set_codec(xpgb_ctx* ctx, const void* pool, uint64_t pool_bytes, const uint64_t* rec_offsets,
+                   const uint64_t* bits_lens, const uint8_t* lengths256, int32_t chunk, int32_t host_compressed);
 
 /* ---------------------------------------------------------------- compute */
 /* routed_experts (pipeline.py:154-170) for layers [layer_first, layer_first+layer_count):

@@ -53,7 +53,7 @@ class Report(C.Structure):
                 ("copy_busy_ns", C.c_int64 * 2), ("page_fault", C.c_int32), ("n_records", C.c_int32),
                 ("kern_gate_up_ns", C.c_double), ("kern_down_ns", C.c_double), ("kern_aux_ns", C.c_double),
                 ("gate_up_bytes", C.c_int64), ("down_bytes", C.c_int64), ("down_splits", C.c_int32),
-                ("active_experts", C.c_int32)]
+                ("active_experts", C.c_int32), ("decoded_bytes", C.c_int64)]
 
 
 class KernelTimes(C.Structure):
@@ -110,9 +110,18 @@ _SIGS = {
     "xpgb_set_expert_shard": [_P, _I, _I],
     "xpgb_experts_forward": [_P, _I, _P, _P, _I, _P, _P],
     "xpgb_combine_rows": [_P, _P, _I, _I, _I, _I, _P, _P],
+    "xpgb_codec_histogram": [_P, _U64, C.POINTER(_U64), _I],
+    "xpgb_codec_encode": [_P, _U64, C.POINTER(C.c_uint8), _P, _P, _U64, C.POINTER(_U64), C.POINTER(_U64),
+                          C.POINTER(C.c_uint32), _I],
+    "xpgb_codec_pack": [_P, _I, C.POINTER(_U64), C.POINTER(C.c_uint8), _I, _I, _P, _U64, C.POINTER(_U64),
+                        C.POINTER(_U64), C.POINTER(_U64), C.POINTER(_U64)],
+    "xpgb_codec_record_bytes": [_U64, _U64, _I],
+    "xpgb_codec_index": [_P, _U64, _U64, C.POINTER(C.c_uint8), _I, C.POINTER(C.c_uint32)],
+    "xpgb_codec_decode": [_P, _U64, _U64, _I, C.POINTER(C.c_uint8), _P, _P],
+    "xpgb_set_codec": [_P, _P, _U64, C.POINTER(_U64), C.POINTER(_U64), C.POINTER(C.c_uint8), _I, _I],
     "xpgb_profile_layer": [_P, _I, _P, _P, _I, _I, _U64, _I, C.POINTER(KernelTimes)],
 }
-_RESTYPES = {"xpgb_last_error": C.c_char_p, "xpgb_kernel_launches": C.c_int64}
+_RESTYPES = {"xpgb_last_error": C.c_char_p, "xpgb_kernel_launches": C.c_int64, "xpgb_codec_record_bytes": C.c_uint64}
 
 # every symbol declared in include/xpgb.h (tests check the export table against this)
 DECLARED = tuple(_SIGS)

@@ -1,0 +1,261 @@
+// Exponent-Huffman codec: multi-threaded host encoder (bit-identical to
+// xpg codec.py:235-272) and the sm_100a decoder kernel (codec.py:275-330).
+#include <algorithm>
+#include <thread>
+#include <vector>
+
+#include "codec.cuh"
+#include "launch_count.h"
+
+namespace xpgb {
+
+bool codec_canonical_codes(const uint8_t* lengths, uint32_t* codes) {
+  // canonical order (length, symbol) ascending, as HuffmanTable.from_lengths (codec.py:152-173)
+  double kraft = 0.0;
+  int present = 0;
+  for (int s = 0; s < kCodecSymbols; ++s) {
+    codes[s] = 0;
+    if (lengths[s] > kCodecMaxLen) return false;
+    if (lengths[s]) {
+      kraft += 1.0 / (double)(1ull << lengths[s]);
+      ++present;
+    }
+  }
+  if (!present || kraft > 1.0 + 1e-12) return false;
+  uint64_t code = 0;
+  int prev = 0;
+  for (int l = 1; l <= kCodecMaxLen; ++l)
+    for (int s = 0; s < kCodecSymbols; ++s)
+      if (lengths[s] == l) {
+        code <<= (l - prev);
+        codes[s] = (uint32_t)code;
+        code += 1;
+        prev = l;
+      }
+  return true;
+}
+
+void codec_histogram(const uint8_t* data, size_t bytes, uint64_t* counts, int threads) {
+  const size_t n = bytes / 2;
+  threads = std::max(1, std::min(threads, (int)std::max<size_t>(1, n / (1 << 20))));
+  std::vector<std::vector<uint64_t>> part(threads, std::vector<uint64_t>(kCodecSymbols, 0));
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([&, t] {
+      const size_t a = n * t / threads, b = n * (t + 1) / threads;
+      const uint16_t* w = reinterpret_cast<const uint16_t*>(data);
+      uint64_t* c = part[t].data();
+      for (size_t i = a; i < b; ++i) ++c[(w[i] >> 7) & 0xFF];
+    });
+  for (auto& th : pool) th.join();
+  for (int s = 0; s < kCodecSymbols; ++s) {
+    uint64_t v = 0;
+    for (int t = 0; t < threads; ++t) v += part[t][s];
+    counts[s] = v;
+  }
+}
+
+size_t codec_bits_bound(size_t n, const uint8_t* lengths) {
+  int mx = 0;
+  for (int s = 0; s < kCodecSymbols; ++s) mx = std::max<int>(mx, lengths[s]);
+  return (n * (size_t)mx + 7) / 8;
+}
+
+bool codec_encode(const uint16_t* words, size_t n, const uint8_t* lengths, const uint32_t* codes, uint8_t* sm_out,
+                  uint8_t* bits_out, size_t bits_cap, size_t* bits_len, uint64_t* bit_count, uint32_t* index_out,
+                  int chunk, int* missing) {
+  uint64_t acc = 0;
+  int nacc = 0;
+  size_t out = 0;
+  uint64_t total = 0;
+  for (size_t i = 0; i < n; ++i) {
+    const uint16_t w = words[i];
+    const int e = (w >> 7) & 0xFF;
+    const int l = lengths[e];
+    if (!l) {
+      if (missing) *missing = e;
+      return false;
+    }
+    if (index_out && chunk > 0 && (i % (size_t)chunk) == 0) index_out[i / chunk] = (uint32_t)total;
+    sm_out[i] = (uint8_t)(((w >> 8) & 0x80) | (w & 0x7F));
+    acc = (acc << l) | codes[e];
+    nacc += l;
+    total += l;
+    while (nacc >= 8) {
+      nacc -= 8;
+      if (out < bits_cap) bits_out[out] = (uint8_t)(acc >> nacc);
+      ++out;
+    }
+    acc &= (nacc ? ((1ull << nacc) - 1) : 0ull);
+  }
+  if (nacc) {
+    if (out < bits_cap) bits_out[out] = (uint8_t)(acc << (8 - nacc));
+    ++out;
+  }
+  *bits_len = out;
+  *bit_count = total;
+  if (missing) *missing = -1;
+  return out <= bits_cap && total < (1ull << 32);
+}
+
+// Sequential host scan of a stream: rebuilds the chunk index and validates it the way
+// decompress() does (codec.py:304-327).  Returns 0, 1 = truncated, 2 = invalid code.
+int codec_build_index(const uint8_t* bits, size_t bits_len, size_t n, const uint8_t* lengths, int chunk,
+                      uint32_t* index_out, size_t* consumed_bits) {
+  int count[kCodecMaxLen + 1] = {0};
+  uint32_t first_code[kCodecMaxLen + 1] = {0};
+  for (int s = 0; s < kCodecSymbols; ++s)
+    if (lengths[s]) ++count[lengths[s]];
+  uint32_t code = 0;
+  int prev = 0, maxlen = 0;
+  for (int l = 1; l <= kCodecMaxLen; ++l)
+    if (count[l]) {
+      code <<= (l - prev);
+      first_code[l] = code;
+      code += count[l];
+      prev = l;
+      maxlen = l;
+    }
+  const uint64_t total_bits = (uint64_t)bits_len * 8;
+  uint64_t pos = 0;
+  for (size_t i = 0; i < n; ++i) {
+    if (index_out && (i % (size_t)chunk) == 0) index_out[i / chunk] = (uint32_t)pos;
+    uint32_t c = 0;
+    int l = 0;
+    for (;;) {
+      if (pos >= total_bits) return 1;
+      c = (c << 1) | ((bits[pos >> 3] >> (7 - (pos & 7))) & 1);
+      ++pos;
+      ++l;
+      if (l > maxlen) return 2;
+      if (count[l] && c - first_code[l] < (uint32_t)count[l]) break;
+    }
+  }
+  if (consumed_bits) *consumed_bits = pos;
+  return 0;
+}
+
+// ----------------------------------------------------------------------------- GPU decoder
+
+struct DecodeParams {
+  const uint8_t* sm;
+  const uint32_t* bits;
+  const uint32_t* index;
+  uint64_t n;
+  int chunk;
+  uint16_t* out;
+  CodecTable t;
+};
+
+__device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
+
+// One thread decodes one chunk (`chunk` values) starting at index[c]: a 64-bit
+// MSB-first window, a 4096-entry LUT for codes <= 12 bits, canonical
+// first-code search for longer ones.  Output words are assembled as
+// (sign << 15) | (exponent << 7) | mantissa, 8 per 16-byte store.
+__global__ void __launch_bounds__(256) k_exp_decode(DecodeParams p) {
+  __shared__ uint16_t lut[1 << kLutBits];
+  __shared__ uint32_t first_code[kCodecMaxLen + 1];
+  __shared__ int count[kCodecMaxLen + 1], first_rank[kCodecMaxLen + 1];
+  __shared__ uint8_t sorted_sym[kCodecSymbols];
+  __shared__ int maxlen;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < (1 << kLutBits); i += blockDim.x) lut[i] = 0;
+  if (tid <= kCodecMaxLen) count[tid] = 0;
+  __syncthreads();
+  if (tid < kCodecSymbols && p.t.len[tid]) atomicAdd(&count[p.t.len[tid]], 1);
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t code = 0;
+    int prev = 0, rank = 0, ml = 0;
+    for (int l = 1; l <= kCodecMaxLen; ++l) {
+      first_rank[l] = rank;
+      first_code[l] = 0;
+      if (count[l]) {
+        code <<= (l - prev);
+        first_code[l] = code;
+        code += count[l];
+        prev = l;
+        rank += count[l];
+        ml = l;
+      }
+    }
+    maxlen = ml;
+  }
+  __syncthreads();
+  if (tid < kCodecSymbols) {
+    const int l = p.t.len[tid];
+    if (l) {
+      int r = 0;
+      for (int s = 0; s < tid; ++s) r += (p.t.len[s] == l);
+      sorted_sym[first_rank[l] + r] = (uint8_t)tid;
+      if (l <= kLutBits) {
+        const uint32_t code = first_code[l] + r;
+        const uint32_t base = code << (kLutBits - l), span = 1u << (kLutBits - l);
+        for (uint32_t i = 0; i < span; ++i) lut[base + i] = (uint16_t)(tid | (l << 8));
+      }
+    }
+  }
+  __syncthreads();
+
+  const uint64_t n = p.n;
+  const uint64_t n_chunks = (n + p.chunk - 1) / p.chunk;
+  const int ml = maxlen;
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + tid; c < n_chunks; c += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t v0 = c * p.chunk;
+    const uint64_t v1 = (v0 + p.chunk < n) ? v0 + p.chunk : n;
+    const uint32_t bitpos = p.index[c];
+    const uint32_t w = bitpos >> 5, sh = bitpos & 31;
+    uint64_t win = (((uint64_t)bswap32(p.bits[w]) << 32) | bswap32(p.bits[w + 1])) << sh;
+    int avail = 64 - (int)sh;
+    const uint32_t* wp = p.bits + w + 2;
+    for (uint64_t v = v0; v < v1; v += 8) {
+      const int cnt = (int)((v1 - v) < 8 ? (v1 - v) : 8);
+      uint32_t packed[4] = {0, 0, 0, 0};
+      uint2 smv = make_uint2(0, 0);
+      if (cnt == 8) smv = *reinterpret_cast<const uint2*>(p.sm + v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j >= cnt) break;
+        if (avail < 32) {
+          win |= (uint64_t)bswap32(*wp++) << (32 - avail);
+          avail += 32;
+        }
+        const uint16_t e = lut[win >> (64 - kLutBits)];
+        int l = e >> 8;
+        int sym = e & 0xFF;
+        if (!l) {
+          for (l = kLutBits + 1; l <= ml; ++l) {
+            const uint32_t code = (uint32_t)(win >> (64 - l));
+            if (count[l] && code - first_code[l] < (uint32_t)count[l]) {
+              sym = sorted_sym[first_rank[l] + (code - first_code[l])];
+              break;
+            }
+          }
+        }
+        win <<= l;
+        avail -= l;
+        const uint32_t s = (cnt == 8) ? (((j < 4 ? smv.x : smv.y) >> (8 * (j & 3))) & 0xFF) : p.sm[v + j];
+        const uint32_t word = ((s & 0x80u) << 8) | ((uint32_t)sym << 7) | (s & 0x7Fu);
+        packed[j >> 1] |= word << (16 * (j & 1));
+      }
+      if (cnt == 8) {
+        *reinterpret_cast<uint4*>(p.out + v) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+      } else {
+        for (int j = 0; j < cnt; ++j) p.out[v + j] = (uint16_t)(packed[j >> 1] >> (16 * (j & 1)));
+      }
+    }
+  }
+}
+
+void launch_exp_decode(const uint8_t* sm, const uint32_t* bits, const uint32_t* index, uint64_t n, int chunk,
+                       const CodecTable& table, uint16_t* out, cudaStream_t s) {
+  if (n == 0) return;
+  DecodeParams p{sm, bits, index, n, chunk, out, table};
+  const uint64_t n_chunks = (n + chunk - 1) / chunk;
+  const uint64_t blocks = std::min<uint64_t>((n_chunks + 255) / 256, 148 * 8);
+  k_exp_decode<<<(unsigned)blocks, 256, 0, s>>>(p);
+  note_launch();
+}
+
+}  // namespace xpgb

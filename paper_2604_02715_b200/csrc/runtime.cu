@@ -20,10 +20,12 @@
 #include <cstring>
 #include <exception>
 #include <set>
+#include <thread>
 #include <string>
 #include <vector>
 
 #include "../../include/xpgb.h"
+#include "codec.cuh"
 #include "launch_count.h"
 #include "moe_kernels.cuh"
 #include "ptx_sm100.cuh"
@@ -222,6 +224,19 @@ struct Ctx {
   int32_t* d_log_count = nullptr;
   int log_cap = 0;
   std::vector<xpgb_record> last_log;
+
+  // exponent codec (compressed tiers)
+  bool codec = false, host_codec = false;
+  const uint8_t* cpool = nullptr;  // packed records, container order of this shard (pinned host)
+  uint64_t cpool_bytes = 0;
+  std::vector<uint64_t> rec_off, rec_bits;  // [N*E*2]
+  CodecTable ctab{};
+  int cchunk = 1024;
+  uint8_t* stage[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [kind][buffer]
+  uint64_t stage_cap[2] = {0, 0};
+  cudaStream_t s_dec[2] = {nullptr, nullptr};
+  cudaEvent_t ev_copied[2][2], ev_decoded[2][2], ev_mapped[2], ev_raw[2];
+  bool codec_events = false;
 
   // profiling
   bool prof = false;
@@ -532,6 +547,7 @@ struct RunState {
   float* acts;
   long long h2d = 0, d2d = 0;
   bool log;
+  long long decoded = 0;
 };
 
 static void set_rec(PtOp& op, int idx, int ev, int it, int layer, int kind, int tit, int tl) {
@@ -601,21 +617,77 @@ static void materialize(RunState& rs, int g, int it, int layer, int kind) {
     launch_op(o2, s);
   }
   const float* delays = rs.o->fetch_delay_s;
-  for (int e = 0; e < E; ++e) {
-    const int pi = (layer - 1) * E + e;
-    if (delays) {
-      const float d = delays[((size_t)(layer - 1) * c->L + (c->e_first + e)) * 2 + k];
-      if (d > 0) {
-        k_sleep<<<1, 1, 0, s>>>((uint64_t)(d * 1e9));
-        note_launch();
+  auto delay_of = [&](int e) -> float {
+    return delays ? delays[((size_t)(layer - 1) * c->L + (c->e_first + e)) * 2 + k] : 0.f;
+  };
+  auto sleep_on = [&](cudaStream_t st, float d) {
+    k_sleep<<<1, 1, 0, st>>>((uint64_t)(d * 1e9));
+    note_launch();
+    CKLAUNCH();
+  };
+  cudaStream_t done_stream = s;
+  if (!c->codec) {
+    for (int e = 0; e < E; ++e) {
+      if (delay_of(e) > 0) sleep_on(s, delay_of(e));
+      bool from_host = true;
+      const uint64_t n = fetch(c, layer, c->e_first + e + 1, kind, block_ptr(c, kind, blocks[e]), sigma_of(c, kind), s,
+                               &from_host);
+      (from_host ? rs.h2d : rs.d2d) += n;
+    }
+  } else {
+    // compressed tiers: records reach a decode stream (copied over PCIe into a staging
+    // buffer for the host tier, read in place for the device tier) and are expanded
+    // straight into the ring block; staging is double-buffered so the link never waits.
+    cudaStream_t d = c->s_dec[k];
+    CK(cudaEventRecord(c->ev_mapped[k], s));
+    CK(cudaStreamWaitEvent(d, c->ev_mapped[k], 0));
+    bool raw_on_s = false;
+    int hb = 0;
+    for (int e = 0; e < E; ++e) {
+      const size_t pi = (size_t)(layer - 1) * E + e, ti = pi * 2 + k;
+      const uint64_t n = sigma_of(c, kind) / 2;
+      uint8_t* dst = block_ptr(c, kind, blocks[e]);
+      const float dl = delay_of(e);
+      if (c->backend[ti] == 1) {
+        if (dl > 0) sleep_on(d, dl);
+        const uint8_t* rec = c->dev_tier + c->dev_off[ti];
+        const uint64_t nb = c->rec_bits[ti];
+        const uint64_t sm16 = (n + 15) & ~15ull, bits16 = (nb + 8 + 15) & ~15ull;
+        launch_exp_decode(rec, reinterpret_cast<const uint32_t*>(rec + sm16),
+                          reinterpret_cast<const uint32_t*>(rec + sm16 + bits16), n, c->cchunk, c->ctab,
+                          reinterpret_cast<uint16_t*>(dst), d);
         CKLAUNCH();
+        rs.decoded += 2 * n;
+      } else if (c->host_codec) {
+        const int buf = hb++ & 1;
+        const uint64_t nb = c->rec_bits[ti];
+        const uint64_t rb = xpgb_codec_record_bytes(n, nb, c->cchunk);
+        CK(cudaStreamWaitEvent(s, c->ev_decoded[k][buf], 0));
+        if (dl > 0) sleep_on(s, dl);
+        CK(cudaMemcpyAsync(c->stage[k][buf], c->cpool + c->rec_off[ti], rb, cudaMemcpyHostToDevice, s));
+        CK(cudaEventRecord(c->ev_copied[k][buf], s));
+        rs.h2d += rb;
+        CK(cudaStreamWaitEvent(d, c->ev_copied[k][buf], 0));
+        const uint8_t* rec = c->stage[k][buf];
+        const uint64_t sm16 = (n + 15) & ~15ull, bits16 = (nb + 8 + 15) & ~15ull;
+        launch_exp_decode(rec, reinterpret_cast<const uint32_t*>(rec + sm16),
+                          reinterpret_cast<const uint32_t*>(rec + sm16 + bits16), n, c->cchunk, c->ctab,
+                          reinterpret_cast<uint16_t*>(dst), d);
+        CKLAUNCH();
+        CK(cudaEventRecord(c->ev_decoded[k][buf], d));
+        rs.decoded += 2 * n;
+      } else {
+        if (dl > 0) sleep_on(s, dl);
+        bool from_host = true;
+        rs.h2d += fetch(c, layer, c->e_first + e + 1, kind, dst, sigma_of(c, kind), s, &from_host);
+        raw_on_s = true;
       }
     }
-    bool from_host = true;
-    const uint64_t n = fetch(c, layer, c->e_first + e + 1, kind, block_ptr(c, kind, blocks[e]), sigma_of(c, kind), s,
-                             &from_host);
-    (from_host ? rs.h2d : rs.d2d) += n;
-    (void)pi;
+    if (raw_on_s) {
+      CK(cudaEventRecord(c->ev_raw[k], s));
+      CK(cudaStreamWaitEvent(d, c->ev_raw[k], 0));
+    }
+    done_stream = d;
   }
   for (int e = 0; e < E; ++e) pt_mark_resident(c, layer, c->e_first + e + 1, kind);
   for (int e0 = 0; e0 < E; e0 += chunk) {
@@ -624,10 +696,13 @@ static void materialize(RunState& rs, int g, int it, int layer, int kind) {
     o3.set_n = std::min(chunk, E - e0);
     for (int i = 0; i < o3.set_n; ++i) o3.vals[i] = pt_entry(blocks[e0 + i] - 1, XPGB_PAGE_RESIDENT);
     if (o3.log) set_rec(o3, 0, XPGB_EV_LOAD_DONE, it, layer, kind, -1, -1);
-    launch_op(o3, s);
+    launch_op(o3, done_stream);
   }
-  CK(cudaEventRecord(c->ev_load[k][g & 3], s));
-  if (seq) CK(cudaStreamSynchronize(s));
+  CK(cudaEventRecord(c->ev_load[k][g & 3], done_stream));
+  if (seq) {
+    CK(cudaStreamSynchronize(s));
+    CK(cudaStreamSynchronize(done_stream));
+  }
 }
 
 // ---- session: the StreamedRunner schedule, one step at a time --------------------
@@ -829,6 +904,7 @@ static void session_end(Ctx* c, xpgb_report* rep) {
   rep->arena_peak_bytes = (int64_t)c->peak;
   rep->h2d_bytes = rs.h2d;
   rep->d2d_bytes = rs.d2d;
+  rep->decoded_bytes = rs.decoded;
   rep->n_records = (int32_t)c->last_log.size();
   long long fw = 0;
   CK(cudaMemcpy(&fw, c->d_fault, sizeof(fw), cudaMemcpyDeviceToHost));
@@ -932,22 +1008,75 @@ static void stage_device_tier(Ctx* c) {
     c->dev_tier = nullptr;
   }
   const size_t pages = (size_t)c->N * c->E;
-  uint64_t n = 0;
-  for (size_t pi = 0; pi < pages; ++pi)
-    for (int k = 0; k < 2; ++k) n += (c->backend[pi * 2 + k] ? (k ? c->s2 : c->s1) : 0);
+  auto tensor_bytes = [&](size_t ti) -> uint64_t {
+    const uint64_t raw = (ti & 1) ? c->s2 : c->s1;
+    if (!c->codec) return raw;
+    return xpgb_codec_record_bytes(raw / 2, c->rec_bits[ti], c->cchunk);
+  };
+  uint64_t total = 0;
+  for (size_t ti = 0; ti < pages * 2; ++ti)
+    if (c->backend[ti]) total += (tensor_bytes(ti) + 255) & ~255ull;
   std::fill(c->dev_off.begin(), c->dev_off.end(), -1);
-  if (n == 0) return;
-  if (!c->host) XFAIL(XPGB_ERR_BACKEND_MISS, "device-tier staging needs the host pool");
-  CK(cudaMalloc(&c->dev_tier, n));
+  if (total == 0) return;
+  if (!c->codec && !c->host) XFAIL(XPGB_ERR_BACKEND_MISS, "device-tier staging needs the host pool");
+  CK(cudaMalloc(&c->dev_tier, total));
   uint64_t at = 0;
-  for (size_t pi = 0; pi < pages; ++pi)
+  for (size_t ti = 0; ti < pages * 2; ++ti) {
+    if (!c->backend[ti]) continue;
+    const uint64_t sz = tensor_bytes(ti);
+    const uint8_t* src = c->codec ? c->cpool + c->rec_off[ti]
+                                  : c->host + (ti / 2) * (c->s1 + c->s2) + ((ti & 1) ? c->s1 : 0);
+    c->dev_off[ti] = (int64_t)at;
+    CK(cudaMemcpy(c->dev_tier + at, src, sz, cudaMemcpyHostToDevice));
+    at += (sz + 255) & ~255ull;
+  }
+}
+
+static void set_codec(Ctx* c, const void* pool, uint64_t pool_bytes, const uint64_t* rec_offsets,
+                      const uint64_t* bits_lens, const uint8_t* lengths, int chunk, bool host_compressed) {
+  if (chunk <= 0 || chunk % 8) XFAIL(XPGB_ERR_CONFIG, "codec chunk must be a positive multiple of 8");
+  uint32_t codes[kCodecSymbols];
+  if (!codec_canonical_codes(lengths, codes)) XFAIL(XPGB_ERR_CONFIG, "invalid code lengths");
+  const size_t nt = (size_t)c->N * c->E * 2;
+  CK(cudaDeviceSynchronize());
+  c->cpool = static_cast<const uint8_t*>(pool);
+  c->cpool_bytes = pool_bytes;
+  c->rec_off.assign(rec_offsets, rec_offsets + nt);
+  c->rec_bits.assign(bits_lens, bits_lens + nt);
+  memcpy(c->ctab.len, lengths, kCodecSymbols);
+  c->cchunk = chunk;
+  c->codec = true;
+  c->host_codec = host_compressed;
+  for (size_t ti = 0; ti < nt; ++ti) {
+    const uint64_t rb = xpgb_codec_record_bytes(((ti & 1) ? c->s2 : c->s1) / 2, c->rec_bits[ti], chunk);
+    if (c->rec_off[ti] + rb > pool_bytes) XFAIL(XPGB_ERR_CONTAINER_FORMAT, "record %zu outside the packed pool", ti);
+  }
+  if (!c->codec_events) {
     for (int k = 0; k < 2; ++k) {
-      if (!c->backend[pi * 2 + k]) continue;
-      const uint64_t sz = k ? c->s2 : c->s1;
-      c->dev_off[pi * 2 + k] = (int64_t)at;
-      CK(cudaMemcpy(c->dev_tier + at, c->host + pi * (c->s1 + c->s2) + (k ? c->s1 : 0), sz, cudaMemcpyHostToDevice));
-      at += sz;
+      CK(cudaStreamCreateWithFlags(&c->s_dec[k], cudaStreamNonBlocking));
+      for (int b = 0; b < 2; ++b) {
+        CK(cudaEventCreateWithFlags(&c->ev_copied[k][b], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_decoded[k][b], cudaEventDisableTiming));
+      }
+      CK(cudaEventCreateWithFlags(&c->ev_mapped[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_raw[k], cudaEventDisableTiming));
     }
+    c->codec_events = true;
+  }
+  // staging: two buffers per kind, each the largest record of that kind
+  for (int k = 0; k < 2; ++k) {
+    uint64_t cap = 0;
+    if (host_compressed)
+      for (size_t ti = k; ti < nt; ti += 2)
+        cap = std::max(cap, xpgb_codec_record_bytes(((ti & 1) ? c->s2 : c->s1) / 2, c->rec_bits[ti], chunk));
+    for (int b = 0; b < 2; ++b) {
+      if (c->stage[k][b]) cudaFree(c->stage[k][b]);
+      c->stage[k][b] = nullptr;
+      if (cap) CK(cudaMalloc(&c->stage[k][b], cap));
+    }
+    c->stage_cap[k] = cap;
+  }
+  stage_device_tier(c);
 }
 
 }  // namespace xpgb
@@ -1039,6 +1168,18 @@ int xpgb_destroy(xpgb_ctx* h) {
     for (int i = 0; i < 7; ++i) cudaEventDestroy(c->pev[i]);
     for (cudaEvent_t e : c->run_ev) cudaEventDestroy(e);
     delete c->sess;
+    if (c->codec_events) {
+      for (int k = 0; k < 2; ++k) {
+        cudaStreamDestroy(c->s_dec[k]);
+        for (int b = 0; b < 2; ++b) {
+          cudaEventDestroy(c->ev_copied[k][b]);
+          cudaEventDestroy(c->ev_decoded[k][b]);
+          if (c->stage[k][b]) cudaFree(c->stage[k][b]);
+        }
+        cudaEventDestroy(c->ev_mapped[k]);
+        cudaEventDestroy(c->ev_raw[k]);
+      }
+    }
     cudaStreamDestroy(c->s_comp);
     delete h;
   });
@@ -1250,6 +1391,144 @@ int xpgb_make_resident(xpgb_ctx* h) {
       for (size_t pi = 0; pi < pages; ++pi)
         tab[k * pages + pi] = c->st[k][pi] == XPGB_PAGE_UNMAPPED ? -1 : pt_entry(c->blk[k][pi] - 1, c->st[k][pi]);
     CK(cudaMemcpy(c->d_pt, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
+  });
+}
+
+uint64_t xpgb_codec_record_bytes(uint64_t n, uint64_t bits_len, int32_t chunk) {
+  const uint64_t ch = chunk > 0 ? (uint64_t)chunk : 1;
+  return ((n + 15) & ~15ull) + ((bits_len + 8 + 15) & ~15ull) + ((((n + ch - 1) / ch) * 4 + 15) & ~15ull);
+}
+
+int xpgb_codec_histogram(const void* data, uint64_t bytes, uint64_t* counts256, int32_t threads) {
+  return guard([&] {
+    if (bytes % 2) XFAIL(XPGB_ERR_ODD_LENGTH, "bf16 payload has odd length %llu", (unsigned long long)bytes);
+    codec_histogram(static_cast<const uint8_t*>(data), bytes, counts256, threads);
+  });
+}
+
+int xpgb_codec_encode(const void* data, uint64_t bytes, const uint8_t* lengths256, void* sm_out, void* bits_out,
+                      uint64_t bits_cap, uint64_t* bits_len, uint64_t* bit_count, uint32_t* index_out,
+                      int32_t chunk) {
+  return guard([&] {
+    if (bytes % 2) XFAIL(XPGB_ERR_ODD_LENGTH, "bf16 payload has odd length %llu", (unsigned long long)bytes);
+    uint32_t codes[kCodecSymbols];
+    if (!codec_canonical_codes(lengths256, codes)) XFAIL(XPGB_ERR_CONFIG, "invalid code lengths");
+    size_t bl = 0;
+    uint64_t bc = 0;
+    int missing = -1;
+    const bool ok = codec_encode(static_cast<const uint16_t*>(data), bytes / 2, lengths256, codes,
+                                 static_cast<uint8_t*>(sm_out), static_cast<uint8_t*>(bits_out), bits_cap, &bl, &bc,
+                                 index_out, chunk, &missing);
+    if (missing >= 0) XFAIL(XPGB_ERR_SYMBOL_NOT_IN_TABLE, "exponent bytes [%d] have no codeword; wrong table?", missing);
+    if (!ok) XFAIL(XPGB_ERR_OUT_OF_RANGE, "bitstream needs %llu bytes, buffer holds %llu", (unsigned long long)bl,
+                   (unsigned long long)bits_cap);
+    *bits_len = bl;
+    *bit_count = bc;
+  });
+}
+
+int xpgb_codec_pack(const void* payload, int32_t n_tensors, const uint64_t* value_counts, const uint8_t* lengths256,
+                    int32_t chunk, int32_t threads, void* out, uint64_t out_cap, uint64_t* pool_bytes,
+                    uint64_t* rec_offsets, uint64_t* bits_lens, uint64_t* bit_counts) {
+  return guard([&] {
+    if (chunk <= 0 || chunk % 8) XFAIL(XPGB_ERR_CONFIG, "codec chunk must be a positive multiple of 8");
+    uint32_t codes[kCodecSymbols];
+    if (!codec_canonical_codes(lengths256, codes)) XFAIL(XPGB_ERR_CONFIG, "invalid code lengths");
+    const uint16_t* words = static_cast<const uint16_t*>(payload);
+    std::vector<uint64_t> first(n_tensors + 1, 0);
+    for (int i = 0; i < n_tensors; ++i) first[i + 1] = first[i] + value_counts[i];
+    const int nthr = std::max(1, threads);
+    std::vector<int> bad(n_tensors, -1);
+    // pass 1: exact stream bits per tensor from per-tensor histograms -> record layout
+    {
+      std::vector<std::thread> pool_t;
+      std::atomic<int> next{0};
+      for (int t = 0; t < nthr; ++t)
+        pool_t.emplace_back([&] {
+          for (int i = next++; i < n_tensors; i = next++) {
+            uint64_t cnt[kCodecSymbols] = {0};
+            for (uint64_t v = first[i]; v < first[i + 1]; ++v) ++cnt[(words[v] >> 7) & 0xFF];
+            uint64_t bits = 0;
+            for (int sy = 0; sy < kCodecSymbols; ++sy) {
+              if (cnt[sy] && !lengths256[sy]) bad[i] = sy;
+              bits += cnt[sy] * lengths256[sy];
+            }
+            bit_counts[i] = bits;
+            bits_lens[i] = (bits + 7) / 8;
+          }
+        });
+      for (auto& th : pool_t) th.join();
+    }
+    for (int i = 0; i < n_tensors; ++i)
+      if (bad[i] >= 0)
+        XFAIL(XPGB_ERR_SYMBOL_NOT_IN_TABLE, "exponent bytes [%d] have no codeword; wrong table?", bad[i]);
+    uint64_t total = 0;
+    for (int i = 0; i < n_tensors; ++i) {
+      rec_offsets[i] = total;
+      total += xpgb_codec_record_bytes(value_counts[i], bits_lens[i], chunk);
+    }
+    *pool_bytes = total;
+    if (!out) return;  // layout only
+    if (out_cap < total) XFAIL(XPGB_ERR_OUT_OF_RANGE, "packed pool needs %llu bytes, buffer holds %llu",
+                               (unsigned long long)total, (unsigned long long)out_cap);
+    // pass 2: encode every tensor into its record
+    std::atomic<int> next{0};
+    std::atomic<int> fail{0};
+    std::vector<std::thread> pool_t;
+    for (int t = 0; t < nthr; ++t)
+      pool_t.emplace_back([&] {
+        for (int i = next++; i < n_tensors; i = next++) {
+          uint8_t* rec = static_cast<uint8_t*>(out) + rec_offsets[i];
+          const uint64_t n = value_counts[i];
+          const uint64_t sm16 = (n + 15) & ~15ull, bits16 = (bits_lens[i] + 8 + 15) & ~15ull;
+          const uint64_t rb = xpgb_codec_record_bytes(n, bits_lens[i], chunk);
+          memset(rec, 0, rb);
+          size_t bl = 0;
+          uint64_t bc = 0;
+          int missing = -1;
+          if (!codec_encode(words + first[i], n, lengths256, codes, rec, rec + sm16, bits_lens[i], &bl, &bc,
+                            reinterpret_cast<uint32_t*>(rec + sm16 + bits16), chunk, &missing) ||
+              bl != bits_lens[i] || bc != bit_counts[i])
+            fail = 1;
+        }
+      });
+    for (auto& th : pool_t) th.join();
+    if (fail) XFAIL(XPGB_ERR, "codec pack: stream size mismatch");
+  });
+}
+
+int xpgb_codec_index(const void* bits, uint64_t bits_len, uint64_t n, const uint8_t* lengths256, int32_t chunk,
+                     uint32_t* index_out) {
+  return guard([&] {
+    if (chunk <= 0 || chunk % 8) XFAIL(XPGB_ERR_CONFIG, "codec chunk must be a positive multiple of 8");
+    size_t used = 0;
+    const int r = codec_build_index(static_cast<const uint8_t*>(bits), bits_len, n, lengths256, chunk, index_out, &used);
+    if (r == 1) XFAIL(XPGB_ERR_TRUNCATED_STREAM, "bitstream ended before all %llu values", (unsigned long long)n);
+    if (r == 2) XFAIL(XPGB_ERR_INVALID_CODE, "no codeword matches a bit pattern in the stream");
+  });
+}
+
+int xpgb_codec_decode(const void* record_dev, uint64_t n, uint64_t bits_len, int32_t chunk, const uint8_t* lengths256,
+                      void* out_dev, void* stream) {
+  return guard([&] {
+    if (chunk <= 0 || chunk % 8) XFAIL(XPGB_ERR_CONFIG, "codec chunk must be a positive multiple of 8");
+    uint32_t codes[kCodecSymbols];
+    if (!codec_canonical_codes(lengths256, codes)) XFAIL(XPGB_ERR_CONFIG, "invalid code lengths");
+    CodecTable t;
+    memcpy(t.len, lengths256, kCodecSymbols);
+    const uint8_t* rec = static_cast<const uint8_t*>(record_dev);
+    const uint64_t sm16 = (n + 15) & ~15ull, bits16 = (bits_len + 8 + 15) & ~15ull;
+    launch_exp_decode(rec, reinterpret_cast<const uint32_t*>(rec + sm16),
+                      reinterpret_cast<const uint32_t*>(rec + sm16 + bits16), n, chunk, t,
+                      static_cast<uint16_t*>(out_dev), (cudaStream_t)stream);
+    CKLAUNCH();
+  });
+}
+
+int xpgb_set_codec(xpgb_ctx* h, const void* pool, uint64_t pool_bytes, const uint64_t* rec_offsets,
+                   const uint64_t* bits_lens, const uint8_t* lengths256, int32_t chunk, int32_t host_compressed) {
+  return guard([&] {
+    set_codec(&h->c, pool, pool_bytes, rec_offsets, bits_lens, lengths256, chunk, host_compressed != 0);
   });
 }
 

@@ -88,6 +88,17 @@ class Context:
         arr = np.ascontiguousarray(backend_of, dtype=np.uint8)
         call("xpgb_set_placement", self._h, arr.ctypes.data_as(C.POINTER(C.c_uint8)))
 
+    def set_codec(self, cm, host_compressed: bool) -> None:
+        """Attach a CompressedModel (exponent_codec) of this context's tensors."""
+        p64 = C.POINTER(C.c_uint64)
+        offs = np.ascontiguousarray(cm.rec_offsets, dtype=np.uint64)
+        bits = np.ascontiguousarray(cm.bits_lens, dtype=np.uint64)
+        lengths = cm.table.lengths_array()
+        call("xpgb_set_codec", self._h, C.c_void_p(cm.pool.data_ptr()), C.c_uint64(cm.pool.numel()),
+             offs.ctypes.data_as(p64), bits.ctypes.data_as(p64), lengths.ctypes.data_as(C.POINTER(C.c_uint8)),
+             int(cm.chunk), 1 if host_compressed else 0)
+        self._codec_ref = cm
+
     def set_expert_shard(self, first: int, count: int) -> None:
         call("xpgb_set_expert_shard", self._h, first, count)
         self.expert_first, self.expert_count = first, count

@@ -106,6 +106,7 @@ class RunReport:
     copy_busy_seconds: tuple = (0.0, 0.0)
     elapsed_seconds: float = 0.0
     kernels: dict = field(default_factory=dict)
+    decoded_bytes: int = 0
 
     @property
     def checksum(self) -> str:
@@ -198,7 +199,8 @@ class StreamedRunner:
     """Paged pipeline for n iterations over N layers on one B200."""
 
     def __init__(self, spec: ModelSpec, hierarchy: StorageHierarchy, fwd: ForwardSpec, mode: str = "threaded",
-                 compute_delay_fn=None, sabotage_skip_raw=None, trace=None, device: int = 0):
+                 compute_delay_fn=None, sabotage_skip_raw=None, trace=None, device: int = 0,
+                 host_codec: bool = False):
         if mode not in ("threaded", "sequential"):
             raise XpgError(f"unknown mode {mode!r}")
         self.spec = spec
@@ -209,7 +211,14 @@ class StreamedRunner:
         self.sabotage_skip_raw = sabotage_skip_raw
         self.ctx = Context(spec, _lib.POOL_RING, device, max_tokens=fwd.tokens_per_step)
         self.ctx.attach_host_pool(hierarchy.container.pinned)
-        self.ctx.set_placement(hierarchy.backend_map())
+        placement = hierarchy.backend_map()
+        cm = _codec_model(hierarchy, host_codec or bool(placement.any()))
+        if cm is not None:
+            # compressed tiers (codec.py): device-tier tensors live compressed in HBM; with
+            # host_codec the host tier also ships compressed records over PCIe.  Both are
+            # decoded on the GPU straight into the ring block.
+            self.ctx.set_codec(cm, host_compressed=host_codec)
+        self.ctx.set_placement(placement)
         self.table = PageTable(spec, trace=trace, context=self.ctx)
         self.stall_seconds = 0.0
         self.war_wait_seconds = 0.0
@@ -244,6 +253,7 @@ class StreamedRunner:
             copy_busy_seconds=(rep.copy_busy_ns[0] * 1e-9, rep.copy_busy_ns[1] * 1e-9),
             elapsed_seconds=rep.elapsed_ns * 1e-9,
             kernels=_kernel_stats(rep),
+            decoded_bytes=int(rep.decoded_bytes),
         )
 
 
@@ -253,6 +263,19 @@ def _kernel_stats(rep) -> dict:
         "gate_up_bytes": int(rep.gate_up_bytes), "down_bytes": int(rep.down_bytes),
         "down_splits": int(rep.down_splits), "active_experts": int(rep.active_experts),
     }
+
+
+def _codec_model(hierarchy: StorageHierarchy, needed: bool):
+    """The hierarchy's CompressedModel (built on demand) when a compressed tier is in use."""
+    if not needed:
+        return None
+    from .exponent_codec import CompressedModel
+
+    cm = hierarchy.compressed
+    if not isinstance(cm, CompressedModel):
+        cm = CompressedModel.from_container(hierarchy.container)
+        hierarchy.compressed = cm
+    return cm
 
 
 def run_iterations(iterations: int, spec: ModelSpec, hierarchy: StorageHierarchy, fwd: ForwardSpec,

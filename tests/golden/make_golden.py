@@ -160,6 +160,38 @@ def main():
             "tau_load": est.tau_load,
         }
 
+    # 8. exponent codec (codec.py): tables, per-tensor streams, XPGC bytes
+    from xpg import codec as X
+
+    for (N, L, H, F, seed) in [(2, 2, 16, 32, 6), (3, 2, 32, 64, 4), (4, 8, 256, 512, 7)]:
+        spec = M.ModelSpec(N, L, H, F)
+        container = M.generate_synthetic_model(spec, seed)
+        cm = X.CompressedModel.from_container(container)
+        key = f"xpgc_{N}_{L}_{H}_{F}_{seed}"
+        arrays[key + "_lengths"] = np.array(cm.table.code_lengths, dtype=np.uint8)
+        arrays[key + "_bits"] = np.array([len(cm.tensors[t].exponent_bitstream) for t in M.iter_tensor_ids(spec)],
+                                         dtype=np.int64)
+        arrays[key + "_bitcount"] = np.array([cm.tensors[t].exponent_bit_count for t in M.iter_tensor_ids(spec)],
+                                             dtype=np.int64)
+        meta["cases"][key] = {"sha256": hashlib.sha256(cm.to_bytes()).hexdigest(), "ratio": cm.ratio}
+    adv = np.arange(65536, dtype=np.uint16).astype("<u2").tobytes()
+    t_adv = X.build_table(X.build_histogram(adv))
+    ct_adv = X.compress(adv, t_adv)
+    arrays["codec_adv_lengths"] = np.array(t_adv.code_lengths, dtype=np.uint8)
+    meta["cases"]["codec_adv"] = {"stream_sha256": hashlib.sha256(ct_adv.exponent_bitstream).hexdigest(),
+                                  "bit_count": ct_adv.exponent_bit_count}
+    rnd = np.random.default_rng(9).integers(0, 65536, 200_000, dtype=np.uint16).astype("<u2").tobytes()
+    t_rnd = X.build_table(X.build_histogram(rnd))
+    ct_rnd = X.compress(rnd, t_rnd)
+    arrays["codec_rnd_lengths"] = np.array(t_rnd.code_lengths, dtype=np.uint8)
+    meta["cases"]["codec_rnd"] = {"stream_sha256": hashlib.sha256(ct_rnd.exponent_bitstream).hexdigest(),
+                                  "bit_count": ct_rnd.exponent_bit_count}
+    skew = np.zeros(256, dtype=np.int64)
+    skew[:40] = [2 ** min(i, 40) for i in range(40)]  # forces the 32-bit length cap
+    arrays["codec_skew_counts"] = skew
+    arrays["codec_skew_lengths"] = np.array(X.build_table(X.ExponentHistogram(tuple(int(v) for v in skew))).code_lengths,
+                                            dtype=np.uint8)
+
     np.savez_compressed(os.path.join(HERE, "golden_v1.npz"), **arrays)
     with open(os.path.join(HERE, "golden_v1.json"), "w") as fh:
         json.dump(meta, fh, indent=1, sort_keys=True)

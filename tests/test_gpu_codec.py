@@ -1,0 +1,100 @@
+"""GPU exponent decoder (k_exp_decode): bit-exact with the reference codec; compressed tiers."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def XC():
+    from paper_2604_02715_b200 import exponent_codec as XC
+
+    return XC
+
+
+@pytest.fixture(scope="module")
+def X():
+    import paper_2604_02715_b200 as X
+
+    return X
+
+
+def test_roundtrip_adversarial_patterns(XC):
+    data = np.arange(65536, dtype=np.uint16).astype("<u2").tobytes()  # NaN, Inf, subnormals, every exponent
+    t = XC.build_table(XC.build_histogram(data))
+    for chunk in (8, 64, 1024):
+        assert XC.decompress(XC.compress(data, t, chunk=chunk), t) == data
+
+
+@pytest.mark.parametrize("n", [1, 7, 8, 9, 1023, 1024, 1025, 200_000])
+def test_roundtrip_random_and_gaussian(XC, X, n):
+    rng = np.random.default_rng(n)
+    for data in (rng.integers(0, 65536, n, dtype=np.uint16).astype("<u2").tobytes(),
+                 X.float32_to_bf16(rng.standard_normal(n).astype(np.float32) * 0.02).astype("<u2").tobytes()):
+        t = XC.build_table(XC.build_histogram(data))
+        assert XC.decompress(XC.compress(data, t), t) == data
+
+
+def test_roundtrip_long_codes(XC):
+    # a skewed histogram forces codes up to the 32-bit cap (LUT misses take the slow path)
+    counts = [0] * 256
+    for i in range(40):
+        counts[i] = 2 ** min(i, 40)
+    t = XC.build_table(XC.ExponentHistogram(tuple(counts)))
+    rng = np.random.default_rng(3)
+    exps = rng.integers(0, 40, 100_000)
+    words = ((exps.astype(np.uint16) << 7) | rng.integers(0, 128, exps.size).astype(np.uint16)).astype("<u2")
+    data = words.tobytes()
+    assert XC.decompress(XC.compress(data, t, chunk=64), t) == data
+
+
+def test_compressed_model_tensor_bytes_and_xpgc_roundtrip(XC, X, tmp_path):
+    spec = X.ModelSpec(3, 2, 32, 64)
+    c = X.generate_synthetic_model(spec, 4)
+    cm = XC.CompressedModel.from_container(c)
+    for tid in X.iter_tensor_ids(spec):
+        assert cm.tensor_bytes(tid) == c.tensor_bytes(tid)
+    path = tmp_path / "m.xpgc"
+    cm.write(path)
+    loaded = XC.CompressedModel.read(path)  # no chunk index in XPGC: rebuilt on the host
+    for tid in X.iter_tensor_ids(spec):
+        assert loaded.tensor_bytes(tid) == c.tensor_bytes(tid)
+    assert loaded.to_bytes() == cm.to_bytes()
+
+
+def _runner(X, spec, seed, alpha, host_codec):
+    container = X.generate_synthetic_model(spec, seed)
+    if alpha is None:
+        backends = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 30e9, 1 << 40)]
+    else:
+        backends = [X.Backend(1, X.BackendKind.COMPRESSED_DEVICE, 300e9, 1 << 40),
+                    X.Backend(2, X.BackendKind.HOST_OFFLOAD, 30e9, 1 << 40)]
+    hier = X.StorageHierarchy(container, None, X.plan_placement(spec, backends, alpha=alpha), backends)
+    return container, hier
+
+
+@pytest.mark.parametrize("alpha,host_codec", [(None, True), (0.25, False), (0.5, True), (1.0, False)])
+def test_compressed_tiers_streamed_equals_resident(X, alpha, host_codec):
+    spec = X.ModelSpec(4, 8, 256, 512)
+    fwd = X.ForwardSpec(16, 2, 7)
+    container, hier = _runner(X, spec, 7, alpha, host_codec)
+    x = X.initial_activations(spec, fwd, 7)
+    runner = X.StreamedRunner(spec, hier, fwd, host_codec=host_codec)
+    rep = runner.run(2, acts=x.copy())
+    base = X.resident_baseline(2, spec, container, fwd, acts=x.copy())
+    assert rep.page_fault is None and rep.violations == []
+    assert rep.final_activations.tobytes() == base.tobytes()
+    if host_codec:
+        assert rep.decoded_bytes > 0
+        assert rep.h2d_bytes < 0.8 * (2 * spec.total_bytes)  # compressed records cross the link
+
+
+def test_host_codec_sabotage_still_faults(X):
+    spec = X.ModelSpec(4, 2, 64, 128)
+    _, hier = _runner(X, spec, 2, None, True)
+    hier.delay_fn = lambda tid: 0.03 if tid.layer == 3 else 0.0
+    runner = X.StreamedRunner(spec, hier, X.ForwardSpec(3, 2, 5), host_codec=True, sabotage_skip_raw=(1, 3))
+    rep = runner.run(2)
+    assert rep.page_fault is not None
+    assert any(v.startswith("RAW") for v in rep.violations)
