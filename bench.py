@@ -221,6 +221,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-resident", action="store_true")
     ap.add_argument("--ep", action="store_true", help="use the expert-parallel runner even at N=1")
+    ap.add_argument("--host-codec", action="store_true",
+                    help="ship exponent-Huffman compressed records over PCIe, decode on the GPU (lossless)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.tokens:
@@ -261,7 +263,14 @@ def main():
     else:
         backends = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 55e9, 1 << 50)]
         hier = X.StorageHierarchy(container, None, X.plan_placement(spec, backends), backends)
-        runner = X.StreamedRunner(spec, hier, fwd, mode="threaded", device=dev)
+        if args.host_codec:
+            from paper_2604_02715_b200.exponent_codec import CompressedModel
+
+            t1 = time.time()
+            hier.compressed = CompressedModel.from_container(container)
+            log(f"packed compressed host pool: ratio {hier.compressed.ratio:.4f} "
+                f"({hier.compressed.wire_bytes / 1e9:.2f} GB) in {time.time() - t1:.1f}s")
+        runner = X.StreamedRunner(spec, hier, fwd, mode="threaded", device=dev, host_codec=args.host_codec)
         budget = runner.table.pool_bytes / spec.total_bytes
     x_host = X.initial_activations(spec, fwd, SEED + rank)
     x_dev = torch.from_numpy(x_host).to(f"cuda:{dev}")
@@ -345,7 +354,11 @@ def main():
                    "expert_hbm_budget": round(budget, 4), "placement": "2-layer ring, host-only (alpha=0)",
                    "l2": "inputs larger than L2: all %.1f GB of expert weights stream from host each step" % (spec.total_bytes / 1e9)},
         "page_in": {"achieved_gbps": page_in_gbps, "peak_gbps": h2d_peak, "frac": page_in_gbps / h2d_peak if h2d_peak else None,
-                    "bytes_per_step": rep.h2d_bytes / args.steps, "peak_how": "pinned 1 GiB cudaMemcpyAsync H2D, best of 5, this box"},
+                    "bytes_per_step": rep.h2d_bytes / args.steps, "peak_how": "pinned 1 GiB cudaMemcpyAsync H2D, best of 5, this box",
+                    "host_codec": bool(args.host_codec),
+                    "raw_bytes_per_step": spec.total_bytes if not use_ep else None,
+                    "decoded_bytes_per_step": rep.decoded_bytes / args.steps,
+                    "effective_raw_gbps": (spec.total_bytes * args.steps / rep.elapsed_seconds / 1e9) if not use_ep else None},
         "exposed_xfer_pct": 100.0 * exposed,
         "war_wait_ms": rep.war_wait_seconds * 1e3,
         "roofline": {"bound": "hbm", "kernel": "k_gate_up (tcgen05 grouped SwiGLU GEMM, resident run)",

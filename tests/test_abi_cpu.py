@@ -22,7 +22,7 @@ def libpath():
 def header_functions():
     text = open(HEADER).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(xpgb_\w+)\s*\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|uint64_t|const char\*)\s+(xpgb_\w+)\s*\(", text, flags=re.M)))
 
 
 def test_header_and_binding_agree():
