@@ -221,9 +221,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-resident", action="store_true")
     ap.add_argument("--ep", action="store_true", help="use the expert-parallel runner even at N=1")
-    ap.add_argument("--host-codec", action="store_true",
-                    help="ship exponent-Huffman compressed records over PCIe, decode on the GPU (lossless)")
+    ap.add_argument("--raw", action="store_true",
+                    help="page raw bf16 over PCIe (the reference host tier) instead of exponent-Huffman records")
     args = ap.parse_args()
+    args.host_codec = not args.raw
     cfg = dict(CONFIGS[args.config])
     if args.tokens:
         cfg["T"] = args.tokens
@@ -263,6 +264,24 @@ def main():
     else:
         backends = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 55e9, 1 << 50)]
         hier = X.StorageHierarchy(container, None, X.plan_placement(spec, backends), backends)
+        raw_path = None
+        if args.host_codec:
+            # the reference host tier (raw bf16 over PCIe) on the same weights, for comparison
+            raw_runner = X.StreamedRunner(spec, hier, fwd, mode="threaded", device=dev)
+            xr = torch.from_numpy(X.initial_activations(spec, fwd, SEED + rank)).to(f"cuda:{dev}")
+            raw_runner.run(max(1, args.warmup - 1), acts=xr)
+            torch.cuda.synchronize()
+            q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            q0.record()
+            rrep_raw = raw_runner.run(args.steps, acts=xr)
+            q1.record()
+            torch.cuda.synchronize()
+            raw_s = q0.elapsed_time(q1) * 1e-3
+            raw_path = {"tok_s": T * args.steps / raw_s, "ms_per_step": 1e3 * raw_s / args.steps,
+                        "page_in_gbps": rrep_raw.h2d_bytes / rrep_raw.elapsed_seconds / 1e9,
+                        "exposed_xfer_pct": 100.0 * rrep_raw.stall_seconds / rrep_raw.elapsed_seconds}
+            del raw_runner
+            log(f"raw host tier: {raw_path['tok_s']:.1f} tok/s")
         if args.host_codec:
             from paper_2604_02715_b200.exponent_codec import CompressedModel
 
@@ -271,7 +290,8 @@ def main():
             log(f"packed compressed host pool: ratio {hier.compressed.ratio:.4f} "
                 f"({hier.compressed.wire_bytes / 1e9:.2f} GB) in {time.time() - t1:.1f}s")
         runner = X.StreamedRunner(spec, hier, fwd, mode="threaded", device=dev, host_codec=args.host_codec)
-        budget = runner.table.pool_bytes / spec.total_bytes
+        hbm = runner.ctx.hbm_bytes()
+        budget = (hbm["ring"] + hbm["staging"] + hbm["device_tier"]) / spec.total_bytes
     x_host = X.initial_activations(spec, fwd, SEED + rank)
     x_dev = torch.from_numpy(x_host).to(f"cuda:{dev}")
 
@@ -351,7 +371,10 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init N(0,0.02) bf16 weights drawn on-GPU, N(0,1) activations)",
         "config": {"workload": cfg["name"], "tokens_per_step": T, "top_k": k, "layers": N,
-                   "expert_hbm_budget": round(budget, 4), "placement": "2-layer ring, host-only (alpha=0)",
+                   "expert_hbm_budget": round(budget, 4),
+                   "placement": "2-layer ring, host-only (alpha=0)" + (
+                       ", exponent-Huffman records over PCIe decoded on-GPU into the ring (lossless)"
+                       if args.host_codec else ""),
                    "l2": "inputs larger than L2: all %.1f GB of expert weights stream from host each step" % (spec.total_bytes / 1e9)},
         "page_in": {"achieved_gbps": page_in_gbps, "peak_gbps": h2d_peak, "frac": page_in_gbps / h2d_peak if h2d_peak else None,
                     "bytes_per_step": rep.h2d_bytes / args.steps, "peak_how": "pinned 1 GiB cudaMemcpyAsync H2D, best of 5, this box",
@@ -378,6 +401,8 @@ def main():
     }
     if not args.no_resident and not use_ep:
         line["paged_kernels"] = paged_kern
+    if not use_ep and raw_path is not None:
+        line["raw_host_tier"] = raw_path
     if use_ep:
         line["config"]["parallelism"] = f"ep{world} (experts sharded, NCCL all_to_all dispatch/combine)"
         line["config"]["tokens_per_rank"] = T

@@ -210,6 +210,9 @@ int xpgb_codec_decode(const void* record_dev, uint64_t n, uint64_t bits_len, int
 int xpgb_set_codec(xpgb_ctx* ctx, const void* pool, uint64_t pool_bytes, const uint64_t* rec_offsets,
                    const uint64_t* bits_lens, const uint8_t* lengths256, int32_t chunk, int32_t host_compressed);
 
+/* Expert-weight HBM footprint of a context: ring/pool blocks, codec staging, device tier. */
+int xpgb_hbm_bytes(xpgb_ctx* ctx, uint64_t* ring, uint64_t* staging, uint64_t* device_tier);
+
 /* ---------------------------------------------------------------- compute */
 /* routed_experts (pipeline.py:154-170) for layers [layer_first, layer_first+layer_count):
  * out_dev int32 [layer_count][T][min(top_k, L)], ascending 1-based ids. Stateless. */

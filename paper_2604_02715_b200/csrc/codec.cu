@@ -143,6 +143,7 @@ struct DecodeParams {
   const uint32_t* index;
   uint64_t n;
   int chunk;
+  uint32_t bit_base;  // subtracted from index[] (a piece of a stream staged on its own)
   uint16_t* out;
   CodecTable t;
 };
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(256) k_exp_decode(DecodeParams p) {
   for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + tid; c < n_chunks; c += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t v0 = c * p.chunk;
     const uint64_t v1 = (v0 + p.chunk < n) ? v0 + p.chunk : n;
-    const uint32_t bitpos = p.index[c];
+    const uint32_t bitpos = p.index[c] - p.bit_base;
     const uint32_t w = bitpos >> 5, sh = bitpos & 31;
     uint64_t win = (((uint64_t)bswap32(p.bits[w]) << 32) | bswap32(p.bits[w + 1])) << sh;
     int avail = 64 - (int)sh;
@@ -249,9 +250,9 @@ __global__ void __launch_bounds__(256) k_exp_decode(DecodeParams p) {
 }
 
 void launch_exp_decode(const uint8_t* sm, const uint32_t* bits, const uint32_t* index, uint64_t n, int chunk,
-                       const CodecTable& table, uint16_t* out, cudaStream_t s) {
+                       const CodecTable& table, uint16_t* out, cudaStream_t s, uint32_t bit_base) {
   if (n == 0) return;
-  DecodeParams p{sm, bits, index, n, chunk, out, table};
+  DecodeParams p{sm, bits, index, n, chunk, bit_base, out, table};
   const uint64_t n_chunks = (n + chunk - 1) / chunk;
   const uint64_t blocks = std::min<uint64_t>((n_chunks + 255) / 256, 148 * 8);
   k_exp_decode<<<(unsigned)blocks, 256, 0, s>>>(p);

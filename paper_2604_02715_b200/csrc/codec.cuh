@@ -45,7 +45,9 @@ int codec_build_index(const uint8_t* bits, size_t bits_len, size_t n, const uint
 size_t codec_bits_bound(size_t n, const uint8_t* lengths);
 
 // GPU decode: bits must be readable as 32-bit words up to round_up(bits_len, 4) + 8 bytes.
+// bit_base is subtracted from every index entry (decoding one staged piece of a stream).
 void launch_exp_decode(const uint8_t* sm, const uint32_t* bits, const uint32_t* index, uint64_t n, int chunk,
-                       const CodecTable& table, uint16_t* out, cudaStream_t s);
+                       const CodecTable& table, uint16_t* out, cudaStream_t s, uint32_t bit_base = 0);
+constexpr uint64_t kStagePieceBytes = 32ull << 20;  // max bytes of one staged record piece
 
 }  // namespace xpgb

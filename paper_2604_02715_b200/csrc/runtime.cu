@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <set>
@@ -659,22 +660,49 @@ static void materialize(RunState& rs, int g, int it, int layer, int kind) {
         CKLAUNCH();
         rs.decoded += 2 * n;
       } else if (c->host_codec) {
-        const int buf = hb++ & 1;
+        // stream the record in pieces of whole chunks (<= kStagePieceBytes) so the staging
+        // buffers stay small: sm slice | stream slice (+8 B lookahead) | index slice
         const uint64_t nb = c->rec_bits[ti];
-        const uint64_t rb = xpgb_codec_record_bytes(n, nb, c->cchunk);
-        CK(cudaStreamWaitEvent(s, c->ev_decoded[k][buf], 0));
-        if (dl > 0) sleep_on(s, dl);
-        CK(cudaMemcpyAsync(c->stage[k][buf], c->cpool + c->rec_off[ti], rb, cudaMemcpyHostToDevice, s));
-        CK(cudaEventRecord(c->ev_copied[k][buf], s));
-        rs.h2d += rb;
-        CK(cudaStreamWaitEvent(d, c->ev_copied[k][buf], 0));
-        const uint8_t* rec = c->stage[k][buf];
+        const uint64_t ch = (uint64_t)c->cchunk;
+        const uint64_t nc = (n + ch - 1) / ch;
         const uint64_t sm16 = (n + 15) & ~15ull, bits16 = (nb + 8 + 15) & ~15ull;
-        launch_exp_decode(rec, reinterpret_cast<const uint32_t*>(rec + sm16),
-                          reinterpret_cast<const uint32_t*>(rec + sm16 + bits16), n, c->cchunk, c->ctab,
-                          reinterpret_cast<uint16_t*>(dst), d);
-        CKLAUNCH();
-        CK(cudaEventRecord(c->ev_decoded[k][buf], d));
+        const uint8_t* rec = c->cpool + c->rec_off[ti];
+        const uint32_t* idx = reinterpret_cast<const uint32_t*>(rec + sm16 + bits16);
+        auto piece_bytes = [&](uint64_t a, uint64_t b) -> uint64_t {  // staged size of chunks [a, b)
+          const uint64_t va = a * ch, vb = std::min(n, b * ch);
+          const uint64_t ba = ((uint64_t)idx[a] >> 5) * 4, bb = (b < nc) ? (((uint64_t)idx[b] + 7) / 8) : nb;
+          return ((vb - va + 15) & ~15ull) + ((bb - ba + 8 + 15) & ~15ull) + (b - a) * 4;
+        };
+        if (dl > 0) sleep_on(s, dl);
+        for (uint64_t c0 = 0, c1 = 0; c0 < nc; c0 = c1) {
+          // largest c1 whose piece fits the staging buffer (sizes grow with c1)
+          uint64_t lo = c0 + 1, hi = nc;
+          while (lo < hi) {
+            const uint64_t mid = (lo + hi + 1) / 2;
+            if (piece_bytes(c0, mid) <= c->stage_cap[k]) lo = mid; else hi = mid - 1;
+          }
+          c1 = lo;
+          const uint64_t v0 = c0 * ch, v1 = std::min(n, c1 * ch);
+          const uint64_t b0 = ((uint64_t)idx[c0] >> 5) * 4;
+          const uint64_t b1 = (c1 < nc) ? (((uint64_t)idx[c1] + 7) / 8) : nb;
+          const uint64_t ns = v1 - v0, nbits = b1 - b0 + 8;
+          const uint64_t o_bits = (ns + 15) & ~15ull, o_idx = o_bits + ((nbits + 15) & ~15ull);
+          if (o_idx + (c1 - c0) * 4 > c->stage_cap[k]) XFAIL(XPGB_ERR, "codec piece exceeds staging buffer");
+          const int buf = hb++ & 1;
+          uint8_t* st = c->stage[k][buf];
+          CK(cudaStreamWaitEvent(s, c->ev_decoded[k][buf], 0));
+          CK(cudaMemcpyAsync(st, rec + v0, ns, cudaMemcpyHostToDevice, s));
+          CK(cudaMemcpyAsync(st + o_bits, rec + sm16 + b0, nbits, cudaMemcpyHostToDevice, s));
+          CK(cudaMemcpyAsync(st + o_idx, idx + c0, (c1 - c0) * 4, cudaMemcpyHostToDevice, s));
+          CK(cudaEventRecord(c->ev_copied[k][buf], s));
+          rs.h2d += ns + nbits + (c1 - c0) * 4;
+          CK(cudaStreamWaitEvent(d, c->ev_copied[k][buf], 0));
+          launch_exp_decode(st, reinterpret_cast<const uint32_t*>(st + o_bits),
+                            reinterpret_cast<const uint32_t*>(st + o_idx), ns, c->cchunk, c->ctab,
+                            reinterpret_cast<uint16_t*>(dst) + v0, d, (uint32_t)(b0 * 8));
+          CKLAUNCH();
+          CK(cudaEventRecord(c->ev_decoded[k][buf], d));
+        }
         rs.decoded += 2 * n;
       } else {
         if (dl > 0) sleep_on(s, dl);
@@ -1063,12 +1091,16 @@ static void set_codec(Ctx* c, const void* pool, uint64_t pool_bytes, const uint6
     }
     c->codec_events = true;
   }
-  // staging: two buffers per kind, each the largest record of that kind
+  // staging: two buffers per kind, each min(largest record, kStagePieceBytes) + alignment slack
   for (int k = 0; k < 2; ++k) {
     uint64_t cap = 0;
-    if (host_compressed)
+    if (host_compressed) {
       for (size_t ti = k; ti < nt; ti += 2)
         cap = std::max(cap, xpgb_codec_record_bytes(((ti & 1) ? c->s2 : c->s1) / 2, c->rec_bits[ti], chunk));
+      uint64_t piece = kStagePieceBytes;
+      if (const char* env = getenv("XPGB_STAGE_BYTES")) piece = std::max<uint64_t>(4096, strtoull(env, nullptr, 10));
+      cap = std::min(cap, piece) + 64 + (uint64_t)chunk * 8;
+    }
     for (int b = 0; b < 2; ++b) {
       if (c->stage[k][b]) cudaFree(c->stage[k][b]);
       c->stage[k][b] = nullptr;
@@ -1529,6 +1561,22 @@ int xpgb_set_codec(xpgb_ctx* h, const void* pool, uint64_t pool_bytes, const uin
                    const uint64_t* bits_lens, const uint8_t* lengths256, int32_t chunk, int32_t host_compressed) {
   return guard([&] {
     set_codec(&h->c, pool, pool_bytes, rec_offsets, bits_lens, lengths256, chunk, host_compressed != 0);
+  });
+}
+
+int xpgb_hbm_bytes(xpgb_ctx* h, uint64_t* ring, uint64_t* staging, uint64_t* device_tier) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    *ring = (uint64_t)c->blocks * (c->s1 + c->s2);
+    *staging = 2 * (c->stage_cap[0] + c->stage_cap[1]);
+    uint64_t dt = 0;
+    const size_t nt = (size_t)c->N * c->E * 2;
+    for (size_t ti = 0; ti < nt && c->dev_tier; ++ti)
+      if (c->backend[ti]) {
+        const uint64_t raw = (ti & 1) ? c->s2 : c->s1;
+        dt += c->codec ? xpgb_codec_record_bytes(raw / 2, c->rec_bits[ti], c->cchunk) : raw;
+      }
+    *device_tier = dt;
   });
 }
 

@@ -103,6 +103,11 @@ class Context:
         call("xpgb_set_expert_shard", self._h, first, count)
         self.expert_first, self.expert_count = first, count
 
+    def hbm_bytes(self) -> dict:
+        r, st, dt = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        call("xpgb_hbm_bytes", self._h, C.byref(r), C.byref(st), C.byref(dt))
+        return {"ring": int(r.value), "staging": int(st.value), "device_tier": int(dt.value)}
+
     def make_resident(self) -> None:
         call("xpgb_make_resident", self._h)
 

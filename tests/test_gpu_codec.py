@@ -98,3 +98,16 @@ def test_host_codec_sabotage_still_faults(X):
     rep = runner.run(2)
     assert rep.page_fault is not None
     assert any(v.startswith("RAW") for v in rep.violations)
+
+
+def test_host_codec_small_staging_pieces(X, monkeypatch):
+    """Records streamed through a 16 KiB staging buffer (many pieces per tensor) stay exact."""
+    monkeypatch.setenv("XPGB_STAGE_BYTES", "16384")
+    spec = X.ModelSpec(4, 4, 128, 256)
+    fwd = X.ForwardSpec(8, 2, 3)
+    container, hier = _runner(X, spec, 3, None, True)
+    x = X.initial_activations(spec, fwd, 3)
+    rep = X.StreamedRunner(spec, hier, fwd, host_codec=True).run(2, acts=x.copy())
+    base = X.resident_baseline(2, spec, container, fwd, acts=x.copy())
+    assert rep.violations == [] and rep.page_fault is None
+    assert rep.final_activations.tobytes() == base.tobytes()
