@@ -234,6 +234,8 @@ struct Ctx {
   CodecTable ctab{};
   int cchunk = 1024;
   uint8_t* stage[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [kind][buffer]
+  uint32_t* d_index = nullptr;           // chunk indexes of host-tier records, device-resident
+  std::vector<uint64_t> d_index_off;     // [N*E*2] offset (entries) into d_index
   uint64_t stage_cap[2] = {0, 0};
   cudaStream_t s_dec[2] = {nullptr, nullptr};
   cudaEvent_t ev_copied[2][2], ev_decoded[2][2], ev_mapped[2], ev_raw[2];
@@ -671,7 +673,7 @@ static void materialize(RunState& rs, int g, int it, int layer, int kind) {
         auto piece_bytes = [&](uint64_t a, uint64_t b) -> uint64_t {  // staged size of chunks [a, b)
           const uint64_t va = a * ch, vb = std::min(n, b * ch);
           const uint64_t ba = ((uint64_t)idx[a] >> 5) * 4, bb = (b < nc) ? (((uint64_t)idx[b] + 7) / 8) : nb;
-          return ((vb - va + 15) & ~15ull) + ((bb - ba + 8 + 15) & ~15ull) + (b - a) * 4;
+          return ((vb - va + 15) & ~15ull) + ((bb - ba + 8 + 15) & ~15ull);
         };
         if (dl > 0) sleep_on(s, dl);
         for (uint64_t c0 = 0, c1 = 0; c0 < nc; c0 = c1) {
@@ -686,20 +688,18 @@ static void materialize(RunState& rs, int g, int it, int layer, int kind) {
           const uint64_t b0 = ((uint64_t)idx[c0] >> 5) * 4;
           const uint64_t b1 = (c1 < nc) ? (((uint64_t)idx[c1] + 7) / 8) : nb;
           const uint64_t ns = v1 - v0, nbits = b1 - b0 + 8;
-          const uint64_t o_bits = (ns + 15) & ~15ull, o_idx = o_bits + ((nbits + 15) & ~15ull);
-          if (o_idx + (c1 - c0) * 4 > c->stage_cap[k]) XFAIL(XPGB_ERR, "codec piece exceeds staging buffer");
+          const uint64_t o_bits = (ns + 15) & ~15ull;
+          if (o_bits + nbits > c->stage_cap[k]) XFAIL(XPGB_ERR, "codec piece exceeds staging buffer");
           const int buf = hb++ & 1;
           uint8_t* st = c->stage[k][buf];
           CK(cudaStreamWaitEvent(s, c->ev_decoded[k][buf], 0));
           CK(cudaMemcpyAsync(st, rec + v0, ns, cudaMemcpyHostToDevice, s));
           CK(cudaMemcpyAsync(st + o_bits, rec + sm16 + b0, nbits, cudaMemcpyHostToDevice, s));
-          CK(cudaMemcpyAsync(st + o_idx, idx + c0, (c1 - c0) * 4, cudaMemcpyHostToDevice, s));
           CK(cudaEventRecord(c->ev_copied[k][buf], s));
-          rs.h2d += ns + nbits + (c1 - c0) * 4;
+          rs.h2d += ns + nbits;
           CK(cudaStreamWaitEvent(d, c->ev_copied[k][buf], 0));
-          launch_exp_decode(st, reinterpret_cast<const uint32_t*>(st + o_bits),
-                            reinterpret_cast<const uint32_t*>(st + o_idx), ns, c->cchunk, c->ctab,
-                            reinterpret_cast<uint16_t*>(dst) + v0, d, (uint32_t)(b0 * 8));
+          launch_exp_decode(st, reinterpret_cast<const uint32_t*>(st + o_bits), c->d_index + c->d_index_off[ti] + c0,
+                            ns, c->cchunk, c->ctab, reinterpret_cast<uint16_t*>(dst) + v0, d, (uint32_t)(b0 * 8));
           CKLAUNCH();
           CK(cudaEventRecord(c->ev_decoded[k][buf], d));
         }
@@ -1108,6 +1108,24 @@ static void set_codec(Ctx* c, const void* pool, uint64_t pool_bytes, const uint6
     }
     c->stage_cap[k] = cap;
   }
+  if (c->d_index) cudaFree(c->d_index);
+  c->d_index = nullptr;
+  c->d_index_off.assign(nt, 0);
+  if (host_compressed) {
+    uint64_t total = 0;
+    for (size_t ti = 0; ti < nt; ++ti) {
+      c->d_index_off[ti] = total;
+      const uint64_t n = ((ti & 1) ? c->s2 : c->s1) / 2;
+      total += (n + chunk - 1) / chunk;
+    }
+    CK(cudaMalloc(&c->d_index, std::max<uint64_t>(total, 1) * 4));
+    for (size_t ti = 0; ti < nt; ++ti) {
+      const uint64_t n = ((ti & 1) ? c->s2 : c->s1) / 2;
+      const uint64_t sm16 = (n + 15) & ~15ull, bits16 = (c->rec_bits[ti] + 8 + 15) & ~15ull;
+      CK(cudaMemcpy(c->d_index + c->d_index_off[ti], c->cpool + c->rec_off[ti] + sm16 + bits16,
+                    ((n + chunk - 1) / chunk) * 4, cudaMemcpyHostToDevice));
+    }
+  }
   stage_device_tier(c);
 }
 
@@ -1211,6 +1229,7 @@ int xpgb_destroy(xpgb_ctx* h) {
         cudaEventDestroy(c->ev_mapped[k]);
         cudaEventDestroy(c->ev_raw[k]);
       }
+      if (c->d_index) cudaFree(c->d_index);
     }
     cudaStreamDestroy(c->s_comp);
     delete h;
@@ -1569,6 +1588,12 @@ int xpgb_hbm_bytes(xpgb_ctx* h, uint64_t* ring, uint64_t* staging, uint64_t* dev
     Ctx* c = &h->c;
     *ring = (uint64_t)c->blocks * (c->s1 + c->s2);
     *staging = 2 * (c->stage_cap[0] + c->stage_cap[1]);
+    if (c->d_index) {
+      uint64_t entries = 0;
+      const size_t nt = (size_t)c->N * c->E * 2;
+      for (size_t ti = 0; ti < nt; ++ti) entries += ((((ti & 1) ? c->s2 : c->s1) / 2) + c->cchunk - 1) / c->cchunk;
+      *staging += entries * 4;
+    }
     uint64_t dt = 0;
     const size_t nt = (size_t)c->N * c->E * 2;
     for (size_t ti = 0; ti < nt && c->dev_tier; ++ti)
