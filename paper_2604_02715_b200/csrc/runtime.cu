@@ -238,6 +238,7 @@ struct Ctx {
   std::vector<uint64_t> d_index_off;     // [N*E*2] offset (entries) into d_index
   uint64_t stage_cap[2] = {0, 0};
   cudaStream_t s_dec[2] = {nullptr, nullptr};
+  cudaStream_t s_alt[2] = {nullptr, nullptr};  // second copy stream per kind for staged pieces
   cudaEvent_t ev_copied[2][2], ev_decoded[2][2], ev_mapped[2], ev_raw[2];
   bool codec_events = false;
 
@@ -644,6 +645,7 @@ static void materialize(RunState& rs, int g, int it, int layer, int kind) {
     cudaStream_t d = c->s_dec[k];
     CK(cudaEventRecord(c->ev_mapped[k], s));
     CK(cudaStreamWaitEvent(d, c->ev_mapped[k], 0));
+    if (c->host_codec) CK(cudaStreamWaitEvent(c->s_alt[k], c->ev_mapped[k], 0));
     bool raw_on_s = false;
     int hb = 0;
     for (int e = 0; e < E; ++e) {
@@ -692,10 +694,13 @@ static void materialize(RunState& rs, int g, int it, int layer, int kind) {
           if (o_bits + nbits > c->stage_cap[k]) XFAIL(XPGB_ERR, "codec piece exceeds staging buffer");
           const int buf = hb++ & 1;
           uint8_t* st = c->stage[k][buf];
-          CK(cudaStreamWaitEvent(s, c->ev_decoded[k][buf], 0));
-          CK(cudaMemcpyAsync(st, rec + v0, ns, cudaMemcpyHostToDevice, s));
-          CK(cudaMemcpyAsync(st + o_bits, rec + sm16 + b0, nbits, cudaMemcpyHostToDevice, s));
-          CK(cudaEventRecord(c->ev_copied[k][buf], s));
+          // buffer b is filled by its own copy stream, so one stream's wait/turnaround
+          // bubble hides behind the other's transfer
+          cudaStream_t cs = buf ? c->s_alt[k] : s;
+          CK(cudaStreamWaitEvent(cs, c->ev_decoded[k][buf], 0));
+          CK(cudaMemcpyAsync(st, rec + v0, ns, cudaMemcpyHostToDevice, cs));
+          CK(cudaMemcpyAsync(st + o_bits, rec + sm16 + b0, nbits, cudaMemcpyHostToDevice, cs));
+          CK(cudaEventRecord(c->ev_copied[k][buf], cs));
           rs.h2d += ns + nbits;
           CK(cudaStreamWaitEvent(d, c->ev_copied[k][buf], 0));
           launch_exp_decode(st, reinterpret_cast<const uint32_t*>(st + o_bits), c->d_index + c->d_index_off[ti] + c0,
@@ -1082,6 +1087,7 @@ static void set_codec(Ctx* c, const void* pool, uint64_t pool_bytes, const uint6
   if (!c->codec_events) {
     for (int k = 0; k < 2; ++k) {
       CK(cudaStreamCreateWithFlags(&c->s_dec[k], cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&c->s_alt[k], cudaStreamNonBlocking));
       for (int b = 0; b < 2; ++b) {
         CK(cudaEventCreateWithFlags(&c->ev_copied[k][b], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_decoded[k][b], cudaEventDisableTiming));
@@ -1221,6 +1227,7 @@ int xpgb_destroy(xpgb_ctx* h) {
     if (c->codec_events) {
       for (int k = 0; k < 2; ++k) {
         cudaStreamDestroy(c->s_dec[k]);
+        cudaStreamDestroy(c->s_alt[k]);
         for (int b = 0; b < 2; ++b) {
           cudaEventDestroy(c->ev_copied[k][b]);
           cudaEventDestroy(c->ev_decoded[k][b]);
