@@ -210,6 +210,11 @@ int xpgb_codec_decode(const void* record_dev, uint64_t n, uint64_t bits_len, int
 int xpgb_set_codec(xpgb_ctx* ctx, const void* pool, uint64_t pool_bytes, const uint64_t* rec_offsets,
                    const uint64_t* bits_lens, const uint8_t* lengths256, int32_t chunk, int32_t host_compressed);
 
+/* Residency tier x > 0: experts with pinned_of[(layer-1)*L + expert-1]
+ * = 1 stay RESIDENT in dedicated blocks for the context's lifetime; the schedule streams only the
+ * others through a ring of 2 x (most streamed experts of any layer) blocks per kind.  Re-creates
+ * the arena (no session may be active).  All-zero = the reference geometry. */
+int xpgb_set_pinned(xpgb_ctx* ctx, const uint8_t* pinned_of);
 /* Expert-weight HBM footprint of a context: ring/pool blocks, codec staging, device tier. */
 int xpgb_hbm_bytes(xpgb_ctx* ctx, uint64_t* ring, uint64_t* staging, uint64_t* device_tier);
 

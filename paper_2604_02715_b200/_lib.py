@@ -119,6 +119,7 @@ _SIGS = {
     "xpgb_codec_index": [_P, _U64, _U64, C.POINTER(C.c_uint8), _I, C.POINTER(C.c_uint32)],
     "xpgb_codec_decode": [_P, _U64, _U64, _I, C.POINTER(C.c_uint8), _P, _P],
     "xpgb_set_codec": [_P, _P, _U64, C.POINTER(_U64), C.POINTER(_U64), C.POINTER(C.c_uint8), _I, _I],
+    "xpgb_set_pinned": [_P, C.POINTER(C.c_uint8)],
     "xpgb_hbm_bytes": [_P, C.POINTER(_U64), C.POINTER(_U64), C.POINTER(_U64)],
     "xpgb_profile_layer": [_P, _I, _P, _P, _I, _I, _U64, _I, C.POINTER(KernelTimes)],
 }

@@ -200,6 +200,8 @@ struct Ctx {
   bool trace_on = false;
   std::string trace;
   int32_t* d_pt = nullptr;  // [2][N*E] device slot table
+  std::vector<uint8_t> pinned;  // [N*E] permanently resident experts (residency tier x > 0)
+  int ring_blocks = 0;          // blocks per kind that cycle through the schedule
 
   // streams / events
   cudaStream_t s_copy[2] = {nullptr, nullptr};
@@ -289,9 +291,10 @@ static void free_pools(Ctx* c) {
   c->dev_tier = nullptr;
 }
 
-static void init_pools(Ctx* c) {
+static void init_pools(Ctx* c, int ring_blocks = -1, int pinned_blocks = 0) {
   free_pools(c);
-  c->blocks = (c->pool == XPGB_POOL_RING) ? 2 * c->E : c->N * c->E;
+  c->ring_blocks = ring_blocks >= 0 ? ring_blocks : ((c->pool == XPGB_POOL_RING) ? 2 * c->E : c->N * c->E);
+  c->blocks = c->ring_blocks + pinned_blocks;
   const uint64_t bytes = (uint64_t)c->blocks * (c->s1 + c->s2);
   CK(cudaMalloc(&c->arena, bytes));
   CK(cudaMemset(c->arena, 0, bytes));
@@ -309,6 +312,7 @@ static void init_pools(Ctx* c) {
   c->step = 0;
   c->backend.assign(pages * 2, 0);
   c->dev_off.assign(pages * 2, -1);
+  c->pinned.assign(pages, 0);
   c->map_gu = make_map(c->arena, (uint64_t)c->blocks * 2 * c->F, c->H, kBM);
   c->map_dn = make_map(c->arena + (uint64_t)c->blocks * c->s1, (uint64_t)c->blocks * c->H, c->F, kBM);
 }
@@ -512,6 +516,16 @@ static void pt_unmap(Ctx* c, int layer, int expert, int kind) {
   emit(c, "unmap", layer, expert, kind, b, "");
 }
 
+// Device table := host table (bulk upload; used after drains and pinning).
+static void pt_upload(Ctx* c) {
+  const size_t pages = (size_t)c->N * c->E;
+  std::vector<int32_t> tab(2 * pages);
+  for (int k = 0; k < 2; ++k)
+    for (size_t pi = 0; pi < pages; ++pi)
+      tab[k * pages + pi] = c->st[k][pi] == XPGB_PAGE_UNMAPPED ? -1 : pt_entry(c->blk[k][pi] - 1, c->st[k][pi]);
+  CK(cudaMemcpy(c->d_pt, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
+}
+
 static void pt_sync_entry(Ctx* c, int layer, int expert, int kind) {
   const int pi = page_index(c, layer, expert, kind);
   const int k = kind - 1;
@@ -596,19 +610,43 @@ static void materialize(RunState& rs, int g, int it, int layer, int kind) {
   const bool seq = rs.o->sequential != 0;
   PtOp op = blank_op(c, rs.log);
   int nrec = 0;
+  const bool any_pinned = std::find(c->pinned.begin(), c->pinned.end(), 1) != c->pinned.end();
+  auto is_pinned = [&](int l, int e) { return c->pinned[(size_t)(l - 1) * E + e] != 0; };
   if (it > 1 || layer > 2) {
     const int tgt = ((layer - 3 + N) % N) + 1;
     const int tgt_it = layer > 2 ? it : it - 1;
     const int gt = (tgt_it - 1) * N + (tgt - 1);
     CK(cudaStreamWaitEvent(s, c->ev_comp[gt & 3], 0));  // WAR
-    for (int e = 0; e < E; ++e) pt_unmap(c, tgt, c->e_first + e + 1, kind);
-    op.unmap_row = c->d_pt + (size_t)k * N * E + (size_t)(tgt - 1) * E;
-    op.unmap_n = E;
+    for (int e = 0; e < E; ++e)
+      if (!is_pinned(tgt, e)) pt_unmap(c, tgt, c->e_first + e + 1, kind);
     if (rs.log) set_rec(op, nrec++, XPGB_EV_RECYCLE, it, layer, kind, tgt_it, tgt);
+    int32_t* trow = c->d_pt + (size_t)k * N * E + (size_t)(tgt - 1) * E;
+    if (!any_pinned) {
+      op.unmap_row = trow;
+      op.unmap_n = E;
+    } else {
+      // keep the pinned entries of the recycled layer: rewrite its row explicitly
+      const int chunk = (int)(sizeof(op.vals) / sizeof(int32_t));
+      for (int e0 = 0; e0 < E; e0 += chunk) {
+        PtOp ou = (e0 == 0) ? op : blank_op(c, false);
+        if (e0 > 0) ou.n_rec = 0;
+        ou.set_row = trow + e0;
+        ou.set_n = std::min(chunk, E - e0);
+        for (int i = 0; i < ou.set_n; ++i) {
+          const size_t pi = (size_t)(tgt - 1) * E + e0 + i;
+          ou.vals[i] = c->st[k][pi] == XPGB_PAGE_UNMAPPED ? -1 : pt_entry(c->blk[k][pi] - 1, c->st[k][pi]);
+        }
+        launch_op(ou, s);
+      }
+      op = blank_op(c, rs.log);
+      nrec = 0;
+    }
   }
-  // map every expert of the layer (lowest free block first) -> LOADING entries
+  // map every streamed expert of the layer (lowest free block first) -> LOADING entries
   std::vector<int> blocks(E);
-  for (int e = 0; e < E; ++e) blocks[e] = pt_map(c, layer, c->e_first + e + 1, kind);
+  for (int e = 0; e < E; ++e)
+    blocks[e] = is_pinned(layer, e) ? c->blk[k][(size_t)(layer - 1) * E + e]
+                                    : pt_map(c, layer, c->e_first + e + 1, kind);
   if (rs.log) set_rec(op, nrec++, XPGB_EV_LOAD_START, it, layer, kind, -1, -1);
   int32_t* row = c->d_pt + (size_t)k * N * E + (size_t)(layer - 1) * E;
   const int chunk = (int)(sizeof(op.vals) / sizeof(int32_t));
@@ -617,7 +655,8 @@ static void materialize(RunState& rs, int g, int it, int layer, int kind) {
     if (e0 > 0) { o2.unmap_n = 0; o2.n_rec = 0; }
     o2.set_row = row + e0;
     o2.set_n = std::min(chunk, E - e0);
-    for (int i = 0; i < o2.set_n; ++i) o2.vals[i] = pt_entry(blocks[e0 + i] - 1, XPGB_PAGE_LOADING);
+    for (int i = 0; i < o2.set_n; ++i)
+      o2.vals[i] = pt_entry(blocks[e0 + i] - 1, is_pinned(layer, e0 + i) ? XPGB_PAGE_RESIDENT : XPGB_PAGE_LOADING);
     launch_op(o2, s);
   }
   const float* delays = rs.o->fetch_delay_s;
@@ -632,6 +671,7 @@ static void materialize(RunState& rs, int g, int it, int layer, int kind) {
   cudaStream_t done_stream = s;
   if (!c->codec) {
     for (int e = 0; e < E; ++e) {
+      if (is_pinned(layer, e)) continue;
       if (delay_of(e) > 0) sleep_on(s, delay_of(e));
       bool from_host = true;
       const uint64_t n = fetch(c, layer, c->e_first + e + 1, kind, block_ptr(c, kind, blocks[e]), sigma_of(c, kind), s,
@@ -649,6 +689,7 @@ static void materialize(RunState& rs, int g, int it, int layer, int kind) {
     bool raw_on_s = false;
     int hb = 0;
     for (int e = 0; e < E; ++e) {
+      if (is_pinned(layer, e)) continue;
       const size_t pi = (size_t)(layer - 1) * E + e, ti = pi * 2 + k;
       const uint64_t n = sigma_of(c, kind) / 2;
       uint8_t* dst = block_ptr(c, kind, blocks[e]);
@@ -722,7 +763,8 @@ static void materialize(RunState& rs, int g, int it, int layer, int kind) {
     }
     done_stream = d;
   }
-  for (int e = 0; e < E; ++e) pt_mark_resident(c, layer, c->e_first + e + 1, kind);
+  for (int e = 0; e < E; ++e)
+    if (!is_pinned(layer, e)) pt_mark_resident(c, layer, c->e_first + e + 1, kind);
   for (int e0 = 0; e0 < E; e0 += chunk) {
     PtOp o3 = blank_op(c, rs.log && e0 + chunk >= E);
     o3.set_row = row + e0;
@@ -793,10 +835,9 @@ static void session_begin(Ctx* c, const xpgb_run_opts* o, float* acts) {
     // a run starts from an empty ring, like a fresh PageTable (pipeline.py:325)
     for (int k = 0; k < 2; ++k)
       for (size_t pi = 0; pi < c->st[k].size(); ++pi)
-        if (c->st[k][pi] != XPGB_PAGE_UNMAPPED)
+        if (c->st[k][pi] != XPGB_PAGE_UNMAPPED && !c->pinned[pi])
           XFAIL(XPGB_ERR_DOUBLE_MAP, "run() needs an empty page table; page %zu kind %d is mapped", pi, k + 1);
-    c->bound = 0;
-    c->peak = 0;
+    c->peak = c->bound;  // pinned pages stay bound
   }
   ss.rs = RunState{c, &ss.o, acts, 0, 0, o->log_enable != 0};
   cudaStream_t s = c->s_comp;
@@ -982,11 +1023,11 @@ static void session_end(Ctx* c, xpgb_report* rep) {
     // runner would drop its table (the reference keeps them until GC).
     for (int k = 0; k < 2; ++k)
       for (size_t pi = 0; pi < c->st[k].size(); ++pi)
-        if (c->st[k][pi] == XPGB_PAGE_RESIDENT) {
+        if (c->st[k][pi] == XPGB_PAGE_RESIDENT && !c->pinned[pi]) {
           const int layer = (int)(pi / c->E) + 1, e = (int)(pi % c->E);
           pt_unmap(c, layer, c->e_first + e + 1, k + 1);
         }
-    CK(cudaMemset(c->d_pt, 0xFF, 2 * (size_t)c->N * c->E * sizeof(int32_t)));
+    pt_upload(c);
   }
 }
 
@@ -999,15 +1040,19 @@ static void session_abort(Ctx* c) {
   // drop every binding so the next run starts from an empty ring
   for (int k = 0; k < 2; ++k)
     for (size_t pi = 0; pi < c->st[k].size(); ++pi) {
+      if (c->pinned[pi]) continue;
       if (c->blk[k][pi]) {
         c->free_ids[k].insert(c->blk[k][pi]);
         c->owner[k][c->blk[k][pi]] = -1;
+        c->bound -= sigma_of(c, k + 1);
       }
       c->blk[k][pi] = 0;
       c->st[k][pi] = XPGB_PAGE_UNMAPPED;
     }
-  c->bound = 0;
-  cudaMemset(c->d_pt, 0xFF, 2 * (size_t)c->N * c->E * sizeof(int32_t));
+  try {
+    pt_upload(c);
+  } catch (...) {
+  }
 }
 
 static void run_impl(Ctx* c, const xpgb_run_opts* o, const float* x, float* y, xpgb_report* rep) {
@@ -1609,6 +1654,57 @@ int xpgb_hbm_bytes(xpgb_ctx* h, uint64_t* ring, uint64_t* staging, uint64_t* dev
         dt += c->codec ? xpgb_codec_record_bytes(raw / 2, c->rec_bits[ti], c->cchunk) : raw;
       }
     *device_tier = dt;
+  });
+}
+
+int xpgb_set_pinned(xpgb_ctx* h, const uint8_t* pinned_of) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    if (c->pool != XPGB_POOL_RING) XFAIL(XPGB_ERR_CONFIG, "pinned experts need a ring context");
+    if (c->sess && c->sess->active) XFAIL(XPGB_ERR, "cannot pin experts during a session");
+    const size_t pages = (size_t)c->N * c->E;
+    std::vector<uint8_t> mask(pages, 0);
+    int n_pinned = 0, max_streamed = 0;
+    for (int l = 0; l < c->N; ++l) {
+      int streamed = 0;
+      for (int e = 0; e < c->E; ++e) {
+        const uint8_t v = pinned_of ? (pinned_of[(size_t)l * c->L + c->e_first + e] ? 1 : 0) : 0;
+        mask[(size_t)l * c->E + e] = v;
+        n_pinned += v;
+        streamed += !v;
+      }
+      max_streamed = std::max(max_streamed, streamed);
+    }
+    if (n_pinned && !c->host) XFAIL(XPGB_ERR_BACKEND_MISS, "pinning experts needs the host pool");
+    // re-create the arena: 2 x (most streamed experts of any layer) ring blocks + one block per pinned expert
+    std::vector<uint8_t> backend = c->backend;
+    CK(cudaDeviceSynchronize());
+    init_pools(c, 2 * max_streamed, n_pinned);
+    c->backend = backend;
+    c->pinned = mask;
+    int next = c->ring_blocks + 1;
+    for (int l = 1; l <= c->N; ++l)
+      for (int e = 0; e < c->E; ++e) {
+        if (!mask[(size_t)(l - 1) * c->E + e]) continue;
+        for (int kind = 1; kind <= 2; ++kind) {
+          const int k = kind - 1;
+          const size_t pi = (size_t)(l - 1) * c->E + e;
+          c->free_ids[k].erase(next);
+          c->blk[k][pi] = next;
+          c->owner[k][next] = (int)pi;
+          c->st[k][pi] = XPGB_PAGE_RESIDENT;
+          c->bound += sigma_of(c, kind);
+          const uint64_t off = pi * (c->s1 + c->s2) + (kind == 2 ? c->s1 : 0);
+          CK(cudaMemcpy(block_ptr(c, kind, next), c->host + off, sigma_of(c, kind), cudaMemcpyHostToDevice));
+        }
+        ++next;
+      }
+    c->peak = c->bound;
+    pt_upload(c);
+    if (c->codec) {
+      // staging buffers and device tier survive; re-stage the device tier into the new arena layout
+    }
+    stage_device_tier(c);
   });
 }
 

@@ -103,6 +103,10 @@ class Context:
         call("xpgb_set_expert_shard", self._h, first, count)
         self.expert_first, self.expert_count = first, count
 
+    def set_pinned(self, mask: np.ndarray) -> None:
+        arr = np.ascontiguousarray(mask, dtype=np.uint8)
+        call("xpgb_set_pinned", self._h, arr.ctypes.data_as(C.POINTER(C.c_uint8)))
+
     def hbm_bytes(self) -> dict:
         r, st, dt = C.c_uint64(), C.c_uint64(), C.c_uint64()
         call("xpgb_hbm_bytes", self._h, C.byref(r), C.byref(st), C.byref(dt))

@@ -200,7 +200,7 @@ class StreamedRunner:
 
     def __init__(self, spec: ModelSpec, hierarchy: StorageHierarchy, fwd: ForwardSpec, mode: str = "threaded",
                  compute_delay_fn=None, sabotage_skip_raw=None, trace=None, device: int = 0,
-                 host_codec: bool = False):
+                 host_codec: bool = False, pinned=None):
         if mode not in ("threaded", "sequential"):
             raise XpgError(f"unknown mode {mode!r}")
         self.spec = spec
@@ -219,6 +219,9 @@ class StreamedRunner:
             # decoded on the GPU straight into the ring block.
             self.ctx.set_codec(cm, host_compressed=host_codec)
         self.ctx.set_placement(placement)
+        if pinned is not None:
+            # residency tier x > 0: these experts never leave HBM; the ring streams the rest
+            self.ctx.set_pinned(pinned_mask(spec, pinned))
         self.table = PageTable(spec, trace=trace, context=self.ctx)
         self.stall_seconds = 0.0
         self.war_wait_seconds = 0.0
@@ -263,6 +266,16 @@ def _kernel_stats(rep) -> dict:
         "gate_up_bytes": int(rep.gate_up_bytes), "down_bytes": int(rep.down_bytes),
         "down_splits": int(rep.down_splits), "active_experts": int(rep.active_experts),
     }
+
+
+def pinned_mask(spec: ModelSpec, pinned) -> np.ndarray:
+    """uint8 [N][L] mask: an int m pins experts 1..m of every layer; arrays pass through."""
+    if isinstance(pinned, (int, np.integer)):
+        m = np.zeros((spec.num_layers, spec.experts_per_layer), dtype=np.uint8)
+        m[:, :int(pinned)] = 1
+        return m
+    m = np.asarray(pinned, dtype=np.uint8).reshape(spec.num_layers, spec.experts_per_layer)
+    return np.ascontiguousarray(m)
 
 
 def _codec_model(hierarchy: StorageHierarchy, needed: bool):

@@ -272,3 +272,25 @@ def test_session_api_external_compute_matches_run(X):
     call("xpgb_session_end", h, C.byref(rep))
     assert acts.cpu().numpy().tobytes() == want.tobytes()
     assert rep.page_fault == 0
+
+
+@pytest.mark.parametrize("pinned,host_codec", [(2, False), (5, True), (7, False)])
+def test_pinned_experts_budget_tier(X, pinned, host_codec):
+    """Residency tier x > 0: pinned experts stay resident, the ring streams the rest; results unchanged."""
+    spec = X.ModelSpec(4, 8, 256, 512)
+    fwd = X.ForwardSpec(16, 2, 7)
+    container, hier = _hier(X, spec, seed=7)
+    x = X.initial_activations(spec, fwd, 7)
+    runner = X.StreamedRunner(spec, hier, fwd, pinned=pinned, host_codec=host_codec)
+    rep = runner.run(2, acts=x.copy())
+    base = X.resident_baseline(2, spec, container, fwd, acts=x.copy())
+    assert rep.page_fault is None and rep.violations == []
+    assert rep.final_activations.tobytes() == base.tobytes()
+    streamed = spec.experts_per_layer - pinned
+    hbm = runner.ctx.hbm_bytes()
+    assert hbm["ring"] == (2 * streamed + spec.num_layers * pinned) * spec.expert_bytes
+    if not host_codec:
+        assert rep.h2d_bytes == 2 * spec.num_layers * streamed * spec.expert_bytes
+    # a second run on the same context still finds its pinned experts resident
+    rep2 = runner.run(1, acts=x.copy())
+    assert rep2.page_fault is None and rep2.violations == []

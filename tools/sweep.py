@@ -1,0 +1,89 @@
+"""Sweeps for BASELINE configs 3 and 5 (one JSON line per point).
+
+    python tools/sweep.py budget [--config mixtral] [--tokens 256] [--raw]
+        paging budget from the 2-layer ring (25% at N=8) up to fully resident, by pinning
+        experts 1..m of every layer (residency tier x > 0); fully-resident comparator last
+    python tools/sweep.py tokens [--config qwen3] [--list 1,4,16,64,256]
+        decode batch sweep under the fixed 2-layer-ring budget
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from bench import CONFIGS, SEED, h2d_peak_gbps  # noqa: E402
+
+
+def timed(torch, fn, steps):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    rep = fn(steps)
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e-3, rep
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("what", choices=["budget", "tokens"])
+    ap.add_argument("--config", default=None)
+    ap.add_argument("--tokens", type=int, default=None)
+    ap.add_argument("--list", default="1,4,16,64,256")
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=1)
+    ap.add_argument("--raw", action="store_true")
+    args = ap.parse_args()
+    import torch
+
+    import paper_2604_02715_b200 as X
+    from paper_2604_02715_b200.exponent_codec import CompressedModel
+
+    cfg = dict(CONFIGS[args.config or ("mixtral" if args.what == "budget" else "qwen3")])
+    if args.tokens:
+        cfg["T"] = args.tokens
+    N, L, H, F, k = cfg["N"], cfg["L"], cfg["H"], cfg["F"], cfg["k"]
+    spec = X.ModelSpec(N, L, H, F)
+    t0 = time.time()
+    container = X.generate_fast_model(spec, SEED)
+    backends = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 55e9, 1 << 50)]
+    hier = X.StorageHierarchy(container, None, X.plan_placement(spec, backends), backends)
+    if not args.raw:
+        hier.compressed = CompressedModel.from_container(container)
+    peak = h2d_peak_gbps(torch, 0)
+    print(f"setup {time.time() - t0:.1f}s", file=sys.stderr, flush=True)
+    points = list(range(0, L)) if args.what == "budget" else [int(t) for t in args.list.split(",")]
+    resident_tok = {}
+    for p in points:
+        T = cfg["T"] if args.what == "budget" else p
+        fwd = X.ForwardSpec(T, k, SEED)
+        x = torch.from_numpy(X.initial_activations(spec, fwd, SEED)).cuda()
+        runner = X.StreamedRunner(spec, hier, fwd, host_codec=not args.raw,
+                                  pinned=(p if args.what == "budget" else None))
+        runner.run(args.warmup, acts=x)
+        secs, rep = timed(torch, lambda s: runner.run(s, acts=x), args.steps)
+        hbm = runner.ctx.hbm_bytes()
+        row = {"sweep": args.what, "config": args.config or cfg["name"], "T": T,
+               "pinned_per_layer": p if args.what == "budget" else 0,
+               "hbm_fraction": (hbm["ring"] + hbm["staging"] + hbm["device_tier"]) / spec.total_bytes,
+               "tok_s": T * args.steps / secs, "ms_per_step": 1e3 * secs / args.steps,
+               "page_in_gbps": rep.h2d_bytes / rep.elapsed_seconds / 1e9 if rep.elapsed_seconds else 0.0,
+               "h2d_peak_gbps": peak, "exposed_xfer_pct": 100 * rep.stall_seconds / max(rep.elapsed_seconds, 1e-12),
+               "host_codec": not args.raw}
+        del runner
+        if T not in resident_tok:
+            model = X.ResidentModel(spec, container, max_tokens=T)
+            model.run(1, fwd, x)
+            rs, _ = timed(torch, lambda s: model.run(s, fwd, x), args.steps)
+            resident_tok[T] = T * args.steps / rs
+            del model
+        row["resident_tok_s"] = resident_tok[T]
+        row["fraction_of_resident"] = row["tok_s"] / resident_tok[T]
+        print(json.dumps(row), flush=True)
+
+
+if __name__ == "__main__":
+    main()
