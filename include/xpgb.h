@@ -190,10 +190,13 @@ int xpgb_codec_encode(const void* data, uint64_t bytes, const uint8_t* lengths25
                       int32_t chunk);
 /* Compress n_tensors consecutive tensors of a payload into packed records (multi-threaded,
  * host only).  out == NULL computes the layout only (pool_bytes, rec_offsets, bits_lens,
- * bit_counts: [n_tensors]); otherwise out (>= pool_bytes) receives the records. */
+ * bit_counts: [n_tensors]); otherwise out (>= pool_bytes) receives the records.
+ * place_order (nullable = payload order) lists tensor indices in the order their records
+ * are laid out in the pool; the runtime stages runs of consecutive records with one copy,
+ * so (layer, kind, expert) order lets a layer's small records travel together. */
 int xpgb_codec_pack(const void* payload, int32_t n_tensors, const uint64_t* value_counts, const uint8_t* lengths256,
-                    int32_t chunk, int32_t threads, void* out, uint64_t out_cap, uint64_t* pool_bytes,
-                    uint64_t* rec_offsets, uint64_t* bits_lens, uint64_t* bit_counts);
+                    int32_t chunk, int32_t threads, const int32_t* place_order, void* out, uint64_t out_cap,
+                    uint64_t* pool_bytes, uint64_t* rec_offsets, uint64_t* bits_lens, uint64_t* bit_counts);
 /* Byte size of a packed record. */
 uint64_t xpgb_codec_record_bytes(uint64_t n, uint64_t bits_len, int32_t chunk);
 /* Rebuild the chunk index of a stream on the host, validating it like decompress():
@@ -215,7 +218,14 @@ int xpgb_set_codec(xpgb_ctx* ctx, const void* pool, uint64_t pool_bytes, const u
  * others through a ring of 2 x (most streamed experts of any layer) blocks per kind.  Re-creates
  * the arena (no session may be active).  All-zero = the reference geometry. */
 int xpgb_set_pinned(xpgb_ctx* ctx, const uint8_t* pinned_of);
-/* Expert-weight HBM footprint of a context: ring/pool blocks, codec staging, device tier. */
+/* Shared experts (DeepSeek-V3 style; absent from the reference, our convention): n_shared
+ * always-on experts per layer that every token passes through after its routed experts,
+ * weight 1.0 (the routed sum keeps its f32(1/top_k) scale).  host = N*n_shared*(sigma1+sigma2)
+ * bytes in (layer, shared expert, kind) order; they stay resident in HBM and are never paged.
+ * n_shared = 0 removes them.  Single-device contexts only (not the expert-parallel path). */
+int xpgb_set_shared(xpgb_ctx* ctx, const void* host, uint64_t bytes, int32_t n_shared);
+/* Expert-weight HBM footprint of a context: ring/pool blocks (+ shared experts), codec
+ * staging, device tier. */
 int xpgb_hbm_bytes(xpgb_ctx* ctx, uint64_t* ring, uint64_t* staging, uint64_t* device_tier);
 
 /* ---------------------------------------------------------------- compute */

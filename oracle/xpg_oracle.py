@@ -219,6 +219,22 @@ class WordPool:
         return bf16_to_f32(self.tensor_words(layer, expert, kind))
 
 
+class SharedPool:
+    """Shared (always-on) experts: uint16 words in (layer, shared expert, kind) order.
+    No reference counterpart -- our convention (parity unpinned)."""
+
+    def __init__(self, N, S, H, F, words):
+        self.N, self.S, self.H, self.F = N, S, H, F
+        self.words = np.asarray(words, dtype=np.uint16).reshape(-1)
+
+    def tensor_f32(self, layer, index, kind):
+        eb = sigma(self.H, self.F, 1) + sigma(self.H, self.F, 2)
+        off = (((layer - 1) * self.S + (index - 1)) * eb + (sigma(self.H, self.F, 1) if kind == 2 else 0)) // 2
+        n = sigma(self.H, self.F, kind) // 2
+        shape = (2 * self.F, self.H) if kind == 1 else (self.H, self.F)
+        return bf16_to_f32(self.words[off:off + n].reshape(shape))
+
+
 # ---------------------------------------------------------------------------
 # SwiGLU expert + MoE layer (reference pipeline.py:180-208, 216-230)
 
@@ -236,11 +252,13 @@ def expert_rows(gate_up: np.ndarray, down: np.ndarray, xs: np.ndarray) -> np.nda
         return (silu(g) * u) @ down.T
 
 
-def layer_forward(pool: WordPool, layer: int, acts: np.ndarray, top_k: int, seed: int) -> np.ndarray:
+def layer_forward(pool: WordPool, layer: int, acts: np.ndarray, top_k: int, seed: int,
+                  shared: "SharedPool | None" = None) -> np.ndarray:
     """One MoE layer: y_t = sum_{j in routed(t), ascending} expert_j(x_t) * f32(1/top_k).
 
     Vectorised per expert over its tokens; per-token accumulation order is
-    the reference's (ascending j, pipeline.py:203-206).
+    the reference's (ascending j, pipeline.py:203-206).  With ``shared``, each
+    shared expert's output is then added with weight 1 (our convention).
     """
     acts = np.asarray(acts, dtype=np.float32)
     T = acts.shape[0]
@@ -255,15 +273,19 @@ def layer_forward(pool: WordPool, layer: int, acts: np.ndarray, top_k: int, seed
     y = np.zeros_like(acts)
     for s in range(routes.shape[1]):
         y += per_slot[s]
+    if shared is not None:
+        for i in range(1, shared.S + 1):
+            y += expert_rows(shared.tensor_f32(layer, i, 1), shared.tensor_f32(layer, i, 2), acts)
     return y
 
 
-def resident_stack(pool: WordPool, acts: np.ndarray, top_k: int, seed: int, iterations: int = 1):
+def resident_stack(pool: WordPool, acts: np.ndarray, top_k: int, seed: int, iterations: int = 1,
+                   shared: "SharedPool | None" = None):
     """resident_baseline restated: iterations x layers 1..N."""
     a = np.array(acts, dtype=np.float32, copy=True)
     for _ in range(iterations):
         for layer in range(1, pool.N + 1):
-            a = layer_forward(pool, layer, a, top_k, seed)
+            a = layer_forward(pool, layer, a, top_k, seed, shared)
     return a
 
 

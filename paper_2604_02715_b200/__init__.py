@@ -25,6 +25,7 @@ from .errors import (
 from .geometry import (
     ExpertTensorId,
     ModelSpec,
+    SharedExperts,
     TensorKind,
     WeightContainer,
     bf16_to_float32,

@@ -108,12 +108,14 @@ _SIGS = {
     "xpgb_session_abort": [_P],
     "xpgb_log_get": [_P, C.POINTER(Record), _I, C.POINTER(_I)],
     "xpgb_set_expert_shard": [_P, _I, _I],
+    "xpgb_set_shared": [_P, _P, _U64, _I],
     "xpgb_experts_forward": [_P, _I, _P, _P, _I, _P, _P],
     "xpgb_combine_rows": [_P, _P, _I, _I, _I, _I, _P, _P],
     "xpgb_codec_histogram": [_P, _U64, C.POINTER(_U64), _I],
     "xpgb_codec_encode": [_P, _U64, C.POINTER(C.c_uint8), _P, _P, _U64, C.POINTER(_U64), C.POINTER(_U64),
                           C.POINTER(C.c_uint32), _I],
-    "xpgb_codec_pack": [_P, _I, C.POINTER(_U64), C.POINTER(C.c_uint8), _I, _I, _P, _U64, C.POINTER(_U64),
+    "xpgb_codec_pack": [_P, _I, C.POINTER(_U64), C.POINTER(C.c_uint8), _I, _I, C.POINTER(C.c_int32), _P, _U64,
+                        C.POINTER(_U64),
                         C.POINTER(_U64), C.POINTER(_U64), C.POINTER(_U64)],
     "xpgb_codec_record_bytes": [_U64, _U64, _I],
     "xpgb_codec_index": [_P, _U64, _U64, C.POINTER(C.c_uint8), _I, C.POINTER(C.c_uint32)],

@@ -138,14 +138,11 @@ int codec_build_index(const uint8_t* bits, size_t bits_len, size_t n, const uint
 // ----------------------------------------------------------------------------- GPU decoder
 
 struct DecodeParams {
-  const uint8_t* sm;
-  const uint32_t* bits;
-  const uint32_t* index;
+  DecodeTensor t[kMaxDecodeTensors];  // tensors of one launch, each n values
+  int ntensors;
   uint64_t n;
   int chunk;
-  uint32_t bit_base;  // subtracted from index[] (a piece of a stream staged on its own)
-  uint16_t* out;
-  CodecTable t;
+  CodecTable table;
 };
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
@@ -154,7 +151,7 @@ __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 
 // MSB-first window, a 4096-entry LUT for codes <= 12 bits, canonical
 // first-code search for longer ones.  Output words are assembled as
 // (sign << 15) | (exponent << 7) | mantissa, 8 per 16-byte store.
-__global__ void __launch_bounds__(256) k_exp_decode(DecodeParams p) {
+__global__ void __launch_bounds__(256) k_exp_decode(const __grid_constant__ DecodeParams p) {
   __shared__ uint16_t lut[1 << kLutBits];
   __shared__ uint32_t first_code[kCodecMaxLen + 1];
   __shared__ int count[kCodecMaxLen + 1], first_rank[kCodecMaxLen + 1];
@@ -164,7 +161,7 @@ __global__ void __launch_bounds__(256) k_exp_decode(DecodeParams p) {
   for (int i = tid; i < (1 << kLutBits); i += blockDim.x) lut[i] = 0;
   if (tid <= kCodecMaxLen) count[tid] = 0;
   __syncthreads();
-  if (tid < kCodecSymbols && p.t.len[tid]) atomicAdd(&count[p.t.len[tid]], 1);
+  if (tid < kCodecSymbols && p.table.len[tid]) atomicAdd(&count[p.table.len[tid]], 1);
   __syncthreads();
   if (tid == 0) {
     uint32_t code = 0;
@@ -185,10 +182,10 @@ __global__ void __launch_bounds__(256) k_exp_decode(DecodeParams p) {
   }
   __syncthreads();
   if (tid < kCodecSymbols) {
-    const int l = p.t.len[tid];
+    const int l = p.table.len[tid];
     if (l) {
       int r = 0;
-      for (int s = 0; s < tid; ++s) r += (p.t.len[s] == l);
+      for (int s = 0; s < tid; ++s) r += (p.table.len[s] == l);
       sorted_sym[first_rank[l] + r] = (uint8_t)tid;
       if (l <= kLutBits) {
         const uint32_t code = first_code[l] + r;
@@ -200,21 +197,27 @@ __global__ void __launch_bounds__(256) k_exp_decode(DecodeParams p) {
   __syncthreads();
 
   const uint64_t n = p.n;
-  const uint64_t n_chunks = (n + p.chunk - 1) / p.chunk;
+  const uint64_t cpt = (n + p.chunk - 1) / p.chunk;  // chunks per tensor
+  const uint64_t n_chunks = cpt * (uint64_t)p.ntensors;
   const int ml = maxlen;
-  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + tid; c < n_chunks; c += (uint64_t)gridDim.x * blockDim.x) {
+  for (uint64_t gc = blockIdx.x * (uint64_t)blockDim.x + tid; gc < n_chunks; gc += (uint64_t)gridDim.x * blockDim.x) {
+    const int ti = (int)(gc / cpt);
+    const uint64_t c = gc - (uint64_t)ti * cpt;
+    const DecodeTensor& d = p.t[ti];
+    const uint8_t* __restrict__ sm = d.sm;
+    uint16_t* __restrict__ out = d.out;
     const uint64_t v0 = c * p.chunk;
     const uint64_t v1 = (v0 + p.chunk < n) ? v0 + p.chunk : n;
-    const uint32_t bitpos = p.index[c] - p.bit_base;
+    const uint32_t bitpos = d.index[c] - d.bit_base;
     const uint32_t w = bitpos >> 5, sh = bitpos & 31;
-    uint64_t win = (((uint64_t)bswap32(p.bits[w]) << 32) | bswap32(p.bits[w + 1])) << sh;
+    uint64_t win = (((uint64_t)bswap32(d.bits[w]) << 32) | bswap32(d.bits[w + 1])) << sh;
     int avail = 64 - (int)sh;
-    const uint32_t* wp = p.bits + w + 2;
+    const uint32_t* wp = d.bits + w + 2;
     for (uint64_t v = v0; v < v1; v += 8) {
       const int cnt = (int)((v1 - v) < 8 ? (v1 - v) : 8);
       uint32_t packed[4] = {0, 0, 0, 0};
       uint2 smv = make_uint2(0, 0);
-      if (cnt == 8) smv = *reinterpret_cast<const uint2*>(p.sm + v);
+      if (cnt == 8) smv = *reinterpret_cast<const uint2*>(sm + v);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         if (j >= cnt) break;
@@ -236,14 +239,14 @@ __global__ void __launch_bounds__(256) k_exp_decode(DecodeParams p) {
         }
         win <<= l;
         avail -= l;
-        const uint32_t s = (cnt == 8) ? (((j < 4 ? smv.x : smv.y) >> (8 * (j & 3))) & 0xFF) : p.sm[v + j];
+        const uint32_t s = (cnt == 8) ? (((j < 4 ? smv.x : smv.y) >> (8 * (j & 3))) & 0xFF) : sm[v + j];
         const uint32_t word = ((s & 0x80u) << 8) | ((uint32_t)sym << 7) | (s & 0x7Fu);
         packed[j >> 1] |= word << (16 * (j & 1));
       }
       if (cnt == 8) {
-        *reinterpret_cast<uint4*>(p.out + v) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        *reinterpret_cast<uint4*>(out + v) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
       } else {
-        for (int j = 0; j < cnt; ++j) p.out[v + j] = (uint16_t)(packed[j >> 1] >> (16 * (j & 1)));
+        for (int j = 0; j < cnt; ++j) out[v + j] = (uint16_t)(packed[j >> 1] >> (16 * (j & 1)));
       }
     }
   }
@@ -251,9 +254,20 @@ __global__ void __launch_bounds__(256) k_exp_decode(DecodeParams p) {
 
 void launch_exp_decode(const uint8_t* sm, const uint32_t* bits, const uint32_t* index, uint64_t n, int chunk,
                        const CodecTable& table, uint16_t* out, cudaStream_t s, uint32_t bit_base) {
-  if (n == 0) return;
-  DecodeParams p{sm, bits, index, n, chunk, bit_base, out, table};
-  const uint64_t n_chunks = (n + chunk - 1) / chunk;
+  DecodeTensor t{sm, bits, index, out, bit_base};
+  launch_exp_decode_multi(&t, 1, n, chunk, table, s);
+}
+
+void launch_exp_decode_multi(const DecodeTensor* tensors, int ntensors, uint64_t n, int chunk, const CodecTable& table,
+                             cudaStream_t s) {
+  if (n == 0 || ntensors <= 0) return;
+  DecodeParams p;
+  p.ntensors = ntensors;
+  p.n = n;
+  p.chunk = chunk;
+  p.table = table;
+  for (int i = 0; i < ntensors; ++i) p.t[i] = tensors[i];
+  const uint64_t n_chunks = ((n + chunk - 1) / chunk) * (uint64_t)ntensors;
   const uint64_t blocks = std::min<uint64_t>((n_chunks + 255) / 256, 148 * 8);
   k_exp_decode<<<(unsigned)blocks, 256, 0, s>>>(p);
   note_launch();

@@ -44,10 +44,25 @@ int codec_build_index(const uint8_t* bits, size_t bits_len, size_t n, const uint
 // Upper bound of the stream bytes of n values under `lengths`.
 size_t codec_bits_bound(size_t n, const uint8_t* lengths);
 
+// One tensor of a multi-tensor decode launch: stream pointers (index entries minus
+// bit_base give bit offsets into `bits`) and the destination of its n values.
+struct DecodeTensor {
+  const uint8_t* sm;
+  const uint32_t* bits;
+  const uint32_t* index;
+  uint16_t* out;
+  uint32_t bit_base;
+};
+constexpr int kMaxDecodeTensors = 64;
+
 // GPU decode: bits must be readable as 32-bit words up to round_up(bits_len, 4) + 8 bytes.
 // bit_base is subtracted from every index entry (decoding one staged piece of a stream).
 void launch_exp_decode(const uint8_t* sm, const uint32_t* bits, const uint32_t* index, uint64_t n, int chunk,
                        const CodecTable& table, uint16_t* out, cudaStream_t s, uint32_t bit_base = 0);
+// Up to kMaxDecodeTensors tensors of n values each in one launch (one staged run of
+// consecutive records, or consecutive device-tier records of a layer).
+void launch_exp_decode_multi(const DecodeTensor* tensors, int ntensors, uint64_t n, int chunk, const CodecTable& table,
+                             cudaStream_t s);
 constexpr uint64_t kStagePieceBytes = 32ull << 20;  // max bytes of one staged record piece
 
 }  // namespace xpgb

@@ -25,24 +25,32 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
 }
 
 // Warp-cooperative top-k of one (layer, token).  Lane l owns experts
-// j = l+1, l+33, ...; each of the kk rounds takes the warp-wide minimum of
-// (score, j) over untaken candidates (ties -> smaller j, the reference's tuple
-// order).  Returns, in lanes 0..kk-1, the selected id and its ascending rank.
+// j = l+1, l+33, ... (NC slots, the scores hashed once into registers); each of
+// the kk rounds takes the warp-wide minimum of (score, j) over untaken
+// candidates (ties -> smaller j, the reference's tuple order).  Returns, in
+// lanes 0..kk-1, the selected id and its ascending rank.
+template <int NC>
 __device__ __forceinline__ void route_token(uint64_t seed, int layer, int t, int L, int kk, int lane, int* id,
                                             int* rank) {
   const uint64_t base =
       seed * 0x9E37ull + (uint64_t)(uint32_t)layer * 0xC2B2ull + (uint64_t)(uint32_t)t * 0x85EBull;
-  const int ncand = (L - lane + 31) / 32;
-  uint32_t taken = 0;
+  uint64_t sc[NC];
+  uint32_t live = 0;  // candidate slots still in play
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int j = lane + 1 + 32 * c;
+    sc[c] = splitmix64(base + (uint64_t)j);
+    if (j <= L) live |= 1u << c;
+  }
   int mine = 0x7fffffff;
   for (int r = 0; r < kk; ++r) {
     uint64_t bs = ~0ull;
     int bj = 0x7fffffff;
-    for (int c = 0; c < ncand; ++c) {
-      if (taken & (1u << c)) continue;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
       const int j = lane + 1 + 32 * c;
-      const uint64_t s = splitmix64(base + (uint64_t)j);
-      if (s < bs || (s == bs && j < bj)) { bs = s; bj = j; }
+      if ((live >> c) & 1u)
+        if (sc[c] < bs || (sc[c] == bs && j < bj)) { bs = sc[c]; bj = j; }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -50,7 +58,7 @@ __device__ __forceinline__ void route_token(uint64_t seed, int layer, int t, int
       const int oj = __shfl_xor_sync(0xffffffffu, bj, off);
       if (os < bs || (os == bs && oj < bj)) { bs = os; bj = oj; }
     }
-    if (((bj - 1) & 31) == lane) taken |= 1u << ((bj - 1) >> 5);
+    if (((bj - 1) & 31) == lane) live &= ~(1u << ((bj - 1) >> 5));
     if (lane == r) mine = bj;
   }
   int rk = 0;
@@ -59,6 +67,23 @@ __device__ __forceinline__ void route_token(uint64_t seed, int layer, int t, int
   *rank = rk;
 }
 
+// Candidate slots per lane for L experts, rounded to an instantiated width.
+static inline int route_nc(int L) {
+  const int n = (L + 31) / 32;
+  return n <= 1 ? 1 : n <= 2 ? 2 : n <= 4 ? 4 : n <= 8 ? 8 : n <= 16 ? 16 : 32;
+}
+
+#define XPGB_ROUTE_DISPATCH(NCV, KERNEL, GRID, BLOCK, STREAM, ...)                 \
+  switch (NCV) {                                                                   \
+    case 1: KERNEL<1><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;              \
+    case 2: KERNEL<2><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;              \
+    case 4: KERNEL<4><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;              \
+    case 8: KERNEL<8><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;              \
+    case 16: KERNEL<16><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;            \
+    default: KERNEL<32><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;            \
+  }
+
+template <int NC>
 __global__ void k_route(uint64_t seed, int layer_first, int layer_count, int T, int L, int top_k,
                         int32_t* __restrict__ out) {
   const int lane = threadIdx.x & 31;
@@ -67,7 +92,7 @@ __global__ void k_route(uint64_t seed, int layer_first, int layer_count, int T, 
   const int li = (int)(gw / T), t = (int)(gw % T);
   const int kk = min(top_k, L);
   int id, rank;
-  route_token(seed, layer_first + li, t, L, kk, lane, &id, &rank);
+  route_token<NC>(seed, layer_first + li, t, L, kk, lane, &id, &rank);
   if (lane < kk) out[((long long)li * T + t) * kk + rank] = id;
 }
 
@@ -77,7 +102,8 @@ void launch_route(uint64_t seed, int layer_first, int layer_count, int T, int L,
   if (warps == 0) return;
   const int threads = 256;
   const long long blocks = (warps * 32 + threads - 1) / threads;
-  k_route<<<(unsigned)blocks, threads, 0, s>>>(seed, layer_first, layer_count, T, L, top_k, out);
+  XPGB_ROUTE_DISPATCH(route_nc(L), k_route, (unsigned)blocks, threads, s, seed, layer_first, layer_count, T, L,
+                      top_k, out);
   note_launch();
 }
 
@@ -108,12 +134,21 @@ __device__ int block_exclusive_scan(int v, int* warp_tot, int* total) {
   return excl;
 }
 
+// Local GEMM group of a plan id: routed ids 1..L map onto this shard's experts
+// [0, E) (or -1 off-shard); shared ids L+1..L+S onto groups E..E+S-1.
+__device__ __forceinline__ int local_group(int id, int L, int e_first, int E) {
+  if (id > L) return E + (id - L - 1);
+  const int el = id - 1 - e_first;
+  return (el >= 0 && el < E) ? el : -1;
+}
+
 // One CTA (1024 threads) per layer: route every token, count rows per local
 // expert, exclusive-scan the counts into row offsets, place each (token, slot)
 // pair.  Row order inside an expert is irrelevant to the result: every GEMM
 // output column depends only on its own activation row.
+template <int NC>
 __global__ void __launch_bounds__(1024, 1)
-    k_route_plan(uint64_t seed, int layer_first, int T, int L, int top_k, int e_first, int E,
+    k_route_plan(uint64_t seed, int layer_first, int T, int L, int top_k, int e_first, int E, int S,
                  int32_t* __restrict__ topk, int32_t* __restrict__ pos, int32_t* __restrict__ offsets,
                  const long long* __restrict__ fault) {
   __shared__ int cnt[kMaxExperts];
@@ -121,47 +156,163 @@ __global__ void __launch_bounds__(1024, 1)
   __shared__ int total;
   if (fault && *fault) return;
   const int li = blockIdx.x, layer = layer_first + li;
-  const int kk = min(top_k, L);
+  const int kk = min(top_k, L), kt = kk + S, G = E + S;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  int32_t* tk = topk + (long long)li * T * kk;
-  int32_t* ps = pos + (long long)li * T * kk;
-  int32_t* of = offsets + (long long)li * (E + 1);
-  for (int e = threadIdx.x; e < E; e += blockDim.x) cnt[e] = 0;
+  int32_t* tk = topk + (long long)li * T * kt;
+  int32_t* ps = pos + (long long)li * T * kt;
+  int32_t* of = offsets + (long long)li * (G + 1);
+  for (int e = threadIdx.x; e < G; e += blockDim.x) cnt[e] = 0;
   __syncthreads();
   for (int t = warp; t < T; t += nwarps) {
     int id, rank;
-    route_token(seed, layer, t, L, kk, lane, &id, &rank);
+    route_token<NC>(seed, layer, t, L, kk, lane, &id, &rank);
     if (lane < kk) {
-      tk[(long long)t * kk + rank] = id;
-      const int el = id - 1 - e_first;
-      if (el >= 0 && el < E) atomicAdd(&cnt[el], 1);
+      tk[(long long)t * kt + rank] = id;
+      const int el = local_group(id, L, e_first, E);
+      if (el >= 0) atomicAdd(&cnt[el], 1);
+    } else if (lane < kt) {
+      tk[(long long)t * kt + lane] = L + 1 + (lane - kk);  // shared expert: every token, after the routed
     }
   }
+  for (int e = threadIdx.x; e < S; e += blockDim.x) cnt[E + e] = T;
   __syncthreads();
   int carry = 0;
-  for (int e0 = 0; e0 < E; e0 += blockDim.x) {
+  for (int e0 = 0; e0 < G; e0 += blockDim.x) {
     const int e = e0 + threadIdx.x;
-    const int v = e < E ? cnt[e] : 0;
+    const int v = e < G ? cnt[e] : 0;
     const int ex = block_exclusive_scan(v, warp_tot, &total);
-    if (e < E) {
+    if (e < G) {
       of[e] = carry + ex;
       cnt[e] = carry + ex;  // becomes the placement cursor
     }
     carry += total;
     __syncthreads();
   }
-  if (threadIdx.x == 0) of[E] = carry;
+  if (threadIdx.x == 0) of[G] = carry;
   __syncthreads();
-  for (int p = threadIdx.x; p < T * kk; p += blockDim.x) {
-    const int el = tk[p] - 1 - e_first;
-    ps[p] = (el >= 0 && el < E) ? atomicAdd(&cnt[el], 1) : -1;
+  for (int p = threadIdx.x; p < T * kt; p += blockDim.x) {
+    const int el = local_group(tk[p], L, e_first, E);
+    ps[p] = el >= 0 ? atomicAdd(&cnt[el], 1) : -1;
+  }
+}
+
+// ---- multi-CTA plan (large T): route+count, then scan+place, for every layer at once.
+// cnt / cur: [layers][E] zeroed scratch.  Row order inside an expert comes from
+// atomics, which the result does not depend on (see k_route_plan).
+constexpr int kPlanTokensPerCta = 16;    // k_route_count: 8 warps x 2 tokens (spread over the SMs)
+constexpr int kPlanPairsPerCta = 4096;   // k_plan_place: (token, slot) pairs per CTA
+
+template <int NC>
+__global__ void __launch_bounds__(256)
+    k_route_count(uint64_t seed, int layer_first, int T, int L, int top_k, int e_first, int E, int S,
+                  int32_t* __restrict__ topk, int32_t* __restrict__ cnt, const long long* __restrict__ fault) {
+  __shared__ int lc[kMaxExperts];
+  if (fault && *fault) return;
+  const int li = blockIdx.y, layer = layer_first + li;
+  const int kk = min(top_k, L), kt = kk + S;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) lc[e] = 0;
+  __syncthreads();
+  int32_t* tk = topk + (long long)li * T * kt;
+  const int t0 = blockIdx.x * kPlanTokensPerCta, t1 = min(T, t0 + kPlanTokensPerCta);
+  for (int t = t0 + warp; t < t1; t += nwarps) {
+    int id, rank;
+    route_token<NC>(seed, layer, t, L, kk, lane, &id, &rank);
+    if (lane < kk) {
+      tk[(long long)t * kt + rank] = id;
+      const int el = local_group(id, L, e_first, E);
+      if (el >= 0) atomicAdd(&lc[el], 1);
+    } else if (lane < kt) {
+      tk[(long long)t * kt + lane] = L + 1 + (lane - kk);
+    }
+  }
+  __syncthreads();
+  int* gc = cnt + (long long)li * (E + S);
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    if (lc[e]) atomicAdd(&gc[e], lc[e]);
+  if (blockIdx.x == 0)
+    for (int e = threadIdx.x; e < S; e += blockDim.x) atomicAdd(&gc[E + e], T);
+}
+
+__global__ void __launch_bounds__(1024, 1)
+    k_plan_place(int T, int kt, int L, int e_first, int Er, int E, const int32_t* __restrict__ topk, int32_t* __restrict__ pos,
+                 int32_t* __restrict__ offsets, const int32_t* __restrict__ cnt, int32_t* __restrict__ cur,
+                 const long long* __restrict__ fault) {
+  __shared__ int off[kMaxExperts];
+  __shared__ int lc[kMaxExperts];
+  __shared__ int warp_tot[32];
+  __shared__ int total;
+  if (fault && *fault) return;
+  const int li = blockIdx.y;
+  const int32_t* gc = cnt + (long long)li * E;
+  int carry = 0;
+  for (int e0 = 0; e0 < E; e0 += blockDim.x) {
+    const int e = e0 + threadIdx.x;
+    const int v = e < E ? gc[e] : 0;
+    const int ex = block_exclusive_scan(v, warp_tot, &total);
+    if (e < E) {
+      off[e] = carry + ex;
+      lc[e] = 0;
+    }
+    carry += total;
+    __syncthreads();
+  }
+  int32_t* of = offsets + (long long)li * (E + 1);
+  if (blockIdx.x == 0) {
+    for (int e = threadIdx.x; e < E; e += blockDim.x) of[e] = off[e];
+    if (threadIdx.x == 0) of[E] = carry;
+  }
+  __syncthreads();
+  const int32_t* tk = topk + (long long)li * T * kt;
+  int32_t* ps = pos + (long long)li * T * kt;
+  const int p0 = blockIdx.x * kPlanPairsPerCta, p1 = min(T * kt, p0 + kPlanPairsPerCta);
+  constexpr int PER = kPlanPairsPerCta / 1024;
+  int el[PER], rk[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int p = p0 + i * 1024 + threadIdx.x;
+    el[i] = -1;
+    if (p < p1) {
+      const int x = local_group(tk[p], L, e_first, Er);
+      if (x >= 0) {
+        el[i] = x;
+        rk[i] = atomicAdd(&lc[x], 1);
+      }
+    }
+  }
+  __syncthreads();
+  int32_t* gcur = cur + (long long)li * E;
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    if (lc[e]) lc[e] = off[e] + atomicAdd(&gcur[e], lc[e]);  // this CTA's base row of expert e
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int p = p0 + i * 1024 + threadIdx.x;
+    if (p < p1) ps[p] = el[i] >= 0 ? lc[el[i]] + rk[i] : -1;
   }
 }
 
 void launch_route_plan(uint64_t seed, int layer_first, int layer_count, int T, int L, int top_k, int e_first, int E,
-                       int32_t* topk, int32_t* pos, int32_t* offsets, const long long* fault, cudaStream_t s) {
+                       int S, int32_t* topk, int32_t* pos, int32_t* offsets, int32_t* scratch,
+                       const long long* fault, cudaStream_t s) {
   if (layer_count <= 0) return;
-  k_route_plan<<<layer_count, 1024, 0, s>>>(seed, layer_first, T, L, top_k, e_first, E, topk, pos, offsets, fault);
+  const int kk = min(top_k, L), kt = kk + S, G = E + S;
+  const int nc = route_nc(L);
+  if ((long long)T * kt <= kPlanSingleCtaPairs || scratch == nullptr) {
+    XPGB_ROUTE_DISPATCH(nc, k_route_plan, layer_count, 1024, s, seed, layer_first, T, L, top_k, e_first, E, S, topk,
+                        pos, offsets, fault);
+    note_launch();
+    return;
+  }
+  int32_t* cnt = scratch;
+  int32_t* cur = scratch + (size_t)layer_count * G;
+  cudaMemsetAsync(scratch, 0, (size_t)2 * layer_count * G * sizeof(int32_t), s);
+  const dim3 g1((T + kPlanTokensPerCta - 1) / kPlanTokensPerCta, layer_count);
+  XPGB_ROUTE_DISPATCH(nc, k_route_count, g1, 256, s, seed, layer_first, T, L, top_k, e_first, E, S, topk, cnt,
+                      fault);
+  note_launch();
+  const dim3 g2((T * kt + kPlanPairsPerCta - 1) / kPlanPairsPerCta, layer_count);
+  k_plan_place<<<g2, 1024, 0, s>>>(T, kt, L, e_first, E, G, topk, pos, offsets, cnt, cur, fault);
   note_launch();
 }
 
@@ -205,8 +356,8 @@ void launch_gather(const float* x, const int32_t* pos, const long long* fault, _
 // accumulation mirrors `y += expert_output(...) * inv_k` (pipeline.py:206).
 // With next_pos, bf16(y_t) also lands in the next layer's expert-major rows.
 __global__ void k_combine(const float* __restrict__ part, const int32_t* __restrict__ pos,
-                          const long long* __restrict__ fault, float* __restrict__ y, int kk, int H, int splits,
-                          long long split_stride, float inv_k, const int32_t* __restrict__ next_pos,
+                          const long long* __restrict__ fault, float* __restrict__ y, int kk, int kr, int H,
+                          int splits, long long split_stride, float inv_k, const int32_t* __restrict__ next_pos,
                           __nv_bfloat16* __restrict__ xp) {
   if (*fault) return;
   const int t = blockIdx.x;
@@ -225,10 +376,11 @@ __global__ void k_combine(const float* __restrict__ part, const int32_t* __restr
         const float4 w = src[k * split_stride / 4];
         v.x = __fadd_rn(v.x, w.x); v.y = __fadd_rn(v.y, w.y); v.z = __fadd_rn(v.z, w.z); v.w = __fadd_rn(v.w, w.w);
       }
-      acc.x = __fadd_rn(acc.x, __fmul_rn(v.x, inv_k));
-      acc.y = __fadd_rn(acc.y, __fmul_rn(v.y, inv_k));
-      acc.z = __fadd_rn(acc.z, __fmul_rn(v.z, inv_k));
-      acc.w = __fadd_rn(acc.w, __fmul_rn(v.w, inv_k));
+      const float sc = s < kr ? inv_k : 1.0f;  // routed slots x 1/top_k, shared experts x 1
+      acc.x = __fadd_rn(acc.x, __fmul_rn(v.x, sc));
+      acc.y = __fadd_rn(acc.y, __fmul_rn(v.y, sc));
+      acc.z = __fadd_rn(acc.z, __fmul_rn(v.z, sc));
+      acc.w = __fadd_rn(acc.w, __fmul_rn(v.w, sc));
     }
     reinterpret_cast<float4*>(y + (size_t)t * H)[i] = acc;
     if (next_pos) {
@@ -239,12 +391,12 @@ __global__ void k_combine(const float* __restrict__ part, const int32_t* __restr
   }
 }
 
-void launch_combine(const float* part, const int32_t* pos, const long long* fault, float* y, int T, int kk, int H,
-                    int splits, long long split_stride, float inv_k, const int32_t* next_pos, __nv_bfloat16* xp,
-                    cudaStream_t s) {
+void launch_combine(const float* part, const int32_t* pos, const long long* fault, float* y, int T, int kk, int kr,
+                    int H, int splits, long long split_stride, float inv_k, const int32_t* next_pos,
+                    __nv_bfloat16* xp, cudaStream_t s) {
   if (T == 0) return;
   const int threads = min(256, max(32, H / 4));
-  k_combine<<<T, threads, 0, s>>>(part, pos, fault, y, kk, H, splits, split_stride, inv_k, next_pos, xp);
+  k_combine<<<T, threads, 0, s>>>(part, pos, fault, y, kk, kr, H, splits, split_stride, inv_k, next_pos, xp);
   note_launch();
 }
 
@@ -341,7 +493,8 @@ __device__ __forceinline__ Unit decode_unit(int u, const int* s_up, const int* s
 
 template <bool GU, int BN, int STAGES>
 __global__ void __launch_bounds__(192, 1)
-    k_moe_gemm(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_b, GemmParams p) {
+    k_moe_gemm(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_b,
+               const __grid_constant__ CUtensorMap map_ws, GemmParams p) {
   using C = GemmCfg<GU, BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
@@ -377,13 +530,17 @@ __global__ void __launch_bounds__(192, 1)
         const int n = s_off[e + 1] - s_off[e];
         if (n > 0) {
           u = ((n + BN - 1) / BN) * MT * S;
-          const int32_t ent = p.pt[e];
-          if (pt_state(ent) != 2) {
-            atomicCAS((unsigned long long*)p.fault, 0ull,
-                      (unsigned long long)fault_pack(p.layer, p.e_first + e + 1, GU ? 1 : 2, pt_state(ent)));
-            bad = true;
+          if (e < p.E_routed) {
+            const int32_t ent = p.pt[e];
+            if (pt_state(ent) != 2) {
+              atomicCAS((unsigned long long*)p.fault, 0ull,
+                        (unsigned long long)fault_pack(p.layer, p.e_first + e + 1, GU ? 1 : 2, pt_state(ent)));
+              bad = true;
+            }
+            s_slot[e] = pt_block0(ent);
+          } else {
+            s_slot[e] = p.shared_block0 + (e - p.E_routed);  // always-resident shared expert
           }
-          s_slot[e] = pt_block0(ent);
         }
       }
       int x = u;
@@ -404,6 +561,7 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_w);
     tma_prefetch_desc(&map_b);
+    if (p.E > p.E_routed) tma_prefetch_desc(&map_ws);
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
     fence_mbar_init();
@@ -428,13 +586,14 @@ __global__ void __launch_bounds__(192, 1)
         const int kb0 = GU ? 0 : un.split * KB / S, kb1 = GU ? KB : (un.split + 1) * KB / S;
         const int nb = (un.n_rows + kBoxRowsB - 1) / kBoxRowsB;
         const int wrow = s_slot[un.e] * rows_per_block + un.m0;
+        const CUtensorMap* mw = un.e < p.E_routed ? &map_w : &map_ws;
         const uint32_t bytes = C::NA * C::A_BYTES + nb * kBoxRowsB * kBK * 2;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE;
           mbar_arrive_expect_tx(&full[stage], bytes);
-          tma_load_2d(sa, &map_w, &full[stage], kb * kBK, wrow, pol_w);
-          if (GU) tma_load_2d(sa + C::A_BYTES, &map_w, &full[stage], kb * kBK, wrow + p.F, pol_w);
+          tma_load_2d(sa, mw, &full[stage], kb * kBK, wrow, pol_w);
+          if (GU) tma_load_2d(sa + C::A_BYTES, mw, &full[stage], kb * kBK, wrow + p.F, pol_w);
           uint8_t* sb = sa + C::NA * C::A_BYTES;
           for (int i = 0; i < nb; ++i)
             tma_load_2d(sb + i * kBoxRowsB * kBK * 2, &map_b, &full[stage], kb * kBK, un.row_begin + i * kBoxRowsB,
@@ -524,7 +683,7 @@ __global__ void __launch_bounds__(192, 1)
 
 // ---- instantiations / launchers
 
-using GemmKernel = void (*)(const CUtensorMap, const CUtensorMap, GemmParams);
+using GemmKernel = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, GemmParams);
 
 template <bool GU, int BN, int ST>
 static void set_attr() {
@@ -540,25 +699,25 @@ void set_gemm_attrs() {
   set_attr<false, 128, 6>();
 }
 
-void launch_gate_up(const CUtensorMap& map_w, const CUtensorMap& map_x, const GemmParams& p, int bn, int grid,
-                    cudaStream_t s) {
+void launch_gate_up(const CUtensorMap& map_w, const CUtensorMap& map_x, const CUtensorMap& map_ws,
+                    const GemmParams& p, int bn, int grid, cudaStream_t s) {
   GemmKernel kern;
   int smem;
   if (bn == 32) { kern = k_moe_gemm<true, 32, 5>; smem = GemmCfg<true, 32, 5>::SMEM; }
   else if (bn == 64) { kern = k_moe_gemm<true, 64, 4>; smem = GemmCfg<true, 64, 4>::SMEM; }
   else { kern = k_moe_gemm<true, 128, 4>; smem = GemmCfg<true, 128, 4>::SMEM; }
-  kern<<<grid, 192, smem, s>>>(map_w, map_x, p);
+  kern<<<grid, 192, smem, s>>>(map_w, map_x, map_ws, p);
   note_launch();
 }
 
-void launch_down(const CUtensorMap& map_w, const CUtensorMap& map_h, const GemmParams& p, int bn, int grid,
-                 cudaStream_t s) {
+void launch_down(const CUtensorMap& map_w, const CUtensorMap& map_h, const CUtensorMap& map_ws,
+                 const GemmParams& p, int bn, int grid, cudaStream_t s) {
   GemmKernel kern;
   int smem;
   if (bn == 32) { kern = k_moe_gemm<false, 32, 9>; smem = GemmCfg<false, 32, 9>::SMEM; }
   else if (bn == 64) { kern = k_moe_gemm<false, 64, 8>; smem = GemmCfg<false, 64, 8>::SMEM; }
   else { kern = k_moe_gemm<false, 128, 6>; smem = GemmCfg<false, 128, 6>::SMEM; }
-  kern<<<grid, 192, smem, s>>>(map_w, map_h, p);
+  kern<<<grid, 192, smem, s>>>(map_w, map_h, map_ws, p);
   note_launch();
 }
 

@@ -40,26 +40,36 @@ struct GemmParams {
   float* part;             // down output     [splits][rows][H] fp32
   long long split_stride;  // elements between split planes of `part`
   int layer, e_first, E, F, H, splits;
+  int E_routed;       // groups [0, E_routed) are paged experts (slot table); [E_routed, E) shared experts
+  int shared_block0;  // block of this layer's first shared expert in the shared-weights maps
 };
 
 // ---- launchers (moe_kernels.cu)
 void launch_route(uint64_t seed, int layer_first, int layer_count, int T, int L, int top_k, int32_t* out,
                   cudaStream_t s);
-// Route + count + scan + positions for `layer_count` layers (one CTA per layer).
+// Route + count + scan + positions for `layer_count` layers.  Up to kPlanSingleCtaPairs
+// (token, slot) pairs per layer: one fused CTA per layer; above: route+count over
+// token blocks, then scan+place over pair blocks (scratch: 2*layer_count*E int32).
 // Views for layer i live at topk/pos + i*T*kk and offsets + i*(E+1).
+constexpr int kPlanSingleCtaPairs = 128;
+// S shared experts per layer join every token after its routed slots (ids L+1..L+S,
+// groups E..E+S-1): plan rows are [T][kk+S], offsets [E+S+1].
 void launch_route_plan(uint64_t seed, int layer_first, int layer_count, int T, int L, int top_k, int e_first, int E,
-                       int32_t* topk, int32_t* pos, int32_t* offsets, const long long* fault, cudaStream_t s);
+                       int S, int32_t* topk, int32_t* pos, int32_t* offsets, int32_t* scratch,
+                       const long long* fault, cudaStream_t s);
 void launch_gather(const float* x, const int32_t* pos, const long long* fault, __nv_bfloat16* xp, int T, int kk,
                    int H, cudaStream_t s);
-void launch_gate_up(const CUtensorMap& map_w, const CUtensorMap& map_x, const GemmParams& p, int bn, int grid,
-                    cudaStream_t s);
-void launch_down(const CUtensorMap& map_w, const CUtensorMap& map_h, const GemmParams& p, int bn, int grid,
-                 cudaStream_t s);
-// y_t = ordered weighted sum of the token's expert rows; optionally also writes
-// bf16(y_t) to the next layer's expert-major rows (fused gather).
-void launch_combine(const float* part, const int32_t* pos, const long long* fault, float* y, int T, int kk, int H,
-                    int splits, long long split_stride, float inv_k, const int32_t* next_pos, __nv_bfloat16* xp,
-                    cudaStream_t s);
+// map_ws: the shared experts' weights (read for groups >= p.E_routed).
+void launch_gate_up(const CUtensorMap& map_w, const CUtensorMap& map_x, const CUtensorMap& map_ws,
+                    const GemmParams& p, int bn, int grid, cudaStream_t s);
+void launch_down(const CUtensorMap& map_w, const CUtensorMap& map_h, const CUtensorMap& map_ws,
+                 const GemmParams& p, int bn, int grid, cudaStream_t s);
+// y_t = ordered weighted sum of the token's kk expert rows (the first kr scaled by
+// inv_k, the rest -- shared experts -- by 1); optionally also writes bf16(y_t) to
+// the next layer's expert-major rows (fused gather).
+void launch_combine(const float* part, const int32_t* pos, const long long* fault, float* y, int T, int kk, int kr,
+                    int H, int splits, long long split_stride, float inv_k, const int32_t* next_pos,
+                    __nv_bfloat16* xp, cudaStream_t s);
 void launch_reduce_rows(const float* part, const long long* fault, float* out, int n_rows, int H, int splits,
                         long long split_stride, cudaStream_t s);
 void set_gemm_attrs();

@@ -172,6 +172,9 @@ struct Ctx {
   int device;
   int pool;
   int e_first = 0, E = 0;  // expert shard
+  int S = 0;               // shared (always-on, always-resident) experts per layer
+  uint8_t* shared_w = nullptr;  // [N*S] gate/up blocks, then [N*S] down blocks
+  CUtensorMap map_gu_sh{}, map_dn_sh{};
   uint64_t s1, s2;         // sigma per kind
   int num_sms = 148;
 
@@ -214,6 +217,7 @@ struct Ctx {
   int32_t* plan_topk[3] = {nullptr, nullptr, nullptr};  // [N][T][kk]
   int32_t* plan_pos[3] = {nullptr, nullptr, nullptr};   // [N][T][kk]
   int32_t* plan_off[3] = {nullptr, nullptr, nullptr};   // [N][E+1]
+  int32_t* plan_scr[3] = {nullptr, nullptr, nullptr};   // [2][N][E] multi-CTA plan counters
   __nv_bfloat16* xp = nullptr;  // [cap_rows][H]
   __nv_bfloat16* hbuf = nullptr;  // [cap_rows][F]
   float* part = nullptr;          // [cap_splits][cap_rows][H]
@@ -262,6 +266,10 @@ static int page_index(Ctx* c, int layer, int expert, int kind) {
           c->e_first + c->E);
   return (layer - 1) * c->E + el;
 }
+
+// Plan slots per token: routed min(top_k, L) + shared S.
+static int slots_of(Ctx* c, int top_k) { return std::min(top_k, c->L) + c->S; }
+static int groups_of(Ctx* c) { return c->E + c->S; }
 
 static std::string tid_str(int layer, int expert, int kind) { return fmt("L%dE%dK%d", layer, expert, kind); }
 
@@ -331,8 +339,8 @@ static void ensure_log(Ctx* c, int cap) {
 static void free_work(Ctx* c) {
   auto fr = [](void* p) { if (p) cudaFree(p); };
   for (int b = 0; b < 3; ++b) {
-    fr(c->plan_topk[b]); fr(c->plan_pos[b]); fr(c->plan_off[b]);
-    c->plan_topk[b] = c->plan_pos[b] = c->plan_off[b] = nullptr;
+    fr(c->plan_topk[b]); fr(c->plan_pos[b]); fr(c->plan_off[b]); fr(c->plan_scr[b]);
+    c->plan_topk[b] = c->plan_pos[b] = c->plan_off[b] = c->plan_scr[b] = nullptr;
   }
   fr(c->xp); fr(c->hbuf); fr(c->part); fr(c->ep_off);
   c->xp = c->hbuf = nullptr;
@@ -349,11 +357,12 @@ static void ensure_work(Ctx* c, int T, int kk) {
   CK(cudaDeviceSynchronize());
   free_work(c);
   const long long rows = (long long)nT * nkk;
-  const int E = c->E, N = c->N;
+  const int E = groups_of(c), N = c->N;
   for (int b = 0; b < 3; ++b) {
     CK(cudaMalloc(&c->plan_topk[b], (size_t)N * rows * 4));
     CK(cudaMalloc(&c->plan_pos[b], (size_t)N * rows * 4));
     CK(cudaMalloc(&c->plan_off[b], (size_t)N * (E + 1) * 4));
+    CK(cudaMalloc(&c->plan_scr[b], (size_t)2 * N * E * 4));
   }
   CK(cudaMalloc(&c->xp, (size_t)rows * c->H * 2));
   CK(cudaMemset(c->xp, 0, (size_t)rows * c->H * 2));
@@ -393,7 +402,8 @@ static void prof_rec(Ctx* c, int i, cudaStream_t s) {
   else if (c->prof) CK(cudaEventRecord(c->pev[i], s));
 }
 
-static GemmParams gemm_params(Ctx* c, int layer, int kind, const int32_t* offsets, int splits) {
+static GemmParams gemm_params(Ctx* c, int layer, int kind, const int32_t* offsets, int splits,
+                              bool with_shared = true) {
   GemmParams p;
   p.offsets = offsets;
   p.pt = c->d_pt + (size_t)(kind - 1) * c->N * c->E + (size_t)(layer - 1) * c->E;
@@ -403,7 +413,9 @@ static GemmParams gemm_params(Ctx* c, int layer, int kind, const int32_t* offset
   p.split_stride = (long long)c->cap_rows * c->H;
   p.layer = layer;
   p.e_first = c->e_first;
-  p.E = c->E;
+  p.E = with_shared ? groups_of(c) : c->E;
+  p.E_routed = c->E;
+  p.shared_block0 = (layer - 1) * c->S;
   p.F = c->F;
   p.H = c->H;
   p.splits = splits;
@@ -413,11 +425,11 @@ static GemmParams gemm_params(Ctx* c, int layer, int kind, const int32_t* offset
 // Plan (route + positions) layers [1, N] of one iteration into buffer b.
 static void enqueue_plan(Ctx* c, int b, int layer_first, int layer_count, int T, int top_k, uint64_t seed,
                          cudaStream_t s) {
-  const int kk = std::min(top_k, c->L);
+  const int kt = slots_of(c, top_k);
   const size_t lo = (size_t)(layer_first - 1);
-  launch_route_plan(seed, layer_first, layer_count, T, c->L, top_k, c->e_first, c->E,
-                    c->plan_topk[b] + lo * T * kk, c->plan_pos[b] + lo * T * kk, c->plan_off[b] + lo * (c->E + 1),
-                    c->d_fault, s);
+  launch_route_plan(seed, layer_first, layer_count, T, c->L, top_k, c->e_first, c->E, c->S,
+                    c->plan_topk[b] + lo * T * kt, c->plan_pos[b] + lo * T * kt,
+                    c->plan_off[b] + lo * (groups_of(c) + 1), c->plan_scr[b], c->d_fault, s);
   CKLAUNCH();
 }
 
@@ -426,26 +438,28 @@ static void enqueue_plan(Ctx* c, int b, int layer_first, int layer_count, int T,
 // next_pos: fuse the next layer's gather into this layer's combine.
 static void enqueue_forward(Ctx* c, int layer, const float* x, float* y, int T, int top_k, int b, bool gather,
                             const int32_t* next_pos, cudaStream_t s) {
-  const int kk = std::min(top_k, c->L);
+  const int kk = std::min(top_k, c->L), kt = slots_of(c, top_k);
   if (T == 0) return;
-  const int32_t* pos = c->plan_pos[b] + (size_t)(layer - 1) * T * kk;
-  const int32_t* off = c->plan_off[b] + (size_t)(layer - 1) * (c->E + 1);
+  const int32_t* pos = c->plan_pos[b] + (size_t)(layer - 1) * T * kt;
+  const int32_t* off = c->plan_off[b] + (size_t)(layer - 1) * (groups_of(c) + 1);
   const int bn = pick_bn(T);
-  const int splits = pick_splits(c, T, kk, bn);
+  const int splits = pick_splits(c, T, kt, bn);
   prof_rec(c, 1, s);
   if (gather) {
-    launch_gather(x, pos, c->d_fault, c->xp, T, kk, c->H, s);
+    launch_gather(x, pos, c->d_fault, c->xp, T, kt, c->H, s);
     CKLAUNCH();
   }
   prof_rec(c, 2, s);
   prof_rec(c, 3, s);
-  launch_gate_up(c->map_gu, c->map_xp, gemm_params(c, layer, 1, off, 1), bn, c->num_sms, s);
+  launch_gate_up(c->map_gu, c->map_xp, c->S ? c->map_gu_sh : c->map_gu, gemm_params(c, layer, 1, off, 1), bn,
+                 c->num_sms, s);
   CKLAUNCH();
   prof_rec(c, 4, s);
-  launch_down(c->map_dn, c->map_h, gemm_params(c, layer, 2, off, splits), bn, c->num_sms, s);
+  launch_down(c->map_dn, c->map_h, c->S ? c->map_dn_sh : c->map_dn, gemm_params(c, layer, 2, off, splits), bn,
+              c->num_sms, s);
   CKLAUNCH();
   prof_rec(c, 5, s);
-  launch_combine(c->part, pos, c->d_fault, y, T, kk, c->H, splits, (long long)c->cap_rows * c->H,
+  launch_combine(c->part, pos, c->d_fault, y, T, kt, kk, c->H, splits, (long long)c->cap_rows * c->H,
                  (float)(1.0 / top_k), next_pos, c->xp, s);
   CKLAUNCH();
   prof_rec(c, 6, s);
@@ -455,8 +469,7 @@ static void enqueue_forward(Ctx* c, int layer, const float* x, float* y, int T, 
 // Standalone layer_forward: plan this layer into buffer 2, then the chain.
 static void enqueue_layer(Ctx* c, int layer, const float* x, float* y, int T, int top_k, uint64_t seed,
                           cudaStream_t s) {
-  const int kk = std::min(top_k, c->L);
-  ensure_work(c, T, kk);
+  ensure_work(c, T, slots_of(c, top_k));
   if (T == 0) return;
   prof_rec(c, 0, s);
   enqueue_plan(c, 2, layer, 1, T, top_k, seed, s);
@@ -688,29 +701,78 @@ static void materialize(RunState& rs, int g, int it, int layer, int kind) {
     if (c->host_codec) CK(cudaStreamWaitEvent(c->s_alt[k], c->ev_mapped[k], 0));
     bool raw_on_s = false;
     int hb = 0;
-    for (int e = 0; e < E; ++e) {
-      if (is_pinned(layer, e)) continue;
-      const size_t pi = (size_t)(layer - 1) * E + e, ti = pi * 2 + k;
-      const uint64_t n = sigma_of(c, kind) / 2;
+    const uint64_t n = sigma_of(c, kind) / 2;
+    const uint64_t sm16 = (n + 15) & ~15ull;
+    auto tix = [&](int e) { return ((size_t)(layer - 1) * E + e) * 2 + k; };
+    auto rec_bytes = [&](int e) { return xpgb_codec_record_bytes(n, c->rec_bits[tix(e)], c->cchunk); };
+    // a staged run may take expert e' after e when its record follows e's in the pool
+    auto joins_run = [&](int e, int e2, int tier) {
+      return e2 < E && !is_pinned(layer, e2) && c->backend[tix(e2)] == tier && delay_of(e2) <= 0.f &&
+             (tier == 1 || c->rec_off[tix(e2)] == c->rec_off[tix(e)] + rec_bytes(e));
+    };
+    DecodeTensor dt[kMaxDecodeTensors];
+    for (int e = 0; e < E;) {
+      if (is_pinned(layer, e)) { ++e; continue; }
+      const size_t ti = tix(e);
       uint8_t* dst = block_ptr(c, kind, blocks[e]);
       const float dl = delay_of(e);
       if (c->backend[ti] == 1) {
+        // device tier: consecutive device-tier experts of the layer decode in one launch
         if (dl > 0) sleep_on(d, dl);
-        const uint8_t* rec = c->dev_tier + c->dev_off[ti];
-        const uint64_t nb = c->rec_bits[ti];
-        const uint64_t sm16 = (n + 15) & ~15ull, bits16 = (nb + 8 + 15) & ~15ull;
-        launch_exp_decode(rec, reinterpret_cast<const uint32_t*>(rec + sm16),
-                          reinterpret_cast<const uint32_t*>(rec + sm16 + bits16), n, c->cchunk, c->ctab,
-                          reinterpret_cast<uint16_t*>(dst), d);
+        int cnt = 0;
+        for (int e2 = e;; ++e2) {
+          const size_t t2 = tix(e2);
+          const uint8_t* rec = c->dev_tier + c->dev_off[t2];
+          const uint64_t bits16 = (c->rec_bits[t2] + 8 + 15) & ~15ull;
+          dt[cnt++] = DecodeTensor{rec, reinterpret_cast<const uint32_t*>(rec + sm16),
+                                   reinterpret_cast<const uint32_t*>(rec + sm16 + bits16),
+                                   reinterpret_cast<uint16_t*>(block_ptr(c, kind, blocks[e2])), 0u};
+          if (cnt == kMaxDecodeTensors || !joins_run(e2, e2 + 1, 1)) break;
+        }
+        launch_exp_decode_multi(dt, cnt, n, c->cchunk, c->ctab, d);
         CKLAUNCH();
-        rs.decoded += 2 * n;
+        rs.decoded += 2 * n * cnt;
+        e += cnt;
+      } else if (c->host_codec && rec_bytes(e) <= c->stage_cap[k]) {
+        // host tier, small records: a run of whole consecutive records in ONE copy and
+        // ONE decode launch (per-copy turnaround would otherwise dominate small experts)
+        if (dl > 0) sleep_on(s, dl);
+        uint64_t run = rec_bytes(e);
+        int cnt = 1;
+        while (cnt < kMaxDecodeTensors && joins_run(e + cnt - 1, e + cnt, 0) && run + rec_bytes(e + cnt) <= c->stage_cap[k]) {
+          run += rec_bytes(e + cnt);
+          ++cnt;
+        }
+        const uint64_t base = c->rec_off[ti];
+        const int lastx = e + cnt - 1;
+        // the last record's trailing chunk index stays home (it is device-resident)
+        const uint64_t bytes = c->rec_off[tix(lastx)] - base + sm16 + ((c->rec_bits[tix(lastx)] + 8 + 15) & ~15ull);
+        const int buf = hb++ & 1;
+        uint8_t* st = c->stage[k][buf];
+        cudaStream_t cs = buf ? c->s_alt[k] : s;
+        CK(cudaStreamWaitEvent(cs, c->ev_decoded[k][buf], 0));
+        CK(cudaMemcpyAsync(st, c->cpool + base, bytes, cudaMemcpyHostToDevice, cs));
+        CK(cudaEventRecord(c->ev_copied[k][buf], cs));
+        rs.h2d += bytes;
+        CK(cudaStreamWaitEvent(d, c->ev_copied[k][buf], 0));
+        for (int i = 0; i < cnt; ++i) {
+          const size_t t2 = tix(e + i);
+          uint8_t* rec = st + (c->rec_off[t2] - base);
+          dt[i] = DecodeTensor{rec, reinterpret_cast<const uint32_t*>(rec + sm16), c->d_index + c->d_index_off[t2],
+                               reinterpret_cast<uint16_t*>(block_ptr(c, kind, blocks[e + i])), 0u};
+        }
+        launch_exp_decode_multi(dt, cnt, n, c->cchunk, c->ctab, d);
+        CKLAUNCH();
+        CK(cudaEventRecord(c->ev_decoded[k][buf], d));
+        rs.decoded += 2 * n * cnt;
+        e += cnt;
       } else if (c->host_codec) {
         // stream the record in pieces of whole chunks (<= kStagePieceBytes) so the staging
         // buffers stay small: sm slice | stream slice (+8 B lookahead) | index slice
         const uint64_t nb = c->rec_bits[ti];
         const uint64_t ch = (uint64_t)c->cchunk;
         const uint64_t nc = (n + ch - 1) / ch;
-        const uint64_t sm16 = (n + 15) & ~15ull, bits16 = (nb + 8 + 15) & ~15ull;
+        const uint64_t bits16 = (nb + 8 + 15) & ~15ull;
         const uint8_t* rec = c->cpool + c->rec_off[ti];
         const uint32_t* idx = reinterpret_cast<const uint32_t*>(rec + sm16 + bits16);
         auto piece_bytes = [&](uint64_t a, uint64_t b) -> uint64_t {  // staged size of chunks [a, b)
@@ -750,11 +812,13 @@ static void materialize(RunState& rs, int g, int it, int layer, int kind) {
           CK(cudaEventRecord(c->ev_decoded[k][buf], d));
         }
         rs.decoded += 2 * n;
+        ++e;
       } else {
         if (dl > 0) sleep_on(s, dl);
         bool from_host = true;
         rs.h2d += fetch(c, layer, c->e_first + e + 1, kind, dst, sigma_of(c, kind), s, &from_host);
         raw_on_s = true;
+        ++e;
       }
     }
     if (raw_on_s) {
@@ -819,8 +883,7 @@ static void session_begin(Ctx* c, const xpgb_run_opts* o, float* acts) {
   if (o->compute_delay_s) ss.compute_delay.assign(o->compute_delay_s, o->compute_delay_s + (size_t)ss.steps);
   ss.o.fetch_delay_s = ss.fetch_delay.empty() ? nullptr : ss.fetch_delay.data();
   ss.o.compute_delay_s = ss.compute_delay.empty() ? nullptr : ss.compute_delay.data();
-  const int kk = std::min(o->top_k, c->L);
-  ensure_work(c, o->tokens, kk);
+  ensure_work(c, o->tokens, slots_of(c, o->top_k));
   ensure_log(c, ss.steps * 8 + 16);
   if (o->profile) {
     while (c->run_ev.size() < (size_t)ss.steps * 7) {
@@ -900,7 +963,7 @@ static void session_compute(Ctx* c, int g) {
   int it, layer;
   step_of(c, g, &it, &layer);
   cudaStream_t s = c->s_comp;
-  const int kk = std::min(o->top_k, c->L);
+  const int kt = slots_of(c, o->top_k);
   const int T = o->tokens;
   c->cur_ev = (o->profile && T > 0) ? &c->run_ev[(size_t)g * 7] : nullptr;
   prof_rec(c, 0, s);
@@ -913,7 +976,7 @@ static void session_compute(Ctx* c, int g) {
   const int b = (it - 1) & 1;
   const bool last = (g + 1 == ss.steps);
   const int32_t* next_pos = nullptr;
-  if (!last && T > 0) next_pos = layer < c->N ? c->plan_pos[b] + (size_t)layer * T * kk : c->plan_pos[it & 1];
+  if (!last && T > 0) next_pos = layer < c->N ? c->plan_pos[b] + (size_t)layer * T * kt : c->plan_pos[it & 1];
   enqueue_forward(c, layer, ss.rs.acts, ss.rs.acts, T, o->top_k, b, g == 0, next_pos, s);
   c->cur_ev = nullptr;
 }
@@ -926,7 +989,7 @@ static void session_end(Ctx* c, xpgb_report* rep) {
   RunState& rs = ss.rs;
   const int N = c->N;
   const int steps = ss.steps;
-  const int kk = std::min(o->top_k, c->L);
+  const int kk = std::min(o->top_k, c->L), kt = slots_of(c, o->top_k);
   const bool paged = ss.paged;
   cudaStream_t s = c->s_comp;
   CK(cudaEventRecord(c->ev_end, s));
@@ -986,18 +1049,19 @@ static void session_end(Ctx* c, xpgb_report* rep) {
 
   // routed experts per layer (routing is iteration-invariant) -> algorithmic bytes
   if (o->tokens > 0 && rs.acts) {
-    std::vector<int32_t> tk((size_t)N * o->tokens * kk);
+    std::vector<int32_t> tk((size_t)N * o->tokens * kt);
     CK(cudaMemcpy(tk.data(), c->plan_topk[0], tk.size() * 4, cudaMemcpyDeviceToHost));
     long long active = 0;
     for (int l = 0; l < N; ++l) {
-      std::vector<char> seen(c->L + 1, 0);
-      for (size_t i = 0; i < (size_t)o->tokens * kk; ++i) {
-        const int e = tk[(size_t)l * o->tokens * kk + i];
-        const int el = e - 1 - c->e_first;
+      std::vector<char> seen(c->L + c->S + 1, 0);
+      for (size_t i = 0; i < (size_t)o->tokens * kt; ++i) {
+        const int e = tk[(size_t)l * o->tokens * kt + i];
+        const int el = e > c->L ? 0 : e - 1 - c->e_first;  // shared experts are local on every shard
         if (el >= 0 && el < c->E && !seen[e]) { seen[e] = 1; ++active; }
       }
     }
-    const long long pairs = (long long)o->tokens * kk;
+    (void)kk;
+    const long long pairs = (long long)o->tokens * kt;
     rep->active_experts = (int32_t)active;
     rep->down_splits = c->last_splits;
     rep->gate_up_bytes = (long long)((double)active / N * c->s1) + pairs * c->H * 2 + pairs * c->F * 2;
@@ -1146,8 +1210,14 @@ static void set_codec(Ctx* c, const void* pool, uint64_t pool_bytes, const uint6
   for (int k = 0; k < 2; ++k) {
     uint64_t cap = 0;
     if (host_compressed) {
-      for (size_t ti = k; ti < nt; ti += 2)
-        cap = std::max(cap, xpgb_codec_record_bytes(((ti & 1) ? c->s2 : c->s1) / 2, c->rec_bits[ti], chunk));
+      // largest record, or a whole layer's records of this kind when they are small
+      uint64_t layer_sum = 0;
+      for (size_t ti = k; ti < nt; ti += 2) {
+        const uint64_t rb = xpgb_codec_record_bytes(((ti & 1) ? c->s2 : c->s1) / 2, c->rec_bits[ti], chunk);
+        if ((ti / 2) % c->E == 0) layer_sum = 0;
+        layer_sum += rb;
+        cap = std::max(cap, layer_sum);
+      }
       uint64_t piece = kStagePieceBytes;
       if (const char* env = getenv("XPGB_STAGE_BYTES")) piece = std::max<uint64_t>(4096, strtoull(env, nullptr, 10));
       cap = std::min(cap, piece) + 64 + (uint64_t)chunk * 8;
@@ -1253,6 +1323,8 @@ int xpgb_destroy(xpgb_ctx* h) {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     free_pools(c);
+    if (c->shared_w) cudaFree(c->shared_w);
+    c->shared_w = nullptr;
     free_work(c);
     void* ptrs[] = {c->d_fault, c->d_log, c->d_log_count};
     for (void* p : ptrs)
@@ -1531,8 +1603,8 @@ int xpgb_codec_encode(const void* data, uint64_t bytes, const uint8_t* lengths25
 }
 
 int xpgb_codec_pack(const void* payload, int32_t n_tensors, const uint64_t* value_counts, const uint8_t* lengths256,
-                    int32_t chunk, int32_t threads, void* out, uint64_t out_cap, uint64_t* pool_bytes,
-                    uint64_t* rec_offsets, uint64_t* bits_lens, uint64_t* bit_counts) {
+                    int32_t chunk, int32_t threads, const int32_t* place_order, void* out, uint64_t out_cap,
+                    uint64_t* pool_bytes, uint64_t* rec_offsets, uint64_t* bits_lens, uint64_t* bit_counts) {
   return guard([&] {
     if (chunk <= 0 || chunk % 8) XFAIL(XPGB_ERR_CONFIG, "codec chunk must be a positive multiple of 8");
     uint32_t codes[kCodecSymbols];
@@ -1565,8 +1637,17 @@ int xpgb_codec_pack(const void* payload, int32_t n_tensors, const uint64_t* valu
     for (int i = 0; i < n_tensors; ++i)
       if (bad[i] >= 0)
         XFAIL(XPGB_ERR_SYMBOL_NOT_IN_TABLE, "exponent bytes [%d] have no codeword; wrong table?", bad[i]);
+    if (place_order) {
+      std::vector<char> seen(n_tensors, 0);
+      for (int j = 0; j < n_tensors; ++j) {
+        const int i = place_order[j];
+        if (i < 0 || i >= n_tensors || seen[i]) XFAIL(XPGB_ERR_CONFIG, "place_order is not a permutation");
+        seen[i] = 1;
+      }
+    }
     uint64_t total = 0;
-    for (int i = 0; i < n_tensors; ++i) {
+    for (int j = 0; j < n_tensors; ++j) {
+      const int i = place_order ? place_order[j] : j;
       rec_offsets[i] = total;
       total += xpgb_codec_record_bytes(value_counts[i], bits_lens[i], chunk);
     }
@@ -1638,7 +1719,8 @@ int xpgb_set_codec(xpgb_ctx* h, const void* pool, uint64_t pool_bytes, const uin
 int xpgb_hbm_bytes(xpgb_ctx* h, uint64_t* ring, uint64_t* staging, uint64_t* device_tier) {
   return guard([&] {
     Ctx* c = &h->c;
-    *ring = (uint64_t)c->blocks * (c->s1 + c->s2);
+    // resident expert bytes: the ring arena (+ pinned blocks) and the shared experts
+    *ring = (uint64_t)c->blocks * (c->s1 + c->s2) + (uint64_t)c->N * c->S * (c->s1 + c->s2);
     *staging = 2 * (c->stage_cap[0] + c->stage_cap[1]);
     if (c->d_index) {
       uint64_t entries = 0;
@@ -1705,6 +1787,40 @@ int xpgb_set_pinned(xpgb_ctx* h, const uint8_t* pinned_of) {
       // staging buffers and device tier survive; re-stage the device tier into the new arena layout
     }
     stage_device_tier(c);
+  });
+}
+
+int xpgb_set_shared(xpgb_ctx* h, const void* host, uint64_t bytes, int32_t n_shared) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    if (c->sess && c->sess->active) XFAIL(XPGB_ERR, "cannot change shared experts during a session");
+    if (n_shared < 0 || c->E + n_shared > kMaxExperts)
+      XFAIL(XPGB_ERR_OUT_OF_RANGE, "shared experts %d outside [0, %d]", n_shared, kMaxExperts - c->E);
+    if (std::min(c->L, kMaxTopK) + n_shared > kMaxTopK)
+      XFAIL(XPGB_ERR_OUT_OF_RANGE, "top_k + shared experts above the kernel limit %d", kMaxTopK);
+    const uint64_t want = (uint64_t)c->N * n_shared * (c->s1 + c->s2);
+    if (n_shared && (!host || bytes != want))
+      XFAIL(XPGB_ERR_CONTAINER_FORMAT, "shared payload is %llu bytes, expected %llu", (unsigned long long)bytes,
+            (unsigned long long)want);
+    CK(cudaDeviceSynchronize());
+    if (c->shared_w) cudaFree(c->shared_w);
+    c->shared_w = nullptr;
+    c->S = n_shared;
+    c->cap_T = 0;  // plan rows and group counts change
+    ensure_work(c, 16, std::min(c->L, 8) + c->S);
+    if (!n_shared) return;
+    // device layout: every gate/up block, then every down block (one TMA map per kind)
+    const int nb = c->N * n_shared;
+    CK(cudaMalloc(&c->shared_w, want));
+    const uint8_t* src = static_cast<const uint8_t*>(host);
+    for (int b = 0; b < nb; ++b) {
+      CK(cudaMemcpy(c->shared_w + (uint64_t)b * c->s1, src + (uint64_t)b * (c->s1 + c->s2), c->s1,
+                    cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(c->shared_w + (uint64_t)nb * c->s1 + (uint64_t)b * c->s2, src + (uint64_t)b * (c->s1 + c->s2) + c->s1,
+                    c->s2, cudaMemcpyHostToDevice));
+    }
+    c->map_gu_sh = make_map(c->shared_w, (uint64_t)nb * 2 * c->F, c->H, kBM);
+    c->map_dn_sh = make_map(c->shared_w + (uint64_t)nb * c->s1, (uint64_t)nb * c->H, c->F, kBM);
   });
 }
 
@@ -1834,9 +1950,11 @@ int xpgb_experts_forward(xpgb_ctx* h, int32_t layer, const void* rows_dev, const
     CK(cudaMemcpyAsync(c->xp, rows_dev, (size_t)n_rows * c->H * 2, cudaMemcpyDeviceToDevice, s));
     const int bn = pick_bn(n_rows);
     const int splits = pick_splits(c, n_rows, 1, bn);
-    launch_gate_up(c->map_gu, c->map_xp, gemm_params(c, layer, 1, offsets_dev, 1), bn, c->num_sms, s);
+    launch_gate_up(c->map_gu, c->map_xp, c->map_gu, gemm_params(c, layer, 1, offsets_dev, 1, false), bn, c->num_sms,
+                   s);
     CKLAUNCH();
-    launch_down(c->map_dn, c->map_h, gemm_params(c, layer, 2, offsets_dev, splits), bn, c->num_sms, s);
+    launch_down(c->map_dn, c->map_h, c->map_dn, gemm_params(c, layer, 2, offsets_dev, splits, false), bn, c->num_sms,
+                s);
     CKLAUNCH();
     launch_reduce_rows(c->part, c->d_fault, out_dev, n_rows, c->H, splits, (long long)c->cap_rows * c->H, s);
     CKLAUNCH();
@@ -1853,7 +1971,7 @@ int xpgb_combine_rows(const float* rows_dev, const int32_t* index_dev, int32_t t
       CK(cudaMalloc(&zero, sizeof(long long)));
       CK(cudaMemset(zero, 0, sizeof(long long)));
     }
-    launch_combine(rows_dev, index_dev, zero, y_dev, tokens, kk, hidden, 1, 0, (float)(1.0 / top_k), nullptr,
+    launch_combine(rows_dev, index_dev, zero, y_dev, tokens, kk, kk, hidden, 1, 0, (float)(1.0 / top_k), nullptr,
                    nullptr, (cudaStream_t)stream);
     CKLAUNCH();
   });
@@ -1865,7 +1983,7 @@ int xpgb_profile_layer(xpgb_ctx* h, int32_t layer, const float* x_dev, float* y_
     Ctx* c = &h->c;
     cudaStream_t s = c->s_comp;
     xpgb_kernel_times acc{};
-    const int kk = std::min(top_k, c->L);
+    const int kt = slots_of(c, top_k);
     c->prof = true;
     for (int r = 0; r < std::max(1, reps); ++r) {
       enqueue_layer(c, layer, x_dev, y_dev, tokens, top_k, router_seed, s);
@@ -1882,19 +2000,20 @@ int xpgb_profile_layer(xpgb_ctx* h, int32_t layer, const float* x_dev, float* y_
     const double inv = 1.0 / std::max(1, reps);
     acc.route_ns *= inv; acc.plan_ns *= inv; acc.gather_ns *= inv;
     acc.gate_up_ns *= inv; acc.down_ns *= inv; acc.combine_ns *= inv;
-    std::vector<int32_t> offs(c->E + 1);
-    CK(cudaMemcpy(offs.data(), c->plan_off[2] + (size_t)(layer - 1) * (c->E + 1), (c->E + 1) * 4,
+    const int G = groups_of(c);
+    std::vector<int32_t> offs(G + 1);
+    CK(cudaMemcpy(offs.data(), c->plan_off[2] + (size_t)(layer - 1) * (G + 1), (G + 1) * 4,
                   cudaMemcpyDeviceToHost));
     long long active = 0, u1 = 0, u2 = 0;
     const int bn = pick_bn(tokens);
-    for (int e = 0; e < c->E; ++e) {
+    for (int e = 0; e < G; ++e) {
       const int n = offs[e + 1] - offs[e];
       if (n <= 0) continue;
       ++active;
       u1 += (long long)((n + bn - 1) / bn) * ((c->F + kBM - 1) / kBM);
       u2 += (long long)((n + bn - 1) / bn) * ((c->H + kBM - 1) / kBM) * c->last_splits;
     }
-    const long long pairs = (long long)tokens * kk;
+    const long long pairs = (long long)tokens * kt;
     acc.gate_up_bytes = active * (long long)c->s1 + pairs * c->H * 2 + pairs * c->F * 2;
     acc.down_bytes = active * (long long)c->s2 + pairs * c->F * 2 + pairs * c->H * 4 * c->last_splits;
     acc.n_units_gate_up = (int32_t)u1;

@@ -103,6 +103,15 @@ class Context:
         call("xpgb_set_expert_shard", self._h, first, count)
         self.expert_first, self.expert_count = first, count
 
+    def set_shared(self, shared) -> None:
+        """Attach a geometry.SharedExperts (or None to remove): always-on, always-resident experts."""
+        if shared is None:
+            call("xpgb_set_shared", self._h, None, C.c_uint64(0), 0)
+        else:
+            call("xpgb_set_shared", self._h, C.c_void_p(shared.pinned.data_ptr()), C.c_uint64(shared.total_bytes),
+                 int(shared.count))
+        self._shared_ref = shared
+
     def set_pinned(self, mask: np.ndarray) -> None:
         arr = np.ascontiguousarray(mask, dtype=np.uint8)
         call("xpgb_set_pinned", self._h, arr.ctypes.data_as(C.POINTER(C.c_uint8)))

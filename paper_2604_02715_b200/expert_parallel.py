@@ -227,7 +227,10 @@ class ExpertParallelRunner:
     def __init__(self, spec: ModelSpec, container, fwd: ForwardSpec, rank: int, world: int, device: int = 0,
                  group=None, shard_pool=None):
         from .device import Context
+        from .errors import ConfigError
 
+        if container is not None and getattr(container, "shared", None) is not None:
+            raise ConfigError("shared experts are not supported on the expert-parallel path yet")
         self.spec = spec
         self.fwd = fwd
         self.rank, self.world = rank, world

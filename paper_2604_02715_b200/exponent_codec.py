@@ -325,7 +325,12 @@ class CompressedModel:
         total = C.c_uint64()
         lengths = table.lengths_array()
         p64 = C.POINTER(C.c_uint64)
-        args = (C.c_void_p(words.ctypes.data), nt, counts.ctypes.data_as(p64), _u8p(lengths), chunk, _THREADS)
+        # records in (layer, kind, expert) order: a layer's records of one kind are contiguous,
+        # so the page-in stages runs of small records with one copy (offsets stay per tensor id)
+        order = np.array(sorted(range(nt), key=lambda i: (ids[i].layer, int(ids[i].kind), ids[i].expert)),
+                         dtype=np.int32)
+        args = (C.c_void_p(words.ctypes.data), nt, counts.ctypes.data_as(p64), _u8p(lengths), chunk, _THREADS,
+                order.ctypes.data_as(C.POINTER(C.c_int32)))
         call("xpgb_codec_pack", *args, None, C.c_uint64(0), C.byref(total), offs.ctypes.data_as(p64),
              blens.ctypes.data_as(p64), bcnt.ctypes.data_as(p64))
         pool = _pinned_bytes(int(total.value), pin)

@@ -211,6 +211,8 @@ class StreamedRunner:
         self.sabotage_skip_raw = sabotage_skip_raw
         self.ctx = Context(spec, _lib.POOL_RING, device, max_tokens=fwd.tokens_per_step)
         self.ctx.attach_host_pool(hierarchy.container.pinned)
+        if getattr(hierarchy.container, "shared", None) is not None:
+            self.ctx.set_shared(hierarchy.container.shared)
         placement = hierarchy.backend_map()
         cm = _codec_model(hierarchy, host_codec or bool(placement.any()))
         if cm is not None:
@@ -309,6 +311,8 @@ class ResidentModel:
         self.ctx = Context(spec, _lib.POOL_RESIDENT, device, max_tokens=max_tokens)
         self.ctx.attach_host_pool(container.pinned)
         self.ctx.make_resident()
+        if getattr(container, "shared", None) is not None:
+            self.ctx.set_shared(container.shared)
 
     def forward(self, layer: int, acts, fwd: ForwardSpec):
         torch = _torch()

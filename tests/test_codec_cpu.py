@@ -84,3 +84,16 @@ def test_chunk_index_rebuild_and_truncation():
     cut = replace(ct, exponent_bitstream=ct.exponent_bitstream[: len(ct.exponent_bitstream) // 4], chunk_index=b"")
     with pytest.raises(TruncatedStreamError):
         XC._record(cut, t)
+
+
+def test_compressed_pool_layer_kind_order():
+    """Records of one (layer, kind) are contiguous in the packed pool, experts ascending."""
+    import paper_2604_02715_b200 as X
+    from paper_2604_02715_b200.exponent_codec import CompressedModel
+
+    spec = X.ModelSpec(2, 5, 64, 128)
+    cm = CompressedModel.from_container(X.generate_synthetic_model(spec, 1), pin=False)
+    ids = list(X.iter_tensor_ids(spec))
+    order = sorted(range(len(ids)), key=lambda i: (ids[i].layer, int(ids[i].kind), ids[i].expert))
+    offs = [int(cm.rec_offsets[i]) for i in order]
+    assert offs == sorted(offs) and offs[0] == 0

@@ -111,3 +111,21 @@ def test_host_codec_small_staging_pieces(X, monkeypatch):
     base = X.resident_baseline(2, spec, container, fwd, acts=x.copy())
     assert rep.violations == [] and rep.page_fault is None
     assert rep.final_activations.tobytes() == base.tobytes()
+
+
+@pytest.mark.parametrize("alpha,host_codec,pinned", [(None, True, None), (None, True, 5), (1.0, False, None),
+                                                     (0.5, True, 3)])
+def test_grouped_record_runs_exact(X, alpha, host_codec, pinned):
+    """More experts than one multi-tensor decode launch holds (64): runs of consecutive
+    records split at the launch limit, at pinned experts and at the tier boundary."""
+    spec = X.ModelSpec(3, 80, 64, 128)
+    fwd = X.ForwardSpec(32, 4, 11)
+    container, hier = _runner(X, spec, 11, alpha, host_codec)
+    x = X.initial_activations(spec, fwd, 11)
+    rep = X.StreamedRunner(spec, hier, fwd, host_codec=host_codec, pinned=pinned).run(2, acts=x.copy())
+    base = X.resident_baseline(2, spec, container, fwd, acts=x.copy())
+    assert rep.violations == [] and rep.page_fault is None
+    assert rep.final_activations.tobytes() == base.tobytes()
+    iterations, streamed_experts = 2, spec.num_layers * (spec.experts_per_layer - (pinned or 0))
+    assert rep.decoded_bytes == iterations * streamed_experts * spec.expert_bytes  # every streamed tensor decoded
+

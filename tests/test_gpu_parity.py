@@ -294,3 +294,22 @@ def test_pinned_experts_budget_tier(X, pinned, host_codec):
     # a second run on the same context still finds its pinned experts resident
     rep2 = runner.run(1, acts=x.copy())
     assert rep2.page_fault is None and rep2.violations == []
+
+
+@pytest.mark.parametrize("L,k,T", [(8, 2, 1500), (128, 8, 300), (64, 4, 4097), (3, 5, 700)])
+def test_multi_cta_plan_layer_forward_vs_oracle(X, O, L, k, T):
+    """T*k above the single-CTA plan threshold: route+count / scan+place over many CTAs.
+    Layer output within tolerance of the oracle, and the resident run of the same step
+    (all layers planned at once) bit-identical to layer_forward."""
+    spec = X.ModelSpec(2, L, 64, 128)
+    container = X.generate_synthetic_model(spec, 5)
+    pool = O.WordPool(2, L, 64, 128, container.words)
+    x = np.random.default_rng(T).standard_normal((T, 64), dtype=np.float32)
+    fwd = X.ForwardSpec(T, k, 9)
+    y1 = X.layer_forward(container.tensor_f32, spec, fwd, 1, x)
+    assert O.rel_l2(y1, O.layer_forward(pool, 1, x, k, 9)) <= TOL
+    y2 = X.layer_forward(container.tensor_f32, spec, fwd, 2, y1)
+    # resident run of the same step (both layers planned at once, fused next-layer gather)
+    model = X.ResidentModel(spec, container, max_tokens=T)
+    out, _ = model.run(1, fwd, x.copy())
+    assert np.asarray(out).tobytes() == np.asarray(y2).tobytes()

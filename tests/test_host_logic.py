@@ -152,3 +152,21 @@ def test_storage_fetch_host_dest():
     with pytest.raises(X.BackendMissError):
         h.fetch(tid, memoryview(bytearray(3)))
     assert h.backend_map().sum() == 0
+
+
+def test_shared_experts_continue_the_generator_stream():
+    """Routed payload unchanged by shared experts; shared words = the stream continued."""
+    import numpy as np
+
+    import paper_2604_02715_b200 as X
+    from oracle import xpg_oracle as O
+
+    spec = X.ModelSpec(2, 3, 16, 32)
+    plain = X.generate_synthetic_model(spec, 9, pin=False)
+    c = X.generate_synthetic_model(spec, 9, pin=False, shared_experts=2, chunk_values=100)
+    assert np.array_equal(plain.words, c.words)
+    n_routed, n_shared = plain.words.size, c.shared.words.size
+    stream = O.f32_to_bf16(np.random.default_rng(9).standard_normal(n_routed + n_shared, dtype=np.float32)
+                           * O.WEIGHT_STD)
+    assert np.array_equal(stream[n_routed:], c.shared.words)
+    assert c.shared.tensor_f32(2, 2, X.TensorKind.DOWN).shape == (16, 32)
