@@ -35,8 +35,14 @@ CONFIGS = {
                   name="Qwen3-30B-A3B-shaped MoE stack (8 of 48 layers, 128 experts, top-8, hidden 2048, ffn 768)"),
     "tiny": dict(N=4, L=8, H=256, F=512, k=2, T=256,
                  name="tiny synthetic MoE (4 layers, 8 experts, top-2, hidden 256, ffn 512)"),
+    # one GPU = rank 0 of 8-way expert parallelism: its 32-expert shard + the replicated shared
+    # expert, routing the 8 x 256 global tokens (the all-to-all has no peer on one GPU)
+    "dsv3": dict(N=8, L=256, H=7168, F=2048, k=8, T=256, S=1, ep_virtual=8,
+                 name="DeepSeek-V3-shaped MoE layers (8 layers, 256 routed + 1 shared expert, top-8, hidden 7168, "
+                      "ffn 2048), rank 0 of 8-way expert parallelism on one B200"),
 }
 METRIC = "MoE decode tokens/sec at fixed expert-HBM budget (25%); page-in GB/s; exposed xfer %"
+METRIC_PREFILL = "MoE prefill tokens/sec at fixed expert-HBM budget (25%); page-in GB/s; exposed xfer %"
 SEED = 7
 
 
@@ -149,9 +155,30 @@ def barrier(world: int):
         dist.barrier()
 
 
-def cpu_baseline(cfg, words, sample_tokens: int):
+def cpu_baseline(cfg, words, sample_tokens: int, container=None):
     from oracle import cpu_reference  # checker / baseline only
 
+    if cfg.get("ep_virtual"):
+        # the reference has no expert parallelism: one process pages the whole model; the
+        # sample's experts are drawn from this rank's shard payload (same distribution)
+        from paper_2604_02715_b200.geometry import ExpertTensorId, TensorKind
+
+        cnt = container.spec.experts_per_layer
+        tw = lambda layer, e, kind: container.tensor_words(ExpertTensorId(layer, (e - 1) % cnt + 1, TensorKind(kind)))
+        sw = None
+        if container.shared is not None:
+            sw = lambda kind: container.shared.words[container.shared.offset(1, 1, kind) // 2:][
+                :container.spec.value_count(kind)]
+        r = cpu_reference.decode_rate_sampled(tw, cfg["N"], cfg["L"], cfg["H"], cfg["F"], cfg["T"], cfg["k"], SEED,
+                                              sample_tokens, shared_words=sw)
+        return {
+            "value": r["tok_s"], "unit": "tokens/s", "cores": r["threads"], "kind": "port",
+            "sample": (f"oracle/cpu_reference.py decode_rate_sampled: reference single-process path over the whole "
+                       f"model (no expert parallelism in the reference): page-in of the {r['fetched_experts']} experts "
+                       f"{sample_tokens} tokens route to, scaled to {cfg['L']} ({r['fetch_s']:.2f}s/layer), per-token "
+                       f"forward incl. shared expert ({r['compute_s']:.2f}s), extrapolated to {cfg['N']} layers x "
+                       f"T={cfg['T']}"),
+        }
     r = cpu_reference.decode_rate(words, cfg["N"], cfg["L"], cfg["H"], cfg["F"], cfg["T"], cfg["k"], SEED,
                                   sample_tokens)
     return {
@@ -188,7 +215,7 @@ def run_reference_arm(args, cfg):
             rates.append(r["tok_s"])
     value = cfg["T"] * len(times) / sum(times)
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "impl": "reference", "metric": METRIC_PREFILL if args.prefill else METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (reference generator, seed 7)",
@@ -216,6 +243,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="mixtral", choices=sorted(CONFIGS))
     ap.add_argument("--tokens", type=int, default=None)
+    ap.add_argument("--prefill", action="store_true",
+                    help="prefill regime: one step = a T-token prompt chunk through every layer (default T=8192)")
     ap.add_argument("--cpu-sample-tokens", type=int, default=4)
     ap.add_argument("--ref-sample-tokens", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -226,6 +255,8 @@ def main():
     args = ap.parse_args()
     args.host_codec = not args.raw
     cfg = dict(CONFIGS[args.config])
+    if args.prefill and not args.tokens:
+        args.tokens = 8192
     if args.tokens:
         cfg["T"] = args.tokens
     if args.impl == "reference":
@@ -242,8 +273,19 @@ def main():
     torch.cuda.set_device(local)
     dev = local
     N, L, H, F, k, T = cfg["N"], cfg["L"], cfg["H"], cfg["F"], cfg["k"], cfg["T"]
+    S = cfg.get("S", 0)
     spec = X.ModelSpec(N, L, H, F)
-    fwd = X.ForwardSpec(T, k, SEED)
+    G_virt = cfg.get("ep_virtual", 1) if world == 1 and not args.ep else 1
+    T_run = G_virt * T  # rows the step routes (an EP rank routes the global batch)
+    fwd = X.ForwardSpec(T_run, k, SEED)
+    run_kw = {}
+    cspec = spec
+    if G_virt > 1:
+        from paper_2604_02715_b200.expert_parallel import shard_bounds
+
+        first, count = shard_bounds(L, G_virt)[0]
+        cspec = X.ModelSpec(N, count, H, F)  # this rank's shard payload
+        run_kw = {"expert_shard": (first, count), "shared_tokens": (0, T)}
     t0 = time.time()
     use_ep = world > 1 or args.ep
     if use_ep:
@@ -254,7 +296,7 @@ def main():
         shard = X.generate_fast_model(X.ModelSpec(N, count, H, F), SEED + 1000 * rank, device=dev)
         container = None
     else:
-        container = X.generate_fast_model(spec, SEED + rank, device=dev)
+        container = X.generate_fast_model(cspec, SEED + rank, device=dev, shared_experts=S)
     gen_s = time.time() - t0
     log(f"model generated in {gen_s:.1f}s")
     if use_ep:
@@ -263,11 +305,11 @@ def main():
         budget = 2.0 / N  # 2-layer ring of this rank's shard
     else:
         backends = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 55e9, 1 << 50)]
-        hier = X.StorageHierarchy(container, None, X.plan_placement(spec, backends), backends)
+        hier = X.StorageHierarchy(container, None, X.plan_placement(cspec, backends), backends)
         raw_path = None
         if args.host_codec:
             # the reference host tier (raw bf16 over PCIe) on the same weights, for comparison
-            raw_runner = X.StreamedRunner(spec, hier, fwd, mode="threaded", device=dev)
+            raw_runner = X.StreamedRunner(spec, hier, fwd, mode="threaded", device=dev, **run_kw)
             xr = torch.from_numpy(X.initial_activations(spec, fwd, SEED + rank)).to(f"cuda:{dev}")
             raw_runner.run(max(1, args.warmup - 1), acts=xr)
             torch.cuda.synchronize()
@@ -289,9 +331,10 @@ def main():
             hier.compressed = CompressedModel.from_container(container)
             log(f"packed compressed host pool: ratio {hier.compressed.ratio:.4f} "
                 f"({hier.compressed.wire_bytes / 1e9:.2f} GB) in {time.time() - t1:.1f}s")
-        runner = X.StreamedRunner(spec, hier, fwd, mode="threaded", device=dev, host_codec=args.host_codec)
+        runner = X.StreamedRunner(spec, hier, fwd, mode="threaded", device=dev, host_codec=args.host_codec, **run_kw)
         hbm = runner.ctx.hbm_bytes()
-        budget = (hbm["ring"] + hbm["staging"] + hbm["device_tier"]) / spec.total_bytes
+        expert_bytes = cspec.total_bytes + (container.shared.total_bytes if container.shared is not None else 0)
+        budget = (hbm["ring"] + hbm["staging"] + hbm["device_tier"]) / expert_bytes
     x_host = X.initial_activations(spec, fwd, SEED + rank)
     x_dev = torch.from_numpy(x_host).to(f"cuda:{dev}")
 
@@ -341,7 +384,7 @@ def main():
     kern = rep.kernels
     if not args.no_resident and not use_ep:
         del runner
-        model = X.ResidentModel(spec, container, device=dev, max_tokens=T)
+        model = X.ResidentModel(spec, container, device=dev, max_tokens=T_run, **run_kw)
         model.run(args.warmup, fwd, x_dev)
         torch.cuda.synchronize()
         r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -366,7 +409,7 @@ def main():
     dn_ach = kern["down_bytes"] / (kern["down_ns"] * 1e-9) / 1e9 if kern.get("down_ns") else 0.0
 
     line = {
-        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "metric": METRIC_PREFILL if args.prefill else METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init N(0,0.02) bf16 weights drawn on-GPU, N(0,1) activations)",
@@ -375,13 +418,13 @@ def main():
                    "placement": "2-layer ring, host-only (alpha=0)" + (
                        ", exponent-Huffman records over PCIe decoded on-GPU into the ring (lossless)"
                        if args.host_codec else ""),
-                   "l2": "inputs larger than L2: all %.1f GB of expert weights stream from host each step" % (spec.total_bytes / 1e9)},
+                   "l2": "inputs larger than L2: all %.1f GB of expert weights stream from host each step" % (cspec.total_bytes / 1e9)},
         "page_in": {"achieved_gbps": page_in_gbps, "peak_gbps": h2d_peak, "frac": page_in_gbps / h2d_peak if h2d_peak else None,
                     "bytes_per_step": rep.h2d_bytes / args.steps, "peak_how": "pinned 1 GiB cudaMemcpyAsync H2D, best of 5, this box",
                     "host_codec": bool(args.host_codec),
-                    "raw_bytes_per_step": spec.total_bytes if not use_ep else None,
+                    "raw_bytes_per_step": cspec.total_bytes if not use_ep else None,
                     "decoded_bytes_per_step": rep.decoded_bytes / args.steps,
-                    "effective_raw_gbps": (spec.total_bytes * args.steps / rep.elapsed_seconds / 1e9) if not use_ep else None},
+                    "effective_raw_gbps": (cspec.total_bytes * args.steps / rep.elapsed_seconds / 1e9) if not use_ep else None},
         "exposed_xfer_pct": 100.0 * exposed,
         "war_wait_ms": rep.war_wait_seconds * 1e3,
         "roofline": {"bound": "hbm", "kernel": "k_gate_up (tcgen05 grouped SwiGLU GEMM, resident run)",
@@ -406,12 +449,20 @@ def main():
     if use_ep:
         line["config"]["parallelism"] = f"ep{world} (experts sharded, NCCL all_to_all dispatch/combine)"
         line["config"]["tokens_per_rank"] = T
+    if G_virt > 1:
+        line["config"]["parallelism"] = (f"rank 0 of ep{G_virt}: experts {run_kw['expert_shard'][0] + 1}.."
+                                         f"{sum(run_kw['expert_shard'])} of {L} paged on this GPU, shared expert "
+                                         f"replicated; routes the {T_run}-token global batch, applies the shared "
+                                         f"expert to its own {T} tokens; all-to-all not timed (no peer on one GPU)")
+        line["config"]["global_tokens_routed"] = T_run
+    if S:
+        line["config"]["shared_experts"] = S
     if rank == 0 and world == 1 and not args.no_cpu_baseline and container is not None:
         os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count() or 1))
         import numpy as np  # noqa: F811
 
-        words = container.words[: spec.layer_bytes // 2]
-        line["cpu_baseline"] = cpu_baseline(cfg, words, args.cpu_sample_tokens)
+        words = container.words[: cspec.layer_bytes // 2]
+        line["cpu_baseline"] = cpu_baseline(cfg, words, args.cpu_sample_tokens, container)
     log("cpu baseline done")
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -224,6 +224,10 @@ int xpgb_set_pinned(xpgb_ctx* ctx, const uint8_t* pinned_of);
  * bytes in (layer, shared expert, kind) order; they stay resident in HBM and are never paged.
  * n_shared = 0 removes them.  Single-device contexts only (not the expert-parallel path). */
 int xpgb_set_shared(xpgb_ctx* ctx, const void* host, uint64_t bytes, int32_t n_shared);
+/* Step rows [first, first+count) pass through the shared experts (count < 0: every row, the
+ * default).  An expert-parallel rank that also plans the other ranks' rows (global batch)
+ * applies its replica of the shared experts to its own rows only. */
+int xpgb_set_shared_tokens(xpgb_ctx* ctx, int32_t first, int32_t count);
 /* Expert-weight HBM footprint of a context: ring/pool blocks (+ shared experts), codec
  * staging, device tier. */
 int xpgb_hbm_bytes(xpgb_ctx* ctx, uint64_t* ring, uint64_t* staging, uint64_t* device_tier);

@@ -77,3 +77,39 @@ def decode_rate(words: np.ndarray, N: int, L: int, H: int, F: int, T: int, top_k
         "step_s": step,
         "threads": int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1)),
     }
+
+
+def decode_rate_sampled(tensor_words, N: int, L: int, H: int, F: int, T: int, top_k: int, seed: int,
+                        sample_tokens: int, layer: int = 1, shared_words=None):
+    """decode_rate for models too large to hold a layer on the host: the page-in of the
+    experts the sample routes to is timed and scaled to all L experts of the layer.
+    tensor_words(layer, expert, kind) -> uint16 words; shared_words(kind) -> the layer's
+    shared expert (added with weight 1, our convention) or None."""
+    x = np.random.default_rng(seed).standard_normal((sample_tokens, H), dtype=np.float32)
+    routes = O.route(seed, sample_tokens, layer, L, top_k)
+    need = sorted({int(j) for j in routes.reshape(-1)})
+    s1, s2 = O.sigma(H, F, 1) // 2, O.sigma(H, F, 2) // 2
+    t0 = time.perf_counter()
+    arena = {}
+    for j in need:
+        arena[j] = (np.array(tensor_words(layer, j, 1), copy=True), np.array(tensor_words(layer, j, 2), copy=True))
+    t1 = time.perf_counter()
+    inv_k = np.float32(1.0 / top_k)
+    with np.errstate(over="ignore"):
+        for t in range(sample_tokens):
+            y = np.zeros(H, dtype=np.float32)
+            for j in routes[t]:
+                gu = O.bf16_to_f32(arena[int(j)][0].copy()).reshape(2 * F, H)
+                dn = O.bf16_to_f32(arena[int(j)][1].copy()).reshape(H, F)
+                y += (dn @ (_silu(gu[:F] @ x[t]) * (gu[F:] @ x[t]))) * inv_k
+            if shared_words is not None:
+                gu = O.bf16_to_f32(np.asarray(shared_words(1))).reshape(2 * F, H)
+                dn = O.bf16_to_f32(np.asarray(shared_words(2))).reshape(H, F)
+                y += dn @ (_silu(gu[:F] @ x[t]) * (gu[F:] @ x[t]))
+    t2 = time.perf_counter()
+    t_fetch = (t1 - t0) * L / max(1, len(need))
+    per_token = (t2 - t1) / max(sample_tokens, 1)
+    step = N * (t_fetch + T * per_token)
+    return {"tok_s": T / step, "fetch_s": t_fetch, "compute_s": t2 - t1, "per_token_s": per_token, "step_s": step,
+            "threads": int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1)),
+            "fetched_experts": len(need)}

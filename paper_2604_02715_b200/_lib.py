@@ -109,6 +109,7 @@ _SIGS = {
     "xpgb_log_get": [_P, C.POINTER(Record), _I, C.POINTER(_I)],
     "xpgb_set_expert_shard": [_P, _I, _I],
     "xpgb_set_shared": [_P, _P, _U64, _I],
+    "xpgb_set_shared_tokens": [_P, _I, _I],
     "xpgb_experts_forward": [_P, _I, _P, _P, _I, _P, _P],
     "xpgb_combine_rows": [_P, _P, _I, _I, _I, _I, _P, _P],
     "xpgb_codec_histogram": [_P, _U64, C.POINTER(_U64), _I],

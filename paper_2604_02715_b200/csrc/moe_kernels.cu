@@ -137,6 +137,7 @@ __device__ int block_exclusive_scan(int v, int* warp_tot, int* total) {
 // Local GEMM group of a plan id: routed ids 1..L map onto this shard's experts
 // [0, E) (or -1 off-shard); shared ids L+1..L+S onto groups E..E+S-1.
 __device__ __forceinline__ int local_group(int id, int L, int e_first, int E) {
+  if (id < 1) return -1;
   if (id > L) return E + (id - L - 1);
   const int el = id - 1 - e_first;
   return (el >= 0 && el < E) ? el : -1;
@@ -148,8 +149,8 @@ __device__ __forceinline__ int local_group(int id, int L, int e_first, int E) {
 // output column depends only on its own activation row.
 template <int NC>
 __global__ void __launch_bounds__(1024, 1)
-    k_route_plan(uint64_t seed, int layer_first, int T, int L, int top_k, int e_first, int E, int S,
-                 int32_t* __restrict__ topk, int32_t* __restrict__ pos, int32_t* __restrict__ offsets,
+    k_route_plan(uint64_t seed, int layer_first, int T, int L, int top_k, int e_first, int E, int S, int sh0,
+                 int sh1, int32_t* __restrict__ topk, int32_t* __restrict__ pos, int32_t* __restrict__ offsets,
                  const long long* __restrict__ fault) {
   __shared__ int cnt[kMaxExperts];
   __shared__ int warp_tot[32];
@@ -171,10 +172,11 @@ __global__ void __launch_bounds__(1024, 1)
       const int el = local_group(id, L, e_first, E);
       if (el >= 0) atomicAdd(&cnt[el], 1);
     } else if (lane < kt) {
-      tk[(long long)t * kt + lane] = L + 1 + (lane - kk);  // shared expert: every token, after the routed
+      // shared expert: every token of [sh0, sh1) after its routed slots (0 = not here)
+      tk[(long long)t * kt + lane] = (t >= sh0 && t < sh1) ? L + 1 + (lane - kk) : 0;
     }
   }
-  for (int e = threadIdx.x; e < S; e += blockDim.x) cnt[E + e] = T;
+  for (int e = threadIdx.x; e < S; e += blockDim.x) cnt[E + e] = max(0, min(T, sh1) - sh0);
   __syncthreads();
   int carry = 0;
   for (int e0 = 0; e0 < G; e0 += blockDim.x) {
@@ -204,8 +206,8 @@ constexpr int kPlanPairsPerCta = 4096;   // k_plan_place: (token, slot) pairs pe
 
 template <int NC>
 __global__ void __launch_bounds__(256)
-    k_route_count(uint64_t seed, int layer_first, int T, int L, int top_k, int e_first, int E, int S,
-                  int32_t* __restrict__ topk, int32_t* __restrict__ cnt, const long long* __restrict__ fault) {
+    k_route_count(uint64_t seed, int layer_first, int T, int L, int top_k, int e_first, int E, int S, int sh0,
+                  int sh1, int32_t* __restrict__ topk, int32_t* __restrict__ cnt, const long long* __restrict__ fault) {
   __shared__ int lc[kMaxExperts];
   if (fault && *fault) return;
   const int li = blockIdx.y, layer = layer_first + li;
@@ -223,7 +225,7 @@ __global__ void __launch_bounds__(256)
       const int el = local_group(id, L, e_first, E);
       if (el >= 0) atomicAdd(&lc[el], 1);
     } else if (lane < kt) {
-      tk[(long long)t * kt + lane] = L + 1 + (lane - kk);
+      tk[(long long)t * kt + lane] = (t >= sh0 && t < sh1) ? L + 1 + (lane - kk) : 0;
     }
   }
   __syncthreads();
@@ -231,7 +233,7 @@ __global__ void __launch_bounds__(256)
   for (int e = threadIdx.x; e < E; e += blockDim.x)
     if (lc[e]) atomicAdd(&gc[e], lc[e]);
   if (blockIdx.x == 0)
-    for (int e = threadIdx.x; e < S; e += blockDim.x) atomicAdd(&gc[E + e], T);
+    for (int e = threadIdx.x; e < S; e += blockDim.x) atomicAdd(&gc[E + e], max(0, min(T, sh1) - sh0));
 }
 
 __global__ void __launch_bounds__(1024, 1)
@@ -293,13 +295,14 @@ __global__ void __launch_bounds__(1024, 1)
 }
 
 void launch_route_plan(uint64_t seed, int layer_first, int layer_count, int T, int L, int top_k, int e_first, int E,
-                       int S, int32_t* topk, int32_t* pos, int32_t* offsets, int32_t* scratch,
+                       int S, int sh0, int sh1, int32_t* topk, int32_t* pos, int32_t* offsets, int32_t* scratch,
                        const long long* fault, cudaStream_t s) {
   if (layer_count <= 0) return;
+  sh0 = max(0, sh0);
   const int kk = min(top_k, L), kt = kk + S, G = E + S;
   const int nc = route_nc(L);
   if ((long long)T * kt <= kPlanSingleCtaPairs || scratch == nullptr) {
-    XPGB_ROUTE_DISPATCH(nc, k_route_plan, layer_count, 1024, s, seed, layer_first, T, L, top_k, e_first, E, S, topk,
+    XPGB_ROUTE_DISPATCH(nc, k_route_plan, layer_count, 1024, s, seed, layer_first, T, L, top_k, e_first, E, S, sh0, sh1, topk,
                         pos, offsets, fault);
     note_launch();
     return;
@@ -308,7 +311,7 @@ void launch_route_plan(uint64_t seed, int layer_first, int layer_count, int T, i
   int32_t* cur = scratch + (size_t)layer_count * G;
   cudaMemsetAsync(scratch, 0, (size_t)2 * layer_count * G * sizeof(int32_t), s);
   const dim3 g1((T + kPlanTokensPerCta - 1) / kPlanTokensPerCta, layer_count);
-  XPGB_ROUTE_DISPATCH(nc, k_route_count, g1, 256, s, seed, layer_first, T, L, top_k, e_first, E, S, topk, cnt,
+  XPGB_ROUTE_DISPATCH(nc, k_route_count, g1, 256, s, seed, layer_first, T, L, top_k, e_first, E, S, sh0, sh1, topk, cnt,
                       fault);
   note_launch();
   const dim3 g2((T * kt + kPlanPairsPerCta - 1) / kPlanPairsPerCta, layer_count);

@@ -52,10 +52,11 @@ void launch_route(uint64_t seed, int layer_first, int layer_count, int T, int L,
 // token blocks, then scan+place over pair blocks (scratch: 2*layer_count*E int32).
 // Views for layer i live at topk/pos + i*T*kk and offsets + i*(E+1).
 constexpr int kPlanSingleCtaPairs = 128;
-// S shared experts per layer join every token after its routed slots (ids L+1..L+S,
-// groups E..E+S-1): plan rows are [T][kk+S], offsets [E+S+1].
+// S shared experts per layer join every token of [sh0, sh1) after its routed slots (ids
+// L+1..L+S, groups E..E+S-1; other tokens get id 0 / pos -1 there): plan rows are
+// [T][kk+S], offsets [E+S+1].
 void launch_route_plan(uint64_t seed, int layer_first, int layer_count, int T, int L, int top_k, int e_first, int E,
-                       int S, int32_t* topk, int32_t* pos, int32_t* offsets, int32_t* scratch,
+                       int S, int sh0, int sh1, int32_t* topk, int32_t* pos, int32_t* offsets, int32_t* scratch,
                        const long long* fault, cudaStream_t s);
 void launch_gather(const float* x, const int32_t* pos, const long long* fault, __nv_bfloat16* xp, int T, int kk,
                    int H, cudaStream_t s);

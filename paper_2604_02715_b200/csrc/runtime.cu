@@ -173,6 +173,7 @@ struct Ctx {
   int pool;
   int e_first = 0, E = 0;  // expert shard
   int S = 0;               // shared (always-on, always-resident) experts per layer
+  int sh0 = 0, sh1 = 0x7fffffff;  // step rows that pass through the shared experts
   uint8_t* shared_w = nullptr;  // [N*S] gate/up blocks, then [N*S] down blocks
   CUtensorMap map_gu_sh{}, map_dn_sh{};
   uint64_t s1, s2;         // sigma per kind
@@ -350,7 +351,8 @@ static void free_work(Ctx* c) {
 }
 
 static void ensure_work(Ctx* c, int T, int kk) {
-  if (kk > kMaxTopK) XFAIL(XPGB_ERR_OUT_OF_RANGE, "top_k %d above the kernel limit %d", kk, kMaxTopK);
+  if (kk > kMaxTopK)
+    XFAIL(XPGB_ERR_OUT_OF_RANGE, "top_k + shared experts = %d slots above the kernel limit %d", kk, kMaxTopK);
   if (T <= c->cap_T && kk <= c->cap_kk && c->xp) return;
   const int nT = std::max(T, std::max(c->cap_T, 16));
   const int nkk = std::max(kk, c->cap_kk);
@@ -427,7 +429,7 @@ static void enqueue_plan(Ctx* c, int b, int layer_first, int layer_count, int T,
                          cudaStream_t s) {
   const int kt = slots_of(c, top_k);
   const size_t lo = (size_t)(layer_first - 1);
-  launch_route_plan(seed, layer_first, layer_count, T, c->L, top_k, c->e_first, c->E, c->S,
+  launch_route_plan(seed, layer_first, layer_count, T, c->L, top_k, c->e_first, c->E, c->S, c->sh0, c->sh1,
                     c->plan_topk[b] + lo * T * kt, c->plan_pos[b] + lo * T * kt,
                     c->plan_off[b] + lo * (groups_of(c) + 1), c->plan_scr[b], c->d_fault, s);
   CKLAUNCH();
@@ -1047,26 +1049,24 @@ static void session_end(Ctx* c, xpgb_report* rep) {
   CK(cudaMemcpy(&fw, c->d_fault, sizeof(fw), cudaMemcpyDeviceToHost));
   rep->page_fault = fw != 0;
 
-  // routed experts per layer (routing is iteration-invariant) -> algorithmic bytes
+  // active groups and local rows per layer (routing is iteration-invariant) -> algorithmic bytes
   if (o->tokens > 0 && rs.acts) {
-    std::vector<int32_t> tk((size_t)N * o->tokens * kt);
-    CK(cudaMemcpy(tk.data(), c->plan_topk[0], tk.size() * 4, cudaMemcpyDeviceToHost));
-    long long active = 0;
+    const int G = groups_of(c);
+    std::vector<int32_t> of((size_t)N * (G + 1));
+    CK(cudaMemcpy(of.data(), c->plan_off[0], of.size() * 4, cudaMemcpyDeviceToHost));
+    long long active = 0, rows = 0;
     for (int l = 0; l < N; ++l) {
-      std::vector<char> seen(c->L + c->S + 1, 0);
-      for (size_t i = 0; i < (size_t)o->tokens * kt; ++i) {
-        const int e = tk[(size_t)l * o->tokens * kt + i];
-        const int el = e > c->L ? 0 : e - 1 - c->e_first;  // shared experts are local on every shard
-        if (el >= 0 && el < c->E && !seen[e]) { seen[e] = 1; ++active; }
-      }
+      const int32_t* o2 = of.data() + (size_t)l * (G + 1);
+      for (int e = 0; e < G; ++e) active += o2[e + 1] > o2[e];
+      rows += o2[G];
     }
     (void)kk;
-    const long long pairs = (long long)o->tokens * kt;
+    (void)kt;
     rep->active_experts = (int32_t)active;
     rep->down_splits = c->last_splits;
-    rep->gate_up_bytes = (long long)((double)active / N * c->s1) + pairs * c->H * 2 + pairs * c->F * 2;
-    rep->down_bytes = (long long)((double)active / N * c->s2) + pairs * c->F * 2 +
-                      pairs * (long long)c->H * 4 * std::max(1, rep->down_splits);
+    const double a = (double)active / N, r = (double)rows / N;
+    rep->gate_up_bytes = (long long)(a * c->s1 + r * c->H * 2 + r * c->F * 2);
+    rep->down_bytes = (long long)(a * c->s2 + r * c->F * 2 + r * (double)c->H * 4 * std::max(1, rep->down_splits));
   }
   if (o->profile && steps > 0 && o->tokens > 0) {
     double gu = 0, dn = 0, aux = 0;
@@ -1796,8 +1796,7 @@ int xpgb_set_shared(xpgb_ctx* h, const void* host, uint64_t bytes, int32_t n_sha
     if (c->sess && c->sess->active) XFAIL(XPGB_ERR, "cannot change shared experts during a session");
     if (n_shared < 0 || c->E + n_shared > kMaxExperts)
       XFAIL(XPGB_ERR_OUT_OF_RANGE, "shared experts %d outside [0, %d]", n_shared, kMaxExperts - c->E);
-    if (std::min(c->L, kMaxTopK) + n_shared > kMaxTopK)
-      XFAIL(XPGB_ERR_OUT_OF_RANGE, "top_k + shared experts above the kernel limit %d", kMaxTopK);
+    if (n_shared >= kMaxTopK) XFAIL(XPGB_ERR_OUT_OF_RANGE, "shared experts %d leave no routed slot", n_shared);
     const uint64_t want = (uint64_t)c->N * n_shared * (c->s1 + c->s2);
     if (n_shared && (!host || bytes != want))
       XFAIL(XPGB_ERR_CONTAINER_FORMAT, "shared payload is %llu bytes, expected %llu", (unsigned long long)bytes,
@@ -1821,6 +1820,15 @@ int xpgb_set_shared(xpgb_ctx* h, const void* host, uint64_t bytes, int32_t n_sha
     }
     c->map_gu_sh = make_map(c->shared_w, (uint64_t)nb * 2 * c->F, c->H, kBM);
     c->map_dn_sh = make_map(c->shared_w + (uint64_t)nb * c->s1, (uint64_t)nb * c->H, c->F, kBM);
+  });
+}
+
+int xpgb_set_shared_tokens(xpgb_ctx* h, int32_t first, int32_t count) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    if (first < 0) XFAIL(XPGB_ERR_OUT_OF_RANGE, "shared token range starts at %d", first);
+    c->sh0 = first;
+    c->sh1 = count < 0 ? 0x7fffffff : first + count;
   });
 }
 
@@ -1935,7 +1943,7 @@ int xpgb_set_expert_shard(xpgb_ctx* h, int32_t expert_first, int32_t expert_coun
     c->E = expert_count;
     c->cap_T = 0;  // force workspace re-creation with the new expert count
     init_pools(c);
-    ensure_work(c, 16, std::min(c->L, 8));
+    ensure_work(c, 16, std::min(c->L, 8) + c->S);
   });
 }
 
@@ -2013,7 +2021,8 @@ int xpgb_profile_layer(xpgb_ctx* h, int32_t layer, const float* x_dev, float* y_
       u1 += (long long)((n + bn - 1) / bn) * ((c->F + kBM - 1) / kBM);
       u2 += (long long)((n + bn - 1) / bn) * ((c->H + kBM - 1) / kBM) * c->last_splits;
     }
-    const long long pairs = (long long)tokens * kt;
+    const long long pairs = offs[G];  // rows this device computes (local routed + shared)
+    (void)kt;
     acc.gate_up_bytes = active * (long long)c->s1 + pairs * c->H * 2 + pairs * c->F * 2;
     acc.down_bytes = active * (long long)c->s2 + pairs * c->F * 2 + pairs * c->H * 4 * c->last_splits;
     acc.n_units_gate_up = (int32_t)u1;

@@ -112,6 +112,10 @@ class Context:
                  int(shared.count))
         self._shared_ref = shared
 
+    def set_shared_tokens(self, first: int = 0, count: int = -1) -> None:
+        """Step rows [first, first+count) pass through the shared experts (count < 0: all)."""
+        call("xpgb_set_shared_tokens", self._h, int(first), int(count))
+
     def set_pinned(self, mask: np.ndarray) -> None:
         arr = np.ascontiguousarray(mask, dtype=np.uint8)
         call("xpgb_set_pinned", self._h, arr.ctypes.data_as(C.POINTER(C.c_uint8)))

@@ -200,7 +200,12 @@ class StreamedRunner:
 
     def __init__(self, spec: ModelSpec, hierarchy: StorageHierarchy, fwd: ForwardSpec, mode: str = "threaded",
                  compute_delay_fn=None, sabotage_skip_raw=None, trace=None, device: int = 0,
-                 host_codec: bool = False, pinned=None):
+                 host_codec: bool = False, pinned=None, expert_shard=None, shared_tokens=None):
+        """expert_shard=(first, count): this device holds only experts [first, first+count) of
+        every layer -- one expert-parallel rank's slice -- and ``hierarchy`` is built on that
+        shard's container (ModelSpec(N, count, H, F), shard-local order); the router still
+        spans all L experts and rows routed elsewhere are skipped.  shared_tokens=(first,
+        count): the step rows that pass through the shared experts (default all)."""
         if mode not in ("threaded", "sequential"):
             raise XpgError(f"unknown mode {mode!r}")
         self.spec = spec
@@ -210,10 +215,15 @@ class StreamedRunner:
         self.compute_delay_fn = compute_delay_fn
         self.sabotage_skip_raw = sabotage_skip_raw
         self.ctx = Context(spec, _lib.POOL_RING, device, max_tokens=fwd.tokens_per_step)
+        first, count = expert_shard if expert_shard is not None else (0, spec.experts_per_layer)
+        if expert_shard is not None:
+            self.ctx.set_expert_shard(first, count)
         self.ctx.attach_host_pool(hierarchy.container.pinned)
         if getattr(hierarchy.container, "shared", None) is not None:
             self.ctx.set_shared(hierarchy.container.shared)
-        placement = hierarchy.backend_map()
+        if shared_tokens is not None:
+            self.ctx.set_shared_tokens(*shared_tokens)
+        placement = _full_width(spec, hierarchy.backend_map(), first, count)
         cm = _codec_model(hierarchy, host_codec or bool(placement.any()))
         if cm is not None:
             # compressed tiers (codec.py): device-tier tensors live compressed in HBM; with
@@ -223,7 +233,7 @@ class StreamedRunner:
         self.ctx.set_placement(placement)
         if pinned is not None:
             # residency tier x > 0: these experts never leave HBM; the ring streams the rest
-            self.ctx.set_pinned(pinned_mask(spec, pinned))
+            self.ctx.set_pinned(pinned_mask(spec, pinned, first, count))
         self.table = PageTable(spec, trace=trace, context=self.ctx)
         self.stall_seconds = 0.0
         self.war_wait_seconds = 0.0
@@ -270,11 +280,21 @@ def _kernel_stats(rep) -> dict:
     }
 
 
-def pinned_mask(spec: ModelSpec, pinned) -> np.ndarray:
-    """uint8 [N][L] mask: an int m pins experts 1..m of every layer; arrays pass through."""
+def _full_width(spec: ModelSpec, shard_map: np.ndarray, first: int, count: int) -> np.ndarray:
+    """A shard's [N][count][2] placement map widened to the context's [N][L][2] indexing."""
+    if count == spec.experts_per_layer:
+        return shard_map
+    out = np.zeros((spec.num_layers, spec.experts_per_layer, 2), dtype=np.uint8)
+    out[:, first:first + count] = shard_map.reshape(spec.num_layers, count, 2)
+    return out
+
+
+def pinned_mask(spec: ModelSpec, pinned, first: int = 0, count: int | None = None) -> np.ndarray:
+    """uint8 [N][L] mask: an int m pins the first m experts (of the shard) of every layer;
+    arrays pass through."""
     if isinstance(pinned, (int, np.integer)):
         m = np.zeros((spec.num_layers, spec.experts_per_layer), dtype=np.uint8)
-        m[:, :int(pinned)] = 1
+        m[:, first:first + int(pinned)] = 1
         return m
     m = np.asarray(pinned, dtype=np.uint8).reshape(spec.num_layers, spec.experts_per_layer)
     return np.ascontiguousarray(m)
@@ -305,14 +325,19 @@ class ResidentModel:
     table, which simply never changes (pipeline.py:216-230).
     """
 
-    def __init__(self, spec: ModelSpec, container: WeightContainer, device: int = 0, max_tokens: int = 16):
+    def __init__(self, spec: ModelSpec, container: WeightContainer, device: int = 0, max_tokens: int = 16,
+                 expert_shard=None, shared_tokens=None):
         self.spec = spec
         self.container = container
         self.ctx = Context(spec, _lib.POOL_RESIDENT, device, max_tokens=max_tokens)
+        if expert_shard is not None:  # container = the shard's payload (see StreamedRunner)
+            self.ctx.set_expert_shard(*expert_shard)
         self.ctx.attach_host_pool(container.pinned)
         self.ctx.make_resident()
         if getattr(container, "shared", None) is not None:
             self.ctx.set_shared(container.shared)
+        if shared_tokens is not None:
+            self.ctx.set_shared_tokens(*shared_tokens)
 
     def forward(self, layer: int, acts, fwd: ForwardSpec):
         torch = _torch()

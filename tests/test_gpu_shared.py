@@ -74,3 +74,30 @@ def test_shared_hbm_footprint_and_removal(X):
     pool = O.WordPool(2, 4, 64, 128, c.words)
     assert O.rel_l2(plain, O.layer_forward(pool, 1, x, 2, 1)) <= TOL
     assert not np.array_equal(plain, with_shared)
+
+
+def test_expert_shards_with_shared_sum_to_full_layer(X, O):
+    """One expert-parallel rank's slice on one device (expert_shard + shared_tokens): the
+    shards' partial layer outputs add up to the full layer (shared experts applied once)."""
+    from paper_2604_02715_b200.expert_parallel import shard_payload
+
+    spec = X.ModelSpec(2, 8, 128, 256)
+    c = X.generate_synthetic_model(spec, 4, shared_experts=1)
+    T, fwd = 40, X.ForwardSpec(40, 2, 6)
+    x = np.random.default_rng(1).standard_normal((T, 128), dtype=np.float32)
+    full = X.ResidentModel(spec, c, max_tokens=T).forward(1, x, fwd)
+    parts = []
+    for first, count, sh in ((0, 3, (0, T)), (3, 5, (0, 0))):
+        shard = X.WeightContainer._adopt(X.ModelSpec(2, count, 128, 256), shard_payload(c, first, count))
+        shard.shared = c.shared
+        m = X.ResidentModel(spec, shard, max_tokens=T, expert_shard=(first, count), shared_tokens=sh)
+        parts.append(m.forward(1, x, fwd))
+    assert O.rel_l2(parts[0] + parts[1], full) <= 1e-5
+    # paged shard run of the same slice equals its resident twin
+    shard = X.WeightContainer._adopt(X.ModelSpec(2, 5, 128, 256), shard_payload(c, 3, 5))
+    backends = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 30e9, 1 << 40)]
+    hier = X.StorageHierarchy(shard, None, X.plan_placement(shard.spec, backends), backends)
+    rep = X.StreamedRunner(spec, hier, fwd, host_codec=True, expert_shard=(3, 5)).run(1, acts=x.copy())
+    twin, _ = X.ResidentModel(spec, shard, max_tokens=T, expert_shard=(3, 5)).run(1, fwd, x.copy())
+    assert rep.violations == [] and rep.page_fault is None
+    assert rep.final_activations.tobytes() == np.asarray(twin).tobytes()
