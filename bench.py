@@ -55,6 +55,46 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
+def load_tensor_peak():
+    """Sustained dense bf16 TFLOP/s (the GEMMs run inside a long step), else the recipe's fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p.get("bf16_tflops_sustained") or p["bf16_tflops"]), "measured (sustained)"
+    except Exception:
+        return 1590.0, "fallback"
+
+
+def ncu_traffic(config: str, tokens: int):
+    """DRAM bytes (read + write) of one gate/up launch from the committed ncu --set full
+    capture of this workload (profiles/), or None when none was taken for it."""
+    path = {("mixtral", 256): os.path.join(ROOT, "profiles", "r1_ncu_gemm_T256_v3.jsonl")}.get((config, tokens))
+    try:
+        for line in open(path):
+            rec = json.loads(line)
+            if "<1," in rec.get("kernel", "") or "<true" in rec.get("kernel", ""):
+                return rec.get("traffic_bytes")
+    except Exception:
+        return None
+    return None
+
+
+def gemm_roofline(kind, bytes_, ns, rows, H, F, hbm_peak, hbm_src, tc_peak, tc_src):
+    """Roofline of one grouped-GEMM launch: HBM-bound (weights dominate) at decode sizes,
+    tensor-bound once the rows per expert make the contraction compute-heavy."""
+    flops = 2.0 * rows * H * (2 * F if kind == "gate_up" else F)
+    t = ns * 1e-9 if ns else 0.0
+    if bytes_ and flops / bytes_ > tc_peak * 1e12 / (hbm_peak * 1e9):
+        ach = flops / t / 1e12 if t else 0.0
+        return {"bound": "tensor", "achieved": ach, "peak": tc_peak, "unit": "TFLOP/s",
+                "frac": ach / tc_peak, "peak_source": tc_src, "flops_per_launch": flops,
+                "algorithmic_bytes_per_launch": bytes_, "avg_launch_us": ns / 1e3}
+    ach = bytes_ / t / 1e9 if t else 0.0
+    return {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+            "peak_source": hbm_src, "algorithmic_bytes_per_launch": bytes_, "flops_per_launch": flops,
+            "avg_launch_us": ns / 1e3}
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled every 200 ms while active."""
 
@@ -405,8 +445,18 @@ def main():
     log("resident done")
     hbm_peak, peak_src = load_peaks()
     h2d_peak = h2d_peak_gbps(torch, dev)
-    gu_ach = kern["gate_up_bytes"] / (kern["gate_up_ns"] * 1e-9) / 1e9 if kern.get("gate_up_ns") else 0.0
-    dn_ach = kern["down_bytes"] / (kern["down_ns"] * 1e-9) / 1e9 if kern.get("down_ns") else 0.0
+    tc_peak, tc_src = load_tensor_peak()
+    # local rows per launch, from the algorithmic bytes (a experts x sigma1 + rows x (H + F) x 2 B)
+    a_per_layer = kern.get("active_experts", 0) / N
+    rows = max(0.0, (kern.get("gate_up_bytes", 0) - a_per_layer * 4 * H * F) / (2 * (H + F)))
+    roof = gemm_roofline("gate_up", kern.get("gate_up_bytes", 0), kern.get("gate_up_ns", 0), rows, H, F,
+                         hbm_peak, peak_src, tc_peak, tc_src)
+    roof_dn = gemm_roofline("down", kern.get("down_bytes", 0), kern.get("down_ns", 0), rows, H, F,
+                            hbm_peak, peak_src, tc_peak, tc_src)
+    roof.update({"kernel": "k_moe_gemm<gate_up> (tcgen05 grouped SwiGLU GEMM, resident run)",
+                 "traffic": ncu_traffic(args.config, T_run), "rows_per_launch": rows,
+                 "down": {k: roof_dn[k] for k in ("bound", "achieved", "peak", "unit", "frac", "avg_launch_us")}})
+    roof["down"]["splits"] = kern.get("down_splits")
 
     line = {
         "metric": METRIC_PREFILL if args.prefill else METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -427,13 +477,7 @@ def main():
                     "effective_raw_gbps": (cspec.total_bytes * args.steps / rep.elapsed_seconds / 1e9) if not use_ep else None},
         "exposed_xfer_pct": 100.0 * exposed,
         "war_wait_ms": rep.war_wait_seconds * 1e3,
-        "roofline": {"bound": "hbm", "kernel": "k_gate_up (tcgen05 grouped SwiGLU GEMM, resident run)",
-                     "achieved": gu_ach, "peak": hbm_peak, "unit": "GB/s", "frac": gu_ach / hbm_peak if hbm_peak else None,
-                     "traffic": None, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": kern.get("gate_up_bytes"), "avg_launch_us": kern.get("gate_up_ns", 0) / 1e3,
-                     "down": {"achieved": dn_ach, "frac": dn_ach / hbm_peak if hbm_peak else None,
-                              "avg_launch_us": kern.get("down_ns", 0) / 1e3, "bytes_per_launch": kern.get("down_bytes"),
-                              "splits": kern.get("down_splits")}},
+        "roofline": roof,
         "resident": resident,
         "paged_over_resident": (value / world) / resident["tok_s"] if resident else None,
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": int(x_host.nbytes),

@@ -237,6 +237,47 @@ class StreamedRunner:
         self.table = PageTable(spec, trace=trace, context=self.ctx)
         self.stall_seconds = 0.0
         self.war_wait_seconds = 0.0
+        self.host_codec = host_codec
+        self._shard = (first, count)
+        self._codec_on = cm is not None
+        self.device_experts = None  # per-layer device-tier experts once set_device_experts ran
+
+    # ---- residency control (residency.LiveResidencyController)
+    def _compressed(self):
+        cm = _codec_model(self.hierarchy, True)
+        if not self._codec_on:
+            self.ctx.set_codec(cm, host_compressed=self.host_codec)
+            self._codec_on = True
+        return cm
+
+    def device_tier_bytes(self, m: int) -> int:
+        """HBM bytes of the device tier holding experts 1..m of every layer (compressed records)."""
+        cm = self._compressed()
+        from ._lib import lib
+
+        spec, total = self.hierarchy.container.spec, 0
+        for i, tid in enumerate(iter_tensor_ids(spec)):
+            if tid.expert <= m:
+                total += int(lib().xpgb_codec_record_bytes(spec.value_count(tid.kind), int(cm.bits_lens[i]),
+                                                           int(cm.chunk)))
+        return total
+
+    def set_device_experts(self, m_layers) -> None:
+        """Placement: experts 1..m_l of layer l on the compressed device tier, the rest on the
+        host tier (the reference's alpha split per layer, storage.py:143-168).  Re-stages the
+        device tier between runs; results are unchanged (the codec is lossless)."""
+        spec = self.hierarchy.container.spec
+        m_layers = [int(m) for m in m_layers]
+        if len(m_layers) != spec.num_layers or min(m_layers) < 0 or max(m_layers) > spec.experts_per_layer:
+            raise XpgError(f"bad per-layer device experts {m_layers}")
+        if any(m_layers):
+            self._compressed()
+        shard_map = np.zeros((spec.num_layers, spec.experts_per_layer, 2), dtype=np.uint8)
+        for l, m in enumerate(m_layers):
+            shard_map[l, :m] = 1
+        first, count = self._shard
+        self.ctx.set_placement(_full_width(self.spec, shard_map, first, count))
+        self.device_experts = m_layers
 
     def run(self, iterations: int, acts=None, profile: bool = False) -> RunReport:
         if iterations < 1:
