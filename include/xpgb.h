@@ -89,7 +89,8 @@ typedef struct xpgb_record {
   int32_t kind;             /* 1/2 for loads and recycles, -1 otherwise */
   int32_t target_iteration; /* recycle only, else -1 */
   int32_t target_layer;     /* recycle only, else -1 */
-  int32_t pad;
+  int32_t group;            /* sub-layer ring window of the step (bits 0-15); recycles: the recycled
+                               step's window in bits 16-31.  0 in the reference geometry. */
   int64_t wall_ns;          /* %globaltimer when the record was written */
 } xpgb_record;
 
@@ -218,6 +219,13 @@ int xpgb_set_codec(xpgb_ctx* ctx, const void* pool, uint64_t pool_bytes, const u
  * others through a ring of 2 x (most streamed experts of any layer) blocks per kind.  Re-creates
  * the arena (no session may be active).  All-zero = the reference geometry. */
 int xpgb_set_pinned(xpgb_ctx* ctx, const uint8_t* pinned_of);
+/* Sub-layer ring (budgets below two layers, an extension of the reference): cap the ring at
+ * ring_experts blocks per kind (>= 2; -1 = the reference's two layers).  A layer whose streamed
+ * experts exceed ring_experts/2 is then scheduled as windows of ring_experts/2 streamed experts,
+ * double-buffered in the two halves of the ring: window w+2 recycles window w's blocks after its
+ * compute event (the reference's WAR rule one window at a time), each window's GEMMs read only
+ * its experts, and the layer's combine runs after its last window.  Re-creates the arena. */
+int xpgb_set_ring_experts(xpgb_ctx* ctx, int32_t ring_experts);
 /* Shared experts (DeepSeek-V3 style; absent from the reference, our convention): n_shared
  * always-on experts per layer that every token passes through after its routed experts,
  * weight 1.0 (the routed sum keeps its f32(1/top_k) scale).  host = N*n_shared*(sigma1+sigma2)

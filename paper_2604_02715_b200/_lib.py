@@ -37,7 +37,7 @@ class Spec(C.Structure):
 class Record(C.Structure):
     _fields_ = [("t", C.c_int32), ("event", C.c_int32), ("iteration", C.c_int32), ("layer", C.c_int32),
                 ("kind", C.c_int32), ("target_iteration", C.c_int32), ("target_layer", C.c_int32),
-                ("pad", C.c_int32), ("wall_ns", C.c_int64)]
+                ("group", C.c_int32), ("wall_ns", C.c_int64)]
 
 
 class RunOpts(C.Structure):
@@ -109,6 +109,7 @@ _SIGS = {
     "xpgb_log_get": [_P, C.POINTER(Record), _I, C.POINTER(_I)],
     "xpgb_set_expert_shard": [_P, _I, _I],
     "xpgb_set_shared": [_P, _P, _U64, _I],
+    "xpgb_set_ring_experts": [_P, _I],
     "xpgb_set_shared_tokens": [_P, _I, _I],
     "xpgb_experts_forward": [_P, _I, _P, _P, _I, _P, _P],
     "xpgb_combine_rows": [_P, _P, _I, _I, _I, _I, _P, _P],

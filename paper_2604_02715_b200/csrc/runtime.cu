@@ -114,7 +114,7 @@ struct PtOp {
   int32_t* log_count;
   int32_t log_cap;
   int32_t n_rec;
-  int32_t rec[2][6];  // event, it, layer, kind, target_it, target_layer
+  int32_t rec[2][7];  // event, it, layer, kind, target_it, target_layer, group word
   int32_t vals[448];
 };
 static_assert(sizeof(PtOp) < 4000, "kernel parameter block too large");
@@ -130,7 +130,7 @@ __device__ void write_record(xpgb_record* log, int32_t* count, int cap, const in
     rec.kind = r[3];
     rec.target_iteration = r[4];
     rec.target_layer = r[5];
-    rec.pad = 0;
+    rec.group = r[6];
     rec.wall_ns = (int64_t)globaltimer_ns();
     log[t] = rec;
     __threadfence();
@@ -206,6 +206,7 @@ struct Ctx {
   int32_t* d_pt = nullptr;  // [2][N*E] device slot table
   std::vector<uint8_t> pinned;  // [N*E] permanently resident experts (residency tier x > 0)
   int ring_blocks = 0;          // blocks per kind that cycle through the schedule
+  int ring_limit = 0;           // cap on ring blocks per kind (sub-layer ring); 0 = 2 x streamed experts
 
   // streams / events
   cudaStream_t s_copy[2] = {nullptr, nullptr};
@@ -436,10 +437,12 @@ static void enqueue_plan(Ctx* c, int b, int layer_first, int layer_count, int T,
 }
 
 // layer_forward (pipeline.py:192-208) on `s` from plan buffer b; y may alias x.
+// Window [e0, e1) of local expert groups: the GEMMs of those experts only (rows are
+// absolute, so windows of one layer write disjoint rows); `last` runs the combine.
 // gather: x -> expert-major bf16 rows first (else the previous combine already did it);
 // next_pos: fuse the next layer's gather into this layer's combine.
-static void enqueue_forward(Ctx* c, int layer, const float* x, float* y, int T, int top_k, int b, bool gather,
-                            const int32_t* next_pos, cudaStream_t s) {
+static void enqueue_window(Ctx* c, int layer, const float* x, float* y, int T, int top_k, int b, bool gather,
+                           int e0, int e1, bool last, const int32_t* next_pos, cudaStream_t s) {
   const int kk = std::min(top_k, c->L), kt = slots_of(c, top_k);
   if (T == 0) return;
   const int32_t* pos = c->plan_pos[b] + (size_t)(layer - 1) * T * kt;
@@ -453,19 +456,32 @@ static void enqueue_forward(Ctx* c, int layer, const float* x, float* y, int T, 
   }
   prof_rec(c, 2, s);
   prof_rec(c, 3, s);
-  launch_gate_up(c->map_gu, c->map_xp, c->S ? c->map_gu_sh : c->map_gu, gemm_params(c, layer, 1, off, 1), bn,
-                 c->num_sms, s);
+  GemmParams pg = gemm_params(c, layer, 1, off, 1), pd = gemm_params(c, layer, 2, off, splits);
+  for (GemmParams* p : {&pg, &pd}) {  // restrict to the window: groups [e0, e1)
+    p->offsets += e0;
+    p->pt += std::min(e0, c->E);
+    p->e_first += e0;
+    p->E = e1 - e0;
+    p->E_routed = std::max(0, std::min(e1, c->E) - e0);
+  }
+  launch_gate_up(c->map_gu, c->map_xp, c->S ? c->map_gu_sh : c->map_gu, pg, bn, c->num_sms, s);
   CKLAUNCH();
   prof_rec(c, 4, s);
-  launch_down(c->map_dn, c->map_h, c->S ? c->map_dn_sh : c->map_dn, gemm_params(c, layer, 2, off, splits), bn,
-              c->num_sms, s);
+  launch_down(c->map_dn, c->map_h, c->S ? c->map_dn_sh : c->map_dn, pd, bn, c->num_sms, s);
   CKLAUNCH();
   prof_rec(c, 5, s);
-  launch_combine(c->part, pos, c->d_fault, y, T, kt, kk, c->H, splits, (long long)c->cap_rows * c->H,
-                 (float)(1.0 / top_k), next_pos, c->xp, s);
-  CKLAUNCH();
+  if (last) {
+    launch_combine(c->part, pos, c->d_fault, y, T, kt, kk, c->H, splits, (long long)c->cap_rows * c->H,
+                   (float)(1.0 / top_k), next_pos, c->xp, s);
+    CKLAUNCH();
+  }
   prof_rec(c, 6, s);
   c->last_splits = splits;
+}
+
+static void enqueue_forward(Ctx* c, int layer, const float* x, float* y, int T, int top_k, int b, bool gather,
+                            const int32_t* next_pos, cudaStream_t s) {
+  enqueue_window(c, layer, x, y, T, top_k, b, gather, 0, groups_of(c), true, next_pos, s);
 }
 
 // Standalone layer_forward: plan this layer into buffer 2, then the chain.
@@ -583,7 +599,8 @@ struct RunState {
   long long decoded = 0;
 };
 
-static void set_rec(PtOp& op, int idx, int ev, int it, int layer, int kind, int tit, int tl) {
+static void set_rec(PtOp& op, int idx, int ev, int it, int layer, int kind, int tit, int tl, int group = 0) {
+  op.rec[idx][6] = group;
   op.rec[idx][0] = ev;
   op.rec[idx][1] = it;
   op.rec[idx][2] = layer;
@@ -610,43 +627,54 @@ static void launch_op(const PtOp& op, cudaStream_t s) {
   CKLAUNCH();
 }
 
-static void log_only(Ctx* c, bool log, cudaStream_t s, int ev, int it, int layer) {
+static void log_only(Ctx* c, bool log, cudaStream_t s, int ev, int it, int layer, int group = 0) {
   if (!log) return;
   PtOp op = blank_op(c, true);
-  set_rec(op, 0, ev, it, layer, -1, -1, -1);
+  set_rec(op, 0, ev, it, layer, -1, -1, -1, group);
   launch_op(op, s);
 }
 
-// Alg. 1 MaterializeLayer (pipeline.py:335-360) for one kind, enqueued on copy stream `kind`.
-static void materialize(RunState& rs, int g, int it, int layer, int kind) {
+// One step of the schedule: a layer, or -- with a sub-layer ring -- one window of it.
+// The window [e0, e1) of local expert groups holds exactly the step's streamed experts
+// (plus any pinned ones between them); the layer's last window also covers its shared
+// experts [E, E+S).  Reference geometry: one window [0, E+S) per layer.
+struct Step {
+  int it, layer, w, e0, e1;
+  bool first, last;
+};
+
+// Alg. 1 MaterializeLayer (pipeline.py:335-360) for one kind, enqueued on copy stream `kind`:
+// recycle the blocks of step g-2 (the reference's target_layer, paging.py:29-38, once the
+// steps are layers) after its compute event, map + load this step's streamed experts.
+static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int kind) {
   Ctx* c = rs.c;
   const int N = c->N, E = c->E, k = kind - 1;
+  const int it = st.it, layer = st.layer;
+  const int wlo = st.e0, whi = std::min(st.e1, E);
   cudaStream_t s = c->s_copy[k];
   const bool seq = rs.o->sequential != 0;
   PtOp op = blank_op(c, rs.log);
   int nrec = 0;
   const bool any_pinned = std::find(c->pinned.begin(), c->pinned.end(), 1) != c->pinned.end();
   auto is_pinned = [&](int l, int e) { return c->pinned[(size_t)(l - 1) * E + e] != 0; };
-  if (it > 1 || layer > 2) {
-    const int tgt = ((layer - 3 + N) % N) + 1;
-    const int tgt_it = layer > 2 ? it : it - 1;
-    const int gt = (tgt_it - 1) * N + (tgt - 1);
-    CK(cudaStreamWaitEvent(s, c->ev_comp[gt & 3], 0));  // WAR
-    for (int e = 0; e < E; ++e)
+  const int chunk = (int)(sizeof(op.vals) / sizeof(int32_t));
+  if (tg) {
+    const int tgt = tg->layer, tlo = tg->e0, thi = std::min(tg->e1, E);
+    CK(cudaStreamWaitEvent(s, c->ev_comp[(g - 2) & 3], 0));  // WAR
+    for (int e = tlo; e < thi; ++e)
       if (!is_pinned(tgt, e)) pt_unmap(c, tgt, c->e_first + e + 1, kind);
-    if (rs.log) set_rec(op, nrec++, XPGB_EV_RECYCLE, it, layer, kind, tgt_it, tgt);
+    if (rs.log) set_rec(op, nrec++, XPGB_EV_RECYCLE, it, layer, kind, tg->it, tgt, st.w | (tg->w << 16));
     int32_t* trow = c->d_pt + (size_t)k * N * E + (size_t)(tgt - 1) * E;
     if (!any_pinned) {
-      op.unmap_row = trow;
-      op.unmap_n = E;
+      op.unmap_row = trow + tlo;
+      op.unmap_n = thi - tlo;
     } else {
-      // keep the pinned entries of the recycled layer: rewrite its row explicitly
-      const int chunk = (int)(sizeof(op.vals) / sizeof(int32_t));
-      for (int e0 = 0; e0 < E; e0 += chunk) {
-        PtOp ou = (e0 == 0) ? op : blank_op(c, false);
-        if (e0 > 0) ou.n_rec = 0;
+      // keep the pinned entries of the recycled window: rewrite its range explicitly
+      for (int e0 = tlo; e0 < thi; e0 += chunk) {
+        PtOp ou = (e0 == tlo) ? op : blank_op(c, false);
+        if (e0 > tlo) ou.n_rec = 0;
         ou.set_row = trow + e0;
-        ou.set_n = std::min(chunk, E - e0);
+        ou.set_n = std::min(chunk, thi - e0);
         for (int i = 0; i < ou.set_n; ++i) {
           const size_t pi = (size_t)(tgt - 1) * E + e0 + i;
           ou.vals[i] = c->st[k][pi] == XPGB_PAGE_UNMAPPED ? -1 : pt_entry(c->blk[k][pi] - 1, c->st[k][pi]);
@@ -657,23 +685,23 @@ static void materialize(RunState& rs, int g, int it, int layer, int kind) {
       nrec = 0;
     }
   }
-  // map every streamed expert of the layer (lowest free block first) -> LOADING entries
-  std::vector<int> blocks(E);
-  for (int e = 0; e < E; ++e)
+  // map every streamed expert of the window (lowest free block first) -> LOADING entries
+  std::vector<int> blocks(E, 0);
+  for (int e = wlo; e < whi; ++e)
     blocks[e] = is_pinned(layer, e) ? c->blk[k][(size_t)(layer - 1) * E + e]
                                     : pt_map(c, layer, c->e_first + e + 1, kind);
-  if (rs.log) set_rec(op, nrec++, XPGB_EV_LOAD_START, it, layer, kind, -1, -1);
+  if (rs.log) set_rec(op, nrec++, XPGB_EV_LOAD_START, it, layer, kind, -1, -1, st.w);
   int32_t* row = c->d_pt + (size_t)k * N * E + (size_t)(layer - 1) * E;
-  const int chunk = (int)(sizeof(op.vals) / sizeof(int32_t));
-  for (int e0 = 0; e0 < E; e0 += chunk) {
-    PtOp o2 = (e0 == 0) ? op : blank_op(c, false);
-    if (e0 > 0) { o2.unmap_n = 0; o2.n_rec = 0; }
+  for (int e0 = wlo; e0 < whi; e0 += chunk) {
+    PtOp o2 = (e0 == wlo) ? op : blank_op(c, false);
+    if (e0 > wlo) { o2.unmap_n = 0; o2.n_rec = 0; }
     o2.set_row = row + e0;
-    o2.set_n = std::min(chunk, E - e0);
+    o2.set_n = std::min(chunk, whi - e0);
     for (int i = 0; i < o2.set_n; ++i)
       o2.vals[i] = pt_entry(blocks[e0 + i] - 1, is_pinned(layer, e0 + i) ? XPGB_PAGE_RESIDENT : XPGB_PAGE_LOADING);
     launch_op(o2, s);
   }
+  if (whi <= wlo && (op.n_rec > 0 || op.unmap_n > 0)) launch_op(op, s);  // window without routed experts
   const float* delays = rs.o->fetch_delay_s;
   auto delay_of = [&](int e) -> float {
     return delays ? delays[((size_t)(layer - 1) * c->L + (c->e_first + e)) * 2 + k] : 0.f;
@@ -685,7 +713,7 @@ static void materialize(RunState& rs, int g, int it, int layer, int kind) {
   };
   cudaStream_t done_stream = s;
   if (!c->codec) {
-    for (int e = 0; e < E; ++e) {
+    for (int e = wlo; e < whi; ++e) {
       if (is_pinned(layer, e)) continue;
       if (delay_of(e) > 0) sleep_on(s, delay_of(e));
       bool from_host = true;
@@ -709,11 +737,11 @@ static void materialize(RunState& rs, int g, int it, int layer, int kind) {
     auto rec_bytes = [&](int e) { return xpgb_codec_record_bytes(n, c->rec_bits[tix(e)], c->cchunk); };
     // a staged run may take expert e' after e when its record follows e's in the pool
     auto joins_run = [&](int e, int e2, int tier) {
-      return e2 < E && !is_pinned(layer, e2) && c->backend[tix(e2)] == tier && delay_of(e2) <= 0.f &&
+      return e2 < whi && !is_pinned(layer, e2) && c->backend[tix(e2)] == tier && delay_of(e2) <= 0.f &&
              (tier == 1 || c->rec_off[tix(e2)] == c->rec_off[tix(e)] + rec_bytes(e));
     };
     DecodeTensor dt[kMaxDecodeTensors];
-    for (int e = 0; e < E;) {
+    for (int e = wlo; e < whi;) {
       if (is_pinned(layer, e)) { ++e; continue; }
       const size_t ti = tix(e);
       uint8_t* dst = block_ptr(c, kind, blocks[e]);
@@ -829,14 +857,14 @@ static void materialize(RunState& rs, int g, int it, int layer, int kind) {
     }
     done_stream = d;
   }
-  for (int e = 0; e < E; ++e)
+  for (int e = wlo; e < whi; ++e)
     if (!is_pinned(layer, e)) pt_mark_resident(c, layer, c->e_first + e + 1, kind);
-  for (int e0 = 0; e0 < E; e0 += chunk) {
-    PtOp o3 = blank_op(c, rs.log && e0 + chunk >= E);
+  for (int e0 = wlo; e0 < std::max(whi, wlo + 1); e0 += chunk) {
+    PtOp o3 = blank_op(c, rs.log && e0 + chunk >= whi);
     o3.set_row = row + e0;
-    o3.set_n = std::min(chunk, E - e0);
+    o3.set_n = std::max(0, std::min(chunk, whi - e0));
     for (int i = 0; i < o3.set_n; ++i) o3.vals[i] = pt_entry(blocks[e0 + i] - 1, XPGB_PAGE_RESIDENT);
-    if (o3.log) set_rec(o3, 0, XPGB_EV_LOAD_DONE, it, layer, kind, -1, -1);
+    if (o3.log) set_rec(o3, 0, XPGB_EV_LOAD_DONE, it, layer, kind, -1, -1, st.w);
     launch_op(o3, done_stream);
   }
   CK(cudaEventRecord(c->ev_load[k][g & 3], done_stream));
@@ -855,6 +883,7 @@ struct Session {
   RunState rs{};
   int steps = 0;
   bool paged = false;
+  std::vector<Step> sv;  // the flattened schedule: iterations x layers x windows
 };
 
 static Session& session_of(Ctx* c) {
@@ -862,10 +891,46 @@ static Session& session_of(Ctx* c) {
   return *c->sess;
 }
 
-static void step_of(Ctx* c, int g, int* it, int* layer) {
-  *it = g / c->N + 1;
-  *layer = g % c->N + 1;
+// Windows of one layer for the current ring: each holds ring_blocks/2 streamed experts
+// (double-buffered halves of the ring); one window per layer when the ring holds two
+// whole layers (the reference geometry).
+static std::vector<std::pair<int, int>> layer_windows(Ctx* c, int layer) {
+  const int E = c->E, G = groups_of(c);
+  int streamed = 0;
+  for (int e = 0; e < E; ++e) streamed += !c->pinned[(size_t)(layer - 1) * E + e];
+  const int gs = std::max(1, c->ring_blocks / 2);
+  std::vector<std::pair<int, int>> w;
+  if (c->pool != XPGB_POOL_RING || gs >= streamed) {
+    w.push_back({0, G});
+    return w;
+  }
+  int lo = 0, n = 0;
+  for (int e = 0; e < E; ++e) {
+    n += !c->pinned[(size_t)(layer - 1) * E + e];
+    if (n == gs) {
+      w.push_back({lo, e + 1});
+      lo = e + 1;
+      n = 0;
+    }
+  }
+  if (lo < E) w.push_back({lo, E});
+  w.back().second = G;  // the last window also computes the shared experts
+  return w;
 }
+
+static void build_schedule(Ctx* c, Session& ss, int iterations) {
+  ss.sv.clear();
+  std::vector<std::vector<std::pair<int, int>>> per_layer;
+  for (int l = 1; l <= c->N; ++l) per_layer.push_back(layer_windows(c, l));
+  for (int it = 1; it <= iterations; ++it)
+    for (int l = 1; l <= c->N; ++l) {
+      const auto& w = per_layer[l - 1];
+      for (int i = 0; i < (int)w.size(); ++i)
+        ss.sv.push_back(Step{it, l, i, w[i].first, w[i].second, i == 0, i + 1 == (int)w.size()});
+    }
+  ss.steps = (int)ss.sv.size();
+}
+
 
 // Begin a run: empty ring, fresh log, RUN_BEGIN on the compute stream; copy streams
 // start after it.  `acts` (device fp32 [T][H]) is the buffer the built-in compute
@@ -878,11 +943,12 @@ static void session_begin(Ctx* c, const xpgb_run_opts* o, float* acts) {
     XFAIL(XPGB_ERR_OUT_OF_RANGE, "bad ForwardSpec (T=%d, top_k=%d)", o->tokens, o->top_k);
   const int N = c->N;
   ss.o = *o;
-  ss.steps = o->iterations * N;
+  build_schedule(c, ss, o->iterations);
   ss.fetch_delay.clear();
   ss.compute_delay.clear();
   if (o->fetch_delay_s) ss.fetch_delay.assign(o->fetch_delay_s, o->fetch_delay_s + (size_t)N * c->L * 2);
-  if (o->compute_delay_s) ss.compute_delay.assign(o->compute_delay_s, o->compute_delay_s + (size_t)ss.steps);
+  if (o->compute_delay_s)
+    ss.compute_delay.assign(o->compute_delay_s, o->compute_delay_s + (size_t)o->iterations * N);
   ss.o.fetch_delay_s = ss.fetch_delay.empty() ? nullptr : ss.fetch_delay.data();
   ss.o.compute_delay_s = ss.compute_delay.empty() ? nullptr : ss.compute_delay.data();
   ensure_work(c, o->tokens, slots_of(c, o->top_k));
@@ -919,26 +985,24 @@ static void session_materialize(Ctx* c, int g) {
   Session& ss = session_of(c);
   if (!ss.active) XFAIL(XPGB_ERR, "no active session");
   if (!ss.paged || g < 0 || g >= ss.steps) return;
-  int it, ly;
-  step_of(c, g, &it, &ly);
-  for (int kind = 1; kind <= 2; ++kind) materialize(ss.rs, g, it, ly, kind);
+  const Step* tg = g >= 2 ? &ss.sv[g - 2] : nullptr;  // cold start: the first two steps recycle nothing
+  for (int kind = 1; kind <= 2; ++kind) materialize(ss.rs, g, ss.sv[g], tg, kind);
 }
 
 // RAW: `s` waits for both load events of step g, then compute-start is logged on it.
 static void session_acquire(Ctx* c, int g, cudaStream_t s) {
   Session& ss = session_of(c);
   if (!ss.active) XFAIL(XPGB_ERR, "no active session");
-  int it, layer;
-  step_of(c, g, &it, &layer);
+  const Step& st = ss.sv[g];
   const xpgb_run_opts* o = &ss.o;
-  const bool skip = (o->sabotage_iteration == it && o->sabotage_layer == layer);
+  const bool skip = (o->sabotage_iteration == st.it && o->sabotage_layer == st.layer);
   if (ss.paged && !skip) {
     CK(cudaStreamWaitEvent(s, c->ev_load[0][g & 3], 0));
     CK(cudaStreamWaitEvent(s, c->ev_load[1][g & 3], 0));
   }
-  log_only(c, ss.rs.log, s, XPGB_EV_COMPUTE_START, it, layer);
-  if (o->compute_delay_s) {
-    const float d = o->compute_delay_s[(size_t)g];
+  log_only(c, ss.rs.log, s, XPGB_EV_COMPUTE_START, st.it, st.layer, st.w);
+  if (o->compute_delay_s && st.first) {
+    const float d = o->compute_delay_s[(size_t)(st.it - 1) * c->N + (st.layer - 1)];
     if (d > 0) {
       k_sleep<<<1, 1, 0, s>>>((uint64_t)(d * 1e9));
       note_launch();
@@ -951,25 +1015,25 @@ static void session_acquire(Ctx* c, int g, cudaStream_t s) {
 static void session_release(Ctx* c, int g, cudaStream_t s) {
   Session& ss = session_of(c);
   if (!ss.active) XFAIL(XPGB_ERR, "no active session");
-  int it, layer;
-  step_of(c, g, &it, &layer);
-  log_only(c, ss.rs.log, s, XPGB_EV_COMPUTE_DONE, it, layer);
+  const Step& st = ss.sv[g];
+  log_only(c, ss.rs.log, s, XPGB_EV_COMPUTE_DONE, st.it, st.layer, st.w);
   CK(cudaEventRecord(c->ev_comp[g & 3], s));
   if (ss.o.sequential) CK(cudaStreamSynchronize(s));
 }
 
-// Built-in compute of step g (single-GPU layer_forward chain) on the compute stream.
+// Built-in compute of step g (single-GPU layer_forward chain) on the compute stream:
+// the window's expert GEMMs; the layer's combine after its last window.
 static void session_compute(Ctx* c, int g) {
   Session& ss = session_of(c);
   const xpgb_run_opts* o = &ss.o;
-  int it, layer;
-  step_of(c, g, &it, &layer);
+  const Step& st = ss.sv[g];
+  const int it = st.it, layer = st.layer;
   cudaStream_t s = c->s_comp;
   const int kt = slots_of(c, o->top_k);
   const int T = o->tokens;
   c->cur_ev = (o->profile && T > 0) ? &c->run_ev[(size_t)g * 7] : nullptr;
   prof_rec(c, 0, s);
-  if (layer == 1 && T > 0) {
+  if (layer == 1 && st.first && T > 0) {
     // one route+plan launch per decode step covers all N layers; plans alternate between
     // buffers 0/1 so the next step's plan never overwrites rows still in use
     if (it == 1) enqueue_plan(c, 0, 1, c->N, T, o->top_k, o->router_seed, s);
@@ -979,7 +1043,7 @@ static void session_compute(Ctx* c, int g) {
   const bool last = (g + 1 == ss.steps);
   const int32_t* next_pos = nullptr;
   if (!last && T > 0) next_pos = layer < c->N ? c->plan_pos[b] + (size_t)layer * T * kt : c->plan_pos[it & 1];
-  enqueue_forward(c, layer, ss.rs.acts, ss.rs.acts, T, o->top_k, b, g == 0, next_pos, s);
+  enqueue_window(c, layer, ss.rs.acts, ss.rs.acts, T, o->top_k, b, g == 0, st.e0, st.e1, st.last, next_pos, s);
   c->cur_ev = nullptr;
 }
 
@@ -1739,54 +1803,75 @@ int xpgb_hbm_bytes(xpgb_ctx* h, uint64_t* ring, uint64_t* staging, uint64_t* dev
   });
 }
 
+}  // extern "C"
+
+// Re-create the arena for a residency mask and ring cap: pinned experts get dedicated
+// blocks (filled from the host pool), the ring gets 2 x (most streamed experts of any
+// layer) blocks per kind, capped by ring_limit (sub-layer ring).
+static void apply_residency(Ctx* c, const std::vector<uint8_t>& mask) {
+  int n_pinned = 0, max_streamed = 0;
+  for (int l = 0; l < c->N; ++l) {
+    int streamed = 0;
+    for (int e = 0; e < c->E; ++e) {
+      n_pinned += mask[(size_t)l * c->E + e];
+      streamed += !mask[(size_t)l * c->E + e];
+    }
+    max_streamed = std::max(max_streamed, streamed);
+  }
+  if (n_pinned && !c->host) XFAIL(XPGB_ERR_BACKEND_MISS, "pinning experts needs the host pool");
+  int ring = 2 * max_streamed;
+  if (c->ring_limit > 0) ring = std::min(ring, c->ring_limit & ~1);
+  std::vector<uint8_t> backend = c->backend;
+  CK(cudaDeviceSynchronize());
+  init_pools(c, ring, n_pinned);
+  c->backend = backend;
+  c->pinned = mask;
+  int next = c->ring_blocks + 1;
+  for (int l = 1; l <= c->N; ++l)
+    for (int e = 0; e < c->E; ++e) {
+      if (!mask[(size_t)(l - 1) * c->E + e]) continue;
+      for (int kind = 1; kind <= 2; ++kind) {
+        const int k = kind - 1;
+        const size_t pi = (size_t)(l - 1) * c->E + e;
+        c->free_ids[k].erase(next);
+        c->blk[k][pi] = next;
+        c->owner[k][next] = (int)pi;
+        c->st[k][pi] = XPGB_PAGE_RESIDENT;
+        c->bound += sigma_of(c, kind);
+        const uint64_t off = pi * (c->s1 + c->s2) + (kind == 2 ? c->s1 : 0);
+        CK(cudaMemcpy(block_ptr(c, kind, next), c->host + off, sigma_of(c, kind), cudaMemcpyHostToDevice));
+      }
+      ++next;
+    }
+  c->peak = c->bound;
+  pt_upload(c);
+  stage_device_tier(c);  // the device tier survives; re-stage it beside the new arena
+}
+
+extern "C" {
+
 int xpgb_set_pinned(xpgb_ctx* h, const uint8_t* pinned_of) {
   return guard([&] {
     Ctx* c = &h->c;
     if (c->pool != XPGB_POOL_RING) XFAIL(XPGB_ERR_CONFIG, "pinned experts need a ring context");
     if (c->sess && c->sess->active) XFAIL(XPGB_ERR, "cannot pin experts during a session");
-    const size_t pages = (size_t)c->N * c->E;
-    std::vector<uint8_t> mask(pages, 0);
-    int n_pinned = 0, max_streamed = 0;
-    for (int l = 0; l < c->N; ++l) {
-      int streamed = 0;
-      for (int e = 0; e < c->E; ++e) {
-        const uint8_t v = pinned_of ? (pinned_of[(size_t)l * c->L + c->e_first + e] ? 1 : 0) : 0;
-        mask[(size_t)l * c->E + e] = v;
-        n_pinned += v;
-        streamed += !v;
-      }
-      max_streamed = std::max(max_streamed, streamed);
-    }
-    if (n_pinned && !c->host) XFAIL(XPGB_ERR_BACKEND_MISS, "pinning experts needs the host pool");
-    // re-create the arena: 2 x (most streamed experts of any layer) ring blocks + one block per pinned expert
-    std::vector<uint8_t> backend = c->backend;
-    CK(cudaDeviceSynchronize());
-    init_pools(c, 2 * max_streamed, n_pinned);
-    c->backend = backend;
-    c->pinned = mask;
-    int next = c->ring_blocks + 1;
-    for (int l = 1; l <= c->N; ++l)
-      for (int e = 0; e < c->E; ++e) {
-        if (!mask[(size_t)(l - 1) * c->E + e]) continue;
-        for (int kind = 1; kind <= 2; ++kind) {
-          const int k = kind - 1;
-          const size_t pi = (size_t)(l - 1) * c->E + e;
-          c->free_ids[k].erase(next);
-          c->blk[k][pi] = next;
-          c->owner[k][next] = (int)pi;
-          c->st[k][pi] = XPGB_PAGE_RESIDENT;
-          c->bound += sigma_of(c, kind);
-          const uint64_t off = pi * (c->s1 + c->s2) + (kind == 2 ? c->s1 : 0);
-          CK(cudaMemcpy(block_ptr(c, kind, next), c->host + off, sigma_of(c, kind), cudaMemcpyHostToDevice));
-        }
-        ++next;
-      }
-    c->peak = c->bound;
-    pt_upload(c);
-    if (c->codec) {
-      // staging buffers and device tier survive; re-stage the device tier into the new arena layout
-    }
-    stage_device_tier(c);
+    std::vector<uint8_t> mask((size_t)c->N * c->E, 0);
+    for (int l = 0; l < c->N; ++l)
+      for (int e = 0; e < c->E; ++e)
+        mask[(size_t)l * c->E + e] = pinned_of ? (pinned_of[(size_t)l * c->L + c->e_first + e] ? 1 : 0) : 0;
+    apply_residency(c, mask);
+  });
+}
+
+int xpgb_set_ring_experts(xpgb_ctx* h, int32_t ring_experts) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    if (c->pool != XPGB_POOL_RING) XFAIL(XPGB_ERR_CONFIG, "a sub-layer ring needs a ring context");
+    if (c->sess && c->sess->active) XFAIL(XPGB_ERR, "cannot resize the ring during a session");
+    if (ring_experts == 1 || ring_experts == 0 || ring_experts < -1)
+      XFAIL(XPGB_ERR_OUT_OF_RANGE, "ring of %d experts per kind: need >= 2 (or -1 for two layers)", ring_experts);
+    c->ring_limit = ring_experts < 0 ? 0 : ring_experts;
+    apply_residency(c, c->pinned);
   });
 }
 

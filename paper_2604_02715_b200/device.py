@@ -116,6 +116,10 @@ class Context:
         """Step rows [first, first+count) pass through the shared experts (count < 0: all)."""
         call("xpgb_set_shared_tokens", self._h, int(first), int(count))
 
+    def set_ring_experts(self, ring_experts: int) -> None:
+        """Sub-layer ring of ``ring_experts`` blocks per kind (-1: the reference's two layers)."""
+        call("xpgb_set_ring_experts", self._h, int(ring_experts))
+
     def set_pinned(self, mask: np.ndarray) -> None:
         arr = np.ascontiguousarray(mask, dtype=np.uint8)
         call("xpgb_set_pinned", self._h, arr.ctypes.data_as(C.POINTER(C.c_uint8)))

@@ -51,42 +51,53 @@ class OrderingRecord:
     target_iteration: int | None = None
     target_layer: int | None = None
     wall: float = 0.0
+    group: int = 0                   # sub-layer ring window of the step (0: reference geometry)
+    target_group: int | None = None  # recycles: the recycled step's window
 
 
 def validate_ordering(records) -> list:
-    """RAW/WAR replay of an ordering log (pipeline.py:119-147): one message per violation."""
+    """RAW/WAR replay of an ordering log (pipeline.py:119-147): one message per violation.
+    The unit is the (iteration, layer) step -- or, with a sub-layer ring, its window."""
     first = {}
     for r in records:
-        first.setdefault((r.event, r.iteration, r.layer, r.kind), r.t)
+        first.setdefault((r.event, r.iteration, r.layer, r.group, r.kind), r.t)
 
-    def before(event, it, layer, kind, t):
-        at = first.get((event, it, layer, kind))
+    def before(event, it, layer, group, kind, t):
+        at = first.get((event, it, layer, group, kind))
         return at is not None and at < t
+
+    def where(it, layer, group):
+        return f"iter={it} layer={layer}" + (f" window={group}" if group else "")
 
     problems = []
     for r in records:
         if r.event == "compute-start":
             problems += [
-                f"RAW: compute-start iter={r.iteration} layer={r.layer} before load-done kind={k}"
-                for k in (1, 2) if not before("load-done", r.iteration, r.layer, k, r.t)
+                f"RAW: compute-start {where(r.iteration, r.layer, r.group)} before load-done kind={k}"
+                for k in (1, 2) if not before("load-done", r.iteration, r.layer, r.group, k, r.t)
             ]
-        elif r.event == "recycle" and not before("compute-done", r.target_iteration, r.target_layer, None, r.t):
-            problems.append(
-                f"WAR: recycle of iter={r.target_iteration} layer={r.target_layer} kind={r.kind} before its compute-done")
+        elif r.event == "recycle" and not before("compute-done", r.target_iteration, r.target_layer,
+                                                 r.target_group or 0, None, r.t):
+            problems.append(f"WAR: recycle of {where(r.target_iteration, r.target_layer, r.target_group or 0)} "
+                            f"kind={r.kind} before its compute-done")
     return problems
 
 
 def _intervals(records) -> dict:
+    """{(iteration, layer): {"load1"|"load2"|"compute": (start, done)}}; the windows of a
+    sub-layer ring merge into their layer's span (first start .. last done)."""
     spans, opened = {}, {}
     for r in records:
         phase, _, edge = r.event.partition("-")
         if edge == "start":
-            opened[(phase, r.iteration, r.layer, r.kind)] = r.wall
+            opened[(phase, r.iteration, r.layer, r.group, r.kind)] = r.wall
         elif edge == "done":
-            t0 = opened.get((phase, r.iteration, r.layer, r.kind))
+            t0 = opened.get((phase, r.iteration, r.layer, r.group, r.kind))
             if t0 is not None:
                 name = f"load{r.kind}" if phase == "load" else "compute"
-                spans.setdefault((r.iteration, r.layer), {})[name] = (t0, r.wall)
+                layer = spans.setdefault((r.iteration, r.layer), {})
+                a, b = layer.get(name, (t0, r.wall))
+                layer[name] = (min(a, t0), max(b, r.wall))
     return spans
 
 
@@ -160,7 +171,8 @@ def _records_from_log(ctx: Context):
             t=t, event=_lib.EVENT_NAMES[r.event], iteration=r.iteration, layer=r.layer, kind=kind,
             target_iteration=r.target_iteration if r.target_iteration > 0 else None,
             target_layer=r.target_layer if r.target_layer > 0 else None,
-            wall=(r.wall_ns - base) * 1e-9))
+            wall=(r.wall_ns - base) * 1e-9, group=r.group & 0xFFFF,
+            target_group=((r.group >> 16) & 0xFFFF) if r.target_layer > 0 else None))
         t += 1
     return out
 
@@ -200,12 +212,15 @@ class StreamedRunner:
 
     def __init__(self, spec: ModelSpec, hierarchy: StorageHierarchy, fwd: ForwardSpec, mode: str = "threaded",
                  compute_delay_fn=None, sabotage_skip_raw=None, trace=None, device: int = 0,
-                 host_codec: bool = False, pinned=None, expert_shard=None, shared_tokens=None):
+                 host_codec: bool = False, pinned=None, expert_shard=None, shared_tokens=None,
+                 ring_experts=None):
         """expert_shard=(first, count): this device holds only experts [first, first+count) of
         every layer -- one expert-parallel rank's slice -- and ``hierarchy`` is built on that
         shard's container (ModelSpec(N, count, H, F), shard-local order); the router still
         spans all L experts and rows routed elsewhere are skipped.  shared_tokens=(first,
-        count): the step rows that pass through the shared experts (default all)."""
+        count): the step rows that pass through the shared experts (default all).
+        ring_experts: a sub-layer ring of that many expert blocks per kind (budgets below the
+        reference's two layers; each layer then streams in windows of ring_experts/2)."""
         if mode not in ("threaded", "sequential"):
             raise XpgError(f"unknown mode {mode!r}")
         self.spec = spec
@@ -231,6 +246,8 @@ class StreamedRunner:
             # decoded on the GPU straight into the ring block.
             self.ctx.set_codec(cm, host_compressed=host_codec)
         self.ctx.set_placement(placement)
+        if ring_experts is not None:
+            self.ctx.set_ring_experts(int(ring_experts))
         if pinned is not None:
             # residency tier x > 0: these experts never leave HBM; the ring streams the rest
             self.ctx.set_pinned(pinned_mask(spec, pinned, first, count))

@@ -119,3 +119,58 @@ def test_layer_forward_through_page_table_faults_on_unmapped(X):
     table = X.PageTable(spec)
     with pytest.raises(X.PageFaultError):
         X.layer_forward(table, spec, X.ForwardSpec(2, 2, 1), 1, np.ones((2, 16), np.float32))
+
+
+@pytest.mark.parametrize("ring,pinned,host_codec,S", [(2, None, False, 0), (4, None, True, 0), (6, None, False, 1),
+                                                       (4, 3, True, 0), (2, 5, False, 1), (16, None, False, 0)])
+def test_sub_layer_ring_windows_stay_exact(ring, pinned, host_codec, S):
+    """Budgets below two layers: the ring holds `ring` blocks per kind and each layer streams
+    in windows of ring/2 experts; results stay bit-identical to the resident model, the log
+    replays clean window by window and the arena never exceeds the ring (+ pinned)."""
+    import paper_2604_02715_b200 as X
+
+    spec = X.ModelSpec(3, 8, 128, 256)
+    fwd = X.ForwardSpec(24, 2, 3)
+    c = X.generate_synthetic_model(spec, 3, shared_experts=S)
+    backends = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 30e9, 1 << 40)]
+    hier = X.StorageHierarchy(c, None, X.plan_placement(spec, backends), backends)
+    x = X.initial_activations(spec, fwd, 3)
+    runner = X.StreamedRunner(spec, hier, fwd, host_codec=host_codec, pinned=pinned, ring_experts=ring)
+    rep = runner.run(2, acts=x.copy())
+    base = X.resident_baseline(2, spec, c, fwd, acts=x.copy())
+    assert rep.page_fault is None and rep.violations == []
+    assert rep.final_activations.tobytes() == base.tobytes()
+    p = pinned or 0
+    streamed = spec.experts_per_layer - p
+    ring_used = min(ring, 2 * streamed)
+    assert rep.arena_peak_bytes == ring_used * spec.expert_bytes + p * spec.num_layers * spec.expert_bytes
+    windows = max(1, -(-streamed // max(1, ring_used // 2)))
+    starts = [r for r in rep.records if r.event == "compute-start"]
+    assert len(starts) == 2 * spec.num_layers * windows
+    if windows > 1:
+        assert max(r.group for r in starts) == windows - 1
+        assert any(r.event == "recycle" and r.target_group is not None for r in rep.records)
+
+
+def test_sub_layer_ring_sabotage_faults():
+    import paper_2604_02715_b200 as X
+
+    spec = X.ModelSpec(3, 6, 64, 128)
+    c = X.generate_synthetic_model(spec, 2)
+    backends = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 30e9, 1 << 40)]
+    hier = X.StorageHierarchy(c, None, X.plan_placement(spec, backends), backends, lambda tid: 0.02)
+    runner = X.StreamedRunner(spec, hier, X.ForwardSpec(8, 2, 1), sabotage_skip_raw=(1, 2), ring_experts=2)
+    rep = runner.run(1)
+    assert rep.page_fault is not None
+    assert any(v.startswith("RAW") for v in rep.violations)
+
+
+def test_ring_experts_argument_checks():
+    import paper_2604_02715_b200 as X
+    from paper_2604_02715_b200.errors import OutOfRangeError
+
+    spec = X.ModelSpec(2, 4, 64, 128)
+    ctx = X.PageTable(spec).ctx
+    with pytest.raises(OutOfRangeError):
+        ctx.set_ring_experts(1)
+    ctx.set_ring_experts(-1)

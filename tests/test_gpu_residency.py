@@ -11,9 +11,9 @@ def test_live_controller_moves_experts_and_stays_exact():
     import paper_2604_02715_b200 as X
     from paper_2604_02715_b200 import residency as R
 
-    spec = X.ModelSpec(4, 8, 256, 512)
+    spec = X.ModelSpec(4, 8, 1024, 2048)  # 12.6 MB experts: page-in dominates a T=16 step
     fwd = X.ForwardSpec(16, 2, 7)
-    c = X.generate_synthetic_model(spec, 7)
+    c = X.generate_fast_model(spec, 7)
     backends = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 30e9, 1 << 40)]
     hier = X.StorageHierarchy(c, None, X.plan_placement(spec, backends), backends)
     runner = X.StreamedRunner(spec, hier, fwd, host_codec=True)
@@ -26,7 +26,8 @@ def test_live_controller_moves_experts_and_stays_exact():
     for _ in range(14):
         s = ctl.step(x.copy())
         assert s.tau_load > 0 and s.tau_comp > 0
-    # decode at T=16 is load-bound (rho << theta): the loop fills the budget and stops there
+    # decode at T=16 is load-bound (rho < theta): the loop fills the budget and stops there
+    assert all(s.rho < 0.9 for s in ctl.samples), [s.rho for s in ctl.samples]
     assert ctl.state.device_experts == 3
     assert runner.device_experts == [3, 3, 3, 3]
     assert any(s.adjusted == 1 for s in ctl.samples)

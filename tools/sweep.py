@@ -1,8 +1,10 @@
 """Sweeps for BASELINE configs 3 and 5 (one JSON line per point).
 
-    python tools/sweep.py budget [--config mixtral] [--tokens 256] [--raw]
-        paging budget from the 2-layer ring (25% at N=8) up to fully resident, by pinning
-        experts 1..m of every layer (residency tier x > 0); fully-resident comparator last
+    python tools/sweep.py budget [--config mixtral] [--tokens 256] [--raw] [--rings 6,8,12]
+        paging budget from a sub-layer ring (--rings: expert blocks per kind, below the
+        reference's two layers) through the 2-layer ring (25% at N=8) up to fully resident,
+        by pinning experts 1..m of every layer (residency tier x > 0); fully-resident
+        comparator beside every point
     python tools/sweep.py tokens [--config qwen3] [--list 1,4,16,64,256]
         decode batch sweep under the fixed 2-layer-ring budget
 """
@@ -36,6 +38,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--raw", action="store_true")
+    ap.add_argument("--rings", default="6,8,12", help="sub-layer ring sizes (expert blocks per kind) for budget")
     args = ap.parse_args()
     import torch
 
@@ -55,19 +58,24 @@ def main():
         hier.compressed = CompressedModel.from_container(container)
     peak = h2d_peak_gbps(torch, 0)
     print(f"setup {time.time() - t0:.1f}s", file=sys.stderr, flush=True)
-    points = list(range(0, L)) if args.what == "budget" else [int(t) for t in args.list.split(",")]
+    if args.what == "budget":
+        points = [("ring", int(r)) for r in args.rings.split(",") if r] + [("pinned", p) for p in range(0, L)]
+    else:
+        points = [("tokens", int(t)) for t in args.list.split(",")]
     resident_tok = {}
-    for p in points:
-        T = cfg["T"] if args.what == "budget" else p
+    for what, p in points:
+        T = p if what == "tokens" else cfg["T"]
         fwd = X.ForwardSpec(T, k, SEED)
         x = torch.from_numpy(X.initial_activations(spec, fwd, SEED)).cuda()
         runner = X.StreamedRunner(spec, hier, fwd, host_codec=not args.raw,
-                                  pinned=(p if args.what == "budget" else None))
+                                  pinned=(p if what == "pinned" else None),
+                                  ring_experts=(p if what == "ring" else None))
         runner.run(args.warmup, acts=x)
         secs, rep = timed(torch, lambda s: runner.run(s, acts=x), args.steps)
         hbm = runner.ctx.hbm_bytes()
         row = {"sweep": args.what, "config": args.config or cfg["name"], "T": T,
-               "pinned_per_layer": p if args.what == "budget" else 0,
+               "pinned_per_layer": p if what == "pinned" else 0,
+               "ring_experts": p if what == "ring" else 2 * (L - (p if what == "pinned" else 0)),
                "hbm_fraction": (hbm["ring"] + hbm["staging"] + hbm["device_tier"]) / spec.total_bytes,
                "tok_s": T * args.steps / secs, "ms_per_step": 1e3 * secs / args.steps,
                "page_in_gbps": rep.h2d_bytes / rep.elapsed_seconds / 1e9 if rep.elapsed_seconds else 0.0,
