@@ -42,7 +42,7 @@ def main():
     runner = X.StreamedRunner(spec, hier, fwd, host_codec=True)
     x = torch.from_numpy(X.initial_activations(spec, fwd, SEED)).cuda()
     b_dev, b_host = R.calibrate_bandwidths(runner, x)
-    budget = runner.device_tier_bytes(args.budget_experts) + 1
+    budget = runner.device_tier_bytes(spec.experts_per_layer) * (args.budget_experts + 0.5) / spec.experts_per_layer
     print(json.dumps({"setup_s": time.time() - t0, "config": args.config, "T": T, "b_dev_GBps": b_dev / 1e9,
                       "b_host_GBps": b_host / 1e9, "device_tier_budget_bytes": budget}), flush=True)
     ctl = R.LiveResidencyController(runner, R.PlannerState(spec.experts_per_layer, 1, cooldown=args.cooldown),
