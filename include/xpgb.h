@@ -107,6 +107,9 @@ typedef struct xpgb_run_opts {
   const float* compute_delay_s; /* optional [iterations][N] seconds (compute_delay_fn hook), host memory */
   int32_t log_enable;        /* record the ordering log (default on) */
   int32_t profile;           /* time every MoE kernel launch with CUDA events (report.kern_*) */
+  int32_t fresh_inputs;      /* 1: every iteration starts from activations the caller wrote into acts_dev
+                                (a serving session: step(acts) per decode step); 0: iteration i+1 consumes
+                                iteration i's output, as run() does */
 } xpgb_run_opts;
 
 typedef struct xpgb_report {
@@ -267,6 +270,10 @@ int xpgb_session_compute(xpgb_ctx* ctx, int32_t step);      /* built-in layer_fo
 int xpgb_session_release(xpgb_ctx* ctx, int32_t step, void* stream); /* compute-done + WAR event */
 int xpgb_session_end(xpgb_ctx* ctx, xpgb_report* rep);
 int xpgb_session_abort(xpgb_ctx* ctx);
+/* Shape of the active session's schedule and the stream the built-in compute runs on (the
+ * caller orders its own H2D/D2H of acts_dev on it).  steps_per_iteration = N in the reference
+ * geometry, N x windows with a sub-layer ring. */
+int xpgb_session_info(xpgb_ctx* ctx, int32_t* steps_total, int32_t* steps_per_iteration, void** compute_stream);
 /* Ordering log of the last run (OrderingLog.records, pipeline.py:94-116). */
 int xpgb_log_get(xpgb_ctx* ctx, xpgb_record* out, int32_t cap, int32_t* n);
 

@@ -44,7 +44,7 @@ class RunOpts(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("tokens", C.c_int32), ("top_k", C.c_int32), ("sequential", C.c_int32),
                 ("router_seed", C.c_uint64), ("sabotage_iteration", C.c_int32), ("sabotage_layer", C.c_int32),
                 ("fetch_delay_s", C.POINTER(C.c_float)), ("compute_delay_s", C.POINTER(C.c_float)),
-                ("log_enable", C.c_int32), ("profile", C.c_int32)]
+                ("log_enable", C.c_int32), ("profile", C.c_int32), ("fresh_inputs", C.c_int32)]
 
 
 class Report(C.Structure):
@@ -106,6 +106,7 @@ _SIGS = {
     "xpgb_session_release": [_P, _I, _P],
     "xpgb_session_end": [_P, C.POINTER(Report)],
     "xpgb_session_abort": [_P],
+    "xpgb_session_info": [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_void_p)],
     "xpgb_log_get": [_P, C.POINTER(Record), _I, C.POINTER(_I)],
     "xpgb_set_expert_shard": [_P, _I, _I],
     "xpgb_set_shared": [_P, _P, _U64, _I],

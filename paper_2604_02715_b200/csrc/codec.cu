@@ -148,17 +148,34 @@ struct DecodeParams {
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
 // One thread decodes one chunk (`chunk` values) starting at index[c]: a 64-bit
-// MSB-first window, a 4096-entry LUT for codes <= 12 bits, canonical
-// first-code search for longer ones.  Output words are assembled as
+// MSB-first window and a multi-symbol table -- every 11-bit pattern maps to the
+// up-to-3 whole codewords it starts with (exponents average ~2.6 bits, so one
+// lookup usually yields 3 values).  Codes longer than the table, and a chunk's
+// last values (never decode past the chunk), take the canonical first-code search.
+// The table is 8 KB of shared memory so decode blocks still fit beside a resident
+// GEMM CTA; the next bitstream word is always in flight.  Output words are
 // (sign << 15) | (exponent << 7) | mantissa, 8 per 16-byte store.
+constexpr int kMultiBits = 11;
+
+__device__ __forceinline__ int canon_decode(uint64_t win, int ml, const int* count, const uint32_t* first_code,
+                                            const int* first_rank, const uint8_t* sorted_sym, int* sym) {
+  for (int l = 1; l <= ml; ++l) {
+    const uint32_t code = (uint32_t)(win >> (64 - l));
+    if (count[l] && code - first_code[l] < (uint32_t)count[l]) {
+      *sym = sorted_sym[first_rank[l] + (code - first_code[l])];
+      return l;
+    }
+  }
+  return 0;  // invalid code: the host index scan rejects such streams before they get here
+}
+
 __global__ void __launch_bounds__(256) k_exp_decode(const __grid_constant__ DecodeParams p) {
-  __shared__ uint16_t lut[1 << kLutBits];
+  __shared__ uint32_t lut3[1 << kMultiBits];  // syms (3 x 8 b) | count << 24 | total length << 26
   __shared__ uint32_t first_code[kCodecMaxLen + 1];
   __shared__ int count[kCodecMaxLen + 1], first_rank[kCodecMaxLen + 1];
   __shared__ uint8_t sorted_sym[kCodecSymbols];
   __shared__ int maxlen;
   const int tid = threadIdx.x;
-  for (int i = tid; i < (1 << kLutBits); i += blockDim.x) lut[i] = 0;
   if (tid <= kCodecMaxLen) count[tid] = 0;
   __syncthreads();
   if (tid < kCodecSymbols && p.table.len[tid]) atomicAdd(&count[p.table.len[tid]], 1);
@@ -187,19 +204,31 @@ __global__ void __launch_bounds__(256) k_exp_decode(const __grid_constant__ Deco
       int r = 0;
       for (int s = 0; s < tid; ++s) r += (p.table.len[s] == l);
       sorted_sym[first_rank[l] + r] = (uint8_t)tid;
-      if (l <= kLutBits) {
-        const uint32_t code = first_code[l] + r;
-        const uint32_t base = code << (kLutBits - l), span = 1u << (kLutBits - l);
-        for (uint32_t i = 0; i < span; ++i) lut[base + i] = (uint16_t)(tid | (l << 8));
-      }
     }
+  }
+  __syncthreads();
+  const int ml = maxlen;
+  // whole codes at the head of every 11-bit pattern: a code is whole when its length
+  // fits the known bits (a prefix code is decided by its own bits only)
+  for (int i = tid; i < (1 << kMultiBits); i += blockDim.x) {
+    const uint64_t w = (uint64_t)i << (64 - kMultiBits);
+    uint32_t syms = 0;
+    int tot = 0, c = 0;
+    while (c < 3) {
+      int sym;
+      const int l = canon_decode(w << tot, ml, count, first_code, first_rank, sorted_sym, &sym);
+      if (!l || tot + l > kMultiBits) break;
+      syms |= (uint32_t)sym << (8 * c);
+      tot += l;
+      ++c;
+    }
+    lut3[i] = syms | ((uint32_t)c << 24) | ((uint32_t)tot << 26);
   }
   __syncthreads();
 
   const uint64_t n = p.n;
   const uint64_t cpt = (n + p.chunk - 1) / p.chunk;  // chunks per tensor
   const uint64_t n_chunks = cpt * (uint64_t)p.ntensors;
-  const int ml = maxlen;
   for (uint64_t gc = blockIdx.x * (uint64_t)blockDim.x + tid; gc < n_chunks; gc += (uint64_t)gridDim.x * blockDim.x) {
     const int ti = (int)(gc / cpt);
     const uint64_t c = gc - (uint64_t)ti * cpt;
@@ -210,39 +239,52 @@ __global__ void __launch_bounds__(256) k_exp_decode(const __grid_constant__ Deco
     const uint64_t v1 = (v0 + p.chunk < n) ? v0 + p.chunk : n;
     const uint32_t bitpos = d.index[c] - d.bit_base;
     const uint32_t w = bitpos >> 5, sh = bitpos & 31;
+    const uint32_t* __restrict__ wp = d.bits + w + 2;
     uint64_t win = (((uint64_t)bswap32(d.bits[w]) << 32) | bswap32(d.bits[w + 1])) << sh;
     int avail = 64 - (int)sh;
-    const uint32_t* wp = d.bits + w + 2;
+    uint32_t nxt = bswap32(*wp++);  // the next word is always in flight
+    uint64_t lo = 0, hi = 0;        // decoded exponent bytes not yet written (np of them)
+    int np = 0;
     for (uint64_t v = v0; v < v1; v += 8) {
       const int cnt = (int)((v1 - v) < 8 ? (v1 - v) : 8);
-      uint32_t packed[4] = {0, 0, 0, 0};
       uint2 smv = make_uint2(0, 0);
       if (cnt == 8) smv = *reinterpret_cast<const uint2*>(sm + v);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if (j >= cnt) break;
+      while (np < cnt) {
         if (avail < 32) {
-          win |= (uint64_t)bswap32(*wp++) << (32 - avail);
+          win |= (uint64_t)nxt << (32 - avail);
           avail += 32;
+          nxt = bswap32(*wp++);
         }
-        const uint16_t e = lut[win >> (64 - kLutBits)];
-        int l = e >> 8;
-        int sym = e & 0xFF;
-        if (!l) {
-          for (l = kLutBits + 1; l <= ml; ++l) {
-            const uint32_t code = (uint32_t)(win >> (64 - l));
-            if (count[l] && code - first_code[l] < (uint32_t)count[l]) {
-              sym = sorted_sym[first_rank[l] + (code - first_code[l])];
-              break;
-            }
-          }
+        const uint32_t e = lut3[win >> (64 - kMultiBits)];
+        int k = (e >> 24) & 3, l;
+        uint32_t bytes;
+        if (k == 0 || k > (int)(v1 - v) - np) {
+          int sym = 0;
+          l = canon_decode(win, ml, count, first_code, first_rank, sorted_sym, &sym);
+          bytes = (uint32_t)sym;
+          k = 1;
+        } else {
+          l = (int)(e >> 26);
+          bytes = e & 0xFFFFFFu;
         }
         win <<= l;
         avail -= l;
+        lo |= (uint64_t)bytes << (8 * np);  // np <= 7 here
+        if (np > 5) hi |= (uint64_t)bytes >> (64 - 8 * np);
+        np += k;
+      }
+      uint32_t packed[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j >= cnt) break;
+        const uint32_t sym = (uint32_t)(lo >> (8 * j)) & 0xFFu;
         const uint32_t s = (cnt == 8) ? (((j < 4 ? smv.x : smv.y) >> (8 * (j & 3))) & 0xFF) : sm[v + j];
-        const uint32_t word = ((s & 0x80u) << 8) | ((uint32_t)sym << 7) | (s & 0x7Fu);
+        const uint32_t word = ((s & 0x80u) << 8) | (sym << 7) | (s & 0x7Fu);
         packed[j >> 1] |= word << (16 * (j & 1));
       }
+      lo = hi;
+      hi = 0;
+      np -= cnt;
       if (cnt == 8) {
         *reinterpret_cast<uint4*>(out + v) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
       } else {

@@ -455,7 +455,8 @@ struct GemmCfg {
   static constexpr int NA = GU ? 2 : 1;  // A tiles per stage (gate + up)
   static constexpr int B_BYTES = BN * kBK * 2;
   static constexpr int STAGE = NA * A_BYTES + B_BYTES;
-  static constexpr int ACC_COLS = GU ? 256 : 128;  // TMEM columns per accumulator stage
+  // TMEM columns per accumulator stage: gate+up = 2 x 128; down = BN (128 or 256 for prefill)
+  static constexpr int ACC_COLS = GU ? 256 : (BN > 128 ? BN : 128);
   static constexpr int TMEM_COLS = 2 * ACC_COLS;
   static constexpr int TAB_BYTES = (3 * kMaxExperts + 8) * 4;
   static constexpr int SMEM = STAGES * STAGE + 1024 + 256 + TAB_BYTES;
@@ -700,6 +701,7 @@ void set_gemm_attrs() {
   set_attr<false, 32, 9>();
   set_attr<false, 64, 8>();
   set_attr<false, 128, 6>();
+  set_attr<false, 256, 4>();
 }
 
 void launch_gate_up(const CUtensorMap& map_w, const CUtensorMap& map_x, const CUtensorMap& map_ws,
@@ -719,7 +721,8 @@ void launch_down(const CUtensorMap& map_w, const CUtensorMap& map_h, const CUten
   int smem;
   if (bn == 32) { kern = k_moe_gemm<false, 32, 9>; smem = GemmCfg<false, 32, 9>::SMEM; }
   else if (bn == 64) { kern = k_moe_gemm<false, 64, 8>; smem = GemmCfg<false, 64, 8>::SMEM; }
-  else { kern = k_moe_gemm<false, 128, 6>; smem = GemmCfg<false, 128, 6>::SMEM; }
+  else if (bn == 128) { kern = k_moe_gemm<false, 128, 6>; smem = GemmCfg<false, 128, 6>::SMEM; }
+  else { kern = k_moe_gemm<false, 256, 4>; smem = GemmCfg<false, 256, 4>::SMEM; }
   kern<<<grid, 192, smem, s>>>(map_w, map_h, map_ws, p);
   note_launch();
 }

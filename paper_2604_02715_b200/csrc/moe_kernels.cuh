@@ -74,5 +74,11 @@ void launch_combine(const float* part, const int32_t* pos, const long long* faul
 void launch_reduce_rows(const float* part, const long long* fault, float* out, int n_rows, int H, int splits,
                         long long split_stride, cudaStream_t s);
 void set_gemm_attrs();
+// CTA-pair (cta_group::2) grouped GEMM for prefill-sized expert groups (moe_gemm_pair.cu):
+// 256 token rows x 256 weight rows per pair, unsplit (down writes split plane 0).
+bool pair_gemm_supported(int H, int F);
+void set_pair_gemm_attrs();
+void launch_gemm_pair(bool gate_up, const CUtensorMap& map_x, const CUtensorMap& map_w, const CUtensorMap& map_ws,
+                      const GemmParams& p, int num_sms, cudaStream_t s);
 
 }  // namespace xpgb

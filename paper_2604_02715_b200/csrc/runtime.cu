@@ -226,6 +226,8 @@ struct Ctx {
   int32_t* ep_off = nullptr;      // [E+1] scratch for experts_forward
   int last_splits = 1;
   CUtensorMap map_xp{}, map_h{};
+  CUtensorMap map_xp_pair{}, map_h_pair{};  // 128-row boxes: the CTA-pair prefill GEMM's A operand
+  int pair_mode = -1;                        // CTA-pair GEMM: -1 auto (prefill-sized groups), 0 off, 1 always
   long long* d_fault = nullptr;
 
   // log
@@ -378,9 +380,18 @@ static void ensure_work(Ctx* c, int T, int kk) {
   c->cap_rows = (int)rows;
   c->map_xp = make_map(c->xp, rows, c->H, kBoxRowsB);
   c->map_h = make_map(c->hbuf, rows, c->F, kBoxRowsB);
+  c->map_xp_pair = make_map(c->xp, rows, c->H, kBM);
+  c->map_h_pair = make_map(c->hbuf, rows, c->F, kBM);
 }
 
 static int pick_bn(int T) { return T <= 32 ? 32 : (T <= 64 ? 64 : 128); }
+
+// Down projection at prefill sizes: N = 256 token rows per tile halves the weight-tile
+// re-reads and the smem traffic per MMA flop (one 256-column accumulator, double-buffered).
+static int pick_bn_down(Ctx* c, int T, int kt) {
+  const long long per_expert = (long long)T * kt / std::max(1, std::min(c->E + c->S, T * kt));
+  return per_expert >= 384 ? 256 : pick_bn(T);
+}
 
 // Split-K factor for the down projection: balance (units x splits) over the SMs.
 static int pick_splits(Ctx* c, int T, int kk, int bn) {
@@ -448,7 +459,12 @@ static void enqueue_window(Ctx* c, int layer, const float* x, float* y, int T, i
   const int32_t* pos = c->plan_pos[b] + (size_t)(layer - 1) * T * kt;
   const int32_t* off = c->plan_off[b] + (size_t)(layer - 1) * (groups_of(c) + 1);
   const int bn = pick_bn(T);
-  const int splits = pick_splits(c, T, kt, bn);
+  const int bn_dn = pick_bn_down(c, T, kt);
+  // prefill-sized expert groups run on CTA pairs (256 x 256 tiles, unsplit)
+  const long long groups = std::max(1, std::min(e1 - e0, T * kt));
+  const bool pair = pair_gemm_supported(c->H, c->F) &&
+                    (c->pair_mode == 1 || (c->pair_mode < 0 && (long long)T * kt / groups >= 1024));
+  const int splits = pair ? 1 : pick_splits(c, T, kt, bn_dn);
   prof_rec(c, 1, s);
   if (gather) {
     launch_gather(x, pos, c->d_fault, c->xp, T, kt, c->H, s);
@@ -464,10 +480,16 @@ static void enqueue_window(Ctx* c, int layer, const float* x, float* y, int T, i
     p->E = e1 - e0;
     p->E_routed = std::max(0, std::min(e1, c->E) - e0);
   }
-  launch_gate_up(c->map_gu, c->map_xp, c->S ? c->map_gu_sh : c->map_gu, pg, bn, c->num_sms, s);
+  if (pair)
+    launch_gemm_pair(true, c->map_xp_pair, c->map_gu, c->S ? c->map_gu_sh : c->map_gu, pg, c->num_sms, s);
+  else
+    launch_gate_up(c->map_gu, c->map_xp, c->S ? c->map_gu_sh : c->map_gu, pg, bn, c->num_sms, s);
   CKLAUNCH();
   prof_rec(c, 4, s);
-  launch_down(c->map_dn, c->map_h, c->S ? c->map_dn_sh : c->map_dn, pd, bn, c->num_sms, s);
+  if (pair)
+    launch_gemm_pair(false, c->map_h_pair, c->map_dn, c->S ? c->map_dn_sh : c->map_dn, pd, c->num_sms, s);
+  else
+    launch_down(c->map_dn, c->map_h, c->S ? c->map_dn_sh : c->map_dn, pd, bn_dn, c->num_sms, s);
   CKLAUNCH();
   prof_rec(c, 5, s);
   if (last) {
@@ -1041,9 +1063,14 @@ static void session_compute(Ctx* c, int g) {
   }
   const int b = (it - 1) & 1;
   const bool last = (g + 1 == ss.steps);
+  const bool fresh = o->fresh_inputs != 0;  // each iteration gathers its own new inputs
   const int32_t* next_pos = nullptr;
-  if (!last && T > 0) next_pos = layer < c->N ? c->plan_pos[b] + (size_t)layer * T * kt : c->plan_pos[it & 1];
-  enqueue_window(c, layer, ss.rs.acts, ss.rs.acts, T, o->top_k, b, g == 0, st.e0, st.e1, st.last, next_pos, s);
+  if (!last && T > 0) {
+    if (layer < c->N) next_pos = c->plan_pos[b] + (size_t)layer * T * kt;
+    else if (!fresh) next_pos = c->plan_pos[it & 1];
+  }
+  const bool gather = g == 0 || (fresh && layer == 1 && st.first);
+  enqueue_window(c, layer, ss.rs.acts, ss.rs.acts, T, o->top_k, b, gather, st.e0, st.e1, st.last, next_pos, s);
   c->cur_ev = nullptr;
 }
 
@@ -1362,6 +1389,8 @@ int xpgb_create(const xpgb_spec* spec, int32_t device, int32_t pool, int32_t max
     c->s2 = 2ull * c->F * c->H;
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     set_gemm_attrs();
+    set_pair_gemm_attrs();
+    if (const char* env = getenv("XPGB_PAIR_GEMM")) c->pair_mode = atoi(env) ? 1 : 0;
     for (int k = 0; k < 2; ++k) CK(cudaStreamCreateWithFlags(&c->s_copy[k], cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
     for (int k = 0; k < 2; ++k)
@@ -2005,6 +2034,15 @@ int xpgb_session_end(xpgb_ctx* h, xpgb_report* rep) {
 int xpgb_session_abort(xpgb_ctx* h) {
   return guard([&] { session_abort(&h->c); });
 }
+int xpgb_session_info(xpgb_ctx* h, int32_t* steps_total, int32_t* steps_per_iteration, void** compute_stream) {
+  return guard([&] {
+    Session& ss = session_of(&h->c);
+    if (!ss.active) XFAIL(XPGB_ERR, "no active session");
+    if (steps_total) *steps_total = ss.steps;
+    if (steps_per_iteration) *steps_per_iteration = ss.steps / std::max(1, ss.o.iterations);
+    if (compute_stream) *compute_stream = (void*)h->c.s_comp;
+  });
+}
 
 int xpgb_log_get(xpgb_ctx* h, xpgb_record* out, int32_t cap, int32_t* n) {
   return guard([&] {
@@ -2104,7 +2142,8 @@ int xpgb_profile_layer(xpgb_ctx* h, int32_t layer, const float* x_dev, float* y_
       if (n <= 0) continue;
       ++active;
       u1 += (long long)((n + bn - 1) / bn) * ((c->F + kBM - 1) / kBM);
-      u2 += (long long)((n + bn - 1) / bn) * ((c->H + kBM - 1) / kBM) * c->last_splits;
+      const int bd = pick_bn_down(c, tokens, kt);
+      u2 += (long long)((n + bd - 1) / bd) * ((c->H + kBM - 1) / kBM) * c->last_splits;
     }
     const long long pairs = offs[G];  // rows this device computes (local routed + shared)
     (void)kt;

@@ -308,6 +308,9 @@ class StreamedRunner:
         out, rep = _run_context(self.ctx, self.spec, self.fwd, iterations, acts, self.mode == "sequential",
                                 fetch_delay=self.hierarchy.delay_table(), compute_delay=cd,
                                 sabotage=self.sabotage_skip_raw, profile=profile)
+        return self._report(out, rep)
+
+    def _report(self, out, rep) -> RunReport:
         self.table.sync_trace()
         records = _records_from_log(self.ctx)
         self.stall_seconds = rep.stall_ns * 1e-9
@@ -328,6 +331,112 @@ class StreamedRunner:
             kernels=_kernel_stats(rep),
             decoded_bytes=int(rep.decoded_bytes),
         )
+
+    def open_session(self, max_iterations: int, log: bool = True) -> "DecodeSession":
+        """A serving session: ``step(acts)`` runs one decode iteration on new activations while
+        the copy streams keep prefetching the next iteration's first layers in the background."""
+        return DecodeSession(self, max_iterations, log=log)
+
+
+class DecodeSession:
+    """One long schedule of up to ``max_iterations`` decode steps, fed one step at a time.
+
+    ``run(iterations)`` starts every call from an empty ring, so the first two layers of
+    each call page in with nothing to overlap.  A session keeps the schedule open between
+    calls: while the caller prepares step i+1 (attention, sampling), layers 1-2 of step
+    i+1 are already paging in -- the reference's lookahead carried across decode steps.
+    Each step copies its inputs into the device activation buffer on the library's compute
+    stream (H2D from pinned memory when given a pinned tensor), runs the step's layers, and
+    copies the output back (``out=`` pinned tensor, or a new numpy array).
+    """
+
+    def __init__(self, runner: StreamedRunner, max_iterations: int, log: bool = True):
+        torch = _torch()
+        if max_iterations < 1:
+            raise XpgError("need at least one iteration")
+        self.runner, self.max_iterations = runner, max_iterations
+        spec, fwd, ctx = runner.spec, runner.fwd, runner.ctx
+        self.acts = torch.zeros(fwd.tokens_per_step, spec.hidden_dim, dtype=torch.float32,
+                                device=f"cuda:{ctx.device}")
+        opts = _lib.RunOpts()
+        opts.iterations = max_iterations
+        opts.tokens = fwd.tokens_per_step
+        opts.top_k = fwd.top_k
+        opts.router_seed = int(fwd.router_seed) & 0xFFFFFFFFFFFFFFFF
+        opts.log_enable = 1 if log else 0
+        opts.fresh_inputs = 1
+        h = ctx.handle
+        call("xpgb_session_begin", h, C.byref(opts), C.c_void_p(self.acts.data_ptr()))
+        total, per_it, stream = C.c_int32(), C.c_int32(), C.c_void_p()
+        call("xpgb_session_info", h, C.byref(total), C.byref(per_it), C.byref(stream))
+        self.steps_total, self.steps_per_iteration = total.value, per_it.value
+        self._stream_ptr = stream.value
+        self.stream = torch.cuda.ExternalStream(stream.value, device=f"cuda:{ctx.device}")
+        self.g = 0
+        self.iteration = 0
+        self.closed = False
+        try:
+            call("xpgb_session_materialize", h, 0)
+            call("xpgb_session_materialize", h, 1)
+        except Exception:
+            _lib.lib().xpgb_session_abort(h)
+            raise
+
+    def step(self, acts, out=None):
+        torch = _torch()
+        if self.closed:
+            raise XpgError("session is closed")
+        if self.iteration >= self.max_iterations:
+            raise XpgError(f"session holds {self.max_iterations} iterations")
+        h = self.runner.ctx.handle
+        src = torch.from_numpy(np.ascontiguousarray(acts, dtype=np.float32)) if isinstance(acts, np.ndarray) else acts
+        # host copies run on torch's stream (its pinned-memory allocator tracks only its own
+        # streams) and are ordered against the library's compute stream by events
+        cur = torch.cuda.current_stream(self.acts.device)
+        self.acts.copy_(src, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        self.stream.wait_event(ev)
+        try:
+            for _ in range(self.steps_per_iteration):
+                call("xpgb_session_acquire", h, self.g, C.c_void_p(self._stream_ptr))
+                call("xpgb_session_compute", h, self.g)
+                call("xpgb_session_release", h, self.g, C.c_void_p(self._stream_ptr))
+                call("xpgb_session_materialize", h, self.g + 2)
+                self.g += 1
+        except Exception:
+            _lib.lib().xpgb_session_abort(h)
+            self.closed = True
+            raise
+        self.iteration += 1
+        dst = out if out is not None else torch.empty(self.acts.shape, dtype=torch.float32,
+                                                      pin_memory=True)
+        done = torch.cuda.Event()
+        done.record(self.stream)
+        cur.wait_event(done)
+        dst.copy_(self.acts, non_blocking=True)
+        cur.synchronize()
+        return dst if out is not None else dst.numpy()
+
+    def close(self) -> RunReport:
+        """End the schedule (pages still bound are released) and report over the steps run."""
+        if self.closed:
+            raise XpgError("session is closed")
+        rep = _lib.Report()
+        call("xpgb_session_end", self.runner.ctx.handle, C.byref(rep))
+        self.closed = True
+        return self.runner._report(self.acts, rep)
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        if not self.closed:
+            if exc[0] is None:
+                self.close()
+            else:
+                _lib.lib().xpgb_session_abort(self.runner.ctx.handle)
+                self.closed = True
 
 
 def _kernel_stats(rep) -> dict:

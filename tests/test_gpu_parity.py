@@ -261,12 +261,15 @@ def test_session_api_external_compute_matches_run(X):
     h = runner.ctx.handle
     torch.cuda.synchronize()
     call("xpgb_session_begin", h, C.byref(opts), C.c_void_p(acts.data_ptr()))
+    total, per_it, st = C.c_int32(), C.c_int32(), C.c_void_p()
+    call("xpgb_session_info", h, C.byref(total), C.byref(per_it), C.byref(st))
+    assert (total.value, per_it.value) == (2 * spec.num_layers, spec.num_layers)
     call("xpgb_session_materialize", h, 0)
     call("xpgb_session_materialize", h, 1)
-    for g in range(2 * spec.num_layers):
-        call("xpgb_session_acquire", h, g, None)
+    for g in range(2 * spec.num_layers):  # built-in compute runs on the session's compute stream
+        call("xpgb_session_acquire", h, g, st)
         call("xpgb_session_compute", h, g)
-        call("xpgb_session_release", h, g, None)
+        call("xpgb_session_release", h, g, st)
         call("xpgb_session_materialize", h, g + 2)
     rep = _lib.Report()
     call("xpgb_session_end", h, C.byref(rep))
@@ -296,7 +299,7 @@ def test_pinned_experts_budget_tier(X, pinned, host_codec):
     assert rep2.page_fault is None and rep2.violations == []
 
 
-@pytest.mark.parametrize("L,k,T", [(8, 2, 1500), (128, 8, 300), (64, 4, 4097), (3, 5, 700)])
+@pytest.mark.parametrize("L,k,T", [(8, 2, 1500), (128, 8, 300), (64, 4, 4097), (3, 5, 700), (4, 2, 2001)])
 def test_multi_cta_plan_layer_forward_vs_oracle(X, O, L, k, T):
     """T*k above the single-CTA plan threshold: route+count / scan+place over many CTAs.
     Layer output within tolerance of the oracle, and the resident run of the same step
@@ -313,3 +316,32 @@ def test_multi_cta_plan_layer_forward_vs_oracle(X, O, L, k, T):
     model = X.ResidentModel(spec, container, max_tokens=T)
     out, _ = model.run(1, fwd, x.copy())
     assert np.asarray(out).tobytes() == np.asarray(y2).tobytes()
+
+
+@pytest.mark.parametrize("ring,host_codec", [(None, False), (4, True)])
+def test_decode_session_steps_equal_resident(X, ring, host_codec):
+    """A serving session: each step runs one decode iteration on fresh inputs while the next
+    step's first layers prefetch; every output equals the resident model on that input."""
+    spec = X.ModelSpec(4, 8, 256, 512)
+    fwd = X.ForwardSpec(16, 2, 7)
+    container, hier = _hier(X, spec, seed=7)
+    runner = X.StreamedRunner(spec, hier, fwd, host_codec=host_codec, ring_experts=ring)
+    model = X.ResidentModel(spec, container, max_tokens=16)
+    rng = np.random.default_rng(0)
+    sess = runner.open_session(max_iterations=5)
+    for i in range(3):  # closes early: 3 of 5
+        x = rng.standard_normal((16, 256), dtype=np.float32)
+        got = sess.step(x)
+        want, _ = model.run(1, fwd, x.copy())
+        assert np.asarray(got).tobytes() == np.asarray(want).tobytes(), i
+    rep = sess.close()
+    assert rep.violations == [] and rep.page_fault is None
+    assert sum(1 for r in rep.records if r.event == "compute-start") == 3 * sess.steps_per_iteration
+    with pytest.raises(X.XpgError):
+        sess.close()
+    # the runner is reusable afterwards, also through the context-manager form
+    x = rng.standard_normal((16, 256), dtype=np.float32)
+    with runner.open_session(max_iterations=1) as s2:
+        assert np.asarray(s2.step(x)).tobytes() == np.asarray(model.run(1, fwd, x.copy())[0]).tobytes()
+    r2 = runner.run(1, acts=x.copy())
+    assert r2.violations == [] and r2.final_activations.tobytes() == np.asarray(model.run(1, fwd, x.copy())[0]).tobytes()
