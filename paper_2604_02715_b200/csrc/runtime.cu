@@ -384,7 +384,15 @@ static void ensure_work(Ctx* c, int T, int kk) {
   c->map_h_pair = make_map(c->hbuf, rows, c->F, kBM);
 }
 
-static int pick_bn(int T) { return T <= 32 ? 32 : (T <= 64 ? 64 : 128); }
+static int pick_bn(int T) {
+  static const int forced = [] {  // XPGB_BN=32|64|128: tile experiments (profiling only)
+    const char* e = getenv("XPGB_BN");
+    const int v = e ? atoi(e) : 0;
+    return (v == 32 || v == 64 || v == 128) ? v : 0;
+  }();
+  if (forced) return forced;
+  return T <= 32 ? 32 : (T <= 64 ? 64 : 128);
+}
 
 // Down projection at prefill sizes: N = 256 token rows per tile halves the weight-tile
 // re-reads and the smem traffic per MMA flop (one 256-column accumulator, double-buffered).
