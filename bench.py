@@ -272,7 +272,16 @@ _T0 = time.time()
 
 
 def log(msg):
-    print(f"[bench {time.time() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+    mem = ""
+    try:
+        import torch
+
+        if torch.cuda.is_available() and torch.cuda.is_initialized():
+            free, total = torch.cuda.mem_get_info()
+            mem = f" [HBM free {free / 2**30:.1f}/{total / 2**30:.1f} GiB]"
+    except Exception:
+        pass
+    print(f"[bench {time.time() - _T0:7.1f}s] {msg}{mem}", file=sys.stderr, flush=True)
 
 
 def main():
@@ -428,6 +437,7 @@ def main():
     torch.cuda.synchronize()
     if sess is not None:
         sess.close()
+        del sess  # the session holds the runner (and its HBM ring) alive
     e2e_elapsed = max_over_ranks(torch, world, e0.elapsed_time(e1) * 1e-3, dev)
     e2e_value = T * e2e_steps * world / e2e_elapsed
     assert tuple(out.shape) == x_host.shape  # (deep synthetic stacks overflow by design)
@@ -438,6 +448,10 @@ def main():
     kern = rep.kernels
     if not args.no_resident and not use_ep:
         del runner
+        import gc
+
+        gc.collect()
+        torch.cuda.empty_cache()
         model = X.ResidentModel(spec, container, device=dev, max_tokens=T_run, **run_kw)
         model.run(args.warmup, fwd, x_dev)
         torch.cuda.synchronize()

@@ -151,6 +151,11 @@ int xpgb_sync(xpgb_ctx* ctx);
 /* Exact-size pinned (page-locked, portable) host allocation, no context needed. */
 int xpgb_pinned_alloc(uint64_t bytes, void** out);
 int xpgb_pinned_free(void* ptr);
+/* Container ingest (model.py:142-202 without the read copy): page-lock caller memory, e.g. an
+ * mmap'd XPGW file, so the page-in DMAs straight from the page cache.  The range is widened to
+ * whole pages; read_only = 1 for PROT_READ mappings (cudaHostRegisterReadOnly). */
+int xpgb_host_register(void* ptr, uint64_t bytes, int32_t read_only);
+int xpgb_host_unregister(void* ptr);
 /* Allocate a pinned host pool of total_bytes; *host_ptr receives it for filling. */
 int xpgb_host_pool_alloc(xpgb_ctx* ctx, void** host_ptr, uint64_t* bytes);
 /* Use caller memory (cudaHostRegister'd here) as the host pool. */
@@ -203,10 +208,11 @@ int xpgb_codec_pack(const void* payload, int32_t n_tensors, const uint64_t* valu
                     uint64_t* pool_bytes, uint64_t* rec_offsets, uint64_t* bits_lens, uint64_t* bit_counts);
 /* Byte size of a packed record. */
 uint64_t xpgb_codec_record_bytes(uint64_t n, uint64_t bits_len, int32_t chunk);
-/* Rebuild the chunk index of a stream on the host, validating it like decompress():
+/* Rebuild the chunk index of a stream on the host, validating it like decompress()
+ * (consumed_bits, nullable: the exact exponent bit count the stream codes):
  * TruncatedStreamError / InvalidCodeError statuses (codec.py:304-327). */
 int xpgb_codec_index(const void* bits, uint64_t bits_len, uint64_t n, const uint8_t* lengths256, int32_t chunk,
-                     uint32_t* index_out);
+                     uint32_t* index_out, uint64_t* consumed_bits);
 /* decompress() on the GPU: packed record in device memory -> n bf16 words at out_dev. */
 int xpgb_codec_decode(const void* record_dev, uint64_t n, uint64_t bits_len, int32_t chunk,
                       const uint8_t* lengths256, void* out_dev, void* stream);

@@ -34,6 +34,7 @@ from .geometry import (
     generate_synthetic_model,
     initial_activations,
     iter_tensor_ids,
+    open_container,
     tensor_offset,
 )
 from .pagetable import AddressSpace, PageState, PageTable, page_vaddr, target_layer

@@ -110,6 +110,8 @@ _SIGS = {
     "xpgb_log_get": [_P, C.POINTER(Record), _I, C.POINTER(_I)],
     "xpgb_set_expert_shard": [_P, _I, _I],
     "xpgb_set_shared": [_P, _P, _U64, _I],
+    "xpgb_host_register": [_P, _U64, _I],
+    "xpgb_host_unregister": [_P],
     "xpgb_set_ring_experts": [_P, _I],
     "xpgb_set_shared_tokens": [_P, _I, _I],
     "xpgb_experts_forward": [_P, _I, _P, _P, _I, _P, _P],
@@ -121,7 +123,7 @@ _SIGS = {
                         C.POINTER(_U64),
                         C.POINTER(_U64), C.POINTER(_U64), C.POINTER(_U64)],
     "xpgb_codec_record_bytes": [_U64, _U64, _I],
-    "xpgb_codec_index": [_P, _U64, _U64, C.POINTER(C.c_uint8), _I, C.POINTER(C.c_uint32)],
+    "xpgb_codec_index": [_P, _U64, _U64, C.POINTER(C.c_uint8), _I, C.POINTER(C.c_uint32), C.POINTER(_U64)],
     "xpgb_codec_decode": [_P, _U64, _U64, _I, C.POINTER(C.c_uint8), _P, _P],
     "xpgb_set_codec": [_P, _P, _U64, C.POINTER(_U64), C.POINTER(_U64), C.POINTER(C.c_uint8), _I, _I],
     "xpgb_set_pinned": [_P, C.POINTER(C.c_uint8)],

@@ -215,6 +215,7 @@ struct Ctx {
 
   // workspace
   int cap_T = 0, cap_kk = 0, cap_rows = 0, cap_splits = 8;
+  long long part_rows = 0;  // rows of `part`: split-K planes are packed at the launch's row count
   // routing plans: buffer 0/1 alternate per iteration of a run, buffer 2 serves layer_forward
   int32_t* plan_topk[3] = {nullptr, nullptr, nullptr};  // [N][T][kk]
   int32_t* plan_pos[3] = {nullptr, nullptr, nullptr};   // [N][T][kk]
@@ -222,7 +223,7 @@ struct Ctx {
   int32_t* plan_scr[3] = {nullptr, nullptr, nullptr};   // [2][N][E] multi-CTA plan counters
   __nv_bfloat16* xp = nullptr;  // [cap_rows][H]
   __nv_bfloat16* hbuf = nullptr;  // [cap_rows][F]
-  float* part = nullptr;          // [cap_splits][cap_rows][H]
+  float* part = nullptr;          // [part_rows][H]: splits x (rows of a launch) x H
   int32_t* ep_off = nullptr;      // [E+1] scratch for experts_forward
   int last_splits = 1;
   CUtensorMap map_xp{}, map_h{};
@@ -373,7 +374,10 @@ static void ensure_work(Ctx* c, int T, int kk) {
   CK(cudaMemset(c->xp, 0, (size_t)rows * c->H * 2));
   CK(cudaMalloc(&c->hbuf, (size_t)rows * c->F * 2));
   CK(cudaMemset(c->hbuf, 0, (size_t)rows * c->F * 2));
-  CK(cudaMalloc(&c->part, (size_t)c->cap_splits * rows * c->H * 4));
+  // split-K only pays for few rows (decode); prefill launches run unsplit, so the partial
+  // buffer holds all rows once, or up to 8 planes of small launches
+  c->part_rows = std::max<long long>(rows, (long long)c->cap_splits * std::min<long long>(rows, 4096));
+  CK(cudaMalloc(&c->part, (size_t)c->part_rows * c->H * 4));
   CK(cudaMalloc(&c->ep_off, (size_t)(E + 1) * 4));
   c->cap_T = nT;
   c->cap_kk = nkk;
@@ -404,13 +408,14 @@ static int pick_bn_down(Ctx* c, int T, int kt) {
 // Split-K factor for the down projection: balance (units x splits) over the SMs.
 static int pick_splits(Ctx* c, int T, int kk, int bn) {
   const int KB = (c->F + kBK - 1) / kBK;
+  const long long max_s = std::min<long long>(c->cap_splits, c->part_rows / std::max<long long>(1, (long long)T * kk));
   const long long active = std::min<long long>(c->E, (long long)T * kk);
   if (active <= 0) return 1;
   const long long rows_per = std::max<long long>(1, ((long long)T * kk + active - 1) / active);
   const long long tiles = active * ((c->H + kBM - 1) / kBM) * ((rows_per + bn - 1) / bn);
   int best = 1;
   double best_eff = -1;
-  for (int s = 1; s <= c->cap_splits; ++s) {
+  for (int s = 1; s <= max_s; ++s) {
     if (KB / s < 4) break;
     const double work = (double)tiles * s / c->num_sms;
     const double eff = work / std::ceil(work) * std::min(1.0, work);  // wave quantisation x fill
@@ -432,7 +437,7 @@ static GemmParams gemm_params(Ctx* c, int layer, int kind, const int32_t* offset
   p.fault = c->d_fault;
   p.hbuf = c->hbuf;
   p.part = c->part;
-  p.split_stride = (long long)c->cap_rows * c->H;
+  p.split_stride = 0;  // set per launch: (rows of the launch) x H
   p.layer = layer;
   p.e_first = c->e_first;
   p.E = with_shared ? groups_of(c) : c->E;
@@ -468,10 +473,13 @@ static void enqueue_window(Ctx* c, int layer, const float* x, float* y, int T, i
   const int32_t* off = c->plan_off[b] + (size_t)(layer - 1) * (groups_of(c) + 1);
   const int bn = pick_bn(T);
   const int bn_dn = pick_bn_down(c, T, kt);
-  // prefill-sized expert groups run on CTA pairs (256 x 256 tiles, unsplit)
-  const long long groups = std::max(1, std::min(e1 - e0, T * kt));
+  // expert groups of >= 128 rows on average run on CTA pairs (256 x 256 tiles, unsplit);
+  // measured crossover on B200 (profiles/r1_pair_crossover.jsonl): at 64 rows per expert the
+  // 1-CTA swap-AB kernel is ahead, from 128 rows the pair kernel wins (up to 2.4x at 8K rows)
+  const double local_rows = (double)T * kk * c->E / c->L + (double)std::max(0, std::min(T, c->sh1) - c->sh0) * c->S;
+  const double per_group = local_rows / std::max(1, c->E + c->S);
   const bool pair = pair_gemm_supported(c->H, c->F) &&
-                    (c->pair_mode == 1 || (c->pair_mode < 0 && (long long)T * kt / groups >= 1024));
+                    (c->pair_mode == 1 || (c->pair_mode < 0 && per_group >= 128.0));
   const int splits = pair ? 1 : pick_splits(c, T, kt, bn_dn);
   prof_rec(c, 1, s);
   if (gather) {
@@ -481,6 +489,8 @@ static void enqueue_window(Ctx* c, int layer, const float* x, float* y, int T, i
   prof_rec(c, 2, s);
   prof_rec(c, 3, s);
   GemmParams pg = gemm_params(c, layer, 1, off, 1), pd = gemm_params(c, layer, 2, off, splits);
+  const long long split_stride = (long long)T * kt * c->H;
+  pd.split_stride = split_stride;
   for (GemmParams* p : {&pg, &pd}) {  // restrict to the window: groups [e0, e1)
     p->offsets += e0;
     p->pt += std::min(e0, c->E);
@@ -501,7 +511,7 @@ static void enqueue_window(Ctx* c, int layer, const float* x, float* y, int T, i
   CKLAUNCH();
   prof_rec(c, 5, s);
   if (last) {
-    launch_combine(c->part, pos, c->d_fault, y, T, kt, kk, c->H, splits, (long long)c->cap_rows * c->H,
+    launch_combine(c->part, pos, c->d_fault, y, T, kt, kk, c->H, splits, split_stride,
                    (float)(1.0 / top_k), next_pos, c->xp, s);
     CKLAUNCH();
   }
@@ -1471,6 +1481,32 @@ int xpgb_pinned_alloc(uint64_t bytes, void** out) {
     CK(cudaHostAlloc(out, std::max<uint64_t>(bytes, 1), cudaHostAllocPortable));
   });
 }
+int xpgb_host_register(void* ptr, uint64_t bytes, int32_t read_only) {
+  return guard([&] {
+    if (!ptr || !bytes) XFAIL(XPGB_ERR, "null host range");
+    const uintptr_t page = 4096, a = reinterpret_cast<uintptr_t>(ptr) & ~(page - 1);
+    const uintptr_t b = (reinterpret_cast<uintptr_t>(ptr) + bytes + page - 1) & ~(page - 1);
+    unsigned flags = cudaHostRegisterPortable | (read_only ? cudaHostRegisterReadOnly : 0u);
+    cudaError_t e = cudaHostRegister(reinterpret_cast<void*>(a), b - a, flags);
+    if (e == cudaErrorHostMemoryAlreadyRegistered) {
+      cudaGetLastError();
+      return;
+    }
+    if (e != cudaSuccess) throw Err{XPGB_ERR_CUDA, std::string("cudaHostRegister: ") + cudaGetErrorString(e)};
+  });
+}
+
+int xpgb_host_unregister(void* ptr) {
+  return guard([&] {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(ptr) & ~uintptr_t(4095);
+    cudaError_t e = cudaHostUnregister(reinterpret_cast<void*>(a));
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      XFAIL(XPGB_ERR_CUDA, "cudaHostUnregister: %s", cudaGetErrorString(e));
+    }
+  });
+}
+
 int xpgb_pinned_free(void* ptr) {
   return guard([&] {
     if (ptr) CK(cudaFreeHost(ptr));
@@ -1783,13 +1819,14 @@ int xpgb_codec_pack(const void* payload, int32_t n_tensors, const uint64_t* valu
 }
 
 int xpgb_codec_index(const void* bits, uint64_t bits_len, uint64_t n, const uint8_t* lengths256, int32_t chunk,
-                     uint32_t* index_out) {
+                     uint32_t* index_out, uint64_t* consumed_bits) {
   return guard([&] {
     if (chunk <= 0 || chunk % 8) XFAIL(XPGB_ERR_CONFIG, "codec chunk must be a positive multiple of 8");
     size_t used = 0;
     const int r = codec_build_index(static_cast<const uint8_t*>(bits), bits_len, n, lengths256, chunk, index_out, &used);
     if (r == 1) XFAIL(XPGB_ERR_TRUNCATED_STREAM, "bitstream ended before all %llu values", (unsigned long long)n);
     if (r == 2) XFAIL(XPGB_ERR_INVALID_CODE, "no codeword matches a bit pattern in the stream");
+    if (consumed_bits) *consumed_bits = used;
   });
 }
 
@@ -2092,10 +2129,11 @@ int xpgb_experts_forward(xpgb_ctx* h, int32_t layer, const void* rows_dev, const
     launch_gate_up(c->map_gu, c->map_xp, c->map_gu, gemm_params(c, layer, 1, offsets_dev, 1, false), bn, c->num_sms,
                    s);
     CKLAUNCH();
-    launch_down(c->map_dn, c->map_h, c->map_dn, gemm_params(c, layer, 2, offsets_dev, splits, false), bn, c->num_sms,
-                s);
+    GemmParams pd = gemm_params(c, layer, 2, offsets_dev, splits, false);
+    pd.split_stride = (long long)n_rows * c->H;
+    launch_down(c->map_dn, c->map_h, c->map_dn, pd, bn, c->num_sms, s);
     CKLAUNCH();
-    launch_reduce_rows(c->part, c->d_fault, out_dev, n_rows, c->H, splits, (long long)c->cap_rows * c->H, s);
+    launch_reduce_rows(c->part, c->d_fault, out_dev, n_rows, c->H, splits, pd.split_stride, s);
     CKLAUNCH();
   });
 }

@@ -226,6 +226,18 @@ def compress(data, table: HuffmanTable, tensor_id=None, chunk: int = DEFAULT_CHU
                             tensor_id, index[:nidx].tobytes(), chunk)
 
 
+def _stream_bits(ct: CompressedTensor, table: HuffmanTable) -> int:
+    """Exact exponent bit count of a stream (host scan; XPGC does not store it)."""
+    if ct.exponent_bit_count or not ct.value_count:
+        return int(ct.exponent_bit_count)
+    nb = len(ct.exponent_bitstream)
+    bits = np.frombuffer(ct.exponent_bitstream, dtype=np.uint8) if nb else np.zeros(1, np.uint8)
+    used = C.c_uint64()
+    call("xpgb_codec_index", C.c_void_p(bits.ctypes.data), C.c_uint64(nb), C.c_uint64(ct.value_count),
+         _u8p(table.lengths_array()), ct.chunk, None, C.byref(used))
+    return int(used.value)
+
+
 def _record(ct: CompressedTensor, table: HuffmanTable) -> np.ndarray:
     """Packed record (sm | stream + 8 pad | index), 16-byte aligned parts."""
     n, nb, ch = ct.value_count, len(ct.exponent_bitstream), ct.chunk
@@ -234,7 +246,7 @@ def _record(ct: CompressedTensor, table: HuffmanTable) -> np.ndarray:
         idx = np.zeros(max(1, (n + ch - 1) // ch), dtype=np.uint32)
         bits = np.frombuffer(ct.exponent_bitstream, dtype=np.uint8) if nb else np.zeros(1, np.uint8)
         call("xpgb_codec_index", C.c_void_p(bits.ctypes.data), C.c_uint64(nb), C.c_uint64(n),
-             _u8p(table.lengths_array()), ch, idx.ctypes.data_as(C.POINTER(C.c_uint32)))
+             _u8p(table.lengths_array()), ch, idx.ctypes.data_as(C.POINTER(C.c_uint32)), None)
         index = idx[:(n + ch - 1) // ch].tobytes()
     size = int(lib().xpgb_codec_record_bytes(n, nb, ch))
     rec = np.zeros(size, dtype=np.uint8)
@@ -438,14 +450,7 @@ class CompressedModel:
         for i, r in enumerate(recs):
             arr[int(offs[i]):int(offs[i]) + r.size] = r
         lengths = table.code_lengths
-        bit_counts = []
-        for ct in cts:
-            if ct.exponent_bit_count:
-                bit_counts.append(ct.exponent_bit_count)
-            else:  # not stored in XPGC: exact count from the stream's exponent histogram
-                words = np.frombuffer(decompress(ct, table), dtype="<u2") if ct.value_count else np.zeros(0, "<u2")
-                hist = np.bincount((words >> 7) & 0xFF, minlength=NUM_SYMBOLS)
-                bit_counts.append(int(sum(int(c) * lengths[s] for s, c in enumerate(hist) if c)))
+        bit_counts = [_stream_bits(ct, table) for ct in cts]
         return cls(spec, table, pool, offs, [len(ct.exponent_bitstream) for ct in cts], bit_counts, chunk)
 
     def write(self, path) -> None:

@@ -129,3 +129,21 @@ def test_grouped_record_runs_exact(X, alpha, host_codec, pinned):
     iterations, streamed_experts = 2, spec.num_layers * (spec.experts_per_layer - (pinned or 0))
     assert rep.decoded_bytes == iterations * streamed_experts * spec.expert_bytes  # every streamed tensor decoded
 
+
+
+def test_mmap_container_pages_in_exactly(X, tmp_path):
+    """A container ingested by mmap + in-place page-locking streams like the pinned copy."""
+    spec = X.ModelSpec(4, 8, 256, 512)
+    fwd = X.ForwardSpec(16, 2, 7)
+    c = X.generate_synthetic_model(spec, 7)
+    path = tmp_path / "m.xpgw"
+    c.write(path)
+    o = X.open_container(path)
+    backends = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 30e9, 1 << 40)]
+    for host_codec in (False, True):
+        hier = X.StorageHierarchy(o, None, X.plan_placement(spec, backends), backends)
+        x = X.initial_activations(spec, fwd, 7)
+        rep = X.StreamedRunner(spec, hier, fwd, host_codec=host_codec).run(2, acts=x.copy())
+        base = X.resident_baseline(2, spec, c, fwd, acts=x.copy())
+        assert rep.violations == [] and rep.page_fault is None
+        assert rep.final_activations.tobytes() == base.tobytes()

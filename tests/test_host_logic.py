@@ -170,3 +170,53 @@ def test_shared_experts_continue_the_generator_stream():
                            * O.WEIGHT_STD)
     assert np.array_equal(stream[n_routed:], c.shared.words)
     assert c.shared.tensor_f32(2, 2, X.TensorKind.DOWN).shape == (16, 32)
+
+
+def test_open_container_mmap_ingest(tmp_path):
+    """XPGW ingest by mmap (no read copy): same words/tensors as the generated container,
+    and the reference's header checks."""
+    import numpy as np
+    import pytest
+
+    import paper_2604_02715_b200 as X
+    from paper_2604_02715_b200.errors import ContainerFormatError
+
+    spec = X.ModelSpec(2, 3, 16, 32)
+    c = X.generate_synthetic_model(spec, 4, pin=False)
+    path = tmp_path / "m.xpgw"
+    c.write(path)
+    o = X.open_container(path, register=False)
+    assert o.spec == spec and np.array_equal(o.words, c.words)
+    tid = X.ExpertTensorId(2, 3, X.TensorKind.DOWN)
+    assert o.tensor_bytes(tid) == c.tensor_bytes(tid)
+    raw = path.read_bytes()
+    bad = tmp_path / "bad.xpgw"
+    bad.write_bytes(b"XPGX" + raw[4:])
+    with pytest.raises(ContainerFormatError):
+        X.open_container(bad, register=False)
+    bad.write_bytes(raw[:-2])
+    with pytest.raises(ContainerFormatError):
+        X.open_container(bad, register=False)
+
+
+def test_cli_generate_compress_match_reference_bytes(tmp_path):
+    """`python -m paper_2604_02715_b200 generate/compress` write the reference's XPGW/XPGC
+    bytes (sha256 pinned to tests/golden from the reference itself)."""
+    import hashlib
+    import json
+    import os
+
+    from paper_2604_02715_b200.__main__ import main
+    from paper_2604_02715_b200.exponent_codec import CompressedModel
+
+    meta = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden_v1.json")))["cases"]
+    xpgw, xpgc = tmp_path / "m.xpgw", tmp_path / "m.xpgc"
+    assert main(["generate", str(xpgw), "--model", "2,3,64,96", "--seed", "11"]) == 0
+    payload = xpgw.read_bytes()[40:]
+    assert hashlib.sha256(payload).hexdigest() == meta["gen_2_3_64_96_11"]
+    assert main(["generate", str(xpgw), "--model", "2,3,64,96"]) == 1  # exists, no --force
+    assert main(["generate", str(xpgw), "--model", "3,2,32,64", "--seed", "4", "--force"]) == 0
+    assert main(["compress", str(xpgw), str(xpgc)]) == 0
+    assert hashlib.sha256(xpgc.read_bytes()).hexdigest() == meta["xpgc_3_2_32_64_4"]["sha256"]
+    # XPGC ingest is host-only (bit counts from the index scan) and round-trips its bytes
+    assert CompressedModel.read(xpgc).to_bytes() == xpgc.read_bytes()
