@@ -296,6 +296,10 @@ int xpgb_experts_forward(xpgb_ctx* ctx, int32_t layer, const void* rows_dev, con
 /* Ordered combine (pipeline.py:198-207) of rows returned by the expert owners:
  * y[t] = sum_{s ascending} rows[index[t][s]] * f32(1/top_k); index < 0 skips the slot.
  * rows fp32 [*][hidden], index int32 [tokens][kk], kk = number of routed slots. */
+/* Shared experts of one layer on caller rows (the expert-parallel path: every rank applies its
+ * replica to its own tokens after the routed combine): y[t] += sum_s shared_s(x[t]) in fp32,
+ * shared experts in ascending order, weight 1.  x, y: device fp32 [tokens][H]. */
+int xpgb_shared_forward(xpgb_ctx* ctx, int32_t layer, const float* x_dev, float* y_dev, int32_t tokens, void* stream);
 int xpgb_combine_rows(const float* rows_dev, const int32_t* index_dev, int32_t tokens, int32_t kk, int32_t top_k,
                       int32_t hidden, float* y_dev, void* stream);
 

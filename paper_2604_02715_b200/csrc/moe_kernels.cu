@@ -361,7 +361,7 @@ void launch_gather(const float* x, const int32_t* pos, const long long* fault, _
 __global__ void k_combine(const float* __restrict__ part, const int32_t* __restrict__ pos,
                           const long long* __restrict__ fault, float* __restrict__ y, int kk, int kr, int H,
                           int splits, long long split_stride, float inv_k, const int32_t* __restrict__ next_pos,
-                          __nv_bfloat16* __restrict__ xp) {
+                          __nv_bfloat16* __restrict__ xp, int accumulate) {
   if (*fault) return;
   const int t = blockIdx.x;
   int p[kMaxTopK], q[kMaxTopK];
@@ -370,7 +370,7 @@ __global__ void k_combine(const float* __restrict__ part, const int32_t* __restr
     q[s] = next_pos ? next_pos[t * kk + s] : -1;
   }
   for (int i = threadIdx.x; i < H / 4; i += blockDim.x) {
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 acc = accumulate ? reinterpret_cast<const float4*>(y + (size_t)t * H)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
     for (int s = 0; s < kk; ++s) {
       if (p[s] < 0) continue;
       const float4* src = reinterpret_cast<const float4*>(part + (size_t)p[s] * H) + i;
@@ -396,10 +396,11 @@ __global__ void k_combine(const float* __restrict__ part, const int32_t* __restr
 
 void launch_combine(const float* part, const int32_t* pos, const long long* fault, float* y, int T, int kk, int kr,
                     int H, int splits, long long split_stride, float inv_k, const int32_t* next_pos,
-                    __nv_bfloat16* xp, cudaStream_t s) {
+                    __nv_bfloat16* xp, cudaStream_t s, bool accumulate) {
   if (T == 0) return;
   const int threads = min(256, max(32, H / 4));
-  k_combine<<<T, threads, 0, s>>>(part, pos, fault, y, kk, kr, H, splits, split_stride, inv_k, next_pos, xp);
+  k_combine<<<T, threads, 0, s>>>(part, pos, fault, y, kk, kr, H, splits, split_stride, inv_k, next_pos, xp,
+                                  accumulate ? 1 : 0);
   note_launch();
 }
 

@@ -68,9 +68,10 @@ void launch_down(const CUtensorMap& map_w, const CUtensorMap& map_h, const CUten
 // y_t = ordered weighted sum of the token's kk expert rows (the first kr scaled by
 // inv_k, the rest -- shared experts -- by 1); optionally also writes bf16(y_t) to
 // the next layer's expert-major rows (fused gather).
+// accumulate: y_t starts from its current value (a later pass adds shared experts).
 void launch_combine(const float* part, const int32_t* pos, const long long* fault, float* y, int T, int kk, int kr,
                     int H, int splits, long long split_stride, float inv_k, const int32_t* next_pos,
-                    __nv_bfloat16* xp, cudaStream_t s);
+                    __nv_bfloat16* xp, cudaStream_t s, bool accumulate = false);
 void launch_reduce_rows(const float* part, const long long* fault, float* out, int n_rows, int H, int splits,
                         long long split_stride, cudaStream_t s);
 void set_gemm_attrs();

@@ -2138,6 +2138,43 @@ int xpgb_experts_forward(xpgb_ctx* h, int32_t layer, const void* rows_dev, const
   });
 }
 
+int xpgb_shared_forward(xpgb_ctx* h, int32_t layer, const float* x_dev, float* y_dev, int32_t tokens, void* stream) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    if (layer < 1 || layer > c->N) XFAIL(XPGB_ERR_OUT_OF_RANGE, "layer %d outside [1, %d]", layer, c->N);
+    if (!c->S || tokens <= 0) return;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int S = c->S, T = tokens;
+    if ((long long)T * S > c->cap_rows || !c->xp) ensure_work(c, T, S);
+    // rows s*T + t hold token t for shared expert s; offsets [0, T, 2T, ...]
+    std::vector<int32_t> host((size_t)T * S + S + 1);
+    for (int t = 0; t < T; ++t)
+      for (int e = 0; e < S; ++e) host[(size_t)t * S + e] = e * T + t;
+    for (int e = 0; e <= S; ++e) host[(size_t)T * S + e] = e * T;
+    int32_t* d_pos = c->plan_pos[2];  // layer_forward's plan buffer doubles as scratch here
+    int32_t* d_off = c->plan_off[2];
+    CK(cudaMemcpyAsync(d_pos, host.data(), (size_t)T * S * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_off, host.data() + (size_t)T * S, (size_t)(S + 1) * 4, cudaMemcpyHostToDevice, s));
+    launch_gather(x_dev, d_pos, c->d_fault, c->xp, T, S, c->H, s);
+    CKLAUNCH();
+    const int bn = pick_bn(T);
+    GemmParams pg = gemm_params(c, layer, 1, d_off, 1), pd = gemm_params(c, layer, 2, d_off, 1);
+    for (GemmParams* p : {&pg, &pd}) {  // only the shared groups
+      p->E = S;
+      p->E_routed = 0;
+    }
+    pd.split_stride = (long long)T * S * c->H;
+    launch_gate_up(c->map_gu, c->map_xp, c->map_gu_sh, pg, bn, c->num_sms, s);
+    CKLAUNCH();
+    launch_down(c->map_dn, c->map_h, c->map_dn_sh, pd, bn, c->num_sms, s);
+    CKLAUNCH();
+    launch_combine(c->part, d_pos, c->d_fault, y_dev, T, S, 0, c->H, 1, pd.split_stride, 1.0f, nullptr, nullptr, s,
+                   true);
+    CKLAUNCH();
+    CK(cudaStreamSynchronize(s));  // the host index vector is pageable scratch
+  });
+}
+
 int xpgb_combine_rows(const float* rows_dev, const int32_t* index_dev, int32_t tokens, int32_t kk, int32_t top_k,
                       int32_t hidden, float* y_dev, void* stream) {
   return guard([&] {

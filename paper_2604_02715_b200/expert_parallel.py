@@ -132,12 +132,15 @@ class ExpertParallelMoE:
     route_fn(seed, n_tokens, layer, L, k) -> int [n_tokens, kk] (default: libxpgb router kernel);
     expert_fn(layer, rows_bf16 [n, H], offsets int32 [count+1]) -> fp32 [n, H] unscaled expert outputs
     (default: libxpgb grouped SwiGLU through this rank's page table);
-    combine_fn(rows fp32, index int32 [T, kk], top_k) -> fp32 [T, H] (default: libxpgb ordered combine).
+    combine_fn(rows fp32, index int32 [T, kk], top_k) -> fp32 [T, H] (default: libxpgb ordered combine);
+    shared_fn(layer, x fp32 [T, H], y fp32 [T, H]) adds the shared experts' outputs to y in place (each
+    rank applies its replica to its own tokens after the routed combine; default: libxpgb when the
+    context holds shared experts, else none).
     The defaults need a CUDA device; the CPU tests inject oracle-backed functions.
     """
 
     def __init__(self, spec: ModelSpec, fwd: ForwardSpec, rank: int, world: int, group=None, ctx=None,
-                 route_fn=None, expert_fn=None, combine_fn=None):
+                 route_fn=None, expert_fn=None, combine_fn=None, shared_fn=None, has_shared: bool = False):
         self.spec = spec
         self.fwd = fwd
         self.rank = rank
@@ -148,6 +151,7 @@ class ExpertParallelMoE:
         self.route_fn = route_fn or self._gpu_route
         self.expert_fn = expert_fn or self._gpu_experts
         self.combine_fn = combine_fn or self._gpu_combine
+        self.shared_fn = shared_fn or (self._gpu_shared if has_shared else None)
 
     # ---- defaults on the GPU
     def _gpu_route(self, seed, n_tokens, layer, L, k):
@@ -179,6 +183,12 @@ class ExpertParallelMoE:
                  self.spec.hidden_dim, C.c_void_p(y.data_ptr()), C.c_void_p(current_stream_ptr(self.ctx.device)))
         return y
 
+    def _gpu_shared(self, layer, x, y):
+        from .device import current_stream_ptr
+
+        call("xpgb_shared_forward", self.ctx.handle, layer, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
+             int(x.shape[0]), C.c_void_p(current_stream_ptr(self.ctx.device)))
+
     # ---- one layer
     def plan(self, layer: int, tokens: int) -> DispatchPlan:
         routes = self.route_fn(self.fwd.router_seed, self.world * tokens, layer, self.spec.experts_per_layer,
@@ -199,7 +209,10 @@ class ExpertParallelMoE:
         back = out.index_select(0, plan.from_expert)
         ret = torch.empty((send.shape[0], H), dtype=torch.float32, device=x.device)
         self._a2a(ret, back, plan.send_counts, plan.recv_counts)
-        return self.combine_fn(ret, plan.ret_index, self.fwd.top_k)
+        y = self.combine_fn(ret, plan.ret_index, self.fwd.top_k)
+        if self.shared_fn is not None:
+            self.shared_fn(layer, x, y)  # after the routed sum, weight 1 (single-device slot order)
+        return y
 
     def _a2a(self, out, inp, out_splits, in_splits):
         import torch
@@ -225,12 +238,10 @@ class ExpertParallelRunner:
     """
 
     def __init__(self, spec: ModelSpec, container, fwd: ForwardSpec, rank: int, world: int, device: int = 0,
-                 group=None, shard_pool=None):
+                 group=None, shard_pool=None, shared=None):
         from .device import Context
-        from .errors import ConfigError
 
-        if container is not None and getattr(container, "shared", None) is not None:
-            raise ConfigError("shared experts are not supported on the expert-parallel path yet")
+        shared = shared if shared is not None else getattr(container, "shared", None)
         self.spec = spec
         self.fwd = fwd
         self.rank, self.world = rank, world
@@ -239,7 +250,10 @@ class ExpertParallelRunner:
         self.ctx.set_expert_shard(first, count)
         pool = shard_pool if shard_pool is not None else shard_payload(container, first, count)
         self.ctx.attach_host_pool(pool)
-        self.moe = ExpertParallelMoE(spec, fwd, rank, world, group=group, ctx=self.ctx)
+        if shared is not None:
+            self.ctx.set_shared(shared)  # every rank holds a replica (resident, never paged)
+        self.moe = ExpertParallelMoE(spec, fwd, rank, world, group=group, ctx=self.ctx,
+                                     has_shared=shared is not None)
 
     def run(self, iterations: int, acts, profile: bool = False) -> RunReport:
         import torch

@@ -61,7 +61,19 @@ def _oracle_fns(bounds, rank, words):
     return route_fn, expert_fn, combine_fn
 
 
-def _worker(rank, world, port, seed, q):
+def _shared_fn(words_shared):
+    from oracle import xpg_oracle as O
+
+    sp = O.SharedPool(N, 1, H, F, words_shared)
+
+    def shared_fn(layer, x, y):
+        xs = O.bf16_to_f32(O.f32_to_bf16(x.numpy()))  # the GPU path feeds bf16 rows
+        y += torch.from_numpy(O.expert_rows(sp.tensor_f32(layer, 1, 1), sp.tensor_f32(layer, 1, 2), xs))
+
+    return shared_fn, sp
+
+
+def _worker(rank, world, port, seed, q, shared=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -74,8 +86,9 @@ def _worker(rank, world, port, seed, q):
         fwd = ForwardSpec(T, K, seed)
         bounds = shard_bounds(L, world)
         route_fn, expert_fn, combine_fn = _oracle_fns(bounds, rank, words)
+        shared_fn = _shared_fn(O.synth_payload(N, 1, H, F, 5))[0] if shared else None
         moe = ExpertParallelMoE(spec, fwd, rank, world, route_fn=route_fn, expert_fn=expert_fn,
-                                combine_fn=combine_fn)
+                                combine_fn=combine_fn, shared_fn=shared_fn)
         x_all = np.random.default_rng(seed).standard_normal((world * T, H), dtype=np.float32)
         x = torch.from_numpy(x_all[rank * T:(rank + 1) * T].copy())
         for layer in (1, 2):
@@ -89,15 +102,15 @@ def _worker(rank, world, port, seed, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_ep_matches_single_gpu_oracle(world):
+@pytest.mark.parametrize("world,shared", [(2, False), (3, False), (2, True)])
+def test_ep_matches_single_gpu_oracle(world, shared):
     from oracle import xpg_oracle as O
 
     seed = 11
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, seed, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, seed, q, shared)) for r in range(world)]
     for p in procs:
         p.start()
     got = dict(q.get(timeout=120) for _ in range(world))
@@ -112,8 +125,9 @@ def test_ep_matches_single_gpu_oracle(world):
     words = O.synth_payload(N, L, H, F, 4)
     pool = O.WordPool(N, L, H, F, words)
     a = np.random.default_rng(seed).standard_normal((world * T, H), dtype=np.float32)
+    sp = _shared_fn(O.synth_payload(N, 1, H, F, 5))[1] if shared else None
     for layer in (1, 2):
-        a = O.layer_forward(pool, layer, O.bf16_to_f32(O.f32_to_bf16(a)), K, seed)
+        a = O.layer_forward(pool, layer, O.bf16_to_f32(O.f32_to_bf16(a)), K, seed, shared=sp)
     assert O.rel_l2(y, a) < 1e-5
 
 

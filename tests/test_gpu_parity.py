@@ -224,13 +224,15 @@ def test_report_json_fields(X):
     assert doc["violation_count"] == 0
 
 
-def test_expert_parallel_runner_world1_matches_resident(X, O):
-    """The EP runner (session API + experts_forward + ordered combine) on one GPU."""
+@pytest.mark.parametrize("shared", [0, 1])
+def test_expert_parallel_runner_world1_matches_resident(X, O, shared):
+    """The EP runner (session API + experts_forward + ordered combine [+ the rank's shared
+    expert replica on its own tokens]) on one GPU."""
     from paper_2604_02715_b200.expert_parallel import ExpertParallelRunner
 
     spec = X.ModelSpec(4, 8, 256, 512)
     fwd = X.ForwardSpec(16, 2, 7)
-    container = X.generate_synthetic_model(spec, 7)
+    container = X.generate_synthetic_model(spec, 7, shared_experts=shared)
     x = X.initial_activations(spec, fwd, 7)
     runner = ExpertParallelRunner(spec, container, fwd, rank=0, world=1)
     rep = runner.run(2, x)
