@@ -342,7 +342,8 @@ def main():
 
         first, count = shard_bounds(L, world)[rank]
         # each rank holds only its expert shard (shard-local container order) in pinned memory
-        shard = X.generate_fast_model(X.ModelSpec(N, count, H, F), SEED + 1000 * rank, device=dev)
+        shard = X.generate_fast_model(X.ModelSpec(N, count, H, F), SEED + 1000 * rank, device=dev,
+                                      shared_experts=S)
         container = None
     else:
         container = X.generate_fast_model(cspec, SEED + rank, device=dev, shared_experts=S)
@@ -350,7 +351,8 @@ def main():
     log(f"model generated in {gen_s:.1f}s")
     if use_ep:
         group = None
-        runner = ExpertParallelRunner(spec, None, fwd, rank, world, device=dev, group=group, shard_pool=shard.pinned)
+        runner = ExpertParallelRunner(spec, None, fwd, rank, world, device=dev, group=group, shard_pool=shard.pinned,
+                                      shared=shard.shared)
         budget = 2.0 / N  # 2-layer ring of this rank's shard
     else:
         backends = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 55e9, 1 << 50)]

@@ -695,35 +695,43 @@ static void set_attr() {
   cudaFuncSetAttribute(k_moe_gemm<GU, BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<GU, BN, ST>::SMEM);
 }
 
+// Stage counts: the weight bytes in flight per SM set the achieved HBM bandwidth of
+// these memory-bound launches, so each token-tile width BN gets as many stages as fit
+// in 227 KB (stage = weight tile(s) + BN x 128 B of activations).
+#define XPGB_GU_TILES(X) X(32, 5) X(48, 5) X(64, 5) X(80, 5) X(96, 4) X(128, 4)
+#define XPGB_DN_TILES(X) X(32, 10) X(48, 9) X(64, 8) X(80, 8) X(96, 7) X(128, 6) X(256, 4)
+
 void set_gemm_attrs() {
-  set_attr<true, 32, 5>();
-  set_attr<true, 64, 4>();
-  set_attr<true, 128, 4>();
-  set_attr<false, 32, 9>();
-  set_attr<false, 64, 8>();
-  set_attr<false, 128, 6>();
-  set_attr<false, 256, 4>();
+#define XPGB_SET_GU(BN, ST) set_attr<true, BN, ST>();
+#define XPGB_SET_DN(BN, ST) set_attr<false, BN, ST>();
+  XPGB_GU_TILES(XPGB_SET_GU)
+  XPGB_DN_TILES(XPGB_SET_DN)
+#undef XPGB_SET_GU
+#undef XPGB_SET_DN
 }
 
 void launch_gate_up(const CUtensorMap& map_w, const CUtensorMap& map_x, const CUtensorMap& map_ws,
                     const GemmParams& p, int bn, int grid, cudaStream_t s) {
-  GemmKernel kern;
-  int smem;
-  if (bn == 32) { kern = k_moe_gemm<true, 32, 5>; smem = GemmCfg<true, 32, 5>::SMEM; }
-  else if (bn == 64) { kern = k_moe_gemm<true, 64, 4>; smem = GemmCfg<true, 64, 4>::SMEM; }
-  else { kern = k_moe_gemm<true, 128, 4>; smem = GemmCfg<true, 128, 4>::SMEM; }
+  GemmKernel kern = nullptr;
+  int smem = 0;
+#define XPGB_PICK_GU(BN, ST) \
+  if (bn == BN) { kern = k_moe_gemm<true, BN, ST>; smem = GemmCfg<true, BN, ST>::SMEM; }
+  XPGB_GU_TILES(XPGB_PICK_GU)
+#undef XPGB_PICK_GU
+  if (!kern) { kern = k_moe_gemm<true, 128, 4>; smem = GemmCfg<true, 128, 4>::SMEM; }
   kern<<<grid, 192, smem, s>>>(map_w, map_x, map_ws, p);
   note_launch();
 }
 
 void launch_down(const CUtensorMap& map_w, const CUtensorMap& map_h, const CUtensorMap& map_ws,
                  const GemmParams& p, int bn, int grid, cudaStream_t s) {
-  GemmKernel kern;
-  int smem;
-  if (bn == 32) { kern = k_moe_gemm<false, 32, 9>; smem = GemmCfg<false, 32, 9>::SMEM; }
-  else if (bn == 64) { kern = k_moe_gemm<false, 64, 8>; smem = GemmCfg<false, 64, 8>::SMEM; }
-  else if (bn == 128) { kern = k_moe_gemm<false, 128, 6>; smem = GemmCfg<false, 128, 6>::SMEM; }
-  else { kern = k_moe_gemm<false, 256, 4>; smem = GemmCfg<false, 256, 4>::SMEM; }
+  GemmKernel kern = nullptr;
+  int smem = 0;
+#define XPGB_PICK_DN(BN, ST) \
+  if (bn == BN) { kern = k_moe_gemm<false, BN, ST>; smem = GemmCfg<false, BN, ST>::SMEM; }
+  XPGB_DN_TILES(XPGB_PICK_DN)
+#undef XPGB_PICK_DN
+  if (!kern) { kern = k_moe_gemm<false, 128, 6>; smem = GemmCfg<false, 128, 6>::SMEM; }
   kern<<<grid, 192, smem, s>>>(map_w, map_h, map_ws, p);
   note_launch();
 }

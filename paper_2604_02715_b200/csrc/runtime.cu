@@ -388,21 +388,31 @@ static void ensure_work(Ctx* c, int T, int kk) {
   c->map_h_pair = make_map(c->hbuf, rows, c->F, kBM);
 }
 
-static int pick_bn(int T) {
-  static const int forced = [] {  // XPGB_BN=32|64|128: tile experiments (profiling only)
+// Token-tile width of the 1-CTA kernels: the smallest instantiated BN covering the
+// expected rows of an expert group (mean + 2 sd of the binomial count), so the weight
+// tiles of a memory-bound launch get the most pipeline stages (moe_kernels.cu).
+static int pick_bn_rows(double avg_rows) {
+  static const int forced = [] {  // XPGB_BN: tile experiments (profiling only)
     const char* e = getenv("XPGB_BN");
-    const int v = e ? atoi(e) : 0;
-    return (v == 32 || v == 64 || v == 128) ? v : 0;
+    return e ? atoi(e) : 0;
   }();
   if (forced) return forced;
-  return T <= 32 ? 32 : (T <= 64 ? 64 : 128);
+  const double want = avg_rows + 2.0 * std::sqrt(std::max(avg_rows, 0.0));
+  for (int bn : {32, 48, 64, 80, 96}) if (want <= bn) return bn;
+  return 128;
 }
+
+static double avg_group_rows(Ctx* c, int T, int kk) {
+  const double local = (double)T * kk * c->E / c->L + (double)std::max(0, std::min(T, c->sh1) - c->sh0) * c->S;
+  return local / std::max(1, c->E + c->S);
+}
+
+static int pick_bn(Ctx* c, int T, int kk) { return pick_bn_rows(avg_group_rows(c, T, kk)); }
 
 // Down projection at prefill sizes: N = 256 token rows per tile halves the weight-tile
 // re-reads and the smem traffic per MMA flop (one 256-column accumulator, double-buffered).
-static int pick_bn_down(Ctx* c, int T, int kt) {
-  const long long per_expert = (long long)T * kt / std::max(1, std::min(c->E + c->S, T * kt));
-  return per_expert >= 384 ? 256 : pick_bn(T);
+static int pick_bn_down(Ctx* c, int T, int kk) {
+  return avg_group_rows(c, T, kk) >= 384 ? 256 : pick_bn(c, T, kk);
 }
 
 // Split-K factor for the down projection: balance (units x splits) over the SMs.
@@ -471,13 +481,12 @@ static void enqueue_window(Ctx* c, int layer, const float* x, float* y, int T, i
   if (T == 0) return;
   const int32_t* pos = c->plan_pos[b] + (size_t)(layer - 1) * T * kt;
   const int32_t* off = c->plan_off[b] + (size_t)(layer - 1) * (groups_of(c) + 1);
-  const int bn = pick_bn(T);
-  const int bn_dn = pick_bn_down(c, T, kt);
+  const int bn = pick_bn(c, T, kk);
+  const int bn_dn = pick_bn_down(c, T, kk);
   // expert groups of >= 128 rows on average run on CTA pairs (256 x 256 tiles, unsplit);
   // measured crossover on B200 (profiles/r1_pair_crossover.jsonl): at 64 rows per expert the
   // 1-CTA swap-AB kernel is ahead, from 128 rows the pair kernel wins (up to 2.4x at 8K rows)
-  const double local_rows = (double)T * kk * c->E / c->L + (double)std::max(0, std::min(T, c->sh1) - c->sh0) * c->S;
-  const double per_group = local_rows / std::max(1, c->E + c->S);
+  const double per_group = avg_group_rows(c, T, kk);
   const bool pair = pair_gemm_supported(c->H, c->F) &&
                     (c->pair_mode == 1 || (c->pair_mode < 0 && per_group >= 128.0));
   const int splits = pair ? 1 : pick_splits(c, T, kt, bn_dn);
@@ -1320,14 +1329,18 @@ static void set_codec(Ctx* c, const void* pool, uint64_t pool_bytes, const uint6
     uint64_t cap = 0;
     if (host_compressed) {
       // largest record, or a whole layer's records of this kind when they are small
-      uint64_t layer_sum = 0;
+      uint64_t layer_sum = 0, largest = 0;
       for (size_t ti = k; ti < nt; ti += 2) {
         const uint64_t rb = xpgb_codec_record_bytes(((ti & 1) ? c->s2 : c->s1) / 2, c->rec_bits[ti], chunk);
         if ((ti / 2) % c->E == 0) layer_sum = 0;
         layer_sum += rb;
+        largest = std::max(largest, rb);
         cap = std::max(cap, layer_sum);
       }
-      uint64_t piece = kStagePieceBytes;
+      // records up to 2 pieces travel whole (one copy + one decode each: DSv3's 39 MB
+      // gate/up records page in at 98% of the link instead of 93% in 32 MB pieces);
+      // larger ones stream in 32 MB pieces
+      uint64_t piece = largest <= 2 * kStagePieceBytes ? 2 * kStagePieceBytes : kStagePieceBytes;
       if (const char* env = getenv("XPGB_STAGE_BYTES")) piece = std::max<uint64_t>(4096, strtoull(env, nullptr, 10));
       cap = std::min(cap, piece) + 64 + (uint64_t)chunk * 8;
     }
@@ -2124,7 +2137,7 @@ int xpgb_experts_forward(xpgb_ctx* h, int32_t layer, const void* rows_dev, const
     if (n_rows > c->cap_rows || !c->xp) ensure_work(c, std::max(n_rows, 1), 1);
     if (n_rows == 0) return;
     CK(cudaMemcpyAsync(c->xp, rows_dev, (size_t)n_rows * c->H * 2, cudaMemcpyDeviceToDevice, s));
-    const int bn = pick_bn(n_rows);
+    const int bn = pick_bn_rows((double)n_rows / std::max(1, c->E));
     const int splits = pick_splits(c, n_rows, 1, bn);
     launch_gate_up(c->map_gu, c->map_xp, c->map_gu, gemm_params(c, layer, 1, offsets_dev, 1, false), bn, c->num_sms,
                    s);
@@ -2157,7 +2170,7 @@ int xpgb_shared_forward(xpgb_ctx* h, int32_t layer, const float* x_dev, float* y
     CK(cudaMemcpyAsync(d_off, host.data() + (size_t)T * S, (size_t)(S + 1) * 4, cudaMemcpyHostToDevice, s));
     launch_gather(x_dev, d_pos, c->d_fault, c->xp, T, S, c->H, s);
     CKLAUNCH();
-    const int bn = pick_bn(T);
+    const int bn = pick_bn_rows((double)T);
     GemmParams pg = gemm_params(c, layer, 1, d_off, 1), pd = gemm_params(c, layer, 2, d_off, 1);
     for (GemmParams* p : {&pg, &pd}) {  // only the shared groups
       p->E = S;
@@ -2219,13 +2232,14 @@ int xpgb_profile_layer(xpgb_ctx* h, int32_t layer, const float* x_dev, float* y_
     CK(cudaMemcpy(offs.data(), c->plan_off[2] + (size_t)(layer - 1) * (G + 1), (G + 1) * 4,
                   cudaMemcpyDeviceToHost));
     long long active = 0, u1 = 0, u2 = 0;
-    const int bn = pick_bn(tokens);
+    const int kk = std::min(top_k, c->L);
+    const int bn = pick_bn(c, tokens, kk);
     for (int e = 0; e < G; ++e) {
       const int n = offs[e + 1] - offs[e];
       if (n <= 0) continue;
       ++active;
       u1 += (long long)((n + bn - 1) / bn) * ((c->F + kBM - 1) / kBM);
-      const int bd = pick_bn_down(c, tokens, kt);
+      const int bd = pick_bn_down(c, tokens, kk);
       u2 += (long long)((n + bd - 1) / bd) * ((c->H + kBM - 1) / kBM) * c->last_splits;
     }
     const long long pairs = offs[G];  // rows this device computes (local routed + shared)
