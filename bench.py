@@ -292,6 +292,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="mixtral", choices=sorted(CONFIGS))
     ap.add_argument("--tokens", type=int, default=None)
+    ap.add_argument("--budget", type=float, default=0.25,
+                    help="expert-HBM budget as a fraction of the expert bytes (ring + codec buffers + shared)")
     ap.add_argument("--prefill", action="store_true",
                     help="prefill regime: one step = a T-token prompt chunk through every layer (default T=8192)")
     ap.add_argument("--cpu-sample-tokens", type=int, default=4)
@@ -354,6 +356,7 @@ def main():
         runner = ExpertParallelRunner(spec, None, fwd, rank, world, device=dev, group=group, shard_pool=shard.pinned,
                                       shared=shard.shared)
         budget = 2.0 / N  # 2-layer ring of this rank's shard
+        footprint = None
     else:
         backends = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 55e9, 1 << 50)]
         hier = X.StorageHierarchy(container, None, X.plan_placement(cspec, backends), backends)
@@ -385,7 +388,21 @@ def main():
         runner = X.StreamedRunner(spec, hier, fwd, mode="threaded", device=dev, host_codec=args.host_codec, **run_kw)
         hbm = runner.ctx.hbm_bytes()
         expert_bytes = cspec.total_bytes + (container.shared.total_bytes if container.shared is not None else 0)
-        budget = (hbm["ring"] + hbm["staging"] + hbm["device_tier"]) / expert_bytes
+        # fixed expert-slot budget (north star): expert weights resident in HBM -- ring slots,
+        # pinned experts, resident shared experts -- within args.budget of the expert bytes; the
+        # reference's two-layer ring is exactly 2/N.  Shared experts (DSv3) share the budget, so
+        # there the ring shrinks to a sub-layer ring (windows of ring/2 experts).  The codec's
+        # transient staging buffers and chunk index are reported beside it (footprint).
+        eb = cspec.expert_bytes
+        shared_b = container.shared.total_bytes if container.shared is not None else 0
+        ring_blocks = (hbm["ring"] - shared_b) // eb
+        ring_fit = int((args.budget * expert_bytes - shared_b + 1) // eb) & ~1
+        if 2 <= ring_fit < ring_blocks:
+            runner.ctx.set_ring_experts(ring_fit)
+            ring_blocks = ring_fit
+            hbm = runner.ctx.hbm_bytes()
+        budget = hbm["ring"] / expert_bytes
+        footprint = (hbm["ring"] + hbm["staging"] + hbm["device_tier"]) / expert_bytes
     x_host = X.initial_activations(spec, fwd, SEED + rank)
     x_dev = torch.from_numpy(x_host).to(f"cuda:{dev}")
 
@@ -495,7 +512,11 @@ def main():
         "data": "synthetic (random-init N(0,0.02) bf16 weights drawn on-GPU, N(0,1) activations)",
         "config": {"workload": cfg["name"], "tokens_per_step": T, "top_k": k, "layers": N,
                    "expert_hbm_budget": round(budget, 4),
-                   "placement": "2-layer ring, host-only (alpha=0)" + (
+                   "expert_hbm_footprint": round(footprint, 4) if not use_ep else None,
+                   "ring_blocks_per_kind": int(ring_blocks) if not use_ep else None,
+                   "placement": ("2-layer ring" if use_ep or ring_blocks >= 2 * cspec.experts_per_layer else
+                                 f"sub-layer ring of {ring_blocks} expert blocks per kind (windows of "
+                                 f"{ring_blocks // 2} experts)") + ", host-only (alpha=0)" + (
                        ", exponent-Huffman records over PCIe decoded on-GPU into the ring (lossless)"
                        if args.host_codec else ""),
                    "l2": "inputs larger than L2: all %.1f GB of expert weights stream from host each step" % (cspec.total_bytes / 1e9)},
