@@ -63,6 +63,6 @@ void launch_exp_decode(const uint8_t* sm, const uint32_t* bits, const uint32_t* 
 // consecutive records, or consecutive device-tier records of a layer).
 void launch_exp_decode_multi(const DecodeTensor* tensors, int ntensors, uint64_t n, int chunk, const CodecTable& table,
                              cudaStream_t s);
-constexpr uint64_t kStagePieceBytes = 32ull << 20;  // max bytes of one staged record piece
+constexpr uint64_t kStagePieceBytes = 64ull << 20;  // max bytes of one staged record piece
 
 }  // namespace xpgb

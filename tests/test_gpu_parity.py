@@ -347,3 +347,23 @@ def test_decode_session_steps_equal_resident(X, ring, host_codec):
         assert np.asarray(s2.step(x)).tobytes() == np.asarray(model.run(1, fwd, x.copy())[0]).tobytes()
     r2 = runner.run(1, acts=x.copy())
     assert r2.violations == [] and r2.final_activations.tobytes() == np.asarray(model.run(1, fwd, x.copy())[0]).tobytes()
+
+
+def test_empty_step_and_single_expert_edge_cases(X, O):
+    """T = 0 (an empty decode step) pages like any other step and returns an empty batch;
+    L = 1 with top_k > L routes every token to the one expert with scale 1/top_k."""
+    spec = X.ModelSpec(3, 4, 64, 128)
+    container, hier = _hier(X, spec, seed=2)
+    fwd0 = X.ForwardSpec(0, 2, 1)
+    rep = X.StreamedRunner(spec, hier, fwd0).run(2, acts=np.zeros((0, 64), np.float32))
+    assert rep.final_activations.shape == (0, 64)
+    assert rep.violations == [] and rep.page_fault is None
+    assert rep.arena_peak_bytes == 2 * spec.experts_per_layer * spec.expert_bytes
+    y0 = X.layer_forward(container.tensor_f32, spec, fwd0, 1, np.zeros((0, 64), np.float32))
+    assert np.asarray(y0).shape == (0, 64)
+    spec1 = X.ModelSpec(2, 1, 64, 128)
+    c1 = X.generate_synthetic_model(spec1, 3)
+    pool = O.WordPool(2, 1, 64, 128, c1.words)
+    x = np.random.default_rng(0).standard_normal((9, 64), dtype=np.float32)
+    y = X.layer_forward(c1.tensor_f32, spec1, X.ForwardSpec(9, 3, 5), 2, x)
+    assert O.rel_l2(y, O.layer_forward(pool, 2, x, 3, 5)) <= TOL
