@@ -68,7 +68,7 @@ def load_tensor_peak():
 def ncu_traffic(config: str, tokens: int):
     """DRAM bytes (read + write) of one gate/up launch from the committed ncu --set full
     capture of this workload (profiles/), or None when none was taken for it."""
-    path = {("mixtral", 256): os.path.join(ROOT, "profiles", "r1_ncu_gemm_T256_v3.jsonl")}.get((config, tokens))
+    path = {("mixtral", 256): os.path.join(ROOT, "profiles", "r1_ncu_gemm_T256_v4.jsonl")}.get((config, tokens))
     try:
         for line in open(path):
             rec = json.loads(line)

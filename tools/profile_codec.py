@@ -15,7 +15,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--values", type=int, default=117_440_512)  # Mixtral gate/up tensor
     ap.add_argument("--chunk", type=int, default=1024)
-    ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--reps", type=int, default=50)
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -40,6 +40,16 @@ def main():
     once()
     torch.cuda.synchronize()
     ok = out.cpu().numpy().view("<u2").tobytes() == w.tobytes()
+    # hold the GPU busy ~0.5 s first: short launches on an idle GPU time its clock ramp
+    warm = torch.empty(1 << 28, dtype=torch.float32, device="cuda")
+    t_end = torch.cuda.Event(enable_timing=True)
+    import time as _t
+    t0 = _t.time()
+    while _t.time() - t0 < 0.5:
+        warm.mul_(1.0001)
+        once()
+    torch.cuda.synchronize()
+    del warm
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.reps):
