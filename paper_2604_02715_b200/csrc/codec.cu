@@ -169,6 +169,13 @@ __device__ __forceinline__ int canon_decode(uint64_t win, int ml, const int* cou
   return 0;  // invalid code: the host index scan rejects such streams before they get here
 }
 
+// Eight (sign/mantissa, exponent) byte pairs -> bf16 words by byte permutes:
+// x = [e1 s1 e0 s0] per 16-bit lane -> (s >> 7) << 15 | e << 7 | (s & 0x7F).
+__device__ __forceinline__ uint32_t pack_words(uint32_t sm4, uint32_t ex4, uint32_t sel) {
+  const uint32_t x = __byte_perm(sm4, ex4, sel);
+  return ((x >> 1) & 0x7F807F80u) | (x & 0x007F007Fu) | ((x << 8) & 0x80008000u);
+}
+
 __global__ void __launch_bounds__(256) k_exp_decode(const __grid_constant__ DecodeParams p) {
   __shared__ uint32_t lut3[1 << kMultiBits];  // syms (3 x 8 b) | count << 24 | total length << 26
   __shared__ uint32_t first_code[kCodecMaxLen + 1];
@@ -273,23 +280,21 @@ __global__ void __launch_bounds__(256) k_exp_decode(const __grid_constant__ Deco
         if (np > 5) hi |= (uint64_t)bytes >> (64 - 8 * np);
         np += k;
       }
-      uint32_t packed[4] = {0, 0, 0, 0};
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if (j >= cnt) break;
-        const uint32_t sym = (uint32_t)(lo >> (8 * j)) & 0xFFu;
-        const uint32_t s = (cnt == 8) ? (((j < 4 ? smv.x : smv.y) >> (8 * (j & 3))) & 0xFF) : sm[v + j];
-        const uint32_t word = ((s & 0x80u) << 8) | (sym << 7) | (s & 0x7Fu);
-        packed[j >> 1] |= word << (16 * (j & 1));
+      if (cnt == 8) {
+        const uint32_t e0 = (uint32_t)lo, e1 = (uint32_t)(lo >> 32);
+        *reinterpret_cast<uint4*>(out + v) =
+            make_uint4(pack_words(smv.x, e0, 0x5140u), pack_words(smv.x, e0, 0x7362u),
+                       pack_words(smv.y, e1, 0x5140u), pack_words(smv.y, e1, 0x7362u));
+      } else {
+        for (int j = 0; j < cnt; ++j) {
+          const uint32_t sym = (uint32_t)(lo >> (8 * j)) & 0xFFu;
+          const uint32_t sb = sm[v + j];
+          out[v + j] = (uint16_t)(((sb & 0x80u) << 8) | (sym << 7) | (sb & 0x7Fu));
+        }
       }
       lo = hi;
       hi = 0;
       np -= cnt;
-      if (cnt == 8) {
-        *reinterpret_cast<uint4*>(out + v) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-      } else {
-        for (int j = 0; j < cnt; ++j) out[v + j] = (uint16_t)(packed[j >> 1] >> (16 * (j & 1)));
-      }
     }
   }
 }
