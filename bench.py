@@ -171,10 +171,12 @@ def dist_setup():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        import torch
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(local)  # one rank per GPU, bound before NCCL picks a device
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     return world, rank, local
 
 
@@ -240,16 +242,32 @@ def run_reference_arm(args, cfg):
 
     threads = os.cpu_count() or 1
     os.environ.setdefault("OPENBLAS_NUM_THREADS", str(threads))
-    # weights of one layer (+ the layer-1 prefix is all the sample touches): reference generator
-    spec_words = cfg["L"] * (O.sigma(cfg["H"], cfg["F"], 1) + O.sigma(cfg["H"], cfg["F"], 2)) // 2
-    rng = np.random.default_rng(SEED)
-    words = O.f32_to_bf16(rng.standard_normal(spec_words, dtype=np.float32) * O.WEIGHT_STD)
-    words_full = words  # tensor_offset of layer 1 only
     sample = args.ref_sample_tokens
+    H, F = cfg["H"], cfg["F"]
+    layer_words = cfg["L"] * (O.sigma(H, F, 1) + O.sigma(H, F, 2)) // 2
+    rng = np.random.default_rng(SEED)
+    if layer_words * 2 <= (4 << 30):
+        # weights of layer 1 (all the sample touches): the reference generator's first draws
+        words = O.f32_to_bf16(rng.standard_normal(layer_words, dtype=np.float32) * O.WEIGHT_STD)
+        step_fn = lambda: cpu_reference.decode_rate(words, cfg["N"], cfg["L"], H, F, cfg["T"], cfg["k"], SEED, sample)
+    else:
+        # a layer too large to hold (DSv3: 22.5 GB): draw only the experts the sample routes to
+        # (same distribution), time their page-in and scale it to the layer (decode_rate_sampled)
+        routed = sorted({int(j) for j in O.route(SEED, sample, 1, cfg["L"], cfg["k"]).reshape(-1)})
+        n1, n2 = O.sigma(H, F, 1) // 2, O.sigma(H, F, 2) // 2
+        pool = {j: (O.f32_to_bf16(rng.standard_normal(n1, dtype=np.float32) * O.WEIGHT_STD),
+                    O.f32_to_bf16(rng.standard_normal(n2, dtype=np.float32) * O.WEIGHT_STD)) for j in routed}
+        shared = None
+        if cfg.get("S"):
+            sh = (O.f32_to_bf16(rng.standard_normal(n1, dtype=np.float32) * O.WEIGHT_STD),
+                  O.f32_to_bf16(rng.standard_normal(n2, dtype=np.float32) * O.WEIGHT_STD))
+            shared = lambda kind: sh[kind - 1]
+        step_fn = lambda: cpu_reference.decode_rate_sampled(lambda layer, j, kind: pool[j][kind - 1], cfg["N"],
+                                                            cfg["L"], H, F, cfg["T"], cfg["k"], SEED, sample,
+                                                            shared_words=shared)
     times, rates = [], []
     for i in range(args.warmup + args.steps):
-        r = cpu_reference.decode_rate(words_full, cfg["N"], cfg["L"], cfg["H"], cfg["F"], cfg["T"], cfg["k"], SEED,
-                                      sample)
+        r = step_fn()
         if i >= args.warmup:
             times.append(r["step_s"])
             rates.append(r["tok_s"])
@@ -354,7 +372,7 @@ def main():
     if use_ep:
         group = None
         runner = ExpertParallelRunner(spec, None, fwd, rank, world, device=dev, group=group, shard_pool=shard.pinned,
-                                      shared=shard.shared)
+                                      shared=shard.shared, host_codec=args.host_codec)
         budget = 2.0 / N  # 2-layer ring of this rank's shard
         footprint = None
     else:

@@ -238,7 +238,9 @@ class ExpertParallelRunner:
     """
 
     def __init__(self, spec: ModelSpec, container, fwd: ForwardSpec, rank: int, world: int, device: int = 0,
-                 group=None, shard_pool=None, shared=None):
+                 group=None, shard_pool=None, shared=None, host_codec: bool = False):
+        """host_codec: the rank's shard pages in as exponent-Huffman records over its own host
+        link, decoded on its GPU (as StreamedRunner(host_codec=True))."""
         from .device import Context
 
         shared = shared if shared is not None else getattr(container, "shared", None)
@@ -250,6 +252,14 @@ class ExpertParallelRunner:
         self.ctx.set_expert_shard(first, count)
         pool = shard_pool if shard_pool is not None else shard_payload(container, first, count)
         self.ctx.attach_host_pool(pool)
+        if host_codec:
+            from .exponent_codec import CompressedModel
+            from .geometry import WeightContainer
+
+            shard = WeightContainer._adopt(ModelSpec(spec.num_layers, count, spec.hidden_dim, spec.intermediate_dim),
+                                           pool)
+            self._codec = CompressedModel.from_container(shard)
+            self.ctx.set_codec(self._codec, host_compressed=True)
         if shared is not None:
             self.ctx.set_shared(shared)  # every rank holds a replica (resident, never paged)
         self.moe = ExpertParallelMoE(spec, fwd, rank, world, group=group, ctx=self.ctx,
@@ -296,4 +306,4 @@ class ExpertParallelRunner:
             intervals=_intervals(records), page_fault=self.ctx.fault() if rep.page_fault else None,
             h2d_bytes=int(rep.h2d_bytes), d2d_bytes=int(rep.d2d_bytes),
             copy_busy_seconds=(rep.copy_busy_ns[0] * 1e-9, rep.copy_busy_ns[1] * 1e-9),
-            elapsed_seconds=rep.elapsed_ns * 1e-9, kernels=_kernel_stats(rep))
+            elapsed_seconds=rep.elapsed_ns * 1e-9, kernels=_kernel_stats(rep), decoded_bytes=int(rep.decoded_bytes))

@@ -224,8 +224,8 @@ def test_report_json_fields(X):
     assert doc["violation_count"] == 0
 
 
-@pytest.mark.parametrize("shared", [0, 1])
-def test_expert_parallel_runner_world1_matches_resident(X, O, shared):
+@pytest.mark.parametrize("shared,host_codec", [(0, False), (1, False), (0, True)])
+def test_expert_parallel_runner_world1_matches_resident(X, O, shared, host_codec):
     """The EP runner (session API + experts_forward + ordered combine [+ the rank's shared
     expert replica on its own tokens]) on one GPU."""
     from paper_2604_02715_b200.expert_parallel import ExpertParallelRunner
@@ -234,7 +234,7 @@ def test_expert_parallel_runner_world1_matches_resident(X, O, shared):
     fwd = X.ForwardSpec(16, 2, 7)
     container = X.generate_synthetic_model(spec, 7, shared_experts=shared)
     x = X.initial_activations(spec, fwd, 7)
-    runner = ExpertParallelRunner(spec, container, fwd, rank=0, world=1)
+    runner = ExpertParallelRunner(spec, container, fwd, rank=0, world=1, host_codec=host_codec)
     rep = runner.run(2, x)
     assert rep.page_fault is None and rep.violations == []
     assert rep.arena_peak_bytes == 2 * spec.experts_per_layer * spec.expert_bytes
