@@ -312,6 +312,8 @@ def main():
     ap.add_argument("--tokens", type=int, default=None)
     ap.add_argument("--budget", type=float, default=0.25,
                     help="expert-HBM budget as a fraction of the expert bytes (ring + codec buffers + shared)")
+    ap.add_argument("--tiering", default="device", choices=["device", "ring"],
+                    help="spend the budget on a compressed device tier + small ring (FluxMoE), or ring only")
     ap.add_argument("--prefill", action="store_true",
                     help="prefill regime: one step = a T-token prompt chunk through every layer (default T=8192)")
     ap.add_argument("--cpu-sample-tokens", type=int, default=4)
@@ -406,20 +408,54 @@ def main():
         runner = X.StreamedRunner(spec, hier, fwd, mode="threaded", device=dev, host_codec=args.host_codec, **run_kw)
         hbm = runner.ctx.hbm_bytes()
         expert_bytes = cspec.total_bytes + (container.shared.total_bytes if container.shared is not None else 0)
-        # fixed expert-slot budget (north star): expert weights resident in HBM -- ring slots,
-        # pinned experts, resident shared experts -- within args.budget of the expert bytes; the
-        # reference's two-layer ring is exactly 2/N.  Shared experts (DSv3) share the budget, so
-        # there the ring shrinks to a sub-layer ring (windows of ring/2 experts).  The codec's
-        # transient staging buffers and chunk index are reported beside it (footprint).
+        # fixed expert-HBM budget (north star): HBM holding expert weights -- ring slots, the
+        # compressed device tier, resident shared experts -- within args.budget of the expert
+        # bytes (the reference's own accounting: window + alpha x compressed pool,
+        # simulate.py:50-66).  --tiering device (default with the codec) spends the budget like
+        # FluxMoE: a small sub-layer ring, and every byte left holds experts 1..m of each layer
+        # compressed in HBM (decoded on-GPU into the ring), so only L-m experts per layer cross
+        # PCIe; --tiering ring keeps the reference's ring-only geometry.  The codec's transient
+        # staging buffers and chunk index are reported beside it (footprint).
         eb = cspec.expert_bytes
         shared_b = container.shared.total_bytes if container.shared is not None else 0
         ring_blocks = (hbm["ring"] - shared_b) // eb
-        ring_fit = int((args.budget * expert_bytes - shared_b + 1) // eb) & ~1
-        if 2 <= ring_fit < ring_blocks:
-            runner.ctx.set_ring_experts(ring_fit)
-            ring_blocks = ring_fit
-            hbm = runner.ctx.hbm_bytes()
-        budget = hbm["ring"] / expert_bytes
+        cap = args.budget * expert_bytes * 0.998 - shared_b  # margin: record sizes vary a little per expert
+        m_dev = 0
+        if args.tiering == "device" and args.host_codec:
+            Lc = cspec.experts_per_layer
+            dev_bytes = [runner.device_tier_bytes(m) for m in range(Lc + 1)]
+            best = None
+            # a window must carry >= 128 MB of raw weights (~1.5 ms of link time), so its fixed
+            # per-window costs (events, page-table ops, two GEMM launches) stay small
+            r_min = 2 * max(1, min(Lc, -(-(128 << 20) // eb)))
+            for r in range(r_min, 2 * Lc + 1, 2):  # most device-tier experts; then the largest ring
+                fit = [m for m in range(Lc + 1) if r * eb + dev_bytes[m] <= cap]
+                if fit and (best is None or (max(fit), r) > best):
+                    best = (max(fit), r)
+            if best and best[0] > 0:
+                m_dev, r = best
+                # m experts of every layer, spread over the ring windows (r/2 experts each) so
+                # every window mixes device-tier and host-tier experts (the link never idles on a
+                # window); inside a window they sit together, keeping the host records of a
+                # window contiguous in the pool (one DMA per run of small records)
+                w = r // 2
+                nw = -(-Lc // w)
+                per = [(j + 1) * m_dev // nw - j * m_dev // nw for j in range(nw)]  # evenly spread
+                mask = np.zeros((cspec.num_layers, Lc), dtype=bool)
+                for j in range(nw):
+                    mask[:, j * w:j * w + min(per[j], w, Lc - j * w)] = True
+                runner.set_device_mask(mask)
+                m_dev = int(mask[0].sum())
+                if r < ring_blocks:
+                    runner.ctx.set_ring_experts(r)
+                ring_blocks = min(r, ring_blocks)
+        if not m_dev:
+            ring_fit = int((cap + 1) // eb) & ~1
+            if 2 <= ring_fit < ring_blocks:
+                runner.ctx.set_ring_experts(ring_fit)
+                ring_blocks = ring_fit
+        hbm = runner.ctx.hbm_bytes()
+        budget = (hbm["ring"] + hbm["device_tier"]) / expert_bytes
         footprint = (hbm["ring"] + hbm["staging"] + hbm["device_tier"]) / expert_bytes
     x_host = X.initial_activations(spec, fwd, SEED + rank)
     x_dev = torch.from_numpy(x_host).to(f"cuda:{dev}")
@@ -532,9 +568,13 @@ def main():
                    "expert_hbm_budget": round(budget, 4),
                    "expert_hbm_footprint": round(footprint, 4) if not use_ep else None,
                    "ring_blocks_per_kind": int(ring_blocks) if not use_ep else None,
+                   "device_tier_experts_per_layer": m_dev if not use_ep else 0,
                    "placement": ("2-layer ring" if use_ep or ring_blocks >= 2 * cspec.experts_per_layer else
                                  f"sub-layer ring of {ring_blocks} expert blocks per kind (windows of "
-                                 f"{ring_blocks // 2} experts)") + ", host-only (alpha=0)" + (
+                                 f"{ring_blocks // 2} experts)") + (
+                       f", experts 1..{m_dev} of every layer compressed in HBM (device tier, alpha="
+                       f"{m_dev / cspec.experts_per_layer:.3f}), the rest host" if (not use_ep and m_dev) else
+                       ", host-only (alpha=0)") + (
                        ", exponent-Huffman records over PCIe decoded on-GPU into the ring (lossless)"
                        if args.host_codec else ""),
                    "l2": "inputs larger than L2: all %.1f GB of expert weights stream from host each step" % (cspec.total_bytes / 1e9)},

@@ -279,6 +279,19 @@ class StreamedRunner:
                                                            int(cm.chunk)))
         return total
 
+    def set_device_mask(self, mask) -> None:
+        """Placement by an explicit bool [N][L] mask of device-tier experts (the reference's
+        alpha split puts experts 1..m there; spreading them lets every window of a sub-layer
+        ring mix device-tier and host-tier experts, so the link never idles on a window)."""
+        spec = self.hierarchy.container.spec
+        mask = np.asarray(mask, dtype=bool).reshape(spec.num_layers, spec.experts_per_layer)
+        if mask.any():
+            self._compressed()
+        shard_map = np.repeat(mask[:, :, None], 2, axis=2).astype(np.uint8)
+        first, count = self._shard
+        self.ctx.set_placement(_full_width(self.spec, shard_map, first, count))
+        self.device_experts = [int(v) for v in mask.sum(axis=1)]
+
     def set_device_experts(self, m_layers) -> None:
         """Placement: experts 1..m_l of layer l on the compressed device tier, the rest on the
         host tier (the reference's alpha split per layer, storage.py:143-168).  Re-stages the

@@ -147,3 +147,25 @@ def test_mmap_container_pages_in_exactly(X, tmp_path):
         base = X.resident_baseline(2, spec, c, fwd, acts=x.copy())
         assert rep.violations == [] and rep.page_fault is None
         assert rep.final_activations.tobytes() == base.tobytes()
+
+
+def test_device_mask_spread_with_sub_layer_ring_exact(X):
+    """The bench's tiering: device-tier experts spread over the windows of a sub-layer ring,
+    host tier as compressed records -- still bit-identical to the resident model."""
+    import numpy as np
+
+    spec = X.ModelSpec(3, 12, 128, 256)
+    fwd = X.ForwardSpec(40, 3, 5)
+    container, hier = _runner(X, spec, 5, None, True)
+    runner = X.StreamedRunner(spec, hier, fwd, host_codec=True, ring_experts=6)
+    mask = np.zeros((3, 12), dtype=bool)
+    mask[:, [0, 4, 5, 9]] = True
+    runner.set_device_mask(mask)
+    assert runner.device_experts == [4, 4, 4]
+    x = X.initial_activations(spec, fwd, 5)
+    rep = runner.run(2, acts=x.copy())
+    base = X.resident_baseline(2, spec, container, fwd, acts=x.copy())
+    assert rep.violations == [] and rep.page_fault is None
+    assert rep.final_activations.tobytes() == base.tobytes()
+    hbm = runner.ctx.hbm_bytes()
+    assert hbm["device_tier"] > 0 and hbm["ring"] == 6 * spec.expert_bytes
