@@ -422,33 +422,37 @@ def main():
         cap = args.budget * expert_bytes * 0.998 - shared_b  # margin: record sizes vary a little per expert
         m_dev = 0
         if args.tiering == "device" and args.host_codec:
-            Lc = cspec.experts_per_layer
-            dev_bytes = [runner.device_tier_bytes(m) for m in range(Lc + 1)]
+            Lc, Nl = cspec.experts_per_layer, cspec.num_layers
+            cexp = runner.device_tier_bytes(Lc) / (Nl * Lc) * 1.002  # compressed expert (+ margin)
+            # a window holds >= 2 experts (so device- and host-tier experts can share it and the
+            # link never idles on a device-only window) and >= 128 MB of raw weights (~1.5 ms of
+            # link time, so its fixed per-window costs -- events, page-table ops, two GEMM
+            # launches -- stay small)
+            r_min = 2 * min(Lc, max(2, -(-(128 << 20) // eb)))
             best = None
-            # a window must carry >= 128 MB of raw weights (~1.5 ms of link time), so its fixed
-            # per-window costs (events, page-table ops, two GEMM launches) stay small
-            r_min = 2 * max(1, min(Lc, -(-(128 << 20) // eb)))
             for r in range(r_min, 2 * Lc + 1, 2):  # most device-tier experts; then the largest ring
-                fit = [m for m in range(Lc + 1) if r * eb + dev_bytes[m] <= cap]
-                if fit and (best is None or (max(fit), r) > best):
-                    best = (max(fit), r)
+                D = min(Nl * Lc, int((cap - r * eb) // cexp)) if cap >= r * eb else -1
+                if D >= 0 and (best is None or (D, r) > best):
+                    best = (D, r)
             if best and best[0] > 0:
-                m_dev, r = best
-                # m experts of every layer, spread over the ring windows (r/2 experts each) so
-                # every window mixes device-tier and host-tier experts (the link never idles on a
-                # window); inside a window they sit together, keeping the host records of a
-                # window contiguous in the pool (one DMA per run of small records)
+                D, r = best
+                # D experts over the layers (per-layer counts differ by at most one), each layer's
+                # spread over the ring windows (r/2 experts each) so every window mixes device-
+                # and host-tier experts (the link never idles on a window); inside a window they
+                # sit together, keeping that window's host records contiguous (one DMA per run)
                 w = r // 2
                 nw = -(-Lc // w)
-                per = [(j + 1) * m_dev // nw - j * m_dev // nw for j in range(nw)]  # evenly spread
-                mask = np.zeros((cspec.num_layers, Lc), dtype=bool)
-                for j in range(nw):
-                    mask[:, j * w:j * w + min(per[j], w, Lc - j * w)] = True
+                mask = np.zeros((Nl, Lc), dtype=bool)
+                for l in range(Nl):
+                    m_l = (l + 1) * D // Nl - l * D // Nl
+                    per = [(j + 1) * m_l // nw - j * m_l // nw for j in range(nw)]
+                    for j in range(nw):
+                        mask[l, j * w:j * w + min(per[j], w, Lc - j * w)] = True
                 runner.set_device_mask(mask)
-                m_dev = int(mask[0].sum())
                 if r < ring_blocks:
                     runner.ctx.set_ring_experts(r)
                 ring_blocks = min(r, ring_blocks)
+                m_dev = int(mask.sum()) / Nl
         if not m_dev:
             ring_fit = int((cap + 1) // eb) & ~1
             if 2 <= ring_fit < ring_blocks:
@@ -568,12 +572,13 @@ def main():
                    "expert_hbm_budget": round(budget, 4),
                    "expert_hbm_footprint": round(footprint, 4) if not use_ep else None,
                    "ring_blocks_per_kind": int(ring_blocks) if not use_ep else None,
-                   "device_tier_experts_per_layer": m_dev if not use_ep else 0,
+                   "device_tier_experts_per_layer": round(m_dev, 3) if not use_ep else 0,
                    "placement": ("2-layer ring" if use_ep or ring_blocks >= 2 * cspec.experts_per_layer else
                                  f"sub-layer ring of {ring_blocks} expert blocks per kind (windows of "
                                  f"{ring_blocks // 2} experts)") + (
-                       f", experts 1..{m_dev} of every layer compressed in HBM (device tier, alpha="
-                       f"{m_dev / cspec.experts_per_layer:.3f}), the rest host" if (not use_ep and m_dev) else
+                       f", {m_dev:.2f} experts per layer compressed in HBM (device tier, alpha="
+                       f"{m_dev / cspec.experts_per_layer:.3f}, spread over the ring windows), the rest host"
+                       if (not use_ep and m_dev) else
                        ", host-only (alpha=0)") + (
                        ", exponent-Huffman records over PCIe decoded on-GPU into the ring (lossless)"
                        if args.host_codec else ""),
