@@ -421,39 +421,19 @@ def main():
         ring_blocks = (hbm["ring"] - shared_b) // eb
         cap = args.budget * expert_bytes * 0.998 - shared_b  # margin: record sizes vary a little per expert
         m_dev = 0
+        pinned_per_layer = 0
         if args.tiering == "device" and args.host_codec:
+            from paper_2604_02715_b200.budget import plan_residency
+
             Lc, Nl = cspec.experts_per_layer, cspec.num_layers
-            cexp = runner.device_tier_bytes(Lc) / (Nl * Lc) * 1.002  # compressed expert (+ margin)
-            # a window holds >= 2 experts (so device- and host-tier experts can share it and the
-            # link never idles on a device-only window) and >= 128 MB of raw weights (~1.5 ms of
-            # link time, so its fixed per-window costs -- events, page-table ops, two GEMM
-            # launches -- stay small)
-            r_min = 2 * min(Lc, max(2, -(-(128 << 20) // eb)))
-            best = None
-            for r in range(r_min, 2 * Lc + 1, 2):  # most device-tier experts; then the largest ring
-                D = min(Nl * Lc, int((cap - r * eb) // cexp)) if cap >= r * eb else -1
-                if D >= 0 and (best is None or (D, r) > best):
-                    best = (D, r)
-            if best and best[0] > 0:
-                D, r = best
-                # D experts over the layers (per-layer counts differ by at most one), each layer's
-                # spread over the ring windows (r/2 experts each) so every window mixes device-
-                # and host-tier experts (the link never idles on a window); inside a window they
-                # sit together, keeping that window's host records contiguous (one DMA per run)
-                w = r // 2
-                nw = -(-Lc // w)
-                mask = np.zeros((Nl, Lc), dtype=bool)
-                for l in range(Nl):
-                    m_l = (l + 1) * D // Nl - l * D // Nl
-                    per = [(j + 1) * m_l // nw - j * m_l // nw for j in range(nw)]
-                    for j in range(nw):
-                        mask[l, j * w:j * w + min(per[j], w, Lc - j * w)] = True
-                runner.set_device_mask(mask)
-                if r < ring_blocks:
-                    runner.ctx.set_ring_experts(r)
-                ring_blocks = min(r, ring_blocks)
-                m_dev = int(mask.sum()) / Nl
-        if not m_dev:
+            ceb = runner.device_tier_bytes(Lc) / (Nl * Lc) * 1.002  # compressed expert (+ margin)
+            plan = plan_residency(Nl, Lc, eb, ceb, cap + shared_b, shared_bytes=shared_b)
+            if plan.device_experts or plan.pinned_experts:
+                runner.apply_plan(plan)
+                ring_blocks = min(plan.ring, ring_blocks) if plan.ring else ring_blocks
+                m_dev = plan.device_experts / Nl
+                pinned_per_layer = plan.pinned_experts / Nl
+        if not (m_dev or pinned_per_layer):
             ring_fit = int((cap + 1) // eb) & ~1
             if 2 <= ring_fit < ring_blocks:
                 runner.ctx.set_ring_experts(ring_fit)
@@ -573,6 +553,7 @@ def main():
                    "expert_hbm_footprint": round(footprint, 4) if not use_ep else None,
                    "ring_blocks_per_kind": int(ring_blocks) if not use_ep else None,
                    "device_tier_experts_per_layer": round(m_dev, 3) if not use_ep else 0,
+                   "pinned_experts_per_layer": round(pinned_per_layer, 3) if not use_ep else 0,
                    "placement": ("2-layer ring" if use_ep or ring_blocks >= 2 * cspec.experts_per_layer else
                                  f"sub-layer ring of {ring_blocks} expert blocks per kind (windows of "
                                  f"{ring_blocks // 2} experts)") + (

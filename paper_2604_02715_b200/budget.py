@@ -1,0 +1,110 @@
+"""Spending a fixed expert-HBM budget (BASELINE configs 2-5).
+
+The reference holds a two-layer window and moves a device-resident fraction alpha of
+the compressed experts (storage.py:143-168, simulate.py:50-66: window + alpha x
+compressed pool must fit the device budget).  On a B200 three kinds of residency
+compete for the same bytes:
+
+* ring blocks (raw, `eb` bytes each): the window every streamed expert passes through;
+  a sub-layer ring needs only 2 windows of w experts;
+* device-tier experts (compressed, `ceb` ≈ 0.66 eb each): no PCIe traffic, but decoded on
+  the GPU into the ring every step;
+* pinned experts (raw, `eb` each): neither link nor decode cost.
+
+`plan_residency` picks the ring, the device-tier and the pinned experts that minimise a
+step-time model -- link time of the host-tier records vs decode plus compute on the SMs
+-- under the budget.  It returns bool masks the runner applies (`StreamedRunner.apply_plan`).
+Counts are balanced across layers; inside a layer the pinned experts sit at the end, and
+the device-tier experts spread over the ring windows (each window mixes device- and
+host-tier experts, so the link never idles on a window, while a window's host records
+stay contiguous in the pool).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass
+class ResidencyPlan:
+    ring: int                 # ring blocks per kind (sub-layer ring when < 2 x streamed experts)
+    device_mask: np.ndarray   # bool [N][L]: compressed in HBM, decoded into the ring each step
+    pinned_mask: np.ndarray   # bool [N][L]: raw, resident for good
+    hbm_bytes: float          # ring + device tier + pinned (+ shared), the budget's numerator
+    est_step_s: float         # modelled step time
+    link_bytes: float         # host-tier record bytes per step
+
+    @property
+    def device_experts(self) -> int:
+        return int(self.device_mask.sum())
+
+    @property
+    def pinned_experts(self) -> int:
+        return int(self.pinned_mask.sum())
+
+
+def _spread_row(streamed: int, m: int, window: int) -> np.ndarray:
+    """m of the first `streamed` positions, spread over windows of `window`, contiguous inside."""
+    row = np.zeros(streamed, dtype=bool)
+    if m <= 0 or streamed <= 0:
+        return row
+    w = max(1, min(window, streamed))
+    nw = -(-streamed // w)
+    per = [(j + 1) * m // nw - j * m // nw for j in range(nw)]
+    for j in range(nw):
+        a = j * w
+        row[a:a + min(per[j], w, streamed - a)] = True
+    return row
+
+
+def _balanced(total: int, N: int):
+    return [(l + 1) * total // N - l * total // N for l in range(N)]
+
+
+def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *, shared_bytes: float = 0.0,
+                   b_link: float = 54e9, b_dec: float = 700e9, t_compute: float = 0.0,
+                   min_window_bytes: float = 128 * 2**20, allow_pinned: bool = True) -> ResidencyPlan:
+    """Choose (ring, device tier, pinned) for N layers x L experts under `budget_bytes`.
+
+    eb: raw bytes of one expert (both tensors); ceb: its compressed record bytes.
+    Step model: max(link_bytes / b_link, decoded_raw_bytes / b_dec + t_compute).
+    """
+    total = N * L
+    cap = budget_bytes - shared_bytes
+    w_min = int(min(L, max(2, -(-min_window_bytes // eb))))
+    best = None
+    p_grid = range(0, total + 1) if allow_pinned else [0]
+    for p in p_grid:
+        p_layer = _balanced(p, N)
+        streamed_max = L - min(p_layer)
+        if streamed_max == 0:
+            ring = 0
+        else:
+            ring = 2 * min(w_min, streamed_max)
+        room = cap - ring * eb - p * eb
+        if room < 0:
+            continue
+        d = int(min(total - p, room // ceb))
+        link = (total - p - d) * ceb
+        decode = (total - p) * eb
+        est = max(link / b_link, decode / b_dec + t_compute)
+        key = (est, -ring)
+        if best is None or key < best[0]:
+            best = (key, p, d, ring, link)
+    if best is None:
+        raise ValueError(f"budget {budget_bytes:.3g} B cannot hold a two-expert ring")
+    (est, _), p, d, ring, link = best
+    p_layer, d_layer = _balanced(p, N), _balanced(d, N)
+    pinned = np.zeros((N, L), dtype=bool)
+    for l in range(N):
+        if p_layer[l]:
+            pinned[l, L - p_layer[l]:] = True
+    device = np.zeros((N, L), dtype=bool)
+    w = max(1, ring // 2)
+    for l in range(N):
+        streamed = L - p_layer[l]
+        device[l, :streamed] = _spread_row(streamed, min(d_layer[l], streamed), w)
+    hbm = ring * eb + p * eb + device.sum() * ceb + shared_bytes
+    return ResidencyPlan(ring, device, pinned, float(hbm), float(est), float(link))

@@ -292,6 +292,19 @@ class StreamedRunner:
         self.ctx.set_placement(_full_width(self.spec, shard_map, first, count))
         self.device_experts = [int(v) for v in mask.sum(axis=1)]
 
+    def apply_plan(self, plan) -> None:
+        """Apply a budget.ResidencyPlan: pinned experts, device-tier experts, ring size."""
+        spec = self.hierarchy.container.spec
+        first, count = self._shard
+        if plan.pinned_mask.any():
+            full = np.zeros((self.spec.num_layers, self.spec.experts_per_layer), dtype=np.uint8)
+            full[:, first:first + count] = plan.pinned_mask.reshape(spec.num_layers, spec.experts_per_layer)
+            self.ctx.set_pinned(full)
+        streamed = spec.experts_per_layer - plan.pinned_mask.sum(axis=1).min()
+        if 0 < plan.ring < 2 * streamed:
+            self.ctx.set_ring_experts(int(plan.ring))
+        self.set_device_mask(plan.device_mask)
+
     def set_device_experts(self, m_layers) -> None:
         """Placement: experts 1..m_l of layer l on the compressed device tier, the rest on the
         host tier (the reference's alpha split per layer, storage.py:143-168).  Re-stages the

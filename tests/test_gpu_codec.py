@@ -169,3 +169,25 @@ def test_device_mask_spread_with_sub_layer_ring_exact(X):
     assert rep.final_activations.tobytes() == base.tobytes()
     hbm = runner.ctx.hbm_bytes()
     assert hbm["device_tier"] > 0 and hbm["ring"] == 6 * spec.expert_bytes
+
+
+@pytest.mark.parametrize("budget", [0.2, 0.6, 0.9, 1.0])
+def test_residency_plan_applied_stays_exact(X, budget):
+    """budget.plan_residency -> StreamedRunner.apply_plan (sub-layer ring + compressed device
+    tier + pinned experts in one context): bit-identical to resident, footprint in budget."""
+    from paper_2604_02715_b200.budget import plan_residency
+
+    spec = X.ModelSpec(3, 8, 128, 256)
+    fwd = X.ForwardSpec(24, 2, 9)
+    container, hier = _runner(X, spec, 9, None, True)
+    runner = X.StreamedRunner(spec, hier, fwd, host_codec=True)
+    ceb = runner.device_tier_bytes(8) / 24 * 1.002
+    plan = plan_residency(3, 8, spec.expert_bytes, ceb, budget * spec.total_bytes, min_window_bytes=1)
+    runner.apply_plan(plan)
+    x = X.initial_activations(spec, fwd, 9)
+    rep = runner.run(2, acts=x.copy())
+    base = X.resident_baseline(2, spec, container, fwd, acts=x.copy())
+    assert rep.violations == [] and rep.page_fault is None
+    assert rep.final_activations.tobytes() == base.tobytes()
+    hbm = runner.ctx.hbm_bytes()
+    assert hbm["ring"] + hbm["device_tier"] <= budget * spec.total_bytes * 1.001

@@ -220,3 +220,31 @@ def test_cli_generate_compress_match_reference_bytes(tmp_path):
     assert hashlib.sha256(xpgc.read_bytes()).hexdigest() == meta["xpgc_3_2_32_64_4"]["sha256"]
     # XPGC ingest is host-only (bit counts from the index scan) and round-trips its bytes
     assert CompressedModel.read(xpgc).to_bytes() == xpgc.read_bytes()
+
+
+def test_residency_plan_spends_the_budget():
+    """budget.plan_residency: within budget, link-bound budgets buy compressed device-tier
+    experts (1.5x more experts per byte than pinning), large budgets pin experts, masks are
+    disjoint and every ring window mixes device- and host-tier experts."""
+    import numpy as np
+
+    from paper_2604_02715_b200.budget import plan_residency
+
+    eb = 352321536
+    ceb = 0.662 * eb
+    total = 64 * eb
+    prev = None
+    for b in (0.1, 0.25, 0.5, 0.8, 1.0):
+        pl = plan_residency(8, 8, eb, ceb, b * total)
+        assert pl.hbm_bytes <= b * total + 1
+        assert not (pl.device_mask & pl.pinned_mask).any()
+        if prev is not None:
+            assert pl.est_step_s <= prev + 1e-12  # more budget never slower
+        prev = pl.est_step_s
+    pl = plan_residency(8, 8, eb, ceb, 0.25 * total)
+    assert pl.pinned_experts == 0 and pl.device_experts == 18 and pl.ring == 4
+    w = pl.ring // 2
+    for l in range(8):  # windows of 2 experts: a device expert never shares a window with another
+        for j in range(0, 8, w):
+            assert pl.device_mask[l, j:j + w].sum() <= 1
+    assert plan_residency(8, 8, eb, ceb, 1.0 * total).pinned_experts == 64

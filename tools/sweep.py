@@ -1,10 +1,11 @@
 """Sweeps for BASELINE configs 3 and 5 (one JSON line per point).
 
-    python tools/sweep.py budget [--config mixtral] [--tokens 256] [--raw] [--rings 6,8,12]
-        paging budget from a sub-layer ring (--rings: expert blocks per kind, below the
-        reference's two layers) through the 2-layer ring (25% at N=8) up to fully resident,
-        by pinning experts 1..m of every layer (residency tier x > 0); fully-resident
-        comparator beside every point
+    python tools/sweep.py budget [--config mixtral] [--tokens 256] [--budgets 0.1,0.15,...]
+        expert-HBM budget 10-100%: each budget spent by budget.plan_residency (sub-layer ring,
+        compressed device tier, pinned experts); fully-resident comparator beside every point
+    python tools/sweep.py budget-ring [--config mixtral] [--rings 6,8,12]
+        the reference's geometry instead: sub-layer rings below two layers, then pinning
+        experts 1..m of every layer (residency tier x > 0), host tier only
     python tools/sweep.py tokens [--config qwen3] [--list 1,4,16,64,256]
         decode batch sweep under the fixed 2-layer-ring budget
 """
@@ -31,7 +32,8 @@ def timed(torch, fn, steps):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["budget", "tokens"])
+    ap.add_argument("what", choices=["budget", "budget-ring", "tokens"])
+    ap.add_argument("--budgets", default="0.1,0.15,0.2,0.25,0.35,0.5,0.65,0.8,1.0")
     ap.add_argument("--config", default=None)
     ap.add_argument("--tokens", type=int, default=None)
     ap.add_argument("--list", default="1,4,16,64,256")
@@ -45,7 +47,7 @@ def main():
     import paper_2604_02715_b200 as X
     from paper_2604_02715_b200.exponent_codec import CompressedModel
 
-    cfg = dict(CONFIGS[args.config or ("mixtral" if args.what == "budget" else "qwen3")])
+    cfg = dict(CONFIGS[args.config or ("qwen3" if args.what == "tokens" else "mixtral")])
     if args.tokens:
         cfg["T"] = args.tokens
     N, L, H, F, k = cfg["N"], cfg["L"], cfg["H"], cfg["F"], cfg["k"]
@@ -58,25 +60,37 @@ def main():
         hier.compressed = CompressedModel.from_container(container)
     peak = h2d_peak_gbps(torch, 0)
     print(f"setup {time.time() - t0:.1f}s", file=sys.stderr, flush=True)
-    if args.what == "budget":
+    if args.what == "budget-ring":
         points = [("ring", int(r)) for r in args.rings.split(",") if r] + [("pinned", p) for p in range(0, L)]
+    elif args.what == "budget":
+        points = [("plan", float(b)) for b in args.budgets.split(",") if b]
     else:
         points = [("tokens", int(t)) for t in args.list.split(",")]
     resident_tok = {}
     for what, p in points:
-        T = p if what == "tokens" else cfg["T"]
+        T = int(p) if what == "tokens" else cfg["T"]
         fwd = X.ForwardSpec(T, k, SEED)
         x = torch.from_numpy(X.initial_activations(spec, fwd, SEED)).cuda()
         runner = X.StreamedRunner(spec, hier, fwd, host_codec=not args.raw,
                                   pinned=(p if what == "pinned" else None),
                                   ring_experts=(p if what == "ring" else None))
+        plan = None
+        if what == "plan":
+            from paper_2604_02715_b200.budget import plan_residency
+
+            ceb = runner.device_tier_bytes(L) / (N * L) * 1.002
+            plan = plan_residency(N, L, spec.expert_bytes, ceb, p * spec.total_bytes)
+            runner.apply_plan(plan)
         runner.run(args.warmup, acts=x)
         secs, rep = timed(torch, lambda s: runner.run(s, acts=x), args.steps)
         hbm = runner.ctx.hbm_bytes()
         row = {"sweep": args.what, "config": args.config or cfg["name"], "T": T,
-               "pinned_per_layer": p if what == "pinned" else 0,
-               "ring_experts": p if what == "ring" else 2 * (L - (p if what == "pinned" else 0)),
-               "hbm_fraction": (hbm["ring"] + hbm["staging"] + hbm["device_tier"]) / spec.total_bytes,
+               "budget": p if what == "plan" else None,
+               "pinned_per_layer": (plan.pinned_experts / N if plan else (p if what == "pinned" else 0)),
+               "device_tier_per_layer": plan.device_experts / N if plan else 0,
+               "ring_experts": (plan.ring if plan else (p if what == "ring" else 2 * (L - (p if what == "pinned" else 0)))),
+               "hbm_fraction": (hbm["ring"] + hbm["device_tier"]) / spec.total_bytes,
+               "hbm_footprint": (hbm["ring"] + hbm["staging"] + hbm["device_tier"]) / spec.total_bytes,
                "tok_s": T * args.steps / secs, "ms_per_step": 1e3 * secs / args.steps,
                "page_in_gbps": rep.h2d_bytes / rep.elapsed_seconds / 1e9 if rep.elapsed_seconds else 0.0,
                "h2d_peak_gbps": peak, "exposed_xfer_pct": 100 * rep.stall_seconds / max(rep.elapsed_seconds, 1e-12),
