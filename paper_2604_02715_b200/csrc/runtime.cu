@@ -1895,7 +1895,7 @@ int xpgb_hbm_bytes(xpgb_ctx* h, uint64_t* ring, uint64_t* staging, uint64_t* dev
 // Re-create the arena for a residency mask and ring cap: pinned experts get dedicated
 // blocks (filled from the host pool), the ring gets 2 x (most streamed experts of any
 // layer) blocks per kind, capped by ring_limit (sub-layer ring).
-static void apply_residency(Ctx* c, const std::vector<uint8_t>& mask) {
+static void apply_residency(Ctx* c, std::vector<uint8_t> mask) {  // by value: callers pass c->pinned, which init_pools clears
   int n_pinned = 0, max_streamed = 0;
   for (int l = 0; l < c->N; ++l) {
     int streamed = 0;

@@ -174,3 +174,21 @@ def test_ring_experts_argument_checks():
     with pytest.raises(OutOfRangeError):
         ctx.set_ring_experts(1)
     ctx.set_ring_experts(-1)
+
+
+def test_ring_resize_keeps_pinned_experts():
+    """set_ring_experts after set_pinned keeps the pinned experts resident (regression: the
+    arena rebuild used to clear the mask it was reading)."""
+    import paper_2604_02715_b200 as X
+
+    spec = X.ModelSpec(3, 6, 64, 128)
+    c = X.generate_synthetic_model(spec, 2)
+    backends = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 30e9, 1 << 40)]
+    hier = X.StorageHierarchy(c, None, X.plan_placement(spec, backends), backends)
+    fwd = X.ForwardSpec(8, 2, 1)
+    runner = X.StreamedRunner(spec, hier, fwd, pinned=2)
+    runner.ctx.set_ring_experts(2)
+    x = X.initial_activations(spec, fwd, 1)
+    rep = runner.run(1, acts=x.copy())
+    assert rep.h2d_bytes == spec.num_layers * (spec.experts_per_layer - 2) * spec.expert_bytes
+    assert rep.final_activations.tobytes() == X.resident_baseline(1, spec, c, fwd, acts=x.copy()).tobytes()
