@@ -375,8 +375,22 @@ def main():
         group = None
         runner = ExpertParallelRunner(spec, None, fwd, rank, world, device=dev, group=group, shard_pool=shard.pinned,
                                       shared=shard.shared, host_codec=args.host_codec)
-        budget = 2.0 / N  # 2-layer ring of this rank's shard
-        footprint = None
+        shard_bytes = shard.spec.total_bytes + (shard.shared.total_bytes if shard.shared is not None else 0)
+        m_dev = pinned_per_layer = 0
+        if args.tiering == "device" and args.host_codec:
+            # the same budget planner on this rank's shard (budget.plan_residency)
+            from paper_2604_02715_b200.budget import plan_residency
+
+            ceb = runner.device_tier_bytes(count) / (N * count) * 1.002
+            sh_b = shard.shared.total_bytes if shard.shared is not None else 0
+            plan = plan_residency(N, count, shard.spec.expert_bytes, ceb, args.budget * shard_bytes * 0.998,
+                                  shared_bytes=sh_b)
+            if plan.device_experts or plan.pinned_experts:
+                runner.apply_plan(plan)
+                m_dev, pinned_per_layer = plan.device_experts / N, plan.pinned_experts / N
+        hbm = runner.ctx.hbm_bytes()
+        budget = (hbm["ring"] + hbm["device_tier"]) / shard_bytes
+        footprint = (hbm["ring"] + hbm["staging"] + hbm["device_tier"]) / shard_bytes
     else:
         backends = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 55e9, 1 << 50)]
         hier = X.StorageHierarchy(container, None, X.plan_placement(cspec, backends), backends)
@@ -550,16 +564,16 @@ def main():
         "data": "synthetic (random-init N(0,0.02) bf16 weights drawn on-GPU, N(0,1) activations)",
         "config": {"workload": cfg["name"], "tokens_per_step": T, "top_k": k, "layers": N,
                    "expert_hbm_budget": round(budget, 4),
-                   "expert_hbm_footprint": round(footprint, 4) if not use_ep else None,
+                   "expert_hbm_footprint": round(footprint, 4),
                    "ring_blocks_per_kind": int(ring_blocks) if not use_ep else None,
-                   "device_tier_experts_per_layer": round(m_dev, 3) if not use_ep else 0,
-                   "pinned_experts_per_layer": round(pinned_per_layer, 3) if not use_ep else 0,
+                   "device_tier_experts_per_layer": round(m_dev, 3),
+                   "pinned_experts_per_layer": round(pinned_per_layer, 3),
                    "placement": ("2-layer ring" if use_ep or ring_blocks >= 2 * cspec.experts_per_layer else
                                  f"sub-layer ring of {ring_blocks} expert blocks per kind (windows of "
                                  f"{ring_blocks // 2} experts)") + (
                        f", {m_dev:.2f} experts per layer compressed in HBM (device tier, alpha="
-                       f"{m_dev / cspec.experts_per_layer:.3f}, spread over the ring windows), the rest host"
-                       if (not use_ep and m_dev) else
+                       f"{m_dev / (count if use_ep else cspec.experts_per_layer):.3f}, spread over the ring windows), "
+                       f"the rest host" if m_dev else
                        ", host-only (alpha=0)") + (
                        ", exponent-Huffman records over PCIe decoded on-GPU into the ring (lossless)"
                        if args.host_codec else ""),

@@ -280,6 +280,9 @@ int xpgb_session_abort(xpgb_ctx* ctx);
  * caller orders its own H2D/D2H of acts_dev on it).  steps_per_iteration = N in the reference
  * geometry, N x windows with a sub-layer ring. */
 int xpgb_session_info(xpgb_ctx* ctx, int32_t* steps_total, int32_t* steps_per_iteration, void** compute_stream);
+/* Step `step` of the active session: info[7] = {iteration, layer, window, first local expert,
+ * end local expert (exclusive, routed experts only), first window of its layer (0/1), last (0/1)}. */
+int xpgb_session_step(xpgb_ctx* ctx, int32_t step, int32_t* info);
 /* Ordering log of the last run (OrderingLog.records, pipeline.py:94-116). */
 int xpgb_log_get(xpgb_ctx* ctx, xpgb_record* out, int32_t cap, int32_t* n);
 
@@ -300,6 +303,11 @@ int xpgb_experts_forward(xpgb_ctx* ctx, int32_t layer, const void* rows_dev, con
  * replica to its own tokens after the routed combine): y[t] += sum_s shared_s(x[t]) in fp32,
  * shared experts in ascending order, weight 1.  x, y: device fp32 [tokens][H]. */
 int xpgb_shared_forward(xpgb_ctx* ctx, int32_t layer, const float* x_dev, float* y_dev, int32_t tokens, void* stream);
+/* One window of a layer on pre-grouped rows: GEMMs of local experts [e0, e1) only (rows stay
+ * absolute; the rows are copied in with the e0 == 0 window); reduce = 1 on the layer's last
+ * window writes every row's output (split-K partials of all windows are final by then). */
+int xpgb_experts_forward_range(xpgb_ctx* ctx, int32_t layer, const void* rows_dev, const int32_t* offsets_dev,
+                               int32_t n_rows, int32_t e0, int32_t e1, int32_t reduce, float* out_dev, void* stream);
 int xpgb_combine_rows(const float* rows_dev, const int32_t* index_dev, int32_t tokens, int32_t kk, int32_t top_k,
                       int32_t hidden, float* y_dev, void* stream);
 

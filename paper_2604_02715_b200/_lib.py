@@ -116,6 +116,8 @@ _SIGS = {
     "xpgb_set_shared_tokens": [_P, _I, _I],
     "xpgb_shared_forward": [_P, _I, _P, _P, _I, _P],
     "xpgb_experts_forward": [_P, _I, _P, _P, _I, _P, _P],
+    "xpgb_experts_forward_range": [_P, _I, _P, _P, _I, _I, _I, _I, _P, _P],
+    "xpgb_session_step": [_P, _I, C.POINTER(C.c_int32)],
     "xpgb_combine_rows": [_P, _P, _I, _I, _I, _I, _P, _P],
     "xpgb_codec_histogram": [_P, _U64, C.POINTER(_U64), _I],
     "xpgb_codec_encode": [_P, _U64, C.POINTER(C.c_uint8), _P, _P, _U64, C.POINTER(_U64), C.POINTER(_U64),

@@ -250,7 +250,8 @@ struct Ctx {
   uint64_t stage_cap[2] = {0, 0};
   cudaStream_t s_dec[2] = {nullptr, nullptr};
   cudaStream_t s_alt[2] = {nullptr, nullptr};  // second copy stream per kind for staged pieces
-  cudaEvent_t ev_copied[2][2], ev_decoded[2][2], ev_mapped[2], ev_raw[2];
+  cudaStream_t s_devdec[2] = {nullptr, nullptr};  // device-tier decodes: never queue behind the link
+  cudaEvent_t ev_copied[2][2], ev_decoded[2][2], ev_mapped[2], ev_raw[2], ev_devdec[2];
   bool codec_events = false;
 
   // profiling
@@ -774,9 +775,12 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
     // compressed tiers: records reach a decode stream (copied over PCIe into a staging
     // buffer for the host tier, read in place for the device tier) and are expanded
     // straight into the ring block; staging is double-buffered so the link never waits.
-    cudaStream_t d = c->s_dec[k];
+    // host-tier records decode on d behind their copies; device-tier records decode on dv,
+    // which only waits for the window's mapping, so they run while the link is busy
+    cudaStream_t d = c->s_dec[k], dv = c->s_devdec[k];
     CK(cudaEventRecord(c->ev_mapped[k], s));
     CK(cudaStreamWaitEvent(d, c->ev_mapped[k], 0));
+    bool dev_on_dv = false;
     if (c->host_codec) CK(cudaStreamWaitEvent(c->s_alt[k], c->ev_mapped[k], 0));
     bool raw_on_s = false;
     int hb = 0;
@@ -797,7 +801,9 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
       const float dl = delay_of(e);
       if (c->backend[ti] == 1) {
         // device tier: consecutive device-tier experts of the layer decode in one launch
-        if (dl > 0) sleep_on(d, dl);
+        if (!dev_on_dv) CK(cudaStreamWaitEvent(dv, c->ev_mapped[k], 0));
+        dev_on_dv = true;
+        if (dl > 0) sleep_on(dv, dl);
         int cnt = 0;
         for (int e2 = e;; ++e2) {
           const size_t t2 = tix(e2);
@@ -808,7 +814,7 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
                                    reinterpret_cast<uint16_t*>(block_ptr(c, kind, blocks[e2])), 0u};
           if (cnt == kMaxDecodeTensors || !joins_run(e2, e2 + 1, 1)) break;
         }
-        launch_exp_decode_multi(dt, cnt, n, c->cchunk, c->ctab, d);
+        launch_exp_decode_multi(dt, cnt, n, c->cchunk, c->ctab, dv);
         CKLAUNCH();
         rs.decoded += 2 * n * cnt;
         e += cnt;
@@ -903,6 +909,10 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
     if (raw_on_s) {
       CK(cudaEventRecord(c->ev_raw[k], s));
       CK(cudaStreamWaitEvent(d, c->ev_raw[k], 0));
+    }
+    if (dev_on_dv) {
+      CK(cudaEventRecord(c->ev_devdec[k], dv));
+      CK(cudaStreamWaitEvent(d, c->ev_devdec[k], 0));
     }
     done_stream = d;
   }
@@ -1315,6 +1325,8 @@ static void set_codec(Ctx* c, const void* pool, uint64_t pool_bytes, const uint6
     for (int k = 0; k < 2; ++k) {
       CK(cudaStreamCreateWithFlags(&c->s_dec[k], cudaStreamNonBlocking));
       CK(cudaStreamCreateWithFlags(&c->s_alt[k], cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&c->s_devdec[k], cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&c->ev_devdec[k], cudaEventDisableTiming));
       for (int b = 0; b < 2; ++b) {
         CK(cudaEventCreateWithFlags(&c->ev_copied[k][b], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_decoded[k][b], cudaEventDisableTiming));
@@ -1469,6 +1481,8 @@ int xpgb_destroy(xpgb_ctx* h) {
       for (int k = 0; k < 2; ++k) {
         cudaStreamDestroy(c->s_dec[k]);
         cudaStreamDestroy(c->s_alt[k]);
+        cudaStreamDestroy(c->s_devdec[k]);
+        cudaEventDestroy(c->ev_devdec[k]);
         for (int b = 0; b < 2; ++b) {
           cudaEventDestroy(c->ev_copied[k][b]);
           cudaEventDestroy(c->ev_decoded[k][b]);
@@ -2092,6 +2106,17 @@ int xpgb_session_end(xpgb_ctx* h, xpgb_report* rep) {
 int xpgb_session_abort(xpgb_ctx* h) {
   return guard([&] { session_abort(&h->c); });
 }
+int xpgb_session_step(xpgb_ctx* h, int32_t step, int32_t* info) {
+  return guard([&] {
+    Session& ss = session_of(&h->c);
+    if (!ss.active) XFAIL(XPGB_ERR, "no active session");
+    if (step < 0 || step >= ss.steps) XFAIL(XPGB_ERR_OUT_OF_RANGE, "step %d outside [0, %d)", step, ss.steps);
+    const Step& st = ss.sv[step];
+    const int v[7] = {st.it, st.layer, st.w, st.e0, std::min(st.e1, h->c.E), st.first ? 1 : 0, st.last ? 1 : 0};
+    memcpy(info, v, sizeof(v));
+  });
+}
+
 int xpgb_session_info(xpgb_ctx* h, int32_t* steps_total, int32_t* steps_per_iteration, void** compute_stream) {
   return guard([&] {
     Session& ss = session_of(&h->c);
@@ -2128,26 +2153,46 @@ int xpgb_set_expert_shard(xpgb_ctx* h, int32_t expert_first, int32_t expert_coun
   });
 }
 
+static void experts_forward_range(Ctx* c, int layer, const void* rows_dev, const int32_t* offsets_dev, int n_rows,
+                                  int e0, int e1, bool reduce, float* out_dev, cudaStream_t s) {
+  if (layer < 1 || layer > c->N) XFAIL(XPGB_ERR_OUT_OF_RANGE, "layer %d outside [1, %d]", layer, c->N);
+  if (e0 < 0 || e1 > c->E || e0 >= e1) XFAIL(XPGB_ERR_OUT_OF_RANGE, "expert range [%d, %d) outside [0, %d)", e0, e1, c->E);
+  if (n_rows > c->cap_rows || !c->xp) ensure_work(c, std::max(n_rows, 1), 1);
+  if (n_rows == 0) return;
+  // the layer's rows arrive once, with its first window; later windows reuse them
+  if (e0 == 0) CK(cudaMemcpyAsync(c->xp, rows_dev, (size_t)n_rows * c->H * 2, cudaMemcpyDeviceToDevice, s));
+  const int bn = pick_bn_rows((double)n_rows / std::max(1, c->E));
+  const int splits = pick_splits(c, n_rows, 1, bn);  // same for every window of the layer
+  GemmParams pg = gemm_params(c, layer, 1, offsets_dev, 1, false), pd = gemm_params(c, layer, 2, offsets_dev, splits, false);
+  pd.split_stride = (long long)n_rows * c->H;
+  for (GemmParams* p : {&pg, &pd}) {  // window: groups [e0, e1), rows stay absolute
+    p->offsets += e0;
+    p->pt += e0;
+    p->e_first += e0;
+    p->E = p->E_routed = e1 - e0;
+  }
+  launch_gate_up(c->map_gu, c->map_xp, c->map_gu, pg, bn, c->num_sms, s);
+  CKLAUNCH();
+  launch_down(c->map_dn, c->map_h, c->map_dn, pd, bn, c->num_sms, s);
+  CKLAUNCH();
+  if (reduce) {  // after the layer's last window: every row's split-K partials are final
+    launch_reduce_rows(c->part, c->d_fault, out_dev, n_rows, c->H, splits, pd.split_stride, s);
+    CKLAUNCH();
+  }
+}
+
 int xpgb_experts_forward(xpgb_ctx* h, int32_t layer, const void* rows_dev, const int32_t* offsets_dev,
                          int32_t n_rows, float* out_dev, void* stream) {
   return guard([&] {
-    Ctx* c = &h->c;
-    if (layer < 1 || layer > c->N) XFAIL(XPGB_ERR_OUT_OF_RANGE, "layer %d outside [1, %d]", layer, c->N);
-    cudaStream_t s = (cudaStream_t)stream;
-    if (n_rows > c->cap_rows || !c->xp) ensure_work(c, std::max(n_rows, 1), 1);
-    if (n_rows == 0) return;
-    CK(cudaMemcpyAsync(c->xp, rows_dev, (size_t)n_rows * c->H * 2, cudaMemcpyDeviceToDevice, s));
-    const int bn = pick_bn_rows((double)n_rows / std::max(1, c->E));
-    const int splits = pick_splits(c, n_rows, 1, bn);
-    launch_gate_up(c->map_gu, c->map_xp, c->map_gu, gemm_params(c, layer, 1, offsets_dev, 1, false), bn, c->num_sms,
-                   s);
-    CKLAUNCH();
-    GemmParams pd = gemm_params(c, layer, 2, offsets_dev, splits, false);
-    pd.split_stride = (long long)n_rows * c->H;
-    launch_down(c->map_dn, c->map_h, c->map_dn, pd, bn, c->num_sms, s);
-    CKLAUNCH();
-    launch_reduce_rows(c->part, c->d_fault, out_dev, n_rows, c->H, splits, pd.split_stride, s);
-    CKLAUNCH();
+    experts_forward_range(&h->c, layer, rows_dev, offsets_dev, n_rows, 0, h->c.E, true, out_dev, (cudaStream_t)stream);
+  });
+}
+
+int xpgb_experts_forward_range(xpgb_ctx* h, int32_t layer, const void* rows_dev, const int32_t* offsets_dev,
+                               int32_t n_rows, int32_t e0, int32_t e1, int32_t reduce, float* out_dev, void* stream) {
+  return guard([&] {
+    experts_forward_range(&h->c, layer, rows_dev, offsets_dev, n_rows, e0, std::min(e1, h->c.E), reduce != 0, out_dev,
+                          (cudaStream_t)stream);
   });
 }
 

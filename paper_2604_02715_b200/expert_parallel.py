@@ -196,18 +196,27 @@ class ExpertParallelMoE:
         return build_plan(routes, self.rank, self.world, tokens, self.bounds)
 
     def forward(self, layer: int, x, plan: DispatchPlan | None = None):
-        import torch
-        import torch.distributed as dist
+        plan = plan or self.plan(layer, x.shape[0])
+        rows = self.dispatch(x, plan)
+        return self.combine(layer, x, self.expert_fn(layer, rows, plan.offsets), plan)
 
-        T, H = x.shape
-        plan = plan or self.plan(layer, T)
+    def dispatch(self, x, plan: DispatchPlan):
+        """Send this rank's (token, expert) rows to the owners; returns the rows of its own
+        experts, expert-major (bf16 [n_recv, H])."""
+        import torch
+
         send = x.index_select(0, plan.send_rows).to(torch.bfloat16)
-        recv = torch.empty((sum(plan.recv_counts), H), dtype=torch.bfloat16, device=x.device)
+        recv = torch.empty((sum(plan.recv_counts), x.shape[1]), dtype=torch.bfloat16, device=x.device)
         self._a2a(recv, send, plan.recv_counts, plan.send_counts)
-        rows = recv.index_select(0, plan.to_expert)
-        out = self.expert_fn(layer, rows, plan.offsets)
+        return recv.index_select(0, plan.to_expert)
+
+    def combine(self, layer: int, x, out, plan: DispatchPlan):
+        """Return the owners' fp32 expert outputs to their tokens; ordered weighted sum
+        (+ this rank's shared-expert replica on its own tokens)."""
+        import torch
+
         back = out.index_select(0, plan.from_expert)
-        ret = torch.empty((send.shape[0], H), dtype=torch.float32, device=x.device)
+        ret = torch.empty((plan.send_rows.shape[0], x.shape[1]), dtype=torch.float32, device=x.device)
         self._a2a(ret, back, plan.send_counts, plan.recv_counts)
         y = self.combine_fn(ret, plan.ret_index, self.fwd.top_k)
         if self.shared_fn is not None:
@@ -248,6 +257,8 @@ class ExpertParallelRunner:
         self.fwd = fwd
         self.rank, self.world = rank, world
         first, count = shard_bounds(spec.experts_per_layer, world)[rank]
+        self.shard = (first, count)
+        self._codec = None
         self.ctx = Context(spec, _lib.POOL_RING, device, max_tokens=world * fwd.tokens_per_step)
         self.ctx.set_expert_shard(first, count)
         pool = shard_pool if shard_pool is not None else shard_payload(container, first, count)
@@ -264,6 +275,33 @@ class ExpertParallelRunner:
             self.ctx.set_shared(shared)  # every rank holds a replica (resident, never paged)
         self.moe = ExpertParallelMoE(spec, fwd, rank, world, group=group, ctx=self.ctx,
                                      has_shared=shared is not None)
+
+    def device_tier_bytes(self, m: int) -> int:
+        from ._lib import lib
+        from .geometry import iter_tensor_ids
+
+        cm, total = self._codec, 0
+        for i, tid in enumerate(iter_tensor_ids(cm.spec)):
+            if tid.expert <= m:
+                total += int(lib().xpgb_codec_record_bytes(cm.spec.value_count(tid.kind), int(cm.bits_lens[i]),
+                                                           int(cm.chunk)))
+        return total
+
+    def apply_plan(self, plan) -> None:
+        """A budget.ResidencyPlan for this rank's shard (pinned, device tier, ring)."""
+        from .streamed import _full_width
+
+        N, L = self.spec.num_layers, self.spec.experts_per_layer
+        first, count = self.shard
+        if plan.pinned_mask.any():
+            full = np.zeros((N, L), dtype=np.uint8)
+            full[:, first:first + count] = plan.pinned_mask
+            self.ctx.set_pinned(full)
+        streamed = count - plan.pinned_mask.sum(axis=1).min()
+        if 0 < plan.ring < 2 * streamed:
+            self.ctx.set_ring_experts(int(plan.ring))
+        shard_map = np.repeat(plan.device_mask[:, :, None], 2, axis=2).astype(np.uint8)
+        self.ctx.set_placement(_full_width(self.spec, shard_map, first, count))
 
     def run(self, iterations: int, acts, profile: bool = False) -> RunReport:
         import torch
@@ -287,13 +325,27 @@ class ExpertParallelRunner:
         try:
             call("xpgb_session_materialize", h, 0)
             call("xpgb_session_materialize", h, 1)
-            for g in range(iterations * N):
-                layer = g % N + 1
+            total = C.c_int32()
+            call("xpgb_session_info", h, C.byref(total), None, None)
+            info = (C.c_int32 * 7)()
+            rows = out = None
+            for g in range(total.value):  # steps are layers, or windows of a sub-layer ring
+                call("xpgb_session_step", h, g, info)
+                layer, e0, e1, first, last = info[1], info[3], info[4], info[5], info[6]
+                plan = plans[layer - 1]
                 st = C.c_void_p(current_stream_ptr(self.ctx.device))
+                if first:
+                    rows = self.moe.dispatch(x, plan)
+                    out = torch.empty((rows.shape[0], self.spec.hidden_dim), dtype=torch.float32, device=x.device)
                 call("xpgb_session_acquire", h, g, st)
-                x = self.moe.forward(layer, x, plans[layer - 1])
+                if rows.shape[0] and e1 > e0:
+                    call("xpgb_experts_forward_range", h, layer, C.c_void_p(rows.data_ptr()),
+                         C.c_void_p(plan.offsets.data_ptr()), int(rows.shape[0]), e0, e1, 1 if last else 0,
+                         C.c_void_p(out.data_ptr()), st)
                 call("xpgb_session_release", h, g, st)
                 call("xpgb_session_materialize", h, g + 2)
+                if last:
+                    x = self.moe.combine(layer, x, out, plan)
         except Exception:
             _lib.lib().xpgb_session_abort(h)
             raise

@@ -242,6 +242,28 @@ def test_expert_parallel_runner_world1_matches_resident(X, O, shared, host_codec
     assert O.rel_l2(rep.final_activations.cpu().numpy(), base) <= 1e-3
 
 
+def test_expert_parallel_runner_windows_and_device_tier(X, O):
+    """EP runner on a budget plan: sub-layer ring windows (experts_forward_range per window,
+    dispatch before the first, combine after the last) + compressed device tier + pinned."""
+    from paper_2604_02715_b200.budget import plan_residency
+    from paper_2604_02715_b200.expert_parallel import ExpertParallelRunner
+
+    spec = X.ModelSpec(3, 8, 128, 256)
+    fwd = X.ForwardSpec(24, 2, 5)
+    container = X.generate_synthetic_model(spec, 5)
+    x = X.initial_activations(spec, fwd, 5)
+    base = X.resident_baseline(2, spec, container, fwd, acts=x.copy())
+    for budget in (0.3, 0.7):
+        runner = ExpertParallelRunner(spec, container, fwd, rank=0, world=1, host_codec=True)
+        ceb = runner.device_tier_bytes(8) / 24 * 1.002
+        plan = plan_residency(3, 8, spec.expert_bytes, ceb, budget * spec.total_bytes, min_window_bytes=1)
+        assert plan.ring < 16  # a sub-layer ring: several windows per layer
+        runner.apply_plan(plan)
+        rep = runner.run(2, x)
+        assert rep.page_fault is None and rep.violations == []
+        assert O.rel_l2(rep.final_activations.cpu().numpy(), base) <= 1e-3
+
+
 def test_session_api_external_compute_matches_run(X):
     """begin/materialize/acquire/compute/release/end reproduces run() bit for bit."""
     import ctypes as C
