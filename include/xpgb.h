@@ -235,6 +235,12 @@ int xpgb_set_pinned(xpgb_ctx* ctx, const uint8_t* pinned_of);
  * compute event (the reference's WAR rule one window at a time), each window's GEMMs read only
  * its experts, and the layer's combine runs after its last window.  Re-creates the arena. */
 int xpgb_set_ring_experts(xpgb_ctx* ctx, int32_t ring_experts);
+/* Staging ring of the compressed host tier: n_buffers (2..16, default 2) buffers per kind of
+ * min(largest record, 64 MB).  A staged copy waits only for its buffer's previous decode, never
+ * for the arena's WAR event, so the link runs n_buffers-1 pieces ahead of the decoder -- across
+ * device-tier windows that need no link at all.  Counted in xpgb_hbm_bytes' staging.  No session
+ * may be active. */
+int xpgb_set_stage_buffers(xpgb_ctx* ctx, int32_t n_buffers);
 /* Shared experts (DeepSeek-V3 style; absent from the reference, our convention): n_shared
  * always-on experts per layer that every token passes through after its routed experts,
  * weight 1.0 (the routed sum keeps its f32(1/top_k) scale).  host = N*n_shared*(sigma1+sigma2)

@@ -64,5 +64,6 @@ void launch_exp_decode(const uint8_t* sm, const uint32_t* bits, const uint32_t* 
 void launch_exp_decode_multi(const DecodeTensor* tensors, int ntensors, uint64_t n, int chunk, const CodecTable& table,
                              cudaStream_t s);
 constexpr uint64_t kStagePieceBytes = 64ull << 20;  // max bytes of one staged record piece
+constexpr int kMaxStageBufs = 16;                   // staging buffers per kind (ring of pieces)
 
 }  // namespace xpgb

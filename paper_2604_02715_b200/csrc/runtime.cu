@@ -244,14 +244,20 @@ struct Ctx {
   std::vector<uint64_t> rec_off, rec_bits;  // [N*E*2]
   CodecTable ctab{};
   int cchunk = 1024;
-  uint8_t* stage[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [kind][buffer]
+  // staging ring per kind: n_stage buffers of stage_cap bytes.  Host-tier copies wait only
+  // for their buffer's previous decode (never for the ring's WAR), so the link runs up to
+  // n_stage - 1 pieces ahead of the decoder, across windows and layers.
+  uint8_t* stage[2][kMaxStageBufs] = {};  // [kind][buffer]
+  int n_stage = 2;
+  uint32_t stage_next[2] = {0, 0};
   uint32_t* d_index = nullptr;           // chunk indexes of host-tier records, device-resident
   std::vector<uint64_t> d_index_off;     // [N*E*2] offset (entries) into d_index
   uint64_t stage_cap[2] = {0, 0};
   cudaStream_t s_dec[2] = {nullptr, nullptr};
-  cudaStream_t s_alt[2] = {nullptr, nullptr};  // second copy stream per kind for staged pieces
+  cudaStream_t s_cp[2] = {nullptr, nullptr};   // staged host-tier copies (even buffers)
+  cudaStream_t s_alt[2] = {nullptr, nullptr};  // staged host-tier copies (odd buffers): hides turnaround
   cudaStream_t s_devdec[2] = {nullptr, nullptr};  // device-tier decodes: never queue behind the link
-  cudaEvent_t ev_copied[2][2], ev_decoded[2][2], ev_mapped[2], ev_raw[2], ev_devdec[2];
+  cudaEvent_t ev_copied[2][kMaxStageBufs], ev_decoded[2][kMaxStageBufs], ev_mapped[2], ev_raw[2], ev_devdec[2];
   bool codec_events = false;
 
   // profiling
@@ -781,9 +787,7 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
     CK(cudaEventRecord(c->ev_mapped[k], s));
     CK(cudaStreamWaitEvent(d, c->ev_mapped[k], 0));
     bool dev_on_dv = false;
-    if (c->host_codec) CK(cudaStreamWaitEvent(c->s_alt[k], c->ev_mapped[k], 0));
     bool raw_on_s = false;
-    int hb = 0;
     const uint64_t n = sigma_of(c, kind) / 2;
     const uint64_t sm16 = (n + 15) & ~15ull;
     auto tix = [&](int e) { return ((size_t)(layer - 1) * E + e) * 2 + k; };
@@ -832,9 +836,9 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
         const int lastx = e + cnt - 1;
         // the last record's trailing chunk index stays home (it is device-resident)
         const uint64_t bytes = c->rec_off[tix(lastx)] - base + sm16 + ((c->rec_bits[tix(lastx)] + 8 + 15) & ~15ull);
-        const int buf = hb++ & 1;
+        const int buf = (int)(c->stage_next[k]++ % (uint32_t)c->n_stage);
         uint8_t* st = c->stage[k][buf];
-        cudaStream_t cs = buf ? c->s_alt[k] : s;
+        cudaStream_t cs = (buf & 1) ? c->s_alt[k] : c->s_cp[k];
         CK(cudaStreamWaitEvent(cs, c->ev_decoded[k][buf], 0));
         CK(cudaMemcpyAsync(st, c->cpool + base, bytes, cudaMemcpyHostToDevice, cs));
         CK(cudaEventRecord(c->ev_copied[k][buf], cs));
@@ -880,11 +884,11 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
           const uint64_t ns = v1 - v0, nbits = b1 - b0 + 8;
           const uint64_t o_bits = (ns + 15) & ~15ull;
           if (o_bits + nbits > c->stage_cap[k]) XFAIL(XPGB_ERR, "codec piece exceeds staging buffer");
-          const int buf = hb++ & 1;
+          const int buf = (int)(c->stage_next[k]++ % (uint32_t)c->n_stage);
           uint8_t* st = c->stage[k][buf];
-          // buffer b is filled by its own copy stream, so one stream's wait/turnaround
-          // bubble hides behind the other's transfer
-          cudaStream_t cs = buf ? c->s_alt[k] : s;
+          // odd and even buffers fill from their own copy streams, so one stream's
+          // wait/turnaround bubble hides behind the other's transfer
+          cudaStream_t cs = (buf & 1) ? c->s_alt[k] : c->s_cp[k];
           CK(cudaStreamWaitEvent(cs, c->ev_decoded[k][buf], 0));
           CK(cudaMemcpyAsync(st, rec + v0, ns, cudaMemcpyHostToDevice, cs));
           CK(cudaMemcpyAsync(st + o_bits, rec + sm16 + b0, nbits, cudaMemcpyHostToDevice, cs));
@@ -1325,9 +1329,10 @@ static void set_codec(Ctx* c, const void* pool, uint64_t pool_bytes, const uint6
     for (int k = 0; k < 2; ++k) {
       CK(cudaStreamCreateWithFlags(&c->s_dec[k], cudaStreamNonBlocking));
       CK(cudaStreamCreateWithFlags(&c->s_alt[k], cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&c->s_cp[k], cudaStreamNonBlocking));
       CK(cudaStreamCreateWithFlags(&c->s_devdec[k], cudaStreamNonBlocking));
       CK(cudaEventCreateWithFlags(&c->ev_devdec[k], cudaEventDisableTiming));
-      for (int b = 0; b < 2; ++b) {
+      for (int b = 0; b < kMaxStageBufs; ++b) {
         CK(cudaEventCreateWithFlags(&c->ev_copied[k][b], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_decoded[k][b], cudaEventDisableTiming));
       }
@@ -1336,7 +1341,8 @@ static void set_codec(Ctx* c, const void* pool, uint64_t pool_bytes, const uint6
     }
     c->codec_events = true;
   }
-  // staging: two buffers per kind, each min(largest record, kStagePieceBytes) + alignment slack
+  // staging: n_stage buffers per kind, each min(largest record, kStagePieceBytes) + alignment slack
+  if (const char* env = getenv("XPGB_STAGE_BUFS")) c->n_stage = std::max(2, std::min(kMaxStageBufs, atoi(env)));
   for (int k = 0; k < 2; ++k) {
     uint64_t cap = 0;
     if (host_compressed) {
@@ -1356,10 +1362,10 @@ static void set_codec(Ctx* c, const void* pool, uint64_t pool_bytes, const uint6
       if (const char* env = getenv("XPGB_STAGE_BYTES")) piece = std::max<uint64_t>(4096, strtoull(env, nullptr, 10));
       cap = std::min(cap, piece) + 64 + (uint64_t)chunk * 8;
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kMaxStageBufs; ++b) {
       if (c->stage[k][b]) cudaFree(c->stage[k][b]);
       c->stage[k][b] = nullptr;
-      if (cap) CK(cudaMalloc(&c->stage[k][b], cap));
+      if (cap && b < c->n_stage) CK(cudaMalloc(&c->stage[k][b], cap));
     }
     c->stage_cap[k] = cap;
   }
@@ -1481,9 +1487,10 @@ int xpgb_destroy(xpgb_ctx* h) {
       for (int k = 0; k < 2; ++k) {
         cudaStreamDestroy(c->s_dec[k]);
         cudaStreamDestroy(c->s_alt[k]);
+        cudaStreamDestroy(c->s_cp[k]);
         cudaStreamDestroy(c->s_devdec[k]);
         cudaEventDestroy(c->ev_devdec[k]);
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < kMaxStageBufs; ++b) {
           cudaEventDestroy(c->ev_copied[k][b]);
           cudaEventDestroy(c->ev_decoded[k][b]);
           if (c->stage[k][b]) cudaFree(c->stage[k][b]);
@@ -1886,7 +1893,7 @@ int xpgb_hbm_bytes(xpgb_ctx* h, uint64_t* ring, uint64_t* staging, uint64_t* dev
     Ctx* c = &h->c;
     // resident expert bytes: the ring arena (+ pinned blocks) and the shared experts
     *ring = (uint64_t)c->blocks * (c->s1 + c->s2) + (uint64_t)c->N * c->S * (c->s1 + c->s2);
-    *staging = 2 * (c->stage_cap[0] + c->stage_cap[1]);
+    *staging = (uint64_t)c->n_stage * (c->stage_cap[0] + c->stage_cap[1]);
     if (c->d_index) {
       uint64_t entries = 0;
       const size_t nt = (size_t)c->N * c->E * 2;
@@ -1973,6 +1980,28 @@ int xpgb_set_ring_experts(xpgb_ctx* h, int32_t ring_experts) {
       XFAIL(XPGB_ERR_OUT_OF_RANGE, "ring of %d experts per kind: need >= 2 (or -1 for two layers)", ring_experts);
     c->ring_limit = ring_experts < 0 ? 0 : ring_experts;
     apply_residency(c, c->pinned);
+  });
+}
+
+int xpgb_set_stage_buffers(xpgb_ctx* h, int32_t n_buffers) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    if (c->sess && c->sess->active) XFAIL(XPGB_ERR, "cannot resize the staging ring during a session");
+    if (n_buffers < 2 || n_buffers > kMaxStageBufs)
+      XFAIL(XPGB_ERR_OUT_OF_RANGE, "%d staging buffers per kind: need 2..%d", n_buffers, kMaxStageBufs);
+    CK(cudaDeviceSynchronize());
+    for (int k = 0; k < 2; ++k) {
+      for (int b = 0; b < kMaxStageBufs; ++b) {
+        const bool want = b < n_buffers && c->stage_cap[k] > 0;
+        if (want && !c->stage[k][b]) CK(cudaMalloc(&c->stage[k][b], c->stage_cap[k]));
+        if (!want && c->stage[k][b]) {
+          CK(cudaFree(c->stage[k][b]));
+          c->stage[k][b] = nullptr;
+        }
+      }
+      c->stage_next[k] = 0;
+    }
+    c->n_stage = n_buffers;
   });
 }
 

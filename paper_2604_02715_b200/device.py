@@ -120,6 +120,10 @@ class Context:
         """Sub-layer ring of ``ring_experts`` blocks per kind (-1: the reference's two layers)."""
         call("xpgb_set_ring_experts", self._h, int(ring_experts))
 
+    def set_stage_buffers(self, n: int) -> None:
+        """Staging ring of the compressed host tier: ``n`` buffers per kind (link run-ahead)."""
+        call("xpgb_set_stage_buffers", self._h, int(n))
+
     def set_pinned(self, mask: np.ndarray) -> None:
         arr = np.ascontiguousarray(mask, dtype=np.uint8)
         call("xpgb_set_pinned", self._h, arr.ctypes.data_as(C.POINTER(C.c_uint8)))

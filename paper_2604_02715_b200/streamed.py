@@ -213,14 +213,16 @@ class StreamedRunner:
     def __init__(self, spec: ModelSpec, hierarchy: StorageHierarchy, fwd: ForwardSpec, mode: str = "threaded",
                  compute_delay_fn=None, sabotage_skip_raw=None, trace=None, device: int = 0,
                  host_codec: bool = False, pinned=None, expert_shard=None, shared_tokens=None,
-                 ring_experts=None):
+                 ring_experts=None, stage_buffers=None):
         """expert_shard=(first, count): this device holds only experts [first, first+count) of
         every layer -- one expert-parallel rank's slice -- and ``hierarchy`` is built on that
         shard's container (ModelSpec(N, count, H, F), shard-local order); the router still
         spans all L experts and rows routed elsewhere are skipped.  shared_tokens=(first,
         count): the step rows that pass through the shared experts (default all).
         ring_experts: a sub-layer ring of that many expert blocks per kind (budgets below the
-        reference's two layers; each layer then streams in windows of ring_experts/2)."""
+        reference's two layers; each layer then streams in windows of ring_experts/2).
+        stage_buffers: staging buffers per kind for the compressed host tier (2..16): how far
+        the link runs ahead of the decoder."""
         if mode not in ("threaded", "sequential"):
             raise XpgError(f"unknown mode {mode!r}")
         self.spec = spec
@@ -245,6 +247,8 @@ class StreamedRunner:
             # host_codec the host tier also ships compressed records over PCIe.  Both are
             # decoded on the GPU straight into the ring block.
             self.ctx.set_codec(cm, host_compressed=host_codec)
+        if stage_buffers is not None:
+            self.ctx.set_stage_buffers(int(stage_buffers))
         self.ctx.set_placement(placement)
         if ring_experts is not None:
             self.ctx.set_ring_experts(int(ring_experts))
