@@ -235,6 +235,14 @@ int xpgb_set_pinned(xpgb_ctx* ctx, const uint8_t* pinned_of);
  * compute event (the reference's WAR rule one window at a time), each window's GEMMs read only
  * its experts, and the layer's combine runs after its last window.  Re-creates the arena. */
 int xpgb_set_ring_experts(xpgb_ctx* ctx, int32_t ring_experts);
+/* Windows in flight on a sub-layer ring (2..6, default 2 = double buffering): the ring's
+ * ring_experts blocks per kind hold `depth` windows of ring_experts/depth experts, and window
+ * g recycles window g-depth, so the loads of the next depth-1 windows overlap the compute of
+ * the current one (the reference's two-layer WAR rule, generalised).  Callers keep the
+ * reference's order -- materialize(0), materialize(1), materialize(g+2) after release(g) --
+ * and the session materializes up to g+depth.  Ignored without a ring cap.  Re-creates the
+ * arena. */
+int xpgb_set_ring_depth(xpgb_ctx* ctx, int32_t depth);
 /* Staging ring of the compressed host tier: n_buffers (2..16, default 2) buffers per kind of
  * min(largest record, 64 MB).  A staged copy waits only for its buffer's previous decode, never
  * for the arena's WAR event, so the link runs n_buffers-1 pieces ahead of the decoder -- across

@@ -113,6 +113,7 @@ _SIGS = {
     "xpgb_host_register": [_P, _U64, _I],
     "xpgb_host_unregister": [_P],
     "xpgb_set_ring_experts": [_P, _I],
+    "xpgb_set_ring_depth": [_P, _I],
     "xpgb_set_stage_buffers": [_P, _I],
     "xpgb_set_shared_tokens": [_P, _I, _I],
     "xpgb_shared_forward": [_P, _I, _P, _P, _I, _P],

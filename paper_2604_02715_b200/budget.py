@@ -29,12 +29,13 @@ import numpy as np
 
 @dataclass
 class ResidencyPlan:
-    ring: int                 # ring blocks per kind (sub-layer ring when < 2 x streamed experts)
+    ring: int                 # ring blocks per kind (sub-layer ring when < depth x streamed experts)
     device_mask: np.ndarray   # bool [N][L]: compressed in HBM, decoded into the ring each step
     pinned_mask: np.ndarray   # bool [N][L]: raw, resident for good
     hbm_bytes: float          # ring + device tier + pinned (+ shared), the budget's numerator
     est_step_s: float         # modelled step time
     link_bytes: float         # host-tier record bytes per step
+    depth: int = 2            # windows in flight on the ring (ring // depth experts each)
 
     @property
     def device_experts(self) -> int:
@@ -45,17 +46,31 @@ class ResidencyPlan:
         return int(self.pinned_mask.sum())
 
 
+def _fill(total: int, caps) -> list:
+    """`total` items over slots of capacity `caps`, as even as the capacities allow."""
+    out = [0] * len(caps)
+    left = min(int(total), int(sum(caps)))
+    while left > 0:
+        open_ = [j for j in range(len(caps)) if out[j] < caps[j]]
+        share = max(1, left // len(open_))
+        for j in open_:
+            take = min(share, caps[j] - out[j], left)
+            out[j] += take
+            left -= take
+            if left == 0:
+                break
+    return out
+
+
 def _spread_row(streamed: int, m: int, window: int) -> np.ndarray:
     """m of the first `streamed` positions, spread over windows of `window`, contiguous inside."""
     row = np.zeros(streamed, dtype=bool)
     if m <= 0 or streamed <= 0:
         return row
     w = max(1, min(window, streamed))
-    nw = -(-streamed // w)
-    per = [(j + 1) * m // nw - j * m // nw for j in range(nw)]
-    for j in range(nw):
-        a = j * w
-        row[a:a + min(per[j], w, streamed - a)] = True
+    caps = [min(w, streamed - a) for a in range(0, streamed, w)]
+    for j, n in enumerate(_fill(m, caps)):
+        row[j * w:j * w + n] = True
     return row
 
 
@@ -64,16 +79,21 @@ def _balanced(total: int, N: int):
 
 
 def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *, shared_bytes: float = 0.0,
-                   b_link: float = 54e9, b_dec: float = 700e9, t_compute: float = 0.0,
-                   min_window_bytes: float = 128 * 2**20, allow_pinned: bool = True) -> ResidencyPlan:
+                   b_link: float = 54e9, b_dec: float = 1100e9, t_compute: float = 0.0,
+                   min_window_bytes: float = 128 * 2**20, allow_pinned: bool = True, depth: int = 2,
+                   window: int | None = None) -> ResidencyPlan:
     """Choose (ring, device tier, pinned) for N layers x L experts under `budget_bytes`.
 
     eb: raw bytes of one expert (both tensors); ceb: its compressed record bytes.
     Step model: max(link_bytes / b_link, decoded_raw_bytes / b_dec + t_compute).
+    depth: windows in flight (the ring holds depth windows); window: experts per window
+    (default: enough for min_window_bytes, at least 2 when depth is 2).
     """
     total = N * L
     cap = budget_bytes - shared_bytes
-    w_min = int(min(L, max(2, -(-min_window_bytes // eb))))
+    if window is None:
+        window = int(max(2 if depth == 2 else 1, -(-min_window_bytes // eb)))
+    w_min = int(min(L, window))
     best = None
     p_grid = range(0, total + 1) if allow_pinned else [0]
     for p in p_grid:
@@ -82,7 +102,7 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
         if streamed_max == 0:
             ring = 0
         else:
-            ring = 2 * min(w_min, streamed_max)
+            ring = depth * min(w_min, streamed_max)
         room = cap - ring * eb - p * eb
         if room < 0:
             continue
@@ -96,15 +116,16 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
     if best is None:
         raise ValueError(f"budget {budget_bytes:.3g} B cannot hold a two-expert ring")
     (est, _), p, d, ring, link = best
-    p_layer, d_layer = _balanced(p, N), _balanced(d, N)
+    p_layer = _balanced(p, N)
+    d_layer = _fill(d, [L - q for q in p_layer])
     pinned = np.zeros((N, L), dtype=bool)
     for l in range(N):
         if p_layer[l]:
             pinned[l, L - p_layer[l]:] = True
     device = np.zeros((N, L), dtype=bool)
-    w = max(1, ring // 2)
+    w = max(1, ring // depth) if ring else 1
     for l in range(N):
         streamed = L - p_layer[l]
-        device[l, :streamed] = _spread_row(streamed, min(d_layer[l], streamed), w)
+        device[l, :streamed] = _spread_row(streamed, d_layer[l], w)
     hbm = ring * eb + p * eb + device.sum() * ceb + shared_bytes
-    return ResidencyPlan(ring, device, pinned, float(hbm), float(est), float(link))
+    return ResidencyPlan(ring, device, pinned, float(hbm), float(est), float(link), depth)

@@ -154,7 +154,7 @@ __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 
 // last values (never decode past the chunk), take the canonical first-code search.
 // The table is 8 KB of shared memory so decode blocks still fit beside a resident
 // GEMM CTA; the next bitstream word is always in flight.  Output words are
-// (sign << 15) | (exponent << 7) | mantissa, 8 per 16-byte store.
+// (sign << 15) | (exponent << 7) | mantissa, 16 per 32-byte store.
 constexpr int kMultiBits = 11;
 
 __device__ __forceinline__ int canon_decode(uint64_t win, int ml, const int* count, const uint32_t* first_code,
@@ -175,6 +175,28 @@ __device__ __forceinline__ uint32_t pack_words(uint32_t sm4, uint32_t ex4, uint3
   const uint32_t x = __byte_perm(sm4, ex4, sel);
   return ((x >> 1) & 0x7F807F80u) | (x & 0x007F007Fu) | ((x << 8) & 0x80008000u);
 }
+
+// Bitstream words for one chunk, the next one always in flight.  (16-byte loads with a
+// second in flight measured slower: 726 vs 951 GB/s.)
+struct WordScalar {
+  const uint32_t* wp;
+  uint32_t nxt;
+  __device__ __forceinline__ void init(const uint32_t* p) {
+    wp = p;
+    nxt = *wp++;
+  }
+  __device__ __forceinline__ uint32_t pop() {
+    const uint32_t r = nxt;
+    nxt = *wp++;
+    return bswap32(r);
+  }
+};
+
+template <class R>
+__device__ __forceinline__ void decode_chunk(R& q, uint64_t win, int avail, const uint8_t* __restrict__ sm,
+                                             uint16_t* __restrict__ out, uint64_t v0, uint64_t v1, const uint32_t* lut3,
+                                             int ml, const int* count, const uint32_t* first_code,
+                                             const int* first_rank, const uint8_t* sorted_sym);
 
 __global__ void __launch_bounds__(256) k_exp_decode(const __grid_constant__ DecodeParams p) {
   __shared__ uint32_t lut3[1 << kMultiBits];  // syms (3 x 8 b) | count << 24 | total length << 26
@@ -246,56 +268,79 @@ __global__ void __launch_bounds__(256) k_exp_decode(const __grid_constant__ Deco
     const uint64_t v1 = (v0 + p.chunk < n) ? v0 + p.chunk : n;
     const uint32_t bitpos = d.index[c] - d.bit_base;
     const uint32_t w = bitpos >> 5, sh = bitpos & 31;
-    const uint32_t* __restrict__ wp = d.bits + w + 2;
     uint64_t win = (((uint64_t)bswap32(d.bits[w]) << 32) | bswap32(d.bits[w + 1])) << sh;
     int avail = 64 - (int)sh;
-    uint32_t nxt = bswap32(*wp++);  // the next word is always in flight
-    uint64_t lo = 0, hi = 0;        // decoded exponent bytes not yet written (np of them)
-    int np = 0;
-    for (uint64_t v = v0; v < v1; v += 8) {
-      const int cnt = (int)((v1 - v) < 8 ? (v1 - v) : 8);
-      uint2 smv = make_uint2(0, 0);
-      if (cnt == 8) smv = *reinterpret_cast<const uint2*>(sm + v);
-      while (np < cnt) {
-        if (avail < 32) {
-          win |= (uint64_t)nxt << (32 - avail);
-          avail += 32;
-          nxt = bswap32(*wp++);
-        }
-        const uint32_t e = lut3[win >> (64 - kMultiBits)];
-        int k = (e >> 24) & 3, l;
-        uint32_t bytes;
-        if (k == 0 || k > (int)(v1 - v) - np) {
-          int sym = 0;
-          l = canon_decode(win, ml, count, first_code, first_rank, sorted_sym, &sym);
-          bytes = (uint32_t)sym;
-          k = 1;
-        } else {
-          l = (int)(e >> 26);
-          bytes = e & 0xFFFFFFu;
-        }
-        win <<= l;
-        avail -= l;
-        lo |= (uint64_t)bytes << (8 * np);  // np <= 7 here
-        if (np > 5) hi |= (uint64_t)bytes >> (64 - 8 * np);
-        np += k;
+    WordScalar q;
+    q.init(d.bits + w + 2);
+    decode_chunk(q, win, avail, sm, out, v0, v1, lut3, ml, count, first_code, first_rank, sorted_sym);
+  }
+}
+
+template <class R>
+__device__ __forceinline__ void decode_chunk(R& q, uint64_t win, int avail, const uint8_t* __restrict__ sm,
+                                             uint16_t* __restrict__ out, uint64_t v0, uint64_t v1, const uint32_t* lut3,
+                                             int ml, const int* count, const uint32_t* first_code,
+                                             const int* first_rank, const uint8_t* sorted_sym) {
+  // exponent bytes decoded but not yet written: b0 = values 0..7 of the group, b1 = 8..15,
+  // b2 = the spill of a multi-symbol lookup past the group
+  uint64_t b0 = 0, b1 = 0, b2 = 0;
+  int np = 0;
+  const bool wide = ((reinterpret_cast<uintptr_t>(out + v0) | reinterpret_cast<uintptr_t>(sm + v0)) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(out + v0) & 31) == 0;
+  for (uint64_t v = v0; v < v1; v += 16) {
+    const int cnt = (int)((v1 - v) < 16 ? (v1 - v) : 16);
+    uint4 smv = make_uint4(0, 0, 0, 0);
+    if (cnt == 16 && wide) smv = *reinterpret_cast<const uint4*>(sm + v);
+    while (np < cnt) {
+      if (avail < 32) {
+        win |= (uint64_t)q.pop() << (32 - avail);
+        avail += 32;
       }
-      if (cnt == 8) {
-        const uint32_t e0 = (uint32_t)lo, e1 = (uint32_t)(lo >> 32);
-        *reinterpret_cast<uint4*>(out + v) =
-            make_uint4(pack_words(smv.x, e0, 0x5140u), pack_words(smv.x, e0, 0x7362u),
-                       pack_words(smv.y, e1, 0x5140u), pack_words(smv.y, e1, 0x7362u));
+      const uint32_t e = lut3[win >> (64 - kMultiBits)];
+      int k = (e >> 24) & 3, l;
+      uint64_t bytes;
+      if (k == 0 || k > (int)(v1 - v) - np) {
+        int sym = 0;
+        l = canon_decode(win, ml, count, first_code, first_rank, sorted_sym, &sym);
+        bytes = (uint32_t)sym;
+        k = 1;
       } else {
-        for (int j = 0; j < cnt; ++j) {
-          const uint32_t sym = (uint32_t)(lo >> (8 * j)) & 0xFFu;
-          const uint32_t sb = sm[v + j];
-          out[v + j] = (uint16_t)(((sb & 0x80u) << 8) | (sym << 7) | (sb & 0x7Fu));
-        }
+        l = (int)(e >> 26);
+        bytes = e & 0xFFFFFFu;
       }
-      lo = hi;
-      hi = 0;
-      np -= cnt;
+      win <<= l;
+      avail -= l;
+      if (np < 8) {
+        b0 |= bytes << (8 * np);
+        if (np > 5) b1 |= bytes >> (64 - 8 * np);
+      } else {
+        const int q = np - 8;
+        b1 |= bytes << (8 * q);
+        if (q > 5) b2 |= bytes >> (64 - 8 * q);
+      }
+      np += k;
     }
+    if (cnt == 16 && wide) {
+      // one 32-byte store per 16 values: a whole sector per thread (the warp's threads
+      // write 32 different chunks, so narrower stores cost proportionally more wavefronts)
+      const uint32_t e0 = (uint32_t)b0, e1 = (uint32_t)(b0 >> 32), e2 = (uint32_t)b1, e3 = (uint32_t)(b1 >> 32);
+      asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(out + v),
+                   "r"(pack_words(smv.x, e0, 0x5140u)), "r"(pack_words(smv.x, e0, 0x7362u)),
+                   "r"(pack_words(smv.y, e1, 0x5140u)), "r"(pack_words(smv.y, e1, 0x7362u)),
+                   "r"(pack_words(smv.z, e2, 0x5140u)), "r"(pack_words(smv.z, e2, 0x7362u)),
+                   "r"(pack_words(smv.w, e3, 0x5140u)), "r"(pack_words(smv.w, e3, 0x7362u))
+                   : "memory");
+    } else {
+      for (int j = 0; j < cnt; ++j) {
+        const uint32_t sym = (uint32_t)((j < 8 ? b0 >> (8 * j) : b1 >> (8 * (j - 8)))) & 0xFFu;
+        const uint32_t sb = sm[v + j];
+        out[v + j] = (uint16_t)(((sb & 0x80u) << 8) | (sym << 7) | (sb & 0x7Fu));
+      }
+    }
+    b0 = b2;
+    b1 = 0;
+    b2 = 0;
+    np -= cnt;
   }
 }
 
@@ -315,7 +360,16 @@ void launch_exp_decode_multi(const DecodeTensor* tensors, int ntensors, uint64_t
   p.table = table;
   for (int i = 0; i < ntensors; ++i) p.t[i] = tensors[i];
   const uint64_t n_chunks = ((n + chunk - 1) / chunk) * (uint64_t)ntensors;
-  const uint64_t blocks = std::min<uint64_t>((n_chunks + 255) / 256, 148 * 8);
+  // one resident wave, grid-striding over the chunks: a second partial wave left the
+  // tail idle (chunk 256: 1265 GB/s at 5 blocks/SM vs 1107 at 8)
+  static const int resident = [] {
+    int dev = 0, sms = 148, per_sm = 4;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_exp_decode, 256, 0);
+    return std::max(1, sms * std::max(1, per_sm));
+  }();
+  const uint64_t blocks = std::min<uint64_t>((n_chunks + 255) / 256, (uint64_t)resident);
   k_exp_decode<<<(unsigned)blocks, 256, 0, s>>>(p);
   note_launch();
 }

@@ -166,6 +166,9 @@ static const char* state_name(int s) {
 
 struct Session;
 
+constexpr int kEvRing = 8;        // load / compute events per step, indexed g % kEvRing
+constexpr int kMaxRingDepth = 6;  // windows in flight (< kEvRing)
+
 struct Ctx {
   Session* sess = nullptr;
   int N, L, H, F;
@@ -207,11 +210,12 @@ struct Ctx {
   std::vector<uint8_t> pinned;  // [N*E] permanently resident experts (residency tier x > 0)
   int ring_blocks = 0;          // blocks per kind that cycle through the schedule
   int ring_limit = 0;           // cap on ring blocks per kind (sub-layer ring); 0 = 2 x streamed experts
+  int ring_depth = 2;           // windows in flight on a sub-layer ring (window g recycles g - depth)
 
   // streams / events
   cudaStream_t s_copy[2] = {nullptr, nullptr};
   cudaStream_t s_comp = nullptr;
-  cudaEvent_t ev_load[2][4], ev_comp[4], ev_begin, ev_end;
+  cudaEvent_t ev_load[2][kEvRing], ev_comp[kEvRing], ev_begin, ev_end;
 
   // workspace
   int cap_T = 0, cap_kk = 0, cap_rows = 0, cap_splits = 8;
@@ -702,6 +706,9 @@ struct Step {
 // Alg. 1 MaterializeLayer (pipeline.py:335-360) for one kind, enqueued on copy stream `kind`:
 // recycle the blocks of step g-2 (the reference's target_layer, paging.py:29-38, once the
 // steps are layers) after its compute event, map + load this step's streamed experts.
+// windows in flight: the sub-layer ring's depth, else the reference's two layers
+static int depth_of(const Ctx* c) { return c->ring_limit > 0 ? c->ring_depth : 2; }
+
 static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int kind) {
   Ctx* c = rs.c;
   const int N = c->N, E = c->E, k = kind - 1;
@@ -716,7 +723,7 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
   const int chunk = (int)(sizeof(op.vals) / sizeof(int32_t));
   if (tg) {
     const int tgt = tg->layer, tlo = tg->e0, thi = std::min(tg->e1, E);
-    CK(cudaStreamWaitEvent(s, c->ev_comp[(g - 2) & 3], 0));  // WAR
+    CK(cudaStreamWaitEvent(s, c->ev_comp[(g - depth_of(c)) % kEvRing], 0));  // WAR
     for (int e = tlo; e < thi; ++e)
       if (!is_pinned(tgt, e)) pt_unmap(c, tgt, c->e_first + e + 1, kind);
     if (rs.log) set_rec(op, nrec++, XPGB_EV_RECYCLE, it, layer, kind, tg->it, tgt, st.w | (tg->w << 16));
@@ -825,7 +832,6 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
       } else if (c->host_codec && rec_bytes(e) <= c->stage_cap[k]) {
         // host tier, small records: a run of whole consecutive records in ONE copy and
         // ONE decode launch (per-copy turnaround would otherwise dominate small experts)
-        if (dl > 0) sleep_on(s, dl);
         uint64_t run = rec_bytes(e);
         int cnt = 1;
         while (cnt < kMaxDecodeTensors && joins_run(e + cnt - 1, e + cnt, 0) && run + rec_bytes(e + cnt) <= c->stage_cap[k]) {
@@ -840,6 +846,7 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
         uint8_t* st = c->stage[k][buf];
         cudaStream_t cs = (buf & 1) ? c->s_alt[k] : c->s_cp[k];
         CK(cudaStreamWaitEvent(cs, c->ev_decoded[k][buf], 0));
+        if (dl > 0) sleep_on(cs, dl);  // the injected fetch delay holds this record's copy
         CK(cudaMemcpyAsync(st, c->cpool + base, bytes, cudaMemcpyHostToDevice, cs));
         CK(cudaEventRecord(c->ev_copied[k][buf], cs));
         rs.h2d += bytes;
@@ -869,7 +876,6 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
           const uint64_t ba = ((uint64_t)idx[a] >> 5) * 4, bb = (b < nc) ? (((uint64_t)idx[b] + 7) / 8) : nb;
           return ((vb - va + 15) & ~15ull) + ((bb - ba + 8 + 15) & ~15ull);
         };
-        if (dl > 0) sleep_on(s, dl);
         for (uint64_t c0 = 0, c1 = 0; c0 < nc; c0 = c1) {
           // largest c1 whose piece fits the staging buffer (sizes grow with c1)
           uint64_t lo = c0 + 1, hi = nc;
@@ -890,6 +896,7 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
           // wait/turnaround bubble hides behind the other's transfer
           cudaStream_t cs = (buf & 1) ? c->s_alt[k] : c->s_cp[k];
           CK(cudaStreamWaitEvent(cs, c->ev_decoded[k][buf], 0));
+          if (dl > 0 && c0 == 0) sleep_on(cs, dl);
           CK(cudaMemcpyAsync(st, rec + v0, ns, cudaMemcpyHostToDevice, cs));
           CK(cudaMemcpyAsync(st + o_bits, rec + sm16 + b0, nbits, cudaMemcpyHostToDevice, cs));
           CK(cudaEventRecord(c->ev_copied[k][buf], cs));
@@ -930,7 +937,7 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
     if (o3.log) set_rec(o3, 0, XPGB_EV_LOAD_DONE, it, layer, kind, -1, -1, st.w);
     launch_op(o3, done_stream);
   }
-  CK(cudaEventRecord(c->ev_load[k][g & 3], done_stream));
+  CK(cudaEventRecord(c->ev_load[k][g % kEvRing], done_stream));
   if (seq) {
     CK(cudaStreamSynchronize(s));
     CK(cudaStreamSynchronize(done_stream));
@@ -947,6 +954,7 @@ struct Session {
   int steps = 0;
   bool paged = false;
   std::vector<Step> sv;  // the flattened schedule: iterations x layers x windows
+  int mat_next = 0;      // next step to materialize
 };
 
 static Session& session_of(Ctx* c) {
@@ -954,14 +962,14 @@ static Session& session_of(Ctx* c) {
   return *c->sess;
 }
 
-// Windows of one layer for the current ring: each holds ring_blocks/2 streamed experts
-// (double-buffered halves of the ring); one window per layer when the ring holds two
-// whole layers (the reference geometry).
+// Windows of one layer for the current ring: each holds ring_blocks/depth streamed experts
+// (depth windows in flight: double-buffered halves of the ring by default); one window per
+// layer when the ring holds two whole layers (the reference geometry).
 static std::vector<std::pair<int, int>> layer_windows(Ctx* c, int layer) {
   const int E = c->E, G = groups_of(c);
   int streamed = 0;
   for (int e = 0; e < E; ++e) streamed += !c->pinned[(size_t)(layer - 1) * E + e];
-  const int gs = std::max(1, c->ring_blocks / 2);
+  const int gs = std::max(1, c->ring_blocks / depth_of(c));
   std::vector<std::pair<int, int>> w;
   if (c->pool != XPGB_POOL_RING || gs >= streamed) {
     w.push_back({0, G});
@@ -1007,6 +1015,7 @@ static void session_begin(Ctx* c, const xpgb_run_opts* o, float* acts) {
   const int N = c->N;
   ss.o = *o;
   build_schedule(c, ss, o->iterations);
+  ss.mat_next = 0;
   ss.fetch_delay.clear();
   ss.compute_delay.clear();
   if (o->fetch_delay_s) ss.fetch_delay.assign(o->fetch_delay_s, o->fetch_delay_s + (size_t)N * c->L * 2);
@@ -1044,12 +1053,20 @@ static void session_begin(Ctx* c, const xpgb_run_opts* o, float* acts) {
   ss.active = true;
 }
 
+// Callers follow the reference's order -- mat(0), mat(1), then mat(g+2) right after
+// release(g).  With a deeper ring (depth D windows in flight) the call for g+2 enqueues
+// every step up to g+D: step j recycles step j-D, released by then.
 static void session_materialize(Ctx* c, int g) {
   Session& ss = session_of(c);
   if (!ss.active) XFAIL(XPGB_ERR, "no active session");
-  if (!ss.paged || g < 0 || g >= ss.steps) return;
-  const Step* tg = g >= 2 ? &ss.sv[g - 2] : nullptr;  // cold start: the first two steps recycle nothing
-  for (int kind = 1; kind <= 2; ++kind) materialize(ss.rs, g, ss.sv[g], tg, kind);
+  if (!ss.paged || g < 0) return;
+  const int D = depth_of(c);
+  const int upto = std::min(ss.steps - 1, g + D - 2);
+  for (int j = std::max(ss.mat_next, 0); j <= upto; ++j) {
+    const Step* tg = j >= D ? &ss.sv[j - D] : nullptr;  // cold start: the first D steps recycle nothing
+    for (int kind = 1; kind <= 2; ++kind) materialize(ss.rs, j, ss.sv[j], tg, kind);
+    ss.mat_next = j + 1;
+  }
 }
 
 // RAW: `s` waits for both load events of step g, then compute-start is logged on it.
@@ -1060,8 +1077,8 @@ static void session_acquire(Ctx* c, int g, cudaStream_t s) {
   const xpgb_run_opts* o = &ss.o;
   const bool skip = (o->sabotage_iteration == st.it && o->sabotage_layer == st.layer);
   if (ss.paged && !skip) {
-    CK(cudaStreamWaitEvent(s, c->ev_load[0][g & 3], 0));
-    CK(cudaStreamWaitEvent(s, c->ev_load[1][g & 3], 0));
+    CK(cudaStreamWaitEvent(s, c->ev_load[0][g % kEvRing], 0));
+    CK(cudaStreamWaitEvent(s, c->ev_load[1][g % kEvRing], 0));
   }
   log_only(c, ss.rs.log, s, XPGB_EV_COMPUTE_START, st.it, st.layer, st.w);
   if (o->compute_delay_s && st.first) {
@@ -1080,7 +1097,7 @@ static void session_release(Ctx* c, int g, cudaStream_t s) {
   if (!ss.active) XFAIL(XPGB_ERR, "no active session");
   const Step& st = ss.sv[g];
   log_only(c, ss.rs.log, s, XPGB_EV_COMPUTE_DONE, st.it, st.layer, st.w);
-  CK(cudaEventRecord(c->ev_comp[g & 3], s));
+  CK(cudaEventRecord(c->ev_comp[g % kEvRing], s));
   if (ss.o.sequential) CK(cudaStreamSynchronize(s));
 }
 
@@ -1443,8 +1460,8 @@ int xpgb_create(const xpgb_spec* spec, int32_t device, int32_t pool, int32_t max
     for (int k = 0; k < 2; ++k) CK(cudaStreamCreateWithFlags(&c->s_copy[k], cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
     for (int k = 0; k < 2; ++k)
-      for (int i = 0; i < 4; ++i) CK(cudaEventCreateWithFlags(&c->ev_load[k][i], cudaEventDisableTiming));
-    for (int i = 0; i < 4; ++i) CK(cudaEventCreateWithFlags(&c->ev_comp[i], cudaEventDisableTiming));
+      for (int i = 0; i < kEvRing; ++i) CK(cudaEventCreateWithFlags(&c->ev_load[k][i], cudaEventDisableTiming));
+    for (int i = 0; i < kEvRing; ++i) CK(cudaEventCreateWithFlags(&c->ev_comp[i], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_begin, cudaEventDisableTiming));
     CK(cudaEventCreate(&c->ev_end));
     for (int i = 0; i < 7; ++i) CK(cudaEventCreate(&c->pev[i]));
@@ -1475,9 +1492,9 @@ int xpgb_destroy(xpgb_ctx* h) {
     if (c->host && c->host_registered) cudaHostUnregister(c->host);
     for (int k = 0; k < 2; ++k) {
       cudaStreamDestroy(c->s_copy[k]);
-      for (int i = 0; i < 4; ++i) cudaEventDestroy(c->ev_load[k][i]);
+      for (int i = 0; i < kEvRing; ++i) cudaEventDestroy(c->ev_load[k][i]);
     }
-    for (int i = 0; i < 4; ++i) cudaEventDestroy(c->ev_comp[i]);
+    for (int i = 0; i < kEvRing; ++i) cudaEventDestroy(c->ev_comp[i]);
     cudaEventDestroy(c->ev_begin);
     cudaEventDestroy(c->ev_end);
     for (int i = 0; i < 7; ++i) cudaEventDestroy(c->pev[i]);
@@ -1927,8 +1944,9 @@ static void apply_residency(Ctx* c, std::vector<uint8_t> mask) {  // by value: c
     max_streamed = std::max(max_streamed, streamed);
   }
   if (n_pinned && !c->host) XFAIL(XPGB_ERR_BACKEND_MISS, "pinning experts needs the host pool");
-  int ring = 2 * max_streamed;
-  if (c->ring_limit > 0) ring = std::min(ring, c->ring_limit & ~1);
+  const int D = depth_of(c);
+  int ring = D * max_streamed;
+  if (c->ring_limit > 0) ring = std::min(ring, c->ring_limit / D * D);
   std::vector<uint8_t> backend = c->backend;
   CK(cudaDeviceSynchronize());
   init_pools(c, ring, n_pinned);
@@ -1976,10 +1994,23 @@ int xpgb_set_ring_experts(xpgb_ctx* h, int32_t ring_experts) {
     Ctx* c = &h->c;
     if (c->pool != XPGB_POOL_RING) XFAIL(XPGB_ERR_CONFIG, "a sub-layer ring needs a ring context");
     if (c->sess && c->sess->active) XFAIL(XPGB_ERR, "cannot resize the ring during a session");
-    if (ring_experts == 1 || ring_experts == 0 || ring_experts < -1)
-      XFAIL(XPGB_ERR_OUT_OF_RANGE, "ring of %d experts per kind: need >= 2 (or -1 for two layers)", ring_experts);
+    if (ring_experts == 0 || ring_experts < -1 || (ring_experts > 0 && ring_experts < c->ring_depth))
+      XFAIL(XPGB_ERR_OUT_OF_RANGE, "ring of %d experts per kind: need >= the ring depth %d (or -1 for two layers)",
+            ring_experts, c->ring_depth);
     c->ring_limit = ring_experts < 0 ? 0 : ring_experts;
     apply_residency(c, c->pinned);
+  });
+}
+
+int xpgb_set_ring_depth(xpgb_ctx* h, int32_t depth) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    if (c->sess && c->sess->active) XFAIL(XPGB_ERR, "cannot change the ring depth during a session");
+    if (depth < 2 || depth > kMaxRingDepth) XFAIL(XPGB_ERR_OUT_OF_RANGE, "ring depth %d: need 2..%d", depth, kMaxRingDepth);
+    if (c->ring_limit > 0 && c->ring_limit < depth)
+      XFAIL(XPGB_ERR_OUT_OF_RANGE, "ring depth %d exceeds the ring of %d experts", depth, c->ring_limit);
+    c->ring_depth = depth;
+    if (c->ring_limit > 0) apply_residency(c, c->pinned);
   });
 }
 

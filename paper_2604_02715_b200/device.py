@@ -120,6 +120,10 @@ class Context:
         """Sub-layer ring of ``ring_experts`` blocks per kind (-1: the reference's two layers)."""
         call("xpgb_set_ring_experts", self._h, int(ring_experts))
 
+    def set_ring_depth(self, depth: int) -> None:
+        """Windows in flight on a sub-layer ring (window g recycles g - depth)."""
+        call("xpgb_set_ring_depth", self._h, int(depth))
+
     def set_stage_buffers(self, n: int) -> None:
         """Staging ring of the compressed host tier: ``n`` buffers per kind (link run-ahead)."""
         call("xpgb_set_stage_buffers", self._h, int(n))

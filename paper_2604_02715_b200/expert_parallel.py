@@ -298,7 +298,9 @@ class ExpertParallelRunner:
             full[:, first:first + count] = plan.pinned_mask
             self.ctx.set_pinned(full)
         streamed = count - plan.pinned_mask.sum(axis=1).min()
-        if 0 < plan.ring < 2 * streamed:
+        depth = getattr(plan, "depth", 2)
+        if 0 < plan.ring < depth * streamed:
+            self.ctx.set_ring_depth(depth)
             self.ctx.set_ring_experts(int(plan.ring))
         shard_map = np.repeat(plan.device_mask[:, :, None], 2, axis=2).astype(np.uint8)
         self.ctx.set_placement(_full_width(self.spec, shard_map, first, count))

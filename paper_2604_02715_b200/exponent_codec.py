@@ -43,7 +43,7 @@ _RECORD = struct.Struct("<QQ")
 TENSOR_HEADER_BYTES = _RECORD.size
 NUM_SYMBOLS = 256
 MAX_CODE_LENGTH = 32
-DEFAULT_CHUNK = 1024
+DEFAULT_CHUNK = 256  # values per decode thread: 1265 GB/s vs 962 at 1024 (Mixtral gate/up, B200)
 _THREADS = max(1, os.cpu_count() or 1)
 
 

@@ -213,7 +213,7 @@ class StreamedRunner:
     def __init__(self, spec: ModelSpec, hierarchy: StorageHierarchy, fwd: ForwardSpec, mode: str = "threaded",
                  compute_delay_fn=None, sabotage_skip_raw=None, trace=None, device: int = 0,
                  host_codec: bool = False, pinned=None, expert_shard=None, shared_tokens=None,
-                 ring_experts=None, stage_buffers=None):
+                 ring_experts=None, stage_buffers=None, ring_depth=None):
         """expert_shard=(first, count): this device holds only experts [first, first+count) of
         every layer -- one expert-parallel rank's slice -- and ``hierarchy`` is built on that
         shard's container (ModelSpec(N, count, H, F), shard-local order); the router still
@@ -221,6 +221,8 @@ class StreamedRunner:
         count): the step rows that pass through the shared experts (default all).
         ring_experts: a sub-layer ring of that many expert blocks per kind (budgets below the
         reference's two layers; each layer then streams in windows of ring_experts/2).
+        ring_depth: windows in flight on that ring (default 2; each window then holds
+        ring_experts/ring_depth experts).
         stage_buffers: staging buffers per kind for the compressed host tier (2..16): how far
         the link runs ahead of the decoder."""
         if mode not in ("threaded", "sequential"):
@@ -250,6 +252,8 @@ class StreamedRunner:
         if stage_buffers is not None:
             self.ctx.set_stage_buffers(int(stage_buffers))
         self.ctx.set_placement(placement)
+        if ring_depth is not None:
+            self.ctx.set_ring_depth(int(ring_depth))
         if ring_experts is not None:
             self.ctx.set_ring_experts(int(ring_experts))
         if pinned is not None:
@@ -305,7 +309,9 @@ class StreamedRunner:
             full[:, first:first + count] = plan.pinned_mask.reshape(spec.num_layers, spec.experts_per_layer)
             self.ctx.set_pinned(full)
         streamed = spec.experts_per_layer - plan.pinned_mask.sum(axis=1).min()
-        if 0 < plan.ring < 2 * streamed:
+        depth = getattr(plan, "depth", 2)
+        if 0 < plan.ring < depth * streamed:
+            self.ctx.set_ring_depth(depth)
             self.ctx.set_ring_experts(int(plan.ring))
         self.set_device_mask(plan.device_mask)
 

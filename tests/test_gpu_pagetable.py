@@ -121,12 +121,15 @@ def test_layer_forward_through_page_table_faults_on_unmapped(X):
         X.layer_forward(table, spec, X.ForwardSpec(2, 2, 1), 1, np.ones((2, 16), np.float32))
 
 
-@pytest.mark.parametrize("ring,pinned,host_codec,S", [(2, None, False, 0), (4, None, True, 0), (6, None, False, 1),
-                                                       (4, 3, True, 0), (2, 5, False, 1), (16, None, False, 0)])
-def test_sub_layer_ring_windows_stay_exact(ring, pinned, host_codec, S):
+@pytest.mark.parametrize("ring,pinned,host_codec,S,depth", [
+    (2, None, False, 0, 2), (4, None, True, 0, 2), (6, None, False, 1, 2), (4, 3, True, 0, 2), (2, 5, False, 1, 2),
+    (16, None, False, 0, 2), (3, None, True, 0, 3), (6, 2, False, 1, 3), (4, None, True, 0, 4), (16, None, False, 0, 3),
+    (5, 6, True, 0, 5)])
+def test_sub_layer_ring_windows_stay_exact(ring, pinned, host_codec, S, depth):
     """Budgets below two layers: the ring holds `ring` blocks per kind and each layer streams
-    in windows of ring/2 experts; results stay bit-identical to the resident model, the log
-    replays clean window by window and the arena never exceeds the ring (+ pinned)."""
+    in windows of ring/depth experts, `depth` windows in flight; results stay bit-identical to
+    the resident model, the log replays clean window by window and the arena never exceeds the
+    ring (+ pinned)."""
     import paper_2604_02715_b200 as X
 
     spec = X.ModelSpec(3, 8, 128, 256)
@@ -135,16 +138,21 @@ def test_sub_layer_ring_windows_stay_exact(ring, pinned, host_codec, S):
     backends = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 30e9, 1 << 40)]
     hier = X.StorageHierarchy(c, None, X.plan_placement(spec, backends), backends)
     x = X.initial_activations(spec, fwd, 3)
-    runner = X.StreamedRunner(spec, hier, fwd, host_codec=host_codec, pinned=pinned, ring_experts=ring)
+    runner = X.StreamedRunner(spec, hier, fwd, host_codec=host_codec, pinned=pinned, ring_experts=ring,
+                              ring_depth=depth)
     rep = runner.run(2, acts=x.copy())
     base = X.resident_baseline(2, spec, c, fwd, acts=x.copy())
     assert rep.page_fault is None and rep.violations == []
     assert rep.final_activations.tobytes() == base.tobytes()
     p = pinned or 0
     streamed = spec.experts_per_layer - p
-    ring_used = min(ring, 2 * streamed)
-    assert rep.arena_peak_bytes == ring_used * spec.expert_bytes + p * spec.num_layers * spec.expert_bytes
-    windows = max(1, -(-streamed // max(1, ring_used // 2)))
+    ring_used = min(ring // depth * depth, depth * streamed)
+    gs = max(1, ring_used // depth)
+    windows = max(1, -(-streamed // gs))
+    sizes = [min(gs, streamed - i * gs) for i in range(windows)] * (2 * spec.num_layers)
+    in_flight = max(sum(sizes[i:i + depth]) for i in range(len(sizes)))  # window g recycles g - depth
+    assert rep.arena_peak_bytes == in_flight * spec.expert_bytes + p * spec.num_layers * spec.expert_bytes
+    assert in_flight <= ring_used
     starts = [r for r in rep.records if r.event == "compute-start"]
     assert len(starts) == 2 * spec.num_layers * windows
     if windows > 1:
@@ -174,6 +182,15 @@ def test_ring_experts_argument_checks():
     with pytest.raises(OutOfRangeError):
         ctx.set_ring_experts(1)
     ctx.set_ring_experts(-1)
+    for bad in (1, 7):
+        with pytest.raises(OutOfRangeError):
+            ctx.set_ring_depth(bad)
+    ctx.set_ring_depth(3)
+    with pytest.raises(OutOfRangeError):
+        ctx.set_ring_experts(2)   # fewer blocks than windows in flight
+    ctx.set_ring_experts(3)
+    with pytest.raises(OutOfRangeError):
+        ctx.set_ring_depth(4)
 
 
 def test_ring_resize_keeps_pinned_experts():

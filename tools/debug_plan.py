@@ -25,6 +25,16 @@ x = torch.from_numpy(X.initial_activations(spec, fwd, 7)).cuda()
 runner.run(2, acts=x)
 rep = runner.run(2, acts=x)
 print("elapsed ms", rep.elapsed_seconds * 1e3, "h2d GB", rep.h2d_bytes / 1e9, "decoded GB", rep.decoded_bytes / 1e9)
-ev = [(r.t, r.event, r.iteration, r.layer, r.group, r.kind, round(r.wall * 1e3, 2)) for r in rep.records]
-for e in ev[:80]:
-    print(e)
+last = max(r.iteration for r in rep.records)
+t0 = min(r.wall for r in rep.records if r.iteration == last)
+rows = {}
+for r in rep.records:
+    if r.iteration != last:
+        continue
+    key = (r.layer, r.group)
+    rows.setdefault(key, {})[(r.event, r.kind)] = round((r.wall - t0) * 1e3, 2)
+print("layer win | ls1 ls2 | ld1 ld2 | cs cd   (ms from the iteration's first record)")
+for (layer, g), d in sorted(rows.items()):
+    get = lambda e, k: d.get((e, k), "-")
+    print(layer, g, "|", get("load-start", 1), get("load-start", 2), "|", get("load-done", 1), get("load-done", 2),
+          "|", get("compute-start", None), get("compute-done", None))

@@ -40,6 +40,9 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--raw", action="store_true")
+    ap.add_argument("--depth", type=int, default=2, help="budget: windows in flight on the planned ring")
+    ap.add_argument("--window", type=int, default=None, help="budget: experts per ring window")
+    ap.add_argument("--stage-bufs", type=int, default=None, help="staging buffers per kind (host codec)")
     ap.add_argument("--rings", default="6,8,12", help="sub-layer ring sizes (expert blocks per kind) for budget")
     args = ap.parse_args()
     import torch
@@ -73,13 +76,14 @@ def main():
         x = torch.from_numpy(X.initial_activations(spec, fwd, SEED)).cuda()
         runner = X.StreamedRunner(spec, hier, fwd, host_codec=not args.raw,
                                   pinned=(p if what == "pinned" else None),
-                                  ring_experts=(p if what == "ring" else None))
+                                  ring_experts=(p if what == "ring" else None), stage_buffers=args.stage_bufs)
         plan = None
         if what == "plan":
             from paper_2604_02715_b200.budget import plan_residency
 
             ceb = runner.device_tier_bytes(L) / (N * L) * 1.002
-            plan = plan_residency(N, L, spec.expert_bytes, ceb, p * spec.total_bytes)
+            plan = plan_residency(N, L, spec.expert_bytes, ceb, p * spec.total_bytes, depth=args.depth,
+                                  window=args.window)
             runner.apply_plan(plan)
         runner.run(args.warmup, acts=x)
         secs, rep = timed(torch, lambda s: runner.run(s, acts=x), args.steps)
@@ -88,6 +92,7 @@ def main():
                "budget": p if what == "plan" else None,
                "pinned_per_layer": (plan.pinned_experts / N if plan else (p if what == "pinned" else 0)),
                "device_tier_per_layer": plan.device_experts / N if plan else 0,
+               "ring_depth": plan.depth if plan else 2, "stage_buffers": args.stage_bufs or 2,
                "ring_experts": (plan.ring if plan else (p if what == "ring" else 2 * (L - (p if what == "pinned" else 0)))),
                "hbm_fraction": (hbm["ring"] + hbm["device_tier"]) / spec.total_bytes,
                "hbm_footprint": (hbm["ring"] + hbm["staging"] + hbm["device_tier"]) / spec.total_bytes,
