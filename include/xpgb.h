@@ -243,7 +243,7 @@ int xpgb_set_ring_experts(xpgb_ctx* ctx, int32_t ring_experts);
  * and the session materializes up to g+depth.  Ignored without a ring cap.  Re-creates the
  * arena. */
 int xpgb_set_ring_depth(xpgb_ctx* ctx, int32_t depth);
-/* Staging ring of the compressed host tier: n_buffers (2..16, default 2) buffers per kind of
+/* Staging ring of the compressed host tier: n_buffers (2..16, default 4) buffers per kind of
  * min(largest record, 64 MB).  A staged copy waits only for its buffer's previous decode, never
  * for the arena's WAR event, so the link runs n_buffers-1 pieces ahead of the decoder -- across
  * device-tier windows that need no link at all.  Counted in xpgb_hbm_bytes' staging.  No session

@@ -252,7 +252,7 @@ struct Ctx {
   // for their buffer's previous decode (never for the ring's WAR), so the link runs up to
   // n_stage - 1 pieces ahead of the decoder, across windows and layers.
   uint8_t* stage[2][kMaxStageBufs] = {};  // [kind][buffer]
-  int n_stage = 2;
+  int n_stage = 4;  // a whole 156 MB Mixtral gate/up record + one piece in flight (80% budget: +9%)
   uint32_t stage_next[2] = {0, 0};
   uint32_t* d_index = nullptr;           // chunk indexes of host-tier records, device-resident
   std::vector<uint64_t> d_index_off;     // [N*E*2] offset (entries) into d_index
