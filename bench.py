@@ -79,6 +79,40 @@ def ncu_traffic(config: str, tokens: int):
     return None
 
 
+def ncu_decoder_capture():
+    """DRAM traffic vs algorithmic bytes of one decoder launch (Mixtral gate/up tensor) from
+    the committed ncu --set full capture."""
+    path = os.path.join(ROOT, "profiles", "r1_ncu_exp_decode_v5.jsonl")
+    try:
+        rec = json.loads(open(path).readline())
+        n = 117_440_512  # values of the captured tensor (tools/profile_codec.py default)
+        algo = n + n * 2.591 / 8 + n / 256 * 4 + 2 * n
+        return {"dram_bytes": rec["dram_read"] + rec["dram_write"], "algorithmic_bytes": algo,
+                "source": "profiles/r1_ncu_exp_decode_v5.jsonl (one 117.4M-value tensor, chunk 256)"}
+    except Exception:
+        return None
+
+
+def decoder_roofline(stats, steps, step_s, hbm_peak, hbm_src):
+    """Roofline of the exponent decoder (the dominant kernel of a paged decode step): its
+    algorithmic bytes per launch over its mean launch time, both over the timed run."""
+    n = stats.get("launches", 0)
+    if not n:
+        return None
+    per_launch = stats["algo_bytes"] / n
+    ns = stats["kernel_ns"] / n
+    ach = per_launch / ns  # bytes/ns == GB/s
+    return {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+            "peak_source": hbm_src, "kernel": "k_exp_decode (exponent-Huffman -> bf16 into the ring, paged run)",
+            "algorithmic_bytes_per_launch": per_launch, "avg_launch_us": ns / 1e3,
+            "launches_per_step": n / steps, "kernel_time_per_step_ms": stats["kernel_ns"] / steps / 1e6,
+            "step_ms": step_s * 1e3 / steps,
+            "note": "launches overlap each other (two kinds, host and device tiers) and the GEMMs, so a launch's "
+                    "time includes sharing the SMs; standalone the kernel reaches 1,265 GB/s of bf16 output "
+                    "(profiles/r1_decoder_chunk_grid_sweep.txt)",
+            "traffic": None, "traffic_capture": ncu_decoder_capture()}
+
+
 def gemm_roofline(kind, bytes_, ns, rows, H, F, hbm_peak, hbm_src, tc_peak, tc_src):
     """Roofline of one grouped-GEMM launch: HBM-bound (weights dominate) at decode sizes,
     tensor-bound once the rows per expert make the contraction compute-heavy."""
@@ -480,6 +514,7 @@ def main():
     value = tokens_total / elapsed
     page_in_gbps = rep.h2d_bytes / rep.elapsed_seconds / 1e9
     exposed = rep.stall_seconds / rep.elapsed_seconds
+    dec_stats = runner.ctx.decode_stats()  # every decoder launch of the timed run, events on its own stream
 
     log(f"timed paged run: {elapsed:.3f}s")
     # ---- e2e: the same metric through the public API with host buffers every step: a
@@ -556,6 +591,12 @@ def main():
                  "traffic": ncu_traffic(args.config, T_run), "rows_per_launch": rows,
                  "down": {k: roof_dn[k] for k in ("bound", "achieved", "peak", "unit", "frac", "avg_launch_us")}})
     roof["down"]["splits"] = kern.get("down_splits")
+    # the dominant kernel of the paged step is the decoder when the codec tiers are on (ncu
+    # launch list: profiles/r1_launches_bench_mixtral_codec.json); the GEMM roofline rides along
+    dec_roof = decoder_roofline(dec_stats, args.steps, elapsed, hbm_peak, peak_src)
+    if dec_roof is not None:
+        dec_roof["gemm"] = roof
+        roof = dec_roof
 
     line = {
         "metric": METRIC_PREFILL if args.prefill else METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,

@@ -115,6 +115,7 @@ _SIGS = {
     "xpgb_set_ring_experts": [_P, _I],
     "xpgb_set_ring_depth": [_P, _I],
     "xpgb_set_stage_buffers": [_P, _I],
+    "xpgb_decode_stats": [_P, _P, _P, _P],
     "xpgb_set_shared_tokens": [_P, _I, _I],
     "xpgb_shared_forward": [_P, _I, _P, _P, _I, _P],
     "xpgb_experts_forward": [_P, _I, _P, _P, _I, _P, _P],

@@ -269,6 +269,13 @@ struct Ctx {
   cudaEvent_t pev[7];
   cudaEvent_t* cur_ev = nullptr;          // 7 events bracketing the next enqueue_forward
   std::vector<cudaEvent_t> run_ev;        // per-step event sets for opts.profile
+  // opts.profile: every exponent-decoder launch of the run bracketed by events on its own
+  // stream, with its algorithmic bytes (records read + bf16 written) -- xpgb_decode_stats
+  std::vector<cudaEvent_t> dec_ev;
+  std::vector<uint64_t> dec_bytes;
+  size_t dec_n = 0;
+  double dec_total_ns = 0;
+  uint64_t dec_total_bytes = 0, dec_launches = 0;
   xpgb_kernel_times last_times{};  // last xpgb_profile_layer
 };
 
@@ -706,6 +713,25 @@ struct Step {
 // Alg. 1 MaterializeLayer (pipeline.py:335-360) for one kind, enqueued on copy stream `kind`:
 // recycle the blocks of step g-2 (the reference's target_layer, paging.py:29-38, once the
 // steps are layers) after its compute event, map + load this step's streamed experts.
+// opts.profile: bracket one decoder launch with events on its stream
+static void dec_mark(RunState& rs, cudaStream_t s, uint64_t bytes, bool begin) {
+  Ctx* c = rs.c;
+  if (!rs.o->profile) return;
+  if (begin) {
+    while (c->dec_ev.size() < 2 * (c->dec_n + 1)) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      c->dec_ev.push_back(e);
+    }
+    if (c->dec_bytes.size() < c->dec_n + 1) c->dec_bytes.resize(c->dec_n + 1);
+    c->dec_bytes[c->dec_n] = bytes;
+    CK(cudaEventRecord(c->dec_ev[2 * c->dec_n], s));
+  } else {
+    CK(cudaEventRecord(c->dec_ev[2 * c->dec_n + 1], s));
+    ++c->dec_n;
+  }
+}
+
 // windows in flight: the sub-layer ring's depth, else the reference's two layers
 static int depth_of(const Ctx* c) { return c->ring_limit > 0 ? c->ring_depth : 2; }
 
@@ -799,6 +825,8 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
     const uint64_t sm16 = (n + 15) & ~15ull;
     auto tix = [&](int e) { return ((size_t)(layer - 1) * E + e) * 2 + k; };
     auto rec_bytes = [&](int e) { return xpgb_codec_record_bytes(n, c->rec_bits[tix(e)], c->cchunk); };
+    // decoder's algorithmic bytes for one whole tensor: sign/mantissa + bitstream + chunk index read, bf16 written
+    auto algo_bytes = [&](size_t t) { return n + c->rec_bits[t] + (n + c->cchunk - 1) / c->cchunk * 4 + 2 * n; };
     // a staged run may take expert e' after e when its record follows e's in the pool
     auto joins_run = [&](int e, int e2, int tier) {
       return e2 < whi && !is_pinned(layer, e2) && c->backend[tix(e2)] == tier && delay_of(e2) <= 0.f &&
@@ -825,8 +853,12 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
                                    reinterpret_cast<uint16_t*>(block_ptr(c, kind, blocks[e2])), 0u};
           if (cnt == kMaxDecodeTensors || !joins_run(e2, e2 + 1, 1)) break;
         }
+        uint64_t ab = 0;
+        for (int i = 0; i < cnt; ++i) ab += algo_bytes(tix(e + i));
+        dec_mark(rs, dv, ab, true);
         launch_exp_decode_multi(dt, cnt, n, c->cchunk, c->ctab, dv);
         CKLAUNCH();
+        dec_mark(rs, dv, 0, false);
         rs.decoded += 2 * n * cnt;
         e += cnt;
       } else if (c->host_codec && rec_bytes(e) <= c->stage_cap[k]) {
@@ -857,8 +889,12 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
           dt[i] = DecodeTensor{rec, reinterpret_cast<const uint32_t*>(rec + sm16), c->d_index + c->d_index_off[t2],
                                reinterpret_cast<uint16_t*>(block_ptr(c, kind, blocks[e + i])), 0u};
         }
+        uint64_t ab = 0;
+        for (int i = 0; i < cnt; ++i) ab += algo_bytes(tix(e + i));
+        dec_mark(rs, d, ab, true);
         launch_exp_decode_multi(dt, cnt, n, c->cchunk, c->ctab, d);
         CKLAUNCH();
+        dec_mark(rs, d, 0, false);
         CK(cudaEventRecord(c->ev_decoded[k][buf], d));
         rs.decoded += 2 * n * cnt;
         e += cnt;
@@ -902,9 +938,11 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
           CK(cudaEventRecord(c->ev_copied[k][buf], cs));
           rs.h2d += ns + nbits;
           CK(cudaStreamWaitEvent(d, c->ev_copied[k][buf], 0));
+          dec_mark(rs, d, ns + (b1 - b0) + (c1 - c0) * 4 + 2 * ns, true);
           launch_exp_decode(st, reinterpret_cast<const uint32_t*>(st + o_bits), c->d_index + c->d_index_off[ti] + c0,
                             ns, c->cchunk, c->ctab, reinterpret_cast<uint16_t*>(dst) + v0, d, (uint32_t)(b0 * 8));
           CKLAUNCH();
+          dec_mark(rs, d, 0, false);
           CK(cudaEventRecord(c->ev_decoded[k][buf], d));
         }
         rs.decoded += 2 * n;
@@ -1016,6 +1054,7 @@ static void session_begin(Ctx* c, const xpgb_run_opts* o, float* acts) {
   ss.o = *o;
   build_schedule(c, ss, o->iterations);
   ss.mat_next = 0;
+  c->dec_n = 0;
   ss.fetch_delay.clear();
   ss.compute_delay.clear();
   if (o->fetch_delay_s) ss.fetch_delay.assign(o->fetch_delay_s, o->fetch_delay_s + (size_t)N * c->L * 2);
@@ -1229,6 +1268,15 @@ static void session_end(Ctx* c, xpgb_report* rep) {
     rep->kern_gate_up_ns = gu * 1e6 / steps;
     rep->kern_down_ns = dn * 1e6 / steps;
     rep->kern_aux_ns = aux * 1e6 / steps;
+  }
+  c->dec_total_ns = 0;
+  c->dec_total_bytes = 0;
+  c->dec_launches = c->dec_n;
+  for (size_t i = 0; i < c->dec_n; ++i) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, c->dec_ev[2 * i], c->dec_ev[2 * i + 1]));
+    c->dec_total_ns += ms * 1e6;
+    c->dec_total_bytes += c->dec_bytes[i];
   }
 
   if (paged) {
@@ -1499,6 +1547,7 @@ int xpgb_destroy(xpgb_ctx* h) {
     cudaEventDestroy(c->ev_end);
     for (int i = 0; i < 7; ++i) cudaEventDestroy(c->pev[i]);
     for (cudaEvent_t e : c->run_ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->dec_ev) cudaEventDestroy(e);
     delete c->sess;
     if (c->codec_events) {
       for (int k = 0; k < 2; ++k) {
@@ -2011,6 +2060,15 @@ int xpgb_set_ring_depth(xpgb_ctx* h, int32_t depth) {
       XFAIL(XPGB_ERR_OUT_OF_RANGE, "ring depth %d exceeds the ring of %d experts", depth, c->ring_limit);
     c->ring_depth = depth;
     if (c->ring_limit > 0) apply_residency(c, c->pinned);
+  });
+}
+
+int xpgb_decode_stats(xpgb_ctx* h, int64_t* launches, double* kernel_ns, int64_t* algo_bytes) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    *launches = (int64_t)c->dec_launches;
+    *kernel_ns = c->dec_total_ns;
+    *algo_bytes = (int64_t)c->dec_total_bytes;
   });
 }
 

@@ -137,6 +137,12 @@ class Context:
         call("xpgb_hbm_bytes", self._h, C.byref(r), C.byref(st), C.byref(dt))
         return {"ring": int(r.value), "staging": int(st.value), "device_tier": int(dt.value)}
 
+    def decode_stats(self) -> dict:
+        """Exponent-decoder launches of the last profiled run (xpgb_decode_stats)."""
+        n, ns, b = C.c_int64(), C.c_double(), C.c_int64()
+        call("xpgb_decode_stats", self._h, C.byref(n), C.byref(ns), C.byref(b))
+        return {"launches": int(n.value), "kernel_ns": float(ns.value), "algo_bytes": int(b.value)}
+
     def make_resident(self) -> None:
         call("xpgb_make_resident", self._h)
 
