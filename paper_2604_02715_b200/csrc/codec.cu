@@ -192,7 +192,7 @@ struct WordScalar {
   }
 };
 
-template <class R>
+template <bool FAST, class R>
 __device__ __forceinline__ void decode_chunk(R& q, uint64_t win, int avail, const uint8_t* __restrict__ sm,
                                              uint16_t* __restrict__ out, uint64_t v0, uint64_t v1, const uint32_t* lut3,
                                              int ml, const int* count, const uint32_t* first_code,
@@ -272,11 +272,11 @@ __global__ void __launch_bounds__(256) k_exp_decode(const __grid_constant__ Deco
     int avail = 64 - (int)sh;
     WordScalar q;
     q.init(d.bits + w + 2);
-    decode_chunk(q, win, avail, sm, out, v0, v1, lut3, ml, count, first_code, first_rank, sorted_sym);
+    decode_chunk<true>(q, win, avail, sm, out, v0, v1, lut3, ml, count, first_code, first_rank, sorted_sym);
   }
 }
 
-template <class R>
+template <bool FAST, class R>
 __device__ __forceinline__ void decode_chunk(R& q, uint64_t win, int avail, const uint8_t* __restrict__ sm,
                                              uint16_t* __restrict__ out, uint64_t v0, uint64_t v1, const uint32_t* lut3,
                                              int ml, const int* count, const uint32_t* first_code,
@@ -291,6 +291,54 @@ __device__ __forceinline__ void decode_chunk(R& q, uint64_t win, int avail, cons
     const int cnt = (int)((v1 - v) < 16 ? (v1 - v) : 16);
     uint4 smv = make_uint4(0, 0, 0, 0);
     if (cnt == 16 && wide) smv = *reinterpret_cast<const uint4*>(sm + v);
+    if (FAST && cnt == 16 && wide) {
+      // a whole group: two halves of 8 exponent bytes, each a 64-bit register filled at
+      // byte 8*np; a multi-symbol lookup that crosses the half spills into `carry`.  A
+      // lookup may run up to 2 symbols past the chunk (never written): they come from
+      // the next chunk's bits or the stream's 8-byte look-ahead padding.
+      uint64_t h[2];
+      uint64_t cur = b0, carry = 0;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        while (np < 8) {
+          if (avail < 32) {
+            win |= (uint64_t)q.pop() << (32 - avail);
+            avail += 32;
+          }
+          const uint32_t e = lut3[win >> (64 - kMultiBits)];
+          int k = (e >> 24) & 3, l;
+          uint64_t bytes;
+          if (__builtin_expect(k == 0, 0)) {
+            int sym = 0;
+            l = canon_decode(win, ml, count, first_code, first_rank, sorted_sym, &sym);
+            bytes = (uint32_t)sym;
+            k = 1;
+          } else {
+            l = (int)(e >> 26);
+            bytes = e & 0xFFFFFFu;
+          }
+          win <<= l;
+          avail -= l;
+          const int sh = 8 * np;
+          cur |= bytes << sh;
+          carry |= np > 5 ? bytes >> (64 - sh) : 0ull;
+          np += k;
+        }
+        h[half] = cur;
+        cur = carry;
+        carry = 0;
+        np -= 8;
+      }
+      b0 = cur;
+      const uint32_t e0 = (uint32_t)h[0], e1 = (uint32_t)(h[0] >> 32), e2 = (uint32_t)h[1], e3 = (uint32_t)(h[1] >> 32);
+      asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(out + v),
+                   "r"(pack_words(smv.x, e0, 0x5140u)), "r"(pack_words(smv.x, e0, 0x7362u)),
+                   "r"(pack_words(smv.y, e1, 0x5140u)), "r"(pack_words(smv.y, e1, 0x7362u)),
+                   "r"(pack_words(smv.z, e2, 0x5140u)), "r"(pack_words(smv.z, e2, 0x7362u)),
+                   "r"(pack_words(smv.w, e3, 0x5140u)), "r"(pack_words(smv.w, e3, 0x7362u))
+                   : "memory");
+      continue;
+    }
     while (np < cnt) {
       if (avail < 32) {
         win |= (uint64_t)q.pop() << (32 - avail);

@@ -230,6 +230,13 @@ class ExpertParallelMoE:
         if self.world == 1:
             out.copy_(inp)
             return
+        if out.device.type == "cuda" and dist.get_backend(self.group) == "gloo":
+            # gloo moves host memory only (the multi-rank-on-one-GPU test harness); NCCL is
+            # the GPU path
+            host = torch.empty(out.shape, dtype=out.dtype)
+            self._a2a(host, inp.cpu(), out_splits, in_splits)
+            out.copy_(host)
+            return
         if out.dtype == torch.bfloat16 and out.device.type == "cpu":
             # gloo has no 16-bit all_to_all: move pairs of bf16 words as int32 (H is even)
             dist.all_to_all_single(out.view(torch.int32), inp.contiguous().view(torch.int32), out_splits, in_splits,
@@ -321,6 +328,7 @@ class ExpertParallelRunner:
         opts.top_k = self.fwd.top_k
         opts.router_seed = int(self.fwd.router_seed) & 0xFFFFFFFFFFFFFFFF
         opts.log_enable = 1
+        opts.profile = 1 if profile else 0  # decoder launch timing (xpgb_decode_stats)
         h = self.ctx.handle
         torch.cuda.synchronize(self.ctx.device)
         call("xpgb_session_begin", h, C.byref(opts), None)

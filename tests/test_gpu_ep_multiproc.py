@@ -1,0 +1,85 @@
+"""Expert parallelism with two ranks on one B200: two processes, each an
+ExpertParallelRunner on its own expert shard (own ring, own compressed host pool, budget
+plan with sub-layer windows + device tier), exchanging rows over gloo (host-staged; NCCL
+is the multi-GPU transport).  The concatenated outputs must equal the single-device
+resident model on the concatenated batch."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SPEC = (3, 8, 128, 256)
+T, K, SEED = 12, 2, 9
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, budget, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        try:
+            import paper_2604_02715_b200 as X
+            from paper_2604_02715_b200.budget import plan_residency
+            from paper_2604_02715_b200.expert_parallel import ExpertParallelRunner
+
+            spec = X.ModelSpec(*SPEC)
+            fwd = X.ForwardSpec(T, K, SEED)
+            container = X.generate_synthetic_model(spec, SEED)
+            x_all = np.random.default_rng(SEED).standard_normal((world * T, spec.hidden_dim), dtype=np.float32)
+            runner = ExpertParallelRunner(spec, container, fwd, rank, world, host_codec=True)
+            count = runner.shard[1]
+            if budget is not None:
+                eb = spec.expert_bytes
+                ceb = runner.device_tier_bytes(count) / (spec.num_layers * count) * 1.002
+                plan = plan_residency(spec.num_layers, count, eb, ceb, budget * spec.num_layers * count * eb,
+                                      min_window_bytes=1)
+                runner.apply_plan(plan)
+            rep = runner.run(2, x_all[rank * T:(rank + 1) * T].copy())
+            torch.cuda.synchronize()
+            q.put((rank, (rep.final_activations.cpu().numpy(), rep.page_fault, rep.violations)))
+        except Exception:
+            import traceback
+
+            q.put((rank, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("budget", [None, 0.4])
+def test_two_ranks_on_one_gpu_match_resident(budget):
+    import torch.multiprocessing as mp
+
+    import paper_2604_02715_b200 as X
+    from oracle import xpg_oracle as O
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, budget, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    for r, v in got.items():
+        assert not isinstance(v, str), v
+        assert v[1] is None and v[2] == [], (r, v[1], v[2])
+    y = np.concatenate([got[r][0] for r in range(world)])
+    spec = X.ModelSpec(*SPEC)
+    container = X.generate_synthetic_model(spec, SEED)
+    x_all = np.random.default_rng(SEED).standard_normal((world * T, spec.hidden_dim), dtype=np.float32)
+    base = X.resident_baseline(2, spec, container, X.ForwardSpec(world * T, K, SEED), acts=x_all.copy())
+    assert O.rel_l2(y, base) <= 1e-3
