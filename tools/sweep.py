@@ -54,11 +54,21 @@ def main():
     if args.tokens:
         cfg["T"] = args.tokens
     N, L, H, F, k = cfg["N"], cfg["L"], cfg["H"], cfg["F"], cfg["k"]
+    S, G = cfg.get("S", 0), cfg.get("ep_virtual", 1)
     spec = X.ModelSpec(N, L, H, F)
+    cspec, run_kw = spec, {}
+    if G > 1:  # one EP rank's slice on this GPU (as bench.py's dsv3 config)
+        from paper_2604_02715_b200.expert_parallel import shard_bounds
+
+        first, count = shard_bounds(L, G)[0]
+        cspec = X.ModelSpec(N, count, H, F)
+        run_kw = {"expert_shard": (first, count), "shared_tokens": (0, cfg["T"])}
     t0 = time.time()
-    container = X.generate_fast_model(spec, SEED)
+    container = X.generate_fast_model(cspec, SEED, shared_experts=S)
+    shared_b = container.shared.total_bytes if container.shared is not None else 0
+    budget_base = cspec.total_bytes + shared_b
     backends = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 55e9, 1 << 50)]
-    hier = X.StorageHierarchy(container, None, X.plan_placement(spec, backends), backends)
+    hier = X.StorageHierarchy(container, None, X.plan_placement(cspec, backends), backends)
     if not args.raw:
         hier.compressed = CompressedModel.from_container(container)
     peak = h2d_peak_gbps(torch, 0)
@@ -72,18 +82,20 @@ def main():
     resident_tok = {}
     for what, p in points:
         T = int(p) if what == "tokens" else cfg["T"]
-        fwd = X.ForwardSpec(T, k, SEED)
+        fwd = X.ForwardSpec(T * G, k, SEED)
         x = torch.from_numpy(X.initial_activations(spec, fwd, SEED)).cuda()
         runner = X.StreamedRunner(spec, hier, fwd, host_codec=not args.raw,
                                   pinned=(p if what == "pinned" else None),
-                                  ring_experts=(p if what == "ring" else None), stage_buffers=args.stage_bufs)
+                                  ring_experts=(p if what == "ring" else None), stage_buffers=args.stage_bufs,
+                                  **run_kw)
         plan = None
         if what == "plan":
             from paper_2604_02715_b200.budget import plan_residency
 
-            ceb = runner.device_tier_bytes(L) / (N * L) * 1.002
-            plan = plan_residency(N, L, spec.expert_bytes, ceb, p * spec.total_bytes, depth=args.depth,
-                                  window=args.window)
+            Lc = cspec.experts_per_layer
+            ceb = runner.device_tier_bytes(Lc) / (N * Lc) * 1.002
+            plan = plan_residency(N, Lc, spec.expert_bytes, ceb, p * budget_base, shared_bytes=shared_b,
+                                  depth=args.depth, window=args.window)
             runner.apply_plan(plan)
         runner.run(args.warmup, acts=x)
         secs, rep = timed(torch, lambda s: runner.run(s, acts=x), args.steps)
@@ -92,17 +104,17 @@ def main():
                "budget": p if what == "plan" else None,
                "pinned_per_layer": (plan.pinned_experts / N if plan else (p if what == "pinned" else 0)),
                "device_tier_per_layer": plan.device_experts / N if plan else 0,
-               "ring_depth": plan.depth if plan else 2, "stage_buffers": args.stage_bufs or 2,
+               "ring_depth": plan.depth if plan else 2, "stage_buffers": args.stage_bufs or 4,
                "ring_experts": (plan.ring if plan else (p if what == "ring" else 2 * (L - (p if what == "pinned" else 0)))),
-               "hbm_fraction": (hbm["ring"] + hbm["device_tier"]) / spec.total_bytes,
-               "hbm_footprint": (hbm["ring"] + hbm["staging"] + hbm["device_tier"]) / spec.total_bytes,
+               "hbm_fraction": (hbm["ring"] + hbm["device_tier"]) / budget_base,
+               "hbm_footprint": (hbm["ring"] + hbm["staging"] + hbm["device_tier"]) / budget_base,
                "tok_s": T * args.steps / secs, "ms_per_step": 1e3 * secs / args.steps,
                "page_in_gbps": rep.h2d_bytes / rep.elapsed_seconds / 1e9 if rep.elapsed_seconds else 0.0,
                "h2d_peak_gbps": peak, "exposed_xfer_pct": 100 * rep.stall_seconds / max(rep.elapsed_seconds, 1e-12),
                "host_codec": not args.raw}
         del runner
         if T not in resident_tok:
-            model = X.ResidentModel(spec, container, max_tokens=T)
+            model = X.ResidentModel(spec, container, max_tokens=T * G, **run_kw)
             model.run(1, fwd, x)
             rs, _ = timed(torch, lambda s: model.run(s, fwd, x), args.steps)
             resident_tok[T] = T * args.steps / rs
