@@ -61,10 +61,11 @@ void launch_route_plan(uint64_t seed, int layer_first, int layer_count, int T, i
 void launch_gather(const float* x, const int32_t* pos, const long long* fault, __nv_bfloat16* xp, int T, int kk,
                    int H, cudaStream_t s);
 // map_ws: the shared experts' weights (read for groups >= p.E_routed).
+// lean: one stage fewer so exponent-decoder CTAs co-reside (paged runs with a compressed tier)
 void launch_gate_up(const CUtensorMap& map_w, const CUtensorMap& map_x, const CUtensorMap& map_ws,
-                    const GemmParams& p, int bn, int grid, cudaStream_t s);
+                    const GemmParams& p, int bn, int grid, cudaStream_t s, bool lean = false);
 void launch_down(const CUtensorMap& map_w, const CUtensorMap& map_h, const CUtensorMap& map_ws,
-                 const GemmParams& p, int bn, int grid, cudaStream_t s);
+                 const GemmParams& p, int bn, int grid, cudaStream_t s, bool lean = false);
 // y_t = ordered weighted sum of the token's kk expert rows (the first kr scaled by
 // inv_k, the rest -- shared experts -- by 1); optionally also writes bf16(y_t) to
 // the next layer's expert-major rows (fused gather).

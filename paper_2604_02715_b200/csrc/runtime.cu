@@ -427,6 +427,17 @@ static double avg_group_rows(Ctx* c, int T, int kk) {
 
 static int pick_bn(Ctx* c, int T, int kk) { return pick_bn_rows(avg_group_rows(c, T, kk)); }
 
+// Lean GEMM tiles while a compressed tier decodes on the SMs of a paged run (moe_kernels.cu:
+// XPGB_GU_LEAN); XPGB_COSCHED=0/1 forces either.
+static bool lean_gemm(const Ctx* c) {
+  static const int force = [] {
+    const char* e = getenv("XPGB_COSCHED");
+    return e ? atoi(e) : -1;
+  }();
+  if (force >= 0) return force != 0;
+  return c->codec && c->pool == XPGB_POOL_RING && c->ring_blocks > 0;  // something is decoded each step
+}
+
 // Down projection at prefill sizes: N = 256 token rows per tile halves the weight-tile
 // re-reads and the smem traffic per MMA flop (one 256-column accumulator, double-buffered).
 static int pick_bn_down(Ctx* c, int T, int kk) {
@@ -528,13 +539,13 @@ static void enqueue_window(Ctx* c, int layer, const float* x, float* y, int T, i
   if (pair)
     launch_gemm_pair(true, c->map_xp_pair, c->map_gu, c->S ? c->map_gu_sh : c->map_gu, pg, c->num_sms, s);
   else
-    launch_gate_up(c->map_gu, c->map_xp, c->S ? c->map_gu_sh : c->map_gu, pg, bn, c->num_sms, s);
+    launch_gate_up(c->map_gu, c->map_xp, c->S ? c->map_gu_sh : c->map_gu, pg, bn, c->num_sms, s, lean_gemm(c));
   CKLAUNCH();
   prof_rec(c, 4, s);
   if (pair)
     launch_gemm_pair(false, c->map_h_pair, c->map_dn, c->S ? c->map_dn_sh : c->map_dn, pd, c->num_sms, s);
   else
-    launch_down(c->map_dn, c->map_h, c->S ? c->map_dn_sh : c->map_dn, pd, bn_dn, c->num_sms, s);
+    launch_down(c->map_dn, c->map_h, c->S ? c->map_dn_sh : c->map_dn, pd, bn_dn, c->num_sms, s, lean_gemm(c));
   CKLAUNCH();
   prof_rec(c, 5, s);
   if (last) {
