@@ -321,6 +321,26 @@ int xpgb_experts_forward(xpgb_ctx* ctx, int32_t layer, const void* rows_dev, con
  * replica to its own tokens after the routed combine): y[t] += sum_s shared_s(x[t]) in fp32,
  * shared experts in ascending order, weight 1.  x, y: device fp32 [tokens][H]. */
 int xpgb_shared_forward(xpgb_ctx* ctx, int32_t layer, const float* x_dev, float* y_dev, int32_t tokens, void* stream);
+/* ---------------------------------------------------------------- EP exchange over peer memory
+ * (SURVEY §8(e) fusion target; no reference counterpart).  Each rank allocates one window
+ * (cudaMalloc'd, zeroed, exported as a 64-byte CUDA IPC handle), the ranks swap handles and
+ * open each other's windows (NVLink P2P; the same device works too).  A layer's dispatch and
+ * combine are then one scatter kernel each: row i of src (src_rows[i], or i when src_rows is
+ * null) goes to row dst_row[i] of rank dst_rank[i]'s region peer_rows[dst_rank[i]] -- bf16
+ * when to_bf16, else f32 -- and the kernel's last CTA releases `epoch` into slot `rank` of
+ * every rank's flag array peer_flags[r] (int32[16]).  xpgb_ep_wait makes `stream` wait
+ * (acquire) until all `world` slots of this rank's flags reach `epoch`.  counter: a device
+ * uint32, zero, private to the call site.  peer_rows/peer_flags are host arrays of device
+ * pointers (this rank's own window included). */
+int xpgb_ep_window_alloc(uint64_t bytes, void** dptr, void* ipc_handle64);
+int xpgb_ep_window_open(const void* ipc_handle64, void** dptr);
+int xpgb_ep_window_close(void* dptr);
+int xpgb_ep_window_free(void* dptr);
+int xpgb_ep_scatter_rows(const float* src_dev, const int32_t* src_rows, const int32_t* dst_rank, const int32_t* dst_row,
+                         int32_t n, int32_t hidden, int32_t to_bf16, void* const* peer_rows, int32_t* const* peer_flags,
+                         int32_t world, int32_t rank, int32_t epoch, uint32_t* counter, void* stream);
+int xpgb_ep_wait(const int32_t* flags_dev, int32_t world, int32_t epoch, void* stream);
+
 /* One window of a layer on pre-grouped rows: GEMMs of local experts [e0, e1) only (rows stay
  * absolute; the rows are copied in with the e0 == 0 window); reduce = 1 on the layer's last
  * window writes every row's output (split-K partials of all windows are final by then). */

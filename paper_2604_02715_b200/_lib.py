@@ -116,6 +116,12 @@ _SIGS = {
     "xpgb_set_ring_depth": [_P, _I],
     "xpgb_set_stage_buffers": [_P, _I],
     "xpgb_decode_stats": [_P, _P, _P, _P],
+    "xpgb_ep_window_alloc": [C.c_uint64, _P, _P],
+    "xpgb_ep_window_open": [_P, _P],
+    "xpgb_ep_window_close": [_P],
+    "xpgb_ep_window_free": [_P],
+    "xpgb_ep_scatter_rows": [_P, _P, _P, _P, _I, _I, _I, _P, _P, _I, _I, _I, _P, _P],
+    "xpgb_ep_wait": [_P, _I, _I, _P],
     "xpgb_set_shared_tokens": [_P, _I, _I],
     "xpgb_shared_forward": [_P, _I, _P, _P, _I, _P],
     "xpgb_experts_forward": [_P, _I, _P, _P, _I, _P, _P],

@@ -27,6 +27,7 @@
 
 #include "../../include/xpgb.h"
 #include "codec.cuh"
+#include "ep_p2p.cuh"
 #include "launch_count.h"
 #include "moe_kernels.cuh"
 #include "ptx_sm100.cuh"
@@ -2359,6 +2360,65 @@ int xpgb_shared_forward(xpgb_ctx* h, int32_t layer, const float* x_dev, float* y
                    true);
     CKLAUNCH();
     CK(cudaStreamSynchronize(s));  // the host index vector is pageable scratch
+  });
+}
+
+// ---------------------------------------------------------------- EP over peer memory
+int xpgb_ep_window_alloc(uint64_t bytes, void** dptr, void* ipc_handle) {
+  return guard([&] {
+    CK(cudaMalloc(dptr, bytes));
+    CK(cudaMemset(*dptr, 0, bytes));
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, *dptr));
+    memcpy(ipc_handle, &h, sizeof(h));
+  });
+}
+
+int xpgb_ep_window_open(const void* ipc_handle, void** dptr) {
+  return guard([&] {
+    cudaIpcMemHandle_t h;
+    memcpy(&h, ipc_handle, sizeof(h));
+    CK(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+int xpgb_ep_window_close(void* dptr) {
+  return guard([&] { CK(cudaIpcCloseMemHandle(dptr)); });
+}
+
+int xpgb_ep_window_free(void* dptr) {
+  return guard([&] { CK(cudaFree(dptr)); });
+}
+
+int xpgb_ep_scatter_rows(const float* src_dev, const int32_t* src_rows, const int32_t* dst_rank, const int32_t* dst_row,
+                         int32_t n, int32_t hidden, int32_t to_bf16, void* const* peer_rows, int32_t* const* peer_flags,
+                         int32_t world, int32_t rank, int32_t epoch, uint32_t* counter, void* stream) {
+  return guard([&] {
+    if (world < 1 || world > kMaxEpWorld || rank < 0 || rank >= world)
+      XFAIL(XPGB_ERR_OUT_OF_RANGE, "rank %d of %d (at most %d ranks)", rank, world, kMaxEpWorld);
+    if (hidden % 4) XFAIL(XPGB_ERR_OUT_OF_RANGE, "hidden_dim must be a multiple of 4");
+    if (n < 0) XFAIL(XPGB_ERR_OUT_OF_RANGE, "negative row count");
+    EpPeers peers{};
+    peers.world = world;
+    peers.rank = rank;
+    for (int r = 0; r < world; ++r) {
+      peers.rows[r] = peer_rows[r];
+      peers.flags[r] = peer_flags[r];
+    }
+    int dev = 0, sms = 148;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    launch_ep_scatter(src_dev, src_rows, dst_rank, dst_row, n, hidden, to_bf16 != 0, peers, epoch, counter, sms,
+                      (cudaStream_t)stream);
+    CKLAUNCH();
+  });
+}
+
+int xpgb_ep_wait(const int32_t* flags_dev, int32_t world, int32_t epoch, void* stream) {
+  return guard([&] {
+    if (world < 1 || world > kMaxEpWorld) XFAIL(XPGB_ERR_OUT_OF_RANGE, "%d ranks (at most %d)", world, kMaxEpWorld);
+    launch_ep_wait(flags_dev, world, epoch, (cudaStream_t)stream);
+    CKLAUNCH();
   });
 }
 

@@ -69,6 +69,12 @@ class DispatchPlan:
     from_expert: object    # [n_recv] expert-major index of each arrival row
     offsets: object        # [count+1] expert-major row offsets of the local experts (int32)
     ret_index: object      # [T, kk] position of each (token, slot) in the returned buffer (int32)
+    # peer-memory exchange (PeerExchange): where each row goes, computed from the global routing
+    p2p_src_rows: object = None   # [T*kk] local token of each of my pairs, in send order (int32)
+    p2p_dst_rank: object = None   # [T*kk] owner rank of each of my pairs
+    p2p_dst_row: object = None    # [T*kk] its row in the owner's expert-major input
+    c_rank: object = None         # [n_own] token-owner rank of each of my expert-major rows
+    c_row: object = None          # [n_own] its row in that rank's return buffer (= its send position)
 
 
 def build_plan(routes, rank: int, world: int, tokens: int, bounds) -> DispatchPlan:
@@ -115,7 +121,7 @@ def build_plan(routes, rank: int, world: int, tokens: int, bounds) -> DispatchPl
     per_exp = torch.bincount(a_exp - first, minlength=count) if a_exp.numel() else torch.zeros(count, dtype=torch.int64, device=dev)
     offsets = torch.zeros(count + 1, dtype=torch.int32, device=dev)
     offsets[1:] = torch.cumsum(per_exp, 0).to(torch.int32)
-    return DispatchPlan(
+    plan = DispatchPlan(
         send_counts=[int(v) for v in send_counts.tolist()],
         recv_counts=[int(v) for v in recv_counts.tolist()],
         send_rows=send_rows,
@@ -124,6 +130,117 @@ def build_plan(routes, rank: int, world: int, tokens: int, bounds) -> DispatchPl
         offsets=offsets,
         ret_index=ret_index.reshape(T, kk).to(torch.int32),
     )
+    # ---- peer-memory exchange: every pair's row at its owner and at its sender, for all ranks
+    P = G * T * kk
+    ar = torch.arange(P, device=dev)
+    src_f, dst_f, e_f, in_f = src.reshape(-1), dst.reshape(-1), e0.reshape(-1), inner.reshape(-1)
+    order_s = torch.argsort((src_f * G + dst_f) * span + in_f)          # each sender's send order
+    pos_s = torch.empty_like(ar)
+    pos_s[order_s] = ar
+    send_pos = pos_s - src_f * (T * kk)
+    order_e = torch.argsort((e_f * G + src_f) * span + in_f)            # each owner's expert-major order
+    pos_e = torch.empty_like(ar)
+    pos_e[order_e] = ar
+    n_dst = torch.bincount(dst_f, minlength=G)
+    before = torch.cumsum(n_dst, 0) - n_dst
+    em_pos = pos_e - before[dst_f]
+    mine_s = order_s[rank * T * kk:(rank + 1) * T * kk]
+    b0, n_own = int(before[rank]), int(n_dst[rank])
+    own_e = order_e[b0:b0 + n_own]
+    plan.p2p_src_rows = (mine_s // kk - rank * T).to(torch.int32)
+    plan.p2p_dst_rank = dst_f[mine_s].to(torch.int32)
+    plan.p2p_dst_row = em_pos[mine_s].to(torch.int32)
+    plan.c_rank = src_f[own_e].to(torch.int32)
+    plan.c_row = send_pos[own_e].to(torch.int32)
+    return plan
+
+
+class PeerExchange:
+    """Dispatch/combine over peer memory: one window per rank (CUDA IPC, opened by every
+    other rank), one scatter kernel per exchange writing rows straight into the owner's
+    expert-major input / the sender's return buffer, an epoch flag per (rank, peer) released
+    by the scatter's last CTA and acquired by the receiver's stream (xpgb_ep_*)."""
+
+    FLAG_BYTES = 512  # int32 flags[16] at 0, the scatter's CTA counter at 256; rows from 512
+
+    def __init__(self, rank: int, world: int, tokens: int, kk: int, hidden: int, group=None):
+        import torch.distributed as dist
+
+        self.rank, self.world, self.H = rank, world, hidden
+        self.in_rows = world * tokens * kk           # worst case: every pair of the step lands here
+        self.ret_rows = tokens * kk
+        self.xp_off = self.FLAG_BYTES
+        self.ret_off = self.xp_off + ((self.in_rows * hidden * 2 + 255) // 256) * 256
+        size = self.ret_off + self.ret_rows * hidden * 4
+        base = C.c_void_p()
+        handle = (C.c_uint8 * 64)()
+        call("xpgb_ep_window_alloc", C.c_uint64(size), C.byref(base), handle)
+        self._own = base.value
+        handles = [None] * world
+        if world > 1:
+            dist.all_gather_object(handles, bytes(handle), group=group)
+        self._opened = []
+        bases = []
+        for r in range(world):
+            if r == rank:
+                bases.append(self._own)
+                continue
+            p = C.c_void_p()
+            call("xpgb_ep_window_open", (C.c_uint8 * 64).from_buffer_copy(handles[r]), C.byref(p))
+            self._opened.append(p.value)
+            bases.append(p.value)
+        self.bases = bases
+        self._xp = (C.c_void_p * world)(*[b + self.xp_off for b in bases])
+        self._ret = (C.c_void_p * world)(*[b + self.ret_off for b in bases])
+        self._flags = (C.c_void_p * world)(*bases)
+        self.counter = self._own + 256
+        self.epoch = 0
+
+    @property
+    def xp(self) -> int:
+        """This rank's expert-major bf16 input rows (device pointer)."""
+        return self._own + self.xp_off
+
+    @property
+    def ret(self) -> int:
+        """This rank's returned fp32 rows, in send order (device pointer)."""
+        return self._own + self.ret_off
+
+    def _scatter(self, src, src_rows, dst_rank, dst_row, n, to_bf16, regions, stream):
+        self.epoch += 1
+        call("xpgb_ep_scatter_rows", C.c_void_p(src.data_ptr()),
+             C.c_void_p(src_rows.data_ptr()) if src_rows is not None else None,
+             C.c_void_p(dst_rank.data_ptr()), C.c_void_p(dst_row.data_ptr()), int(n), self.H, 1 if to_bf16 else 0,
+             regions, self._flags, self.world, self.rank, self.epoch, C.c_void_p(self.counter), C.c_void_p(stream))
+        call("xpgb_ep_wait", C.c_void_p(self._own), self.world, self.epoch, C.c_void_p(stream))
+
+    def dispatch(self, x, plan, stream) -> int:
+        """x fp32 [T, H] -> every owner's expert-major bf16 rows; returns this rank's xp."""
+        self._scatter(x, plan.p2p_src_rows, plan.p2p_dst_rank, plan.p2p_dst_row, plan.p2p_src_rows.numel(), True,
+                      self._xp, stream)
+        return self.xp
+
+    def combine(self, out, plan, stream) -> int:
+        """This rank's expert outputs fp32 [n_own, H] -> the token owners' return buffers."""
+        self._scatter(out, None, plan.c_rank, plan.c_row, plan.c_rank.numel(), False, self._ret, stream)
+        return self.ret
+
+    def close(self):
+        import torch
+
+        torch.cuda.synchronize()
+        for p in self._opened:
+            _lib.lib().xpgb_ep_window_close(C.c_void_p(p))
+        self._opened = []
+        if self._own:
+            _lib.lib().xpgb_ep_window_free(C.c_void_p(self._own))
+            self._own = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class ExpertParallelMoE:
@@ -254,9 +371,11 @@ class ExpertParallelRunner:
     """
 
     def __init__(self, spec: ModelSpec, container, fwd: ForwardSpec, rank: int, world: int, device: int = 0,
-                 group=None, shard_pool=None, shared=None, host_codec: bool = False):
+                 group=None, shard_pool=None, shared=None, host_codec: bool = False, transport: str = "nccl"):
         """host_codec: the rank's shard pages in as exponent-Huffman records over its own host
-        link, decoded on its GPU (as StreamedRunner(host_codec=True))."""
+        link, decoded on its GPU (as StreamedRunner(host_codec=True)).
+        transport: "nccl" (all_to_all_single), "p2p" (PeerExchange: scatter kernels into the
+        peers' windows over NVLink), or "auto" (p2p when every window opens, else nccl)."""
         from .device import Context
 
         shared = shared if shared is not None else getattr(container, "shared", None)
@@ -282,6 +401,33 @@ class ExpertParallelRunner:
             self.ctx.set_shared(shared)  # every rank holds a replica (resident, never paged)
         self.moe = ExpertParallelMoE(spec, fwd, rank, world, group=group, ctx=self.ctx,
                                      has_shared=shared is not None)
+        self.peer = None
+        self.transport = "nccl"
+        self.transport_note = None
+        if transport not in ("nccl", "p2p", "auto"):
+            raise ValueError(f"unknown transport {transport!r}")
+        if transport in ("p2p", "auto"):
+            kk = min(fwd.top_k, spec.experts_per_layer)
+            try:
+                self.peer = PeerExchange(rank, world, fwd.tokens_per_step, kk, spec.hidden_dim, group=group)
+                self.transport = "p2p"
+            except Exception as exc:  # noqa: BLE001 -- auto falls back to the collective
+                if transport == "p2p":
+                    raise
+                self.transport_note = f"p2p unavailable ({exc}); nccl all_to_all"
+
+    def close(self) -> None:
+        """Release the peer windows (collective: every rank closes its mappings first)."""
+        if self.peer is not None:
+            import torch.distributed as dist
+
+            peer, self.peer = self.peer, None
+            for p in peer._opened:
+                _lib.lib().xpgb_ep_window_close(C.c_void_p(p))
+            peer._opened = []
+            if self.world > 1:
+                dist.barrier(group=self.moe.group)
+            peer.close()
 
     def device_tier_bytes(self, m: int) -> int:
         from ._lib import lib
@@ -338,24 +484,44 @@ class ExpertParallelRunner:
             total = C.c_int32()
             call("xpgb_session_info", h, C.byref(total), None, None)
             info = (C.c_int32 * 7)()
-            rows = out = None
+            out = None
+            n_rows, rows_ptr = 0, 0
+            peer = self.peer
+            kk = min(self.fwd.top_k, self.spec.experts_per_layer)
+            H = self.spec.hidden_dim
             for g in range(total.value):  # steps are layers, or windows of a sub-layer ring
                 call("xpgb_session_step", h, g, info)
                 layer, e0, e1, first, last = info[1], info[3], info[4], info[5], info[6]
                 plan = plans[layer - 1]
-                st = C.c_void_p(current_stream_ptr(self.ctx.device))
+                stream = current_stream_ptr(self.ctx.device)
+                st = C.c_void_p(stream)
                 if first:
-                    rows = self.moe.dispatch(x, plan)
-                    out = torch.empty((rows.shape[0], self.spec.hidden_dim), dtype=torch.float32, device=x.device)
+                    if peer is not None:
+                        n_rows = int(plan.c_rank.numel())
+                        rows_ptr = peer.dispatch(x, plan, stream)  # rows land expert-major in my window
+                    else:
+                        rows = self.moe.dispatch(x, plan)
+                        n_rows, rows_ptr = int(rows.shape[0]), rows.data_ptr()
+                    out = torch.empty((n_rows, H), dtype=torch.float32, device=x.device)
                 call("xpgb_session_acquire", h, g, st)
-                if rows.shape[0] and e1 > e0:
-                    call("xpgb_experts_forward_range", h, layer, C.c_void_p(rows.data_ptr()),
-                         C.c_void_p(plan.offsets.data_ptr()), int(rows.shape[0]), e0, e1, 1 if last else 0,
+                if n_rows and e1 > e0:
+                    call("xpgb_experts_forward_range", h, layer, C.c_void_p(rows_ptr),
+                         C.c_void_p(plan.offsets.data_ptr()), n_rows, e0, e1, 1 if last else 0,
                          C.c_void_p(out.data_ptr()), st)
                 call("xpgb_session_release", h, g, st)
                 call("xpgb_session_materialize", h, g + 2)
                 if last:
-                    x = self.moe.combine(layer, x, out, plan)
+                    if peer is not None:
+                        ret = peer.combine(out, plan, stream)
+                        y = torch.empty((T, H), dtype=torch.float32, device=x.device)
+                        if T:
+                            call("xpgb_combine_rows", C.c_void_p(ret), C.c_void_p(plan.ret_index.data_ptr()), T, kk,
+                                 self.fwd.top_k, H, C.c_void_p(y.data_ptr()), st)
+                        if self.moe.shared_fn is not None:
+                            self.moe.shared_fn(layer, x, y)
+                        x = y
+                    else:
+                        x = self.moe.combine(layer, x, out, plan)
         except Exception:
             _lib.lib().xpgb_session_abort(h)
             raise

@@ -1,8 +1,10 @@
 """Expert parallelism with two ranks on one B200: two processes, each an
 ExpertParallelRunner on its own expert shard (own ring, own compressed host pool, budget
-plan with sub-layer windows + device tier), exchanging rows over gloo (host-staged; NCCL
-is the multi-GPU transport).  The concatenated outputs must equal the single-device
-resident model on the concatenated batch."""
+plan with sub-layer windows + device tier).  Rows move either through the collective
+(gloo, host-staged here; NCCL across GPUs) or through peer memory (PeerExchange: CUDA IPC
+windows, scatter kernels, epoch flags -- the same code path as across NVLink).  The
+concatenated outputs must equal the single-device resident model on the concatenated
+batch."""
 import os
 import socket
 
@@ -21,7 +23,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, budget, q):
+def _worker(rank, world, port, budget, transport, q):
     import torch
     import torch.distributed as dist
 
@@ -38,7 +40,8 @@ def _worker(rank, world, port, budget, q):
             fwd = X.ForwardSpec(T, K, SEED)
             container = X.generate_synthetic_model(spec, SEED)
             x_all = np.random.default_rng(SEED).standard_normal((world * T, spec.hidden_dim), dtype=np.float32)
-            runner = ExpertParallelRunner(spec, container, fwd, rank, world, host_codec=True)
+            runner = ExpertParallelRunner(spec, container, fwd, rank, world, host_codec=True, transport=transport)
+            assert runner.transport == transport, runner.transport_note
             count = runner.shard[1]
             if budget is not None:
                 eb = spec.expert_bytes
@@ -47,7 +50,10 @@ def _worker(rank, world, port, budget, q):
                                       min_window_bytes=1)
                 runner.apply_plan(plan)
             rep = runner.run(2, x_all[rank * T:(rank + 1) * T].copy())
+            rep2 = runner.run(1, x_all[rank * T:(rank + 1) * T].copy())  # epochs keep counting across runs
             torch.cuda.synchronize()
+            runner.close()
+            assert rep2.page_fault is None
             q.put((rank, (rep.final_activations.cpu().numpy(), rep.page_fault, rep.violations)))
         except Exception:
             import traceback
@@ -57,8 +63,8 @@ def _worker(rank, world, port, budget, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("budget", [None, 0.4])
-def test_two_ranks_on_one_gpu_match_resident(budget):
+@pytest.mark.parametrize("budget,transport", [(None, "nccl"), (0.4, "nccl"), (None, "p2p"), (0.4, "p2p")])
+def test_two_ranks_on_one_gpu_match_resident(budget, transport):
     import torch.multiprocessing as mp
 
     import paper_2604_02715_b200 as X
@@ -68,12 +74,14 @@ def test_two_ranks_on_one_gpu_match_resident(budget):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, budget, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, budget, transport, q)) for r in range(world)]
     for p in procs:
         p.start()
-    got = dict(q.get(timeout=300) for _ in range(world))
+    got = dict(q.get(timeout=180) for _ in range(world))
     for p in procs:
         p.join(timeout=60)
+        if p.is_alive():
+            p.kill()
     for r, v in got.items():
         assert not isinstance(v, str), v
         assert v[1] is None and v[2] == [], (r, v[1], v[2])
@@ -83,3 +91,21 @@ def test_two_ranks_on_one_gpu_match_resident(budget):
     x_all = np.random.default_rng(SEED).standard_normal((world * T, spec.hidden_dim), dtype=np.float32)
     base = X.resident_baseline(2, spec, container, X.ForwardSpec(world * T, K, SEED), acts=x_all.copy())
     assert O.rel_l2(y, base) <= 1e-3
+
+
+def test_peer_exchange_world1_matches_resident():
+    """PeerExchange with one rank (the scatter writes into its own window)."""
+    import paper_2604_02715_b200 as X
+    from oracle import xpg_oracle as O
+    from paper_2604_02715_b200.expert_parallel import ExpertParallelRunner
+
+    spec = X.ModelSpec(*SPEC)
+    fwd = X.ForwardSpec(T, K, SEED)
+    container = X.generate_synthetic_model(spec, SEED, shared_experts=1)
+    x = X.initial_activations(spec, fwd, SEED)
+    runner = ExpertParallelRunner(spec, container, fwd, 0, 1, host_codec=True, transport="p2p")
+    rep = runner.run(2, x.copy())
+    runner.close()
+    assert rep.page_fault is None and rep.violations == []
+    base = X.resident_baseline(2, spec, container, fwd, acts=x.copy())
+    assert O.rel_l2(rep.final_activations.cpu().numpy(), base) <= 1e-3
