@@ -355,6 +355,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-resident", action="store_true")
     ap.add_argument("--ep", action="store_true", help="use the expert-parallel runner even at N=1")
+    ap.add_argument("--transport", default="auto", choices=["auto", "p2p", "nccl"],
+                    help="EP dispatch/combine: peer-memory scatter kernels (p2p), NCCL all_to_all, or p2p when "
+                         "every peer window opens (auto)")
     ap.add_argument("--raw", action="store_true",
                     help="page raw bf16 over PCIe (the reference host tier) instead of exponent-Huffman records")
     args = ap.parse_args()
@@ -408,7 +411,11 @@ def main():
     if use_ep:
         group = None
         runner = ExpertParallelRunner(spec, None, fwd, rank, world, device=dev, group=group, shard_pool=shard.pinned,
+                                      transport=args.transport,
                                       shared=shard.shared, host_codec=args.host_codec)
+        ep_transport = ("scatter kernels into peer windows over NVLink (CUDA IPC), epoch flags)"
+                        if runner.transport == "p2p" else "NCCL all_to_all)") + (
+                           f"; {runner.transport_note}" if runner.transport_note else "")
         shard_bytes = shard.spec.total_bytes + (shard.shared.total_bytes if shard.shared is not None else 0)
         m_dev = pinned_per_layer = 0
         if args.tiering == "device" and args.host_codec:
@@ -545,6 +552,8 @@ def main():
         sess.close()
         del sess  # the session holds the runner (and its HBM ring) alive
     e2e_elapsed = max_over_ranks(torch, world, e0.elapsed_time(e1) * 1e-3, dev)
+    if use_ep:
+        runner.close()  # peer windows: every rank unmaps, barrier, then frees its own
     e2e_value = T * e2e_steps * world / e2e_elapsed
     assert tuple(out.shape) == x_host.shape  # (deep synthetic stacks overflow by design)
 
@@ -643,7 +652,7 @@ def main():
     if not use_ep and raw_path is not None:
         line["raw_host_tier"] = raw_path
     if use_ep:
-        line["config"]["parallelism"] = f"ep{world} (experts sharded, NCCL all_to_all dispatch/combine)"
+        line["config"]["parallelism"] = f"ep{world} (experts sharded; dispatch/combine: {ep_transport}"
         line["config"]["tokens_per_rank"] = T
     if G_virt > 1:
         line["config"]["parallelism"] = (f"rank 0 of ep{G_virt}: experts {run_kw['expert_shard'][0] + 1}.."

@@ -1005,6 +1005,7 @@ struct Session {
   bool paged = false;
   std::vector<Step> sv;  // the flattened schedule: iterations x layers x windows
   int mat_next = 0;      // next step to materialize
+  bool builtin_compute = false;  // session_compute ran (its per-launch profile events exist)
 };
 
 static Session& session_of(Ctx* c) {
@@ -1066,6 +1067,7 @@ static void session_begin(Ctx* c, const xpgb_run_opts* o, float* acts) {
   ss.o = *o;
   build_schedule(c, ss, o->iterations);
   ss.mat_next = 0;
+  ss.builtin_compute = false;
   c->dec_n = 0;
   ss.fetch_delay.clear();
   ss.compute_delay.clear();
@@ -1156,6 +1158,7 @@ static void session_release(Ctx* c, int g, cudaStream_t s) {
 // the window's expert GEMMs; the layer's combine after its last window.
 static void session_compute(Ctx* c, int g) {
   Session& ss = session_of(c);
+  ss.builtin_compute = true;
   const xpgb_run_opts* o = &ss.o;
   const Step& st = ss.sv[g];
   const int it = st.it, layer = st.layer;
@@ -1268,7 +1271,7 @@ static void session_end(Ctx* c, xpgb_report* rep) {
     rep->gate_up_bytes = (long long)(a * c->s1 + r * c->H * 2 + r * c->F * 2);
     rep->down_bytes = (long long)(a * c->s2 + r * c->F * 2 + r * (double)c->H * 4 * std::max(1, rep->down_splits));
   }
-  if (o->profile && steps > 0 && o->tokens > 0) {
+  if (o->profile && ss.builtin_compute && steps > 0 && o->tokens > 0) {
     double gu = 0, dn = 0, aux = 0;
     for (int g = 0; g < steps; ++g) {
       float ms[6];
