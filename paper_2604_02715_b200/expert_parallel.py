@@ -164,6 +164,9 @@ class PeerExchange:
     FLAG_BYTES = 512  # int32 flags[16] at 0, the scatter's CTA counter at 256; rows from 512
 
     def __init__(self, rank: int, world: int, tokens: int, kk: int, hidden: int, group=None):
+        """Collective: every rank of the group must construct its PeerExchange together.  Any
+        rank's failure (allocation, IPC open) makes every rank raise, so the ranks never end
+        up on different transports."""
         import torch.distributed as dist
 
         self.rank, self.world, self.H = rank, world, hidden
@@ -172,23 +175,42 @@ class PeerExchange:
         self.xp_off = self.FLAG_BYTES
         self.ret_off = self.xp_off + ((self.in_rows * hidden * 2 + 255) // 256) * 256
         size = self.ret_off + self.ret_rows * hidden * 4
-        base = C.c_void_p()
+        self._own, self._opened, err = 0, [], None
         handle = (C.c_uint8 * 64)()
-        call("xpgb_ep_window_alloc", C.c_uint64(size), C.byref(base), handle)
-        self._own = base.value
-        handles = [None] * world
-        if world > 1:
-            dist.all_gather_object(handles, bytes(handle), group=group)
-        self._opened = []
+        try:
+            base = C.c_void_p()
+            call("xpgb_ep_window_alloc", C.c_uint64(size), C.byref(base), handle)
+            self._own = base.value
+        except Exception as exc:  # noqa: BLE001 -- reported to every rank below
+            err = f"rank {rank}: window alloc failed: {exc}"
+
+        def agree(mine):
+            if world == 1:
+                return [mine]
+            out = [None] * world
+            dist.all_gather_object(out, mine, group=group)
+            return out
+
+        handles = agree(bytes(handle) if err is None else None)
         bases = []
-        for r in range(world):
-            if r == rank:
-                bases.append(self._own)
-                continue
-            p = C.c_void_p()
-            call("xpgb_ep_window_open", (C.c_uint8 * 64).from_buffer_copy(handles[r]), C.byref(p))
-            self._opened.append(p.value)
-            bases.append(p.value)
+        if err is None and all(h is not None for h in handles):
+            try:
+                for r in range(world):
+                    if r == rank:
+                        bases.append(self._own)
+                        continue
+                    p = C.c_void_p()
+                    call("xpgb_ep_window_open", (C.c_uint8 * 64).from_buffer_copy(handles[r]), C.byref(p))
+                    self._opened.append(p.value)
+                    bases.append(p.value)
+            except Exception as exc:  # noqa: BLE001
+                err = f"rank {rank}: peer window open failed: {exc}"
+        elif err is None:
+            err = "a peer could not allocate its window"
+        errors = [e for e in agree(err) if e]
+        if errors:
+            self.close()
+            raise RuntimeError("; ".join(errors))
         self.bases = bases
         self._xp = (C.c_void_p * world)(*[b + self.xp_off for b in bases])
         self._ret = (C.c_void_p * world)(*[b + self.ret_off for b in bases])
