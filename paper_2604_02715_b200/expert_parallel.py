@@ -163,12 +163,14 @@ class PeerExchange:
 
     FLAG_BYTES = 512  # int32 flags[16] at 0, the scatter's CTA counter at 256; rows from 512
 
-    def __init__(self, rank: int, world: int, tokens: int, kk: int, hidden: int, group=None):
+    def __init__(self, rank: int, world: int, tokens: int, kk: int, hidden: int, group=None, device: int = 0):
         """Collective: every rank of the group must construct its PeerExchange together.  Any
         rank's failure (allocation, IPC open) makes every rank raise, so the ranks never end
         up on different transports."""
+        import torch
         import torch.distributed as dist
 
+        torch.cuda.set_device(device)  # the window and every launch belong to this rank's GPU
         self.rank, self.world, self.H = rank, world, hidden
         self.in_rows = world * tokens * kk           # worst case: every pair of the step lands here
         self.ret_rows = tokens * kk
@@ -431,7 +433,8 @@ class ExpertParallelRunner:
         if transport in ("p2p", "auto"):
             kk = min(fwd.top_k, spec.experts_per_layer)
             try:
-                self.peer = PeerExchange(rank, world, fwd.tokens_per_step, kk, spec.hidden_dim, group=group)
+                self.peer = PeerExchange(rank, world, fwd.tokens_per_step, kk, spec.hidden_dim, group=group,
+                                         device=device)
                 self.transport = "p2p"
             except Exception as exc:  # noqa: BLE001 -- auto falls back to the collective
                 if transport == "p2p":
