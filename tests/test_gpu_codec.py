@@ -191,3 +191,51 @@ def test_residency_plan_applied_stays_exact(X, budget):
     assert rep.final_activations.tobytes() == base.tobytes()
     hbm = runner.ctx.hbm_bytes()
     assert hbm["ring"] + hbm["device_tier"] <= budget * spec.total_bytes * 1.001
+
+
+@pytest.mark.parametrize("stage_buffers", [2, 3, 16])
+def test_staging_ring_sizes_exact_and_profiled(X, stage_buffers):
+    """Any staging-ring size (link run-ahead) pages in the same bytes; with profile on, every
+    decoder launch is timed on its own stream (xpgb_decode_stats) and its algorithmic bytes
+    cover what it produced."""
+    from paper_2604_02715_b200.errors import OutOfRangeError
+
+    spec = X.ModelSpec(4, 4, 128, 256)
+    fwd = X.ForwardSpec(8, 2, 3)
+    container, hier = _runner(X, spec, 3, None, True)
+    x = X.initial_activations(spec, fwd, 3)
+    runner = X.StreamedRunner(spec, hier, fwd, host_codec=True, stage_buffers=stage_buffers)
+    rep = runner.run(2, acts=x.copy(), profile=True)
+    base = X.resident_baseline(2, spec, container, fwd, acts=x.copy())
+    assert rep.violations == [] and rep.page_fault is None
+    assert rep.final_activations.tobytes() == base.tobytes()
+    st = runner.ctx.decode_stats()
+    assert st["launches"] > 0 and st["kernel_ns"] > 0
+    assert st["algo_bytes"] >= 1.5 * rep.decoded_bytes  # >= bf16 written + sign/mantissa read
+    with pytest.raises(OutOfRangeError):
+        runner.ctx.set_stage_buffers(1)
+    with pytest.raises(OutOfRangeError):
+        runner.ctx.set_stage_buffers(17)
+
+
+def test_lean_gemm_tiles_bit_identical(X):
+    """The lean GEMM tiles (one stage fewer, co-resident with decoder CTAs) change the
+    pipeline depth only: results are bit-identical to the full tiles."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, paper_2604_02715_b200 as X\n"
+        "spec = X.ModelSpec(3, 8, 256, 512); fwd = X.ForwardSpec(96, 2, 4)\n"
+        "c = X.generate_synthetic_model(spec, 4)\n"
+        "b = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 30e9, 1 << 40)]\n"
+        "h = X.StorageHierarchy(c, None, X.plan_placement(spec, b), b)\n"
+        "r = X.StreamedRunner(spec, h, fwd, host_codec=True, ring_experts=4).run(2, acts=X.initial_activations(spec, fwd, 4))\n"
+        "import sys; sys.stdout.buffer.write(np.ascontiguousarray(r.final_activations).tobytes())\n")
+    outs = []
+    for lean in ("0", "1"):
+        env = dict(__import__("os").environ, XPGB_COSCHED=lean)
+        root = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+        outs.append(subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, check=True,
+                                   timeout=300, cwd=root).stdout)
+    assert len(outs[0]) > 0 and outs[0] == outs[1]
