@@ -235,7 +235,9 @@ int xpgb_set_pinned(xpgb_ctx* ctx, const uint8_t* pinned_of);
  * compute event (the reference's WAR rule one window at a time), each window's GEMMs read only
  * its experts, and the layer's combine runs after its last window.  Re-creates the arena. */
 int xpgb_set_ring_experts(xpgb_ctx* ctx, int32_t ring_experts);
-/* Windows in flight on a sub-layer ring (2..6, default 2 = double buffering): the ring's
+/* Windows in flight on a sub-layer ring (1..6, default 2 = double buffering; 1 = the next
+ * window's decode waits for this window's compute, the link still runs ahead through the
+ * staging ring): the ring's
  * ring_experts blocks per kind hold `depth` windows of ring_experts/depth experts, and window
  * g recycles window g-depth, so the loads of the next depth-1 windows overlap the compute of
  * the current one (the reference's two-layer WAR rule, generalised).  Callers keep the

@@ -36,6 +36,7 @@ class ResidencyPlan:
     est_step_s: float         # modelled step time
     link_bytes: float         # host-tier record bytes per step
     depth: int = 2            # windows in flight on the ring (ring // depth experts each)
+    decode_bytes: float = 0.0  # raw bytes the GPU decoder produces per step
 
     @property
     def device_experts(self) -> int:
@@ -80,15 +81,28 @@ def _balanced(total: int, N: int):
 
 def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *, shared_bytes: float = 0.0,
                    b_link: float = 54e9, b_dec: float = 1100e9, t_compute: float = 0.0,
-                   min_window_bytes: float = 128 * 2**20, allow_pinned: bool = True, depth: int = 2,
+                   min_window_bytes: float = 128 * 2**20, allow_pinned: bool = True, depth: int | None = None,
                    window: int | None = None) -> ResidencyPlan:
     """Choose (ring, device tier, pinned) for N layers x L experts under `budget_bytes`.
 
     eb: raw bytes of one expert (both tensors); ceb: its compressed record bytes.
     Step model: max(link_bytes / b_link, decoded_raw_bytes / b_dec + t_compute).
     depth: windows in flight (the ring holds depth windows); window: experts per window
-    (default: enough for min_window_bytes).
+    (default: enough for min_window_bytes).  depth None: 1 when the plan is clearly
+    link-bound (link time >= 1.5x decode time: the ring's second window buys nothing while
+    the link is the bottleneck, and its bytes hold more device-tier experts -- Mixtral 50%:
+    +10%), else 2 (decode-bound plans need the decode of window g+1 to overlap window g's
+    compute -- DSv3 65%: depth 1 is 22% slower).
     """
+    if depth is None:
+        one = plan_residency(N, L, eb, ceb, budget_bytes, shared_bytes=shared_bytes, b_link=b_link, b_dec=b_dec,
+                             t_compute=t_compute, min_window_bytes=min_window_bytes, allow_pinned=allow_pinned,
+                             depth=1, window=window)
+        if one.ring and one.link_bytes / b_link >= 1.5 * one.decode_bytes / b_dec:
+            return one
+        return plan_residency(N, L, eb, ceb, budget_bytes, shared_bytes=shared_bytes, b_link=b_link, b_dec=b_dec,
+                              t_compute=t_compute, min_window_bytes=min_window_bytes, allow_pinned=allow_pinned,
+                              depth=2, window=window)
     total = N * L
     cap = budget_bytes - shared_bytes
     if window is None:
@@ -117,7 +131,7 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
         if best is None or key < best[0]:
             best = (key, p, d, ring, link)
     if best is None:
-        raise ValueError(f"budget {budget_bytes:.3g} B cannot hold a two-expert ring")
+        raise ValueError(f"budget {budget_bytes:.3g} B cannot hold a ring")
     (est, _), p, d, ring, link = best
     p_layer = _balanced(p, N)
     d_layer = _fill(d, [L - q for q in p_layer])
@@ -131,4 +145,4 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
         streamed = L - p_layer[l]
         device[l, :streamed] = _spread_row(streamed, d_layer[l], w)
     hbm = ring * eb + p * eb + device.sum() * ceb + shared_bytes
-    return ResidencyPlan(ring, device, pinned, float(hbm), float(est), float(link), depth)
+    return ResidencyPlan(ring, device, pinned, float(hbm), float(est), float(link), depth, float((total - p) * eb))

@@ -2070,7 +2070,7 @@ int xpgb_set_ring_depth(xpgb_ctx* h, int32_t depth) {
   return guard([&] {
     Ctx* c = &h->c;
     if (c->sess && c->sess->active) XFAIL(XPGB_ERR, "cannot change the ring depth during a session");
-    if (depth < 2 || depth > kMaxRingDepth) XFAIL(XPGB_ERR_OUT_OF_RANGE, "ring depth %d: need 2..%d", depth, kMaxRingDepth);
+    if (depth < 1 || depth > kMaxRingDepth) XFAIL(XPGB_ERR_OUT_OF_RANGE, "ring depth %d: need 1..%d", depth, kMaxRingDepth);
     if (c->ring_limit > 0 && c->ring_limit < depth)
       XFAIL(XPGB_ERR_OUT_OF_RANGE, "ring depth %d exceeds the ring of %d experts", depth, c->ring_limit);
     c->ring_depth = depth;

@@ -124,7 +124,7 @@ def test_layer_forward_through_page_table_faults_on_unmapped(X):
 @pytest.mark.parametrize("ring,pinned,host_codec,S,depth", [
     (2, None, False, 0, 2), (4, None, True, 0, 2), (6, None, False, 1, 2), (4, 3, True, 0, 2), (2, 5, False, 1, 2),
     (16, None, False, 0, 2), (3, None, True, 0, 3), (6, 2, False, 1, 3), (4, None, True, 0, 4), (16, None, False, 0, 3),
-    (5, 6, True, 0, 5)])
+    (5, 6, True, 0, 5), (2, None, True, 0, 1), (1, None, False, 1, 1), (3, 4, True, 0, 1)])
 def test_sub_layer_ring_windows_stay_exact(ring, pinned, host_codec, S, depth):
     """Budgets below two layers: the ring holds `ring` blocks per kind and each layer streams
     in windows of ring/depth experts, `depth` windows in flight; results stay bit-identical to
@@ -182,7 +182,7 @@ def test_ring_experts_argument_checks():
     with pytest.raises(OutOfRangeError):
         ctx.set_ring_experts(1)
     ctx.set_ring_experts(-1)
-    for bad in (1, 7):
+    for bad in (0, 7):
         with pytest.raises(OutOfRangeError):
             ctx.set_ring_depth(bad)
     ctx.set_ring_depth(3)

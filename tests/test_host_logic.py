@@ -241,9 +241,12 @@ def test_residency_plan_spends_the_budget():
         if prev is not None:
             assert pl.est_step_s <= prev + 1e-12  # more budget never slower
         prev = pl.est_step_s
-    pl = plan_residency(8, 8, eb, ceb, 0.25 * total)  # one 352 MB expert per window: ring of 2
+    pl = plan_residency(8, 8, eb, ceb, 0.25 * total)  # link-bound: one window in flight, ring of 1
+    assert pl.pinned_experts == 0 and pl.device_experts == 22 and pl.ring == 1 and pl.depth == 1
+    pl = plan_residency(8, 8, eb, ceb, 0.25 * total, depth=2)  # one 352 MB expert per window: ring of 2
     assert pl.pinned_experts == 0 and pl.device_experts == 21 and pl.ring == 2
-    pl = plan_residency(8, 8, eb, ceb, 0.25 * total, window=2)
+    assert plan_residency(8, 8, eb, ceb, 0.65 * total).depth == 2  # decode-bound: double-buffered
+    pl = plan_residency(8, 8, eb, ceb, 0.25 * total, window=2, depth=2)
     assert pl.pinned_experts == 0 and pl.device_experts == 18 and pl.ring == 4
     w = pl.ring // 2
     for l in range(8):  # windows of 2 experts: a device expert never shares a window with another

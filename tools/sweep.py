@@ -40,7 +40,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--raw", action="store_true")
-    ap.add_argument("--depth", type=int, default=2, help="budget: windows in flight on the planned ring")
+    ap.add_argument("--depth", type=int, default=None, help="budget: windows in flight on the planned ring (default: the planner picks 1 or 2)")
     ap.add_argument("--window", type=int, default=None, help="budget: experts per ring window")
     ap.add_argument("--stage-bufs", type=int, default=None, help="staging buffers per kind (host codec)")
     ap.add_argument("--rings", default="6,8,12", help="sub-layer ring sizes (expert blocks per kind) for budget")
