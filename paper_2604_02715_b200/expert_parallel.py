@@ -453,6 +453,7 @@ class ExpertParallelRunner:
             if self.world > 1:
                 dist.barrier(group=self.moe.group)
             peer.close()
+            self.transport = "nccl"  # later runs fall back to the collective
 
     def device_tier_bytes(self, m: int) -> int:
         from ._lib import lib
