@@ -300,15 +300,17 @@ __device__ __forceinline__ void decode_chunk(R& q, uint64_t win, int avail, cons
       uint64_t cur = b0, carry = 0;
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
-        while (np < 8) {
-          if (avail < 32) {
-            win |= (uint64_t)q.pop() << (32 - avail);
-            avail += 32;
-          }
+        // one lookup: the fast path needs kMultiBits valid bits, the canonical path (codes
+        // longer than the table) refills to >= 32 first
+        auto step = [&]() {
           const uint32_t e = lut3[win >> (64 - kMultiBits)];
           int k = (e >> 24) & 3, l;
           uint64_t bytes;
           if (__builtin_expect(k == 0, 0)) {
+            if (avail < 32) {
+              win |= (uint64_t)q.pop() << (32 - avail);
+              avail += 32;
+            }
             int sym = 0;
             l = canon_decode(win, ml, count, first_code, first_rank, sorted_sym, &sym);
             bytes = (uint32_t)sym;
@@ -323,6 +325,17 @@ __device__ __forceinline__ void decode_chunk(R& q, uint64_t win, int avail, cons
           cur |= bytes << sh;
           carry |= np > 5 ? bytes >> (64 - sh) : 0ull;
           np += k;
+        };
+        while (np < 8) {
+          // one refill per up to three lookups: after it avail >= 32, the first lookup
+          // leaves >= 21 bits, and each further one runs while kMultiBits remain
+          if (avail < 32) {
+            win |= (uint64_t)q.pop() << (32 - avail);
+            avail += 32;
+          }
+          step();
+          if (np < 8 && avail >= kMultiBits) step();
+          if (np < 8 && avail >= kMultiBits) step();
         }
         h[half] = cur;
         cur = carry;
