@@ -1,6 +1,8 @@
 // Exponent-Huffman codec: multi-threaded host encoder (bit-identical to
 // xpg codec.py:235-272) and the sm_100a decoder kernel (codec.py:275-330).
 #include <algorithm>
+#include <cstring>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -137,12 +139,13 @@ int codec_build_index(const uint8_t* bits, size_t bits_len, size_t n, const uint
 
 // ----------------------------------------------------------------------------- GPU decoder
 
+struct DecTables;
 struct DecodeParams {
   DecodeTensor t[kMaxDecodeTensors];  // tensors of one launch, each n values
   int ntensors;
   uint64_t n;
   int chunk;
-  CodecTable table;
+  const DecTables* tabs;  // prebuilt by k_build_tables
 };
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
@@ -198,8 +201,19 @@ __device__ __forceinline__ void decode_chunk(R& q, uint64_t win, int avail, cons
                                              int ml, const int* count, const uint32_t* first_code,
                                              const int* first_rank, const uint8_t* sorted_sym);
 
-__global__ void __launch_bounds__(256) k_exp_decode(const __grid_constant__ DecodeParams p) {
-  __shared__ uint32_t lut3[1 << kMultiBits];  // syms (3 x 8 b) | count << 24 | total length << 26
+// Decode tables of one codec table, built once by k_build_tables and copied into every
+// decoder CTA's shared memory (building them per CTA cost ~20 us per launch -- most of a
+// small tensor's decode).
+struct DecTables {
+  uint32_t lut3[1 << kMultiBits];  // syms (3 x 8 b) | count << 24 | total length << 26
+  uint32_t first_code[kCodecMaxLen + 1];
+  int count[kCodecMaxLen + 1], first_rank[kCodecMaxLen + 1];
+  uint8_t sorted_sym[kCodecSymbols];
+  int maxlen;
+};
+
+__global__ void __launch_bounds__(256) k_build_tables(const CodecTable table, DecTables* out) {
+  __shared__ uint32_t lut3[1 << kMultiBits];
   __shared__ uint32_t first_code[kCodecMaxLen + 1];
   __shared__ int count[kCodecMaxLen + 1], first_rank[kCodecMaxLen + 1];
   __shared__ uint8_t sorted_sym[kCodecSymbols];
@@ -207,7 +221,7 @@ __global__ void __launch_bounds__(256) k_exp_decode(const __grid_constant__ Deco
   const int tid = threadIdx.x;
   if (tid <= kCodecMaxLen) count[tid] = 0;
   __syncthreads();
-  if (tid < kCodecSymbols && p.table.len[tid]) atomicAdd(&count[p.table.len[tid]], 1);
+  if (tid < kCodecSymbols && table.len[tid]) atomicAdd(&count[table.len[tid]], 1);
   __syncthreads();
   if (tid == 0) {
     uint32_t code = 0;
@@ -228,10 +242,10 @@ __global__ void __launch_bounds__(256) k_exp_decode(const __grid_constant__ Deco
   }
   __syncthreads();
   if (tid < kCodecSymbols) {
-    const int l = p.table.len[tid];
+    const int l = table.len[tid];
     if (l) {
       int r = 0;
-      for (int s = 0; s < tid; ++s) r += (p.table.len[s] == l);
+      for (int s = 0; s < tid; ++s) r += (table.len[s] == l);
       sorted_sym[first_rank[l] + r] = (uint8_t)tid;
     }
   }
@@ -253,6 +267,37 @@ __global__ void __launch_bounds__(256) k_exp_decode(const __grid_constant__ Deco
     }
     lut3[i] = syms | ((uint32_t)c << 24) | ((uint32_t)tot << 26);
   }
+  __syncthreads();
+
+  for (int i = tid; i < (1 << kMultiBits); i += blockDim.x) out->lut3[i] = lut3[i];
+  if (tid <= kCodecMaxLen) {
+    out->first_code[tid] = first_code[tid];
+    out->count[tid] = count[tid];
+    out->first_rank[tid] = first_rank[tid];
+  }
+  if (tid < kCodecSymbols) out->sorted_sym[tid] = sorted_sym[tid];
+  if (tid == 0) out->maxlen = maxlen;
+}
+
+__global__ void __launch_bounds__(256) k_exp_decode(const __grid_constant__ DecodeParams p) {
+  __shared__ uint32_t lut3[1 << kMultiBits];
+  __shared__ uint32_t first_code[kCodecMaxLen + 1];
+  __shared__ int count[kCodecMaxLen + 1], first_rank[kCodecMaxLen + 1];
+  __shared__ uint8_t sorted_sym[kCodecSymbols];
+  const int tid = threadIdx.x;
+  {
+    const DecTables* t = p.tabs;
+    const uint4* src = reinterpret_cast<const uint4*>(t->lut3);
+    uint4* dst = reinterpret_cast<uint4*>(lut3);
+    for (int i = tid; i < (1 << kMultiBits) / 4; i += blockDim.x) dst[i] = src[i];
+    if (tid <= kCodecMaxLen) {
+      first_code[tid] = t->first_code[tid];
+      count[tid] = t->count[tid];
+      first_rank[tid] = t->first_rank[tid];
+    }
+    if (tid < kCodecSymbols) sorted_sym[tid] = t->sorted_sym[tid];
+  }
+  const int ml = p.tabs->maxlen;
   __syncthreads();
 
   const uint64_t n = p.n;
@@ -411,6 +456,32 @@ void launch_exp_decode(const uint8_t* sm, const uint32_t* bits, const uint32_t* 
   launch_exp_decode_multi(&t, 1, n, chunk, table, s);
 }
 
+// Device tables per (device, codec table), built once on first use (synchronously, so a
+// decode on any stream may read them) and kept for the process.
+static const DecTables* decode_tables(const CodecTable& table, cudaStream_t s) {
+  struct Entry {
+    int dev;
+    CodecTable t;
+    DecTables* d;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  for (const Entry& e : cache)
+    if (e.dev == dev && memcmp(e.t.len, table.len, sizeof(table.len)) == 0) return e.d;
+  DecTables* d = nullptr;
+  if (cudaMalloc(&d, sizeof(DecTables)) != cudaSuccess) return nullptr;
+  k_build_tables<<<1, 256, 0, s>>>(table, d);
+  note_launch();
+  if (cudaStreamSynchronize(s) != cudaSuccess) return nullptr;
+  cache.push_back(Entry{dev, table, d});
+  return d;
+}
+
+void prepare_decode_tables(const CodecTable& table, cudaStream_t s) { decode_tables(table, s); }
+
 void launch_exp_decode_multi(const DecodeTensor* tensors, int ntensors, uint64_t n, int chunk, const CodecTable& table,
                              cudaStream_t s) {
   if (n == 0 || ntensors <= 0) return;
@@ -418,7 +489,8 @@ void launch_exp_decode_multi(const DecodeTensor* tensors, int ntensors, uint64_t
   p.ntensors = ntensors;
   p.n = n;
   p.chunk = chunk;
-  p.table = table;
+  p.tabs = decode_tables(table, s);
+  if (!p.tabs) return;  // the caller's CKLAUNCH reports the CUDA error
   for (int i = 0; i < ntensors; ++i) p.t[i] = tensors[i];
   const uint64_t n_chunks = ((n + chunk - 1) / chunk) * (uint64_t)ntensors;
   // one resident wave, grid-striding over the chunks: a second partial wave left the

@@ -1398,6 +1398,8 @@ static void set_codec(Ctx* c, const void* pool, uint64_t pool_bytes, const uint6
   c->rec_off.assign(rec_offsets, rec_offsets + nt);
   c->rec_bits.assign(bits_lens, bits_lens + nt);
   memcpy(c->ctab.len, lengths, kCodecSymbols);
+  prepare_decode_tables(c->ctab, nullptr);  // decoder tables built once, before any decode stream uses them
+  CKLAUNCH();
   c->cchunk = chunk;
   c->codec = true;
   c->host_codec = host_compressed;
