@@ -2296,8 +2296,12 @@ static void experts_forward_range(Ctx* c, int layer, const void* rows_dev, const
   if (n_rows == 0) return;
   // the layer's rows arrive once, with its first window; later windows reuse them
   if (e0 == 0) CK(cudaMemcpyAsync(c->xp, rows_dev, (size_t)n_rows * c->H * 2, cudaMemcpyDeviceToDevice, s));
-  const int bn = pick_bn_rows((double)n_rows / std::max(1, c->E));
-  const int splits = pick_splits(c, n_rows, 1, bn);  // same for every window of the layer
+  const double per_group = (double)n_rows / std::max(1, c->E);
+  const int bn = pick_bn_rows(per_group);
+  // an EP owner receives every rank's rows for its experts: groups of >= 128 rows run on
+  // CTA pairs, exactly as in enqueue_window
+  const bool pair = pair_gemm_supported(c->H, c->F) && (c->pair_mode == 1 || (c->pair_mode < 0 && per_group >= 128.0));
+  const int splits = pair ? 1 : pick_splits(c, n_rows, 1, bn);  // same for every window of the layer
   GemmParams pg = gemm_params(c, layer, 1, offsets_dev, 1, false), pd = gemm_params(c, layer, 2, offsets_dev, splits, false);
   pd.split_stride = (long long)n_rows * c->H;
   for (GemmParams* p : {&pg, &pd}) {  // window: groups [e0, e1), rows stay absolute
@@ -2306,9 +2310,15 @@ static void experts_forward_range(Ctx* c, int layer, const void* rows_dev, const
     p->e_first += e0;
     p->E = p->E_routed = e1 - e0;
   }
-  launch_gate_up(c->map_gu, c->map_xp, c->map_gu, pg, bn, c->num_sms, s);
+  if (pair)
+    launch_gemm_pair(true, c->map_xp_pair, c->map_gu, c->map_gu, pg, c->num_sms, s);
+  else
+    launch_gate_up(c->map_gu, c->map_xp, c->map_gu, pg, bn, c->num_sms, s, lean_gemm(c));
   CKLAUNCH();
-  launch_down(c->map_dn, c->map_h, c->map_dn, pd, bn, c->num_sms, s);
+  if (pair)
+    launch_gemm_pair(false, c->map_h_pair, c->map_dn, c->map_dn, pd, c->num_sms, s);
+  else
+    launch_down(c->map_dn, c->map_h, c->map_dn, pd, bn, c->num_sms, s, lean_gemm(c));
   CKLAUNCH();
   if (reduce) {  // after the layer's last window: every row's split-K partials are final
     launch_reduce_rows(c->part, c->d_fault, out_dev, n_rows, c->H, splits, pd.split_stride, s);

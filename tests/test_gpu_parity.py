@@ -242,6 +242,25 @@ def test_expert_parallel_runner_world1_matches_resident(X, O, shared, host_codec
     assert O.rel_l2(rep.final_activations.cpu().numpy(), base) <= 1e-3
 
 
+@pytest.mark.parametrize("tokens,pair", [(1024, None), (96, "1")])
+def test_expert_parallel_runner_pair_gemm(X, O, monkeypatch, tokens, pair):
+    """EP owners with prefill-sized groups (>= 128 rows per expert) run the CTA-pair GEMMs
+    in experts_forward_range (forced on for a small batch too)."""
+    from paper_2604_02715_b200.expert_parallel import ExpertParallelRunner
+
+    if pair is not None:
+        monkeypatch.setenv("XPGB_PAIR_GEMM", pair)
+    spec = X.ModelSpec(2, 8, 256, 512)
+    fwd = X.ForwardSpec(tokens, 2, 5)
+    container = X.generate_synthetic_model(spec, 5)
+    x = X.initial_activations(spec, fwd, 5)
+    runner = ExpertParallelRunner(spec, container, fwd, rank=0, world=1, host_codec=True)
+    rep = runner.run(1, x)
+    assert rep.page_fault is None and rep.violations == []
+    base = X.resident_baseline(1, spec, container, fwd, acts=x.copy())
+    assert O.rel_l2(rep.final_activations.cpu().numpy(), base) <= 1e-3
+
+
 def test_expert_parallel_runner_windows_and_device_tier(X, O):
     """EP runner on a budget plan: sub-layer ring windows (experts_forward_range per window,
     dispatch before the first, combine after the last) + compressed device tier + pinned."""
