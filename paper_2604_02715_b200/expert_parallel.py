@@ -478,7 +478,8 @@ class ExpertParallelRunner:
             self.ctx.set_pinned(full)
         streamed = count - plan.pinned_mask.sum(axis=1).min()
         depth = getattr(plan, "depth", 2)
-        if 0 < plan.ring < depth * streamed:
+        # a ring below the reference's two layers, or any ring with one window in flight
+        if 0 < plan.ring and (plan.ring < 2 * streamed or depth != 2):
             self.ctx.set_ring_depth(depth)
             self.ctx.set_ring_experts(int(plan.ring))
         shard_map = np.repeat(plan.device_mask[:, :, None], 2, axis=2).astype(np.uint8)

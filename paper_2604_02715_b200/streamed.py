@@ -310,7 +310,8 @@ class StreamedRunner:
             self.ctx.set_pinned(full)
         streamed = spec.experts_per_layer - plan.pinned_mask.sum(axis=1).min()
         depth = getattr(plan, "depth", 2)
-        if 0 < plan.ring < depth * streamed:
+        # a ring below the reference's two layers, or any ring with one window in flight
+        if 0 < plan.ring and (plan.ring < 2 * streamed or depth != 2):
             self.ctx.set_ring_depth(depth)
             self.ctx.set_ring_experts(int(plan.ring))
         self.set_device_mask(plan.device_mask)

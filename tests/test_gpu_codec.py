@@ -193,6 +193,28 @@ def test_residency_plan_applied_stays_exact(X, budget):
     assert hbm["ring"] + hbm["device_tier"] <= budget * spec.total_bytes * 1.001
 
 
+@pytest.mark.parametrize("L,budget", [(1, 0.25), (2, 0.3), (2, 0.7)])
+def test_residency_plan_whole_layer_windows(X, L, budget):
+    """Plans whose window is a whole layer (an EP rank with 1-2 experts per layer): a ring of
+    one layer at depth 1 or two at depth 2, applied and run exactly, within budget."""
+    from paper_2604_02715_b200.budget import plan_residency
+
+    spec = X.ModelSpec(4, L, 128, 256)
+    fwd = X.ForwardSpec(8, min(2, L), 3)
+    container, hier = _runner(X, spec, 3, None, True)
+    runner = X.StreamedRunner(spec, hier, fwd, host_codec=True)
+    ceb = runner.device_tier_bytes(L) / (4 * L) * 1.002
+    plan = plan_residency(4, L, spec.expert_bytes, ceb, budget * spec.total_bytes)
+    runner.apply_plan(plan)
+    x = X.initial_activations(spec, fwd, 3)
+    rep = runner.run(2, acts=x.copy())
+    base = X.resident_baseline(2, spec, container, fwd, acts=x.copy())
+    assert rep.violations == [] and rep.page_fault is None
+    assert rep.final_activations.tobytes() == base.tobytes()
+    hbm = runner.ctx.hbm_bytes()
+    assert hbm["ring"] + hbm["device_tier"] <= budget * spec.total_bytes * 1.001
+
+
 @pytest.mark.parametrize("stage_buffers", [2, 3, 16])
 def test_staging_ring_sizes_exact_and_profiled(X, stage_buffers):
     """Any staging-ring size (link run-ahead) pages in the same bytes; with profile on, every
