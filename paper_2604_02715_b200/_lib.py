@@ -13,7 +13,7 @@ import os
 from .errors import XpgError, raise_for_status
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libxpgb.so")
+LIB_PATH = os.environ.get("XPGB_LIB_PATH") or os.path.join(_HERE, "libxpgb.so")  # override: A/B builds
 
 # ---- enums (mirror include/xpgb.h)
 POOL_RING = 0

@@ -1,0 +1,6 @@
+#!/bin/bash
+O=gpurun_out/t76; mkdir -p $O
+for r in 1 2 3; do for v in cur pre_sh; do
+  if [ $v = cur ]; then unset XPGB_LIB_PATH; else export XPGB_LIB_PATH=tools/micro/ab/$v/libxpgb.so; fi
+  for n in 117440512 14680064; do echo -n "$v n=$n "; timeout 120 python tools/profile_codec.py --values $n --chunk 256 --reps 30 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['out_GBps'],1))"; done
+done; done | tee $O/ab.txt

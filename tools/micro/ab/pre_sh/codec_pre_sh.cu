@@ -1,0 +1,510 @@
+// Exponent-Huffman codec: multi-threaded host encoder (bit-identical to
+// xpg codec.py:235-272) and the sm_100a decoder kernel (codec.py:275-330).
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "codec.cuh"
+#include "launch_count.h"
+
+namespace xpgb {
+
+bool codec_canonical_codes(const uint8_t* lengths, uint32_t* codes) {
+  // canonical order (length, symbol) ascending, as HuffmanTable.from_lengths (codec.py:152-173)
+  double kraft = 0.0;
+  int present = 0;
+  for (int s = 0; s < kCodecSymbols; ++s) {
+    codes[s] = 0;
+    if (lengths[s] > kCodecMaxLen) return false;
+    if (lengths[s]) {
+      kraft += 1.0 / (double)(1ull << lengths[s]);
+      ++present;
+    }
+  }
+  if (!present || kraft > 1.0 + 1e-12) return false;
+  uint64_t code = 0;
+  int prev = 0;
+  for (int l = 1; l <= kCodecMaxLen; ++l)
+    for (int s = 0; s < kCodecSymbols; ++s)
+      if (lengths[s] == l) {
+        code <<= (l - prev);
+        codes[s] = (uint32_t)code;
+        code += 1;
+        prev = l;
+      }
+  return true;
+}
+
+void codec_histogram(const uint8_t* data, size_t bytes, uint64_t* counts, int threads) {
+  const size_t n = bytes / 2;
+  threads = std::max(1, std::min(threads, (int)std::max<size_t>(1, n / (1 << 20))));
+  std::vector<std::vector<uint64_t>> part(threads, std::vector<uint64_t>(kCodecSymbols, 0));
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([&, t] {
+      const size_t a = n * t / threads, b = n * (t + 1) / threads;
+      const uint16_t* w = reinterpret_cast<const uint16_t*>(data);
+      uint64_t* c = part[t].data();
+      for (size_t i = a; i < b; ++i) ++c[(w[i] >> 7) & 0xFF];
+    });
+  for (auto& th : pool) th.join();
+  for (int s = 0; s < kCodecSymbols; ++s) {
+    uint64_t v = 0;
+    for (int t = 0; t < threads; ++t) v += part[t][s];
+    counts[s] = v;
+  }
+}
+
+size_t codec_bits_bound(size_t n, const uint8_t* lengths) {
+  int mx = 0;
+  for (int s = 0; s < kCodecSymbols; ++s) mx = std::max<int>(mx, lengths[s]);
+  return (n * (size_t)mx + 7) / 8;
+}
+
+bool codec_encode(const uint16_t* words, size_t n, const uint8_t* lengths, const uint32_t* codes, uint8_t* sm_out,
+                  uint8_t* bits_out, size_t bits_cap, size_t* bits_len, uint64_t* bit_count, uint32_t* index_out,
+                  int chunk, int* missing) {
+  uint64_t acc = 0;
+  int nacc = 0;
+  size_t out = 0;
+  uint64_t total = 0;
+  for (size_t i = 0; i < n; ++i) {
+    const uint16_t w = words[i];
+    const int e = (w >> 7) & 0xFF;
+    const int l = lengths[e];
+    if (!l) {
+      if (missing) *missing = e;
+      return false;
+    }
+    if (index_out && chunk > 0 && (i % (size_t)chunk) == 0) index_out[i / chunk] = (uint32_t)total;
+    sm_out[i] = (uint8_t)(((w >> 8) & 0x80) | (w & 0x7F));
+    acc = (acc << l) | codes[e];
+    nacc += l;
+    total += l;
+    while (nacc >= 8) {
+      nacc -= 8;
+      if (out < bits_cap) bits_out[out] = (uint8_t)(acc >> nacc);
+      ++out;
+    }
+    acc &= (nacc ? ((1ull << nacc) - 1) : 0ull);
+  }
+  if (nacc) {
+    if (out < bits_cap) bits_out[out] = (uint8_t)(acc << (8 - nacc));
+    ++out;
+  }
+  *bits_len = out;
+  *bit_count = total;
+  if (missing) *missing = -1;
+  return out <= bits_cap && total < (1ull << 32);
+}
+
+// Sequential host scan of a stream: rebuilds the chunk index and validates it the way
+// decompress() does (codec.py:304-327).  Returns 0, 1 = truncated, 2 = invalid code.
+int codec_build_index(const uint8_t* bits, size_t bits_len, size_t n, const uint8_t* lengths, int chunk,
+                      uint32_t* index_out, size_t* consumed_bits) {
+  int count[kCodecMaxLen + 1] = {0};
+  uint32_t first_code[kCodecMaxLen + 1] = {0};
+  for (int s = 0; s < kCodecSymbols; ++s)
+    if (lengths[s]) ++count[lengths[s]];
+  uint32_t code = 0;
+  int prev = 0, maxlen = 0;
+  for (int l = 1; l <= kCodecMaxLen; ++l)
+    if (count[l]) {
+      code <<= (l - prev);
+      first_code[l] = code;
+      code += count[l];
+      prev = l;
+      maxlen = l;
+    }
+  const uint64_t total_bits = (uint64_t)bits_len * 8;
+  uint64_t pos = 0;
+  for (size_t i = 0; i < n; ++i) {
+    if (index_out && (i % (size_t)chunk) == 0) index_out[i / chunk] = (uint32_t)pos;
+    uint32_t c = 0;
+    int l = 0;
+    for (;;) {
+      if (pos >= total_bits) return 1;
+      c = (c << 1) | ((bits[pos >> 3] >> (7 - (pos & 7))) & 1);
+      ++pos;
+      ++l;
+      if (l > maxlen) return 2;
+      if (count[l] && c - first_code[l] < (uint32_t)count[l]) break;
+    }
+  }
+  if (consumed_bits) *consumed_bits = pos;
+  return 0;
+}
+
+// ----------------------------------------------------------------------------- GPU decoder
+
+struct DecTables;
+struct DecodeParams {
+  DecodeTensor t[kMaxDecodeTensors];  // tensors of one launch, each n values
+  int ntensors;
+  uint64_t n;
+  int chunk;
+  const DecTables* tabs;  // prebuilt by k_build_tables
+};
+
+__device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
+
+// One thread decodes one chunk (`chunk` values) starting at index[c]: a 64-bit
+// MSB-first window and a multi-symbol table -- every 11-bit pattern maps to the
+// up-to-3 whole codewords it starts with (exponents average ~2.6 bits, so one
+// lookup usually yields 3 values).  Codes longer than the table, and a chunk's
+// last values (never decode past the chunk), take the canonical first-code search.
+// The table is 8 KB of shared memory so decode blocks still fit beside a resident
+// GEMM CTA; the next bitstream word is always in flight.  Output words are
+// (sign << 15) | (exponent << 7) | mantissa, 16 per 32-byte store.
+constexpr int kMultiBits = 11;
+
+__device__ __forceinline__ int canon_decode(uint64_t win, int ml, const int* count, const uint32_t* first_code,
+                                            const int* first_rank, const uint8_t* sorted_sym, int* sym) {
+  for (int l = 1; l <= ml; ++l) {
+    const uint32_t code = (uint32_t)(win >> (64 - l));
+    if (count[l] && code - first_code[l] < (uint32_t)count[l]) {
+      *sym = sorted_sym[first_rank[l] + (code - first_code[l])];
+      return l;
+    }
+  }
+  return 0;  // invalid code: the host index scan rejects such streams before they get here
+}
+
+// Eight (sign/mantissa, exponent) byte pairs -> bf16 words by byte permutes:
+// x = [e1 s1 e0 s0] per 16-bit lane -> (s >> 7) << 15 | e << 7 | (s & 0x7F).
+__device__ __forceinline__ uint32_t pack_words(uint32_t sm4, uint32_t ex4, uint32_t sel) {
+  const uint32_t x = __byte_perm(sm4, ex4, sel);
+  return ((x >> 1) & 0x7F807F80u) | (x & 0x007F007Fu) | ((x << 8) & 0x80008000u);
+}
+
+// Bitstream words for one chunk, the next one always in flight.  (16-byte loads with a
+// second in flight measured slower: 726 vs 951 GB/s.)
+struct WordScalar {
+  const uint32_t* wp;
+  uint32_t nxt;
+  __device__ __forceinline__ void init(const uint32_t* p) {
+    wp = p;
+    nxt = *wp++;
+  }
+  __device__ __forceinline__ uint32_t pop() {
+    const uint32_t r = nxt;
+    nxt = *wp++;
+    return bswap32(r);
+  }
+};
+
+template <bool FAST, class R>
+__device__ __forceinline__ void decode_chunk(R& q, uint64_t win, int avail, const uint8_t* __restrict__ sm,
+                                             uint16_t* __restrict__ out, uint64_t v0, uint64_t v1, const uint32_t* lut3,
+                                             int ml, const int* count, const uint32_t* first_code,
+                                             const int* first_rank, const uint8_t* sorted_sym);
+
+// Decode tables of one codec table, built once by k_build_tables and copied into every
+// decoder CTA's shared memory (building them per CTA cost ~20 us per launch -- most of a
+// small tensor's decode).
+struct DecTables {
+  uint32_t lut3[1 << kMultiBits];  // syms (3 x 8 b) | count << 24 | total length << 26
+  uint32_t first_code[kCodecMaxLen + 1];
+  int count[kCodecMaxLen + 1], first_rank[kCodecMaxLen + 1];
+  uint8_t sorted_sym[kCodecSymbols];
+  int maxlen;
+};
+
+__global__ void __launch_bounds__(256) k_build_tables(const CodecTable table, DecTables* out) {
+  __shared__ uint32_t lut3[1 << kMultiBits];
+  __shared__ uint32_t first_code[kCodecMaxLen + 1];
+  __shared__ int count[kCodecMaxLen + 1], first_rank[kCodecMaxLen + 1];
+  __shared__ uint8_t sorted_sym[kCodecSymbols];
+  __shared__ int maxlen;
+  const int tid = threadIdx.x;
+  if (tid <= kCodecMaxLen) count[tid] = 0;
+  __syncthreads();
+  if (tid < kCodecSymbols && table.len[tid]) atomicAdd(&count[table.len[tid]], 1);
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t code = 0;
+    int prev = 0, rank = 0, ml = 0;
+    for (int l = 1; l <= kCodecMaxLen; ++l) {
+      first_rank[l] = rank;
+      first_code[l] = 0;
+      if (count[l]) {
+        code <<= (l - prev);
+        first_code[l] = code;
+        code += count[l];
+        prev = l;
+        rank += count[l];
+        ml = l;
+      }
+    }
+    maxlen = ml;
+  }
+  __syncthreads();
+  if (tid < kCodecSymbols) {
+    const int l = table.len[tid];
+    if (l) {
+      int r = 0;
+      for (int s = 0; s < tid; ++s) r += (table.len[s] == l);
+      sorted_sym[first_rank[l] + r] = (uint8_t)tid;
+    }
+  }
+  __syncthreads();
+  const int ml = maxlen;
+  // whole codes at the head of every 11-bit pattern: a code is whole when its length
+  // fits the known bits (a prefix code is decided by its own bits only)
+  for (int i = tid; i < (1 << kMultiBits); i += blockDim.x) {
+    const uint64_t w = (uint64_t)i << (64 - kMultiBits);
+    uint32_t syms = 0;
+    int tot = 0, c = 0;
+    while (c < 3) {
+      int sym;
+      const int l = canon_decode(w << tot, ml, count, first_code, first_rank, sorted_sym, &sym);
+      if (!l || tot + l > kMultiBits) break;
+      syms |= (uint32_t)sym << (8 * c);
+      tot += l;
+      ++c;
+    }
+    lut3[i] = syms | ((uint32_t)c << 24) | ((uint32_t)tot << 26);
+  }
+  __syncthreads();
+
+  for (int i = tid; i < (1 << kMultiBits); i += blockDim.x) out->lut3[i] = lut3[i];
+  if (tid <= kCodecMaxLen) {
+    out->first_code[tid] = first_code[tid];
+    out->count[tid] = count[tid];
+    out->first_rank[tid] = first_rank[tid];
+  }
+  if (tid < kCodecSymbols) out->sorted_sym[tid] = sorted_sym[tid];
+  if (tid == 0) out->maxlen = maxlen;
+}
+
+__global__ void __launch_bounds__(256) k_exp_decode(const __grid_constant__ DecodeParams p) {
+  __shared__ uint32_t lut3[1 << kMultiBits];
+  __shared__ uint32_t first_code[kCodecMaxLen + 1];
+  __shared__ int count[kCodecMaxLen + 1], first_rank[kCodecMaxLen + 1];
+  __shared__ uint8_t sorted_sym[kCodecSymbols];
+  const int tid = threadIdx.x;
+  {
+    const DecTables* t = p.tabs;
+    const uint4* src = reinterpret_cast<const uint4*>(t->lut3);
+    uint4* dst = reinterpret_cast<uint4*>(lut3);
+    for (int i = tid; i < (1 << kMultiBits) / 4; i += blockDim.x) dst[i] = src[i];
+    if (tid <= kCodecMaxLen) {
+      first_code[tid] = t->first_code[tid];
+      count[tid] = t->count[tid];
+      first_rank[tid] = t->first_rank[tid];
+    }
+    if (tid < kCodecSymbols) sorted_sym[tid] = t->sorted_sym[tid];
+  }
+  const int ml = p.tabs->maxlen;
+  __syncthreads();
+
+  const uint64_t n = p.n;
+  const uint64_t cpt = (n + p.chunk - 1) / p.chunk;  // chunks per tensor
+  const uint64_t n_chunks = cpt * (uint64_t)p.ntensors;
+  for (uint64_t gc = blockIdx.x * (uint64_t)blockDim.x + tid; gc < n_chunks; gc += (uint64_t)gridDim.x * blockDim.x) {
+    const int ti = (int)(gc / cpt);
+    const uint64_t c = gc - (uint64_t)ti * cpt;
+    const DecodeTensor& d = p.t[ti];
+    const uint8_t* __restrict__ sm = d.sm;
+    uint16_t* __restrict__ out = d.out;
+    const uint64_t v0 = c * p.chunk;
+    const uint64_t v1 = (v0 + p.chunk < n) ? v0 + p.chunk : n;
+    const uint32_t bitpos = d.index[c] - d.bit_base;
+    const uint32_t w = bitpos >> 5, sh = bitpos & 31;
+    uint64_t win = (((uint64_t)bswap32(d.bits[w]) << 32) | bswap32(d.bits[w + 1])) << sh;
+    int avail = 64 - (int)sh;
+    WordScalar q;
+    q.init(d.bits + w + 2);
+    decode_chunk<true>(q, win, avail, sm, out, v0, v1, lut3, ml, count, first_code, first_rank, sorted_sym);
+  }
+}
+
+template <bool FAST, class R>
+__device__ __forceinline__ void decode_chunk(R& q, uint64_t win, int avail, const uint8_t* __restrict__ sm,
+                                             uint16_t* __restrict__ out, uint64_t v0, uint64_t v1, const uint32_t* lut3,
+                                             int ml, const int* count, const uint32_t* first_code,
+                                             const int* first_rank, const uint8_t* sorted_sym) {
+  // exponent bytes decoded but not yet written: b0 = values 0..7 of the group, b1 = 8..15,
+  // b2 = the spill of a multi-symbol lookup past the group
+  uint64_t b0 = 0, b1 = 0, b2 = 0;
+  int np = 0;
+  const bool wide = ((reinterpret_cast<uintptr_t>(out + v0) | reinterpret_cast<uintptr_t>(sm + v0)) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(out + v0) & 31) == 0;
+  for (uint64_t v = v0; v < v1; v += 16) {
+    const int cnt = (int)((v1 - v) < 16 ? (v1 - v) : 16);
+    uint4 smv = make_uint4(0, 0, 0, 0);
+    if (cnt == 16 && wide) smv = *reinterpret_cast<const uint4*>(sm + v);
+    if (FAST && cnt == 16 && wide) {
+      // a whole group: two halves of 8 exponent bytes, each a 64-bit register filled at
+      // byte 8*np; a multi-symbol lookup that crosses the half spills into `carry`.  A
+      // lookup may run up to 2 symbols past the chunk (never written): they come from
+      // the next chunk's bits or the stream's 8-byte look-ahead padding.
+      uint64_t h[2];
+      uint64_t cur = b0, carry = 0;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        // one lookup: the fast path needs kMultiBits valid bits, the canonical path (codes
+        // longer than the table) refills to >= 32 first
+        auto step = [&]() {
+          const uint32_t e = lut3[win >> (64 - kMultiBits)];
+          int k = (e >> 24) & 3, l;
+          uint64_t bytes;
+          if (__builtin_expect(k == 0, 0)) {
+            if (avail < 32) {
+              win |= (uint64_t)q.pop() << (32 - avail);
+              avail += 32;
+            }
+            int sym = 0;
+            l = canon_decode(win, ml, count, first_code, first_rank, sorted_sym, &sym);
+            bytes = (uint32_t)sym;
+            k = 1;
+          } else {
+            l = (int)(e >> 26);
+            bytes = e & 0xFFFFFFu;
+          }
+          win <<= l;
+          avail -= l;
+          const int sh = 8 * np;
+          cur |= bytes << sh;
+          carry |= np > 5 ? bytes >> (64 - sh) : 0ull;
+          np += k;
+        };
+        while (np < 8) {
+          // one refill per up to three lookups: after it avail >= 32, the first lookup
+          // leaves >= 21 bits, and each further one runs while kMultiBits remain
+          if (avail < 32) {
+            win |= (uint64_t)q.pop() << (32 - avail);
+            avail += 32;
+          }
+          step();
+          if (np < 8 && avail >= kMultiBits) step();
+          if (np < 8 && avail >= kMultiBits) step();
+        }
+        h[half] = cur;
+        cur = carry;
+        carry = 0;
+        np -= 8;
+      }
+      b0 = cur;
+      const uint32_t e0 = (uint32_t)h[0], e1 = (uint32_t)(h[0] >> 32), e2 = (uint32_t)h[1], e3 = (uint32_t)(h[1] >> 32);
+      asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(out + v),
+                   "r"(pack_words(smv.x, e0, 0x5140u)), "r"(pack_words(smv.x, e0, 0x7362u)),
+                   "r"(pack_words(smv.y, e1, 0x5140u)), "r"(pack_words(smv.y, e1, 0x7362u)),
+                   "r"(pack_words(smv.z, e2, 0x5140u)), "r"(pack_words(smv.z, e2, 0x7362u)),
+                   "r"(pack_words(smv.w, e3, 0x5140u)), "r"(pack_words(smv.w, e3, 0x7362u))
+                   : "memory");
+      continue;
+    }
+    while (np < cnt) {
+      if (avail < 32) {
+        win |= (uint64_t)q.pop() << (32 - avail);
+        avail += 32;
+      }
+      const uint32_t e = lut3[win >> (64 - kMultiBits)];
+      int k = (e >> 24) & 3, l;
+      uint64_t bytes;
+      if (k == 0 || k > (int)(v1 - v) - np) {
+        int sym = 0;
+        l = canon_decode(win, ml, count, first_code, first_rank, sorted_sym, &sym);
+        bytes = (uint32_t)sym;
+        k = 1;
+      } else {
+        l = (int)(e >> 26);
+        bytes = e & 0xFFFFFFu;
+      }
+      win <<= l;
+      avail -= l;
+      if (np < 8) {
+        b0 |= bytes << (8 * np);
+        if (np > 5) b1 |= bytes >> (64 - 8 * np);
+      } else {
+        const int q = np - 8;
+        b1 |= bytes << (8 * q);
+        if (q > 5) b2 |= bytes >> (64 - 8 * q);
+      }
+      np += k;
+    }
+    if (cnt == 16 && wide) {
+      // one 32-byte store per 16 values: a whole sector per thread (the warp's threads
+      // write 32 different chunks, so narrower stores cost proportionally more wavefronts)
+      const uint32_t e0 = (uint32_t)b0, e1 = (uint32_t)(b0 >> 32), e2 = (uint32_t)b1, e3 = (uint32_t)(b1 >> 32);
+      asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(out + v),
+                   "r"(pack_words(smv.x, e0, 0x5140u)), "r"(pack_words(smv.x, e0, 0x7362u)),
+                   "r"(pack_words(smv.y, e1, 0x5140u)), "r"(pack_words(smv.y, e1, 0x7362u)),
+                   "r"(pack_words(smv.z, e2, 0x5140u)), "r"(pack_words(smv.z, e2, 0x7362u)),
+                   "r"(pack_words(smv.w, e3, 0x5140u)), "r"(pack_words(smv.w, e3, 0x7362u))
+                   : "memory");
+    } else {
+      for (int j = 0; j < cnt; ++j) {
+        const uint32_t sym = (uint32_t)((j < 8 ? b0 >> (8 * j) : b1 >> (8 * (j - 8)))) & 0xFFu;
+        const uint32_t sb = sm[v + j];
+        out[v + j] = (uint16_t)(((sb & 0x80u) << 8) | (sym << 7) | (sb & 0x7Fu));
+      }
+    }
+    b0 = b2;
+    b1 = 0;
+    b2 = 0;
+    np -= cnt;
+  }
+}
+
+void launch_exp_decode(const uint8_t* sm, const uint32_t* bits, const uint32_t* index, uint64_t n, int chunk,
+                       const CodecTable& table, uint16_t* out, cudaStream_t s, uint32_t bit_base) {
+  DecodeTensor t{sm, bits, index, out, bit_base};
+  launch_exp_decode_multi(&t, 1, n, chunk, table, s);
+}
+
+// Device tables per (device, codec table), built once on first use (synchronously, so a
+// decode on any stream may read them) and kept for the process.
+static const DecTables* decode_tables(const CodecTable& table, cudaStream_t s) {
+  struct Entry {
+    int dev;
+    CodecTable t;
+    DecTables* d;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  for (const Entry& e : cache)
+    if (e.dev == dev && memcmp(e.t.len, table.len, sizeof(table.len)) == 0) return e.d;
+  DecTables* d = nullptr;
+  if (cudaMalloc(&d, sizeof(DecTables)) != cudaSuccess) return nullptr;
+  k_build_tables<<<1, 256, 0, s>>>(table, d);
+  note_launch();
+  if (cudaStreamSynchronize(s) != cudaSuccess) return nullptr;
+  cache.push_back(Entry{dev, table, d});
+  return d;
+}
+
+void prepare_decode_tables(const CodecTable& table, cudaStream_t s) { decode_tables(table, s); }
+
+void launch_exp_decode_multi(const DecodeTensor* tensors, int ntensors, uint64_t n, int chunk, const CodecTable& table,
+                             cudaStream_t s) {
+  if (n == 0 || ntensors <= 0) return;
+  DecodeParams p;
+  p.ntensors = ntensors;
+  p.n = n;
+  p.chunk = chunk;
+  p.tabs = decode_tables(table, s);
+  if (!p.tabs) return;  // the caller's CKLAUNCH reports the CUDA error
+  for (int i = 0; i < ntensors; ++i) p.t[i] = tensors[i];
+  const uint64_t n_chunks = ((n + chunk - 1) / chunk) * (uint64_t)ntensors;
+  // one resident wave, grid-striding over the chunks: a second partial wave left the
+  // tail idle (chunk 256: 1265 GB/s at 5 blocks/SM vs 1107 at 8)
+  static const int resident = [] {
+    int dev = 0, sms = 148, per_sm = 4;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_exp_decode, 256, 0);
+    return std::max(1, sms * std::max(1, per_sm));
+  }();
+  const uint64_t blocks = std::min<uint64_t>((n_chunks + 255) / 256, (uint64_t)resident);
+  k_exp_decode<<<(unsigned)blocks, 256, 0, s>>>(p);
+  note_launch();
+}
+
+}  // namespace xpgb
