@@ -75,6 +75,16 @@ def _spread_row(streamed: int, m: int, window: int) -> np.ndarray:
     return row
 
 
+def _spaced(total: int, N: int) -> list:
+    """`total` items over N slots, the remainder spaced evenly (1 item over 8 slots: slot 4;
+    3 over 8: slots 1, 4, 6), not bunched at one end."""
+    base, rem = divmod(int(total), N)
+    out = [base] * N
+    for i in range(rem):
+        out[int((i + 0.5) * N / rem)] += 1
+    return out
+
+
 def _balanced(total: int, N: int):
     return [(l + 1) * total // N - l * total // N for l in range(N)]
 
@@ -134,7 +144,14 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
         raise ValueError(f"budget {budget_bytes:.3g} B cannot hold a ring")
     (est, _), p, d, ring, link = best
     p_layer = _balanced(p, N)
-    d_layer = _fill(d, [L - q for q in p_layer])
+    # host-tier experts spaced evenly over the layers: each host record then has the
+    # layers since the previous one to cross the link (the staging ring holds about one
+    # record ahead), instead of queueing behind a neighbour (Mixtral 80%: 3 host experts
+    # bunched in layers 1, 7, 8 stalled 1.8 ms per step)
+    h_layer = _spaced(total - p - d, N)
+    d_layer = [L - q - hh for q, hh in zip(p_layer, h_layer)]
+    if min(d_layer) < 0:
+        d_layer = _fill(d, [L - q for q in p_layer])
     pinned = np.zeros((N, L), dtype=bool)
     for l in range(N):
         if p_layer[l]:
