@@ -141,6 +141,10 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
         if best is None or key < best[0]:
             best = (key, p, d, ring, link)
     if best is None:
+        if w_min > 1:  # small experts: a narrower window still fits (tiny: 8 x 0.8 MB > 25%)
+            return plan_residency(N, L, eb, ceb, budget_bytes, shared_bytes=shared_bytes, b_link=b_link,
+                                  b_dec=b_dec, t_compute=t_compute, min_window_bytes=min_window_bytes,
+                                  allow_pinned=allow_pinned, depth=depth, window=max(1, w_min // 2))
         raise ValueError(f"budget {budget_bytes:.3g} B cannot hold a ring")
     (est, _), p, d, ring, link = best
     p_layer = _balanced(p, N)

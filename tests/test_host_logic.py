@@ -253,3 +253,13 @@ def test_residency_plan_spends_the_budget():
         for j in range(0, 8, w):
             assert pl.device_mask[l, j:j + w].sum() <= 1
     assert plan_residency(8, 8, eb, ceb, 1.0 * total).pinned_experts == 64
+
+
+def test_residency_plan_narrows_windows_for_small_budgets():
+    """Tiny experts: windows sized for min_window_bytes would not fit a 25% budget; the planner
+    narrows the window until the ring fits (the tiny bench config)."""
+    from paper_2604_02715_b200.budget import plan_residency
+
+    eb = 786432
+    pl = plan_residency(4, 8, eb, 0.68 * eb, 0.25 * 32 * eb * 0.998)
+    assert 0 < pl.ring < 8 and pl.hbm_bytes <= 0.25 * 32 * eb
