@@ -142,6 +142,11 @@ int64_t xpgb_kernel_launches(void);
 /* Create a context on `device`.  pool = XPGB_POOL_RING (PageTable, paging.py:97-130)
  * or XPGB_POOL_RESIDENT (resident_baseline).  max_tokens sizes workspaces (grows lazily). */
 int xpgb_create(const xpgb_spec* spec, int32_t device, int32_t pool, int32_t max_tokens, xpgb_ctx** out);
+/* Same, holding only experts [expert_first, expert_first + expert_count) of every layer from the
+ * start (an expert-parallel rank): pools are sized for the shard, never for all L experts (a
+ * DSv3 rank would otherwise allocate the whole 180 GB model transiently). */
+int xpgb_create_shard(const xpgb_spec* spec, int32_t device, int32_t pool, int32_t max_tokens, int32_t expert_first,
+                      int32_t expert_count, xpgb_ctx** out);
 int xpgb_destroy(xpgb_ctx* ctx);
 int xpgb_sync(xpgb_ctx* ctx);
 

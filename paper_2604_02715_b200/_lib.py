@@ -72,6 +72,7 @@ _SIGS = {
     "xpgb_last_error": [],
     "xpgb_kernel_launches": [],
     "xpgb_create": [C.POINTER(Spec), _I, _I, _I, C.POINTER(_P)],
+    "xpgb_create_shard": [C.POINTER(Spec), _I, _I, _I, _I, _I, C.POINTER(_P)],
     "xpgb_destroy": [_P],
     "xpgb_sync": [_P],
     "xpgb_pinned_alloc": [_U64, C.POINTER(_P)],

@@ -1488,8 +1488,23 @@ int xpgb_abi_version(void) { return XPGB_ABI_VERSION; }
 const char* xpgb_last_error(void) { return g_err.c_str(); }
 int64_t xpgb_kernel_launches(void) { return g_launches.load(); }
 
+static void create_impl(const xpgb_spec* spec, int32_t device, int32_t pool, int32_t max_tokens, int32_t expert_first,
+                        int32_t expert_count, xpgb_ctx** out);
+
 int xpgb_create(const xpgb_spec* spec, int32_t device, int32_t pool, int32_t max_tokens, xpgb_ctx** out) {
-  return guard([&] {
+  return guard([&] { create_impl(spec, device, pool, max_tokens, 0, spec ? spec->experts_per_layer : 0, out); });
+}
+
+int xpgb_create_shard(const xpgb_spec* spec, int32_t device, int32_t pool, int32_t max_tokens, int32_t expert_first,
+                      int32_t expert_count, xpgb_ctx** out) {
+  return guard([&] { create_impl(spec, device, pool, max_tokens, expert_first, expert_count, out); });
+}
+
+}  // extern "C"
+
+static void create_impl(const xpgb_spec* spec, int32_t device, int32_t pool, int32_t max_tokens, int32_t expert_first,
+                        int32_t expert_count, xpgb_ctx** out) {
+  {
     if (!spec || !out) XFAIL(XPGB_ERR, "null argument");
     if (spec->num_layers < 2) XFAIL(XPGB_ERR_OUT_OF_RANGE, "num_layers must be >= 2, got %d", spec->num_layers);
     if (spec->experts_per_layer < 1)
@@ -1515,7 +1530,12 @@ int xpgb_create(const xpgb_spec* spec, int32_t device, int32_t pool, int32_t max
     c->F = spec->intermediate_dim;
     c->device = device;
     c->pool = pool;
-    c->E = c->L;
+    if (expert_first < 0 || expert_count < 1 || expert_first + expert_count > c->L) {
+      delete h;
+      XFAIL(XPGB_ERR_OUT_OF_RANGE, "shard [%d, %d) outside [0, %d)", expert_first, expert_first + expert_count, c->L);
+    }
+    c->e_first = expert_first;
+    c->E = expert_count;  // pools and slot tables are sized for the shard from the start
     c->s1 = 2ull * c->H * 2 * c->F;
     c->s2 = 2ull * c->F * c->H;
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
@@ -1537,8 +1557,10 @@ int xpgb_create(const xpgb_spec* spec, int32_t device, int32_t pool, int32_t max
     init_pools(c);
     ensure_work(c, std::max(1, max_tokens), std::min(c->L, 8));
     *out = h;
-  });
+  }
 }
+
+extern "C" {
 
 int xpgb_destroy(xpgb_ctx* h) {
   return guard([&] {

@@ -50,16 +50,19 @@ def as_device_f32(acts, device: int, rows: int, cols: int):
 class Context:
     """One libxpgb context: pools, page table, streams, workspaces."""
 
-    def __init__(self, spec: ModelSpec, pool: int = _lib.POOL_RING, device: int = 0, max_tokens: int = 16):
+    def __init__(self, spec: ModelSpec, pool: int = _lib.POOL_RING, device: int = 0, max_tokens: int = 16,
+                 expert_shard=None):
+        """expert_shard=(first, count): hold only those experts of every layer from the start."""
         _torch()
         self.spec = spec
         self.device = device
         self.pool = pool
-        self.expert_first = 0
-        self.expert_count = spec.experts_per_layer
+        first, count = expert_shard if expert_shard is not None else (0, spec.experts_per_layer)
+        self.expert_first, self.expert_count = int(first), int(count)
         s = _lib.Spec(spec.num_layers, spec.experts_per_layer, spec.hidden_dim, spec.intermediate_dim)
         h = C.c_void_p()
-        call("xpgb_create", C.byref(s), device, pool, max(1, int(max_tokens)), C.byref(h))
+        call("xpgb_create_shard", C.byref(s), device, pool, max(1, int(max_tokens)), self.expert_first,
+             self.expert_count, C.byref(h))
         self._h = h
         self._host_ref = None
 

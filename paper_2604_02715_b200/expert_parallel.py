@@ -409,8 +409,8 @@ class ExpertParallelRunner:
         first, count = shard_bounds(spec.experts_per_layer, world)[rank]
         self.shard = (first, count)
         self._codec = None
-        self.ctx = Context(spec, _lib.POOL_RING, device, max_tokens=world * fwd.tokens_per_step)
-        self.ctx.set_expert_shard(first, count)
+        self.ctx = Context(spec, _lib.POOL_RING, device, max_tokens=world * fwd.tokens_per_step,
+                           expert_shard=(first, count))
         pool = shard_pool if shard_pool is not None else shard_payload(container, first, count)
         self.ctx.attach_host_pool(pool)
         if host_codec:

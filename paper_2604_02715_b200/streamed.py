@@ -233,10 +233,8 @@ class StreamedRunner:
         self.mode = mode
         self.compute_delay_fn = compute_delay_fn
         self.sabotage_skip_raw = sabotage_skip_raw
-        self.ctx = Context(spec, _lib.POOL_RING, device, max_tokens=fwd.tokens_per_step)
         first, count = expert_shard if expert_shard is not None else (0, spec.experts_per_layer)
-        if expert_shard is not None:
-            self.ctx.set_expert_shard(first, count)
+        self.ctx = Context(spec, _lib.POOL_RING, device, max_tokens=fwd.tokens_per_step, expert_shard=(first, count))
         self.ctx.attach_host_pool(hierarchy.container.pinned)
         if getattr(hierarchy.container, "shared", None) is not None:
             self.ctx.set_shared(hierarchy.container.shared)
@@ -533,9 +531,8 @@ class ResidentModel:
                  expert_shard=None, shared_tokens=None):
         self.spec = spec
         self.container = container
-        self.ctx = Context(spec, _lib.POOL_RESIDENT, device, max_tokens=max_tokens)
-        if expert_shard is not None:  # container = the shard's payload (see StreamedRunner)
-            self.ctx.set_expert_shard(*expert_shard)
+        # container = the shard's payload when expert_shard is set (see StreamedRunner)
+        self.ctx = Context(spec, _lib.POOL_RESIDENT, device, max_tokens=max_tokens, expert_shard=expert_shard)
         self.ctx.attach_host_pool(container.pinned)
         self.ctx.make_resident()
         if getattr(container, "shared", None) is not None:
