@@ -527,30 +527,22 @@ def main():
     # ---- e2e: the same metric through the public API with host buffers every step: a
     # serving session (StreamedRunner.open_session) fed from pinned host memory, each step's
     # output read back into pinned host memory; the next step's first layers prefetch while
-    # the host holds the previous result (the EP runner has no session: one run() per step)
+    # the host holds the previous result (the EP runner has the same session API)
     e2e_steps = args.steps
     x_pin = torch.from_numpy(x_host).pin_memory()
     out_pin = torch.empty_like(x_pin).pin_memory()
-    sess = None
-    if not use_ep:
-        sess = runner.open_session(max_iterations=e2e_steps + 1, log=False)
-        sess.step(x_pin, out=out_pin)  # session warm-up step (untimed)
+    sess = runner.open_session(max_iterations=e2e_steps + 1, log=False)
+    sess.step(x_pin, out=out_pin)  # session warm-up step (untimed)
     torch.cuda.synchronize()
     barrier(world)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(e2e_steps):
-        if sess is not None:
-            out = sess.step(x_pin, out=out_pin)  # pinned H2D in, D2H out, every step
-        else:
-            out = runner.run(1, acts=x_host).final_activations
-            if hasattr(out, "cpu"):
-                out = out.cpu()
+        out = sess.step(x_pin, out=out_pin)  # pinned H2D in, D2H out, every step
     e1.record()
     torch.cuda.synchronize()
-    if sess is not None:
-        sess.close()
-        del sess  # the session holds the runner (and its HBM ring) alive
+    sess.close()
+    del sess  # the session holds the runner (and its HBM ring) alive
     e2e_elapsed = max_over_ranks(torch, world, e0.elapsed_time(e1) * 1e-3, dev)
     if use_ep:
         runner.close()  # peer windows: every rank unmaps, barrier, then frees its own
@@ -642,7 +634,7 @@ def main():
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": int(x_host.nbytes),
                 "d2h_bytes_per_step": int(x_host.nbytes),
                 "api": "StreamedRunner.open_session(...).step(pinned host acts)" if not use_ep else
-                       "ExpertParallelRunner.run(1, host acts) per step"},
+                       "ExpertParallelRunner.open_session(...).step(pinned host acts)"},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "model_gen_s": gen_s,

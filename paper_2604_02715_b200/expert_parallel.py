@@ -27,6 +27,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
+from .errors import XpgError
 from ._lib import call
 from .geometry import ModelSpec, tensor_offset, ExpertTensorId, TensorKind
 from .streamed import ForwardSpec, RunReport, _kernel_stats, _records_from_log, _intervals, validate_ordering
@@ -485,73 +486,82 @@ class ExpertParallelRunner:
         shard_map = np.repeat(plan.device_mask[:, :, None], 2, axis=2).astype(np.uint8)
         self.ctx.set_placement(_full_width(self.spec, shard_map, first, count))
 
-    def run(self, iterations: int, acts, profile: bool = False) -> RunReport:
+    def _begin(self, iterations: int, tokens: int, profile: bool = False, log: bool = True):
         import torch
 
-        from .device import current_stream_ptr
-
-        N = self.spec.num_layers
-        x = acts if isinstance(acts, torch.Tensor) else torch.from_numpy(np.asarray(acts, np.float32))
-        x = x.to(f"cuda:{self.ctx.device}", torch.float32).contiguous()
-        T = x.shape[0]
-        plans = [self.moe.plan(layer, T) for layer in range(1, N + 1)]  # routing: pure function of (seed, t, layer)
         opts = _lib.RunOpts()
         opts.iterations = iterations
-        opts.tokens = self.world * T
+        opts.tokens = self.world * tokens
         opts.top_k = self.fwd.top_k
         opts.router_seed = int(self.fwd.router_seed) & 0xFFFFFFFFFFFFFFFF
-        opts.log_enable = 1
+        opts.log_enable = 1 if log else 0
         opts.profile = 1 if profile else 0  # decoder launch timing (xpgb_decode_stats)
+        opts.fresh_inputs = 1
         h = self.ctx.handle
         torch.cuda.synchronize(self.ctx.device)
         call("xpgb_session_begin", h, C.byref(opts), None)
         try:
             call("xpgb_session_materialize", h, 0)
             call("xpgb_session_materialize", h, 1)
-            total = C.c_int32()
-            call("xpgb_session_info", h, C.byref(total), None, None)
-            info = (C.c_int32 * 7)()
-            out = None
-            n_rows, rows_ptr = 0, 0
-            peer = self.peer
-            kk = min(self.fwd.top_k, self.spec.experts_per_layer)
-            H = self.spec.hidden_dim
-            for g in range(total.value):  # steps are layers, or windows of a sub-layer ring
-                call("xpgb_session_step", h, g, info)
-                layer, e0, e1, first, last = info[1], info[3], info[4], info[5], info[6]
-                plan = plans[layer - 1]
-                stream = current_stream_ptr(self.ctx.device)
-                st = C.c_void_p(stream)
-                if first:
-                    if peer is not None:
-                        n_rows = int(plan.c_rank.numel())
-                        rows_ptr = peer.dispatch(x, plan, stream)  # rows land expert-major in my window
-                    else:
-                        rows = self.moe.dispatch(x, plan)
-                        n_rows, rows_ptr = int(rows.shape[0]), rows.data_ptr()
-                    out = torch.empty((n_rows, H), dtype=torch.float32, device=x.device)
-                call("xpgb_session_acquire", h, g, st)
-                if n_rows and e1 > e0:
-                    call("xpgb_experts_forward_range", h, layer, C.c_void_p(rows_ptr),
-                         C.c_void_p(plan.offsets.data_ptr()), n_rows, e0, e1, 1 if last else 0,
-                         C.c_void_p(out.data_ptr()), st)
-                call("xpgb_session_release", h, g, st)
-                call("xpgb_session_materialize", h, g + 2)
-                if last:
-                    if peer is not None:
-                        ret = peer.combine(out, plan, stream)
-                        y = torch.empty((T, H), dtype=torch.float32, device=x.device)
-                        if T:
-                            call("xpgb_combine_rows", C.c_void_p(ret), C.c_void_p(plan.ret_index.data_ptr()), T, kk,
-                                 self.fwd.top_k, H, C.c_void_p(y.data_ptr()), st)
-                        if self.moe.shared_fn is not None:
-                            self.moe.shared_fn(layer, x, y)
-                        x = y
-                    else:
-                        x = self.moe.combine(layer, x, out, plan)
+            total, per_iter = C.c_int32(), C.c_int32()
+            call("xpgb_session_info", h, C.byref(total), C.byref(per_iter), None)
         except Exception:
             _lib.lib().xpgb_session_abort(h)
             raise
+        return int(total.value), int(per_iter.value)
+
+    def _steps(self, x, g0: int, g1: int, plans):
+        """Session steps [g0, g1) (whole layers: dispatch at a layer's first window, the
+        window's grouped GEMMs, combine after its last) on torch's current stream."""
+        import torch
+
+        from .device import current_stream_ptr
+
+        h = self.ctx.handle
+        T = x.shape[0]
+        info = (C.c_int32 * 7)()
+        out = None
+        n_rows, rows_ptr = 0, 0
+        peer = self.peer
+        kk = min(self.fwd.top_k, self.spec.experts_per_layer)
+        H = self.spec.hidden_dim
+        for g in range(g0, g1):  # steps are layers, or windows of a sub-layer ring
+            call("xpgb_session_step", h, g, info)
+            layer, e0, e1, first, last = info[1], info[3], info[4], info[5], info[6]
+            plan = plans[layer - 1]
+            stream = current_stream_ptr(self.ctx.device)
+            st = C.c_void_p(stream)
+            if first:
+                if peer is not None:
+                    n_rows = int(plan.c_rank.numel())
+                    rows_ptr = peer.dispatch(x, plan, stream)  # rows land expert-major in my window
+                else:
+                    rows = self.moe.dispatch(x, plan)
+                    n_rows, rows_ptr = int(rows.shape[0]), rows.data_ptr()
+                out = torch.empty((n_rows, H), dtype=torch.float32, device=x.device)
+            call("xpgb_session_acquire", h, g, st)
+            if n_rows and e1 > e0:
+                call("xpgb_experts_forward_range", h, layer, C.c_void_p(rows_ptr),
+                     C.c_void_p(plan.offsets.data_ptr()), n_rows, e0, e1, 1 if last else 0,
+                     C.c_void_p(out.data_ptr()), st)
+            call("xpgb_session_release", h, g, st)
+            call("xpgb_session_materialize", h, g + 2)
+            if last:
+                if peer is not None:
+                    ret = peer.combine(out, plan, stream)
+                    y = torch.empty((T, H), dtype=torch.float32, device=x.device)
+                    if T:
+                        call("xpgb_combine_rows", C.c_void_p(ret), C.c_void_p(plan.ret_index.data_ptr()), T, kk,
+                             self.fwd.top_k, H, C.c_void_p(y.data_ptr()), st)
+                    if self.moe.shared_fn is not None:
+                        self.moe.shared_fn(layer, x, y)
+                    x = y
+                else:
+                    x = self.moe.combine(layer, x, out, plan)
+        return x
+
+    def _end(self, x) -> RunReport:
+        h = self.ctx.handle
         rep = _lib.Report()
         call("xpgb_session_end", h, C.byref(rep))
         records = _records_from_log(self.ctx)
@@ -562,3 +572,81 @@ class ExpertParallelRunner:
             h2d_bytes=int(rep.h2d_bytes), d2d_bytes=int(rep.d2d_bytes),
             copy_busy_seconds=(rep.copy_busy_ns[0] * 1e-9, rep.copy_busy_ns[1] * 1e-9),
             elapsed_seconds=rep.elapsed_ns * 1e-9, kernels=_kernel_stats(rep), decoded_bytes=int(rep.decoded_bytes))
+
+    def _plans(self, tokens: int):
+        return [self.moe.plan(layer, tokens) for layer in range(1, self.spec.num_layers + 1)]
+
+    def run(self, iterations: int, acts, profile: bool = False) -> RunReport:
+        import torch
+
+        x = acts if isinstance(acts, torch.Tensor) else torch.from_numpy(np.asarray(acts, np.float32))
+        x = x.to(f"cuda:{self.ctx.device}", torch.float32).contiguous()
+        plans = self._plans(x.shape[0])  # routing: a pure function of (seed, token, layer)
+        total, _ = self._begin(iterations, x.shape[0], profile=profile)
+        try:
+            x = self._steps(x, 0, total, plans)
+        except Exception:
+            _lib.lib().xpgb_session_abort(self.ctx.handle)
+            raise
+        return self._end(x)
+
+    def open_session(self, max_iterations: int, log: bool = False) -> "EPDecodeSession":
+        """Serving loop under EP (as StreamedRunner.open_session): one decode iteration per
+        step(acts) on fresh activations; the schedule stays open between steps, so the next
+        step's first windows page in while the caller holds the result."""
+        return EPDecodeSession(self, max_iterations, log)
+
+
+class EPDecodeSession:
+    def __init__(self, runner: ExpertParallelRunner, max_iterations: int, log: bool = False):
+        self.runner = runner
+        self.max_iterations = max_iterations
+        self.T = runner.fwd.tokens_per_step
+        self.plans = runner._plans(self.T)
+        self.total, self.per_iter = runner._begin(max_iterations, self.T, log=log)
+        self.g = 0
+        self.steps_run = 0
+        self.x = None
+        self.closed = False
+
+    def step(self, acts, out=None):
+        """acts: [T, H] fp32 (numpy, pinned CPU tensor or CUDA tensor); returns the layer
+        stack's output (into `out` when given, e.g. pinned host memory)."""
+        import torch
+
+        if self.closed or self.steps_run >= self.max_iterations:
+            raise XpgError("session is closed or out of iterations")
+        dev = f"cuda:{self.runner.ctx.device}"
+        x = acts if isinstance(acts, torch.Tensor) else torch.from_numpy(np.asarray(acts, np.float32))
+        x = x.to(dev, torch.float32, non_blocking=True).contiguous()
+        try:
+            y = self.runner._steps(x, self.g, self.g + self.per_iter, self.plans)
+        except Exception:
+            self.abort()
+            raise
+        self.g += self.per_iter
+        self.steps_run += 1
+        self.x = y
+        if out is not None:
+            out.copy_(y, non_blocking=False)
+            return out
+        return y
+
+    def abort(self):
+        if not self.closed:
+            _lib.lib().xpgb_session_abort(self.runner.ctx.handle)
+            self.closed = True
+
+    def close(self) -> RunReport:
+        """End the session (the unused iterations' pages are released)."""
+        if self.closed:
+            raise XpgError("session already closed")
+        self.closed = True
+        return self.runner._end(self.x)
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        if not self.closed:
+            self.close() if exc[0] is None else self.abort()

@@ -109,3 +109,25 @@ def test_peer_exchange_world1_matches_resident():
     assert rep.page_fault is None and rep.violations == []
     base = X.resident_baseline(2, spec, container, fwd, acts=x.copy())
     assert O.rel_l2(rep.final_activations.cpu().numpy(), base) <= 1e-3
+
+
+def test_ep_decode_session_matches_run():
+    """ExpertParallelRunner.open_session: one decode iteration per step on fresh activations,
+    the same result as run(1) on each input (world 1, peer windows)."""
+    import torch
+
+    import paper_2604_02715_b200 as X
+    from paper_2604_02715_b200.expert_parallel import ExpertParallelRunner
+
+    spec = X.ModelSpec(*SPEC)
+    fwd = X.ForwardSpec(T, K, SEED)
+    container = X.generate_synthetic_model(spec, SEED)
+    runner = ExpertParallelRunner(spec, container, fwd, 0, 1, host_codec=True, transport="p2p")
+    xs = [np.random.default_rng(s).standard_normal((T, spec.hidden_dim), dtype=np.float32) for s in (1, 2, 3)]
+    want = [runner.run(1, x.copy()).final_activations.cpu().numpy() for x in xs]
+    out = torch.empty((T, spec.hidden_dim), dtype=torch.float32).pin_memory()
+    with runner.open_session(max_iterations=4) as sess:
+        for x, w in zip(xs, want):
+            got = sess.step(torch.from_numpy(x).pin_memory(), out=out)
+            assert got.numpy().tobytes() == w.tobytes()
+    runner.close()
