@@ -347,6 +347,14 @@ int xpgb_ep_scatter_rows(const float* src_dev, const int32_t* src_rows, const in
                          int32_t n, int32_t hidden, int32_t to_bf16, void* const* peer_rows, int32_t* const* peer_flags,
                          int32_t world, int32_t rank, int32_t epoch, uint32_t* counter, void* stream);
 int xpgb_ep_wait(const int32_t* flags_dev, int32_t world, int32_t epoch, void* stream);
+/* The combine fused with the down projection's split-K reduction: after
+ * xpgb_experts_forward_range(..., reduce = 0) over a layer's last window, each of the n_rows
+ * expert-major output rows is summed from ctx's partial planes and stored straight into
+ * dst_rank[i]'s region at row dst_row[i] (f32); the last CTA releases `epoch` like
+ * xpgb_ep_scatter_rows.  n_rows must be the rows of that experts_forward_range call. */
+int xpgb_ep_reduce_scatter(xpgb_ctx* ctx, const int32_t* dst_rank, const int32_t* dst_row, int32_t n_rows,
+                           void* const* peer_rows, int32_t* const* peer_flags, int32_t world, int32_t rank,
+                           int32_t epoch, uint32_t* counter, void* stream);
 
 /* One window of a layer on pre-grouped rows: GEMMs of local experts [e0, e1) only (rows stay
  * absolute; the rows are copied in with the e0 == 0 window); reduce = 1 on the layer's last

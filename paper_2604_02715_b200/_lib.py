@@ -123,6 +123,7 @@ _SIGS = {
     "xpgb_ep_window_free": [_P],
     "xpgb_ep_scatter_rows": [_P, _P, _P, _P, _I, _I, _I, _P, _P, _I, _I, _I, _P, _P],
     "xpgb_ep_wait": [_P, _I, _I, _P],
+    "xpgb_ep_reduce_scatter": [_P, _P, _P, _I, _P, _P, _I, _I, _I, _P, _P],
     "xpgb_set_shared_tokens": [_P, _I, _I],
     "xpgb_shared_forward": [_P, _I, _P, _P, _I, _P],
     "xpgb_experts_forward": [_P, _I, _P, _P, _I, _P, _P],

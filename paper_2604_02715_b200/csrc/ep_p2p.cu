@@ -69,6 +69,45 @@ __global__ void __launch_bounds__(256) k_ep_scatter(const float* __restrict__ sr
   }
 }
 
+// Combine fused with the split-K reduction: row i of the owner's expert outputs is the sum
+// of its split-K partials (part + k * split_stride4 float4s), stored straight into rank
+// dst_rank[i]'s return buffer at row dst_row[i]; the last CTA publishes the epoch.  A
+// faulted run (a page read before it was resident) writes nothing but still publishes, so
+// no peer waits forever.
+__global__ void __launch_bounds__(256) k_ep_reduce_scatter(const float* __restrict__ part, const long long* fault,
+                                                           int splits, long long split_stride4,
+                                                           const int32_t* __restrict__ dst_rank,
+                                                           const int32_t* __restrict__ dst_row, int n, int H,
+                                                           const __grid_constant__ EpPeers peers, int32_t epoch,
+                                                           unsigned int* counter) {
+  const int lane = threadIdx.x & 31;
+  const int warps = blockDim.x >> 5;
+  const bool ok = *fault == 0;
+  for (int row = blockIdx.x * warps + (threadIdx.x >> 5); ok && row < n; row += gridDim.x * warps) {
+    const float4* s = reinterpret_cast<const float4*>(part) + (size_t)row * (H / 4);
+    float4* d = reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(peers.rows[dst_rank[row]]) +
+                                          (size_t)dst_row[row] * H * 4);
+    for (int c = lane; c < H / 4; c += 32) {
+      float4 v = s[c];
+      for (int k = 1; k < splits; ++k) {
+        const float4 w = s[c + k * split_stride4];
+        v.x = __fadd_rn(v.x, w.x); v.y = __fadd_rn(v.y, w.y); v.z = __fadd_rn(v.z, w.z); v.w = __fadd_rn(v.w, w.w);
+      }
+      d[c] = v;
+    }
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int t = atomicAdd(counter, 1u);
+    if (t == gridDim.x - 1) {
+      *counter = 0u;
+      __threadfence_system();
+      for (int p = 0; p < peers.world; ++p) st_release_sys(peers.flags[p] + peers.rank, epoch);
+    }
+  }
+}
+
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -100,6 +139,17 @@ void launch_ep_scatter(const float* src, const int32_t* src_rows, const int32_t*
     k_ep_scatter<true><<<grid, warps * 32, 0, s>>>(src, src_rows, dst_rank, dst_row, n, H, peers, epoch, counter);
   else
     k_ep_scatter<false><<<grid, warps * 32, 0, s>>>(src, src_rows, dst_rank, dst_row, n, H, peers, epoch, counter);
+  note_launch();
+}
+
+void launch_ep_reduce_scatter(const float* part, const long long* fault, int splits, long long split_stride,
+                              const int32_t* dst_rank, const int32_t* dst_row, int n, int H, const EpPeers& peers,
+                              int32_t epoch, unsigned int* counter, int num_sms, cudaStream_t s) {
+  const int warps = 8;
+  int grid = (n + warps - 1) / warps;
+  grid = grid < 1 ? 1 : (grid > num_sms * 4 ? num_sms * 4 : grid);
+  k_ep_reduce_scatter<<<grid, warps * 32, 0, s>>>(part, fault, splits, split_stride / 4, dst_rank, dst_row, n, H, peers,
+                                                  epoch, counter);
   note_launch();
 }
 

@@ -23,6 +23,11 @@ struct EpPeers {
 void launch_ep_scatter(const float* src, const int32_t* src_rows, const int32_t* dst_rank, const int32_t* dst_row,
                        int n, int H, bool to_bf16, const EpPeers& peers, int32_t epoch, unsigned int* counter,
                        int num_sms, cudaStream_t s);
+// Combine fused with the split-K reduction: row i = sum of its `splits` partial planes of
+// part (split_stride floats apart), scattered like launch_ep_scatter (f32).
+void launch_ep_reduce_scatter(const float* part, const long long* fault, int splits, long long split_stride,
+                              const int32_t* dst_rank, const int32_t* dst_row, int n, int H, const EpPeers& peers,
+                              int32_t epoch, unsigned int* counter, int num_sms, cudaStream_t s);
 // Stream-ordered acquire wait until flags[0..world) >= epoch.
 void launch_ep_wait(const int32_t* flags, int world, int32_t epoch, cudaStream_t s);
 

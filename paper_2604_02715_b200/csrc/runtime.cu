@@ -212,6 +212,8 @@ struct Ctx {
   int ring_blocks = 0;          // blocks per kind that cycle through the schedule
   int ring_limit = 0;           // cap on ring blocks per kind (sub-layer ring); 0 = 2 x streamed experts
   int ring_depth = 2;           // windows in flight on a sub-layer ring (window g recycles g - depth)
+  int ep_splits = 1, ep_rows = 0;  // last experts_forward_range: split-K planes and rows in part
+  long long ep_split_stride = 0;
 
   // streams / events
   cudaStream_t s_copy[2] = {nullptr, nullptr};
@@ -2342,6 +2344,9 @@ static void experts_forward_range(Ctx* c, int layer, const void* rows_dev, const
   else
     launch_down(c->map_dn, c->map_h, c->map_dn, pd, bn, c->num_sms, s, lean_gemm(c));
   CKLAUNCH();
+  c->ep_splits = splits;  // for a fused reduce + combine scatter (xpgb_ep_reduce_scatter)
+  c->ep_split_stride = pd.split_stride;
+  c->ep_rows = n_rows;
   if (reduce) {  // after the layer's last window: every row's split-K partials are final
     launch_reduce_rows(c->part, c->d_fault, out_dev, n_rows, c->H, splits, pd.split_stride, s);
     CKLAUNCH();
@@ -2447,6 +2452,28 @@ int xpgb_ep_scatter_rows(const float* src_dev, const int32_t* src_rows, const in
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     launch_ep_scatter(src_dev, src_rows, dst_rank, dst_row, n, hidden, to_bf16 != 0, peers, epoch, counter, sms,
                       (cudaStream_t)stream);
+    CKLAUNCH();
+  });
+}
+
+int xpgb_ep_reduce_scatter(xpgb_ctx* h, const int32_t* dst_rank, const int32_t* dst_row, int32_t n_rows,
+                           void* const* peer_rows, int32_t* const* peer_flags, int32_t world, int32_t rank,
+                           int32_t epoch, uint32_t* counter, void* stream) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    if (world < 1 || world > kMaxEpWorld || rank < 0 || rank >= world)
+      XFAIL(XPGB_ERR_OUT_OF_RANGE, "rank %d of %d (at most %d ranks)", rank, world, kMaxEpWorld);
+    if (n_rows != c->ep_rows && n_rows > 0)
+      XFAIL(XPGB_ERR_OUT_OF_RANGE, "%d rows, the last experts_forward_range computed %d", n_rows, c->ep_rows);
+    EpPeers peers{};
+    peers.world = world;
+    peers.rank = rank;
+    for (int r = 0; r < world; ++r) {
+      peers.rows[r] = peer_rows[r];
+      peers.flags[r] = peer_flags[r];
+    }
+    launch_ep_reduce_scatter(c->part, c->d_fault, c->ep_splits, c->ep_split_stride, dst_rank, dst_row, n_rows, c->H,
+                             peers, epoch, counter, c->num_sms, (cudaStream_t)stream);
     CKLAUNCH();
   });
 }

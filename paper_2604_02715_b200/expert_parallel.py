@@ -245,6 +245,17 @@ class PeerExchange:
                       self._xp, stream)
         return self.xp
 
+    def reduce_combine(self, ctx, plan, stream) -> int:
+        """The combine fused with the owner's split-K reduction (xpgb_ep_reduce_scatter): the
+        rows of the last experts_forward_range(reduce=0) go from the partial planes straight
+        into the token owners' return buffers."""
+        self.epoch += 1
+        call("xpgb_ep_reduce_scatter", ctx.handle, C.c_void_p(plan.c_rank.data_ptr()),
+             C.c_void_p(plan.c_row.data_ptr()), int(plan.c_rank.numel()), self._ret, self._flags, self.world,
+             self.rank, self.epoch, C.c_void_p(self.counter), C.c_void_p(stream))
+        call("xpgb_ep_wait", C.c_void_p(self._own), self.world, self.epoch, C.c_void_p(stream))
+        return self.ret
+
     def combine(self, out, plan, stream) -> int:
         """This rank's expert outputs fp32 [n_own, H] -> the token owners' return buffers."""
         self._scatter(out, None, plan.c_rank, plan.c_row, plan.c_rank.numel(), False, self._ret, stream)
@@ -541,14 +552,17 @@ class ExpertParallelRunner:
                 out = torch.empty((n_rows, H), dtype=torch.float32, device=x.device)
             call("xpgb_session_acquire", h, g, st)
             if n_rows and e1 > e0:
+                # peer windows: the last window leaves its split-K partials for the fused
+                # reduce + combine scatter; NCCL reduces into `out` here
+                reduce = 1 if (last and peer is None) else 0
                 call("xpgb_experts_forward_range", h, layer, C.c_void_p(rows_ptr),
-                     C.c_void_p(plan.offsets.data_ptr()), n_rows, e0, e1, 1 if last else 0,
+                     C.c_void_p(plan.offsets.data_ptr()), n_rows, e0, e1, reduce,
                      C.c_void_p(out.data_ptr()), st)
             call("xpgb_session_release", h, g, st)
             call("xpgb_session_materialize", h, g + 2)
             if last:
                 if peer is not None:
-                    ret = peer.combine(out, plan, stream)
+                    ret = peer.reduce_combine(self.ctx, plan, stream)
                     y = torch.empty((T, H), dtype=torch.float32, device=x.device)
                     if T:
                         call("xpgb_combine_rows", C.c_void_p(ret), C.c_void_p(plan.ret_index.data_ptr()), T, kk,
