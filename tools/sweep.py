@@ -40,6 +40,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--raw", action="store_true")
+    ap.add_argument("--budget", type=float, default=0.25, help="tokens: the expert-HBM budget every point plans for")
     ap.add_argument("--depth", type=int, default=None, help="budget: windows in flight on the planned ring (default: the planner picks 1 or 2)")
     ap.add_argument("--window", type=int, default=None, help="budget: experts per ring window")
     ap.add_argument("--stage-bufs", type=int, default=None, help="staging buffers per kind (host codec)")
@@ -89,12 +90,13 @@ def main():
                                   ring_experts=(p if what == "ring" else None), stage_buffers=args.stage_bufs,
                                   **run_kw)
         plan = None
-        if what == "plan":
+        if what in ("plan", "tokens"):
             from paper_2604_02715_b200.budget import plan_residency
 
             Lc = cspec.experts_per_layer
             ceb = runner.device_tier_bytes(Lc) / (N * Lc) * 1.002
-            plan = plan_residency(N, Lc, spec.expert_bytes, ceb, p * budget_base, shared_bytes=shared_b,
+            b = p if what == "plan" else args.budget
+            plan = plan_residency(N, Lc, spec.expert_bytes, ceb, b * budget_base, shared_bytes=shared_b,
                                   depth=args.depth, window=args.window)
             runner.apply_plan(plan)
         runner.run(args.warmup, acts=x)
