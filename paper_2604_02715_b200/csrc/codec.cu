@@ -152,10 +152,11 @@ __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 
 
 // One thread decodes one chunk (`chunk` values) starting at index[c]: a 64-bit
 // MSB-first window and a multi-symbol table -- every 11-bit pattern maps to the
-// up-to-3 whole codewords it starts with (exponents average ~2.6 bits, so one
-// lookup usually yields 3 values).  Codes longer than the table, and a chunk's
+// up-to-4 whole codewords it starts with (exponents average ~2.6 bits, so one
+// lookup usually yields 3-4 values); the symbols sit in one 32-bit table and the
+// count/length in a byte table beside it.  Codes longer than the table, and a chunk's
 // last values (never decode past the chunk), take the canonical first-code search.
-// The table is 8 KB of shared memory so decode blocks still fit beside a resident
+// The tables are 10 KB of shared memory so decode blocks still fit beside a resident
 // GEMM CTA; the next bitstream word is always in flight.  Output words are
 // (sign << 15) | (exponent << 7) | mantissa, 16 per 32-byte store.
 constexpr int kMultiBits = 11;
@@ -197,7 +198,7 @@ struct WordScalar {
 
 template <bool FAST, class R>
 __device__ __forceinline__ void decode_chunk(R& q, uint64_t win, int avail, const uint8_t* __restrict__ sm,
-                                             uint16_t* __restrict__ out, uint64_t v0, uint64_t v1, const uint32_t* lut3,
+                                             uint16_t* __restrict__ out, uint64_t v0, uint64_t v1, const uint32_t* lut3, const uint8_t* lmeta,
                                              int ml, const int* count, const uint32_t* first_code,
                                              const int* first_rank, const uint8_t* sorted_sym);
 
@@ -205,7 +206,8 @@ __device__ __forceinline__ void decode_chunk(R& q, uint64_t win, int avail, cons
 // decoder CTA's shared memory (building them per CTA cost ~20 us per launch -- most of a
 // small tensor's decode).
 struct DecTables {
-  uint32_t lut3[1 << kMultiBits];  // syms (3 x 8 b) | count << 24 | total length << 26
+  uint32_t lut3[1 << kMultiBits];  // up to 4 symbols (4 x 8 b)
+  uint8_t lmeta[1 << kMultiBits];  // count | total length << 3
   uint32_t first_code[kCodecMaxLen + 1];
   int count[kCodecMaxLen + 1], first_rank[kCodecMaxLen + 1];
   uint8_t sorted_sym[kCodecSymbols];
@@ -214,6 +216,7 @@ struct DecTables {
 
 __global__ void __launch_bounds__(256) k_build_tables(const CodecTable table, DecTables* out) {
   __shared__ uint32_t lut3[1 << kMultiBits];
+  __shared__ uint8_t lmeta[1 << kMultiBits];
   __shared__ uint32_t first_code[kCodecMaxLen + 1];
   __shared__ int count[kCodecMaxLen + 1], first_rank[kCodecMaxLen + 1];
   __shared__ uint8_t sorted_sym[kCodecSymbols];
@@ -257,7 +260,7 @@ __global__ void __launch_bounds__(256) k_build_tables(const CodecTable table, De
     const uint64_t w = (uint64_t)i << (64 - kMultiBits);
     uint32_t syms = 0;
     int tot = 0, c = 0;
-    while (c < 3) {
+    while (c < 4) {
       int sym;
       const int l = canon_decode(w << tot, ml, count, first_code, first_rank, sorted_sym, &sym);
       if (!l || tot + l > kMultiBits) break;
@@ -265,11 +268,15 @@ __global__ void __launch_bounds__(256) k_build_tables(const CodecTable table, De
       tot += l;
       ++c;
     }
-    lut3[i] = syms | ((uint32_t)c << 24) | ((uint32_t)tot << 26);
+    lut3[i] = syms;
+    lmeta[i] = (uint8_t)(c | (tot << 3));
   }
   __syncthreads();
 
-  for (int i = tid; i < (1 << kMultiBits); i += blockDim.x) out->lut3[i] = lut3[i];
+  for (int i = tid; i < (1 << kMultiBits); i += blockDim.x) {
+    out->lut3[i] = lut3[i];
+    out->lmeta[i] = lmeta[i];
+  }
   if (tid <= kCodecMaxLen) {
     out->first_code[tid] = first_code[tid];
     out->count[tid] = count[tid];
@@ -281,6 +288,7 @@ __global__ void __launch_bounds__(256) k_build_tables(const CodecTable table, De
 
 __global__ void __launch_bounds__(256) k_exp_decode(const __grid_constant__ DecodeParams p) {
   __shared__ uint32_t lut3[1 << kMultiBits];
+  __shared__ __align__(16) uint8_t lmeta[1 << kMultiBits];
   __shared__ uint32_t first_code[kCodecMaxLen + 1];
   __shared__ int count[kCodecMaxLen + 1], first_rank[kCodecMaxLen + 1];
   __shared__ uint8_t sorted_sym[kCodecSymbols];
@@ -290,6 +298,8 @@ __global__ void __launch_bounds__(256) k_exp_decode(const __grid_constant__ Deco
     const uint4* src = reinterpret_cast<const uint4*>(t->lut3);
     uint4* dst = reinterpret_cast<uint4*>(lut3);
     for (int i = tid; i < (1 << kMultiBits) / 4; i += blockDim.x) dst[i] = src[i];
+    for (int i = tid; i < (1 << kMultiBits) / 16; i += blockDim.x)
+      reinterpret_cast<uint4*>(lmeta)[i] = reinterpret_cast<const uint4*>(t->lmeta)[i];
     if (tid <= kCodecMaxLen) {
       first_code[tid] = t->first_code[tid];
       count[tid] = t->count[tid];
@@ -317,13 +327,13 @@ __global__ void __launch_bounds__(256) k_exp_decode(const __grid_constant__ Deco
     int avail = 64 - (int)sh;
     WordScalar q;
     q.init(d.bits + w + 2);
-    decode_chunk<true>(q, win, avail, sm, out, v0, v1, lut3, ml, count, first_code, first_rank, sorted_sym);
+    decode_chunk<true>(q, win, avail, sm, out, v0, v1, lut3, lmeta, ml, count, first_code, first_rank, sorted_sym);
   }
 }
 
 template <bool FAST, class R>
 __device__ __forceinline__ void decode_chunk(R& q, uint64_t win, int avail, const uint8_t* __restrict__ sm,
-                                             uint16_t* __restrict__ out, uint64_t v0, uint64_t v1, const uint32_t* lut3,
+                                             uint16_t* __restrict__ out, uint64_t v0, uint64_t v1, const uint32_t* lut3, const uint8_t* lmeta,
                                              int ml, const int* count, const uint32_t* first_code,
                                              const int* first_rank, const uint8_t* sorted_sym) {
   // exponent bytes decoded but not yet written: b0 = values 0..7 of the group, b1 = 8..15,
@@ -348,8 +358,10 @@ __device__ __forceinline__ void decode_chunk(R& q, uint64_t win, int avail, cons
         // one lookup: the fast path needs kMultiBits valid bits, the canonical path (codes
         // longer than the table) refills to >= 32 first
         auto step = [&]() {
-          const uint32_t e = lut3[win >> (64 - kMultiBits)];
-          int k = (e >> 24) & 3, l;
+          const uint32_t ix = (uint32_t)(win >> (64 - kMultiBits));
+          const uint32_t e = lut3[ix];
+          const uint32_t mt = lmeta[ix];
+          int k = mt & 7, l;
           uint64_t bytes;
           if (__builtin_expect(k == 0, 0)) {
             if (avail < 32) {
@@ -361,14 +373,14 @@ __device__ __forceinline__ void decode_chunk(R& q, uint64_t win, int avail, cons
             bytes = (uint32_t)sym;
             k = 1;
           } else {
-            l = (int)(e >> 26);
-            bytes = e & 0xFFFFFFu;
+            l = (int)(mt >> 3);
+            bytes = e;
           }
           win <<= l;
           avail -= l;
           const int sh = 8 * np;
           cur |= bytes << sh;
-          carry |= np > 5 ? bytes >> (64 - sh) : 0ull;
+          carry |= np > 4 ? bytes >> (64 - sh) : 0ull;
           np += k;
         };
         while (np < 8) {
@@ -402,8 +414,10 @@ __device__ __forceinline__ void decode_chunk(R& q, uint64_t win, int avail, cons
         win |= (uint64_t)q.pop() << (32 - avail);
         avail += 32;
       }
-      const uint32_t e = lut3[win >> (64 - kMultiBits)];
-      int k = (e >> 24) & 3, l;
+      const uint32_t ix = (uint32_t)(win >> (64 - kMultiBits));
+      const uint32_t e = lut3[ix];
+      const uint32_t mt = lmeta[ix];
+      int k = mt & 7, l;
       uint64_t bytes;
       if (k == 0 || k > (int)(v1 - v) - np) {
         int sym = 0;
@@ -411,18 +425,18 @@ __device__ __forceinline__ void decode_chunk(R& q, uint64_t win, int avail, cons
         bytes = (uint32_t)sym;
         k = 1;
       } else {
-        l = (int)(e >> 26);
-        bytes = e & 0xFFFFFFu;
+        l = (int)(mt >> 3);
+        bytes = e;
       }
       win <<= l;
       avail -= l;
       if (np < 8) {
         b0 |= bytes << (8 * np);
-        if (np > 5) b1 |= bytes >> (64 - 8 * np);
+        if (np > 4) b1 |= bytes >> (64 - 8 * np);
       } else {
         const int q = np - 8;
         b1 |= bytes << (8 * q);
-        if (q > 5) b2 |= bytes >> (64 - 8 * q);
+        if (q > 4) b2 |= bytes >> (64 - 8 * q);
       }
       np += k;
     }
