@@ -147,3 +147,51 @@ def test_plan_bookkeeping_is_consistent():
     # every pair is sent exactly once, to the owner of its expert
     total = sum(sum(p.send_counts) for p in plans)
     assert total == world * Tloc * k
+
+
+@pytest.mark.parametrize("world,Tloc,Lx,k", [(2, 5, 8, 2), (3, 7, 10, 3), (8, 4, 256, 8), (4, 1, 6, 6)])
+def test_peer_exchange_positions_match_the_collective(world, Tloc, Lx, k):
+    """The peer-memory exchange's row positions (build_plan's p2p_* / c_* fields), replayed
+    on host arrays, land every row exactly where the collective path puts it: dispatch rows
+    at the owner's expert-major position, combine rows at the sender's return position."""
+    from oracle import xpg_oracle as O
+
+    bounds = shard_bounds(Lx, world)
+    routes = torch.from_numpy(O.route(9, world * Tloc, 1, Lx, k).astype(np.int64))
+    plans = [build_plan(routes, r, world, Tloc, bounds) for r in range(world)]
+    H = 4
+    xs = [torch.arange(Tloc * H, dtype=torch.float32).reshape(Tloc, H) + 1000 * r for r in range(world)]
+    # collective path: send buffers, all-to-all by counts, expert-major permutation
+    sends = [xs[r].index_select(0, plans[r].send_rows) for r in range(world)]
+    recv = []
+    for d in range(world):
+        parts = []
+        for r in range(world):
+            off = sum(plans[r].send_counts[:d])
+            parts.append(sends[r][off:off + plans[r].send_counts[d]])
+        recv.append(torch.cat(parts).index_select(0, plans[d].to_expert))
+    # peer path: every rank scatters straight into the owners' windows
+    win = [torch.full((int(plans[d].c_rank.numel()), H), float("nan")) for d in range(world)]
+    for r in range(world):
+        p = plans[r]
+        for i in range(p.p2p_src_rows.numel()):
+            win[int(p.p2p_dst_rank[i])][int(p.p2p_dst_row[i])] = xs[r][int(p.p2p_src_rows[i])]
+    for d in range(world):
+        assert torch.equal(win[d], recv[d])
+    # combine: owner rows back to the senders' return buffers
+    outs = [recv[d] * 2 + 1 for d in range(world)]  # stand-in expert outputs, expert-major
+    ret_coll = []
+    for r in range(world):
+        parts = []
+        for d in range(world):
+            back = outs[d].index_select(0, plans[d].from_expert)
+            off = sum(plans[d].recv_counts[:r])
+            parts.append(back[off:off + plans[d].recv_counts[r]])
+        ret_coll.append(torch.cat(parts))
+    ret = [torch.full((Tloc * min(k, Lx), H), float("nan")) for _ in range(world)]
+    for d in range(world):
+        p = plans[d]
+        for i in range(p.c_rank.numel()):
+            ret[int(p.c_rank[i])][int(p.c_row[i])] = outs[d][i]
+    for r in range(world):
+        assert torch.equal(ret[r], ret_coll[r])
