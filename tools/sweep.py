@@ -43,6 +43,7 @@ def main():
     ap.add_argument("--budget", type=float, default=0.25, help="tokens: the expert-HBM budget every point plans for")
     ap.add_argument("--depth", type=int, default=None, help="budget: windows in flight on the planned ring (default: the planner picks 1 or 2)")
     ap.add_argument("--window", type=int, default=None, help="budget: experts per ring window")
+    ap.add_argument("--b-dec", type=float, default=None, help="budget: the planner's decoder GB/s (model input)")
     ap.add_argument("--stage-bufs", type=int, default=None, help="staging buffers per kind (host codec)")
     ap.add_argument("--rings", default="6,8,12", help="sub-layer ring sizes (expert blocks per kind) for budget")
     args = ap.parse_args()
@@ -97,7 +98,8 @@ def main():
             ceb = runner.device_tier_bytes(Lc) / (N * Lc) * 1.002
             b = p if what == "plan" else args.budget
             plan = plan_residency(N, Lc, spec.expert_bytes, ceb, b * budget_base, shared_bytes=shared_b,
-                                  depth=args.depth, window=args.window)
+                                  depth=args.depth, window=args.window,
+                                  **({"b_dec": args.b_dec * 1e9} if args.b_dec else {}))
             runner.apply_plan(plan)
         runner.run(args.warmup, acts=x)
         secs, rep = timed(torch, lambda s: runner.run(s, acts=x), args.steps)
