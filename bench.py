@@ -350,7 +350,7 @@ def main():
                     help="spend the budget on a compressed device tier + small ring (FluxMoE), or ring only")
     ap.add_argument("--prefill", action="store_true",
                     help="prefill regime: one step = a T-token prompt chunk through every layer (default T=8192)")
-    ap.add_argument("--cpu-sample-tokens", type=int, default=4)
+    ap.add_argument("--cpu-sample-tokens", type=int, default=16)  # ~10 s of host work at Mixtral shape
     ap.add_argument("--ref-sample-tokens", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-resident", action="store_true")
