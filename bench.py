@@ -82,13 +82,13 @@ def ncu_traffic(config: str, tokens: int):
 def ncu_decoder_capture():
     """DRAM traffic vs algorithmic bytes of one decoder launch (Mixtral gate/up tensor) from
     the committed ncu --set full capture."""
-    path = os.path.join(ROOT, "profiles", "r1_ncu_exp_decode_v6.jsonl")
+    path = os.path.join(ROOT, "profiles", "r1_ncu_exp_decode_v7.jsonl")
     try:
         rec = json.loads(open(path).readline())
         n = 117_440_512  # values of the captured tensor (tools/profile_codec.py default)
         algo = n + n * 2.591 / 8 + n / 256 * 4 + 2 * n
         return {"dram_bytes": rec["dram_read"] + rec["dram_write"], "algorithmic_bytes": algo,
-                "source": "profiles/r1_ncu_exp_decode_v6.jsonl (one 117.4M-value tensor, chunk 256)"}
+                "source": "profiles/r1_ncu_exp_decode_v7.jsonl (one 117.4M-value tensor, chunk 256)"}
     except Exception:
         return None
 
