@@ -108,8 +108,8 @@ def decoder_roofline(stats, steps, step_s, hbm_peak, hbm_src):
             "launches_per_step": n / steps, "kernel_time_per_step_ms": stats["kernel_ns"] / steps / 1e6,
             "step_ms": step_s * 1e3 / steps,
             "note": "launches overlap each other (two kinds, host and device tiers) and the GEMMs, so a launch's "
-                    "time includes sharing the SMs; standalone the kernel reaches 1,265 GB/s of bf16 output "
-                    "(profiles/r1_decoder_chunk_grid_sweep.txt)",
+                    "time includes sharing the SMs; standalone the kernel reaches ~1,450-1,600 GB/s of bf16 output "
+                    "on a 117M-value tensor (profiles/r1_decoder_experiments.md)",
             "traffic": None, "traffic_capture": ncu_decoder_capture()}
 
 
