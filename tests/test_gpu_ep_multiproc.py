@@ -131,3 +131,20 @@ def test_ep_decode_session_matches_run():
             got = sess.step(torch.from_numpy(x).pin_memory(), out=out)
             assert got.numpy().tobytes() == w.tobytes()
     runner.close()
+
+
+@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+def test_ep_empty_step(transport):
+    """T = 0 under EP: the step still pages and exchanges (epochs published with no rows)
+    and returns an empty batch."""
+    import paper_2604_02715_b200 as X
+    from paper_2604_02715_b200.expert_parallel import ExpertParallelRunner
+
+    spec = X.ModelSpec(*SPEC)
+    fwd = X.ForwardSpec(0, K, SEED)
+    container = X.generate_synthetic_model(spec, SEED)
+    runner = ExpertParallelRunner(spec, container, fwd, 0, 1, host_codec=True, transport=transport)
+    rep = runner.run(2, np.zeros((0, spec.hidden_dim), np.float32))
+    runner.close()
+    assert tuple(rep.final_activations.shape) == (0, spec.hidden_dim)
+    assert rep.page_fault is None and rep.violations == []
