@@ -263,3 +263,22 @@ def test_residency_plan_narrows_windows_for_small_budgets():
     eb = 786432
     pl = plan_residency(4, 8, eb, 0.68 * eb, 0.25 * 32 * eb * 0.998)
     assert 0 < pl.ring < 8 and pl.hbm_bytes <= 0.25 * 32 * eb
+
+
+def test_residency_plan_spaces_host_experts_and_picks_depth():
+    """Host-tier experts are spaced over the layers (not bunched at the ends), and the ring
+    keeps one window in flight only while the plan is clearly link-bound."""
+    import numpy as np
+
+    from paper_2604_02715_b200.budget import _spaced, plan_residency
+
+    assert _spaced(3, 8) == [0, 1, 0, 0, 1, 0, 1, 0] and _spaced(10, 8) == [1, 1, 2, 1, 1, 1, 2, 1]
+    assert sum(_spaced(13, 7)) == 13 and max(_spaced(13, 7)) - min(_spaced(13, 7)) <= 1
+    eb = 352321536
+    ceb = 0.6655 * 1.012 * eb
+    pl = plan_residency(8, 8, eb, ceb, 0.8 * 64 * eb)
+    host = (~(pl.device_mask | pl.pinned_mask)).sum(axis=1)
+    gaps = np.diff(np.flatnonzero(host))
+    assert host.sum() >= 2 and gaps.min() >= 2  # never in adjacent layers at this budget
+    assert plan_residency(8, 8, eb, ceb, 0.25 * 64 * eb).depth == 1
+    assert plan_residency(8, 8, eb, ceb, 0.8 * 64 * eb).depth == 2
