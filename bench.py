@@ -596,7 +596,8 @@ def main():
     # launch list: profiles/r1_launches_bench_mixtral_codec.json); the GEMM roofline rides along
     dec_roof = decoder_roofline(dec_stats, args.steps, elapsed, hbm_peak, peak_src)
     if dec_roof is not None:
-        dec_roof["gemm"] = roof
+        if roof.get("achieved"):  # EP runs have no resident comparator to time the GEMMs on
+            dec_roof["gemm"] = roof
         roof = dec_roof
 
     line = {
