@@ -1,16 +1,25 @@
 #!/usr/bin/env python
 """Benchmark: MoE decode tokens/s at a fixed expert-HBM budget, page-in GB/s, exposed transfer %.
 
-Workload (BASELINE.json configs[1]): Mixtral-8x7B-shaped MoE stack — 8 layers,
-8 experts, top-2, hidden 4096, ffn 14336, bf16 weights (random init, N(0, 0.02)),
-one B200, 25% of expert bytes HBM-resident (the reference's 2-layer ring, host-only
-backend: every expert of every layer is paged in from pinned host memory each
-decode step).  A step = one decode iteration of T=256 tokens through all 8 layers.
+Workload (BASELINE.json configs[1]): Mixtral-8x7B-shaped MoE stack -- 8 layers, 8 experts,
+top-2, hidden 4096, ffn 14336, bf16 weights from the reference generator (model.py:205-214),
+one B200, 25% of the expert bytes in HBM.  The budget counts everything the path keeps in HBM
+for expert weights: ring blocks, the compressed device tier, pinned experts, shared experts,
+the codec's staging buffers and the device-resident chunk index (``expert_hbm_footprint``).
+By default it is spent FluxMoE-style by the budget planner (budget.plan_residency): a
+one-expert sub-layer ring, experts compressed in HBM (device tier), the rest streamed from
+pinned host memory as exponent-Huffman records over PCIe and decoded on the GPU; ``--tiering
+ring`` keeps the reference's 2-layer ring.  A step = one decode iteration of T=256 tokens
+through all 8 layers.  Every timed run is checked for page faults and ordering violations;
+the line is not printed when one is found.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
+--gpus N without torchrun re-launches itself under torch.distributed.run with N ranks.
 --impl reference times the reference algorithm's CPU path (the oracle port in
-oracle/cpu_reference.py) on the host cores, on a bounded sample per step.
+oracle/cpu_reference.py) on the host cores: each step is a bounded, really timed sample (one
+layer's page-in plus the per-token forward of a few tokens of the step), and the line's
+value extrapolates it linearly to the workload (8 layers x 256 tokens).
 """
 
 from __future__ import annotations
@@ -200,7 +209,28 @@ def h2d_peak_gbps(torch, device: int) -> float:
     return best
 
 
-def dist_setup():
+def spawn_ranks(args) -> int:
+    """bench.py --gpus N without torchrun: re-launch under torch.distributed.run with N ranks
+    (one per GPU).  Fewer visible GPUs than N is an error unless --oversubscribe, which puts
+    ranks round-robin on the GPUs there are (a test of the N-rank path, not a scaling number;
+    the line says so)."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus and not args.oversubscribe:
+        raise SystemExit(f"bench: --gpus {args.gpus} but only {have} GPU(s) visible "
+                         "(--oversubscribe runs the ranks on shared GPUs)")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def dist_setup(oversubscribe: bool = False):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -209,8 +239,15 @@ def dist_setup():
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        torch.cuda.set_device(local)  # one rank per GPU, bound before NCCL picks a device
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if oversubscribe:
+            # ranks share GPUs: NCCL refuses two ranks on one device, so the plumbing (barrier,
+            # max over ranks) runs on gloo; the EP data path uses peer windows (CUDA IPC)
+            local = local % max(1, torch.cuda.device_count())
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)  # one rank per GPU, bound before NCCL picks a device
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     return world, rank, local
 
 
@@ -219,7 +256,8 @@ def max_over_ranks(torch, world: int, value: float, device: int) -> float:
         return value
     import torch.distributed as dist
 
-    t = torch.tensor([value], dtype=torch.float64, device=f"cuda:{device}")
+    on_gpu = dist.get_backend() == "nccl"
+    t = torch.tensor([value], dtype=torch.float64, device=f"cuda:{device}" if on_gpu else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -282,7 +320,11 @@ def run_reference_arm(args, cfg):
     rng = np.random.default_rng(SEED)
     if layer_words * 2 <= (4 << 30):
         # weights of layer 1 (all the sample touches): the reference generator's first draws
-        words = O.f32_to_bf16(rng.standard_normal(layer_words, dtype=np.float32) * O.WEIGHT_STD)
+        # (numpy's PCG64 stream decoded in parallel segments; data setup, outside the timing)
+        from paper_2604_02715_b200.geometry import _fill_normal_bf16
+
+        words = np.empty(layer_words, dtype=np.uint16)
+        _fill_normal_bf16(SEED, [words])
         step_fn = lambda: cpu_reference.decode_rate(words, cfg["N"], cfg["L"], H, F, cfg["T"], cfg["k"], SEED, sample)
     else:
         # a layer too large to hold (DSv3: 22.5 GB): draw only the experts the sample routes to
@@ -299,28 +341,55 @@ def run_reference_arm(args, cfg):
         step_fn = lambda: cpu_reference.decode_rate_sampled(lambda layer, j, kind: pool[j][kind - 1], cfg["N"],
                                                             cfg["L"], H, F, cfg["T"], cfg["k"], SEED, sample,
                                                             shared_words=shared)
-    times, rates = [], []
+    samples = []
     for i in range(args.warmup + args.steps):
+        w0 = time.perf_counter()
         r = step_fn()
+        wall = time.perf_counter() - w0
         if i >= args.warmup:
-            times.append(r["step_s"])
-            rates.append(r["tok_s"])
-    value = cfg["T"] * len(times) / sum(times)
+            samples.append((wall, r))
+    # each step is a real, timed bounded sample: one layer's page-in (all L experts copied into
+    # the arena, storage.py:235-243) + the reference per-token forward of `sample` tokens of
+    # the step (pipeline.py:192-208).  The workload's rate is the linear extrapolation of the
+    # measured costs: every layer does the same work, and a step is N x (fetch + T x per-token).
+    fetch = sum(r["fetch_s"] for _, r in samples) / len(samples)
+    per_tok = sum(r["per_token_s"] for _, r in samples) / len(samples)
+    full_step = cfg["N"] * (fetch + cfg["T"] * per_tok)
+    value = cfg["T"] / full_step
+    wall_ms = 1e3 * sum(w for w, _ in samples) / len(samples)
+    sample_desc = (f"per step: layer-1 page-in of {cfg['L']} experts ({fetch:.2f}s) + reference per-token forward "
+                   f"of {sample} of the step's {cfg['T']} tokens ({per_tok:.2f}s/token), really timed; value = "
+                   f"T / (N x (fetch + T x per-token)) for N={cfg['N']} layers, T={cfg['T']} "
+                   f"(oracle/cpu_reference.py, a port of xpg pipeline.py/storage.py)")
     line = {
-        "impl": "reference", "metric": METRIC_PREFILL if args.prefill else METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+        "impl": "reference", "metric": METRIC_PREFILL if args.prefill else METRIC, "value": value,
+        "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": wall_ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (reference generator, seed 7)",
-        "config": {"workload": cfg["name"], "tokens_per_step": cfg["T"], "top_k": cfg["k"], "budget": "25% (2-layer ring, host-only)"},
+        "config": {"workload": cfg["name"], "tokens_per_step": cfg["T"], "top_k": cfg["k"], "layers": cfg["N"]},
+        "sample": {"tokens": sample, "layers": 1, "measured_ms_per_sample": wall_ms,
+                   "fetch_s_per_layer": fetch, "per_token_s_per_layer": per_tok,
+                   "extrapolated_ms_per_full_step": 1e3 * full_step,
+                   "measured_tok_s_at_sample_batch": sample / (cfg["N"] * (fetch + sample * per_tok))},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
-                         "sample": f"per step: one layer page-in + reference per-token forward on {sample} tokens, "
-                                   f"extrapolated to {cfg['N']} layers x T={cfg['T']} (oracle/cpu_reference.py)"},
+                         "sample": sample_desc},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 _T0 = time.time()
+_VERIFIED = []
+
+
+def verify(what: str, fault, violations) -> None:
+    """A timed run must have done all its work: a device page fault makes every kernel of the
+    step return early (only the copies would be timed), an ordering violation means a RAW/WAR
+    hazard.  Either one aborts the bench before a number is printed."""
+    if fault is not None or violations:
+        raise SystemExit(f"bench: {what} is invalid: page_fault={fault!r} violations={list(violations)[:3]}")
+    _VERIFIED.append(what)
 
 
 def log(msg):
@@ -358,10 +427,19 @@ def main():
     ap.add_argument("--transport", default="auto", choices=["auto", "p2p", "nccl"],
                     help="EP dispatch/combine: peer-memory scatter kernels (p2p), NCCL all_to_all, or p2p when "
                          "every peer window opens (auto)")
+    ap.add_argument("--weights", default=None, choices=["reference", "fast"],
+                    help="reference: the reference generator's bf16 weights (bit-identical, default when the "
+                         "model's stream is <= 32 GB); fast: the same distribution drawn on the GPU (torch Philox)")
+    ap.add_argument("--oversubscribe", action="store_true",
+                    help="--gpus N with fewer GPUs: run the N ranks on shared GPUs (tests the N-rank path)")
     ap.add_argument("--raw", action="store_true",
                     help="page raw bf16 over PCIe (the reference host tier) instead of exponent-Huffman records")
     args = ap.parse_args()
     args.host_codec = not args.raw
+    if args.weights is None:
+        c0 = CONFIGS[args.config]
+        stream = c0["N"] * (c0["L"] + c0.get("S", 0)) * 6 * c0["H"] * c0["F"]  # bytes of the generator stream
+        args.weights = "reference" if stream <= (32 << 30) and not c0.get("ep_virtual") else "fast"
     cfg = dict(CONFIGS[args.config])
     if args.prefill and not args.tokens:
         args.tokens = 8192
@@ -371,7 +449,11 @@ def main():
         run_reference_arm(args, cfg)
         return
 
-    world, rank, local = dist_setup()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    world, rank, local = dist_setup(args.oversubscribe)
+    if world != args.gpus and args.gpus > 1:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
     import numpy as np
     import torch
 
@@ -404,6 +486,9 @@ def main():
         shard = X.generate_fast_model(X.ModelSpec(N, count, H, F), SEED + 1000 * rank, device=dev,
                                       shared_experts=S)
         container = None
+    elif args.weights == "reference":
+        # the reference generator (model.py:205-214), bit-identical, decoded in parallel segments
+        container = X.generate_synthetic_model(cspec, SEED + rank, shared_experts=S)
     else:
         container = X.generate_fast_model(cspec, SEED + rank, device=dev, shared_experts=S)
     gen_s = time.time() - t0
@@ -425,7 +510,7 @@ def main():
             ceb = runner.device_tier_bytes(count) / (N * count) * 1.002
             sh_b = shard.shared.total_bytes if shard.shared is not None else 0
             plan = plan_residency(N, count, shard.spec.expert_bytes, ceb, args.budget * shard_bytes * 0.998,
-                                  shared_bytes=sh_b)
+                                  shared_bytes=sh_b, overhead_bytes=runner.ctx.hbm_bytes()["staging"])
             if plan.device_experts or plan.pinned_experts:
                 runner.apply_plan(plan)
                 m_dev, pinned_per_layer = plan.device_experts / N, plan.pinned_experts / N
@@ -469,12 +554,14 @@ def main():
         # simulate.py:50-66).  --tiering device (default with the codec) spends the budget like
         # FluxMoE: a small sub-layer ring, and every byte left holds experts 1..m of each layer
         # compressed in HBM (decoded on-GPU into the ring), so only L-m experts per layer cross
-        # PCIe; --tiering ring keeps the reference's ring-only geometry.  The codec's transient
-        # staging buffers and chunk index are reported beside it (footprint).
+        # PCIe; --tiering ring keeps the reference's ring-only geometry.  The codec's staging
+        # buffers and device-resident chunk index are part of the footprint the budget bounds.
         eb = cspec.expert_bytes
         shared_b = container.shared.total_bytes if container.shared is not None else 0
         ring_blocks = (hbm["ring"] - shared_b) // eb
-        cap = args.budget * expert_bytes * 0.998 - shared_b  # margin: record sizes vary a little per expert
+        # the codec's staging buffers and device-resident chunk index count inside the budget
+        overhead = hbm["staging"]
+        cap = args.budget * expert_bytes * 0.998 - shared_b - overhead  # margin: record sizes vary per expert
         m_dev = 0
         pinned_per_layer = 0
         if args.tiering == "device" and args.host_codec:
@@ -482,7 +569,8 @@ def main():
 
             Lc, Nl = cspec.experts_per_layer, cspec.num_layers
             ceb = runner.device_tier_bytes(Lc) / (Nl * Lc) * 1.002  # compressed expert (+ margin)
-            plan = plan_residency(Nl, Lc, eb, ceb, cap + shared_b, shared_bytes=shared_b)
+            plan = plan_residency(Nl, Lc, eb, ceb, cap + shared_b + overhead, shared_bytes=shared_b,
+                                  overhead_bytes=overhead)
             if plan.device_experts or plan.pinned_experts:
                 runner.apply_plan(plan)
                 ring_blocks = min(plan.ring, ring_blocks) if plan.ring else ring_blocks
@@ -515,6 +603,7 @@ def main():
         ev1.record()
         torch.cuda.synchronize()
         launches = kernel_launches() - launches0
+    verify("timed paged run", rep.page_fault, rep.violations)
     barrier(world)
     elapsed = max_over_ranks(torch, world, ev0.elapsed_time(ev1) * 1e-3, dev)
     tokens_total = T * args.steps * world
@@ -541,7 +630,8 @@ def main():
         out = sess.step(x_pin, out=out_pin)  # pinned H2D in, D2H out, every step
     e1.record()
     torch.cuda.synchronize()
-    sess.close()
+    srep = sess.close()
+    verify("e2e session", srep.page_fault, srep.violations)
     del sess  # the session holds the runner (and its HBM ring) alive
     e2e_elapsed = max_over_ranks(torch, world, e0.elapsed_time(e1) * 1e-3, dev)
     if use_ep:
@@ -567,6 +657,7 @@ def main():
         _, rrep = model.run(args.steps, fwd, x_dev, profile=True)
         r1.record()
         torch.cuda.synchronize()
+        verify("resident run", model.ctx.fault() if rrep.page_fault else None, [])
         rt = r0.elapsed_time(r1) * 1e-3
         resident = {"tok_s": T * args.steps / rt, "ms_per_step": 1e3 * rt / args.steps}
         kern = {n: getattr(rrep, n) for n in ("kern_gate_up_ns", "kern_down_ns", "kern_aux_ns", "gate_up_bytes",
@@ -604,10 +695,16 @@ def main():
         "metric": METRIC_PREFILL if args.prefill else METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (random-init N(0,0.02) bf16 weights drawn on-GPU, N(0,1) activations)",
+        "data": ("synthetic: bf16 weights from the reference generator (default_rng(7) N(0,0.02), bit-identical "
+                 "to xpg model.py:205-214), N(0,1) activations" if args.weights == "reference" and not use_ep else
+                 "synthetic: random-init N(0,0.02) bf16 weights drawn on-GPU (torch Philox; the reference generator's "
+                 "stream for this model is too long to draw per run), N(0,1) activations"),
         "config": {"workload": cfg["name"], "tokens_per_step": T, "top_k": k, "layers": N,
-                   "expert_hbm_budget": round(budget, 4),
+                   "expert_hbm_budget": args.budget,
                    "expert_hbm_footprint": round(footprint, 4),
+                   "expert_hbm_weights": round(budget, 4),
+                   "footprint_counts": "ring + pinned + shared + compressed device tier + staging buffers + "
+                                       "device-resident chunk index, / expert bytes",
                    "ring_blocks_per_kind": int(ring_blocks) if not use_ep else None,
                    "device_tier_experts_per_layer": round(m_dev, 3),
                    "pinned_experts_per_layer": round(pinned_per_layer, 3),
@@ -620,7 +717,13 @@ def main():
                        ", host-only (alpha=0)") + (
                        ", exponent-Huffman records over PCIe decoded on-GPU into the ring (lossless)"
                        if args.host_codec else ""),
-                   "l2": "inputs larger than L2: all %.1f GB of expert weights stream from host each step" % (cspec.total_bytes / 1e9)},
+                   "l2": ("inputs larger than L2 (126 MB): each step reads %.1f GB of expert weights -- %.2f GB of "
+                          "records over PCIe, %.2f GB of bf16 decoded on-GPU from HBM records, the rest pinned/ring"
+                          % (cspec.total_bytes / 1e9, rep.h2d_bytes / args.steps / 1e9,
+                             rep.decoded_bytes / args.steps / 1e9))},
+        "verified": {"runs": list(_VERIFIED), "page_fault": None, "ordering_violations": 0,
+                     "note": "timed, e2e and resident runs checked for device page faults and RAW/WAR "
+                             "ordering violations (bench aborts otherwise)"},
         "page_in": {"achieved_gbps": page_in_gbps, "peak_gbps": h2d_peak, "frac": page_in_gbps / h2d_peak if h2d_peak else None,
                     "bytes_per_step": rep.h2d_bytes / args.steps, "peak_how": "pinned 1 GiB cudaMemcpyAsync H2D, best of 5, this box",
                     "host_codec": bool(args.host_codec),
@@ -646,6 +749,11 @@ def main():
         line["raw_host_tier"] = raw_path
     if use_ep:
         line["config"]["parallelism"] = f"ep{world} (experts sharded; dispatch/combine: {ep_transport}"
+        if args.oversubscribe:
+            import torch as _t
+
+            line["config"]["oversubscribed"] = (f"{world} ranks on {_t.cuda.device_count()} GPU(s): tests the "
+                                                f"{world}-rank path; not a scaling measurement")
         line["config"]["tokens_per_rank"] = T
     if G_virt > 1:
         line["config"]["parallelism"] = (f"rank 0 of ep{G_virt}: experts {run_kw['expert_shard'][0] + 1}.."

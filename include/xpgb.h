@@ -316,10 +316,14 @@ int xpgb_log_get(xpgb_ctx* ctx, xpgb_record* out, int32_t cap, int32_t* n);
  * shard [expert_first, expert_first+expert_count) of every layer. */
 int xpgb_set_expert_shard(xpgb_ctx* ctx, int32_t expert_first, int32_t expert_count);
 /* Grouped SwiGLU over rows already grouped by local expert:
- * rows_dev bf16 [n_rows][H], offsets_dev int32 [expert_count+1] device row ranges,
- * out_dev fp32 [n_rows][H] (expert output, unscaled).  Pages must be resident. */
-int xpgb_experts_forward(xpgb_ctx* ctx, int32_t layer, const void* rows_dev, const int32_t* offsets_dev,
-                         int32_t n_rows, float* out_dev, void* stream);
+ * rows_dev bf16 [2][lo_rows][H] -- the rows' hi plane bf16_rn(x), then their lo plane
+ * bf16_rn(x - hi) lo_rows rows later (the activations reach the tensor cores as both planes,
+ * so the expert math runs on x to ~2^-17 relative, as the reference's float32 x) -- read in
+ * place; offsets_dev int32 [expert_count+1] device row ranges (n_rows <= lo_rows is an upper
+ * bound of offsets[expert_count]); out_dev fp32 [n_rows][H] (expert output, unscaled).
+ * Pages must be resident. */
+int xpgb_experts_forward(xpgb_ctx* ctx, int32_t layer, const void* rows_dev, int64_t lo_rows,
+                         const int32_t* offsets_dev, int32_t n_rows, float* out_dev, void* stream);
 
 /* Ordered combine (pipeline.py:198-207) of rows returned by the expert owners:
  * y[t] = sum_{s ascending} rows[index[t][s]] * f32(1/top_k); index < 0 skips the slot.
@@ -343,24 +347,53 @@ int xpgb_ep_window_alloc(uint64_t bytes, void** dptr, void* ipc_handle64);
 int xpgb_ep_window_open(const void* ipc_handle64, void** dptr);
 int xpgb_ep_window_close(void* dptr);
 int xpgb_ep_window_free(void* dptr);
+/* to_bf16: the rows land as their two bf16 planes (hi at dst_row, lo at dst_row + lo_rows of
+ * the region).  n_dev (nullable): device row count (n is then an upper bound).  fault_dev
+ * (nullable, xpgb_fault_ptr): when this rank's fault word is set, no rows are written and
+ * every peer's fault word (int32 at index 32 of its flag array) is raised before the release.
+ * xpgb_ep_wait is bounded: after 20 s without an epoch, or when a peer raised this rank's
+ * fault word, it sets fault_dev (a "peer" fault, reported by xpgb_fault_get) instead of
+ * trapping -- the rank's later kernels skip and its report carries the fault. */
 int xpgb_ep_scatter_rows(const float* src_dev, const int32_t* src_rows, const int32_t* dst_rank, const int32_t* dst_row,
-                         int32_t n, int32_t hidden, int32_t to_bf16, void* const* peer_rows, int32_t* const* peer_flags,
-                         int32_t world, int32_t rank, int32_t epoch, uint32_t* counter, void* stream);
-int xpgb_ep_wait(const int32_t* flags_dev, int32_t world, int32_t epoch, void* stream);
+                         int32_t n, const int32_t* n_dev, int32_t hidden, int32_t to_bf16, int64_t lo_rows,
+                         void* const* peer_rows, int32_t* const* peer_flags, int32_t world, int32_t rank, int32_t epoch,
+                         const void* fault_dev, uint32_t* counter, void* stream);
+int xpgb_ep_wait(const int32_t* flags_dev, int32_t world, int32_t epoch, void* fault_dev, void* stream);
+/* Device pointer of the context's fault word (int64; 0 = no fault). */
+int xpgb_fault_ptr(xpgb_ctx* ctx, void** fault_dev);
+/* Test hook: overwrite the fault word (0 clears it; any other value makes the context's
+ * kernels skip as after a page fault). */
+int xpgb_fault_set(xpgb_ctx* ctx, int64_t word);
+/* Per-step dispatch plan of one rank, built on the device from the global routing table
+ * routes_dev int32 [world*tokens][kk] (xpgb_route's output: 1-based ids ascending per row) --
+ * one launch, no host round trip, recomputed every step as the reference routes every forward
+ * (pipeline.py:200-203).  Row positions follow expert_parallel.build_plan's canonical orders
+ * (send order (owner, expert, token); expert-major order (expert, global token)); experts are
+ * sharded contiguously and balanced (shard_bounds).  Buffers (device int32): src_rows,
+ * dst_rank, dst_row, ret_index [tokens*kk]; c_rank, c_row, to_arrival, from_arrival
+ * [world*tokens*kk] (n_own used); offsets [count+1]; counts [2*world+1] = rows sent to each
+ * rank, rows received from each rank, n_own.  scratch_dev: xpgb_ep_plan_scratch_words int32. */
+typedef struct xpgb_ep_plan_bufs {
+  int32_t *src_rows, *dst_rank, *dst_row, *ret_index, *c_rank, *c_row, *to_arrival, *from_arrival, *offsets, *counts;
+} xpgb_ep_plan_bufs;
+int64_t xpgb_ep_plan_scratch_words(int32_t world, int32_t tokens, int32_t num_experts);
+int xpgb_ep_plan(const int32_t* routes_dev, int32_t tokens, int32_t world, int32_t rank, int32_t kk,
+                 int32_t num_experts, int32_t* scratch_dev, const xpgb_ep_plan_bufs* out, void* stream);
 /* The combine fused with the down projection's split-K reduction: after
  * xpgb_experts_forward_range(..., reduce = 0) over a layer's last window, each of the n_rows
  * expert-major output rows is summed from ctx's partial planes and stored straight into
  * dst_rank[i]'s region at row dst_row[i] (f32); the last CTA releases `epoch` like
  * xpgb_ep_scatter_rows.  n_rows must be the rows of that experts_forward_range call. */
 int xpgb_ep_reduce_scatter(xpgb_ctx* ctx, const int32_t* dst_rank, const int32_t* dst_row, int32_t n_rows,
-                           void* const* peer_rows, int32_t* const* peer_flags, int32_t world, int32_t rank,
+                           const int32_t* n_dev, void* const* peer_rows, int32_t* const* peer_flags, int32_t world, int32_t rank,
                            int32_t epoch, uint32_t* counter, void* stream);
 
-/* One window of a layer on pre-grouped rows: GEMMs of local experts [e0, e1) only (rows stay
- * absolute; the rows are copied in with the e0 == 0 window); reduce = 1 on the layer's last
- * window writes every row's output (split-K partials of all windows are final by then). */
-int xpgb_experts_forward_range(xpgb_ctx* ctx, int32_t layer, const void* rows_dev, const int32_t* offsets_dev,
-                               int32_t n_rows, int32_t e0, int32_t e1, int32_t reduce, float* out_dev, void* stream);
+/* One window of a layer on pre-grouped rows (layout as xpgb_experts_forward): GEMMs of local
+ * experts [e0, e1) only (rows stay absolute); reduce = 1 on the layer's last window writes
+ * every row's output (split-K partials of all windows are final by then). */
+int xpgb_experts_forward_range(xpgb_ctx* ctx, int32_t layer, const void* rows_dev, int64_t lo_rows,
+                               const int32_t* offsets_dev, int32_t n_rows, int32_t e0, int32_t e1, int32_t reduce,
+                               float* out_dev, void* stream);
 int xpgb_combine_rows(const float* rows_dev, const int32_t* index_dev, int32_t tokens, int32_t kk, int32_t top_k,
                       int32_t hidden, float* y_dev, void* stream);
 

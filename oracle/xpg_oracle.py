@@ -279,6 +279,37 @@ def layer_forward(pool: WordPool, layer: int, acts: np.ndarray, top_k: int, seed
     return y
 
 
+def layer_forward_shard(pool: WordPool, layer: int, acts: np.ndarray, top_k: int, seed: int, num_experts: int,
+                        first: int = 0, shared: "SharedPool | None" = None, shared_rows=None) -> np.ndarray:
+    """One expert-parallel rank's share of a layer: ``layer_forward`` over the
+    ``num_experts``-wide router (pipeline.py:162-170), keeping only the routed experts
+    ``first+1 .. first+pool.L`` whose weights ``pool`` holds in shard-local order; the
+    other slots add nothing.  ``shared_rows=(r0, n)``: the rows the shared experts apply
+    to (this rank's own tokens; our convention).  Summing the shards of a
+    layer gives ``layer_forward`` up to f32 addition order."""
+    acts = np.asarray(acts, dtype=np.float32)
+    T = acts.shape[0]
+    routes = route(seed, T, layer, num_experts, top_k)
+    inv_k = np.float32(1.0 / top_k)
+    per_slot = np.zeros((routes.shape[1], T, pool.H), dtype=np.float32)
+    for e in np.unique(routes):
+        if not (first < e <= first + pool.L):
+            continue
+        tok, slot = np.nonzero(routes == e)
+        gu = pool.tensor_f32(layer, int(e) - first, 1)
+        dn = pool.tensor_f32(layer, int(e) - first, 2)
+        per_slot[slot, tok] = expert_rows(gu, dn, acts[tok]) * inv_k
+    y = np.zeros_like(acts)
+    for s in range(routes.shape[1]):
+        y += per_slot[s]
+    if shared is not None:
+        r0, n = shared_rows if shared_rows is not None else (0, T)
+        for i in range(1, shared.S + 1):
+            y[r0:r0 + n] += expert_rows(shared.tensor_f32(layer, i, 1), shared.tensor_f32(layer, i, 2),
+                                        acts[r0:r0 + n])
+    return y
+
+
 def resident_stack(pool: WordPool, acts: np.ndarray, top_k: int, seed: int, iterations: int = 1,
                    shared: "SharedPool | None" = None):
     """resident_baseline restated: iterations x layers 1..N."""

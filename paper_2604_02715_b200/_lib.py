@@ -63,6 +63,11 @@ class KernelTimes(C.Structure):
                 ("n_units_gate_up", C.c_int32), ("n_units_down", C.c_int32)]
 
 
+class EpPlanBufs(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("src_rows", "dst_rank", "dst_row", "ret_index", "c_rank", "c_row",
+                                           "to_arrival", "from_arrival", "offsets", "counts")]
+
+
 _P = C.c_void_p
 _I = C.c_int32
 _U64 = C.c_uint64
@@ -121,13 +126,17 @@ _SIGS = {
     "xpgb_ep_window_open": [_P, _P],
     "xpgb_ep_window_close": [_P],
     "xpgb_ep_window_free": [_P],
-    "xpgb_ep_scatter_rows": [_P, _P, _P, _P, _I, _I, _I, _P, _P, _I, _I, _I, _P, _P],
-    "xpgb_ep_wait": [_P, _I, _I, _P],
-    "xpgb_ep_reduce_scatter": [_P, _P, _P, _I, _P, _P, _I, _I, _I, _P, _P],
+    "xpgb_ep_scatter_rows": [_P, _P, _P, _P, _I, _P, _I, _I, C.c_int64, _P, _P, _I, _I, _I, _P, _P, _P],
+    "xpgb_ep_wait": [_P, _I, _I, _P, _P],
+    "xpgb_ep_reduce_scatter": [_P, _P, _P, _I, _P, _P, _P, _I, _I, _I, _P, _P],
+    "xpgb_fault_ptr": [_P, C.POINTER(_P)],
+    "xpgb_fault_set": [_P, C.c_int64],
+    "xpgb_ep_plan_scratch_words": [_I, _I, _I],
+    "xpgb_ep_plan": [_P, _I, _I, _I, _I, _I, _P, C.POINTER(EpPlanBufs), _P],
     "xpgb_set_shared_tokens": [_P, _I, _I],
     "xpgb_shared_forward": [_P, _I, _P, _P, _I, _P],
-    "xpgb_experts_forward": [_P, _I, _P, _P, _I, _P, _P],
-    "xpgb_experts_forward_range": [_P, _I, _P, _P, _I, _I, _I, _I, _P, _P],
+    "xpgb_experts_forward": [_P, _I, _P, C.c_int64, _P, _I, _P, _P],
+    "xpgb_experts_forward_range": [_P, _I, _P, C.c_int64, _P, _I, _I, _I, _I, _P, _P],
     "xpgb_session_step": [_P, _I, C.POINTER(C.c_int32)],
     "xpgb_combine_rows": [_P, _P, _I, _I, _I, _I, _P, _P],
     "xpgb_codec_histogram": [_P, _U64, C.POINTER(_U64), _I],
@@ -144,7 +153,8 @@ _SIGS = {
     "xpgb_hbm_bytes": [_P, C.POINTER(_U64), C.POINTER(_U64), C.POINTER(_U64)],
     "xpgb_profile_layer": [_P, _I, _P, _P, _I, _I, _U64, _I, C.POINTER(KernelTimes)],
 }
-_RESTYPES = {"xpgb_last_error": C.c_char_p, "xpgb_kernel_launches": C.c_int64, "xpgb_codec_record_bytes": C.c_uint64}
+_RESTYPES = {"xpgb_last_error": C.c_char_p, "xpgb_kernel_launches": C.c_int64, "xpgb_codec_record_bytes": C.c_uint64,
+             "xpgb_ep_plan_scratch_words": C.c_int64}
 
 # every symbol declared in include/xpgb.h (tests check the export table against this)
 DECLARED = tuple(_SIGS)

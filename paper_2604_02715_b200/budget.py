@@ -90,12 +90,15 @@ def _balanced(total: int, N: int):
 
 
 def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *, shared_bytes: float = 0.0,
-                   b_link: float = 54e9, b_dec: float = 1100e9, t_compute: float = 0.0,
+                   overhead_bytes: float = 0.0, b_link: float = 54e9, b_dec: float = 1100e9, t_compute: float = 0.0,
                    min_window_bytes: float = 128 * 2**20, allow_pinned: bool = True, depth: int | None = None,
                    window: int | None = None) -> ResidencyPlan:
     """Choose (ring, device tier, pinned) for N layers x L experts under `budget_bytes`.
 
     eb: raw bytes of one expert (both tensors); ceb: its compressed record bytes.
+    overhead_bytes: HBM the codec holds whatever the plan (staging buffers, the device-resident
+    chunk index of the host records): counted inside ``budget_bytes`` like the shared experts,
+    so the plan's whole expert footprint stays within the budget.
     Step model: max(link_bytes / b_link, decoded_raw_bytes / b_dec + t_compute).
     depth: windows in flight (the ring holds depth windows); window: experts per window
     (default: enough for min_window_bytes).  depth None: 1 when the plan is clearly
@@ -105,16 +108,17 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
     compute -- DSv3 65%: depth 1 is 22% slower).
     """
     if depth is None:
-        one = plan_residency(N, L, eb, ceb, budget_bytes, shared_bytes=shared_bytes, b_link=b_link, b_dec=b_dec,
+        one = plan_residency(N, L, eb, ceb, budget_bytes, shared_bytes=shared_bytes, overhead_bytes=overhead_bytes,
+                             b_link=b_link, b_dec=b_dec,
                              t_compute=t_compute, min_window_bytes=min_window_bytes, allow_pinned=allow_pinned,
                              depth=1, window=window)
         if one.ring and one.link_bytes / b_link >= 1.5 * one.decode_bytes / b_dec:
             return one
-        return plan_residency(N, L, eb, ceb, budget_bytes, shared_bytes=shared_bytes, b_link=b_link, b_dec=b_dec,
-                              t_compute=t_compute, min_window_bytes=min_window_bytes, allow_pinned=allow_pinned,
-                              depth=2, window=window)
+        return plan_residency(N, L, eb, ceb, budget_bytes, shared_bytes=shared_bytes, overhead_bytes=overhead_bytes,
+                              b_link=b_link, b_dec=b_dec, t_compute=t_compute, min_window_bytes=min_window_bytes,
+                              allow_pinned=allow_pinned, depth=2, window=window)
     total = N * L
-    cap = budget_bytes - shared_bytes
+    cap = budget_bytes - shared_bytes - overhead_bytes
     if window is None:
         # one expert per window once it is >= min_window_bytes (Mixtral: ring 2 instead of 4
         # frees 0.7 GB for the device tier, +7% at 25%); smaller experts batch into windows
@@ -142,8 +146,8 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
             best = (key, p, d, ring, link)
     if best is None:
         if w_min > 1:  # small experts: a narrower window still fits (tiny: 8 x 0.8 MB > 25%)
-            return plan_residency(N, L, eb, ceb, budget_bytes, shared_bytes=shared_bytes, b_link=b_link,
-                                  b_dec=b_dec, t_compute=t_compute, min_window_bytes=min_window_bytes,
+            return plan_residency(N, L, eb, ceb, budget_bytes, shared_bytes=shared_bytes,
+                                  overhead_bytes=overhead_bytes, b_link=b_link, b_dec=b_dec, t_compute=t_compute, min_window_bytes=min_window_bytes,
                                   allow_pinned=allow_pinned, depth=depth, window=max(1, w_min // 2))
         raise ValueError(f"budget {budget_bytes:.3g} B cannot hold a ring")
     (est, _), p, d, ring, link = best
@@ -165,5 +169,5 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
     for l in range(N):
         streamed = L - p_layer[l]
         device[l, :streamed] = _spread_row(streamed, d_layer[l], w)
-    hbm = ring * eb + p * eb + device.sum() * ceb + shared_bytes
+    hbm = ring * eb + p * eb + device.sum() * ceb + shared_bytes + overhead_bytes
     return ResidencyPlan(ring, device, pinned, float(hbm), float(est), float(link), depth, float((total - p) * eb))

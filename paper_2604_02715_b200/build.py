@@ -36,7 +36,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     deps = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "xpgb.h")]
     dep_time = max(_mtime(d) for d in deps)
-    objs = []
+    objs, jobs = [], []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(OBJ, src.replace(".cu", ".o"))
@@ -45,7 +45,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
             cmd = [nvcc(), *ARCH, *FLAGS, "-c", s, "-o", o]
             if verbose:
                 print(" ".join(cmd), flush=True)
-            subprocess.run(cmd, check=True)
+            jobs.append(subprocess.Popen(cmd))
+    failed = [j.args for j in jobs if j.wait() != 0]  # sources compile in parallel
+    if failed:
+        raise subprocess.CalledProcessError(1, failed[0])
     if force or _mtime(OUT) < max(_mtime(o) for o in objs):
         tmp = OUT + ".tmp"
         cmd = [nvcc(), "-shared", "-cudart", "static", *ARCH, "-o", tmp, *objs]

@@ -1,6 +1,7 @@
 // Exponent-Huffman codec: multi-threaded host encoder (bit-identical to
 // xpg codec.py:235-272) and the sm_100a decoder kernel (codec.py:275-330).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <thread>
@@ -205,9 +206,11 @@ __device__ __forceinline__ void decode_chunk(R& q, uint64_t win, int avail, cons
 // Decode tables of one codec table, built once by k_build_tables and copied into every
 // decoder CTA's shared memory (building them per CTA cost ~20 us per launch -- most of a
 // small tensor's decode).
+constexpr int kPairBits = 12;
 struct DecTables {
   uint32_t lut3[1 << kMultiBits];  // up to 4 symbols (4 x 8 b)
   uint8_t lmeta[1 << kMultiBits];  // count | total length << 3
+  uint32_t pair[1 << kPairBits];   // k_exp_decode2's pair table (see there)
   uint32_t first_code[kCodecMaxLen + 1];
   int count[kCodecMaxLen + 1], first_rank[kCodecMaxLen + 1];
   uint8_t sorted_sym[kCodecSymbols];
@@ -276,6 +279,23 @@ __global__ void __launch_bounds__(256) k_build_tables(const CodecTable table, De
   for (int i = tid; i < (1 << kMultiBits); i += blockDim.x) {
     out->lut3[i] = lut3[i];
     out->lmeta[i] = lmeta[i];
+  }
+  // pair table: every 12-bit pattern -> the first two whole codes it starts with, already in
+  // bf16 position for k_exp_decode2: e0 << 7 and e1 << 23 (the exponent fields of a pair of
+  // bf16 words), their total length in bits 0..3 (0: the pair does not fit in 12 bits), and
+  // the first code's own length in bits 16..20 (0: longer than 12 bits).  Every metadata bit
+  // sits where the final select keeps the sign/mantissa plane, so one LOP3 drops it.
+  for (int i = tid; i < (1 << kPairBits); i += blockDim.x) {
+    const uint64_t w = (uint64_t)i << (64 - kPairBits);
+    int s0 = 0, s1 = 0;
+    const int l0 = canon_decode(w, ml, count, first_code, first_rank, sorted_sym, &s0);
+    uint32_t e = 0;
+    if (l0 && l0 <= kPairBits) {
+      e = ((uint32_t)s0 << 7) | ((uint32_t)l0 << 16);
+      const int l1 = canon_decode(w << l0, ml, count, first_code, first_rank, sorted_sym, &s1);
+      if (l1 && l0 + l1 <= kPairBits) e |= ((uint32_t)s1 << 23) | (uint32_t)(l0 + l1);
+    }
+    out->pair[i] = e;
   }
   if (tid <= kCodecMaxLen) {
     out->first_code[tid] = first_code[tid];
@@ -464,6 +484,137 @@ __device__ __forceinline__ void decode_chunk(R& q, uint64_t win, int avail, cons
   }
 }
 
+// ---------------------------------------------------------------- decoder v2 (pair table)
+//
+// One thread per chunk as k_exp_decode, but built around a 12-bit *pair* table whose entry is
+// already the exponent half of two bf16 words (e0 << 7 | e1 << 23, metadata in the bits the
+// sign/mantissa plane owns).  Per pair of values: one window extract, one table load, one
+// length add, one byte permute that duplicates the two sign/mantissa bytes into their 16-bit
+// lanes, and one LOP3 select (mask 0x807F807F) -- instead of variable-count symbol insertion.
+// 99.7% of pairs of synthetic N(0, 0.02) exponents fit 12 bits; the rest take a per-symbol
+// path (the entry's single-code length, or the canonical first-code search for codes > 12
+// bits).  Window: 64 bits, bit position p; the stream refills one 32-bit word every second
+// pair when p >= 32, so a lookup always has 12 valid bits (p <= 43 at the odd pair).
+struct Window {
+  uint64_t win;  // bits [0, 64) of the stream from the current word, MSB first
+  int p;         // bits already consumed from the top of `win`
+  uint32_t nxt;  // next stream word (raw, in flight)
+  const uint32_t* wp;
+  __device__ __forceinline__ void refill() {
+    if (p >= 32) {
+      win = (win << 32) | bswap32(nxt);
+      nxt = *wp++;
+      p -= 32;
+    }
+  }
+  __device__ __forceinline__ uint32_t peek12() const { return (uint32_t)((win << p) >> (64 - kPairBits)); }
+};
+
+struct CanonTabs {
+  const int* count;
+  const uint32_t* first_code;
+  const int* first_rank;
+  const uint8_t* sorted_sym;
+  int ml;
+};
+
+// One exponent symbol the slow way (p < 32 on entry, so >= 32 bits are valid).
+__device__ __forceinline__ uint32_t symbol_slow(Window& w, uint32_t ent, const CanonTabs& ct) {
+  int l = (int)((ent >> 16) & 31);
+  uint32_t sym = (ent >> 7) & 0xFFu;
+  if (!l) {
+    int s = 0;
+    l = canon_decode(w.win << w.p, ct.ml, ct.count, ct.first_code, ct.first_rank, ct.sorted_sym, &s);
+    sym = (uint32_t)s;
+  }
+  w.p += l;
+  return sym;
+}
+
+// A pair that does not fit the table: two single symbols; leaves p < 32.
+__device__ __forceinline__ uint32_t pair_slow(Window& w, const uint32_t* __restrict__ pair, const CanonTabs& ct) {
+  w.refill();
+  const uint32_t a = symbol_slow(w, pair[w.peek12()], ct);
+  w.refill();
+  const uint32_t b = symbol_slow(w, pair[w.peek12()], ct);
+  w.refill();
+  return (a << 7) | (b << 23);
+}
+
+__global__ void __launch_bounds__(256) k_exp_decode2(const __grid_constant__ DecodeParams p) {
+  __shared__ uint32_t pair[1 << kPairBits];
+  __shared__ uint32_t first_code[kCodecMaxLen + 1];
+  __shared__ int count[kCodecMaxLen + 1], first_rank[kCodecMaxLen + 1];
+  __shared__ uint8_t sorted_sym[kCodecSymbols];
+  const int tid = threadIdx.x;
+  {
+    const DecTables* t = p.tabs;
+    const uint4* src = reinterpret_cast<const uint4*>(t->pair);
+    uint4* dst = reinterpret_cast<uint4*>(pair);
+    for (int i = tid; i < (1 << kPairBits) / 4; i += blockDim.x) dst[i] = src[i];
+    if (tid <= kCodecMaxLen) {
+      first_code[tid] = t->first_code[tid];
+      count[tid] = t->count[tid];
+      first_rank[tid] = t->first_rank[tid];
+    }
+    if (tid < kCodecSymbols) sorted_sym[tid] = t->sorted_sym[tid];
+  }
+  const CanonTabs ct{count, first_code, first_rank, sorted_sym, p.tabs->maxlen};
+  __syncthreads();
+
+  const uint64_t n = p.n;
+  const uint64_t cpt = (n + p.chunk - 1) / p.chunk;  // chunks per tensor
+  const uint64_t n_chunks = cpt * (uint64_t)p.ntensors;
+  for (uint64_t gc = blockIdx.x * (uint64_t)blockDim.x + tid; gc < n_chunks; gc += (uint64_t)gridDim.x * blockDim.x) {
+    const int ti = (int)(gc / cpt);
+    const uint64_t c = gc - (uint64_t)ti * cpt;
+    const DecodeTensor& d = p.t[ti];
+    const uint8_t* __restrict__ sm = d.sm;
+    uint16_t* __restrict__ out = d.out;
+    const uint64_t v0 = c * p.chunk;
+    const uint64_t v1 = (v0 + p.chunk < n) ? v0 + p.chunk : n;
+    const uint32_t bitpos = d.index[c] - d.bit_base;
+    Window w;
+    w.wp = d.bits + (bitpos >> 5);
+    w.win = ((uint64_t)bswap32(w.wp[0]) << 32) | bswap32(w.wp[1]);
+    w.nxt = w.wp[2];
+    w.wp += 3;
+    w.p = (int)(bitpos & 31);
+    const bool fast = ((v1 - v0) & 15) == 0 &&
+                      ((reinterpret_cast<uintptr_t>(out + v0) & 31) | (reinterpret_cast<uintptr_t>(sm + v0) & 15)) == 0;
+    if (fast) {
+      uint4 nsm = *reinterpret_cast<const uint4*>(sm + v0);
+      for (uint64_t v = v0; v < v1; v += 16) {
+        const uint4 smv = nsm;
+        if (v + 16 < v1) nsm = *reinterpret_cast<const uint4*>(sm + v + 16);  // one group ahead
+        const uint32_t smw[4] = {smv.x, smv.y, smv.z, smv.w};
+        uint32_t o[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if ((j & 1) == 0) w.refill();
+          uint32_t e = pair[w.peek12()];
+          const int len = (int)(e & 15u);
+          if (__builtin_expect(len == 0, 0)) e = pair_slow(w, pair, ct);
+          else w.p += len;
+          const uint32_t dup = __byte_perm(smw[j >> 1], 0, (j & 1) ? 0x3322u : 0x1100u);
+          o[j] = (dup & 0x807F807Fu) | (e & 0x7F807F80u);
+        }
+        asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(out + v), "r"(o[0]), "r"(o[1]),
+                     "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7])
+                     : "memory");
+      }
+    } else {
+      // ragged or unaligned chunk: one symbol and one 2-byte store at a time
+      for (uint64_t v = v0; v < v1; ++v) {
+        w.refill();
+        const uint32_t sym = symbol_slow(w, pair[w.peek12()], ct);
+        const uint32_t sb = sm[v];
+        out[v] = (uint16_t)(((sb & 0x80u) << 8) | (sym << 7) | (sb & 0x7Fu));
+      }
+    }
+  }
+}
+
 void launch_exp_decode(const uint8_t* sm, const uint32_t* bits, const uint32_t* index, uint64_t n, int chunk,
                        const CodecTable& table, uint16_t* out, cudaStream_t s, uint32_t bit_base) {
   DecodeTensor t{sm, bits, index, out, bit_base};
@@ -516,8 +667,24 @@ void launch_exp_decode_multi(const DecodeTensor* tensors, int ntensors, uint64_t
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_exp_decode, 256, 0);
     return std::max(1, sms * std::max(1, per_sm));
   }();
-  const uint64_t blocks = std::min<uint64_t>((n_chunks + 255) / 256, (uint64_t)resident);
-  k_exp_decode<<<(unsigned)blocks, 256, 0, s>>>(p);
+  static const bool v1 = [] {  // XPGB_DECODER=1: the round-1 multi-symbol decoder (A/B only)
+    const char* e = getenv("XPGB_DECODER");
+    return e && atoi(e) == 1;
+  }();
+  if (v1) {
+    const uint64_t blocks = std::min<uint64_t>((n_chunks + 255) / 256, (uint64_t)resident);
+    k_exp_decode<<<(unsigned)blocks, 256, 0, s>>>(p);
+  } else {
+    static const int resident2 = [] {
+      int dev = 0, sms = 148, per_sm = 4;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_exp_decode2, 256, 0);
+      return std::max(1, sms * std::max(1, per_sm));
+    }();
+    const uint64_t blocks = std::min<uint64_t>((n_chunks + 255) / 256, (uint64_t)resident2);
+    k_exp_decode2<<<(unsigned)blocks, 256, 0, s>>>(p);
+  }
   note_launch();
 }
 

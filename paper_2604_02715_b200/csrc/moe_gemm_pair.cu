@@ -35,13 +35,21 @@ namespace xpgb {
 
 namespace {
 
-constexpr int kPairStages = 6;
 constexpr int kPairRows = 128;                       // rows per CTA of A and of B
-constexpr int kPairStageBytes = 2 * kPairRows * kBK * 2;  // A half + B half = 32 KB
+constexpr int kPairTile = kPairRows * kBK * 2;       // one 128-row x 64-K bf16 tile (16 KB)
 constexpr int kPairAcc = 256;                        // TMEM columns per accumulator stage
 constexpr int kWeightGroup = 8;                      // weight tiles per rasterization group
 constexpr int kPairTab = (3 * kMaxExperts + 8) * 4;
-constexpr int kPairSmem = kPairStages * kPairStageBytes + 1024 + 256 + kPairTab;
+
+// SPLIT: the token tile comes as its hi and lo bf16 planes (moe_kernels.cuh: split_bf16),
+// two MMAs per K step; otherwise bf16 activations only.
+template <bool SPLIT>
+struct PairCfg {
+  static constexpr int STAGE = (SPLIT ? 3 : 2) * kPairTile;  // A hi (+ A lo) + B half
+  static constexpr int STAGES = SPLIT ? 4 : 6;
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256 + kPairTab;
+  static_assert(SMEM <= 227 * 1024, "pair GEMM stages exceed 227 KB");
+};
 
 __device__ __forceinline__ uint8_t* align1k(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
@@ -74,10 +82,14 @@ __device__ __forceinline__ PairUnit pair_unit(int u, const int* s_up, const int*
 
 }  // namespace
 
-template <bool GU>
+template <bool GU, bool SPLIT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     k_moe_gemm_pair(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
                     const __grid_constant__ CUtensorMap map_ws, GemmParams p) {
+  using PC = PairCfg<SPLIT>;
+  constexpr int kPairStages = PC::STAGES;
+  constexpr int kPairStageBytes = PC::STAGE;
+  constexpr int kBOff = (SPLIT ? 2 : 1) * kPairTile;  // B half after the token plane(s)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kPairStages * kPairStageBytes);
@@ -175,7 +187,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           uint8_t* sa = smem + stage * kPairStageBytes;
           if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * kPairStageBytes);
           tma_load_2d_pair(sa, &map_x, &full[stage], kb * kBK, xrow, pol_x);
-          tma_load_2d_pair(sa + kPairRows * kBK * 2, mw, &full[stage], kb * kBK, wrow, pol_w);
+          if (SPLIT) tma_load_2d_pair(sa + kPairTile, &map_x, &full[stage], kb * kBK, xrow + (int)p.act_lo_rows, pol_x);
+          tma_load_2d_pair(sa + kBOff, mw, &full[stage], kb * kBK, wrow, pol_w);
           if (++stage == kPairStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -202,11 +215,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           tc_fence_after();
           if (lane == 0) {
             const uint32_t a_base = smem_u32(smem + stage * kPairStageBytes);
-            const uint32_t b_base = a_base + kPairRows * kBK * 2;
+            const uint32_t b_base = a_base + kBOff;
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k)
-              umma_bf16_pair(d0, sdesc_k_sw128(a_base + 32 * k), sdesc_k_sw128(b_base + 32 * k), idesc,
-                             (kb > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < kBK / 16; ++k) {
+              const uint64_t bdesc = sdesc_k_sw128(b_base + 32 * k);
+              umma_bf16_pair(d0, sdesc_k_sw128(a_base + 32 * k), bdesc, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+              if (SPLIT) umma_bf16_pair(d0, sdesc_k_sw128(a_base + kPairTile + 32 * k), bdesc, idesc, 1u);
+            }
             umma_commit_pair(&empty[stage], 0x3);
           }
           __syncwarp();
@@ -238,16 +253,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           tmem_ld16(tbase + c0, g);
           tmem_ld16(tbase + kPairRows + c0, v);
           if (valid && f0 + c0 + 16 <= p.F) {
-            uint32_t w[8];
+            __nv_bfloat16 hi[16], lo[16];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              __nv_bfloat162 b2 = __floats2bfloat162_rn(silu_pair(g[2 * i]) * v[2 * i],
-                                                        silu_pair(g[2 * i + 1]) * v[2 * i + 1]);
-              w[i] = *reinterpret_cast<uint32_t*>(&b2);
-            }
+            for (int i = 0; i < 16; ++i) split_bf16(silu_pair(g[i]) * v[i], &hi[i], &lo[i]);
             uint4* dst = reinterpret_cast<uint4*>(hrow + c0);
-            dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-            dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+            dst[0] = reinterpret_cast<const uint4*>(hi)[0];
+            dst[1] = reinterpret_cast<const uint4*>(hi)[1];
+            // the lo plane (read only by a split down projection; every row's h is stored
+            // split, so paths can mix)
+            uint4* dlo = reinterpret_cast<uint4*>(hrow + c0 + (size_t)p.h_lo_rows * p.F);
+            dlo[0] = reinterpret_cast<const uint4*>(lo)[0];
+            dlo[1] = reinterpret_cast<const uint4*>(lo)[1];
           }
         }
       } else {
@@ -277,17 +293,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
 bool pair_gemm_supported(int H, int F) { return H % (2 * kPairRows) == 0 && F % kPairRows == 0; }
 
 void set_pair_gemm_attrs() {
-  cudaFuncSetAttribute(k_moe_gemm_pair<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem);
-  cudaFuncSetAttribute(k_moe_gemm_pair<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem);
+  cudaFuncSetAttribute(k_moe_gemm_pair<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<true>::SMEM);
+  cudaFuncSetAttribute(k_moe_gemm_pair<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<true>::SMEM);
+  cudaFuncSetAttribute(k_moe_gemm_pair<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       PairCfg<false>::SMEM);
+  cudaFuncSetAttribute(k_moe_gemm_pair<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       PairCfg<false>::SMEM);
 }
 
 void launch_gemm_pair(bool gate_up, const CUtensorMap& map_x, const CUtensorMap& map_w, const CUtensorMap& map_ws,
-                      const GemmParams& p, int num_sms, cudaStream_t s) {
+                      const GemmParams& p, int num_sms, cudaStream_t s, bool split) {
   const int grid = (num_sms / 2) * 2;
-  if (gate_up)
-    k_moe_gemm_pair<true><<<grid, 192, kPairSmem, s>>>(map_x, map_w, map_ws, p);
-  else
-    k_moe_gemm_pair<false><<<grid, 192, kPairSmem, s>>>(map_x, map_w, map_ws, p);
+  if (split) {
+    if (gate_up)
+      k_moe_gemm_pair<true, true><<<grid, 192, PairCfg<true>::SMEM, s>>>(map_x, map_w, map_ws, p);
+    else
+      k_moe_gemm_pair<false, true><<<grid, 192, PairCfg<true>::SMEM, s>>>(map_x, map_w, map_ws, p);
+  } else {
+    if (gate_up)
+      k_moe_gemm_pair<true, false><<<grid, 192, PairCfg<false>::SMEM, s>>>(map_x, map_w, map_ws, p);
+    else
+      k_moe_gemm_pair<false, false><<<grid, 192, PairCfg<false>::SMEM, s>>>(map_x, map_w, map_ws, p);
+  }
   note_launch();
 }
 

@@ -321,36 +321,61 @@ void launch_route_plan(uint64_t seed, int layer_first, int layer_count, int T, i
 
 // ============================================================================ gather / combine
 
-__device__ __forceinline__ uint2 pack_bf16x4(float4 v) {
-  __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y);
-  __nv_bfloat162 b = __floats2bfloat162_rn(v.z, v.w);
-  uint2 r;
-  r.x = *reinterpret_cast<uint32_t*>(&a);
-  r.y = *reinterpret_cast<uint32_t*>(&b);
-  return r;
+// fp32 x4 -> the hi and lo bf16 planes (moe_kernels.cuh: split_bf16), 8 bytes each.
+__device__ __forceinline__ void pack_split4(float4 v, uint2* hi, uint2* lo) {
+  __nv_bfloat16 h[4], l[4];
+  split_bf16(v.x, &h[0], &l[0]);
+  split_bf16(v.y, &h[1], &l[1]);
+  split_bf16(v.z, &h[2], &l[2]);
+  split_bf16(v.w, &h[3], &l[3]);
+  *hi = *reinterpret_cast<const uint2*>(h);
+  *lo = *reinterpret_cast<const uint2*>(l);
 }
 
-// One block per token: convert the fp32 row to bf16 once, store it at each of
+// One block per token: split the fp32 row into its bf16 planes once, store both at each of
 // its kk expert-major positions (8-byte vector stores).
 __global__ void k_gather(const float* __restrict__ x, const int32_t* __restrict__ pos,
-                         const long long* __restrict__ fault, __nv_bfloat16* __restrict__ xp, int kk, int H) {
+                         const long long* __restrict__ fault, __nv_bfloat16* __restrict__ xp, long long lo_rows,
+                         int kk, int H) {
   if (*fault) return;
   const int t = blockIdx.x;
   const float4* xr = reinterpret_cast<const float4*>(x + (size_t)t * H);
   int p[kMaxTopK];
   for (int s = 0; s < kk; ++s) p[s] = pos[t * kk + s];
+  const size_t lo_off = (size_t)lo_rows * H;
   for (int i = threadIdx.x; i < H / 4; i += blockDim.x) {
-    const uint2 packed = pack_bf16x4(xr[i]);
+    uint2 hi, lo;
+    pack_split4(xr[i], &hi, &lo);
     for (int s = 0; s < kk; ++s)
-      if (p[s] >= 0) *reinterpret_cast<uint2*>(xp + (size_t)p[s] * H + 4 * i) = packed;
+      if (p[s] >= 0) {
+        __nv_bfloat16* d = xp + (size_t)p[s] * H + 4 * i;
+        *reinterpret_cast<uint2*>(d) = hi;
+        *reinterpret_cast<uint2*>(d + lo_off) = lo;
+      }
   }
 }
 
-void launch_gather(const float* x, const int32_t* pos, const long long* fault, __nv_bfloat16* xp, int T, int kk,
-                   int H, cudaStream_t s) {
+void launch_gather(const float* x, const int32_t* pos, const long long* fault, __nv_bfloat16* xp, long long lo_rows,
+                   int T, int kk, int H, cudaStream_t s) {
   if (T == 0) return;
   const int threads = min(256, max(32, H / 4));
-  k_gather<<<T, threads, 0, s>>>(x, pos, fault, xp, kk, H);
+  k_gather<<<T, threads, 0, s>>>(x, pos, fault, xp, lo_rows, kk, H);
+  note_launch();
+}
+
+// Plan of the shared-expert pass (xpgb_shared_forward): row s*T + t holds token t for
+// shared expert s, offsets [0, T, 2T, ..., S*T].
+__global__ void k_shared_plan(int32_t* __restrict__ pos, int32_t* __restrict__ off, int T, int S) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < T * S; i += gridDim.x * blockDim.x)
+    pos[i] = (i % S) * T + i / S;
+  if (blockIdx.x == 0)
+    for (int e = threadIdx.x; e <= S; e += blockDim.x) off[e] = e * T;
+}
+
+void launch_shared_plan(int32_t* pos, int32_t* off, int T, int S, cudaStream_t s) {
+  const int n = T * S;
+  const int g = (n + 255) / 256;
+  k_shared_plan<<<g < 1 ? 1 : (g > 148 ? 148 : g), 256, 0, s>>>(pos, off, T, S);
   note_launch();
 }
 
@@ -361,7 +386,7 @@ void launch_gather(const float* x, const int32_t* pos, const long long* fault, _
 __global__ void k_combine(const float* __restrict__ part, const int32_t* __restrict__ pos,
                           const long long* __restrict__ fault, float* __restrict__ y, int kk, int kr, int H,
                           int splits, long long split_stride, float inv_k, const int32_t* __restrict__ next_pos,
-                          __nv_bfloat16* __restrict__ xp, int accumulate) {
+                          __nv_bfloat16* __restrict__ xp, long long lo_rows, int accumulate) {
   if (*fault) return;
   const int t = blockIdx.x;
   int p[kMaxTopK], q[kMaxTopK];
@@ -387,20 +412,25 @@ __global__ void k_combine(const float* __restrict__ part, const int32_t* __restr
     }
     reinterpret_cast<float4*>(y + (size_t)t * H)[i] = acc;
     if (next_pos) {
-      const uint2 packed = pack_bf16x4(acc);
+      uint2 hi, lo;
+      pack_split4(acc, &hi, &lo);
       for (int s = 0; s < kk; ++s)
-        if (q[s] >= 0) *reinterpret_cast<uint2*>(xp + (size_t)q[s] * H + 4 * i) = packed;
+        if (q[s] >= 0) {
+          __nv_bfloat16* d = xp + (size_t)q[s] * H + 4 * i;
+          *reinterpret_cast<uint2*>(d) = hi;
+          *reinterpret_cast<uint2*>(d + (size_t)lo_rows * H) = lo;
+        }
     }
   }
 }
 
 void launch_combine(const float* part, const int32_t* pos, const long long* fault, float* y, int T, int kk, int kr,
                     int H, int splits, long long split_stride, float inv_k, const int32_t* next_pos,
-                    __nv_bfloat16* xp, cudaStream_t s, bool accumulate) {
+                    __nv_bfloat16* xp, long long lo_rows, cudaStream_t s, bool accumulate) {
   if (T == 0) return;
   const int threads = min(256, max(32, H / 4));
   k_combine<<<T, threads, 0, s>>>(part, pos, fault, y, kk, kr, H, splits, split_stride, inv_k, next_pos, xp,
-                                  accumulate ? 1 : 0);
+                                  lo_rows, accumulate ? 1 : 0);
   note_launch();
 }
 
@@ -454,13 +484,14 @@ template <bool GU, int BN, int STAGES>
 struct GemmCfg {
   static constexpr int A_BYTES = kBM * kBK * 2;
   static constexpr int NA = GU ? 2 : 1;  // A tiles per stage (gate + up)
-  static constexpr int B_BYTES = BN * kBK * 2;
-  static constexpr int STAGE = NA * A_BYTES + B_BYTES;
+  static constexpr int B_BYTES = BN * kBK * 2;  // one activation plane
+  static constexpr int STAGE = NA * A_BYTES + 2 * B_BYTES;  // weights + the hi and lo activation planes
   // TMEM columns per accumulator stage: gate+up = 2 x 128; down = BN (128 or 256 for prefill)
   static constexpr int ACC_COLS = GU ? 256 : (BN > 128 ? BN : 128);
   static constexpr int TMEM_COLS = 2 * ACC_COLS;
   static constexpr int TAB_BYTES = (3 * kMaxExperts + 8) * 4;
   static constexpr int SMEM = STAGES * STAGE + 1024 + 256 + TAB_BYTES;
+  static_assert(SMEM <= 227 * 1024, "GEMM stages exceed the 227 KB of shared memory per CTA");
 };
 
 struct Unit {
@@ -592,7 +623,7 @@ __global__ void __launch_bounds__(192, 1)
         const int nb = (un.n_rows + kBoxRowsB - 1) / kBoxRowsB;
         const int wrow = s_slot[un.e] * rows_per_block + un.m0;
         const CUtensorMap* mw = un.e < p.E_routed ? &map_w : &map_ws;
-        const uint32_t bytes = C::NA * C::A_BYTES + nb * kBoxRowsB * kBK * 2;
+        const uint32_t bytes = C::NA * C::A_BYTES + 2 * nb * kBoxRowsB * kBK * 2;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE;
@@ -600,9 +631,12 @@ __global__ void __launch_bounds__(192, 1)
           tma_load_2d(sa, mw, &full[stage], kb * kBK, wrow, pol_w);
           if (GU) tma_load_2d(sa + C::A_BYTES, mw, &full[stage], kb * kBK, wrow + p.F, pol_w);
           uint8_t* sb = sa + C::NA * C::A_BYTES;
-          for (int i = 0; i < nb; ++i)
+          for (int i = 0; i < nb; ++i) {
             tma_load_2d(sb + i * kBoxRowsB * kBK * 2, &map_b, &full[stage], kb * kBK, un.row_begin + i * kBoxRowsB,
                         pol_b);
+            tma_load_2d(sb + C::B_BYTES + i * kBoxRowsB * kBK * 2, &map_b, &full[stage], kb * kBK,
+                        (int)(un.row_begin + p.act_lo_rows) + i * kBoxRowsB, pol_b);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -629,9 +663,16 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
             const uint64_t bdesc = sdesc_k_sw128(bbase + 32 * k);
+            const uint64_t bdesc_lo = sdesc_k_sw128(bbase + C::B_BYTES + 32 * k);
             const uint32_t accum = (kb > kb0 || k > 0) ? 1u : 0u;
-            umma_bf16(d0, sdesc_k_sw128(base + 32 * k), bdesc, idesc, accum);
-            if (GU) umma_bf16(d0 + 128, sdesc_k_sw128(base + C::A_BYTES + 32 * k), bdesc, idesc, accum);
+            const uint64_t adesc = sdesc_k_sw128(base + 32 * k);
+            umma_bf16(d0, adesc, bdesc, idesc, accum);
+            umma_bf16(d0, adesc, bdesc_lo, idesc, 1u);
+            if (GU) {
+              const uint64_t adesc_u = sdesc_k_sw128(base + C::A_BYTES + 32 * k);
+              umma_bf16(d0 + 128, adesc_u, bdesc, idesc, accum);
+              umma_bf16(d0 + 128, adesc_u, bdesc_lo, idesc, 1u);
+            }
           }
           umma_commit(&empty[stage]);
         }
@@ -654,6 +695,7 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * C::ACC_COLS;
       if (GU) {
         __nv_bfloat16* hcol = p.hbuf + (size_t)un.row_begin * p.F + r;
+        const size_t lo_off = (size_t)p.h_lo_rows * p.F;
         for (int c0 = 0; c0 < un.n_rows; c0 += 16) {
           float g[16], v[16];
           tmem_ld16(tbase + c0, g);
@@ -661,7 +703,12 @@ __global__ void __launch_bounds__(192, 1)
           if (r < p.F) {
 #pragma unroll
             for (int i = 0; i < 16; ++i)
-              if (c0 + i < un.n_rows) hcol[(size_t)(c0 + i) * p.F] = __float2bfloat16_rn(silu_f(g[i]) * v[i]);
+              if (c0 + i < un.n_rows) {
+                __nv_bfloat16 hi, lo;
+                split_bf16(silu_f(g[i]) * v[i], &hi, &lo);
+                hcol[(size_t)(c0 + i) * p.F] = hi;
+                hcol[(size_t)(c0 + i) * p.F + lo_off] = lo;
+              }
           }
         }
       } else {
@@ -698,14 +745,15 @@ static void set_attr() {
 // Stage counts: the weight bytes in flight per SM set the achieved HBM bandwidth of
 // these memory-bound launches, so each token-tile width BN gets as many stages as fit
 // in 227 KB (stage = weight tile(s) + BN x 128 B of activations).
-#define XPGB_GU_TILES(X) X(32, 5) X(48, 5) X(64, 5) X(80, 5) X(96, 4) X(128, 4)
-#define XPGB_DN_TILES(X) X(32, 10) X(48, 9) X(64, 8) X(80, 8) X(96, 7) X(128, 6) X(256, 4)
+// (stage = weight tile(s) + BN x 128 B of each activation plane)
+#define XPGB_GU_TILES(X) X(32, 5) X(48, 4) X(64, 4) X(80, 4) X(96, 3) X(128, 3)
+#define XPGB_DN_TILES(X) X(32, 8) X(48, 7) X(64, 6) X(80, 5) X(96, 5) X(128, 4) X(256, 2)
 // Lean tiles (<= ~175 KB): one stage fewer, so decoder CTAs (10 KB each) fit on the same
 // SM.  The paged runner with a compressed tier uses them: a window's GEMM then runs beside
 // the decode of the next window instead of waiting for its CTAs to drain (Mixtral, 80%
 // budget: 11.3 K -> 13.2 K tok/s; the GEMM alone loses ~1%).
-#define XPGB_GU_LEAN(X) X(32, 4) X(48, 4) X(64, 4) X(80, 4) X(96, 3) X(128, 3)
-#define XPGB_DN_LEAN(X) X(32, 8) X(48, 7) X(64, 6) X(80, 6) X(96, 5) X(128, 5) X(256, 3)
+#define XPGB_GU_LEAN(X) X(32, 4) X(48, 3) X(64, 3) X(80, 3) X(96, 2) X(128, 2)
+#define XPGB_DN_LEAN(X) X(32, 6) X(48, 5) X(64, 5) X(80, 4) X(96, 3) X(128, 3) X(256, 2)
 
 void set_gemm_attrs() {
 #define XPGB_SET_GU(BN, ST) set_attr<true, BN, ST>();
@@ -730,7 +778,7 @@ void launch_gate_up(const CUtensorMap& map_w, const CUtensorMap& map_x, const CU
     XPGB_GU_TILES(XPGB_PICK_GU)
   }
 #undef XPGB_PICK_GU
-  if (!kern) { kern = k_moe_gemm<true, 128, 4>; smem = GemmCfg<true, 128, 4>::SMEM; }
+  if (!kern) { kern = k_moe_gemm<true, 128, 3>; smem = GemmCfg<true, 128, 3>::SMEM; }
   kern<<<grid, 192, smem, s>>>(map_w, map_x, map_ws, p);
   note_launch();
 }
@@ -747,7 +795,7 @@ void launch_down(const CUtensorMap& map_w, const CUtensorMap& map_h, const CUten
     XPGB_DN_TILES(XPGB_PICK_DN)
   }
 #undef XPGB_PICK_DN
-  if (!kern) { kern = k_moe_gemm<false, 128, 6>; smem = GemmCfg<false, 128, 6>::SMEM; }
+  if (!kern) { kern = k_moe_gemm<false, 128, 4>; smem = GemmCfg<false, 128, 4>::SMEM; }
   kern<<<grid, 192, smem, s>>>(map_w, map_h, map_ws, p);
   note_launch();
 }

@@ -31,12 +31,26 @@ struct PlanView {
   int32_t* offsets;  // [E+1] row ranges per local expert
 };
 
+// Activations reach the tensor cores as two bf16 planes, x = hi + lo with hi = bf16_rn(x)
+// and lo = bf16_rn(x - hi): every activation row buffer (expert-major x rows, h rows) holds
+// the hi rows, then the lo rows `lo_rows` rows later.  A contraction issues one MMA per plane
+// into the same fp32 accumulator, so the weights (exact bf16, as the reference widens them,
+// model.py:130-139) meet activations carried to ~2^-17 relative instead of bf16's 2^-9 --
+// the reference computes x and h in float32 (pipeline.py:180-208).  At decode the GEMMs are
+// HBM-bound on the weights, so the second MMA costs no time.
+__device__ __forceinline__ void split_bf16(float v, __nv_bfloat16* hi, __nv_bfloat16* lo) {
+  *hi = __float2bfloat16_rn(v);
+  *lo = __float2bfloat16_rn(v - __bfloat162float(*hi));
+}
+
 // Arguments of one grouped-GEMM launch (gate/up or down) of one layer.
 struct GemmParams {
   const int32_t* offsets;  // [E+1]
   const int32_t* pt;       // [E] device page-table entries of (layer, kind)
   long long* fault;
-  __nv_bfloat16* hbuf;     // gate/up output  [rows][F] bf16
+  long long act_lo_rows;   // rows between the hi and lo planes of the activation operand (x or h)
+  long long h_lo_rows;     // rows between the hi and lo planes of hbuf (the gate/up output)
+  __nv_bfloat16* hbuf;     // gate/up output  [2][h_lo_rows][F] bf16 (hi plane, lo plane)
   float* part;             // down output     [splits][rows][H] fp32
   long long split_stride;  // elements between split planes of `part`
   int layer, e_first, E, F, H, splits;
@@ -58,8 +72,9 @@ constexpr int kPlanSingleCtaPairs = 128;
 void launch_route_plan(uint64_t seed, int layer_first, int layer_count, int T, int L, int top_k, int e_first, int E,
                        int S, int sh0, int sh1, int32_t* topk, int32_t* pos, int32_t* offsets, int32_t* scratch,
                        const long long* fault, cudaStream_t s);
-void launch_gather(const float* x, const int32_t* pos, const long long* fault, __nv_bfloat16* xp, int T, int kk,
-                   int H, cudaStream_t s);
+// xp: hi plane; its lo plane starts lo_rows rows later.
+void launch_gather(const float* x, const int32_t* pos, const long long* fault, __nv_bfloat16* xp, long long lo_rows,
+                   int T, int kk, int H, cudaStream_t s);
 // map_ws: the shared experts' weights (read for groups >= p.E_routed).
 // lean: one stage fewer so exponent-decoder CTAs co-reside (paged runs with a compressed tier)
 void launch_gate_up(const CUtensorMap& map_w, const CUtensorMap& map_x, const CUtensorMap& map_ws,
@@ -72,7 +87,8 @@ void launch_down(const CUtensorMap& map_w, const CUtensorMap& map_h, const CUten
 // accumulate: y_t starts from its current value (a later pass adds shared experts).
 void launch_combine(const float* part, const int32_t* pos, const long long* fault, float* y, int T, int kk, int kr,
                     int H, int splits, long long split_stride, float inv_k, const int32_t* next_pos,
-                    __nv_bfloat16* xp, cudaStream_t s, bool accumulate = false);
+                    __nv_bfloat16* xp, long long lo_rows, cudaStream_t s, bool accumulate = false);
+void launch_shared_plan(int32_t* pos, int32_t* off, int T, int S, cudaStream_t s);
 void launch_reduce_rows(const float* part, const long long* fault, float* out, int n_rows, int H, int splits,
                         long long split_stride, cudaStream_t s);
 void set_gemm_attrs();
@@ -80,7 +96,10 @@ void set_gemm_attrs();
 // 256 token rows x 256 weight rows per pair, unsplit (down writes split plane 0).
 bool pair_gemm_supported(int H, int F);
 void set_pair_gemm_attrs();
+// split: the token rows' lo plane is a second MMA per K step (as the 1-CTA kernel always
+// does); false takes bf16 activations only (2x the tensor throughput at prefill, per-layer
+// rel-L2 ~3e-3 instead of ~1e-6; XPGB_FAST_PREFILL=1).
 void launch_gemm_pair(bool gate_up, const CUtensorMap& map_x, const CUtensorMap& map_w, const CUtensorMap& map_ws,
-                      const GemmParams& p, int num_sms, cudaStream_t s);
+                      const GemmParams& p, int num_sms, cudaStream_t s, bool split = true);
 
 }  // namespace xpgb

@@ -228,14 +228,18 @@ struct Ctx {
   int32_t* plan_pos[3] = {nullptr, nullptr, nullptr};   // [N][T][kk]
   int32_t* plan_off[3] = {nullptr, nullptr, nullptr};   // [N][E+1]
   int32_t* plan_scr[3] = {nullptr, nullptr, nullptr};   // [2][N][E] multi-CTA plan counters
-  __nv_bfloat16* xp = nullptr;  // [cap_rows][H]
-  __nv_bfloat16* hbuf = nullptr;  // [cap_rows][F]
+  __nv_bfloat16* xp = nullptr;    // [2][cap_rows][H]: hi plane, lo plane (moe_kernels.cuh: split_bf16)
+  __nv_bfloat16* hbuf = nullptr;  // [2][cap_rows][F]
   float* part = nullptr;          // [part_rows][H]: splits x (rows of a launch) x H
   int32_t* ep_off = nullptr;      // [E+1] scratch for experts_forward
   int last_splits = 1;
   CUtensorMap map_xp{}, map_h{};
   CUtensorMap map_xp_pair{}, map_h_pair{};  // 128-row boxes: the CTA-pair prefill GEMM's A operand
+  CUtensorMap map_ep_x{}, map_ep_x_pair{};   // caller rows of experts_forward_range (built per buffer)
+  const void* ep_rows_ptr = nullptr;
+  long long ep_lo_rows = 0;
   int pair_mode = -1;                        // CTA-pair GEMM: -1 auto (prefill-sized groups), 0 off, 1 always
+  bool pair_split = true;                    // CTA-pair GEMM takes both activation planes (XPGB_FAST_PREFILL=1: hi only)
   long long* d_fault = nullptr;
 
   // log
@@ -391,10 +395,10 @@ static void ensure_work(Ctx* c, int T, int kk) {
     CK(cudaMalloc(&c->plan_off[b], (size_t)N * (E + 1) * 4));
     CK(cudaMalloc(&c->plan_scr[b], (size_t)2 * N * E * 4));
   }
-  CK(cudaMalloc(&c->xp, (size_t)rows * c->H * 2));
-  CK(cudaMemset(c->xp, 0, (size_t)rows * c->H * 2));
-  CK(cudaMalloc(&c->hbuf, (size_t)rows * c->F * 2));
-  CK(cudaMemset(c->hbuf, 0, (size_t)rows * c->F * 2));
+  CK(cudaMalloc(&c->xp, (size_t)2 * rows * c->H * 2));  // hi rows, then lo rows
+  CK(cudaMemset(c->xp, 0, (size_t)2 * rows * c->H * 2));
+  CK(cudaMalloc(&c->hbuf, (size_t)2 * rows * c->F * 2));
+  CK(cudaMemset(c->hbuf, 0, (size_t)2 * rows * c->F * 2));
   // split-K only pays for few rows (decode); prefill launches run unsplit, so the partial
   // buffer holds all rows once, or up to 8 planes of small launches
   c->part_rows = std::max<long long>(rows, (long long)c->cap_splits * std::min<long long>(rows, 4096));
@@ -403,10 +407,10 @@ static void ensure_work(Ctx* c, int T, int kk) {
   c->cap_T = nT;
   c->cap_kk = nkk;
   c->cap_rows = (int)rows;
-  c->map_xp = make_map(c->xp, rows, c->H, kBoxRowsB);
-  c->map_h = make_map(c->hbuf, rows, c->F, kBoxRowsB);
-  c->map_xp_pair = make_map(c->xp, rows, c->H, kBM);
-  c->map_h_pair = make_map(c->hbuf, rows, c->F, kBM);
+  c->map_xp = make_map(c->xp, 2 * rows, c->H, kBoxRowsB);
+  c->map_h = make_map(c->hbuf, 2 * rows, c->F, kBoxRowsB);
+  c->map_xp_pair = make_map(c->xp, 2 * rows, c->H, kBM);
+  c->map_h_pair = make_map(c->hbuf, 2 * rows, c->F, kBM);
 }
 
 // Token-tile width of the 1-CTA kernels: the smallest instantiated BN covering the
@@ -477,6 +481,8 @@ static GemmParams gemm_params(Ctx* c, int layer, int kind, const int32_t* offset
   p.offsets = offsets;
   p.pt = c->d_pt + (size_t)(kind - 1) * c->N * c->E + (size_t)(layer - 1) * c->E;
   p.fault = c->d_fault;
+  p.act_lo_rows = c->cap_rows;
+  p.h_lo_rows = c->cap_rows;
   p.hbuf = c->hbuf;
   p.part = c->part;
   p.split_stride = 0;  // set per launch: (rows of the launch) x H
@@ -524,7 +530,7 @@ static void enqueue_window(Ctx* c, int layer, const float* x, float* y, int T, i
   const int splits = pair ? 1 : pick_splits(c, T, kt, bn_dn);
   prof_rec(c, 1, s);
   if (gather) {
-    launch_gather(x, pos, c->d_fault, c->xp, T, kt, c->H, s);
+    launch_gather(x, pos, c->d_fault, c->xp, c->cap_rows, T, kt, c->H, s);
     CKLAUNCH();
   }
   prof_rec(c, 2, s);
@@ -540,20 +546,22 @@ static void enqueue_window(Ctx* c, int layer, const float* x, float* y, int T, i
     p->E_routed = std::max(0, std::min(e1, c->E) - e0);
   }
   if (pair)
-    launch_gemm_pair(true, c->map_xp_pair, c->map_gu, c->S ? c->map_gu_sh : c->map_gu, pg, c->num_sms, s);
+    launch_gemm_pair(true, c->map_xp_pair, c->map_gu, c->S ? c->map_gu_sh : c->map_gu, pg, c->num_sms, s,
+                     c->pair_split);
   else
     launch_gate_up(c->map_gu, c->map_xp, c->S ? c->map_gu_sh : c->map_gu, pg, bn, c->num_sms, s, lean_gemm(c));
   CKLAUNCH();
   prof_rec(c, 4, s);
   if (pair)
-    launch_gemm_pair(false, c->map_h_pair, c->map_dn, c->S ? c->map_dn_sh : c->map_dn, pd, c->num_sms, s);
+    launch_gemm_pair(false, c->map_h_pair, c->map_dn, c->S ? c->map_dn_sh : c->map_dn, pd, c->num_sms, s,
+                     c->pair_split);
   else
     launch_down(c->map_dn, c->map_h, c->S ? c->map_dn_sh : c->map_dn, pd, bn_dn, c->num_sms, s, lean_gemm(c));
   CKLAUNCH();
   prof_rec(c, 5, s);
   if (last) {
     launch_combine(c->part, pos, c->d_fault, y, T, kt, kk, c->H, splits, split_stride,
-                   (float)(1.0 / top_k), next_pos, c->xp, s);
+                   (float)(1.0 / top_k), next_pos, c->xp, c->cap_rows, s);
     CKLAUNCH();
   }
   prof_rec(c, 6, s);
@@ -1544,6 +1552,7 @@ static void create_impl(const xpgb_spec* spec, int32_t device, int32_t pool, int
     set_gemm_attrs();
     set_pair_gemm_attrs();
     if (const char* env = getenv("XPGB_PAIR_GEMM")) c->pair_mode = atoi(env) ? 1 : 0;
+    if (const char* env = getenv("XPGB_FAST_PREFILL")) c->pair_split = atoi(env) == 0;
     for (int k = 0; k < 2; ++k) CK(cudaStreamCreateWithFlags(&c->s_copy[k], cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
     for (int k = 0; k < 2; ++k)
@@ -2209,7 +2218,11 @@ int xpgb_fault_get(xpgb_ctx* h, int32_t* faulted, char* msg, uint64_t cap) {
       if (fw) {
         const int kind = (int)((fw >> 1) & 3), state = (int)((fw >> 3) & 7), expert = (int)((fw >> 8) & 0xFFFFFF),
                   layer = (int)(fw >> 32);
-        m = fmt("read through %s while %s", tid_str(layer, expert, kind).c_str(), state_name(state));
+        if (kind == 3)  // an expert-parallel peer event (ep_p2p.cuh: ep_fault)
+          m = fmt("expert-parallel peer rank %d %s", expert - 1,
+                  state == 1 ? "faulted: its rows of this step are invalid" : "published no epoch within 20 s");
+        else
+          m = fmt("read through %s while %s", tid_str(layer, expert, kind).c_str(), state_name(state));
       }
       const size_t n = std::min<size_t>(m.size(), cap - 1);
       memcpy(msg, m.data(), n);
@@ -2312,21 +2325,41 @@ int xpgb_set_expert_shard(xpgb_ctx* h, int32_t expert_first, int32_t expert_coun
   });
 }
 
-static void experts_forward_range(Ctx* c, int layer, const void* rows_dev, const int32_t* offsets_dev, int n_rows,
-                                  int e0, int e1, bool reduce, float* out_dev, cudaStream_t s) {
+static void experts_forward_range(Ctx* c, int layer, const void* rows_dev, long long lo_rows,
+                                  const int32_t* offsets_dev, int n_rows, int e0, int e1, bool reduce, float* out_dev,
+                                  cudaStream_t s) {
   if (layer < 1 || layer > c->N) XFAIL(XPGB_ERR_OUT_OF_RANGE, "layer %d outside [1, %d]", layer, c->N);
   if (e0 < 0 || e1 > c->E || e0 >= e1) XFAIL(XPGB_ERR_OUT_OF_RANGE, "expert range [%d, %d) outside [0, %d)", e0, e1, c->E);
+  if (n_rows < 0 || n_rows > lo_rows)
+    XFAIL(XPGB_ERR_OUT_OF_RANGE, "%d rows do not fit the %lld-row planes of the row buffer", n_rows, lo_rows);
   if (n_rows > c->cap_rows || !c->xp) ensure_work(c, std::max(n_rows, 1), 1);
   if (n_rows == 0) return;
-  // the layer's rows arrive once, with its first window; later windows reuse them
-  if (e0 == 0) CK(cudaMemcpyAsync(c->xp, rows_dev, (size_t)n_rows * c->H * 2, cudaMemcpyDeviceToDevice, s));
-  const double per_group = (double)n_rows / std::max(1, c->E);
+  // the GEMMs read the caller's rows in place ([2][lo_rows][H]: hi plane, lo plane) through
+  // tensor maps built once per buffer -- no copy into the context
+  if (rows_dev != c->ep_rows_ptr || lo_rows != c->ep_lo_rows) {
+    c->map_ep_x = make_map(rows_dev, 2 * lo_rows, c->H, kBoxRowsB);
+    c->map_ep_x_pair = make_map(rows_dev, 2 * lo_rows, c->H, kBM);
+    c->ep_rows_ptr = rows_dev;
+    c->ep_lo_rows = lo_rows;
+  }
+  // rows per expert: under a session the expected share of the global batch (n_rows may be
+  // an upper bound when the row count lives on the device), else n_rows spread evenly
+  double per_group = (double)n_rows / std::max(1, c->E);
+  int n_est = n_rows;
+  if (c->sess && c->sess->active) {
+    per_group = (double)c->sess->o.tokens * std::min(c->sess->o.top_k, c->L) / c->L;
+    n_est = std::max(1, std::min(n_rows, (int)std::ceil(per_group * c->E)));
+  }
   const int bn = pick_bn_rows(per_group);
   // an EP owner receives every rank's rows for its experts: groups of >= 128 rows run on
   // CTA pairs, exactly as in enqueue_window
   const bool pair = pair_gemm_supported(c->H, c->F) && (c->pair_mode == 1 || (c->pair_mode < 0 && per_group >= 128.0));
-  const int splits = pair ? 1 : pick_splits(c, n_rows, 1, bn);  // same for every window of the layer
+  // same for every window of the layer; the planes are n_rows apart, so part_rows bounds them
+  const int splits = pair ? 1
+                          : std::max(1, std::min<int>(pick_splits(c, n_est, 1, bn),
+                                                      (int)(c->part_rows / std::max(1, n_rows))));
   GemmParams pg = gemm_params(c, layer, 1, offsets_dev, 1, false), pd = gemm_params(c, layer, 2, offsets_dev, splits, false);
+  pg.act_lo_rows = lo_rows;  // x rows: the caller's planes; h rows: the context's
   pd.split_stride = (long long)n_rows * c->H;
   for (GemmParams* p : {&pg, &pd}) {  // window: groups [e0, e1), rows stay absolute
     p->offsets += e0;
@@ -2335,12 +2368,12 @@ static void experts_forward_range(Ctx* c, int layer, const void* rows_dev, const
     p->E = p->E_routed = e1 - e0;
   }
   if (pair)
-    launch_gemm_pair(true, c->map_xp_pair, c->map_gu, c->map_gu, pg, c->num_sms, s);
+    launch_gemm_pair(true, c->map_ep_x_pair, c->map_gu, c->map_gu, pg, c->num_sms, s, c->pair_split);
   else
-    launch_gate_up(c->map_gu, c->map_xp, c->map_gu, pg, bn, c->num_sms, s, lean_gemm(c));
+    launch_gate_up(c->map_gu, c->map_ep_x, c->map_gu, pg, bn, c->num_sms, s, lean_gemm(c));
   CKLAUNCH();
   if (pair)
-    launch_gemm_pair(false, c->map_h_pair, c->map_dn, c->map_dn, pd, c->num_sms, s);
+    launch_gemm_pair(false, c->map_h_pair, c->map_dn, c->map_dn, pd, c->num_sms, s, c->pair_split);
   else
     launch_down(c->map_dn, c->map_h, c->map_dn, pd, bn, c->num_sms, s, lean_gemm(c));
   CKLAUNCH();
@@ -2353,18 +2386,20 @@ static void experts_forward_range(Ctx* c, int layer, const void* rows_dev, const
   }
 }
 
-int xpgb_experts_forward(xpgb_ctx* h, int32_t layer, const void* rows_dev, const int32_t* offsets_dev,
-                         int32_t n_rows, float* out_dev, void* stream) {
+int xpgb_experts_forward(xpgb_ctx* h, int32_t layer, const void* rows_dev, int64_t lo_rows,
+                         const int32_t* offsets_dev, int32_t n_rows, float* out_dev, void* stream) {
   return guard([&] {
-    experts_forward_range(&h->c, layer, rows_dev, offsets_dev, n_rows, 0, h->c.E, true, out_dev, (cudaStream_t)stream);
+    experts_forward_range(&h->c, layer, rows_dev, lo_rows, offsets_dev, n_rows, 0, h->c.E, true, out_dev,
+                          (cudaStream_t)stream);
   });
 }
 
-int xpgb_experts_forward_range(xpgb_ctx* h, int32_t layer, const void* rows_dev, const int32_t* offsets_dev,
-                               int32_t n_rows, int32_t e0, int32_t e1, int32_t reduce, float* out_dev, void* stream) {
+int xpgb_experts_forward_range(xpgb_ctx* h, int32_t layer, const void* rows_dev, int64_t lo_rows,
+                               const int32_t* offsets_dev, int32_t n_rows, int32_t e0, int32_t e1, int32_t reduce,
+                               float* out_dev, void* stream) {
   return guard([&] {
-    experts_forward_range(&h->c, layer, rows_dev, offsets_dev, n_rows, e0, std::min(e1, h->c.E), reduce != 0, out_dev,
-                          (cudaStream_t)stream);
+    experts_forward_range(&h->c, layer, rows_dev, lo_rows, offsets_dev, n_rows, e0, std::min(e1, h->c.E),
+                          reduce != 0, out_dev, (cudaStream_t)stream);
   });
 }
 
@@ -2376,16 +2411,13 @@ int xpgb_shared_forward(xpgb_ctx* h, int32_t layer, const float* x_dev, float* y
     cudaStream_t s = (cudaStream_t)stream;
     const int S = c->S, T = tokens;
     if ((long long)T * S > c->cap_rows || !c->xp) ensure_work(c, T, S);
-    // rows s*T + t hold token t for shared expert s; offsets [0, T, 2T, ...]
-    std::vector<int32_t> host((size_t)T * S + S + 1);
-    for (int t = 0; t < T; ++t)
-      for (int e = 0; e < S; ++e) host[(size_t)t * S + e] = e * T + t;
-    for (int e = 0; e <= S; ++e) host[(size_t)T * S + e] = e * T;
+    // rows s*T + t hold token t for shared expert s; offsets [0, T, 2T, ...], written on the
+    // stream (no host index, no synchronisation: this runs once per layer under EP)
     int32_t* d_pos = c->plan_pos[2];  // layer_forward's plan buffer doubles as scratch here
     int32_t* d_off = c->plan_off[2];
-    CK(cudaMemcpyAsync(d_pos, host.data(), (size_t)T * S * 4, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(d_off, host.data() + (size_t)T * S, (size_t)(S + 1) * 4, cudaMemcpyHostToDevice, s));
-    launch_gather(x_dev, d_pos, c->d_fault, c->xp, T, S, c->H, s);
+    launch_shared_plan(d_pos, d_off, T, S, s);
+    CKLAUNCH();
+    launch_gather(x_dev, d_pos, c->d_fault, c->xp, c->cap_rows, T, S, c->H, s);
     CKLAUNCH();
     const int bn = pick_bn_rows((double)T);
     GemmParams pg = gemm_params(c, layer, 1, d_off, 1), pd = gemm_params(c, layer, 2, d_off, 1);
@@ -2398,10 +2430,9 @@ int xpgb_shared_forward(xpgb_ctx* h, int32_t layer, const float* x_dev, float* y
     CKLAUNCH();
     launch_down(c->map_dn, c->map_h, c->map_dn_sh, pd, bn, c->num_sms, s);
     CKLAUNCH();
-    launch_combine(c->part, d_pos, c->d_fault, y_dev, T, S, 0, c->H, 1, pd.split_stride, 1.0f, nullptr, nullptr, s,
+    launch_combine(c->part, d_pos, c->d_fault, y_dev, T, S, 0, c->H, 1, pd.split_stride, 1.0f, nullptr, nullptr, 0, s,
                    true);
     CKLAUNCH();
-    CK(cudaStreamSynchronize(s));  // the host index vector is pageable scratch
   });
 }
 
@@ -2433,8 +2464,9 @@ int xpgb_ep_window_free(void* dptr) {
 }
 
 int xpgb_ep_scatter_rows(const float* src_dev, const int32_t* src_rows, const int32_t* dst_rank, const int32_t* dst_row,
-                         int32_t n, int32_t hidden, int32_t to_bf16, void* const* peer_rows, int32_t* const* peer_flags,
-                         int32_t world, int32_t rank, int32_t epoch, uint32_t* counter, void* stream) {
+                         int32_t n, const int32_t* n_dev, int32_t hidden, int32_t to_bf16, int64_t lo_rows,
+                         void* const* peer_rows, int32_t* const* peer_flags, int32_t world, int32_t rank, int32_t epoch,
+                         const void* fault_dev, uint32_t* counter, void* stream) {
   return guard([&] {
     if (world < 1 || world > kMaxEpWorld || rank < 0 || rank >= world)
       XFAIL(XPGB_ERR_OUT_OF_RANGE, "rank %d of %d (at most %d ranks)", rank, world, kMaxEpWorld);
@@ -2450,14 +2482,14 @@ int xpgb_ep_scatter_rows(const float* src_dev, const int32_t* src_rows, const in
     int dev = 0, sms = 148;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    launch_ep_scatter(src_dev, src_rows, dst_rank, dst_row, n, hidden, to_bf16 != 0, peers, epoch, counter, sms,
-                      (cudaStream_t)stream);
+    launch_ep_scatter(src_dev, src_rows, dst_rank, dst_row, n, n_dev, hidden, to_bf16 != 0, lo_rows, peers, epoch,
+                      static_cast<const long long*>(fault_dev), counter, sms, (cudaStream_t)stream);
     CKLAUNCH();
   });
 }
 
 int xpgb_ep_reduce_scatter(xpgb_ctx* h, const int32_t* dst_rank, const int32_t* dst_row, int32_t n_rows,
-                           void* const* peer_rows, int32_t* const* peer_flags, int32_t world, int32_t rank,
+                           const int32_t* n_dev, void* const* peer_rows, int32_t* const* peer_flags, int32_t world, int32_t rank,
                            int32_t epoch, uint32_t* counter, void* stream) {
   return guard([&] {
     Ctx* c = &h->c;
@@ -2472,17 +2504,51 @@ int xpgb_ep_reduce_scatter(xpgb_ctx* h, const int32_t* dst_rank, const int32_t* 
       peers.rows[r] = peer_rows[r];
       peers.flags[r] = peer_flags[r];
     }
-    launch_ep_reduce_scatter(c->part, c->d_fault, c->ep_splits, c->ep_split_stride, dst_rank, dst_row, n_rows, c->H,
-                             peers, epoch, counter, c->num_sms, (cudaStream_t)stream);
+    launch_ep_reduce_scatter(c->part, c->d_fault, c->ep_splits, c->ep_split_stride, dst_rank, dst_row, n_rows, n_dev,
+                             c->H, peers, epoch, counter, c->num_sms, (cudaStream_t)stream);
     CKLAUNCH();
   });
 }
 
-int xpgb_ep_wait(const int32_t* flags_dev, int32_t world, int32_t epoch, void* stream) {
+int xpgb_ep_wait(const int32_t* flags_dev, int32_t world, int32_t epoch, void* fault_dev, void* stream) {
   return guard([&] {
     if (world < 1 || world > kMaxEpWorld) XFAIL(XPGB_ERR_OUT_OF_RANGE, "%d ranks (at most %d)", world, kMaxEpWorld);
-    launch_ep_wait(flags_dev, world, epoch, (cudaStream_t)stream);
+    launch_ep_wait(flags_dev, world, epoch, static_cast<long long*>(fault_dev), (cudaStream_t)stream);
     CKLAUNCH();
+  });
+}
+
+int64_t xpgb_ep_plan_scratch_words(int32_t world, int32_t tokens, int32_t num_experts) {
+  return ep_plan_scratch_words(world, tokens, num_experts);
+}
+
+int xpgb_ep_plan(const int32_t* routes_dev, int32_t tokens, int32_t world, int32_t rank, int32_t kk,
+                 int32_t num_experts, int32_t* scratch_dev, const xpgb_ep_plan_bufs* out, void* stream) {
+  return guard([&] {
+    if (world < 1 || world > kMaxEpWorld || rank < 0 || rank >= world)
+      XFAIL(XPGB_ERR_OUT_OF_RANGE, "rank %d of %d (at most %d ranks)", rank, world, kMaxEpWorld);
+    if (kk < 1 || kk > num_experts || num_experts < world || tokens < 0)
+      XFAIL(XPGB_ERR_OUT_OF_RANGE, "bad EP plan geometry (T=%d, kk=%d, L=%d, world=%d)", tokens, kk, num_experts, world);
+    if (!out) XFAIL(XPGB_ERR, "null plan buffers");
+    EpPlanOut o{out->src_rows, out->dst_rank, out->dst_row, out->ret_index, out->c_rank, out->c_row, out->to_arrival,
+                out->from_arrival, out->offsets, out->counts};
+    launch_ep_plan(routes_dev, tokens, world, rank, kk, num_experts, scratch_dev, o, (cudaStream_t)stream);
+    CKLAUNCH();
+  });
+}
+
+int xpgb_fault_set(xpgb_ctx* h, int64_t word) {
+  return guard([&] {
+    CK(cudaDeviceSynchronize());
+    long long w = word;
+    CK(cudaMemcpy(h->c.d_fault, &w, sizeof(w), cudaMemcpyHostToDevice));
+  });
+}
+
+int xpgb_fault_ptr(xpgb_ctx* h, void** fault_dev) {
+  return guard([&] {
+    if (!fault_dev) XFAIL(XPGB_ERR, "null argument");
+    *fault_dev = h->c.d_fault;
   });
 }
 
@@ -2497,7 +2563,7 @@ int xpgb_combine_rows(const float* rows_dev, const int32_t* index_dev, int32_t t
       CK(cudaMemset(zero, 0, sizeof(long long)));
     }
     launch_combine(rows_dev, index_dev, zero, y_dev, tokens, kk, kk, hidden, 1, 0, (float)(1.0 / top_k), nullptr,
-                   nullptr, (cudaStream_t)stream);
+                   nullptr, 0, (cudaStream_t)stream);
     CKLAUNCH();
   });
 }

@@ -65,6 +65,7 @@ class Context:
              self.expert_count, C.byref(h))
         self._h = h
         self._host_ref = None
+        self._ring, self._depth = -1, 2  # mirror of the context's ring limit / depth
 
     @property
     def handle(self):
@@ -122,10 +123,31 @@ class Context:
     def set_ring_experts(self, ring_experts: int) -> None:
         """Sub-layer ring of ``ring_experts`` blocks per kind (-1: the reference's two layers)."""
         call("xpgb_set_ring_experts", self._h, int(ring_experts))
+        self._ring = int(ring_experts)
 
     def set_ring_depth(self, depth: int) -> None:
         """Windows in flight on a sub-layer ring (window g recycles g - depth)."""
         call("xpgb_set_ring_depth", self._h, int(depth))
+        self._depth = int(depth)
+
+    def apply_residency(self, pinned_full, ring: int, depth: int) -> None:
+        """Set a whole residency state from any previous one: the pinned mask [N][L] (always
+        applied, so an empty mask clears earlier pins), then ring depth and size in the order
+        the context accepts (a ring is never smaller than the depth in flight).  ring <= 0:
+        the reference's two-layer ring at depth 2."""
+        self.set_pinned(pinned_full)
+        if ring <= 0:
+            if self._ring != -1:
+                self.set_ring_experts(-1)
+            if self._depth != 2:
+                self.set_ring_depth(2)
+            return
+        if ring >= self._depth:
+            self.set_ring_experts(ring)
+            self.set_ring_depth(depth)
+        else:
+            self.set_ring_depth(depth)
+            self.set_ring_experts(ring)
 
     def set_stage_buffers(self, n: int) -> None:
         """Staging ring of the compressed host tier: ``n`` buffers per kind (link run-ahead)."""
@@ -154,6 +176,12 @@ class Context:
         st = current_stream_ptr(self.device) if stream is None else stream
         call("xpgb_layer_forward", self._h, layer, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), tokens,
              top_k, C.c_uint64(int(seed) & 0xFFFFFFFFFFFFFFFF), C.c_void_p(st))
+
+    def fault_ptr(self) -> int:
+        """Device address of the context's fault word (int64; 0 = no fault)."""
+        p = C.c_void_p()
+        call("xpgb_fault_ptr", self._h, C.byref(p))
+        return int(p.value or 0)
 
     def fault(self):
         f = C.c_int32()

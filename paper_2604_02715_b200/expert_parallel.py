@@ -76,6 +76,25 @@ class DispatchPlan:
     p2p_dst_row: object = None    # [T*kk] its row in the owner's expert-major input
     c_rank: object = None         # [n_own] token-owner rank of each of my expert-major rows
     c_row: object = None          # [n_own] its row in that rank's return buffer (= its send position)
+    # a plan built on the device (DevicePlanner): c_* / to_expert / from_expert are sized for the
+    # worst case and n_own lives in counts[2*world]; the host counts are read only when the NCCL
+    # transport needs split sizes (one device->host copy per layer)
+    counts: object = None         # int32 [2*world+1] device: sent to r, received from r, n_own
+    cap_rows: int = 0             # upper bound of n_own (rows of the c_* buffers)
+
+    @property
+    def n_dev(self):
+        """Device pointer of n_own (None for a host-built plan)."""
+        return None if self.counts is None else self.counts.data_ptr() + 4 * (self.counts.numel() - 1)
+
+    def resolve_counts(self) -> None:
+        """Host split sizes of a device plan (NCCL transport only: synchronises once)."""
+        if self.send_counts is None:
+            c = [int(v) for v in self.counts.tolist()]
+            G = (len(c) - 1) // 2
+            self.send_counts, self.recv_counts, n_own = c[:G], c[G:2 * G], c[2 * G]
+            self.to_expert = self.to_expert[:n_own].to(self.send_rows.dtype)
+            self.from_expert = self.from_expert[:n_own].to(self.send_rows.dtype)
 
 
 def build_plan(routes, rank: int, world: int, tokens: int, bounds) -> DispatchPlan:
@@ -156,6 +175,65 @@ def build_plan(routes, rank: int, world: int, tokens: int, bounds) -> DispatchPl
     return plan
 
 
+class DevicePlanner:
+    """The per-step dispatch plan of one rank on the GPU: the router kernel writes the global
+    routing table (xpgb_route) and one CTA derives every row position from it (xpgb_ep_plan),
+    for the layer about to run -- the reference routes on every forward (pipeline.py:200-203),
+    and so does this: nothing is cached across steps, and nothing crosses to the host on the
+    peer-memory transport.  Buffers are sized once for `tokens` tokens per rank."""
+
+    def __init__(self, spec: ModelSpec, fwd: ForwardSpec, rank: int, world: int, tokens: int, device: int = 0):
+        import torch
+
+        L = spec.experts_per_layer
+        self.spec, self.fwd, self.rank, self.world, self.T = spec, fwd, rank, world, int(tokens)
+        self.kk = min(fwd.top_k, L)
+        self.device = device
+        first, count = shard_bounds(L, world)[rank]
+        dev = f"cuda:{device}"
+        i32 = dict(dtype=torch.int32, device=dev)
+        G, T, kk = world, self.T, self.kk
+        self.cap = G * T * kk
+        self.routes = torch.empty(max(1, G * T * kk), **i32)
+        self.src_rows = torch.empty(max(1, T * kk), **i32)
+        self.dst_rank = torch.empty(max(1, T * kk), **i32)
+        self.dst_row = torch.empty(max(1, T * kk), **i32)
+        self.ret_index = torch.empty((T, kk), **i32)
+        self.c_rank = torch.empty(max(1, self.cap), **i32)
+        self.c_row = torch.empty(max(1, self.cap), **i32)
+        self.to_arr = torch.empty(max(1, self.cap), **i32)
+        self.from_arr = torch.empty(max(1, self.cap), **i32)
+        self.offsets = torch.empty(count + 1, **i32)
+        self.counts = torch.empty(2 * G + 1, **i32)
+        words = int(_lib.lib().xpgb_ep_plan_scratch_words(G, max(1, T), L))
+        self.scratch = torch.empty(words, **i32)
+        self.bufs = _lib.EpPlanBufs(*[C.c_void_p(t.data_ptr()) for t in (
+            self.src_rows, self.dst_rank, self.dst_row, self.ret_index, self.c_rank, self.c_row, self.to_arr,
+            self.from_arr, self.offsets, self.counts)])
+
+    def plan(self, layer: int, tokens: int, seed=None) -> DispatchPlan:
+        """Route layer `layer` for world x tokens global rows and build this rank's plan, both on
+        torch's current stream.  seed: the step's router seed (default fwd.router_seed)."""
+        from .device import current_stream_ptr
+
+        if tokens > self.T:
+            raise XpgError(f"{tokens} tokens per rank exceed the {self.T} the expert-parallel runner was built for")
+        st = C.c_void_p(current_stream_ptr(self.device))
+        seed = self.fwd.router_seed if seed is None else seed
+        G, L, kk = self.world, self.spec.experts_per_layer, self.kk
+        if tokens:
+            call("xpgb_route", C.c_uint64(int(seed) & 0xFFFFFFFFFFFFFFFF), int(layer), 1, G * tokens, L,
+                 self.fwd.top_k, C.c_void_p(self.routes.data_ptr()), st)
+        call("xpgb_ep_plan", C.c_void_p(self.routes.data_ptr()), int(tokens), G, self.rank, kk, L,
+             C.c_void_p(self.scratch.data_ptr()), C.byref(self.bufs), st)
+        n = tokens * kk
+        return DispatchPlan(send_counts=None, recv_counts=None, send_rows=self.src_rows[:n].long(),
+                            to_expert=self.to_arr, from_expert=self.from_arr, offsets=self.offsets,
+                            ret_index=self.ret_index[:tokens], p2p_src_rows=self.src_rows[:n],
+                            p2p_dst_rank=self.dst_rank[:n], p2p_dst_row=self.dst_row[:n], c_rank=self.c_rank,
+                            c_row=self.c_row, counts=self.counts, cap_rows=G * tokens * kk)
+
+
 class PeerExchange:
     """Dispatch/combine over peer memory: one window per rank (CUDA IPC, opened by every
     other rank), one scatter kernel per exchange writing rows straight into the owner's
@@ -164,19 +242,29 @@ class PeerExchange:
 
     FLAG_BYTES = 512  # int32 flags[16] at 0, the scatter's CTA counter at 256; rows from 512
 
-    def __init__(self, rank: int, world: int, tokens: int, kk: int, hidden: int, group=None, device: int = 0):
+    MAX_WORLD = 16   # kMaxEpWorld (ep_p2p.cuh): flag slots per window
+
+    def __init__(self, rank: int, world: int, tokens: int, kk: int, hidden: int, group=None, device: int = 0,
+                 fault_ptr: int = 0):
         """Collective: every rank of the group must construct its PeerExchange together.  Any
         rank's failure (allocation, IPC open) makes every rank raise, so the ranks never end
-        up on different transports."""
+        up on different transports.  fault_ptr: the rank's context fault word (a faulted step
+        raises the peers' fault words; a wait that times out or sees one sets it)."""
         import torch
         import torch.distributed as dist
 
+        if world > self.MAX_WORLD:  # before any allocation: "auto" then takes the collective
+            raise XpgError(f"peer exchange supports at most {self.MAX_WORLD} ranks, not {world}")
         torch.cuda.set_device(device)  # the window and every launch belong to this rank's GPU
         self.rank, self.world, self.H = rank, world, hidden
+        self.group = group
+        self.tokens = tokens
+        self.fault_ptr = fault_ptr
         self.in_rows = world * tokens * kk           # worst case: every pair of the step lands here
         self.ret_rows = tokens * kk
         self.xp_off = self.FLAG_BYTES
-        self.ret_off = self.xp_off + ((self.in_rows * hidden * 2 + 255) // 256) * 256
+        # expert-major input rows as two bf16 planes: hi rows, then lo rows in_rows later
+        self.ret_off = self.xp_off + ((2 * self.in_rows * hidden * 2 + 255) // 256) * 256
         size = self.ret_off + self.ret_rows * hidden * 4
         self._own, self._opened, err = 0, [], None
         handle = (C.c_uint8 * 64)()
@@ -231,18 +319,42 @@ class PeerExchange:
         """This rank's returned fp32 rows, in send order (device pointer)."""
         return self._own + self.ret_off
 
-    def _scatter(self, src, src_rows, dst_rank, dst_row, n, to_bf16, regions, stream):
+    def agree_epoch(self) -> None:
+        """Collective (every rank, at session begin): continue from the largest epoch any rank
+        reached, so a rank that raised mid-step (and skipped some exchanges) cannot pass a
+        later wait early on stale flags or wait for an epoch nobody publishes."""
+        import torch
+        import torch.distributed as dist
+
+        if self.world == 1:
+            return
+        on_gpu = dist.get_backend(self.group) == "nccl"
+        t = torch.tensor([self.epoch], dtype=torch.int64, device=f"cuda:{torch.cuda.current_device()}" if on_gpu
+                         else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        self.epoch = int(t.item())
+
+    def _scatter(self, src, src_rows, dst_rank, dst_row, n, n_dev, to_bf16, regions, stream):
         self.epoch += 1
         call("xpgb_ep_scatter_rows", C.c_void_p(src.data_ptr()),
              C.c_void_p(src_rows.data_ptr()) if src_rows is not None else None,
-             C.c_void_p(dst_rank.data_ptr()), C.c_void_p(dst_row.data_ptr()), int(n), self.H, 1 if to_bf16 else 0,
-             regions, self._flags, self.world, self.rank, self.epoch, C.c_void_p(self.counter), C.c_void_p(stream))
-        call("xpgb_ep_wait", C.c_void_p(self._own), self.world, self.epoch, C.c_void_p(stream))
+             C.c_void_p(dst_rank.data_ptr()), C.c_void_p(dst_row.data_ptr()), int(n),
+             C.c_void_p(n_dev) if n_dev else None, self.H, 1 if to_bf16 else 0, self.in_rows, regions, self._flags,
+             self.world, self.rank, self.epoch, C.c_void_p(self.fault_ptr) if self.fault_ptr else None,
+             C.c_void_p(self.counter), C.c_void_p(stream))
+        call("xpgb_ep_wait", C.c_void_p(self._own), self.world, self.epoch,
+             C.c_void_p(self.fault_ptr) if self.fault_ptr else None, C.c_void_p(stream))
+
+    def _check_rows(self, x) -> None:
+        if x.shape[0] > self.tokens:
+            raise XpgError(f"{x.shape[0]} tokens per rank overflow the peer windows sized for {self.tokens}")
 
     def dispatch(self, x, plan, stream) -> int:
-        """x fp32 [T, H] -> every owner's expert-major bf16 rows; returns this rank's xp."""
-        self._scatter(x, plan.p2p_src_rows, plan.p2p_dst_rank, plan.p2p_dst_row, plan.p2p_src_rows.numel(), True,
-                      self._xp, stream)
+        """x fp32 [T, H] -> every owner's expert-major rows (two bf16 planes, lo in_rows later);
+        returns this rank's xp."""
+        self._check_rows(x)
+        self._scatter(x, plan.p2p_src_rows, plan.p2p_dst_rank, plan.p2p_dst_row, plan.p2p_src_rows.numel(), None,
+                      True, self._xp, stream)
         return self.xp
 
     def reduce_combine(self, ctx, plan, stream) -> int:
@@ -250,15 +362,18 @@ class PeerExchange:
         rows of the last experts_forward_range(reduce=0) go from the partial planes straight
         into the token owners' return buffers."""
         self.epoch += 1
+        n = plan.cap_rows if plan.counts is not None else int(plan.c_rank.numel())
         call("xpgb_ep_reduce_scatter", ctx.handle, C.c_void_p(plan.c_rank.data_ptr()),
-             C.c_void_p(plan.c_row.data_ptr()), int(plan.c_rank.numel()), self._ret, self._flags, self.world,
-             self.rank, self.epoch, C.c_void_p(self.counter), C.c_void_p(stream))
-        call("xpgb_ep_wait", C.c_void_p(self._own), self.world, self.epoch, C.c_void_p(stream))
+             C.c_void_p(plan.c_row.data_ptr()), int(n), C.c_void_p(plan.n_dev) if plan.n_dev else None, self._ret,
+             self._flags, self.world, self.rank, self.epoch, C.c_void_p(self.counter), C.c_void_p(stream))
+        call("xpgb_ep_wait", C.c_void_p(self._own), self.world, self.epoch,
+             C.c_void_p(self.fault_ptr) if self.fault_ptr else None, C.c_void_p(stream))
         return self.ret
 
     def combine(self, out, plan, stream) -> int:
         """This rank's expert outputs fp32 [n_own, H] -> the token owners' return buffers."""
-        self._scatter(out, None, plan.c_rank, plan.c_row, plan.c_rank.numel(), False, self._ret, stream)
+        n = plan.cap_rows if plan.counts is not None else int(plan.c_rank.numel())
+        self._scatter(out, None, plan.c_rank, plan.c_row, n, plan.n_dev, False, self._ret, stream)
         return self.ret
 
     def close(self):
@@ -283,8 +398,8 @@ class ExpertParallelMoE:
     """One rank's MoE layer under expert parallelism.
 
     route_fn(seed, n_tokens, layer, L, k) -> int [n_tokens, kk] (default: libxpgb router kernel);
-    expert_fn(layer, rows_bf16 [n, H], offsets int32 [count+1]) -> fp32 [n, H] unscaled expert outputs
-    (default: libxpgb grouped SwiGLU through this rank's page table);
+    expert_fn(layer, rows fp32 [n, H], offsets int32 [count+1]) -> fp32 [n, H] unscaled expert outputs
+    (default: libxpgb grouped SwiGLU through this rank's page table, the rows as their hi/lo bf16 planes);
     combine_fn(rows fp32, index int32 [T, kk], top_k) -> fp32 [T, H] (default: libxpgb ordered combine);
     shared_fn(layer, x fp32 [T, H], y fp32 [T, H]) adds the shared experts' outputs to y in place (each
     rank applies its replica to its own tokens after the routed combine; default: libxpgb when the
@@ -305,12 +420,24 @@ class ExpertParallelMoE:
         self.expert_fn = expert_fn or self._gpu_experts
         self.combine_fn = combine_fn or self._gpu_combine
         self.shared_fn = shared_fn or (self._gpu_shared if has_shared else None)
+        self.planner = None  # DevicePlanner: per-step plans on the GPU (set by the runner)
 
     # ---- defaults on the GPU
     def _gpu_route(self, seed, n_tokens, layer, L, k):
         from .device import route_table
 
         return route_table(seed, n_tokens, 1, L, k, device=self.ctx.device, layer_first=layer)[0]
+
+    @staticmethod
+    def planes(rows):
+        """fp32 rows [n, H] -> bf16 [2, n, H]: hi = bf16_rn(x), lo = bf16_rn(x - hi)
+        (moe_kernels.cuh split_bf16; torch's bf16 cast rounds to nearest even)."""
+        import torch
+
+        out = torch.empty((2,) + tuple(rows.shape), dtype=torch.bfloat16, device=rows.device)
+        out[0].copy_(rows)
+        out[1].copy_(rows - out[0].float())
+        return out
 
     def _gpu_experts(self, layer, rows, offsets):
         import torch
@@ -319,7 +446,8 @@ class ExpertParallelMoE:
 
         out = torch.empty((rows.shape[0], self.spec.hidden_dim), dtype=torch.float32, device=rows.device)
         if rows.shape[0]:
-            call("xpgb_experts_forward", self.ctx.handle, layer, C.c_void_p(rows.data_ptr()),
+            planes = self.planes(rows)
+            call("xpgb_experts_forward", self.ctx.handle, layer, C.c_void_p(planes.data_ptr()), int(rows.shape[0]),
                  C.c_void_p(offsets.data_ptr()), int(rows.shape[0]), C.c_void_p(out.data_ptr()),
                  C.c_void_p(current_stream_ptr(self.ctx.device)))
         return out
@@ -343,9 +471,13 @@ class ExpertParallelMoE:
              int(x.shape[0]), C.c_void_p(current_stream_ptr(self.ctx.device)))
 
     # ---- one layer
-    def plan(self, layer: int, tokens: int) -> DispatchPlan:
-        routes = self.route_fn(self.fwd.router_seed, self.world * tokens, layer, self.spec.experts_per_layer,
-                               self.fwd.top_k)
+    def plan(self, layer: int, tokens: int, seed=None) -> DispatchPlan:
+        """This step's plan for `layer` (routing recomputed every call, as the reference routes
+        every forward): on the GPU with a DevicePlanner, else from route_fn on the host."""
+        seed = self.fwd.router_seed if seed is None else seed
+        if self.planner is not None:
+            return self.planner.plan(layer, tokens, seed)
+        routes = self.route_fn(seed, self.world * tokens, layer, self.spec.experts_per_layer, self.fwd.top_k)
         return build_plan(routes, self.rank, self.world, tokens, self.bounds)
 
     def forward(self, layer: int, x, plan: DispatchPlan | None = None):
@@ -355,11 +487,14 @@ class ExpertParallelMoE:
 
     def dispatch(self, x, plan: DispatchPlan):
         """Send this rank's (token, expert) rows to the owners; returns the rows of its own
-        experts, expert-major (bf16 [n_recv, H])."""
+        experts, expert-major (fp32 [n_recv, H]: as many bytes as the two bf16 planes the
+        expert GEMMs take, and the receiver splits them)."""
         import torch
 
-        send = x.index_select(0, plan.send_rows).to(torch.bfloat16)
-        recv = torch.empty((sum(plan.recv_counts), x.shape[1]), dtype=torch.bfloat16, device=x.device)
+        if plan.counts is not None:
+            plan.resolve_counts()
+        send = x.index_select(0, plan.send_rows)
+        recv = torch.empty((sum(plan.recv_counts), x.shape[1]), dtype=torch.float32, device=x.device)
         self._a2a(recv, send, plan.recv_counts, plan.send_counts)
         return recv.index_select(0, plan.to_expert)
 
@@ -442,11 +577,13 @@ class ExpertParallelRunner:
         self.transport_note = None
         if transport not in ("nccl", "p2p", "auto"):
             raise ValueError(f"unknown transport {transport!r}")
+        # the dispatch plan is rebuilt on the GPU for every layer of every step
+        self.moe.planner = DevicePlanner(spec, fwd, rank, world, fwd.tokens_per_step, device)
         if transport in ("p2p", "auto"):
             kk = min(fwd.top_k, spec.experts_per_layer)
             try:
                 self.peer = PeerExchange(rank, world, fwd.tokens_per_step, kk, spec.hidden_dim, group=group,
-                                         device=device)
+                                         device=device, fault_ptr=self.ctx.fault_ptr())
                 self.transport = "p2p"
             except Exception as exc:  # noqa: BLE001 -- auto falls back to the collective
                 if transport == "p2p":
@@ -484,16 +621,13 @@ class ExpertParallelRunner:
 
         N, L = self.spec.num_layers, self.spec.experts_per_layer
         first, count = self.shard
-        if plan.pinned_mask.any():
-            full = np.zeros((N, L), dtype=np.uint8)
-            full[:, first:first + count] = plan.pinned_mask
-            self.ctx.set_pinned(full)
+        full = np.zeros((N, L), dtype=np.uint8)
+        full[:, first:first + count] = plan.pinned_mask
         streamed = count - plan.pinned_mask.sum(axis=1).min()
         depth = getattr(plan, "depth", 2)
         # a ring below the reference's two layers, or any ring with one window in flight
-        if 0 < plan.ring and (plan.ring < 2 * streamed or depth != 2):
-            self.ctx.set_ring_depth(depth)
-            self.ctx.set_ring_experts(int(plan.ring))
+        sub = 0 < plan.ring and (plan.ring < 2 * streamed or depth != 2)
+        self.ctx.apply_residency(full, int(plan.ring) if sub else 0, depth)
         shard_map = np.repeat(plan.device_mask[:, :, None], 2, axis=2).astype(np.uint8)
         self.ctx.set_placement(_full_width(self.spec, shard_map, first, count))
 
@@ -509,6 +643,8 @@ class ExpertParallelRunner:
         opts.profile = 1 if profile else 0  # decoder launch timing (xpgb_decode_stats)
         opts.fresh_inputs = 1
         h = self.ctx.handle
+        if self.peer is not None:
+            self.peer.agree_epoch()  # collective: every rank begins its session together
         torch.cuda.synchronize(self.ctx.device)
         call("xpgb_session_begin", h, C.byref(opts), None)
         try:
@@ -521,9 +657,11 @@ class ExpertParallelRunner:
             raise
         return int(total.value), int(per_iter.value)
 
-    def _steps(self, x, g0: int, g1: int, plans):
-        """Session steps [g0, g1) (whole layers: dispatch at a layer's first window, the
-        window's grouped GEMMs, combine after its last) on torch's current stream."""
+    def _steps(self, x, g0: int, g1: int, seed=None):
+        """Session steps [g0, g1) (whole layers: route + plan and dispatch at a layer's first
+        window, the window's grouped GEMMs, combine after its last) on torch's current
+        stream.  The plan is rebuilt on the GPU for every layer of every step (no host sync
+        on the peer-memory transport; NCCL reads the split sizes once per layer)."""
         import torch
 
         from .device import current_stream_ptr
@@ -532,32 +670,37 @@ class ExpertParallelRunner:
         T = x.shape[0]
         info = (C.c_int32 * 7)()
         out = None
-        n_rows, rows_ptr = 0, 0
+        n_rows, rows_ptr, lo_rows, planes = 0, 0, 0, None
+        plan = None
         peer = self.peer
         kk = min(self.fwd.top_k, self.spec.experts_per_layer)
         H = self.spec.hidden_dim
         for g in range(g0, g1):  # steps are layers, or windows of a sub-layer ring
             call("xpgb_session_step", h, g, info)
             layer, e0, e1, first, last = info[1], info[3], info[4], info[5], info[6]
-            plan = plans[layer - 1]
             stream = current_stream_ptr(self.ctx.device)
             st = C.c_void_p(stream)
             if first:
+                plan = self.moe.plan(layer, T, seed)
                 if peer is not None:
-                    n_rows = int(plan.c_rank.numel())
-                    rows_ptr = peer.dispatch(x, plan, stream)  # rows land expert-major in my window
+                    # rows land expert-major in my window (n_own stays on the device)
+                    n_rows, lo_rows = plan.cap_rows, peer.in_rows
+                    rows_ptr = peer.dispatch(x, plan, stream)
+                    out = None
                 else:
                     rows = self.moe.dispatch(x, plan)
-                    n_rows, rows_ptr = int(rows.shape[0]), rows.data_ptr()
-                out = torch.empty((n_rows, H), dtype=torch.float32, device=x.device)
+                    n_rows = int(rows.shape[0])
+                    planes = ExpertParallelMoE.planes(rows)
+                    rows_ptr, lo_rows = planes.data_ptr(), max(1, n_rows)
+                    out = torch.empty((n_rows, H), dtype=torch.float32, device=x.device)
             call("xpgb_session_acquire", h, g, st)
             if n_rows and e1 > e0:
                 # peer windows: the last window leaves its split-K partials for the fused
                 # reduce + combine scatter; NCCL reduces into `out` here
                 reduce = 1 if (last and peer is None) else 0
-                call("xpgb_experts_forward_range", h, layer, C.c_void_p(rows_ptr),
+                call("xpgb_experts_forward_range", h, layer, C.c_void_p(rows_ptr), int(lo_rows),
                      C.c_void_p(plan.offsets.data_ptr()), n_rows, e0, e1, reduce,
-                     C.c_void_p(out.data_ptr()), st)
+                     C.c_void_p(out.data_ptr() if out is not None else 0), st)
             call("xpgb_session_release", h, g, st)
             call("xpgb_session_materialize", h, g + 2)
             if last:
@@ -587,18 +730,17 @@ class ExpertParallelRunner:
             copy_busy_seconds=(rep.copy_busy_ns[0] * 1e-9, rep.copy_busy_ns[1] * 1e-9),
             elapsed_seconds=rep.elapsed_ns * 1e-9, kernels=_kernel_stats(rep), decoded_bytes=int(rep.decoded_bytes))
 
-    def _plans(self, tokens: int):
-        return [self.moe.plan(layer, tokens) for layer in range(1, self.spec.num_layers + 1)]
-
     def run(self, iterations: int, acts, profile: bool = False) -> RunReport:
         import torch
 
         x = acts if isinstance(acts, torch.Tensor) else torch.from_numpy(np.asarray(acts, np.float32))
         x = x.to(f"cuda:{self.ctx.device}", torch.float32).contiguous()
-        plans = self._plans(x.shape[0])  # routing: a pure function of (seed, token, layer)
+        if x.shape[0] > self.fwd.tokens_per_step:
+            raise XpgError(f"{x.shape[0]} tokens per rank exceed the runner's {self.fwd.tokens_per_step} "
+                           "(every rank steps the same number of tokens)")
         total, _ = self._begin(iterations, x.shape[0], profile=profile)
         try:
-            x = self._steps(x, 0, total, plans)
+            x = self._steps(x, 0, total)
         except Exception:
             _lib.lib().xpgb_session_abort(self.ctx.handle)
             raise
@@ -616,25 +758,28 @@ class EPDecodeSession:
         self.runner = runner
         self.max_iterations = max_iterations
         self.T = runner.fwd.tokens_per_step
-        self.plans = runner._plans(self.T)
         self.total, self.per_iter = runner._begin(max_iterations, self.T, log=log)
         self.g = 0
         self.steps_run = 0
         self.x = None
         self.closed = False
 
-    def step(self, acts, out=None):
+    def step(self, acts, out=None, router_seed=None):
         """acts: [T, H] fp32 (numpy, pinned CPU tensor or CUDA tensor); returns the layer
-        stack's output (into `out` when given, e.g. pinned host memory)."""
+        stack's output (into `out` when given, e.g. pinned host memory).  Every step routes
+        afresh on the GPU; router_seed (default fwd.router_seed) stands in for a gate whose
+        decisions change from step to step."""
         import torch
 
         if self.closed or self.steps_run >= self.max_iterations:
             raise XpgError("session is closed or out of iterations")
+        if np.shape(acts)[0] != self.T:
+            raise XpgError(f"a session step takes {self.T} tokens per rank, got {np.shape(acts)[0]}")
         dev = f"cuda:{self.runner.ctx.device}"
         x = acts if isinstance(acts, torch.Tensor) else torch.from_numpy(np.asarray(acts, np.float32))
         x = x.to(dev, torch.float32, non_blocking=True).contiguous()
         try:
-            y = self.runner._steps(x, self.g, self.g + self.per_iter, self.plans)
+            y = self.runner._steps(x, self.g, self.g + self.per_iter, router_seed)
         except Exception:
             self.abort()
             raise

@@ -299,19 +299,17 @@ class StreamedRunner:
         self.device_experts = [int(v) for v in mask.sum(axis=1)]
 
     def apply_plan(self, plan) -> None:
-        """Apply a budget.ResidencyPlan: pinned experts, device-tier experts, ring size."""
+        """Apply a budget.ResidencyPlan -- pinned experts, ring size and depth, device-tier
+        experts -- replacing whatever residency state an earlier plan left."""
         spec = self.hierarchy.container.spec
         first, count = self._shard
-        if plan.pinned_mask.any():
-            full = np.zeros((self.spec.num_layers, self.spec.experts_per_layer), dtype=np.uint8)
-            full[:, first:first + count] = plan.pinned_mask.reshape(spec.num_layers, spec.experts_per_layer)
-            self.ctx.set_pinned(full)
+        full = np.zeros((self.spec.num_layers, self.spec.experts_per_layer), dtype=np.uint8)
+        full[:, first:first + count] = plan.pinned_mask.reshape(spec.num_layers, spec.experts_per_layer)
         streamed = spec.experts_per_layer - plan.pinned_mask.sum(axis=1).min()
         depth = getattr(plan, "depth", 2)
         # a ring below the reference's two layers, or any ring with one window in flight
-        if 0 < plan.ring and (plan.ring < 2 * streamed or depth != 2):
-            self.ctx.set_ring_depth(depth)
-            self.ctx.set_ring_experts(int(plan.ring))
+        sub = 0 < plan.ring and (plan.ring < 2 * streamed or depth != 2)
+        self.ctx.apply_residency(full, int(plan.ring) if sub else 0, depth)
         self.set_device_mask(plan.device_mask)
 
     def set_device_experts(self, m_layers) -> None:

@@ -67,8 +67,8 @@ def _shared_fn(words_shared):
     sp = O.SharedPool(N, 1, H, F, words_shared)
 
     def shared_fn(layer, x, y):
-        xs = O.bf16_to_f32(O.f32_to_bf16(x.numpy()))  # the GPU path feeds bf16 rows
-        y += torch.from_numpy(O.expert_rows(sp.tensor_f32(layer, 1, 1), sp.tensor_f32(layer, 1, 2), xs))
+        # the GPU path feeds the rows as their hi/lo bf16 planes: float32 x to ~2^-17
+        y += torch.from_numpy(O.expert_rows(sp.tensor_f32(layer, 1, 1), sp.tensor_f32(layer, 1, 2), x.numpy()))
 
     return shared_fn, sp
 
@@ -120,14 +120,13 @@ def test_ep_matches_single_gpu_oracle(world, shared):
         p.join(timeout=60)
         assert p.exitcode == 0
     y = np.concatenate([got[r] for r in range(world)])
-    # single-device oracle on the concatenated batch, activations rounded to bf16 at
-    # every dispatch exactly as the EP path does
+    # single-device oracle on the concatenated batch (the dispatch moves float32 rows)
     words = O.synth_payload(N, L, H, F, 4)
     pool = O.WordPool(N, L, H, F, words)
     a = np.random.default_rng(seed).standard_normal((world * T, H), dtype=np.float32)
     sp = _shared_fn(O.synth_payload(N, 1, H, F, 5))[1] if shared else None
     for layer in (1, 2):
-        a = O.layer_forward(pool, layer, O.bf16_to_f32(O.f32_to_bf16(a)), K, seed, shared=sp)
+        a = O.layer_forward(pool, layer, a, K, seed, shared=sp)
     assert O.rel_l2(y, a) < 1e-5
 
 

@@ -148,3 +148,75 @@ def test_ep_empty_step(transport):
     runner.close()
     assert tuple(rep.final_activations.shape) == (0, spec.hidden_dim)
     assert rep.page_fault is None and rep.violations == []
+
+
+def _fault_worker(rank, world, port, mode, q):
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        try:
+            import paper_2604_02715_b200 as X
+            from paper_2604_02715_b200.expert_parallel import ExpertParallelRunner
+
+            spec = X.ModelSpec(*SPEC)
+            fwd = X.ForwardSpec(T, K, SEED)
+            container = X.generate_synthetic_model(spec, SEED)
+            x = np.random.default_rng(rank).standard_normal((T, spec.hidden_dim), dtype=np.float32)
+            runner = ExpertParallelRunner(spec, container, fwd, rank, world, host_codec=True, transport="p2p")
+            if mode == "fault" or rank == 1:
+                sess = runner.open_session(max_iterations=1)
+                if mode == "fault" and rank == 0:
+                    from paper_2604_02715_b200._lib import call
+
+                    call("xpgb_fault_set", runner.ctx.handle, 1 | (1 << 8) | (1 << 32))  # as a page fault would
+                t0 = time.time()
+                sess.step(x)
+                rep = sess.close()
+                q.put((rank, (rep.page_fault, time.time() - t0)))
+            else:  # "silent": rank 0 joins the session's epoch agreement, then never steps
+                runner.peer.agree_epoch()
+                time.sleep(30)
+                q.put((rank, (None, 0.0)))
+            torch.cuda.synchronize()
+        except Exception:
+            import traceback
+
+            q.put((rank, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["fault", "silent"])
+def test_peer_fault_and_timeout_reach_every_rank(mode):
+    """A rank whose step faulted raises its peers' fault words with the epoch (its rows are
+    garbage), so the peer reports a fault instead of combining stale rows; a peer that never
+    publishes makes the wait give up after 20 s with a fault, not a trap."""
+    import torch.multiprocessing as mp
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fault_worker, args=(r, world, port, mode, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        if p.is_alive():
+            p.kill()
+    for r, v in got.items():
+        assert not isinstance(v, str), v
+    fault1, secs1 = got[1]
+    assert fault1 is not None and "peer rank 0" in fault1, fault1
+    if mode == "fault":
+        assert got[0][0] is not None
+        assert "faulted" in fault1
+    else:
+        assert "no epoch" in fault1 and secs1 >= 19.0

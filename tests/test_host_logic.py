@@ -51,6 +51,21 @@ def test_generator_bit_identical_to_reference(golden):
             assert hashlib.sha256(c.payload).hexdigest() == digest, key
 
 
+@pytest.mark.parametrize("total,seg_draws,threads", [(1, 1 << 10, 4), (4097, 1 << 10, 3), (1_000_003, 1 << 12, 8),
+                                                      (300_000, 1 << 8, 2), (2_500_000, 1 << 16, 5)])
+def test_parallel_generator_splices_to_one_shot_stream(total, seg_draws, threads):
+    """The segment-parallel decode of the PCG64 normal stream (geometry._fill_normal_bf16)
+    equals the reference's one-shot draw (model.py:205-214), across hundreds of splices,
+    tiny segments and an output split over two arrays (routed + shared payload)."""
+    from paper_2604_02715_b200.geometry import SYNTH_STD, _fill_normal_bf16, float32_to_bf16
+
+    want = float32_to_bf16(np.random.default_rng(11).standard_normal(total, dtype=np.float32) * SYNTH_STD)
+    a = np.zeros(total // 3, np.uint16)
+    b = np.zeros(total - total // 3, np.uint16)
+    _fill_normal_bf16(11, [a, b], threads, seg_draws)
+    np.testing.assert_array_equal(np.concatenate([a, b]), want)
+
+
 def test_container_roundtrip_and_errors():
     c = X.generate_synthetic_model(TINY, 5)
     raw = c.to_bytes()

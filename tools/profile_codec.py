@@ -14,7 +14,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--values", type=int, default=117_440_512)  # Mixtral gate/up tensor
-    ap.add_argument("--chunk", type=int, default=1024)
+    ap.add_argument("--chunk", type=int, default=256)
     ap.add_argument("--reps", type=int, default=50)
     args = ap.parse_args()
     import numpy as np
@@ -57,8 +57,10 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.reps
-    print(json.dumps({"values": n, "chunk": args.chunk, "exact": ok, "ms": ms, "out_GBps": 2 * n / ms / 1e6,
-                      "in_GBps": rec.size / ms / 1e6, "ratio": ct.compressed_bytes / (2 * n),
+    print(json.dumps({"decoder": "v1" if os.environ.get("XPGB_DECODER") == "1" else "v2", "values": n,
+                      "chunk": args.chunk, "exact": ok, "ms": ms, "out_GBps": 2 * n / ms / 1e6,
+                      "in_GBps": rec.size / ms / 1e6, "algo_GBps": (rec.size + 2 * n) / ms / 1e6,
+                      "ratio": ct.compressed_bytes / (2 * n),
                       "bits_per_exponent": ct.exponent_bit_count / n}))
 
 

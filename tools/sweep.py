@@ -98,7 +98,7 @@ def main():
             ceb = runner.device_tier_bytes(Lc) / (N * Lc) * 1.002
             b = p if what == "plan" else args.budget
             plan = plan_residency(N, Lc, spec.expert_bytes, ceb, b * budget_base, shared_bytes=shared_b,
-                                  depth=args.depth, window=args.window,
+                                  overhead_bytes=runner.ctx.hbm_bytes()["staging"], depth=args.depth, window=args.window,
                                   **({"b_dec": args.b_dec * 1e9} if args.b_dec else {}))
             runner.apply_plan(plan)
         runner.run(args.warmup, acts=x)
