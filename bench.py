@@ -517,6 +517,7 @@ def main():
         hbm = runner.ctx.hbm_bytes()
         budget = (hbm["ring"] + hbm["device_tier"]) / shard_bytes
         footprint = (hbm["ring"] + hbm["staging"] + hbm["device_tier"]) / shard_bytes
+        ring_depth = runner.ctx._depth
     else:
         backends = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 55e9, 1 << 50)]
         hier = X.StorageHierarchy(container, None, X.plan_placement(cspec, backends), backends)
@@ -584,6 +585,7 @@ def main():
         hbm = runner.ctx.hbm_bytes()
         budget = (hbm["ring"] + hbm["device_tier"]) / expert_bytes
         footprint = (hbm["ring"] + hbm["staging"] + hbm["device_tier"]) / expert_bytes
+        ring_depth = runner.ctx._depth
     x_host = X.initial_activations(spec, fwd, SEED + rank)
     x_dev = torch.from_numpy(x_host).to(f"cuda:{dev}")
 
@@ -709,8 +711,8 @@ def main():
                    "device_tier_experts_per_layer": round(m_dev, 3),
                    "pinned_experts_per_layer": round(pinned_per_layer, 3),
                    "placement": ("2-layer ring" if use_ep or ring_blocks >= 2 * cspec.experts_per_layer else
-                                 f"sub-layer ring of {ring_blocks} expert blocks per kind (windows of "
-                                 f"{ring_blocks // 2} experts)") + (
+                                 f"sub-layer ring of {ring_blocks} expert blocks per kind ({ring_depth} window(s) "
+                                 f"in flight of {max(1, ring_blocks // ring_depth)} expert(s))") + (
                        f", {m_dev:.2f} experts per layer compressed in HBM (device tier, alpha="
                        f"{m_dev / (count if use_ep else cspec.experts_per_layer):.3f}, spread over the ring windows), "
                        f"the rest host" if m_dev else

@@ -159,8 +159,85 @@ def cmd_calibrate(args) -> int:
            "compression_ratio": ratio, "knee_alpha": knee,
            "note": "b_host/b_dev in raw-equivalent B/s; tau per decode iteration (N layers); knee per "
                    "simulate.knee_alpha with the measured b_host and resident tau"}
-    print(json.dumps(doc, indent=2))
+    text = json.dumps(doc, indent=2)
+    if getattr(args, "out", None):
+        Path(args.out).write_text(text)
+    print(text)
     return EXIT_OK
+
+
+def _sim_config(args):
+    """SimConfig from a `calibrate --out` file (measured on the GPU) or explicit flags."""
+    from .simulate import calibrated_config
+
+    measured = {}
+    if args.calibration:
+        measured = json.loads(Path(args.calibration).read_text())
+    for key in ("b_dev", "b_host", "tau_comp_theory", "compression_ratio"):
+        v = getattr(args, key, None)
+        if v is not None:
+            measured[key] = v
+    missing = [k for k in ("b_dev", "b_host", "tau_comp_theory") if k not in measured]
+    if missing:
+        from .errors import ConfigError
+
+        raise ConfigError(f"need {missing}: pass --calibration (from `calibrate --out`) or the flags")
+    return calibrated_config(_spec(args), measured, batch_size=args.tokens, max_new_tokens=args.iterations,
+                             kv_bytes_per_token=args.kv_bytes_per_token, context_start=args.context_start)
+
+
+def cmd_simulate(args) -> int:
+    """simulate.simulate_decode at a fixed alpha (cli.py:166-174)."""
+    from .simulate import simulate_decode, write_samples_csv
+
+    samples = simulate_decode(_sim_config(args), args.alpha)
+    write_samples_csv(samples, args.csv)
+    print(f"wrote {args.csv}: {len(samples)} iterations at alpha={args.alpha}")
+    return EXIT_OK
+
+
+def cmd_sweep_alpha(args) -> int:
+    """simulate.sweep_alpha over a residency grid + the closed-form knee (cli.py:177-189)."""
+    from .simulate import knee_alpha, sweep_alpha, write_sweep_csv
+
+    sim = _sim_config(args)
+    l = sim.spec.experts_per_layer
+    grid = [m / l for m in range(1, l + 1)] if args.grid is None else [float(x) for x in args.grid.split(",")]
+    rows = sweep_alpha(sim, grid)
+    write_sweep_csv(rows, args.csv)
+    print(f"wrote {args.csv}: {len(rows)} grid points, closed-form knee alpha*={knee_alpha(sim):.4f}")
+    return EXIT_OK
+
+
+def cmd_plan(args) -> int:
+    """The planner's closed loop over the calibrated model (cli.py:192-208)."""
+    from .residency import PlannerState
+    from .simulate import check_trace_safety, run_control_loop, write_trace_csv
+
+    sim = _sim_config(args)
+    l = sim.spec.experts_per_layer
+    state = PlannerState(experts_per_layer=l, device_experts=max(1, min(l, args.m0)), cooldown=args.cooldown,
+                         io_balance=args.io_balance == "on")
+    _, trace = run_control_loop(sim, state)
+    check_trace_safety(sim, trace)
+    write_trace_csv(trace, args.csv)
+    adjustments = sum(1 for row in trace if row.adjusted)
+    print(f"wrote {args.csv}: {len(trace)} iterations, {adjustments} adjustments, final alpha={trace[-1].alpha:.4f}")
+    return EXIT_OK
+
+
+def _sim_args(p):
+    _model_args(p)
+    p.add_argument("--calibration", help="JSON written by `calibrate --out` (b_host, b_dev, tau_comp_theory)")
+    p.add_argument("--b-dev", dest="b_dev", type=float)
+    p.add_argument("--b-host", dest="b_host", type=float)
+    p.add_argument("--tau-comp", dest="tau_comp_theory", type=float)
+    p.add_argument("--compression-ratio", dest="compression_ratio", type=float)
+    p.add_argument("--tokens", type=int, default=256, help="batch size (tokens per decode step)")
+    p.add_argument("--iterations", type=int, default=64)
+    p.add_argument("--kv-bytes-per-token", type=int, default=0)
+    p.add_argument("--context-start", type=int, default=0)
+    p.add_argument("csv", help="output CSV")
 
 
 def build_parser():
@@ -196,7 +273,22 @@ def build_parser():
     _model_args(k)
     k.add_argument("--tokens", type=int, default=256)
     k.add_argument("--top-k", type=int, default=2)
+    k.add_argument("--out", help="also write the measurements here (input of simulate/sweep-alpha/plan)")
     k.set_defaults(fn=cmd_calibrate)
+    sm = sub.add_parser("simulate", help="the reference's decode model at a fixed alpha, calibrated inputs")
+    _sim_args(sm)
+    sm.add_argument("--alpha", type=float, default=0.25)
+    sm.set_defaults(fn=cmd_simulate)
+    sw = sub.add_parser("sweep-alpha", help="steady-state tau_load over a residency grid + knee alpha*")
+    _sim_args(sw)
+    sw.add_argument("--grid", help="comma-separated alphas (default m/L, m = 1..L)")
+    sw.set_defaults(fn=cmd_sweep_alpha)
+    pl = sub.add_parser("plan", help="the residency planner's closed loop over the calibrated model")
+    _sim_args(pl)
+    pl.add_argument("--m0", type=int, default=1, help="initial device-tier experts per layer")
+    pl.add_argument("--cooldown", type=int, default=20)
+    pl.add_argument("--io-balance", choices=["on", "off"], default="on")
+    pl.set_defaults(fn=cmd_plan)
     return p
 
 
