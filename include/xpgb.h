@@ -250,6 +250,23 @@ int xpgb_set_ring_experts(xpgb_ctx* ctx, int32_t ring_experts);
  * and the session materializes up to g+depth.  Ignored without a ring cap.  Re-creates the
  * arena. */
 int xpgb_set_ring_depth(xpgb_ctx* ctx, int32_t depth);
+/* Decode-into-GEMM (B200 addition to the compressed device tier, storage.py:143-168): mode 1
+ * makes the builtin compute (xpgb_run, xpgb_session_compute) read device-tier experts'
+ * records in place -- decoder warps inside the grouped GEMM expand them into the tensor-core
+ * operand tiles -- instead of decoding each into its ring block first; the page table, the
+ * ordering log and the results are unchanged (bit-identical).  Applies to decode-sized expert
+ * groups (the 1-CTA GEMMs) when K of both projections is a multiple of the codec chunk.  Mode 0
+ * (default) keeps every expert in the ring, as callers with their own compute need
+ * (xpgb_experts_forward_range).  No session may be active. */
+int xpgb_set_fused_decode(xpgb_ctx* ctx, int32_t mode);
+/* Race hardening (debug; no reference counterpart -- the reference's sabotage control,
+ * pipeline.py:369-370, covers RAW only).  poison != 0: every ring block a window maps is filled
+ * with 0xFF bytes (bf16 NaN) on the copy stream before its load, so a GEMM that reads a block
+ * whose load has not landed, or that a later window already recycled, produces NaNs.
+ * skip_war_iteration/layer (0 = none): the load of that (iteration, layer) skips its WAR wait on
+ * the compute of the step it recycles -- the WAR twin of opts.sabotage_iteration/layer.  No
+ * session may be active. */
+int xpgb_set_hazard_checks(xpgb_ctx* ctx, int32_t poison, int32_t skip_war_iteration, int32_t skip_war_layer);
 /* Staging ring of the compressed host tier: n_buffers (2..16, default 4) buffers per kind of
  * min(largest record, 64 MB).  A staged copy waits only for its buffer's previous decode, never
  * for the arena's WAR event, so the link runs n_buffers-1 pieces ahead of the decoder -- across

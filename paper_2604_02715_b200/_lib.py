@@ -120,6 +120,8 @@ _SIGS = {
     "xpgb_host_unregister": [_P],
     "xpgb_set_ring_experts": [_P, _I],
     "xpgb_set_ring_depth": [_P, _I],
+    "xpgb_set_fused_decode": [_P, _I],
+    "xpgb_set_hazard_checks": [_P, _I, _I, _I],
     "xpgb_set_stage_buffers": [_P, _I],
     "xpgb_decode_stats": [_P, _P, _P, _P],
     "xpgb_ep_window_alloc": [C.c_uint64, _P, _P],

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "codec.cuh"
+#include "codec_dev.cuh"
 #include "launch_count.h"
 
 namespace xpgb {
@@ -140,7 +141,6 @@ int codec_build_index(const uint8_t* bits, size_t bits_len, size_t n, const uint
 
 // ----------------------------------------------------------------------------- GPU decoder
 
-struct DecTables;
 struct DecodeParams {
   DecodeTensor t[kMaxDecodeTensors];  // tensors of one launch, each n values
   int ntensors;
@@ -149,30 +149,7 @@ struct DecodeParams {
   const DecTables* tabs;  // prebuilt by k_build_tables
 };
 
-__device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
-// One thread decodes one chunk (`chunk` values) starting at index[c]: a 64-bit
-// MSB-first window and a multi-symbol table -- every 11-bit pattern maps to the
-// up-to-4 whole codewords it starts with (exponents average ~2.6 bits, so one
-// lookup usually yields 3-4 values); the symbols sit in one 32-bit table and the
-// count/length in a byte table beside it.  Codes longer than the table, and a chunk's
-// last values (never decode past the chunk), take the canonical first-code search.
-// The tables are 10 KB of shared memory so decode blocks still fit beside a resident
-// GEMM CTA; the next bitstream word is always in flight.  Output words are
-// (sign << 15) | (exponent << 7) | mantissa, 16 per 32-byte store.
-constexpr int kMultiBits = 11;
-
-__device__ __forceinline__ int canon_decode(uint64_t win, int ml, const int* count, const uint32_t* first_code,
-                                            const int* first_rank, const uint8_t* sorted_sym, int* sym) {
-  for (int l = 1; l <= ml; ++l) {
-    const uint32_t code = (uint32_t)(win >> (64 - l));
-    if (count[l] && code - first_code[l] < (uint32_t)count[l]) {
-      *sym = sorted_sym[first_rank[l] + (code - first_code[l])];
-      return l;
-    }
-  }
-  return 0;  // invalid code: the host index scan rejects such streams before they get here
-}
 
 // Eight (sign/mantissa, exponent) byte pairs -> bf16 words by byte permutes:
 // x = [e1 s1 e0 s0] per 16-bit lane -> (s >> 7) << 15 | e << 7 | (s & 0x7F).
@@ -203,19 +180,6 @@ __device__ __forceinline__ void decode_chunk(R& q, uint64_t win, int avail, cons
                                              int ml, const int* count, const uint32_t* first_code,
                                              const int* first_rank, const uint8_t* sorted_sym);
 
-// Decode tables of one codec table, built once by k_build_tables and copied into every
-// decoder CTA's shared memory (building them per CTA cost ~20 us per launch -- most of a
-// small tensor's decode).
-constexpr int kPairBits = 12;
-struct DecTables {
-  uint32_t lut3[1 << kMultiBits];  // up to 4 symbols (4 x 8 b)
-  uint8_t lmeta[1 << kMultiBits];  // count | total length << 3
-  uint32_t pair[1 << kPairBits];   // k_exp_decode2's pair table (see there)
-  uint32_t first_code[kCodecMaxLen + 1];
-  int count[kCodecMaxLen + 1], first_rank[kCodecMaxLen + 1];
-  uint8_t sorted_sym[kCodecSymbols];
-  int maxlen;
-};
 
 __global__ void __launch_bounds__(256) k_build_tables(const CodecTable table, DecTables* out) {
   __shared__ uint32_t lut3[1 << kMultiBits];
@@ -306,6 +270,15 @@ __global__ void __launch_bounds__(256) k_build_tables(const CodecTable table, De
   if (tid == 0) out->maxlen = maxlen;
 }
 
+// One thread decodes one chunk (`chunk` values) starting at index[c]: a 64-bit
+// MSB-first window and a multi-symbol table -- every 11-bit pattern maps to the
+// up-to-4 whole codewords it starts with (exponents average ~2.6 bits, so one
+// lookup usually yields 3-4 values); the symbols sit in one 32-bit table and the
+// count/length in a byte table beside it.  Codes longer than the table, and a chunk's
+// last values (never decode past the chunk), take the canonical first-code search.
+// The tables are 10 KB of shared memory so decode blocks still fit beside a resident
+// GEMM CTA; the next bitstream word is always in flight.  Output words are
+// (sign << 15) | (exponent << 7) | mantissa, 16 per 32-byte store.
 __global__ void __launch_bounds__(256) k_exp_decode(const __grid_constant__ DecodeParams p) {
   __shared__ uint32_t lut3[1 << kMultiBits];
   __shared__ __align__(16) uint8_t lmeta[1 << kMultiBits];
@@ -484,6 +457,7 @@ __device__ __forceinline__ void decode_chunk(R& q, uint64_t win, int avail, cons
   }
 }
 
+
 // ---------------------------------------------------------------- decoder v2 (pair table)
 //
 // One thread per chunk as k_exp_decode, but built around a 12-bit *pair* table whose entry is
@@ -495,52 +469,7 @@ __device__ __forceinline__ void decode_chunk(R& q, uint64_t win, int avail, cons
 // path (the entry's single-code length, or the canonical first-code search for codes > 12
 // bits).  Window: 64 bits, bit position p; the stream refills one 32-bit word every second
 // pair when p >= 32, so a lookup always has 12 valid bits (p <= 43 at the odd pair).
-struct Window {
-  uint64_t win;  // bits [0, 64) of the stream from the current word, MSB first
-  int p;         // bits already consumed from the top of `win`
-  uint32_t nxt;  // next stream word (raw, in flight)
-  const uint32_t* wp;
-  __device__ __forceinline__ void refill() {
-    if (p >= 32) {
-      win = (win << 32) | bswap32(nxt);
-      nxt = *wp++;
-      p -= 32;
-    }
-  }
-  __device__ __forceinline__ uint32_t peek12() const { return (uint32_t)((win << p) >> (64 - kPairBits)); }
-};
-
-struct CanonTabs {
-  const int* count;
-  const uint32_t* first_code;
-  const int* first_rank;
-  const uint8_t* sorted_sym;
-  int ml;
-};
-
-// One exponent symbol the slow way (p < 32 on entry, so >= 32 bits are valid).
-__device__ __forceinline__ uint32_t symbol_slow(Window& w, uint32_t ent, const CanonTabs& ct) {
-  int l = (int)((ent >> 16) & 31);
-  uint32_t sym = (ent >> 7) & 0xFFu;
-  if (!l) {
-    int s = 0;
-    l = canon_decode(w.win << w.p, ct.ml, ct.count, ct.first_code, ct.first_rank, ct.sorted_sym, &s);
-    sym = (uint32_t)s;
-  }
-  w.p += l;
-  return sym;
-}
-
-// A pair that does not fit the table: two single symbols; leaves p < 32.
-__device__ __forceinline__ uint32_t pair_slow(Window& w, const uint32_t* __restrict__ pair, const CanonTabs& ct) {
-  w.refill();
-  const uint32_t a = symbol_slow(w, pair[w.peek12()], ct);
-  w.refill();
-  const uint32_t b = symbol_slow(w, pair[w.peek12()], ct);
-  w.refill();
-  return (a << 7) | (b << 23);
-}
-
+template <class W>
 __global__ void __launch_bounds__(256) k_exp_decode2(const __grid_constant__ DecodeParams p) {
   __shared__ uint32_t pair[1 << kPairBits];
   __shared__ uint32_t first_code[kCodecMaxLen + 1];
@@ -574,12 +503,8 @@ __global__ void __launch_bounds__(256) k_exp_decode2(const __grid_constant__ Dec
     const uint64_t v0 = c * p.chunk;
     const uint64_t v1 = (v0 + p.chunk < n) ? v0 + p.chunk : n;
     const uint32_t bitpos = d.index[c] - d.bit_base;
-    Window w;
-    w.wp = d.bits + (bitpos >> 5);
-    w.win = ((uint64_t)bswap32(w.wp[0]) << 32) | bswap32(w.wp[1]);
-    w.nxt = w.wp[2];
-    w.wp += 3;
-    w.p = (int)(bitpos & 31);
+    W w;
+    w.init(d.bits, bitpos);
     const bool fast = ((v1 - v0) & 15) == 0 &&
                       ((reinterpret_cast<uintptr_t>(out + v0) & 31) | (reinterpret_cast<uintptr_t>(sm + v0) & 15)) == 0;
     if (fast) {
@@ -647,6 +572,8 @@ static const DecTables* decode_tables(const CodecTable& table, cudaStream_t s) {
 
 void prepare_decode_tables(const CodecTable& table, cudaStream_t s) { decode_tables(table, s); }
 
+const DecTables* codec_device_tables(const CodecTable& table, cudaStream_t s) { return decode_tables(table, s); }
+
 void launch_exp_decode_multi(const DecodeTensor* tensors, int ntensors, uint64_t n, int chunk, const CodecTable& table,
                              cudaStream_t s) {
   if (n == 0 || ntensors <= 0) return;
@@ -667,11 +594,13 @@ void launch_exp_decode_multi(const DecodeTensor* tensors, int ntensors, uint64_t
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_exp_decode, 256, 0);
     return std::max(1, sms * std::max(1, per_sm));
   }();
-  static const bool v1 = [] {  // XPGB_DECODER=1: the round-1 multi-symbol decoder (A/B only)
+  // XPGB_DECODER=1: the round-1 multi-symbol decoder; 3: the pair decoder fed from a 16-byte
+  // stream queue (QWindow); 4 / 5: 2 / 3 stream words in flight; default 2 (A/B only)
+  static const int ver = [] {
     const char* e = getenv("XPGB_DECODER");
-    return e && atoi(e) == 1;
+    return e ? atoi(e) : 2;
   }();
-  if (v1) {
+  if (ver == 1) {
     const uint64_t blocks = std::min<uint64_t>((n_chunks + 255) / 256, (uint64_t)resident);
     k_exp_decode<<<(unsigned)blocks, 256, 0, s>>>(p);
   } else {
@@ -679,11 +608,14 @@ void launch_exp_decode_multi(const DecodeTensor* tensors, int ntensors, uint64_t
       int dev = 0, sms = 148, per_sm = 4;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_exp_decode2, 256, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_exp_decode2<Window>, 256, 0);
       return std::max(1, sms * std::max(1, per_sm));
     }();
     const uint64_t blocks = std::min<uint64_t>((n_chunks + 255) / 256, (uint64_t)resident2);
-    k_exp_decode2<<<(unsigned)blocks, 256, 0, s>>>(p);
+    if (ver == 3) k_exp_decode2<QWindow><<<(unsigned)blocks, 256, 0, s>>>(p);
+    else if (ver == 4) k_exp_decode2<WindowD<2>><<<(unsigned)blocks, 256, 0, s>>>(p);
+    else if (ver == 5) k_exp_decode2<WindowD<3>><<<(unsigned)blocks, 256, 0, s>>>(p);
+    else k_exp_decode2<Window><<<(unsigned)blocks, 256, 0, s>>>(p);
   }
   note_launch();
 }

@@ -57,6 +57,9 @@ constexpr int kMaxDecodeTensors = 64;
 // Builds (once per device and table) the decode tables every decoder launch copies into
 // shared memory; launch_exp_decode* build them lazily, a context builds them up front.
 void prepare_decode_tables(const CodecTable& table, cudaStream_t s);
+// The prebuilt device tables (codec_dev.cuh) of `table`, built on first use.
+struct DecTables;
+const DecTables* codec_device_tables(const CodecTable& table, cudaStream_t s);
 
 // GPU decode: bits must be readable as 32-bit words up to round_up(bits_len, 4) + 8 bytes.
 // bit_base is subtracted from every index entry (decoding one staged piece of a stream).

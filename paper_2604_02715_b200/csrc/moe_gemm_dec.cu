@@ -1,0 +1,428 @@
+// Decode-into-GEMM: the grouped SwiGLU expert GEMM reading a device-tier expert's weights
+// straight from its compressed record (exponent-Huffman, codec.py:235-272 stream + chunk
+// index) instead of from a bf16 ring block.
+//
+// The paged path without this kernel expands every device-tier expert into the ring first
+// (k_exp_decode2 writes 2 B/value, the GEMM's TMA reads them back: 4 B/value of HBM traffic
+// on top of the ~1.34 B/value record) and runs the decoder and the GEMM as two launches that
+// compete for the SMs.  Here eight decoder warps per CTA expand the record into the UMMA A
+// tiles in shared memory, in the 128-byte-swizzled K-major layout TMA would have produced,
+// and the tensor cores consume them from there: HBM sees only the record and the activations.
+//
+// Unit = (expert, 256 weight rows, <= BN token rows, K range).  gate/up: the 256 rows are
+// 128 gate rows and the matching 128 up rows (accumulators d0 / d0+128, SwiGLU epilogue as
+// k_moe_gemm); down: 256 consecutive rows of W_down in two 128-row accumulators, fp32
+// split-K partials.  A split's K range starts on a chunk boundary, so a decoder thread
+// enters its row's stream once per unit (one chunk-index read) and then decodes the row
+// continuously across stages and chunks -- the stream of one tensor row is contiguous.
+//
+// Warps (448 threads, one CTA per SM):
+//   0      TMA producer of the activation tiles (hi and lo planes, moe_kernels.cuh)
+//   1      TMEM allocator + MMA issuer
+//   2..5   epilogue (TMEM lanes 32*(w%4)..)
+//   6..13  decoders: thread d owns weight row d of the unit (tile d>>7, tile row d&127);
+//          per 64-value stage it decodes 32 exponent pairs through the 12-bit pair table
+//          (codec_dev.cuh) and writes 8 x 16 B into its swizzled smem row, then
+//          fence.proxy.async + one mbarrier arrive per warp.
+// The "full" barrier of a stage completes on the TMA bytes of the activations plus the
+// eight decoder-warp arrivals.  The prologue repeats read_page's residency check
+// (paging.py:228-237) on every routed expert's slot-table entry, as k_moe_gemm does.
+#include <cuda_bf16.h>
+
+#include <cstdlib>
+
+#include "codec_dev.cuh"
+#include "launch_count.h"
+#include "moe_kernels.cuh"
+#include "ptx_sm100.cuh"
+
+namespace xpgb {
+
+namespace {
+
+constexpr int kDecWarps = 8;
+constexpr int kDecThreads = 192 + 32 * kDecWarps;  // 448
+constexpr int kDecRows = 256;                      // weight rows per unit (two 128-row A tiles)
+
+template <int BN, int STAGES>
+struct DecCfg {
+  static constexpr int A_BYTES = kBM * kBK * 2;             // one 128 x 64 bf16 tile
+  static constexpr int B_BYTES = BN * kBK * 2;              // one activation plane
+  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;   // two A tiles + hi/lo activations
+  static constexpr int TMEM_COLS = 512;                     // 2 accumulator stages x 256 columns
+  static constexpr int TAB_BYTES = (3 * kMaxExperts + 8) * 4;
+  static constexpr int DEC_TAB = (1 << kPairBits) * 4 + 3 * (kCodecMaxLen + 1) * 4 + kCodecSymbols;
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256 + TAB_BYTES + DEC_TAB;
+  static_assert(SMEM <= 227 * 1024, "decode-GEMM stages exceed 227 KB");
+};
+
+__device__ __forceinline__ uint8_t* align_1k(uint8_t* p) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+
+__device__ __forceinline__ float silu_d(float g) { return g * (1.0f / (1.0f + __expf(-g))); }
+
+// Generic-proxy smem writes -> visible to the tensor cores' async proxy.
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void st_smem_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
+struct DUnit {
+  int e, m0, row_begin, n_rows, split;
+};
+
+// Unit u -> (expert, 256-row weight tile, token tile, split); s_up: unit prefix per group.
+__device__ __forceinline__ DUnit dec_unit(int u, const int* s_up, const int* s_off, int E, int bn, int splits) {
+  int lo = 0, hi = E;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (s_up[mid] <= u) lo = mid; else hi = mid;
+  }
+  DUnit r;
+  r.e = lo;
+  const int local = u - s_up[lo];
+  const int n = s_off[lo + 1] - s_off[lo];
+  const int nt_count = (n + bn - 1) / bn;
+  const int m = local / (splits * nt_count);
+  const int rem = local % (splits * nt_count);
+  r.split = rem / nt_count;
+  const int nt = rem % nt_count;
+  r.m0 = m * (kDecRows / 2);  // gate/up: feature tile of 128 (gate + up rows); down: see caller
+  r.row_begin = s_off[lo] + nt * bn;
+  r.n_rows = min(bn, n - nt * bn);
+  return r;
+}
+
+}  // namespace
+
+template <bool GU, int BN, int STAGES, class WIN>
+__global__ void __maxnreg__(128)  // 448 threads x 128 registers (144 was refused at launch)
+    k_moe_gemm_dec(const __grid_constant__ CUtensorMap map_b, GemmParams p, const DecTables* __restrict__ tabs,
+                   int chunk) {
+  using C = DecCfg<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align_1k(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* s_off = reinterpret_cast<int*>(smem + STAGES * C::STAGE + 256);
+  int* s_up = s_off + kMaxExperts + 1;
+  int* s_flag = s_up + kMaxExperts + 1;
+  uint32_t* s_pair = reinterpret_cast<uint32_t*>(s_off + 3 * kMaxExperts + 8);
+  uint32_t* s_first = s_pair + (1 << kPairBits);
+  int* s_count = reinterpret_cast<int*>(s_first + kCodecMaxLen + 1);
+  int* s_rank = s_count + kCodecMaxLen + 1;
+  uint8_t* s_sym = reinterpret_cast<uint8_t*>(s_rank + kCodecMaxLen + 1);
+
+  const int E = p.E;
+  const int MT = GU ? (p.F + kBM - 1) / kBM : (p.H + kDecRows - 1) / kDecRows;
+  const int S = GU ? 1 : p.splits;
+  const uint32_t warp = warp_id_sync();
+  const uint32_t lane = threadIdx.x & 31;
+
+  // ---- prologue: unit prefix over the fused groups + page-table residency check
+  if (threadIdx.x == 0) *s_flag = (*(volatile long long*)p.fault != 0);
+  for (int e = threadIdx.x; e <= E; e += blockDim.x) s_off[e] = p.offsets[e];
+  __syncthreads();
+  if (*s_flag) return;
+  if (warp == 0) {
+    int carry = 0;
+    bool bad = false;
+    if (lane == 0) s_up[0] = 0;
+    for (int e0 = 0; e0 < E; e0 += 32) {
+      const int e = e0 + lane;
+      int u = 0;
+      if (e < E) {
+        const int n = s_off[e + 1] - s_off[e];
+        if (n > 0 && e < p.E_routed && p.dec[e].sm) {
+          u = ((n + BN - 1) / BN) * MT * S;
+          const int32_t ent = p.pt[e];
+          if (pt_state(ent) != 2) {
+            atomicCAS((unsigned long long*)p.fault, 0ull,
+                      (unsigned long long)fault_pack(p.layer, p.e_first + e + 1, GU ? 1 : 2, pt_state(ent)));
+            bad = true;
+          }
+        }
+      }
+      int x = u;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off) x += y;
+      }
+      if (e < E) s_up[e + 1] = carry + x;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) *s_flag = 1;
+  }
+  __syncthreads();
+  const int n_units = s_up[E];
+  if (*s_flag || (int)blockIdx.x >= n_units) return;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1 + kDecWarps);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  if (warp >= 6) {  // decoder tables -> smem
+    const int t = threadIdx.x - 192;
+    const uint4* src = reinterpret_cast<const uint4*>(tabs->pair);
+    for (int i = t; i < (1 << kPairBits) / 4; i += 32 * kDecWarps) reinterpret_cast<uint4*>(s_pair)[i] = src[i];
+    if (t <= kCodecMaxLen) {
+      s_first[t] = tabs->first_code[t];
+      s_count[t] = tabs->count[t];
+      s_rank[t] = tabs->first_rank[t];
+    }
+    if (t < kCodecSymbols) s_sym[t] = tabs->sorted_sym[t];
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int K = GU ? p.H : p.F;
+  const int KB = K / kBK;
+
+  if (warp == 0) {
+    // ---- activation tiles (hi, lo) by TMA
+    if (lane == 0) {
+      const uint64_t pol_b = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const DUnit un = dec_unit(u, s_up, s_off, E, BN, S);
+        int kb0 = 0, kb1 = KB;
+        if (!GU) split_kb(un.split, S, KB, &kb0, &kb1);
+        const int nb = (un.n_rows + kBoxRowsB - 1) / kBoxRowsB;
+        const uint32_t bytes = 2 * nb * kBoxRowsB * kBK * 2;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sb = smem + stage * C::STAGE + 2 * C::A_BYTES;
+          mbar_arrive_expect_tx(&full[stage], bytes);
+          for (int i = 0; i < nb; ++i) {
+            tma_load_2d(sb + i * kBoxRowsB * kBK * 2, &map_b, &full[stage], kb * kBK, un.row_begin + i * kBoxRowsB,
+                        pol_b);
+            tma_load_2d(sb + C::B_BYTES + i * kBoxRowsB * kBK * 2, &map_b, &full[stage], kb * kBK,
+                        (int)(un.row_begin + p.act_lo_rows) + i * kBoxRowsB, pol_b);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer: A tile 0 -> d0, A tile 1 -> d0 + 128, each against the hi and lo planes
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
+      const DUnit un = dec_unit(u, s_up, s_off, E, BN, S);
+      int kb0 = 0, kb1 = KB;
+      if (!GU) split_kb(un.split, S, KB, &kb0, &kb1);
+      const uint32_t idesc = idesc_bf16_f32(kBM, (un.n_rows + 15) & ~15);
+      const int acc = it & 1;
+      const uint32_t acc_par = (it >> 1) & 1;
+      mbar_wait(&tempty[acc], acc_par ^ 1);
+      tc_fence_after();
+      const uint32_t d0 = tmem + acc * 256;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t base = smem_u32(smem + stage * C::STAGE);
+          const uint32_t bbase = base + 2 * C::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            const uint64_t bdesc = sdesc_k_sw128(bbase + 32 * k);
+            const uint64_t bdesc_lo = sdesc_k_sw128(bbase + C::B_BYTES + 32 * k);
+            const uint32_t accum = (kb > kb0 || k > 0) ? 1u : 0u;
+            const uint64_t a0 = sdesc_k_sw128(base + 32 * k);
+            const uint64_t a1 = sdesc_k_sw128(base + C::A_BYTES + 32 * k);
+            umma_bf16(d0, a0, bdesc, idesc, accum);
+            umma_bf16(d0, a0, bdesc_lo, idesc, 1u);
+            umma_bf16(d0 + 128, a1, bdesc, idesc, accum);
+            umma_bf16(d0 + 128, a1, bdesc_lo, idesc, 1u);
+          }
+          umma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (lane == 0) umma_commit(&tfull[acc]);
+      __syncwarp();
+    }
+  } else if (warp < 6) {
+    // ---- epilogue
+    const int q = warp & 3;
+    int it = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
+      const DUnit un = dec_unit(u, s_up, s_off, E, BN, S);
+      const int acc = it & 1;
+      const uint32_t acc_par = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_par);
+      tc_fence_after();
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * 256;
+      if (GU) {
+        const int r = un.m0 + q * 32 + lane;
+        __nv_bfloat16* hcol = p.hbuf + (size_t)un.row_begin * p.F + r;
+        const size_t lo_off = (size_t)p.h_lo_rows * p.F;
+        for (int c0 = 0; c0 < un.n_rows; c0 += 16) {
+          float g[16], v[16];
+          tmem_ld16(tbase + c0, g);
+          tmem_ld16(tbase + 128 + c0, v);
+          if (r < p.F) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (c0 + i < un.n_rows) {
+                __nv_bfloat16 hi, lo;
+                split_bf16(silu_d(g[i]) * v[i], &hi, &lo);
+                hcol[(size_t)(c0 + i) * p.F] = hi;
+                hcol[(size_t)(c0 + i) * p.F + lo_off] = lo;
+              }
+          }
+        }
+      } else {
+        const int m0 = 2 * un.m0;  // 256-row tiles of W_down
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          const int r = m0 + half * 128 + q * 32 + lane;
+          float* out = p.part + un.split * p.split_stride + (size_t)un.row_begin * p.H + r;
+          for (int c0 = 0; c0 < un.n_rows; c0 += 16) {
+            float v[16];
+            tmem_ld16(tbase + half * 128 + c0, v);
+            if (r < p.H) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if (c0 + i < un.n_rows) out[(size_t)(c0 + i) * p.H] = v[i];
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  } else {
+    // ---- decoders: thread d owns weight row d of the unit
+    const int d = threadIdx.x - 192;
+    const int a = d >> 7, lr = d & 127;
+    const uint32_t sw = (uint32_t)(lr & 7);
+    const CanonTabs ct{s_count, s_first, s_rank, s_sym, tabs->maxlen};
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      const DUnit un = dec_unit(u, s_up, s_off, E, BN, S);
+      int kb0 = 0, kb1 = KB;
+      if (!GU) split_kb(un.split, S, KB, &kb0, &kb1);
+      const DecRec R = p.dec[un.e];
+      const int wrow = GU ? (a ? p.F : 0) + un.m0 + lr : 2 * un.m0 + d;
+      const bool valid = GU ? (un.m0 + lr < p.F) : (2 * un.m0 + d < p.H);
+      const uint64_t v0 = (uint64_t)wrow * K + (uint64_t)kb0 * kBK;
+      WIN w;
+      const uint8_t* smp = R.sm + v0;
+      uint4 nsm[4];
+      if (valid) {
+        w.init(R.bits, R.index[v0 / chunk] - R.bit_base);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) nsm[g] = __ldg(reinterpret_cast<const uint4*>(smp) + g);
+      }
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (valid) {
+          uint4 csm[4];
+#pragma unroll
+          for (int g = 0; g < 4; ++g) csm[g] = nsm[g];
+          smp += kBK;
+          if (kb + 1 < kb1) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) nsm[g] = __ldg(reinterpret_cast<const uint4*>(smp) + g);
+          }
+          const uint32_t row = smem_u32(smem + stage * C::STAGE + a * C::A_BYTES + lr * 128);
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const uint32_t smw[4] = {csm[g].x, csm[g].y, csm[g].z, csm[g].w};
+            uint32_t o[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              if ((j & 1) == 0) w.refill();
+              uint32_t e = s_pair[w.peek12()];
+              const int len = (int)(e & 15u);
+              if (__builtin_expect(len == 0, 0)) e = pair_slow(w, s_pair, ct);
+              else w.p += len;
+              const uint32_t dup = __byte_perm(smw[j >> 1], 0, (j & 1) ? 0x3322u : 0x1100u);
+              o[j] = (dup & 0x807F807Fu) | (e & 0x7F807F80u);
+            }
+            st_smem_v4(row + ((((uint32_t)(2 * g)) ^ sw) << 4), o[0], o[1], o[2], o[3]);
+            st_smem_v4(row + ((((uint32_t)(2 * g + 1)) ^ sw) << 4), o[4], o[5], o[6], o[7]);
+          }
+          fence_async_smem();
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<C::TMEM_COLS>(tmem);
+}
+
+// ---- instantiations / launchers
+
+using DecKernel = void (*)(const CUtensorMap, GemmParams, const DecTables*, int);
+
+// stage counts: the A tiles are produced on-chip, so a few stages cover the decoder/MMA overlap
+#define XPGB_DEC_TILES(X) X(32, 4) X(48, 4) X(64, 3) X(80, 3) X(96, 3) X(128, 2)
+
+template <bool GU, int BN, int ST>
+static void set_dec_attr() {
+  cudaFuncSetAttribute(k_moe_gemm_dec<GU, BN, ST, QWindow>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       DecCfg<BN, ST>::SMEM);
+  cudaFuncSetAttribute(k_moe_gemm_dec<GU, BN, ST, Window>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       DecCfg<BN, ST>::SMEM);
+}
+
+void set_gemm_dec_attrs() {
+#define XPGB_SET_DEC(BN, ST) set_dec_attr<true, BN, ST>(); set_dec_attr<false, BN, ST>();
+  XPGB_DEC_TILES(XPGB_SET_DEC)
+#undef XPGB_SET_DEC
+}
+
+// A unit's K range (a split_kb range: multiples of 256 values) must start on a chunk boundary.
+bool gemm_dec_supported(int H, int F, int chunk) {
+  return chunk >= kBK && 256 % chunk == 0 && H % 256 == 0 && F % 256 == 0 && H % kDecRows == 0 && F % kBM == 0;
+}
+
+void launch_gemm_dec(bool gate_up, const CUtensorMap& map_b, const GemmParams& p, const CodecTable& table, int chunk,
+                     int bn, int grid, cudaStream_t s) {
+  const DecTables* tabs = codec_device_tables(table, s);
+  if (!tabs) return;
+  // XPGB_FUSED_WIN=1: the one-word-ahead stream window instead of the 16-byte queue (A/B)
+  static const bool word = getenv("XPGB_FUSED_WIN") && atoi(getenv("XPGB_FUSED_WIN")) == 1;
+  DecKernel kern = nullptr;
+  int smem = 0;
+#define XPGB_PICK_DEC(BN, ST)                                                                          \
+  if (bn == BN) {                                                                                      \
+    kern = word ? (gate_up ? k_moe_gemm_dec<true, BN, ST, Window> : k_moe_gemm_dec<false, BN, ST, Window>) \
+                : (gate_up ? k_moe_gemm_dec<true, BN, ST, QWindow> : k_moe_gemm_dec<false, BN, ST, QWindow>); \
+    smem = DecCfg<BN, ST>::SMEM;                                                                       \
+  }
+  XPGB_DEC_TILES(XPGB_PICK_DEC)
+#undef XPGB_PICK_DEC
+  if (!kern) {
+    kern = gate_up ? k_moe_gemm_dec<true, 128, 2, QWindow> : k_moe_gemm_dec<false, 128, 2, QWindow>;
+    smem = DecCfg<128, 2>::SMEM;
+  }
+  kern<<<grid, kDecThreads, smem, s>>>(map_b, p, tabs, chunk);
+  note_launch();
+}
+
+}  // namespace xpgb

@@ -483,11 +483,14 @@ __device__ __forceinline__ float silu_f(float g) { return g * (1.0f / (1.0f + __
 template <bool GU, int BN, int STAGES>
 struct GemmCfg {
   static constexpr int A_BYTES = kBM * kBK * 2;
-  static constexpr int NA = GU ? 2 : 1;  // A tiles per stage (gate + up)
+  // A tiles per stage: gate + up, or (down, BN <= 128) two consecutive 128-row tiles of W_down
+  // so each activation tile staged feeds 256 weight rows (halves the L2->SM activation bytes)
+  static constexpr int NA = (GU || BN <= 128) ? 2 : 1;
+  static constexpr int UNIT_ROWS = GU ? kBM : NA * kBM;  // weight rows per unit (per projection)
   static constexpr int B_BYTES = BN * kBK * 2;  // one activation plane
   static constexpr int STAGE = NA * A_BYTES + 2 * B_BYTES;  // weights + the hi and lo activation planes
   // TMEM columns per accumulator stage: gate+up = 2 x 128; down = BN (128 or 256 for prefill)
-  static constexpr int ACC_COLS = GU ? 256 : (BN > 128 ? BN : 128);
+  static constexpr int ACC_COLS = (GU || BN <= 128) ? 256 : BN;
   static constexpr int TMEM_COLS = 2 * ACC_COLS;
   static constexpr int TAB_BYTES = (3 * kMaxExperts + 8) * 4;
   static constexpr int SMEM = STAGES * STAGE + 1024 + 256 + TAB_BYTES;
@@ -499,7 +502,7 @@ struct Unit {
 };
 
 __device__ __forceinline__ Unit decode_unit(int u, const int* s_up, const int* s_off, int E, int bn, int splits,
-                                            bool gate_up) {
+                                            bool gate_up, int unit_rows) {
   int lo = 0, hi = E;  // largest e with s_up[e] <= u
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
@@ -521,7 +524,7 @@ __device__ __forceinline__ Unit decode_unit(int u, const int* s_up, const int* s
     r.split = rem / nt_count;
     nt = rem % nt_count;
   }
-  r.m0 = m * kBM;
+  r.m0 = m * unit_rows;
   r.row_begin = s_off[lo] + nt * bn;
   r.n_rows = min(bn, n - nt * bn);
   return r;
@@ -545,7 +548,7 @@ __global__ void __launch_bounds__(192, 1)
   int* s_flag = s_slot + kMaxExperts;
 
   const int E = p.E;
-  const int MT = ((GU ? p.F : p.H) + kBM - 1) / kBM;
+  const int MT = ((GU ? p.F : p.H) + C::UNIT_ROWS - 1) / C::UNIT_ROWS;
   const int S = GU ? 1 : p.splits;
   const uint32_t warp = warp_id_sync();
   const uint32_t lane = threadIdx.x & 31;
@@ -564,7 +567,7 @@ __global__ void __launch_bounds__(192, 1)
       int u = 0;
       if (e < E) {
         const int n = s_off[e + 1] - s_off[e];
-        if (n > 0) {
+        if (n > 0 && !(p.dec && e < p.E_routed && p.dec[e].sm)) {  // fused groups: k_moe_gemm_dec
           u = ((n + BN - 1) / BN) * MT * S;
           if (e < p.E_routed) {
             const int32_t ent = p.pt[e];
@@ -618,8 +621,9 @@ __global__ void __launch_bounds__(192, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-        const Unit un = decode_unit(u, s_up, s_off, E, BN, S, GU);
-        const int kb0 = GU ? 0 : un.split * KB / S, kb1 = GU ? KB : (un.split + 1) * KB / S;
+        const Unit un = decode_unit(u, s_up, s_off, E, BN, S, GU, C::UNIT_ROWS);
+        int kb0 = 0, kb1 = KB;
+        if (!GU) split_kb(un.split, S, KB, &kb0, &kb1);
         const int nb = (un.n_rows + kBoxRowsB - 1) / kBoxRowsB;
         const int wrow = s_slot[un.e] * rows_per_block + un.m0;
         const CUtensorMap* mw = un.e < p.E_routed ? &map_w : &map_ws;
@@ -629,7 +633,7 @@ __global__ void __launch_bounds__(192, 1)
           uint8_t* sa = smem + stage * C::STAGE;
           mbar_arrive_expect_tx(&full[stage], bytes);
           tma_load_2d(sa, mw, &full[stage], kb * kBK, wrow, pol_w);
-          if (GU) tma_load_2d(sa + C::A_BYTES, mw, &full[stage], kb * kBK, wrow + p.F, pol_w);
+          if (C::NA == 2) tma_load_2d(sa + C::A_BYTES, mw, &full[stage], kb * kBK, wrow + (GU ? p.F : kBM), pol_w);
           uint8_t* sb = sa + C::NA * C::A_BYTES;
           for (int i = 0; i < nb; ++i) {
             tma_load_2d(sb + i * kBoxRowsB * kBK * 2, &map_b, &full[stage], kb * kBK, un.row_begin + i * kBoxRowsB,
@@ -646,8 +650,9 @@ __global__ void __launch_bounds__(192, 1)
     uint32_t phase = 0;
     int it = 0;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
-      const Unit un = decode_unit(u, s_up, s_off, E, BN, S, GU);
-      const int kb0 = GU ? 0 : un.split * KB / S, kb1 = GU ? KB : (un.split + 1) * KB / S;
+      const Unit un = decode_unit(u, s_up, s_off, E, BN, S, GU, C::UNIT_ROWS);
+      int kb0 = 0, kb1 = KB;
+        if (!GU) split_kb(un.split, S, KB, &kb0, &kb1);
       const uint32_t idesc = idesc_bf16_f32(kBM, (un.n_rows + 15) & ~15);
       const int acc = it & 1;
       const uint32_t acc_par = (it >> 1) & 1;
@@ -668,7 +673,7 @@ __global__ void __launch_bounds__(192, 1)
             const uint64_t adesc = sdesc_k_sw128(base + 32 * k);
             umma_bf16(d0, adesc, bdesc, idesc, accum);
             umma_bf16(d0, adesc, bdesc_lo, idesc, 1u);
-            if (GU) {
+            if (C::NA == 2) {
               const uint64_t adesc_u = sdesc_k_sw128(base + C::A_BYTES + 32 * k);
               umma_bf16(d0 + 128, adesc_u, bdesc, idesc, accum);
               umma_bf16(d0 + 128, adesc_u, bdesc_lo, idesc, 1u);
@@ -686,7 +691,7 @@ __global__ void __launch_bounds__(192, 1)
     const int q = warp & 3;
     int it = 0;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
-      const Unit un = decode_unit(u, s_up, s_off, E, BN, S, GU);
+      const Unit un = decode_unit(u, s_up, s_off, E, BN, S, GU, C::UNIT_ROWS);
       const int acc = it & 1;
       const uint32_t acc_par = (it >> 1) & 1;
       mbar_wait(&tfull[acc], acc_par);
@@ -712,14 +717,18 @@ __global__ void __launch_bounds__(192, 1)
           }
         }
       } else {
-        float* out = p.part + un.split * p.split_stride + (size_t)un.row_begin * p.H + r;
-        for (int c0 = 0; c0 < un.n_rows; c0 += 16) {
-          float v[16];
-          tmem_ld16(tbase + c0, v);
-          if (r < p.H) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (c0 + i < un.n_rows) out[(size_t)(c0 + i) * p.H] = v[i];
+        for (int half = 0; half < C::NA; ++half) {  // the unit's 128-row tiles of W_down
+          const int rh = r + half * kBM;
+          float* out = p.part + un.split * p.split_stride + (size_t)un.row_begin * p.H + rh;
+          for (int c0 = 0; c0 < un.n_rows; c0 += 16) {
+            float v[16];
+            tmem_ld16(tbase + half * 128 + c0, v);
+            if (rh < p.H) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if (c0 + i < un.n_rows) out[(size_t)(c0 + i) * p.H] = v[i];
+            }
           }
         }
       }
@@ -747,13 +756,13 @@ static void set_attr() {
 // in 227 KB (stage = weight tile(s) + BN x 128 B of activations).
 // (stage = weight tile(s) + BN x 128 B of each activation plane)
 #define XPGB_GU_TILES(X) X(32, 5) X(48, 4) X(64, 4) X(80, 4) X(96, 3) X(128, 3)
-#define XPGB_DN_TILES(X) X(32, 8) X(48, 7) X(64, 6) X(80, 5) X(96, 5) X(128, 4) X(256, 2)
+#define XPGB_DN_TILES(X) X(32, 5) X(48, 4) X(64, 4) X(80, 4) X(96, 3) X(128, 3) X(256, 2)
 // Lean tiles (<= ~175 KB): one stage fewer, so decoder CTAs (10 KB each) fit on the same
 // SM.  The paged runner with a compressed tier uses them: a window's GEMM then runs beside
 // the decode of the next window instead of waiting for its CTAs to drain (Mixtral, 80%
 // budget: 11.3 K -> 13.2 K tok/s; the GEMM alone loses ~1%).
 #define XPGB_GU_LEAN(X) X(32, 4) X(48, 3) X(64, 3) X(80, 3) X(96, 2) X(128, 2)
-#define XPGB_DN_LEAN(X) X(32, 6) X(48, 5) X(64, 5) X(80, 4) X(96, 3) X(128, 3) X(256, 2)
+#define XPGB_DN_LEAN(X) X(32, 4) X(48, 3) X(64, 3) X(80, 3) X(96, 2) X(128, 2) X(256, 2)
 
 void set_gemm_attrs() {
 #define XPGB_SET_GU(BN, ST) set_attr<true, BN, ST>();
@@ -795,7 +804,7 @@ void launch_down(const CUtensorMap& map_w, const CUtensorMap& map_h, const CUten
     XPGB_DN_TILES(XPGB_PICK_DN)
   }
 #undef XPGB_PICK_DN
-  if (!kern) { kern = k_moe_gemm<false, 128, 4>; smem = GemmCfg<false, 128, 4>::SMEM; }
+  if (!kern) { kern = k_moe_gemm<false, 128, 3>; smem = GemmCfg<false, 128, 3>::SMEM; }
   kern<<<grid, 192, smem, s>>>(map_w, map_h, map_ws, p);
   note_launch();
 }

@@ -43,6 +43,31 @@ __device__ __forceinline__ void split_bf16(float v, __nv_bfloat16* hi, __nv_bflo
   *lo = __float2bfloat16_rn(v - __bfloat162float(*hi));
 }
 
+// K blocks [kb0, kb1) of split s of S over KB blocks of kBK: boundaries on multiples of 4
+// blocks (256 values) when KB allows, so a split starts on a codec chunk boundary and the
+// decode-into-GEMM kernel sums exactly the same K ranges as k_moe_gemm (bit-identical).
+__host__ __device__ inline void split_kb(int s, int S, int KB, int* kb0, int* kb1) {
+  if (KB % 4 == 0) {
+    const int n = KB / 4;
+    *kb0 = (s * n / S) * 4;
+    *kb1 = ((s + 1) * n / S) * 4;
+  } else {
+    *kb0 = s * KB / S;
+    *kb1 = (s + 1) * KB / S;
+  }
+}
+
+// A device-tier expert tensor read in place by the decode-into-GEMM kernel
+// (moe_gemm_dec.cu): its exponent-Huffman record (sign/mantissa plane, bitstream, chunk
+// index; index entries minus bit_base are bit offsets into `bits`).
+struct DecRec {
+  const uint8_t* sm;
+  const uint32_t* bits;
+  const uint32_t* index;
+  uint32_t bit_base;
+  uint32_t pad;
+};
+
 // Arguments of one grouped-GEMM launch (gate/up or down) of one layer.
 struct GemmParams {
   const int32_t* offsets;  // [E+1]
@@ -56,6 +81,9 @@ struct GemmParams {
   int layer, e_first, E, F, H, splits;
   int E_routed;       // groups [0, E_routed) are paged experts (slot table); [E_routed, E) shared experts
   int shared_block0;  // block of this layer's first shared expert in the shared-weights maps
+  // per group of the launch: groups whose record pointer is set run in the decode-into-GEMM
+  // kernel and are skipped by k_moe_gemm (nullptr: no fused groups)
+  const DecRec* dec;
 };
 
 // ---- launchers (moe_kernels.cu)
@@ -99,6 +127,14 @@ void set_pair_gemm_attrs();
 // split: the token rows' lo plane is a second MMA per K step (as the 1-CTA kernel always
 // does); false takes bf16 activations only (2x the tensor throughput at prefill, per-layer
 // rel-L2 ~3e-3 instead of ~1e-6; XPGB_FAST_PREFILL=1).
+// Decode-into-GEMM (moe_gemm_dec.cu): the groups g with p.dec[g].sm set, weights expanded
+// from their compressed records into the UMMA tiles on-chip.  Needs K % chunk == 0 for both
+// projections (a split starts on a chunk boundary) and H % 256 == 0.
+struct CodecTable;
+bool gemm_dec_supported(int H, int F, int chunk);
+void set_gemm_dec_attrs();
+void launch_gemm_dec(bool gate_up, const CUtensorMap& map_b, const GemmParams& p, const CodecTable& table, int chunk,
+                     int bn, int grid, cudaStream_t s);
 void launch_gemm_pair(bool gate_up, const CUtensorMap& map_x, const CUtensorMap& map_w, const CUtensorMap& map_ws,
                       const GemmParams& p, int num_sms, cudaStream_t s, bool split = true);
 

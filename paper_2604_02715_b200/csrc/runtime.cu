@@ -270,6 +270,18 @@ struct Ctx {
   cudaStream_t s_devdec[2] = {nullptr, nullptr};  // device-tier decodes: never queue behind the link
   cudaEvent_t ev_copied[2][kMaxStageBufs], ev_decoded[2][kMaxStageBufs], ev_mapped[2], ev_raw[2], ev_devdec[2];
   bool codec_events = false;
+  // decode-into-GEMM (moe_gemm_dec.cu): device-tier experts are read in place by the GEMM
+  // instead of being expanded into their ring block.  fused_mode: 0 off (default; external
+  // compute such as the EP runner reads ring blocks), 1 on for the builtin compute;
+  // fused_now: on for the current run/session (decode-sized groups, supported shape).
+  int fused_mode = 0;
+  bool fused_now = false;
+  // race hardening (xpgb_set_hazard_checks): poison every block a window maps with 0xFF
+  // bytes (bf16 NaN) before its load, and optionally skip one step's WAR wait, so a WAR
+  // hazard shows up as NaNs in the results as well as a violation in the ordering log
+  bool poison = false;
+  int war_sab_it = 0, war_sab_layer = 0;
+  DecRec* d_decrec = nullptr;  // [N][2][E]: record of each device-tier tensor (sm == nullptr: not device tier)
 
   // profiling
   bool prof = false;
@@ -324,6 +336,8 @@ static void free_pools(Ctx* c) {
   if (c->arena) cudaFree(c->arena);
   if (c->d_pt) cudaFree(c->d_pt);
   if (c->dev_tier) cudaFree(c->dev_tier);
+  if (c->d_decrec) cudaFree(c->d_decrec);
+  c->d_decrec = nullptr;
   c->arena = nullptr;
   c->d_pt = nullptr;
   c->dev_tier = nullptr;
@@ -434,6 +448,15 @@ static double avg_group_rows(Ctx* c, int T, int kk) {
 
 static int pick_bn(Ctx* c, int T, int kk) { return pick_bn_rows(avg_group_rows(c, T, kk)); }
 
+// Decode-into-GEMM tile: every extra token tile of an expert decodes its weights again, so
+// cover mean + 3 sd of the rows per expert (capped at the 128-column accumulators).
+static int pick_bn_dec(Ctx* c, int T, int kk) {
+  const double avg = avg_group_rows(c, T, kk);
+  const double want = avg + 3.0 * std::sqrt(std::max(avg, 0.0));
+  for (int bn : {32, 48, 64, 80, 96}) if (want <= bn) return bn;
+  return 128;
+}
+
 // Lean GEMM tiles while a compressed tier decodes on the SMs of a paged run (moe_kernels.cu:
 // XPGB_GU_LEAN); XPGB_COSCHED=0/1 forces either.
 static bool lean_gemm(const Ctx* c) {
@@ -458,7 +481,8 @@ static int pick_splits(Ctx* c, int T, int kk, int bn) {
   const long long active = std::min<long long>(c->E, (long long)T * kk);
   if (active <= 0) return 1;
   const long long rows_per = std::max<long long>(1, ((long long)T * kk + active - 1) / active);
-  const long long tiles = active * ((c->H + kBM - 1) / kBM) * ((rows_per + bn - 1) / bn);
+  const int unit_rows = bn <= 128 ? 2 * kBM : kBM;  // k_moe_gemm<down>: two 128-row tiles per unit at bn <= 128
+  const long long tiles = active * ((c->H + unit_rows - 1) / unit_rows) * ((rows_per + bn - 1) / bn);
   int best = 1;
   double best_eff = -1;
   for (int s = 1; s <= max_s; ++s) {
@@ -473,6 +497,28 @@ static int pick_splits(Ctx* c, int T, int kk, int bn) {
 static void prof_rec(Ctx* c, int i, cudaStream_t s) {
   if (c->cur_ev) CK(cudaEventRecord(c->cur_ev[i], s));
   else if (c->prof) CK(cudaEventRecord(c->pev[i], s));
+}
+
+// Expert groups of >= 128 rows on average run on CTA pairs (256 x 256 tiles, unsplit);
+// measured crossover on B200 (profiles/r1_pair_crossover.jsonl): at 64 rows per expert the
+// 1-CTA swap-AB kernel is ahead, from 128 rows the pair kernel wins (up to 2.4x at 8K rows)
+static bool use_pair(Ctx* c, int T, int kk) {
+  return pair_gemm_supported(c->H, c->F) &&
+         (c->pair_mode == 1 || (c->pair_mode < 0 && avg_group_rows(c, T, kk) >= 128.0));
+}
+
+// Decode-into-GEMM for this run: builtin compute asked for it, a compressed device tier
+// exists, the shape is supported and the groups are decode-sized (1-CTA kernels).
+static bool fused_for(Ctx* c, int T, int top_k) {
+  return c->fused_mode == 1 && c->codec && c->d_decrec && c->pool == XPGB_POOL_RING &&
+         gemm_dec_supported(c->H, c->F, c->cchunk) && !use_pair(c, T, std::min(top_k, c->L));
+}
+
+// Is tensor (layer, local expert e, kind) read in place by the decode-into-GEMM kernel?
+static bool fused_tensor(const Ctx* c, int layer, int e, int kind) {
+  if (!c->fused_now || e >= c->E) return false;
+  const size_t ti = ((size_t)(layer - 1) * c->E + e) * 2 + (kind - 1);
+  return c->backend[ti] == 1 && c->pinned[(size_t)(layer - 1) * c->E + e] == 0;
 }
 
 static GemmParams gemm_params(Ctx* c, int layer, int kind, const int32_t* offsets, int splits,
@@ -494,6 +540,7 @@ static GemmParams gemm_params(Ctx* c, int layer, int kind, const int32_t* offset
   p.F = c->F;
   p.H = c->H;
   p.splits = splits;
+  p.dec = nullptr;
   return p;
 }
 
@@ -521,12 +568,7 @@ static void enqueue_window(Ctx* c, int layer, const float* x, float* y, int T, i
   const int32_t* off = c->plan_off[b] + (size_t)(layer - 1) * (groups_of(c) + 1);
   const int bn = pick_bn(c, T, kk);
   const int bn_dn = pick_bn_down(c, T, kk);
-  // expert groups of >= 128 rows on average run on CTA pairs (256 x 256 tiles, unsplit);
-  // measured crossover on B200 (profiles/r1_pair_crossover.jsonl): at 64 rows per expert the
-  // 1-CTA swap-AB kernel is ahead, from 128 rows the pair kernel wins (up to 2.4x at 8K rows)
-  const double per_group = avg_group_rows(c, T, kk);
-  const bool pair = pair_gemm_supported(c->H, c->F) &&
-                    (c->pair_mode == 1 || (c->pair_mode < 0 && per_group >= 128.0));
+  const bool pair = use_pair(c, T, kk);
   const int splits = pair ? 1 : pick_splits(c, T, kt, bn_dn);
   prof_rec(c, 1, s);
   if (gather) {
@@ -545,18 +587,36 @@ static void enqueue_window(Ctx* c, int layer, const float* x, float* y, int T, i
     p->E = e1 - e0;
     p->E_routed = std::max(0, std::min(e1, c->E) - e0);
   }
+  // decode-into-GEMM: the window's device-tier groups run in k_moe_gemm_dec, the rest
+  // (ring blocks, pinned and shared experts) in k_moe_gemm, which skips the fused groups
+  bool fused[2] = {false, false}, rest[2] = {e1 > c->E, e1 > c->E};
+  if (!pair && c->fused_now) {
+    for (int kind = 1; kind <= 2; ++kind)
+      for (int e = e0; e < std::min(e1, c->E); ++e) (fused_tensor(c, layer, e, kind) ? fused : rest)[kind - 1] = true;
+    const DecRec* base = c->d_decrec + (size_t)(layer - 1) * 2 * c->E + e0;
+    if (fused[0]) pg.dec = base;
+    if (fused[1]) pd.dec = base + c->E;
+  } else {
+    rest[0] = rest[1] = true;
+  }
   if (pair)
     launch_gemm_pair(true, c->map_xp_pair, c->map_gu, c->S ? c->map_gu_sh : c->map_gu, pg, c->num_sms, s,
                      c->pair_split);
-  else
-    launch_gate_up(c->map_gu, c->map_xp, c->S ? c->map_gu_sh : c->map_gu, pg, bn, c->num_sms, s, lean_gemm(c));
+  else {
+    if (fused[0]) launch_gemm_dec(true, c->map_xp, pg, c->ctab, c->cchunk, pick_bn_dec(c, T, kk), c->num_sms, s);
+    if (rest[0])
+      launch_gate_up(c->map_gu, c->map_xp, c->S ? c->map_gu_sh : c->map_gu, pg, bn, c->num_sms, s, lean_gemm(c));
+  }
   CKLAUNCH();
   prof_rec(c, 4, s);
   if (pair)
     launch_gemm_pair(false, c->map_h_pair, c->map_dn, c->S ? c->map_dn_sh : c->map_dn, pd, c->num_sms, s,
                      c->pair_split);
-  else
-    launch_down(c->map_dn, c->map_h, c->S ? c->map_dn_sh : c->map_dn, pd, bn_dn, c->num_sms, s, lean_gemm(c));
+  else {
+    if (fused[1]) launch_gemm_dec(false, c->map_h, pd, c->ctab, c->cchunk, pick_bn_dec(c, T, kk), c->num_sms, s);
+    if (rest[1])
+      launch_down(c->map_dn, c->map_h, c->S ? c->map_dn_sh : c->map_dn, pd, bn_dn, c->num_sms, s, lean_gemm(c));
+  }
   CKLAUNCH();
   prof_rec(c, 5, s);
   if (last) {
@@ -771,7 +831,8 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
   const int chunk = (int)(sizeof(op.vals) / sizeof(int32_t));
   if (tg) {
     const int tgt = tg->layer, tlo = tg->e0, thi = std::min(tg->e1, E);
-    CK(cudaStreamWaitEvent(s, c->ev_comp[(g - depth_of(c)) % kEvRing], 0));  // WAR
+    const bool skip_war = c->war_sab_it == it && c->war_sab_layer == layer;  // hazard test only
+    if (!skip_war) CK(cudaStreamWaitEvent(s, c->ev_comp[(g - depth_of(c)) % kEvRing], 0));  // WAR
     for (int e = tlo; e < thi; ++e)
       if (!is_pinned(tgt, e)) pt_unmap(c, tgt, c->e_first + e + 1, kind);
     if (rs.log) set_rec(op, nrec++, XPGB_EV_RECYCLE, it, layer, kind, tg->it, tgt, st.w | (tg->w << 16));
@@ -813,6 +874,10 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
     launch_op(o2, s);
   }
   if (whi <= wlo && (op.n_rec > 0 || op.unmap_n > 0)) launch_op(op, s);  // window without routed experts
+  static const bool env_poison = getenv("XPGB_POISON") && atoi(getenv("XPGB_POISON")) != 0;
+  if (c->poison || env_poison)
+    for (int e = wlo; e < whi; ++e)
+      if (!is_pinned(layer, e)) CK(cudaMemsetAsync(block_ptr(c, kind, blocks[e]), 0xFF, sigma_of(c, kind), s));
   const float* delays = rs.o->fetch_delay_s;
   auto delay_of = [&](int e) -> float {
     return delays ? delays[((size_t)(layer - 1) * c->L + (c->e_first + e)) * 2 + k] : 0.f;
@@ -857,6 +922,11 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
     DecodeTensor dt[kMaxDecodeTensors];
     for (int e = wlo; e < whi;) {
       if (is_pinned(layer, e)) { ++e; continue; }
+      if (fused_tensor(c, layer, e, kind)) {  // read in place by the GEMM: nothing to expand
+        if (delay_of(e) > 0) sleep_on(d, delay_of(e));  // an injected fetch delay still holds the load
+        ++e;
+        continue;
+      }
       const size_t ti = tix(e);
       uint8_t* dst = block_ptr(c, kind, blocks[e]);
       const float dl = delay_of(e);
@@ -1106,6 +1176,7 @@ static void session_begin(Ctx* c, const xpgb_run_opts* o, float* acts) {
     c->peak = c->bound;  // pinned pages stay bound
   }
   ss.rs = RunState{c, &ss.o, acts, 0, 0, o->log_enable != 0};
+  c->fused_now = fused_for(c, o->tokens, o->top_k);
   cudaStream_t s = c->s_comp;
   CK(cudaDeviceSynchronize());  // inputs written by other streams are complete
   log_only(c, ss.rs.log, s, XPGB_EV_RUN_BEGIN, 0, 0);
@@ -1200,6 +1271,7 @@ static void session_end(Ctx* c, xpgb_report* rep) {
   Session& ss = session_of(c);
   if (!ss.active) XFAIL(XPGB_ERR, "no active session");
   ss.active = false;
+  c->fused_now = false;
   const xpgb_run_opts* o = &ss.o;
   RunState& rs = ss.rs;
   const int N = c->N;
@@ -1322,6 +1394,7 @@ static void session_abort(Ctx* c) {
   Session& ss = session_of(c);
   if (!ss.active) return;
   ss.active = false;
+  c->fused_now = false;
   cudaDeviceSynchronize();
   // drop every binding so the next run starts from an empty ring
   for (int k = 0; k < 2; ++k)
@@ -1371,6 +1444,10 @@ static void stage_device_tier(Ctx* c) {
     cudaFree(c->dev_tier);
     c->dev_tier = nullptr;
   }
+  if (c->d_decrec) {
+    cudaFree(c->d_decrec);
+    c->d_decrec = nullptr;
+  }
   const size_t pages = (size_t)c->N * c->E;
   auto tensor_bytes = [&](size_t ti) -> uint64_t {
     const uint64_t raw = (ti & 1) ? c->s2 : c->s1;
@@ -1383,7 +1460,7 @@ static void stage_device_tier(Ctx* c) {
   std::fill(c->dev_off.begin(), c->dev_off.end(), -1);
   if (total == 0) return;
   if (!c->codec && !c->host) XFAIL(XPGB_ERR_BACKEND_MISS, "device-tier staging needs the host pool");
-  CK(cudaMalloc(&c->dev_tier, total));
+  CK(cudaMalloc(&c->dev_tier, total + 256));  // slack: stream readers fetch 16-byte blocks ahead
   uint64_t at = 0;
   for (size_t ti = 0; ti < pages * 2; ++ti) {
     if (!c->backend[ti]) continue;
@@ -1393,6 +1470,23 @@ static void stage_device_tier(Ctx* c) {
     c->dev_off[ti] = (int64_t)at;
     CK(cudaMemcpy(c->dev_tier + at, src, sz, cudaMemcpyHostToDevice));
     at += (sz + 255) & ~255ull;
+  }
+  if (c->codec) {
+    // records of the device tier as the decode-into-GEMM kernel reads them, [layer][kind][expert]
+    std::vector<DecRec> recs((size_t)c->N * 2 * c->E);
+    memset(recs.data(), 0, recs.size() * sizeof(DecRec));
+    for (size_t ti = 0; ti < pages * 2; ++ti) {
+      if (!c->backend[ti]) continue;
+      const uint64_t n = ((ti & 1) ? c->s2 : c->s1) / 2;
+      const uint64_t sm16 = (n + 15) & ~15ull, bits16 = (c->rec_bits[ti] + 8 + 15) & ~15ull;
+      const uint8_t* rec = c->dev_tier + c->dev_off[ti];
+      const size_t layer0 = ti / 2 / c->E, e = ti / 2 % c->E, k = ti & 1;
+      recs[(layer0 * 2 + k) * c->E + e] = DecRec{rec, reinterpret_cast<const uint32_t*>(rec + sm16),
+                                                 reinterpret_cast<const uint32_t*>(rec + sm16 + bits16), 0u, 0u};
+    }
+    if (c->d_decrec) cudaFree(c->d_decrec);
+    CK(cudaMalloc(&c->d_decrec, recs.size() * sizeof(DecRec)));
+    CK(cudaMemcpy(c->d_decrec, recs.data(), recs.size() * sizeof(DecRec), cudaMemcpyHostToDevice));
   }
 }
 
@@ -1457,7 +1551,7 @@ static void set_codec(Ctx* c, const void* pool, uint64_t pool_bytes, const uint6
     for (int b = 0; b < kMaxStageBufs; ++b) {
       if (c->stage[k][b]) cudaFree(c->stage[k][b]);
       c->stage[k][b] = nullptr;
-      if (cap && b < c->n_stage) CK(cudaMalloc(&c->stage[k][b], cap));
+      if (cap && b < c->n_stage) CK(cudaMalloc(&c->stage[k][b], cap + 256));  // + read-ahead slack
     }
     c->stage_cap[k] = cap;
   }
@@ -1550,6 +1644,7 @@ static void create_impl(const xpgb_spec* spec, int32_t device, int32_t pool, int
     c->s2 = 2ull * c->F * c->H;
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     set_gemm_attrs();
+    set_gemm_dec_attrs();
     set_pair_gemm_attrs();
     if (const char* env = getenv("XPGB_PAIR_GEMM")) c->pair_mode = atoi(env) ? 1 : 0;
     if (const char* env = getenv("XPGB_FAST_PREFILL")) c->pair_split = atoi(env) == 0;
@@ -2101,6 +2196,25 @@ int xpgb_set_ring_experts(xpgb_ctx* h, int32_t ring_experts) {
   });
 }
 
+int xpgb_set_hazard_checks(xpgb_ctx* h, int32_t poison, int32_t skip_war_iteration, int32_t skip_war_layer) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    if (c->sess && c->sess->active) XFAIL(XPGB_ERR, "cannot change hazard checks during a session");
+    c->poison = poison != 0;
+    c->war_sab_it = skip_war_iteration;
+    c->war_sab_layer = skip_war_layer;
+  });
+}
+
+int xpgb_set_fused_decode(xpgb_ctx* h, int32_t mode) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    if (c->sess && c->sess->active) XFAIL(XPGB_ERR, "cannot switch decode-into-GEMM during a session");
+    if (mode < 0 || mode > 1) XFAIL(XPGB_ERR_OUT_OF_RANGE, "fused decode mode %d: need 0 or 1", mode);
+    c->fused_mode = mode;
+  });
+}
+
 int xpgb_set_ring_depth(xpgb_ctx* h, int32_t depth) {
   return guard([&] {
     Ctx* c = &h->c;
@@ -2132,7 +2246,7 @@ int xpgb_set_stage_buffers(xpgb_ctx* h, int32_t n_buffers) {
     for (int k = 0; k < 2; ++k) {
       for (int b = 0; b < kMaxStageBufs; ++b) {
         const bool want = b < n_buffers && c->stage_cap[k] > 0;
-        if (want && !c->stage[k][b]) CK(cudaMalloc(&c->stage[k][b], c->stage_cap[k]));
+        if (want && !c->stage[k][b]) CK(cudaMalloc(&c->stage[k][b], c->stage_cap[k] + 256));
         if (!want && c->stage[k][b]) {
           CK(cudaFree(c->stage[k][b]));
           c->stage[k][b] = nullptr;

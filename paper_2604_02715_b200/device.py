@@ -149,6 +149,16 @@ class Context:
             self.set_ring_depth(depth)
             self.set_ring_experts(ring)
 
+    def set_hazard_checks(self, poison: bool = False, skip_war=None) -> None:
+        """Debug: poison mapped ring blocks with NaN bytes; skip_war=(iteration, layer) drops
+        that load's WAR wait (the WAR twin of the reference's RAW sabotage)."""
+        it, layer = skip_war if skip_war else (0, 0)
+        call("xpgb_set_hazard_checks", self._h, 1 if poison else 0, int(it), int(layer))
+
+    def set_fused_decode(self, on: bool) -> None:
+        """Decode-into-GEMM for the builtin compute: device-tier experts read in place."""
+        call("xpgb_set_fused_decode", self._h, 1 if on else 0)
+
     def set_stage_buffers(self, n: int) -> None:
         """Staging ring of the compressed host tier: ``n`` buffers per kind (link run-ahead)."""
         call("xpgb_set_stage_buffers", self._h, int(n))

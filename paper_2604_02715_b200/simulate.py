@@ -302,3 +302,34 @@ def predict_tiered(config: SimConfig, device_per_layer: float, pinned_per_layer:
     t = max(config.tau_comp_theory, tau_load)
     return {"alpha": alpha, "pinned_fraction": pinned_per_layer / L, "tau_load": tau_load, "iteration_time": t,
             "tok_s": config.batch_size / t, "bound": "load" if tau_load >= config.tau_comp_theory else "compute"}
+
+
+def predict_sm_shared(config: SimConfig, device_per_layer: float, pinned_per_layer: float = 0.0, *,
+                      b_dec: float | None = None, b_fused: float | None = None) -> dict:
+    """Step time of this implementation's tiered decode step (our model, not the reference's).
+
+    The reference overlaps every page-in with compute (``max(tau_comp, N * tau_layer)``,
+    simulate.py:96-146).  On the GPU only the host link is a separate engine: the exponent
+    decoder runs on the same SMs as the GEMMs.  So a step costs the slower of
+      link  = host share x model bytes / b_host          (copy engines, compressed records)
+      SMs   = tau_comp + streamed-compressed share x model bytes / b_dec
+    where the streamed-compressed share is every non-pinned expert (device-tier records and
+    host records are both expanded on the SMs).  With decode-into-GEMM (``b_fused``), the
+    device-tier experts instead cost model bytes / b_fused each *in place of* their share of
+    tau_comp (their GEMM reads the record directly), and only host records pay b_dec.
+    Rates are raw-equivalent B/s; ``b_dec`` defaults to the calibrated b_dev."""
+    spec = config.spec
+    L = spec.experts_per_layer
+    total = spec.num_layers * spec.layer_bytes
+    dev = device_per_layer / L
+    pin = pinned_per_layer / L
+    host = max(0.0, 1.0 - dev - pin)
+    b_dec = config.b_dev if b_dec is None else b_dec
+    link = host * total / config.b_host
+    if b_fused:
+        sm = config.tau_comp_theory * (1.0 - dev) + dev * total / b_fused + host * total / b_dec
+    else:
+        sm = config.tau_comp_theory + (dev + host) * total / b_dec
+    t = max(link, sm)
+    return {"link_s": link, "sm_s": sm, "iteration_time": t, "tok_s": config.batch_size / t,
+            "bound": "link" if link >= sm else "sm"}

@@ -15,6 +15,8 @@ after every task, the deterministic twin of the reference's inline mode.
 
 from __future__ import annotations
 
+import os
+
 import ctypes as C
 import hashlib
 import json
@@ -213,7 +215,7 @@ class StreamedRunner:
     def __init__(self, spec: ModelSpec, hierarchy: StorageHierarchy, fwd: ForwardSpec, mode: str = "threaded",
                  compute_delay_fn=None, sabotage_skip_raw=None, trace=None, device: int = 0,
                  host_codec: bool = False, pinned=None, expert_shard=None, shared_tokens=None,
-                 ring_experts=None, stage_buffers=None, ring_depth=None):
+                 ring_experts=None, stage_buffers=None, ring_depth=None, fused_decode=None):
         """expert_shard=(first, count): this device holds only experts [first, first+count) of
         every layer -- one expert-parallel rank's slice -- and ``hierarchy`` is built on that
         shard's container (ModelSpec(N, count, H, F), shard-local order); the router still
@@ -224,7 +226,10 @@ class StreamedRunner:
         ring_depth: windows in flight on that ring (default 2; each window then holds
         ring_experts/ring_depth experts).
         stage_buffers: staging buffers per kind for the compressed host tier (2..16): how far
-        the link runs ahead of the decoder."""
+        the link runs ahead of the decoder.
+        fused_decode: device-tier experts are read in place by the GEMM (decoder warps expand
+        the records into the tensor-core tiles) instead of being decoded into the ring first;
+        default off (XPGB_FUSED=1 turns it on).  Results are bit-identical either way."""
         if mode not in ("threaded", "sequential"):
             raise XpgError(f"unknown mode {mode!r}")
         self.spec = spec
@@ -249,6 +254,9 @@ class StreamedRunner:
             self.ctx.set_codec(cm, host_compressed=host_codec)
         if stage_buffers is not None:
             self.ctx.set_stage_buffers(int(stage_buffers))
+        if fused_decode is None:
+            fused_decode = os.environ.get("XPGB_FUSED", "0") == "1"
+        self.ctx.set_fused_decode(bool(fused_decode))
         self.ctx.set_placement(placement)
         if ring_depth is not None:
             self.ctx.set_ring_depth(int(ring_depth))
