@@ -102,6 +102,29 @@ def ncu_decoder_capture():
         return None
 
 
+def parity_summary():
+    """Per-config float parity against the oracle (north star: rel err <= 1e-2, stated per
+    config), from the committed -m gpu run of tests/test_gpu_fullshape_*.py (XPGB_PARITY_LOG):
+    worst per-layer rel-L2 (teacher-forced, reference-generator weights, T = 1/16/256 and a
+    CTA-pair size), the free-running short stack, and the paged stack at the bench tiering."""
+    path = os.path.join(ROOT, "profiles", "r2_parity_fullshape.jsonl")
+    try:
+        rows = [json.loads(l) for l in open(path) if l.strip()]
+    except OSError:
+        return None
+    out = {}
+    for r in rows:
+        c = out.setdefault(r["config"], {"per_layer_max": 0.0})
+        if r["case"].startswith(("layer", "stack_teacher")):
+            c["per_layer_max"] = max(c["per_layer_max"], r["rel_l2"])
+        elif r["case"].startswith("stack_free"):
+            c["free_stack"] = {"case": r["case"], "rel_l2": r["rel_l2"]}
+        elif r["case"].startswith("paged"):
+            c["paged_stack"] = {"case": r["case"], "rel_l2": r["rel_l2"]}
+    return {"tolerance": 1e-2, "metric": "rel-L2 vs oracle layer_forward (xpg pipeline.py:192-208)",
+            "per_config": out, "source": "profiles/r2_parity_fullshape.jsonl"}
+
+
 def decoder_roofline(stats, steps, step_s, hbm_peak, hbm_src):
     """Roofline of the exponent decoder (the dominant kernel of a paged decode step): its
     algorithmic bytes per launch over its mean launch time, both over the timed run."""
@@ -741,6 +764,7 @@ def main():
                 "d2h_bytes_per_step": int(x_host.nbytes),
                 "api": "StreamedRunner.open_session(...).step(pinned host acts)" if not use_ep else
                        "ExpertParallelRunner.open_session(...).step(pinned host acts)"},
+        "parity": parity_summary(),
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "model_gen_s": gen_s,

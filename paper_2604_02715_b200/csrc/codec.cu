@@ -9,6 +9,7 @@
 
 #include "codec.cuh"
 #include "codec_dev.cuh"
+#include "ptx_sm100.cuh"
 #include "launch_count.h"
 
 namespace xpgb {
@@ -469,6 +470,44 @@ __device__ __forceinline__ void decode_chunk(R& q, uint64_t win, int avail, cons
 // path (the entry's single-code length, or the canonical first-code search for codes > 12
 // bits).  Window: 64 bits, bit position p; the stream refills one 32-bit word every second
 // pair when p >= 32, so a lookup always has 12 valid bits (p <= 43 at the odd pair).
+// One chunk [v0, v1) of one tensor with the pair table (k_exp_decode2's per-thread loop).
+template <class W>
+__device__ __forceinline__ void decode_chunk_v2(W& w, const uint8_t* __restrict__ sm, uint16_t* __restrict__ out,
+                                                uint64_t v0, uint64_t v1, const uint32_t* pair, const CanonTabs& ct) {
+    const bool fast = ((v1 - v0) & 15) == 0 &&
+                      ((reinterpret_cast<uintptr_t>(out + v0) & 31) | (reinterpret_cast<uintptr_t>(sm + v0) & 15)) == 0;
+    if (fast) {
+      uint4 nsm = *reinterpret_cast<const uint4*>(sm + v0);
+      for (uint64_t v = v0; v < v1; v += 16) {
+        const uint4 smv = nsm;
+        if (v + 16 < v1) nsm = *reinterpret_cast<const uint4*>(sm + v + 16);  // one group ahead
+        const uint32_t smw[4] = {smv.x, smv.y, smv.z, smv.w};
+        uint32_t o[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if ((j & 1) == 0) w.refill();
+          uint32_t e = pair[w.peek12()];
+          const int len = (int)(e & 15u);
+          if (__builtin_expect(len == 0, 0)) e = pair_slow(w, pair, ct);
+          else w.p += len;
+          const uint32_t dup = __byte_perm(smw[j >> 1], 0, (j & 1) ? 0x3322u : 0x1100u);
+          o[j] = (dup & 0x807F807Fu) | (e & 0x7F807F80u);
+        }
+        asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(out + v), "r"(o[0]), "r"(o[1]),
+                     "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7])
+                     : "memory");
+      }
+    } else {
+      // ragged or unaligned chunk: one symbol and one 2-byte store at a time
+      for (uint64_t v = v0; v < v1; ++v) {
+        w.refill();
+        const uint32_t sym = symbol_slow(w, pair[w.peek12()], ct);
+        const uint32_t sb = sm[v];
+        out[v] = (uint16_t)(((sb & 0x80u) << 8) | (sym << 7) | (sb & 0x7Fu));
+      }
+    }
+}
+
 template <class W>
 __global__ void __launch_bounds__(256) k_exp_decode2(const __grid_constant__ DecodeParams p) {
   __shared__ uint32_t pair[1 << kPairBits];
@@ -505,13 +544,64 @@ __global__ void __launch_bounds__(256) k_exp_decode2(const __grid_constant__ Dec
     const uint32_t bitpos = d.index[c] - d.bit_base;
     W w;
     w.init(d.bits, bitpos);
-    const bool fast = ((v1 - v0) & 15) == 0 &&
-                      ((reinterpret_cast<uintptr_t>(out + v0) & 31) | (reinterpret_cast<uintptr_t>(sm + v0) & 15)) == 0;
-    if (fast) {
+    decode_chunk_v2(w, sm, out, v0, v1, pair, ct);
+  }
+}
+
+
+// Decoder v6: the pair decoder of k_exp_decode2 with (a) one contiguous run of chunks per
+// thread -- a tensor's stream is contiguous, so the window enters it once per run instead of
+// once per chunk -- and (b) the stream fed through a per-thread shared-memory ring by cp.async
+// (SWindow, codec_dev.cuh) instead of one-word-ahead global loads, which ncu put under ~25%
+// of v2's stall samples (long scoreboard on the popped word).
+constexpr int kRun6Bytes = 128;  // SWindow ring per thread
+__global__ void __launch_bounds__(256) k_exp_decode6(const __grid_constant__ DecodeParams p) {
+  __shared__ uint32_t pair[1 << kPairBits];
+  __shared__ uint32_t first_code[kCodecMaxLen + 1];
+  __shared__ int count[kCodecMaxLen + 1], first_rank[kCodecMaxLen + 1];
+  __shared__ uint8_t sorted_sym[kCodecSymbols];
+  extern __shared__ __align__(16) uint8_t ring6[];  // 256 x kRun6Bytes
+  const int tid = threadIdx.x;
+  {
+    const DecTables* t = p.tabs;
+    const uint4* src = reinterpret_cast<const uint4*>(t->pair);
+    uint4* dst = reinterpret_cast<uint4*>(pair);
+    for (int i = tid; i < (1 << kPairBits) / 4; i += blockDim.x) dst[i] = src[i];
+    if (tid <= kCodecMaxLen) {
+      first_code[tid] = t->first_code[tid];
+      count[tid] = t->count[tid];
+      first_rank[tid] = t->first_rank[tid];
+    }
+    if (tid < kCodecSymbols) sorted_sym[tid] = t->sorted_sym[tid];
+  }
+  const CanonTabs ct{count, first_code, first_rank, sorted_sym, p.tabs->maxlen};
+  __syncthreads();
+
+  const uint64_t n = p.n;
+  const uint64_t cpt = (n + p.chunk - 1) / p.chunk;  // chunks per tensor
+  const uint64_t threads = (uint64_t)gridDim.x * blockDim.x;
+  // runs of R consecutive chunks, never across tensors: about one run per thread
+  const uint64_t R = (cpt * (uint64_t)p.ntensors + threads - 1) / threads;
+  const uint64_t rpt = (cpt + R - 1) / R;  // runs per tensor
+  const uint32_t ring = smem_u32(ring6 + tid * kRun6Bytes);
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + tid; g < rpt * (uint64_t)p.ntensors; g += threads) {
+    const int ti = (int)(g / rpt);
+    const uint64_t c0 = (g - (uint64_t)ti * rpt) * R;
+    const uint64_t c1 = c0 + R < cpt ? c0 + R : cpt;
+    const DecodeTensor& d = p.t[ti];
+    const uint8_t* __restrict__ sm = d.sm;
+    uint16_t* __restrict__ out = d.out;
+    const uint64_t v0 = c0 * p.chunk;
+    const uint64_t v1 = (c1 * p.chunk < n) ? c1 * p.chunk : n;
+    SWindow w;
+    w.init(d.bits, d.index[c0] - d.bit_base, ring, (uint32_t)(tid & 7));
+    const bool aligned = ((reinterpret_cast<uintptr_t>(out + v0) & 31) | (reinterpret_cast<uintptr_t>(sm + v0) & 15)) == 0;
+    const uint64_t vf = aligned ? v0 + ((v1 - v0) & ~15ull) : v0;  // whole groups on the fast path
+    if (vf > v0) {
       uint4 nsm = *reinterpret_cast<const uint4*>(sm + v0);
-      for (uint64_t v = v0; v < v1; v += 16) {
+      for (uint64_t v = v0; v < vf; v += 16) {
         const uint4 smv = nsm;
-        if (v + 16 < v1) nsm = *reinterpret_cast<const uint4*>(sm + v + 16);  // one group ahead
+        if (v + 16 < vf) nsm = *reinterpret_cast<const uint4*>(sm + v + 16);  // one group ahead
         const uint32_t smw[4] = {smv.x, smv.y, smv.z, smv.w};
         uint32_t o[8];
 #pragma unroll
@@ -528,15 +618,180 @@ __global__ void __launch_bounds__(256) k_exp_decode2(const __grid_constant__ Dec
                      "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7])
                      : "memory");
       }
-    } else {
-      // ragged or unaligned chunk: one symbol and one 2-byte store at a time
-      for (uint64_t v = v0; v < v1; ++v) {
-        w.refill();
-        const uint32_t sym = symbol_slow(w, pair[w.peek12()], ct);
-        const uint32_t sb = sm[v];
-        out[v] = (uint16_t)(((sb & 0x80u) << 8) | (sym << 7) | (sb & 0x7Fu));
+    }
+    for (uint64_t v = vf; v < v1; ++v) {  // ragged tail / unaligned run: one symbol at a time
+      w.refill();
+      const uint32_t sym = symbol_slow(w, pair[w.peek12()], ct);
+      const uint32_t sb = sm[v];
+      out[v] = (uint16_t)(((sb & 0x80u) << 8) | (sym << 7) | (sb & 0x7Fu));
+    }
+  }
+}
+
+
+// Decoder v7: tile-staged.  A CTA takes a tile of up to 256 consecutive chunks of one tensor
+// (64K values at chunk 256).  (A) One thread bulk-copies the tile's bitstream -- one
+// contiguous byte range between two chunk-index entries -- into shared memory with the TMA
+// engine.  (B) Thread t decodes chunk t from shared memory only (stream words and the pair
+// table are LDS; no global load sits on the decode chain) into exponent bytes, stored in a
+// swizzled per-chunk row.  (C) The CTA merges exponents with the sign/mantissa plane in one
+// coalesced sweep: consecutive lanes read consecutive 16-byte pieces of the plane and write
+// consecutive 32-byte pieces of bf16 output.  v2 issued per-lane loads and stores 256 B apart
+// (one chunk per lane) and stalled on them (ncu: long scoreboard on the stream word first).
+// Tiles whose stream exceeds the staging buffer, and each tensor's last tile (its stream end
+// is not known to the kernel), decode chunk by chunk from global memory as v2 does.
+constexpr int kTile7 = 256;  // chunks per tile = threads per CTA
+__host__ __device__ constexpr int bits7_cap(int chunk) { return chunk >= 256 ? 28 * 1024 : 16 * 1024; }
+__host__ __device__ constexpr int smem7_bytes(int chunk) {
+  return bits7_cap(chunk) + kTile7 * chunk + (1 << kPairBits) * 4 + 64;
+}
+
+__device__ __forceinline__ uint32_t exp_pair_bytes(uint32_t ea, uint32_t eb) {
+  // pair-table words (e0 << 7 | e1 << 23 | meta) -> [e0a e1a e0b e1b]
+  return __byte_perm(ea >> 7, eb >> 7, 0x6420);
+}
+
+// Window over a stream staged in shared memory (word addresses, one word in flight).
+struct LWindow {
+  uint64_t win;
+  int p;
+  uint32_t nxt;
+  uint32_t addr;  // smem address of the next word to load
+  __device__ __forceinline__ void init(uint32_t word_addr, uint32_t bit_in_word) {
+    uint32_t a, b;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a) : "r"(word_addr));
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(b) : "r"(word_addr + 4));
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nxt) : "r"(word_addr + 8));
+    win = ((uint64_t)bswap32(a) << 32) | bswap32(b);
+    addr = word_addr + 12;
+    p = (int)bit_in_word;
+  }
+  __device__ __forceinline__ void refill() {
+    if (p >= 32) {
+      win = (win << 32) | bswap32(nxt);
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nxt) : "r"(addr));
+      addr += 4;
+      p -= 32;
+    }
+  }
+  __device__ __forceinline__ uint32_t peek12() const { return (uint32_t)((win << p) >> (64 - kPairBits)); }
+};
+
+__global__ void __launch_bounds__(kTile7) k_exp_decode7(const __grid_constant__ DecodeParams p) {
+  __shared__ uint32_t first_code[kCodecMaxLen + 1];
+  __shared__ int count[kCodecMaxLen + 1], first_rank[kCodecMaxLen + 1];
+  __shared__ uint8_t sorted_sym[kCodecSymbols];
+  __shared__ __align__(8) uint64_t bar;
+  extern __shared__ __align__(16) uint8_t sm7[];
+  const int chunk = p.chunk;
+  const int cap = bits7_cap(chunk);
+  uint8_t* tbits = sm7;                          // staged stream bytes of the tile
+  uint8_t* tex = sm7 + cap;                      // exponent bytes: [chunk t][chunk] swizzled by 16 B
+  uint32_t* pair = reinterpret_cast<uint32_t*>(tex + kTile7 * chunk);
+  const int tid = threadIdx.x;
+  {
+    const DecTables* t = p.tabs;
+    const uint4* src = reinterpret_cast<const uint4*>(t->pair);
+    uint4* dst = reinterpret_cast<uint4*>(pair);
+    for (int i = tid; i < (1 << kPairBits) / 4; i += blockDim.x) dst[i] = src[i];
+    if (tid <= kCodecMaxLen) {
+      first_code[tid] = t->first_code[tid];
+      count[tid] = t->count[tid];
+      first_rank[tid] = t->first_rank[tid];
+    }
+    if (tid < kCodecSymbols) sorted_sym[tid] = t->sorted_sym[tid];
+    if (tid == 0) {
+      mbar_init(&bar, 1);
+      fence_mbar_init();
+    }
+  }
+  const CanonTabs ct{count, first_code, first_rank, sorted_sym, p.tabs->maxlen};
+  __syncthreads();
+
+  const uint64_t n = p.n;
+  const uint64_t cpt = (n + chunk - 1) / chunk;
+  const uint64_t tpt = (cpt + kTile7 - 1) / kTile7;  // tiles per tensor
+  const uint64_t n_tiles = tpt * (uint64_t)p.ntensors;
+  const int upc = chunk / 16;  // 16-byte units per chunk row of tex
+  uint32_t phase = 0;
+  for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int ti = (int)(tile / tpt);
+    const uint64_t j = tile - (uint64_t)ti * tpt;
+    const DecodeTensor& d = p.t[ti];
+    const uint64_t c0 = j * kTile7, c1 = (c0 + kTile7 < cpt) ? c0 + kTile7 : cpt;
+    const uint64_t v0 = c0 * chunk, v1 = (c1 * chunk < n) ? c1 * chunk : n;
+    // staged tiles: a full tile with a known end (not the tensor's last), aligned, fitting the buffer
+    const uint32_t b0 = d.index[c0] - d.bit_base;
+    const uint32_t b1 = (c1 < cpt) ? d.index[c1] - d.bit_base : 0u;
+    const uint8_t* g0 = reinterpret_cast<const uint8_t*>(d.bits) + ((b0 >> 3) & ~15u);
+    // through the tile's last bit + 16 bytes (the window reads up to 96 bits past its position)
+    const uint32_t bytes = (c1 < cpt) ? ((((b1 + 7) >> 3) + 16 + 15) & ~15u) - ((b0 >> 3) & ~15u) : 0u;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(d.out + v0) & 31) | (reinterpret_cast<uintptr_t>(d.sm + v0) & 15) |
+                          (reinterpret_cast<uintptr_t>(d.bits) & 15)) == 0;
+    const bool staged = c1 < cpt && c1 - c0 == kTile7 && bytes <= (uint32_t)cap && aligned;
+    if (!staged) {
+      // chunk by chunk from global memory (k_exp_decode2's window)
+      const uint64_t c = c0 + tid;
+      if (c < c1) {
+        Window w;
+        w.init(d.bits, d.index[c] - d.bit_base);
+        const uint64_t a = c * chunk, b = (a + chunk < n) ? a + chunk : n;
+        decode_chunk_v2(w, d.sm, d.out, a, b, pair, ct);
+      }
+      continue;
+    }
+    // (A) stream bytes of the tile -> tbits
+    if (tid == 0) {
+      mbar_arrive_expect_tx(&bar, bytes);
+      bulk_load_1d(tbits, g0, bytes, &bar);
+    }
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    // (B) chunk tid: exponent bytes into its tex row
+    {
+      const uint32_t bit = d.index[c0 + tid] - d.bit_base - ((b0 >> 3) & ~15u) * 8;
+      LWindow w;
+      w.init(smem_u32(tbits) + (bit >> 5) * 4, bit & 31);
+      const uint32_t row = smem_u32(tex + tid * chunk);
+      const uint32_t swz = (uint32_t)(tid & (upc - 1));
+#pragma unroll 1
+      for (int u = 0; u < upc; ++u) {
+        uint32_t e[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if ((q & 1) == 0) w.refill();
+          uint32_t x = pair[w.peek12()];
+          const int len = (int)(x & 15u);
+          if (__builtin_expect(len == 0, 0)) x = pair_slow(w, pair, ct);
+          else w.p += len;
+          e[q] = x;
+        }
+        const uint32_t o0 = exp_pair_bytes(e[0], e[1]), o1 = exp_pair_bytes(e[2], e[3]);
+        const uint32_t o2 = exp_pair_bytes(e[4], e[5]), o3 = exp_pair_bytes(e[6], e[7]);
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + ((((uint32_t)u) ^ swz) << 4)), "r"(o0),
+                     "r"(o1), "r"(o2), "r"(o3)
+                     : "memory");
       }
     }
+    __syncthreads();
+    // (C) coalesced merge with the sign/mantissa plane
+    const uint64_t units = (v1 - v0) / 16;
+    for (uint64_t i = tid; i < units; i += kTile7) {
+      const uint32_t cc = (uint32_t)(i / upc), uu = (uint32_t)(i % upc);
+      uint4 ex;
+      asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(ex.x), "=r"(ex.y), "=r"(ex.z), "=r"(ex.w)
+                   : "r"(smem_u32(tex + cc * chunk) + ((uu ^ (cc & (upc - 1))) << 4)));
+      const uint4 smv = __ldg(reinterpret_cast<const uint4*>(d.sm + v0) + i);
+      uint16_t* o = d.out + v0 + 16 * i;
+      asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(o),
+                   "r"(pack_words(smv.x, ex.x, 0x5140u)), "r"(pack_words(smv.x, ex.x, 0x7362u)),
+                   "r"(pack_words(smv.y, ex.y, 0x5140u)), "r"(pack_words(smv.y, ex.y, 0x7362u)),
+                   "r"(pack_words(smv.z, ex.z, 0x5140u)), "r"(pack_words(smv.z, ex.z, 0x7362u)),
+                   "r"(pack_words(smv.w, ex.w, 0x5140u)), "r"(pack_words(smv.w, ex.w, 0x7362u))
+                   : "memory");
+    }
+    __syncthreads();  // tex and tbits are reused by the next tile
   }
 }
 
@@ -595,7 +850,9 @@ void launch_exp_decode_multi(const DecodeTensor* tensors, int ntensors, uint64_t
     return std::max(1, sms * std::max(1, per_sm));
   }();
   // XPGB_DECODER=1: the round-1 multi-symbol decoder; 3: the pair decoder fed from a 16-byte
-  // stream queue (QWindow); 4 / 5: 2 / 3 stream words in flight; default 2 (A/B only)
+  // stream queue (QWindow); 4 / 5: 2 / 3 stream words in flight; 6: contiguous chunk runs per
+  // thread fed through a shared-memory ring (k_exp_decode6); 7: tile-staged (k_exp_decode7);
+  // default 2 (A/B only)
   static const int ver = [] {
     const char* e = getenv("XPGB_DECODER");
     return e ? atoi(e) : 2;
@@ -612,7 +869,32 @@ void launch_exp_decode_multi(const DecodeTensor* tensors, int ntensors, uint64_t
       return std::max(1, sms * std::max(1, per_sm));
     }();
     const uint64_t blocks = std::min<uint64_t>((n_chunks + 255) / 256, (uint64_t)resident2);
-    if (ver == 3) k_exp_decode2<QWindow><<<(unsigned)blocks, 256, 0, s>>>(p);
+    if (ver == 7 && chunk % 16 == 0 && chunk <= 256 && (chunk & (chunk - 1)) == 0) {
+      static int resident7[2] = {0, 0};  // chunk 256 / below
+      const int ci = chunk >= 256 ? 0 : 1;
+      if (!resident7[ci]) {
+        int dev = 0, sms = 148, per_sm = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(k_exp_decode7, cudaFuncAttributeMaxDynamicSharedMemorySize, smem7_bytes(256));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_exp_decode7, kTile7, smem7_bytes(chunk));
+        resident7[ci] = std::max(1, sms * std::max(1, per_sm));
+      }
+      const uint64_t tiles = ((n + (uint64_t)chunk * kTile7 - 1) / ((uint64_t)chunk * kTile7)) * ntensors;
+      const uint64_t b7 = std::min<uint64_t>(tiles, (uint64_t)resident7[ci]);
+      k_exp_decode7<<<(unsigned)b7, kTile7, smem7_bytes(chunk), s>>>(p);
+    } else if (ver == 6) {
+      static const int resident6 = [] {
+        int dev = 0, sms = 148, per_sm = 4;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(k_exp_decode6, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * kRun6Bytes);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_exp_decode6, 256, 256 * kRun6Bytes);
+        return std::max(1, sms * std::max(1, per_sm));
+      }();
+      const uint64_t b6 = std::min<uint64_t>((n_chunks + 255) / 256, (uint64_t)resident6);
+      k_exp_decode6<<<(unsigned)b6, 256, 256 * kRun6Bytes, s>>>(p);
+    } else if (ver == 3) k_exp_decode2<QWindow><<<(unsigned)blocks, 256, 0, s>>>(p);
     else if (ver == 4) k_exp_decode2<WindowD<2>><<<(unsigned)blocks, 256, 0, s>>>(p);
     else if (ver == 5) k_exp_decode2<WindowD<3>><<<(unsigned)blocks, 256, 0, s>>>(p);
     else k_exp_decode2<Window><<<(unsigned)blocks, 256, 0, s>>>(p);

@@ -129,6 +129,75 @@ struct WindowD {
   __device__ __forceinline__ uint32_t peek12() const { return (uint32_t)((win << p) >> (64 - kPairBits)); }
 };
 
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+// Stream window of one decoder thread, fed through shared memory.  In the decode-into-GEMM
+// kernel a decoder thread reads its own tensor row's stream -- 256 threads, 256 streams far
+// apart -- and with ~200 KB of the SM in shared memory the L1 cannot hold a line per stream: word-by-word global loads missed to
+// L2 on nearly every refill (measured: the fused GEMM ran ~8x slower than the standalone
+// decoder).  Here the stream is copied ahead with cp.async (LDGSTS, bypassing L1) into a
+// per-thread ring of two 64-byte blocks; the window pops words from it with LDS.  A block is
+// refetched as soon as the window leaves it, so the copy runs ~64 bytes (~200 values) ahead.
+// The ring's 16-byte chunks are XOR-swizzled by the thread index to spread banks.
+struct SWindow {
+  uint64_t win;
+  int p;
+  uint32_t nxt;     // next stream word (raw)
+  uint32_t wi;      // ring word (0..31) that follows nxt
+  uint32_t base;    // smem address of this thread's ring
+  uint32_t sw;      // chunk swizzle (thread & 7)
+  const uint8_t* g; // global address of the next block to fetch
+  __device__ __forceinline__ uint32_t word(uint32_t w) const {
+    return lds32(base + ((((w >> 2) ^ sw)) << 4) + ((w & 3) << 2));
+  }
+  __device__ __forceinline__ void fetch(uint32_t slot) {  // 64 bytes into ring words [16 slot, 16 slot + 16)
+#pragma unroll
+    for (uint32_t i = 0; i < 4; ++i) cp_async16(base + (((slot * 4 + i) ^ sw) << 4), g + 16 * i);
+    cp_async_commit();
+    g += 64;
+  }
+  __device__ __forceinline__ void init(const uint32_t* bits, uint32_t bitpos, uint32_t ring, uint32_t swz) {
+    base = ring;
+    sw = swz;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(bits + (bitpos >> 5));
+    g = reinterpret_cast<const uint8_t*>(a & ~uintptr_t(15));
+    const uint32_t w0 = (uint32_t)((a >> 2) & 3);
+    fetch(0);
+    fetch(1);
+    cp_async_wait1();
+    win = ((uint64_t)bswap32(word(w0)) << 32) | bswap32(word(w0 + 1));
+    nxt = word(w0 + 2);
+    wi = w0 + 3;
+    p = (int)(bitpos & 31);
+  }
+  __device__ __forceinline__ uint32_t pop() {
+    const uint32_t r = nxt;
+    if ((wi & 15) == 0) {  // entering the other block: the one just left is free
+      fetch(((wi >> 4) ^ 1) & 1);
+      cp_async_wait1();
+    }
+    nxt = word(wi);
+    wi = (wi + 1) & 31;
+    return r;
+  }
+  __device__ __forceinline__ void refill() {
+    if (p >= 32) {
+      win = (win << 32) | bswap32(pop());
+      p -= 32;
+    }
+  }
+  __device__ __forceinline__ uint32_t peek12() const { return (uint32_t)((win << p) >> (64 - kPairBits)); }
+};
+
 struct CanonTabs {
   const int* count;
   const uint32_t* first_code;

@@ -43,6 +43,8 @@ namespace {
 constexpr int kDecWarps = 8;
 constexpr int kDecThreads = 192 + 32 * kDecWarps;  // 448
 constexpr int kDecRows = 256;                      // weight rows per unit (two 128-row A tiles)
+constexpr int kDecThreads_dec = 32 * kDecWarps;    // decoder threads
+constexpr int kRingBytes = 128;                    // per decoder thread: two 64-byte stream blocks
 
 template <int BN, int STAGES>
 struct DecCfg {
@@ -51,13 +53,16 @@ struct DecCfg {
   static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;   // two A tiles + hi/lo activations
   static constexpr int TMEM_COLS = 512;                     // 2 accumulator stages x 256 columns
   static constexpr int TAB_BYTES = (3 * kMaxExperts + 8) * 4;
-  static constexpr int DEC_TAB = (1 << kPairBits) * 4 + 3 * (kCodecMaxLen + 1) * 4 + kCodecSymbols;
-  static constexpr int SMEM = STAGES * STAGE + 1024 + 256 + TAB_BYTES + DEC_TAB;
+  static constexpr int DEC_TAB = ((1 << kPairBits) * 4 + 3 * (kCodecMaxLen + 1) * 4 + kCodecSymbols + 15) & ~15;
+  static constexpr int RING = kDecThreads_dec * kRingBytes;  // per-decoder-thread bitstream rings
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256 + TAB_BYTES + DEC_TAB + RING;
   static_assert(SMEM <= 227 * 1024, "decode-GEMM stages exceed 227 KB");
 };
 
+// Offset arithmetic on the shared pointer itself: a round trip through uintptr_t loses the
+// address space, and every table read through the result becomes a generic LD instead of LDS.
 __device__ __forceinline__ uint8_t* align_1k(uint8_t* p) {
-  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+  return p + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(p)) & 1023u)) & 1023u);
 }
 
 __device__ __forceinline__ float silu_d(float g) { return g * (1.0f / (1.0f + __expf(-g))); }
@@ -97,7 +102,7 @@ __device__ __forceinline__ DUnit dec_unit(int u, const int* s_up, const int* s_o
 
 }  // namespace
 
-template <bool GU, int BN, int STAGES, class WIN>
+template <bool GU, int BN, int STAGES>
 __global__ void __maxnreg__(128)  // 448 threads x 128 registers (144 was refused at launch)
     k_moe_gemm_dec(const __grid_constant__ CUtensorMap map_b, GemmParams p, const DecTables* __restrict__ tabs,
                    int chunk) {
@@ -117,6 +122,7 @@ __global__ void __maxnreg__(128)  // 448 threads x 128 registers (144 was refuse
   int* s_count = reinterpret_cast<int*>(s_first + kCodecMaxLen + 1);
   int* s_rank = s_count + kCodecMaxLen + 1;
   uint8_t* s_sym = reinterpret_cast<uint8_t*>(s_rank + kCodecMaxLen + 1);
+  uint8_t* s_ring = smem + STAGES * C::STAGE + 256 + C::TAB_BYTES + C::DEC_TAB;  // 16-byte aligned
 
   const int E = p.E;
   const int MT = GU ? (p.F + kBM - 1) / kBM : (p.H + kDecRows - 1) / kDecRows;
@@ -324,42 +330,47 @@ __global__ void __maxnreg__(128)  // 448 threads x 128 registers (144 was refuse
       const int wrow = GU ? (a ? p.F : 0) + un.m0 + lr : 2 * un.m0 + d;
       const bool valid = GU ? (un.m0 + lr < p.F) : (2 * un.m0 + d < p.H);
       const uint64_t v0 = (uint64_t)wrow * K + (uint64_t)kb0 * kBK;
-      WIN w;
+      SWindow w;
+      // sign/mantissa bytes: 16 per group, kept two groups ahead of use (s0 current, s1, s2);
+      // the smem ring feeds the bitstream, these loads are the decoder's only global reads
       const uint8_t* smp = R.sm + v0;
-      uint4 nsm[4];
+      const uint8_t* smend = R.sm + (uint64_t)wrow * K + (uint64_t)kb1 * kBK;
+      uint4 s0 = make_uint4(0, 0, 0, 0), s1 = s0, s2 = s0;
       if (valid) {
-        w.init(R.bits, R.index[v0 / chunk] - R.bit_base);
-#pragma unroll
-        for (int g = 0; g < 4; ++g) nsm[g] = __ldg(reinterpret_cast<const uint4*>(smp) + g);
+        w.init(R.bits, R.index[v0 / chunk] - R.bit_base, smem_u32(s_ring + d * kRingBytes), (uint32_t)(d & 7));
+        s0 = __ldg(reinterpret_cast<const uint4*>(smp));
+        s1 = __ldg(reinterpret_cast<const uint4*>(smp) + 1);
+        s2 = __ldg(reinterpret_cast<const uint4*>(smp) + 2);
+        smp += 48;
       }
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         if (valid) {
-          uint4 csm[4];
-#pragma unroll
-          for (int g = 0; g < 4; ++g) csm[g] = nsm[g];
-          smp += kBK;
-          if (kb + 1 < kb1) {
-#pragma unroll
-            for (int g = 0; g < 4; ++g) nsm[g] = __ldg(reinterpret_cast<const uint4*>(smp) + g);
-          }
           const uint32_t row = smem_u32(smem + stage * C::STAGE + a * C::A_BYTES + lr * 128);
+          // 8 quads of 8 values (one 16-byte swizzled store each); the quad loop stays rolled so
+          // the hot code fits the instruction cache (fully unrolled, 32 pair sites with their
+          // slow paths made a 140 KB loop: ncu put 44% of the stall cycles on instruction fetch)
+#pragma unroll 1
+          for (uint32_t q = 0; q < 8; ++q) {
+            const uint32_t sa = (q & 1) ? s0.z : s0.x, sb = (q & 1) ? s0.w : s0.y;
+            uint32_t o[4];
 #pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            const uint32_t smw[4] = {csm[g].x, csm[g].y, csm[g].z, csm[g].w};
-            uint32_t o[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < 4; ++j) {
               if ((j & 1) == 0) w.refill();
               uint32_t e = s_pair[w.peek12()];
               const int len = (int)(e & 15u);
               if (__builtin_expect(len == 0, 0)) e = pair_slow(w, s_pair, ct);
               else w.p += len;
-              const uint32_t dup = __byte_perm(smw[j >> 1], 0, (j & 1) ? 0x3322u : 0x1100u);
+              const uint32_t dup = __byte_perm(j < 2 ? sa : sb, 0, (j & 1) ? 0x3322u : 0x1100u);
               o[j] = (dup & 0x807F807Fu) | (e & 0x7F807F80u);
             }
-            st_smem_v4(row + ((((uint32_t)(2 * g)) ^ sw) << 4), o[0], o[1], o[2], o[3]);
-            st_smem_v4(row + ((((uint32_t)(2 * g + 1)) ^ sw) << 4), o[4], o[5], o[6], o[7]);
+            st_smem_v4(row + ((q ^ sw) << 4), o[0], o[1], o[2], o[3]);
+            if (q & 1) {
+              s0 = s1;
+              s1 = s2;
+              if (smp < smend) s2 = __ldg(reinterpret_cast<const uint4*>(smp));
+              smp += 16;
+            }
           }
           fence_async_smem();
         }
@@ -380,14 +391,11 @@ __global__ void __maxnreg__(128)  // 448 threads x 128 registers (144 was refuse
 using DecKernel = void (*)(const CUtensorMap, GemmParams, const DecTables*, int);
 
 // stage counts: the A tiles are produced on-chip, so a few stages cover the decoder/MMA overlap
-#define XPGB_DEC_TILES(X) X(32, 4) X(48, 4) X(64, 3) X(80, 3) X(96, 3) X(128, 2)
+#define XPGB_DEC_TILES(X) X(32, 4) X(48, 3) X(64, 3) X(80, 3) X(96, 2) X(128, 2)
 
 template <bool GU, int BN, int ST>
 static void set_dec_attr() {
-  cudaFuncSetAttribute(k_moe_gemm_dec<GU, BN, ST, QWindow>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       DecCfg<BN, ST>::SMEM);
-  cudaFuncSetAttribute(k_moe_gemm_dec<GU, BN, ST, Window>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       DecCfg<BN, ST>::SMEM);
+  cudaFuncSetAttribute(k_moe_gemm_dec<GU, BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, DecCfg<BN, ST>::SMEM);
 }
 
 void set_gemm_dec_attrs() {
@@ -405,20 +413,17 @@ void launch_gemm_dec(bool gate_up, const CUtensorMap& map_b, const GemmParams& p
                      int bn, int grid, cudaStream_t s) {
   const DecTables* tabs = codec_device_tables(table, s);
   if (!tabs) return;
-  // XPGB_FUSED_WIN=1: the one-word-ahead stream window instead of the 16-byte queue (A/B)
-  static const bool word = getenv("XPGB_FUSED_WIN") && atoi(getenv("XPGB_FUSED_WIN")) == 1;
   DecKernel kern = nullptr;
   int smem = 0;
-#define XPGB_PICK_DEC(BN, ST)                                                                          \
-  if (bn == BN) {                                                                                      \
-    kern = word ? (gate_up ? k_moe_gemm_dec<true, BN, ST, Window> : k_moe_gemm_dec<false, BN, ST, Window>) \
-                : (gate_up ? k_moe_gemm_dec<true, BN, ST, QWindow> : k_moe_gemm_dec<false, BN, ST, QWindow>); \
-    smem = DecCfg<BN, ST>::SMEM;                                                                       \
+#define XPGB_PICK_DEC(BN, ST)                                                                \
+  if (bn == BN) {                                                                            \
+    kern = gate_up ? k_moe_gemm_dec<true, BN, ST> : k_moe_gemm_dec<false, BN, ST>;           \
+    smem = DecCfg<BN, ST>::SMEM;                                                             \
   }
   XPGB_DEC_TILES(XPGB_PICK_DEC)
 #undef XPGB_PICK_DEC
   if (!kern) {
-    kern = gate_up ? k_moe_gemm_dec<true, 128, 2, QWindow> : k_moe_gemm_dec<false, 128, 2, QWindow>;
+    kern = gate_up ? k_moe_gemm_dec<true, 128, 2> : k_moe_gemm_dec<false, 128, 2>;
     smem = DecCfg<128, 2>::SMEM;
   }
   kern<<<grid, kDecThreads, smem, s>>>(map_b, p, tabs, chunk);

@@ -474,8 +474,10 @@ void launch_reduce_rows(const float* part, const long long* fault, float* out, i
 // offsets (no global unit array), and the same prologue performs read_page's
 // residency check (paging.py:228-237) on every routed expert's page.
 
+// Offset arithmetic on the shared pointer itself: a round trip through uintptr_t loses the
+// address space, and every table read through the result becomes a generic LD instead of LDS.
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
-  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+  return p + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(p)) & 1023u)) & 1023u);
 }
 
 __device__ __forceinline__ float silu_f(float g) { return g * (1.0f / (1.0f + __expf(-g))); }

@@ -260,7 +260,7 @@ class LiveResidencyController:
 def calibrate_bandwidths(runner, acts, reps: int = 3) -> tuple:
     """(b_dev, b_host) in raw-equivalent B/s, measured on this GPU.
 
-    b_host: one host-only decode iteration, raw layer bytes over the measured page-in spans.
+    b_host: a host-only paged stack (link-bound), raw model bytes per second of its run.
     b_dev: the on-GPU exponent decoder expanding a device-resident record (the device tier's
     page-in), best of ``reps``."""
     import ctypes as C
@@ -273,8 +273,12 @@ def calibrate_bandwidths(runner, acts, reps: int = 3) -> tuple:
     spec = runner.spec
     saved = list(runner.device_experts) if runner.device_experts is not None else None
     runner.set_device_experts([0] * spec.num_layers)
-    _, tau_load = measured_taus(runner.run(1, acts=acts))
-    b_host = spec.total_bytes / tau_load if tau_load > 0 else float("inf")
+    # host-only stack: link-bound, so the raw bytes streamed per second of wall time are the
+    # link's raw-equivalent rate (the per-layer load spans of one cold iteration overstate the
+    # link time: they include the first layers' start-up and staging waits)
+    runner.run(1, acts=acts)
+    rep = runner.run(3, acts=acts)
+    b_host = 3 * spec.total_bytes / rep.elapsed_seconds if rep.elapsed_seconds > 0 else float("inf")
     cm = runner.hierarchy.compressed
     if not isinstance(cm, CompressedModel):
         cm = CompressedModel.from_container(runner.hierarchy.container)

@@ -39,7 +39,8 @@ def main():
         c = S.calibrated_config(spec, cal, batch_size=int(p.get("T", cal.get("tokens", 256))))
         dev, pin = float(p.get("device_tier_per_layer", 0)), float(p.get("pinned_per_layer", 0))
         ref = S.predict_tiered(c, dev, pin)
-        ours = S.predict_sm_shared(c, dev, pin, b_dec=args.b_dec * 1e9 if args.b_dec else None,
+        b_dec = args.b_dec * 1e9 if args.b_dec else cal.get("b_dec_pipeline")
+        ours = S.predict_sm_shared(c, dev, pin, b_dec=b_dec,
                                    b_fused=args.b_fused * 1e9 if args.b_fused else None)
         meas = float(p["tok_s"])
         row = {"budget": p.get("budget"), "device_per_layer": dev, "pinned_per_layer": pin, "measured_tok_s": meas,
@@ -50,7 +51,7 @@ def main():
         worst["sm_shared_model"] = max(worst["sm_shared_model"], abs(row["sm_shared_model_err"]))
         print(json.dumps(row))
     print(json.dumps({"summary": "max |relative error| over the sweep", **worst,
-                      "inputs": {k: cal[k] for k in ("b_host", "b_dev", "tau_comp_theory") if k in cal}}))
+                      "inputs": {k: cal[k] for k in ("b_host", "b_dev", "b_dec_pipeline", "tau_comp_theory") if k in cal}}))
 
 
 if __name__ == "__main__":
