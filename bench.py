@@ -436,6 +436,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="mixtral", choices=sorted(CONFIGS))
     ap.add_argument("--tokens", type=int, default=None)
+    ap.add_argument("--device-format", default="auto", choices=["auto", "huffman", "fx4"],
+                    help="device-tier records: exponent-Huffman decoded into the ring, or FX4 read in place by "
+                         "the decode-into-GEMM kernel (auto: the planner's step model picks)")
     ap.add_argument("--budget", type=float, default=0.25,
                     help="expert-HBM budget as a fraction of the expert bytes (ring + codec buffers + shared)")
     ap.add_argument("--tiering", default="device", choices=["device", "ring"],
@@ -588,18 +591,21 @@ def main():
         cap = args.budget * expert_bytes * 0.998 - shared_b - overhead  # margin: record sizes vary per expert
         m_dev = 0
         pinned_per_layer = 0
+        dev_format, dev_fused = "huffman", False
         if args.tiering == "device" and args.host_codec:
-            from paper_2604_02715_b200.budget import plan_residency
+            from paper_2604_02715_b200.budget import fx4_expert_bytes, plan_tiers
 
             Lc, Nl = cspec.experts_per_layer, cspec.num_layers
             ceb = runner.device_tier_bytes(Lc) / (Nl * Lc) * 1.002  # compressed expert (+ margin)
-            plan = plan_residency(Nl, Lc, eb, ceb, cap + shared_b + overhead, shared_bytes=shared_b,
-                                  overhead_bytes=overhead)
+            plan = plan_tiers(Nl, Lc, eb, ceb, cap + shared_b + overhead, shared_bytes=shared_b,
+                              overhead_bytes=overhead, device_format=args.device_format,
+                              fx4_ceb=fx4_expert_bytes(cspec.hidden_dim, cspec.intermediate_dim) * 1.002)
             if plan.device_experts or plan.pinned_experts:
                 runner.apply_plan(plan)
                 ring_blocks = min(plan.ring, ring_blocks) if plan.ring else ring_blocks
                 m_dev = plan.device_experts / Nl
                 pinned_per_layer = plan.pinned_experts / Nl
+                dev_format, dev_fused = plan.device_format, plan.fused
         if not (m_dev or pinned_per_layer):
             ring_fit = int((cap + 1) // eb) & ~1
             if 2 <= ring_fit < ring_blocks:
@@ -733,6 +739,8 @@ def main():
                    "ring_blocks_per_kind": int(ring_blocks) if not use_ep else None,
                    "device_tier_experts_per_layer": round(m_dev, 3),
                    "pinned_experts_per_layer": round(pinned_per_layer, 3),
+                   "device_tier_format": dev_format if not use_ep else "huffman",
+                   "decode_into_gemm": bool(dev_fused) if not use_ep else False,
                    "placement": ("2-layer ring" if use_ep or ring_blocks >= 2 * cspec.experts_per_layer else
                                  f"sub-layer ring of {ring_blocks} expert blocks per kind ({ring_depth} window(s) "
                                  f"in flight of {max(1, ring_blocks // ring_depth)} expert(s))") + (
@@ -741,7 +749,9 @@ def main():
                        f"the rest host" if m_dev else
                        ", host-only (alpha=0)") + (
                        ", exponent-Huffman records over PCIe decoded on-GPU into the ring (lossless)"
-                       if args.host_codec else ""),
+                       if args.host_codec else "") + (
+                       "; device tier in FX4 records read in place by the decode-into-GEMM kernel"
+                       if (not use_ep and dev_fused) else ""),
                    "l2": ("inputs larger than L2 (126 MB): each step reads %.1f GB of expert weights -- %.2f GB of "
                           "records over PCIe, %.2f GB of bf16 decoded on-GPU from HBM records, the rest pinned/ring"
                           % (cspec.total_bytes / 1e9, rep.h2d_bytes / args.steps / 1e9,

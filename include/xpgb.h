@@ -221,6 +221,18 @@ int xpgb_codec_index(const void* bits, uint64_t bits_len, uint64_t n, const uint
 /* decompress() on the GPU: packed record in device memory -> n bf16 words at out_dev. */
 int xpgb_codec_decode(const void* record_dev, uint64_t n, uint64_t bits_len, int32_t chunk,
                       const uint8_t* lengths256, void* out_dev, void* stream);
+/* FX4 records (B200 addition, fx4.cuh): a fixed-width exponent format for the compressed device
+ * tier -- 4-bit offsets from a per-tensor base, escapes for exponents outside the 15-wide
+ * window -- that the decode-into-GEMM kernel expands without a serial decode chain; lossless
+ * like the exponent-Huffman record (codec.py:235-272), 12.1 bits per value instead of ~10.7.
+ * n % 256 == 0.  measure: histogram -> base and escape count -> record bytes (synchronises
+ * `stream`); encode: raw bf16 (device) -> record (device, record_bytes); decode: record ->
+ * n bf16 words.  scratch: xpgb_fx4_scratch_bytes(n) bytes of device memory. */
+uint64_t xpgb_fx4_scratch_bytes(uint64_t n);
+int xpgb_fx4_measure(const void* raw_dev, uint64_t n, void* scratch_dev, int32_t* base, uint64_t* n_escapes,
+                     uint64_t* record_bytes, void* stream);
+int xpgb_fx4_encode(const void* raw_dev, uint64_t n, int32_t base, void* scratch_dev, void* record_dev, void* stream);
+int xpgb_fx4_decode(const void* record_dev, uint64_t n, int32_t base, void* out_dev, void* stream);
 /* Attach a packed model (records in container order, tensors of this context's shard) to the
  * context.  Device-tier tensors are then held compressed in HBM and decoded into ring blocks
  * (the reference's compressed device tier, storage.py:235-238); with host_compressed = 1 the
@@ -259,6 +271,13 @@ int xpgb_set_ring_depth(xpgb_ctx* ctx, int32_t depth);
  * (default) keeps every expert in the ring, as callers with their own compute need
  * (xpgb_experts_forward_range).  No session may be active. */
 int xpgb_set_fused_decode(xpgb_ctx* ctx, int32_t mode);
+/* Record format of the compressed device tier: 0 = exponent-Huffman (default; the host pool's
+ * records staged as they are, the reference's device tier, storage.py:143-168), 1 = FX4
+ * (fx4.cuh; encoded on the GPU from the raw host pool when staged).  FX4 costs ~13% more HBM per
+ * expert and decodes without a serial chain, so the decode-into-GEMM kernel runs near the
+ * bandwidth of its compressed bytes.  Lossless either way.  Re-stages the device tier; no
+ * session may be active. */
+int xpgb_set_device_format(xpgb_ctx* ctx, int32_t fmt);
 /* Race hardening (debug; no reference counterpart -- the reference's sabotage control,
  * pipeline.py:369-370, covers RAW only).  poison != 0: every ring block a window maps is filled
  * with 0xFF bytes (bf16 NaN) on the copy stream before its load, so a GEMM that reads a block

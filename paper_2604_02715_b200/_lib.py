@@ -121,6 +121,7 @@ _SIGS = {
     "xpgb_set_ring_experts": [_P, _I],
     "xpgb_set_ring_depth": [_P, _I],
     "xpgb_set_fused_decode": [_P, _I],
+    "xpgb_set_device_format": [_P, _I],
     "xpgb_set_hazard_checks": [_P, _I, _I, _I],
     "xpgb_set_stage_buffers": [_P, _I],
     "xpgb_decode_stats": [_P, _P, _P, _P],
@@ -150,13 +151,17 @@ _SIGS = {
     "xpgb_codec_record_bytes": [_U64, _U64, _I],
     "xpgb_codec_index": [_P, _U64, _U64, C.POINTER(C.c_uint8), _I, C.POINTER(C.c_uint32), C.POINTER(_U64)],
     "xpgb_codec_decode": [_P, _U64, _U64, _I, C.POINTER(C.c_uint8), _P, _P],
+    "xpgb_fx4_scratch_bytes": [_U64],
+    "xpgb_fx4_measure": [_P, _U64, _P, C.POINTER(C.c_int32), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), _P],
+    "xpgb_fx4_encode": [_P, _U64, _I, _P, _P, _P],
+    "xpgb_fx4_decode": [_P, _U64, _I, _P, _P],
     "xpgb_set_codec": [_P, _P, _U64, C.POINTER(_U64), C.POINTER(_U64), C.POINTER(C.c_uint8), _I, _I],
     "xpgb_set_pinned": [_P, C.POINTER(C.c_uint8)],
     "xpgb_hbm_bytes": [_P, C.POINTER(_U64), C.POINTER(_U64), C.POINTER(_U64)],
     "xpgb_profile_layer": [_P, _I, _P, _P, _I, _I, _U64, _I, C.POINTER(KernelTimes)],
 }
 _RESTYPES = {"xpgb_last_error": C.c_char_p, "xpgb_kernel_launches": C.c_int64, "xpgb_codec_record_bytes": C.c_uint64,
-             "xpgb_ep_plan_scratch_words": C.c_int64}
+             "xpgb_ep_plan_scratch_words": C.c_int64, "xpgb_fx4_scratch_bytes": C.c_uint64}
 
 # every symbol declared in include/xpgb.h (tests check the export table against this)
 DECLARED = tuple(_SIGS)

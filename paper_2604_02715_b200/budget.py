@@ -92,7 +92,8 @@ def _balanced(total: int, N: int):
 def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *, shared_bytes: float = 0.0,
                    overhead_bytes: float = 0.0, b_link: float = 54e9, b_dec: float = 1100e9, t_compute: float = 0.0,
                    min_window_bytes: float = 128 * 2**20, allow_pinned: bool = True, depth: int | None = None,
-                   window: int | None = None) -> ResidencyPlan:
+                   window: int | None = None, dev_ceb: float | None = None, b_dev: float | None = None,
+                   dev_fused: bool = False) -> ResidencyPlan:
     """Choose (ring, device tier, pinned) for N layers x L experts under `budget_bytes`.
 
     eb: raw bytes of one expert (both tensors); ceb: its compressed record bytes.
@@ -100,6 +101,10 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
     chunk index of the host records): counted inside ``budget_bytes`` like the shared experts,
     so the plan's whole expert footprint stays within the budget.
     Step model: max(link_bytes / b_link, decoded_raw_bytes / b_dec + t_compute).
+    dev_ceb / b_dev: HBM bytes and raw-equivalent rate of a device-tier expert when the device
+    tier uses another record format than the host tier (FX4: larger records, faster decode);
+    dev_fused: device-tier experts are read in place by the decode-into-GEMM kernel, so b_dev
+    covers their GEMM too and they leave t_compute (which then is the resident step time).
     depth: windows in flight (the ring holds depth windows); window: experts per window
     (default: enough for min_window_bytes).  depth None: 1 when the plan is clearly
     link-bound (link time >= 1.5x decode time: the ring's second window buys nothing while
@@ -107,16 +112,19 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
     +10%), else 2 (decode-bound plans need the decode of window g+1 to overlap window g's
     compute -- DSv3 65%: depth 1 is 22% slower).
     """
+    kw = dict(dev_ceb=dev_ceb, b_dev=b_dev, dev_fused=dev_fused)
     if depth is None:
         one = plan_residency(N, L, eb, ceb, budget_bytes, shared_bytes=shared_bytes, overhead_bytes=overhead_bytes,
                              b_link=b_link, b_dec=b_dec,
                              t_compute=t_compute, min_window_bytes=min_window_bytes, allow_pinned=allow_pinned,
-                             depth=1, window=window)
+                             depth=1, window=window, **kw)
         if one.ring and one.link_bytes / b_link >= 1.5 * one.decode_bytes / b_dec:
             return one
         return plan_residency(N, L, eb, ceb, budget_bytes, shared_bytes=shared_bytes, overhead_bytes=overhead_bytes,
                               b_link=b_link, b_dec=b_dec, t_compute=t_compute, min_window_bytes=min_window_bytes,
-                              allow_pinned=allow_pinned, depth=2, window=window)
+                              allow_pinned=allow_pinned, depth=2, window=window, **kw)
+    dceb = ceb if dev_ceb is None else dev_ceb
+    bdev = b_dec if b_dev is None else b_dev
     total = N * L
     cap = budget_bytes - shared_bytes - overhead_bytes
     if window is None:
@@ -137,10 +145,11 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
         room = cap - ring * eb - p * eb
         if room < 0:
             continue
-        d = int(min(total - p, room // ceb))
+        d = int(min(total - p, room // dceb))
         link = (total - p - d) * ceb
         decode = (total - p) * eb
-        est = max(link / b_link, decode / b_dec + t_compute)
+        sm = (total - p - d) * eb / b_dec + d * eb / bdev + t_compute * (1.0 - (d / total if dev_fused else 0.0))
+        est = max(link / b_link, sm)
         key = (est, -ring)
         if best is None or key < best[0]:
             best = (key, p, d, ring, link)
@@ -148,7 +157,7 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
         if w_min > 1:  # small experts: a narrower window still fits (tiny: 8 x 0.8 MB > 25%)
             return plan_residency(N, L, eb, ceb, budget_bytes, shared_bytes=shared_bytes,
                                   overhead_bytes=overhead_bytes, b_link=b_link, b_dec=b_dec, t_compute=t_compute, min_window_bytes=min_window_bytes,
-                                  allow_pinned=allow_pinned, depth=depth, window=max(1, w_min // 2))
+                                  allow_pinned=allow_pinned, depth=depth, window=max(1, w_min // 2), **kw)
         raise ValueError(f"budget {budget_bytes:.3g} B cannot hold a ring")
     (est, _), p, d, ring, link = best
     p_layer = _balanced(p, N)
@@ -169,5 +178,66 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
     for l in range(N):
         streamed = L - p_layer[l]
         device[l, :streamed] = _spread_row(streamed, d_layer[l], w)
-    hbm = ring * eb + p * eb + device.sum() * ceb + shared_bytes + overhead_bytes
+    hbm = ring * eb + p * eb + device.sum() * dceb + shared_bytes + overhead_bytes
     return ResidencyPlan(ring, device, pinned, float(hbm), float(est), float(link), depth, float((total - p) * eb))
+
+
+# Raw-equivalent rates the format choice is made with (B200 measurements, Mixtral T = 256,
+# profiles/r2_fx4_*.jsonl): the Huffman decoder expanding into the ring beside the GEMMs, and
+# the decode-into-GEMM kernel reading FX4 records (GEMM included).  Resident GEMMs stream raw
+# weights at about 5.2 TB/s.
+B_DEC_HUFFMAN = 1.1e12
+B_FUSED_FX4 = 2.3e12
+B_RESIDENT = 5.2e12
+
+
+def fx4_expert_bytes(H: int, F: int) -> float:
+    """HBM bytes of one expert's FX4 records (fx4.cuh layout, no escapes)."""
+    r16 = lambda x: (x + 15) // 16 * 16
+    total = 0
+    for n in (2 * H * F, F * H):
+        total += r16(n) + r16(n // 2) + r16(4 * (n // 256 + 1)) + 16 + 256
+    return float(total)
+
+
+def plan_tiers(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *, fx4_ceb: float | None = None,
+               shared_bytes: float = 0.0, overhead_bytes: float = 0.0, b_link: float = 54e9,
+               b_dec: float = B_DEC_HUFFMAN, b_fx4: float = B_FUSED_FX4, b_resident: float = B_RESIDENT,
+               device_format: str = "auto", **kw) -> ResidencyPlan:
+    """Plan the budget with the device tier in exponent-Huffman records (decoded into the ring)
+    and, when fx4_ceb is given, in FX4 records read in place by the decode-into-GEMM kernel;
+    return the plan whose modelled step is shorter, tagged with ``device_format`` and ``fused``.
+
+    Both candidates are scored with one model: max(link time, SM time) where the SM time is
+    the Huffman decode of every streamed expert that is not FX4-fused, the fused FX4 experts at
+    b_fx4, and the resident GEMM time of the rest.  Huffman wins while the link dominates
+    (its records are 13% smaller, so more experts stay off the link); FX4 wins once the step
+    is SM-bound."""
+    t_res = N * L * eb / b_resident
+    cands = []
+    if device_format in ("auto", "huffman"):
+        p = plan_residency(N, L, eb, ceb, budget_bytes, shared_bytes=shared_bytes, overhead_bytes=overhead_bytes,
+                           b_link=b_link, b_dec=b_dec, **kw)
+        p.device_format, p.fused = "huffman", False
+        cands.append(p)
+    if fx4_ceb and device_format in ("auto", "fx4"):
+        p = plan_residency(N, L, eb, ceb, budget_bytes, shared_bytes=shared_bytes, overhead_bytes=overhead_bytes,
+                           b_link=b_link, b_dec=b_dec, t_compute=t_res, dev_ceb=fx4_ceb, b_dev=b_fx4,
+                           dev_fused=True, **kw)
+        p.device_format, p.fused = "fx4", True
+        cands.append(p)
+
+    def score(p):
+        total = N * L
+        d, pin = p.device_experts, p.pinned_experts
+        host = total - d - pin
+        link = p.link_bytes / b_link
+        if p.fused:
+            sm = host * eb / b_dec + d * eb / b_fx4 + t_res * (total - d) / total
+        else:
+            sm = (host + d) * eb / b_dec + t_res
+        return max(link, sm)
+
+    best = min(cands, key=score)
+    best.est_step_s = score(best)
+    return best

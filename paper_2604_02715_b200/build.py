@@ -15,8 +15,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "libxpgb.so")
 OBJ = os.path.join(ROOT, "build", "obj")
-SOURCES = ["moe_kernels.cu", "moe_gemm_pair.cu", "moe_gemm_dec.cu", "codec.cu", "ep_p2p.cu", "runtime.cu"]
-HEADERS = ["moe_kernels.cuh", "ptx_sm100.cuh", "launch_count.h", "codec.cuh", "codec_dev.cuh", "ep_p2p.cuh"]
+SOURCES = ["moe_kernels.cu", "moe_gemm_pair.cu", "moe_gemm_dec.cu", "codec.cu", "fx4.cu", "ep_p2p.cu", "runtime.cu"]
+HEADERS = ["moe_kernels.cuh", "ptx_sm100.cuh", "launch_count.h", "codec.cuh", "codec_dev.cuh", "fx4.cuh", "ep_p2p.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include")]
 

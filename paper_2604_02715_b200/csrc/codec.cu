@@ -508,8 +508,8 @@ __device__ __forceinline__ void decode_chunk_v2(W& w, const uint8_t* __restrict_
     }
 }
 
-template <class W>
-__global__ void __launch_bounds__(256) k_exp_decode2(const __grid_constant__ DecodeParams p) {
+template <class W, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_exp_decode2(const __grid_constant__ DecodeParams p) {
   __shared__ uint32_t pair[1 << kPairBits];
   __shared__ uint32_t first_code[kCodecMaxLen + 1];
   __shared__ int count[kCodecMaxLen + 1], first_rank[kCodecMaxLen + 1];
@@ -713,43 +713,62 @@ __global__ void __launch_bounds__(kTile7) k_exp_decode7(const __grid_constant__ 
   const uint64_t tpt = (cpt + kTile7 - 1) / kTile7;  // tiles per tensor
   const uint64_t n_tiles = tpt * (uint64_t)p.ntensors;
   const int upc = chunk / 16;  // 16-byte units per chunk row of tex
+  // a tile is staged when it is full, not the tensor's last (its stream end is known), aligned,
+  // and its stream fits the buffer; returns the byte range to copy
+  auto plan = [&](uint64_t tile, const uint8_t** g0, uint32_t* bytes) -> bool {
+    const int ti = (int)(tile / tpt);
+    const uint64_t c0 = (tile - (uint64_t)ti * tpt) * kTile7, c1 = c0 + kTile7;
+    const DecodeTensor& d = p.t[ti];
+    if (c1 >= cpt) return false;
+    const uint32_t b0 = d.index[c0] - d.bit_base, b1 = d.index[c1] - d.bit_base;
+    const uint64_t v0 = c0 * chunk;
+    if (((reinterpret_cast<uintptr_t>(d.out + v0) & 31) | (reinterpret_cast<uintptr_t>(d.sm + v0) & 15) |
+         (reinterpret_cast<uintptr_t>(d.bits) & 15)) != 0)
+      return false;
+    *g0 = reinterpret_cast<const uint8_t*>(d.bits) + ((b0 >> 3) & ~15u);
+    // through the tile's last bit + 16 bytes (the window reads up to 96 bits past its position)
+    *bytes = ((((b1 + 7) >> 3) + 16 + 15) & ~15u) - ((b0 >> 3) & ~15u);
+    return *bytes <= (uint32_t)cap;
+  };
+  __shared__ int s_staged;
   uint32_t phase = 0;
+  uint64_t prefetched = ~0ull;  // tile whose stream thread 0 already put in flight
   for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int ti = (int)(tile / tpt);
     const uint64_t j = tile - (uint64_t)ti * tpt;
     const DecodeTensor& d = p.t[ti];
     const uint64_t c0 = j * kTile7, c1 = (c0 + kTile7 < cpt) ? c0 + kTile7 : cpt;
     const uint64_t v0 = c0 * chunk, v1 = (c1 * chunk < n) ? c1 * chunk : n;
-    // staged tiles: a full tile with a known end (not the tensor's last), aligned, fitting the buffer
-    const uint32_t b0 = d.index[c0] - d.bit_base;
-    const uint32_t b1 = (c1 < cpt) ? d.index[c1] - d.bit_base : 0u;
-    const uint8_t* g0 = reinterpret_cast<const uint8_t*>(d.bits) + ((b0 >> 3) & ~15u);
-    // through the tile's last bit + 16 bytes (the window reads up to 96 bits past its position)
-    const uint32_t bytes = (c1 < cpt) ? ((((b1 + 7) >> 3) + 16 + 15) & ~15u) - ((b0 >> 3) & ~15u) : 0u;
-    const bool aligned = ((reinterpret_cast<uintptr_t>(d.out + v0) & 31) | (reinterpret_cast<uintptr_t>(d.sm + v0) & 15) |
-                          (reinterpret_cast<uintptr_t>(d.bits) & 15)) == 0;
-    const bool staged = c1 < cpt && c1 - c0 == kTile7 && bytes <= (uint32_t)cap && aligned;
-    if (!staged) {
-      // chunk by chunk from global memory (k_exp_decode2's window)
+    const uint32_t my_bit = (c0 + tid < c1) ? d.index[c0 + tid] - d.bit_base : 0u;  // issued early
+    if (tid == 0) {
+      const uint8_t* g0 = nullptr;
+      uint32_t bytes = 0;
+      const bool st = plan(tile, &g0, &bytes);
+      if (st && prefetched != tile) {
+        mbar_arrive_expect_tx(&bar, bytes);
+        bulk_load_1d(tbits, g0, bytes, &bar);
+      }
+      s_staged = st ? 1 : 0;
+    }
+    __syncthreads();
+    if (!s_staged) {
+      // chunk by chunk from global memory (k_exp_decode2's loop)
       const uint64_t c = c0 + tid;
       if (c < c1) {
         Window w;
-        w.init(d.bits, d.index[c] - d.bit_base);
+        w.init(d.bits, my_bit);
         const uint64_t a = c * chunk, b = (a + chunk < n) ? a + chunk : n;
         decode_chunk_v2(w, d.sm, d.out, a, b, pair, ct);
       }
+      __syncthreads();  // s_staged is rewritten for the next tile
       continue;
     }
-    // (A) stream bytes of the tile -> tbits
-    if (tid == 0) {
-      mbar_arrive_expect_tx(&bar, bytes);
-      bulk_load_1d(tbits, g0, bytes, &bar);
-    }
-    mbar_wait(&bar, phase);
+    const uint32_t base_bit = ((d.index[c0] - d.bit_base) >> 3 & ~15u) * 8;
+    mbar_wait(&bar, phase);  // (A) the tile's stream is in tbits
     phase ^= 1;
     // (B) chunk tid: exponent bytes into its tex row
     {
-      const uint32_t bit = d.index[c0 + tid] - d.bit_base - ((b0 >> 3) & ~15u) * 8;
+      const uint32_t bit = my_bit - base_bit;
       LWindow w;
       w.init(smem_u32(tbits) + (bit >> 5) * 4, bit & 31);
       const uint32_t row = smem_u32(tex + tid * chunk);
@@ -774,24 +793,42 @@ __global__ void __launch_bounds__(kTile7) k_exp_decode7(const __grid_constant__ 
       }
     }
     __syncthreads();
-    // (C) coalesced merge with the sign/mantissa plane
-    const uint64_t units = (v1 - v0) / 16;
-    for (uint64_t i = tid; i < units; i += kTile7) {
-      const uint32_t cc = (uint32_t)(i / upc), uu = (uint32_t)(i % upc);
-      uint4 ex;
-      asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                   : "=r"(ex.x), "=r"(ex.y), "=r"(ex.z), "=r"(ex.w)
-                   : "r"(smem_u32(tex + cc * chunk) + ((uu ^ (cc & (upc - 1))) << 4)));
-      const uint4 smv = __ldg(reinterpret_cast<const uint4*>(d.sm + v0) + i);
-      uint16_t* o = d.out + v0 + 16 * i;
-      asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(o),
-                   "r"(pack_words(smv.x, ex.x, 0x5140u)), "r"(pack_words(smv.x, ex.x, 0x7362u)),
-                   "r"(pack_words(smv.y, ex.y, 0x5140u)), "r"(pack_words(smv.y, ex.y, 0x7362u)),
-                   "r"(pack_words(smv.z, ex.z, 0x5140u)), "r"(pack_words(smv.z, ex.z, 0x7362u)),
-                   "r"(pack_words(smv.w, ex.w, 0x5140u)), "r"(pack_words(smv.w, ex.w, 0x7362u))
-                   : "memory");
+    // tbits is free: put the next tile's stream in flight under this tile's merge
+    if (tid == 0) {
+      const uint64_t nxt = tile + gridDim.x;
+      const uint8_t* g0 = nullptr;
+      uint32_t bytes = 0;
+      if (nxt < n_tiles && plan(nxt, &g0, &bytes)) {
+        mbar_arrive_expect_tx(&bar, bytes);
+        bulk_load_1d(tbits, g0, bytes, &bar);
+        prefetched = nxt;
+      }
     }
-    __syncthreads();  // tex and tbits are reused by the next tile
+    // (C) coalesced merge with the sign/mantissa plane, 4 units per thread in flight
+    const uint32_t units = (uint32_t)((v1 - v0) / 16);  // a multiple of 4 * kTile7 on staged tiles
+    const uint4* smp = reinterpret_cast<const uint4*>(d.sm + v0);
+    for (uint32_t i0 = tid; i0 < units; i0 += 4 * kTile7) {
+      uint4 smv[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) smv[r] = __ldg(smp + i0 + r * kTile7);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const uint32_t i = i0 + r * kTile7;
+        const uint32_t cc = i / upc, uu = i % upc;
+        uint4 ex;
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(ex.x), "=r"(ex.y), "=r"(ex.z), "=r"(ex.w)
+                     : "r"(smem_u32(tex + cc * chunk) + ((uu ^ (cc & (upc - 1))) << 4)));
+        uint16_t* o = d.out + v0 + 16 * (uint64_t)i;
+        asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(o),
+                     "r"(pack_words(smv[r].x, ex.x, 0x5140u)), "r"(pack_words(smv[r].x, ex.x, 0x7362u)),
+                     "r"(pack_words(smv[r].y, ex.y, 0x5140u)), "r"(pack_words(smv[r].y, ex.y, 0x7362u)),
+                     "r"(pack_words(smv[r].z, ex.z, 0x5140u)), "r"(pack_words(smv[r].z, ex.z, 0x7362u)),
+                     "r"(pack_words(smv[r].w, ex.w, 0x5140u)), "r"(pack_words(smv[r].w, ex.w, 0x7362u))
+                     : "memory");
+      }
+    }
+    __syncthreads();  // tex is reused by the next tile
   }
 }
 
@@ -897,6 +934,21 @@ void launch_exp_decode_multi(const DecodeTensor* tensors, int ntensors, uint64_t
     } else if (ver == 3) k_exp_decode2<QWindow><<<(unsigned)blocks, 256, 0, s>>>(p);
     else if (ver == 4) k_exp_decode2<WindowD<2>><<<(unsigned)blocks, 256, 0, s>>>(p);
     else if (ver == 5) k_exp_decode2<WindowD<3>><<<(unsigned)blocks, 256, 0, s>>>(p);
+    else if (ver == 8 || ver == 9) {  // register-capped for 6 / 8 resident CTAs per SM (occupancy A/B)
+      static int res8[2] = {0, 0};
+      const int vi = ver - 8;
+      if (!res8[vi]) {
+        int dev = 0, sms = 148, per_sm = 4;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (vi == 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_exp_decode2<Window, 6>, 256, 0);
+        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_exp_decode2<Window, 8>, 256, 0);
+        res8[vi] = std::max(1, sms * std::max(1, per_sm));
+      }
+      const uint64_t b8 = std::min<uint64_t>((n_chunks + 255) / 256, (uint64_t)res8[vi]);
+      if (vi == 0) k_exp_decode2<Window, 6><<<(unsigned)b8, 256, 0, s>>>(p);
+      else k_exp_decode2<Window, 8><<<(unsigned)b8, 256, 0, s>>>(p);
+    }
     else k_exp_decode2<Window><<<(unsigned)blocks, 256, 0, s>>>(p);
   }
   note_launch();

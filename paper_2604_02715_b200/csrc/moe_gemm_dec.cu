@@ -32,6 +32,7 @@
 #include <cstdlib>
 
 #include "codec_dev.cuh"
+#include "fx4.cuh"
 #include "launch_count.h"
 #include "moe_kernels.cuh"
 #include "ptx_sm100.cuh"
@@ -44,7 +45,7 @@ constexpr int kDecWarps = 8;
 constexpr int kDecThreads = 192 + 32 * kDecWarps;  // 448
 constexpr int kDecRows = 256;                      // weight rows per unit (two 128-row A tiles)
 constexpr int kDecThreads_dec = 32 * kDecWarps;    // decoder threads
-constexpr int kRingBytes = 128;                    // per decoder thread: two 64-byte stream blocks
+constexpr int kRingBytes = 256;                    // per decoder thread: four 64-byte stream blocks
 
 template <int BN, int STAGES>
 struct DecCfg {
@@ -72,6 +73,104 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 
 __device__ __forceinline__ void st_smem_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
+// mbarrier wait for the warps that only feed or drain the decoders (TMA, MMA, epilogue): they
+// back off between polls, so their spinning does not take issue slots and LSU bandwidth from
+// the decoder warps on the same SM (ncu: 50 M polls per launch, each reloading the barrier
+// address from local memory).
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  for (;;) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(64);
+  }
+}
+
+// Branch-free stream window over a per-thread shared-memory ring of four 64-byte blocks
+// (cp.async, bypassing L1).  Every lane of a warp refills at its own time, so a refill behind
+// a branch made nearly every warp execute both paths (ncu: the refill branch diverged in
+// 99.8% of warp executions); here a refill is a handful of predicated instructions.  The
+// ring is topped up once per quad (8 values <= 8 words): while the read position sits in
+// block B, blocks B+1 and B+2 are complete and B+3 is in flight, so no read waits.
+struct PWindow {
+  uint64_t win;
+  int p;
+  uint32_t nxt;     // next stream word (raw)
+  uint32_t wi;      // absolute ring word index of the word after nxt
+  uint32_t blk;     // block the fetches have reached (the next to fetch)
+  uint32_t base;    // smem address of this thread's ring
+  uint32_t sw;      // chunk swizzle
+  const uint8_t* g; // global address of block `blk`
+  __device__ __forceinline__ uint32_t word(uint32_t w) const {
+    return lds32(base + ((((w >> 2) & 15) ^ sw) << 4) + ((w & 3) << 2));
+  }
+  __device__ __forceinline__ void fetch_if(bool pred) {  // block `blk` into its slot, predicated
+    const uint32_t slot = blk & 3;
+    const uint32_t pr = pred ? 1u : 0u;
+#pragma unroll
+    for (uint32_t i = 0; i < 4; ++i)
+      asm volatile(
+          "{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q cp.async.cg.shared.global [%0], [%1], 16;\n}\n" ::"r"(
+              base + (((slot * 4 + i) ^ sw) << 4)),
+          "l"(g + 16 * i), "r"(pr)
+          : "memory");
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q cp.async.commit_group;\n}\n" ::"r"(pr) : "memory");
+    g += pred ? 64 : 0;
+    blk += pred ? 1 : 0;
+  }
+  __device__ __forceinline__ void init(const uint32_t* bits, uint32_t bitpos, uint32_t ring, uint32_t swz) {
+    base = ring;
+    sw = swz;
+    blk = 0;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(bits + (bitpos >> 5));
+    g = reinterpret_cast<const uint8_t*>(a & ~uintptr_t(15));
+    const uint32_t w0 = (uint32_t)((a >> 2) & 3);
+    fetch_if(true);
+    fetch_if(true);
+    fetch_if(true);
+    fetch_if(true);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // blocks 0..2 complete
+    win = ((uint64_t)bswap32(word(w0)) << 32) | bswap32(word(w0 + 1));
+    nxt = word(w0 + 2);
+    wi = w0 + 3;
+    p = (int)(bitpos & 31);
+  }
+  // once per quad: the read position entered block wi/16; keep blocks up to wi/16 + 3 fetched
+  __device__ __forceinline__ void top_up() {
+    const bool need = blk < (wi >> 4) + 4;
+    fetch_if(need);
+    uint32_t pr = need ? 1u : 0u;
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q cp.async.wait_group 1;\n}\n" ::"r"(pr) : "memory");
+  }
+  __device__ __forceinline__ void refill() {
+    const bool r = p >= 32;
+    const uint64_t wn = (win << 32) | bswap32(nxt);
+    uint32_t ld = nxt;
+    const uint32_t addr = base + ((((wi >> 2) & 15) ^ sw) << 4) + ((wi & 3) << 2);
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q ld.shared.u32 %0, [%1];\n}\n"
+                 : "+r"(ld)
+                 : "r"(addr), "r"(r ? 1u : 0u)
+                 : "memory");
+    win = r ? wn : win;
+    p = r ? p - 32 : p;
+    nxt = ld;
+    wi += r ? 1u : 0u;
+  }
+  __device__ __forceinline__ uint32_t peek12() const { return (uint32_t)((win << p) >> (64 - kPairBits)); }
+};
+
+__device__ __forceinline__ void ldg_v4(uint4& v, const uint4* p) {
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
 }
 
 struct DUnit {
@@ -102,7 +201,7 @@ __device__ __forceinline__ DUnit dec_unit(int u, const int* s_up, const int* s_o
 
 }  // namespace
 
-template <bool GU, int BN, int STAGES>
+template <bool GU, int BN, int STAGES, int FMT>
 __global__ void __maxnreg__(128)  // 448 threads x 128 registers (144 was refused at launch)
     k_moe_gemm_dec(const __grid_constant__ CUtensorMap map_b, GemmParams p, const DecTables* __restrict__ tabs,
                    int chunk) {
@@ -210,7 +309,7 @@ __global__ void __maxnreg__(128)  // 448 threads x 128 registers (144 was refuse
         const int nb = (un.n_rows + kBoxRowsB - 1) / kBoxRowsB;
         const uint32_t bytes = 2 * nb * kBoxRowsB * kBK * 2;
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_wait_backoff(&empty[stage], phase ^ 1);
           uint8_t* sb = smem + stage * C::STAGE + 2 * C::A_BYTES;
           mbar_arrive_expect_tx(&full[stage], bytes);
           for (int i = 0; i < nb; ++i) {
@@ -235,11 +334,11 @@ __global__ void __maxnreg__(128)  // 448 threads x 128 registers (144 was refuse
       const uint32_t idesc = idesc_bf16_f32(kBM, (un.n_rows + 15) & ~15);
       const int acc = it & 1;
       const uint32_t acc_par = (it >> 1) & 1;
-      mbar_wait(&tempty[acc], acc_par ^ 1);
+      mbar_wait_backoff(&tempty[acc], acc_par ^ 1);
       tc_fence_after();
       const uint32_t d0 = tmem + acc * 256;
       for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(&full[stage], phase);
+        mbar_wait_backoff(&full[stage], phase);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t base = smem_u32(smem + stage * C::STAGE);
@@ -272,7 +371,7 @@ __global__ void __maxnreg__(128)  // 448 threads x 128 registers (144 was refuse
       const DUnit un = dec_unit(u, s_up, s_off, E, BN, S);
       const int acc = it & 1;
       const uint32_t acc_par = (it >> 1) & 1;
-      mbar_wait(&tfull[acc], acc_par);
+      mbar_wait_backoff(&tfull[acc], acc_par);
       tc_fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * 256;
       if (GU) {
@@ -330,29 +429,44 @@ __global__ void __maxnreg__(128)  // 448 threads x 128 registers (144 was refuse
       const int wrow = GU ? (a ? p.F : 0) + un.m0 + lr : 2 * un.m0 + d;
       const bool valid = GU ? (un.m0 + lr < p.F) : (2 * un.m0 + d < p.H);
       const uint64_t v0 = (uint64_t)wrow * K + (uint64_t)kb0 * kBK;
-      SWindow w;
-      // sign/mantissa bytes: 16 per group, kept two groups ahead of use (s0 current, s1, s2);
-      // the smem ring feeds the bitstream, these loads are the decoder's only global reads
-      const uint8_t* smp = R.sm + v0;
+      if constexpr (FMT == 0) {
+      PWindow w;
+      // sign/mantissa bytes: group g (16 values) of the stage lives in register sg; once
+      // consumed, sg is reloaded with group g of the next stage -- one stage of lead, and no
+      // register rotation (moving a register whose load is in flight waits for the load: ncu
+      // put 11% of the samples on such a move).  g is warp-uniform, so the switches below are
+      // uniform branches.  The row's bytes two stages further are prefetched into L2.
+      const uint8_t* smp = R.sm + v0;  // next stage's sign/mantissa bytes
       const uint8_t* smend = R.sm + (uint64_t)wrow * K + (uint64_t)kb1 * kBK;
-      uint4 s0 = make_uint4(0, 0, 0, 0), s1 = s0, s2 = s0;
+      uint4 s0 = make_uint4(0, 0, 0, 0), s1 = s0, s2 = s0, s3 = s0;
       if (valid) {
         w.init(R.bits, R.index[v0 / chunk] - R.bit_base, smem_u32(s_ring + d * kRingBytes), (uint32_t)(d & 7));
-        s0 = __ldg(reinterpret_cast<const uint4*>(smp));
-        s1 = __ldg(reinterpret_cast<const uint4*>(smp) + 1);
-        s2 = __ldg(reinterpret_cast<const uint4*>(smp) + 2);
-        smp += 48;
+        const uint4* q4 = reinterpret_cast<const uint4*>(smp);
+        s0 = __ldg(q4);
+        s1 = __ldg(q4 + 1);
+        s2 = __ldg(q4 + 2);
+        s3 = __ldg(q4 + 3);
+        smp += 64;
       }
       for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_wait_backoff(&empty[stage], phase ^ 1);
         if (valid) {
+          if (smp + 128 < smend) asm volatile("prefetch.global.L2 [%0];" ::"l"(smp + 128));
           const uint32_t row = smem_u32(smem + stage * C::STAGE + a * C::A_BYTES + lr * 128);
           // 8 quads of 8 values (one 16-byte swizzled store each); the quad loop stays rolled so
           // the hot code fits the instruction cache (fully unrolled, 32 pair sites with their
           // slow paths made a 140 KB loop: ncu put 44% of the stall cycles on instruction fetch)
 #pragma unroll 1
           for (uint32_t q = 0; q < 8; ++q) {
-            const uint32_t sa = (q & 1) ? s0.z : s0.x, sb = (q & 1) ? s0.w : s0.y;
+            w.top_up();
+            uint4 cur;
+            switch (q >> 1) {
+              case 0: cur = s0; break;
+              case 1: cur = s1; break;
+              case 2: cur = s2; break;
+              default: cur = s3; break;
+            }
+            const uint32_t sa = (q & 1) ? cur.z : cur.x, sb = (q & 1) ? cur.w : cur.y;
             uint32_t o[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -365,18 +479,93 @@ __global__ void __maxnreg__(128)  // 448 threads x 128 registers (144 was refuse
               o[j] = (dup & 0x807F807Fu) | (e & 0x7F807F80u);
             }
             st_smem_v4(row + ((q ^ sw) << 4), o[0], o[1], o[2], o[3]);
-            if (q & 1) {
-              s0 = s1;
-              s1 = s2;
-              if (smp < smend) s2 = __ldg(reinterpret_cast<const uint4*>(smp));
-              smp += 16;
+            if ((q & 1) && smp < smend) {  // group q/2 consumed: load the next stage's
+              const uint4* nx = reinterpret_cast<const uint4*>(smp) + (q >> 1);
+              // one load per case straight into its register (the compiler merged plain loads
+              // into one temporary plus predicated moves, and the moves waited for the load)
+              switch (q >> 1) {
+                case 0: ldg_v4(s0, nx); break;
+                case 1: ldg_v4(s1, nx); break;
+                case 2: ldg_v4(s2, nx); break;
+                default: ldg_v4(s3, nx); break;
+              }
             }
           }
+          smp += kBK;
           fence_async_smem();
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&full[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      } else {
+      // FX4 records (fx4.cuh): nibble codes at fixed positions, so every pair decodes
+      // independently -- no window, no table chain; the stage's 64 sign/mantissa bytes and 32
+      // nibble bytes are loaded one stage ahead into registers that are reused in place
+      const uint8_t* smp = R.sm + v0;
+      const uint8_t* nbp = reinterpret_cast<const uint8_t*>(R.bits) + v0 / 2;
+      const uint8_t* smend = R.sm + (uint64_t)wrow * K + (uint64_t)kb1 * kBK;
+      const uint8_t* escp = R.esc;
+      const uint32_t bb = R.bit_base * 0x01010101u;
+      uint4 sv[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+      uint4 nv[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+      if (valid) {
+        const uint4* q4 = reinterpret_cast<const uint4*>(smp);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) ldg_v4(sv[g], q4 + g);
+        ldg_v4(nv[0], reinterpret_cast<const uint4*>(nbp));
+        ldg_v4(nv[1], reinterpret_cast<const uint4*>(nbp) + 1);
+        escp = R.esc + R.index[v0 / kFxSeg];
+        smp += kBK;
+        nbp += kBK / 2;
+      }
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait_backoff(&empty[stage], phase ^ 1);
+        if (valid) {
+          if (smp + 128 < smend) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(smp + 128));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(nbp + 64));
+          }
+          const uint32_t row = smem_u32(smem + stage * C::STAGE + a * C::A_BYTES + lr * 128);
+          const bool more = smp < smend;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const uint4& nq = nv[q >> 2];
+            const uint32_t nw = (q & 3) == 0 ? nq.x : (q & 3) == 1 ? nq.y : (q & 3) == 2 ? nq.z : nq.w;
+            const uint4& sq = sv[q >> 1];
+            const uint32_t sa = (q & 1) ? sq.z : sq.x, sb = (q & 1) ? sq.w : sq.y;
+            const uint32_t lo = nw & 0x0F0F0F0Fu, hi = (nw >> 4) & 0x0F0F0F0Fu;
+            const uint32_t escf = ((lo + 0x01010101u) | (hi + 0x01010101u)) & 0x10101010u;
+            const uint32_t le = lo + bb, he = hi + bb;
+            uint32_t o[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint32_t x = __byte_perm(le, he, (uint32_t)(j | ((4 + j) << 4)));
+              const uint32_t ex = ((x & 0xFFu) << 7) | ((x >> 8) << 23);
+              const uint32_t dup = __byte_perm(j < 2 ? sa : sb, 0, (j & 1) ? 0x3322u : 0x1100u);
+              o[j] = (dup & 0x807F807Fu) | (ex & 0x7F807F80u);
+            }
+            if (__builtin_expect(escf != 0u, 0)) {  // exponents outside the window, in value order
+#pragma unroll
+              for (int v = 0; v < 8; ++v)
+                if (((nw >> (4 * v)) & 15u) == 15u) {
+                  const uint32_t ex = (uint32_t)*escp++;
+                  const int sh = 16 * (v & 1) + 7;
+                  o[v >> 1] = (o[v >> 1] & ~(0xFFu << sh)) | (ex << sh);
+                }
+            }
+            st_smem_v4(row + ((((uint32_t)q) ^ sw) << 4), o[0], o[1], o[2], o[3]);
+            if ((q & 1) && more) ldg_v4(sv[q >> 1], reinterpret_cast<const uint4*>(smp) + (q >> 1));
+            if ((q & 3) == 3 && more) ldg_v4(nv[q >> 2], reinterpret_cast<const uint4*>(nbp) + (q >> 2));
+          }
+          smp += kBK;
+          nbp += kBK / 2;
+          fence_async_smem();
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
       }
     }
   }
@@ -391,11 +580,12 @@ __global__ void __maxnreg__(128)  // 448 threads x 128 registers (144 was refuse
 using DecKernel = void (*)(const CUtensorMap, GemmParams, const DecTables*, int);
 
 // stage counts: the A tiles are produced on-chip, so a few stages cover the decoder/MMA overlap
-#define XPGB_DEC_TILES(X) X(32, 4) X(48, 3) X(64, 3) X(80, 3) X(96, 2) X(128, 2)
+#define XPGB_DEC_TILES(X) X(32, 3) X(48, 2) X(64, 2) X(80, 2) X(96, 2) X(128, 2)
 
 template <bool GU, int BN, int ST>
 static void set_dec_attr() {
-  cudaFuncSetAttribute(k_moe_gemm_dec<GU, BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, DecCfg<BN, ST>::SMEM);
+  cudaFuncSetAttribute(k_moe_gemm_dec<GU, BN, ST, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, DecCfg<BN, ST>::SMEM);
+  cudaFuncSetAttribute(k_moe_gemm_dec<GU, BN, ST, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, DecCfg<BN, ST>::SMEM);
 }
 
 void set_gemm_dec_attrs() {
@@ -410,20 +600,22 @@ bool gemm_dec_supported(int H, int F, int chunk) {
 }
 
 void launch_gemm_dec(bool gate_up, const CUtensorMap& map_b, const GemmParams& p, const CodecTable& table, int chunk,
-                     int bn, int grid, cudaStream_t s) {
+                     int bn, int grid, cudaStream_t s, bool fx4) {
   const DecTables* tabs = codec_device_tables(table, s);
   if (!tabs) return;
   DecKernel kern = nullptr;
   int smem = 0;
-#define XPGB_PICK_DEC(BN, ST)                                                                \
-  if (bn == BN) {                                                                            \
-    kern = gate_up ? k_moe_gemm_dec<true, BN, ST> : k_moe_gemm_dec<false, BN, ST>;           \
-    smem = DecCfg<BN, ST>::SMEM;                                                             \
+#define XPGB_PICK_DEC(BN, ST)                                                                            \
+  if (bn == BN) {                                                                                        \
+    kern = fx4 ? (gate_up ? k_moe_gemm_dec<true, BN, ST, 1> : k_moe_gemm_dec<false, BN, ST, 1>)           \
+               : (gate_up ? k_moe_gemm_dec<true, BN, ST, 0> : k_moe_gemm_dec<false, BN, ST, 0>);          \
+    smem = DecCfg<BN, ST>::SMEM;                                                                         \
   }
   XPGB_DEC_TILES(XPGB_PICK_DEC)
 #undef XPGB_PICK_DEC
   if (!kern) {
-    kern = gate_up ? k_moe_gemm_dec<true, 128, 2> : k_moe_gemm_dec<false, 128, 2>;
+    kern = fx4 ? (gate_up ? k_moe_gemm_dec<true, 128, 2, 1> : k_moe_gemm_dec<false, 128, 2, 1>)
+               : (gate_up ? k_moe_gemm_dec<true, 128, 2, 0> : k_moe_gemm_dec<false, 128, 2, 0>);
     smem = DecCfg<128, 2>::SMEM;
   }
   kern<<<grid, kDecThreads, smem, s>>>(map_b, p, tabs, chunk);

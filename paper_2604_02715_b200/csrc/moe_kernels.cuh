@@ -60,12 +60,15 @@ __host__ __device__ inline void split_kb(int s, int S, int KB, int* kb0, int* kb
 // A device-tier expert tensor read in place by the decode-into-GEMM kernel
 // (moe_gemm_dec.cu): its exponent-Huffman record (sign/mantissa plane, bitstream, chunk
 // index; index entries minus bit_base are bit offsets into `bits`).
+// FX4 records (fx4.cuh) reuse the fields: bits = the nibble plane, index = the escape index,
+// bit_base = the tensor's base exponent, esc = the escape bytes.
 struct DecRec {
   const uint8_t* sm;
   const uint32_t* bits;
   const uint32_t* index;
   uint32_t bit_base;
-  uint32_t pad;
+  uint32_t fmt;  // 0 exponent-Huffman, 1 FX4
+  const uint8_t* esc;
 };
 
 // Arguments of one grouped-GEMM launch (gate/up or down) of one layer.
@@ -134,7 +137,7 @@ struct CodecTable;
 bool gemm_dec_supported(int H, int F, int chunk);
 void set_gemm_dec_attrs();
 void launch_gemm_dec(bool gate_up, const CUtensorMap& map_b, const GemmParams& p, const CodecTable& table, int chunk,
-                     int bn, int grid, cudaStream_t s);
+                     int bn, int grid, cudaStream_t s, bool fx4 = false);
 void launch_gemm_pair(bool gate_up, const CUtensorMap& map_x, const CUtensorMap& map_w, const CUtensorMap& map_ws,
                       const GemmParams& p, int num_sms, cudaStream_t s, bool split = true);
 

@@ -27,6 +27,7 @@
 
 #include "../../include/xpgb.h"
 #include "codec.cuh"
+#include "fx4.cuh"
 #include "ep_p2p.cuh"
 #include "launch_count.h"
 #include "moe_kernels.cuh"
@@ -282,6 +283,11 @@ struct Ctx {
   bool poison = false;
   int war_sab_it = 0, war_sab_layer = 0;
   DecRec* d_decrec = nullptr;  // [N][2][E]: record of each device-tier tensor (sm == nullptr: not device tier)
+  // device-tier record format: 0 exponent-Huffman (the host pool's records, staged as they are),
+  // 1 FX4 (fx4.cuh: encoded on the GPU from the raw pool at staging, for decode-into-GEMM)
+  int dev_fmt = 0;
+  std::vector<int> fx_base;         // [N*E*2] FX4 base exponent of each device-tier tensor
+  std::vector<uint64_t> fx_bytes;   // [N*E*2] FX4 record bytes
 
   // profiling
   bool prof = false;
@@ -603,7 +609,8 @@ static void enqueue_window(Ctx* c, int layer, const float* x, float* y, int T, i
     launch_gemm_pair(true, c->map_xp_pair, c->map_gu, c->S ? c->map_gu_sh : c->map_gu, pg, c->num_sms, s,
                      c->pair_split);
   else {
-    if (fused[0]) launch_gemm_dec(true, c->map_xp, pg, c->ctab, c->cchunk, pick_bn_dec(c, T, kk), c->num_sms, s);
+    if (fused[0])
+      launch_gemm_dec(true, c->map_xp, pg, c->ctab, c->cchunk, pick_bn_dec(c, T, kk), c->num_sms, s, c->dev_fmt == 1);
     if (rest[0])
       launch_gate_up(c->map_gu, c->map_xp, c->S ? c->map_gu_sh : c->map_gu, pg, bn, c->num_sms, s, lean_gemm(c));
   }
@@ -613,7 +620,8 @@ static void enqueue_window(Ctx* c, int layer, const float* x, float* y, int T, i
     launch_gemm_pair(false, c->map_h_pair, c->map_dn, c->S ? c->map_dn_sh : c->map_dn, pd, c->num_sms, s,
                      c->pair_split);
   else {
-    if (fused[1]) launch_gemm_dec(false, c->map_h, pd, c->ctab, c->cchunk, pick_bn_dec(c, T, kk), c->num_sms, s);
+    if (fused[1])
+      launch_gemm_dec(false, c->map_h, pd, c->ctab, c->cchunk, pick_bn_dec(c, T, kk), c->num_sms, s, c->dev_fmt == 1);
     if (rest[1])
       launch_down(c->map_dn, c->map_h, c->S ? c->map_dn_sh : c->map_dn, pd, bn_dn, c->num_sms, s, lean_gemm(c));
   }
@@ -930,7 +938,18 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
       const size_t ti = tix(e);
       uint8_t* dst = block_ptr(c, kind, blocks[e]);
       const float dl = delay_of(e);
-      if (c->backend[ti] == 1) {
+      if (c->backend[ti] == 1 && c->dev_fmt == 1) {
+        // FX4 device tier, expanded into the ring (groups the fused GEMM does not take)
+        if (!dev_on_dv) CK(cudaStreamWaitEvent(dv, c->ev_mapped[k], 0));
+        dev_on_dv = true;
+        if (dl > 0) sleep_on(dv, dl);
+        dec_mark(rs, dv, c->fx_bytes[ti] + 2 * n, true);
+        launch_fx4_decode(c->dev_tier + c->dev_off[ti], n, c->fx_base[ti], reinterpret_cast<uint16_t*>(dst), dv);
+        CKLAUNCH();
+        dec_mark(rs, dv, 0, false);
+        rs.decoded += 2 * n;
+        ++e;
+      } else if (c->backend[ti] == 1) {
         // device tier: consecutive device-tier experts of the layer decode in one launch
         if (!dev_on_dv) CK(cudaStreamWaitEvent(dv, c->ev_mapped[k], 0));
         dev_on_dv = true;
@@ -1439,6 +1458,68 @@ static void run_impl(Ctx* c, const xpgb_run_opts* o, const float* x, float* y, x
   session_end(c, rep);
 }
 
+// FX4 device tier: every device-tier tensor is copied raw from the pinned pool into a scratch
+// buffer and encoded there by the GPU (histogram -> base, escape counts -> size, then the
+// record), straight into its slot of the device tier.  Two passes (sizes, then records), so the
+// allocation is exact.  Setup work: it synchronises.
+static void stage_device_tier_fx4(Ctx* c) {
+  if (!c->host) XFAIL(XPGB_ERR_BACKEND_MISS, "the FX4 device tier is encoded from the raw host pool");
+  const size_t nt = (size_t)c->N * c->E * 2;
+  c->fx_base.assign(nt, 0);
+  c->fx_bytes.assign(nt, 0);
+  bool any = false;
+  for (size_t ti = 0; ti < nt; ++ti) any |= c->backend[ti] != 0;
+  if (!any) return;
+  const uint64_t maxraw = std::max(c->s1, c->s2);
+  uint8_t* raw = nullptr;
+  uint32_t* scratch = nullptr;
+  CK(cudaMalloc(&raw, maxraw));
+  CK(cudaMalloc(&scratch, xpgb_fx4_scratch_bytes(maxraw / 2)));
+  cudaStream_t s = c->s_copy[0];
+  auto src_of = [&](size_t ti) { return c->host + (ti / 2) * (c->s1 + c->s2) + ((ti & 1) ? c->s1 : 0); };
+  uint64_t total = 0;
+  for (size_t ti = 0; ti < nt; ++ti) {
+    if (!c->backend[ti]) continue;
+    const uint64_t sz = (ti & 1) ? c->s2 : c->s1;
+    CK(cudaMemcpyAsync(raw, src_of(ti), sz, cudaMemcpyHostToDevice, s));
+    int base = 0;
+    uint64_t esc = 0;
+    fx4_count(reinterpret_cast<const uint16_t*>(raw), sz / 2, scratch, &base, &esc, s);
+    CKLAUNCH();
+    c->fx_base[ti] = base;
+    c->fx_bytes[ti] = fx_layout(sz / 2, esc).total;
+    total += (c->fx_bytes[ti] + 255) & ~255ull;
+  }
+  CK(cudaMalloc(&c->dev_tier, total + 256));
+  uint64_t at = 0;
+  for (size_t ti = 0; ti < nt; ++ti) {
+    if (!c->backend[ti]) continue;
+    const uint64_t sz = (ti & 1) ? c->s2 : c->s1;
+    CK(cudaMemcpyAsync(raw, src_of(ti), sz, cudaMemcpyHostToDevice, s));
+    c->dev_off[ti] = (int64_t)at;
+    fx4_encode(reinterpret_cast<const uint16_t*>(raw), sz / 2, c->fx_base[ti], scratch, c->dev_tier + at, s);
+    CKLAUNCH();
+    at += (c->fx_bytes[ti] + 255) & ~255ull;
+  }
+  CK(cudaStreamSynchronize(s));
+  cudaFree(raw);
+  cudaFree(scratch);
+  std::vector<DecRec> recs(nt / 2 * 2);
+  memset(recs.data(), 0, recs.size() * sizeof(DecRec));
+  for (size_t ti = 0; ti < nt; ++ti) {
+    if (!c->backend[ti]) continue;
+    const uint64_t n = ((ti & 1) ? c->s2 : c->s1) / 2;
+    const FxLayout L = fx_layout(n, 0);
+    const uint8_t* rec = c->dev_tier + c->dev_off[ti];
+    const size_t layer0 = ti / 2 / c->E, e = ti / 2 % c->E, k = ti & 1;
+    recs[(layer0 * 2 + k) * c->E + e] =
+        DecRec{rec, reinterpret_cast<const uint32_t*>(rec + L.nib), reinterpret_cast<const uint32_t*>(rec + L.idx),
+               (uint32_t)c->fx_base[ti], 1u, rec + L.esc};
+  }
+  CK(cudaMalloc(&c->d_decrec, recs.size() * sizeof(DecRec)));
+  CK(cudaMemcpy(c->d_decrec, recs.data(), recs.size() * sizeof(DecRec), cudaMemcpyHostToDevice));
+}
+
 static void stage_device_tier(Ctx* c) {
   if (c->dev_tier) {
     cudaFree(c->dev_tier);
@@ -1454,10 +1535,14 @@ static void stage_device_tier(Ctx* c) {
     if (!c->codec) return raw;
     return xpgb_codec_record_bytes(raw / 2, c->rec_bits[ti], c->cchunk);
   };
+  std::fill(c->dev_off.begin(), c->dev_off.end(), -1);
+  if (c->dev_fmt == 1) {
+    stage_device_tier_fx4(c);
+    return;
+  }
   uint64_t total = 0;
   for (size_t ti = 0; ti < pages * 2; ++ti)
     if (c->backend[ti]) total += (tensor_bytes(ti) + 255) & ~255ull;
-  std::fill(c->dev_off.begin(), c->dev_off.end(), -1);
   if (total == 0) return;
   if (!c->codec && !c->host) XFAIL(XPGB_ERR_BACKEND_MISS, "device-tier staging needs the host pool");
   CK(cudaMalloc(&c->dev_tier, total + 256));  // slack: stream readers fetch 16-byte blocks ahead
@@ -1482,7 +1567,8 @@ static void stage_device_tier(Ctx* c) {
       const uint8_t* rec = c->dev_tier + c->dev_off[ti];
       const size_t layer0 = ti / 2 / c->E, e = ti / 2 % c->E, k = ti & 1;
       recs[(layer0 * 2 + k) * c->E + e] = DecRec{rec, reinterpret_cast<const uint32_t*>(rec + sm16),
-                                                 reinterpret_cast<const uint32_t*>(rec + sm16 + bits16), 0u, 0u};
+                                                 reinterpret_cast<const uint32_t*>(rec + sm16 + bits16), 0u, 0u,
+                                                 nullptr};
     }
     if (c->d_decrec) cudaFree(c->d_decrec);
     CK(cudaMalloc(&c->d_decrec, recs.size() * sizeof(DecRec)));
@@ -2092,6 +2178,42 @@ int xpgb_codec_decode(const void* record_dev, uint64_t n, uint64_t bits_len, int
   });
 }
 
+uint64_t xpgb_fx4_scratch_bytes(uint64_t n) { return (n / kFxSeg + 1) * 4 + 1024 + 256; }
+
+int xpgb_fx4_measure(const void* raw_dev, uint64_t n, void* scratch_dev, int32_t* base, uint64_t* n_escapes,
+                     uint64_t* record_bytes, void* stream) {
+  return guard([&] {
+    if (n % kFxSeg) XFAIL(XPGB_ERR_CONFIG, "FX4 tensors hold a multiple of %d values", kFxSeg);
+    int b = 0;
+    uint64_t esc = 0;
+    fx4_count(static_cast<const uint16_t*>(raw_dev), n, static_cast<uint32_t*>(scratch_dev), &b, &esc,
+              (cudaStream_t)stream);
+    CKLAUNCH();
+    *base = b;
+    if (n_escapes) *n_escapes = esc;
+    if (record_bytes) *record_bytes = fx_layout(n, esc).total;
+  });
+}
+
+int xpgb_fx4_encode(const void* raw_dev, uint64_t n, int32_t base, void* scratch_dev, void* record_dev, void* stream) {
+  return guard([&] {
+    if (n % kFxSeg) XFAIL(XPGB_ERR_CONFIG, "FX4 tensors hold a multiple of %d values", kFxSeg);
+    if (base < 0 || base > 241) XFAIL(XPGB_ERR_OUT_OF_RANGE, "FX4 base %d outside [0, 241]", base);
+    fx4_encode(static_cast<const uint16_t*>(raw_dev), n, base, static_cast<uint32_t*>(scratch_dev),
+               static_cast<uint8_t*>(record_dev), (cudaStream_t)stream);
+    CKLAUNCH();
+  });
+}
+
+int xpgb_fx4_decode(const void* record_dev, uint64_t n, int32_t base, void* out_dev, void* stream) {
+  return guard([&] {
+    if (n % kFxSeg) XFAIL(XPGB_ERR_CONFIG, "FX4 tensors hold a multiple of %d values", kFxSeg);
+    launch_fx4_decode(static_cast<const uint8_t*>(record_dev), n, base, static_cast<uint16_t*>(out_dev),
+                      (cudaStream_t)stream);
+    CKLAUNCH();
+  });
+}
+
 int xpgb_set_codec(xpgb_ctx* h, const void* pool, uint64_t pool_bytes, const uint64_t* rec_offsets,
                    const uint64_t* bits_lens, const uint8_t* lengths256, int32_t chunk, int32_t host_compressed) {
   return guard([&] {
@@ -2116,7 +2238,9 @@ int xpgb_hbm_bytes(xpgb_ctx* h, uint64_t* ring, uint64_t* staging, uint64_t* dev
     for (size_t ti = 0; ti < nt && c->dev_tier; ++ti)
       if (c->backend[ti]) {
         const uint64_t raw = (ti & 1) ? c->s2 : c->s1;
-        dt += c->codec ? xpgb_codec_record_bytes(raw / 2, c->rec_bits[ti], c->cchunk) : raw;
+        dt += c->dev_fmt == 1 ? c->fx_bytes[ti]
+              : c->codec      ? xpgb_codec_record_bytes(raw / 2, c->rec_bits[ti], c->cchunk)
+                              : raw;
       }
     *device_tier = dt;
   });
@@ -2203,6 +2327,18 @@ int xpgb_set_hazard_checks(xpgb_ctx* h, int32_t poison, int32_t skip_war_iterati
     c->poison = poison != 0;
     c->war_sab_it = skip_war_iteration;
     c->war_sab_layer = skip_war_layer;
+  });
+}
+
+int xpgb_set_device_format(xpgb_ctx* h, int32_t format) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    if (c->sess && c->sess->active) XFAIL(XPGB_ERR, "cannot change the device-tier format during a session");
+    if (format < 0 || format > 1) XFAIL(XPGB_ERR_OUT_OF_RANGE, "device-tier format %d: need 0 (Huffman) or 1 (FX4)", format);
+    if (format == c->dev_fmt) return;
+    CK(cudaDeviceSynchronize());
+    c->dev_fmt = format;
+    if (c->codec) stage_device_tier(c);  // re-stage whatever is placed on the device tier
   });
 }
 

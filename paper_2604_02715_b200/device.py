@@ -155,6 +155,14 @@ class Context:
         it, layer = skip_war if skip_war else (0, 0)
         call("xpgb_set_hazard_checks", self._h, 1 if poison else 0, int(it), int(layer))
 
+    def set_device_format(self, fmt: str) -> None:
+        """Compressed device-tier records: "huffman" (the reference's codec) or "fx4" (fixed-width
+        exponent offsets, fx4.cuh) -- re-stages the device tier."""
+        if fmt not in ("huffman", "fx4"):
+            raise XpgError(f"unknown device-tier format {fmt!r}")
+        call("xpgb_set_device_format", self._h, 1 if fmt == "fx4" else 0)
+        self._dev_fmt = fmt
+
     def set_fused_decode(self, on: bool) -> None:
         """Decode-into-GEMM for the builtin compute: device-tier experts read in place."""
         call("xpgb_set_fused_decode", self._h, 1 if on else 0)

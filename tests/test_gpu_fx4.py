@@ -1,0 +1,105 @@
+"""FX4 device-tier records (fx4.cuh): lossless round trips on the GPU, exact record sizes, and
+paged stacks on an FX4 device tier -- decoded into the ring or read in place by the
+decode-into-GEMM kernel -- byte-identical to the resident model."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def X():
+    import paper_2604_02715_b200 as X
+
+    return X
+
+
+def _roundtrip(words: np.ndarray):
+    import torch
+
+    from paper_2604_02715_b200._lib import call, lib
+
+    n = words.size
+    raw = torch.from_numpy(words.view(np.int16).copy()).cuda()
+    scratch = torch.empty(int(lib().xpgb_fx4_scratch_bytes(n)), dtype=torch.uint8, device="cuda")
+    base, esc, nbytes = C.c_int32(), C.c_uint64(), C.c_uint64()
+    s = torch.cuda.current_stream().cuda_stream
+    call("xpgb_fx4_measure", C.c_void_p(raw.data_ptr()), C.c_uint64(n), C.c_void_p(scratch.data_ptr()),
+         C.byref(base), C.byref(esc), C.byref(nbytes), C.c_void_p(s))
+    rec = torch.full((int(nbytes.value),), 0xAB, dtype=torch.uint8, device="cuda")
+    call("xpgb_fx4_encode", C.c_void_p(raw.data_ptr()), C.c_uint64(n), base.value, C.c_void_p(scratch.data_ptr()),
+         C.c_void_p(rec.data_ptr()), C.c_void_p(s))
+    out = torch.empty_like(raw)
+    call("xpgb_fx4_decode", C.c_void_p(rec.data_ptr()), C.c_uint64(n), base.value, C.c_void_p(out.data_ptr()),
+         C.c_void_p(s))
+    torch.cuda.synchronize()
+    return out.cpu().numpy().view(np.uint16), base.value, esc.value, nbytes.value
+
+
+def test_fx4_roundtrip_gaussian_weights():
+    rng = np.random.default_rng(1)
+    n = 1 << 20
+    w = (rng.standard_normal(n, dtype=np.float32) * 0.02).view(np.uint32)
+    words = ((w + 0x7FFF + ((w >> 16) & 1)) >> 16).astype(np.uint16)  # RNE to bf16
+    out, base, esc, nbytes = _roundtrip(words)
+    assert np.array_equal(out, words)
+    ex = (words >> 7) & 0xFF
+    assert esc == int(((ex < base) | (ex > base + 14)).sum())
+    assert esc < n // 1000  # a 15-wide window covers N(0, 0.02) almost entirely
+    assert nbytes <= n * 1.52 + 8192  # ~12.1 bits per value
+
+
+def test_fx4_roundtrip_every_bf16_pattern_and_escapes():
+    # all 65,536 bf16 patterns (NaN, Inf, subnormals, both signs): most exponents escape
+    words = np.arange(1 << 16, dtype=np.uint32).astype(np.uint16)
+    rng = np.random.default_rng(5)
+    words = np.concatenate([words, rng.permutation(words)])
+    out, base, esc, _ = _roundtrip(words)
+    assert np.array_equal(out, words)
+    assert esc > words.size // 2
+
+
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("T,host_codec", [(16, False), (40, True), (100, True)])
+def test_fx4_device_tier_stack_equals_resident(X, fused, T, host_codec):
+    spec = X.ModelSpec(4, 8, 256, 512)
+    fwd = X.ForwardSpec(T, 2, 7)
+    container = X.generate_synthetic_model(spec, 7)
+    backends = [X.Backend(1, X.BackendKind.COMPRESSED_DEVICE, 300e9, 1 << 50),
+                X.Backend(2, X.BackendKind.HOST_OFFLOAD, 30e9, 1 << 50)]
+    hier = X.StorageHierarchy(container, None, X.plan_placement(spec, backends, alpha=0.5 if host_codec else 1.0),
+                              backends)
+    x = np.random.default_rng(T).standard_normal((T, spec.hidden_dim), dtype=np.float32)
+    runner = X.StreamedRunner(spec, hier, fwd, host_codec=host_codec, fused_decode=fused, device_format="fx4")
+    rep = runner.run(2, acts=x.copy())
+    assert rep.page_fault is None and rep.violations == []
+    base = X.resident_baseline(2, spec, container, fwd, acts=x.copy())
+    assert np.asarray(rep.final_activations).tobytes() == np.asarray(base).tobytes()
+    assert runner.ctx.hbm_bytes()["device_tier"] > 0
+
+
+def test_fx4_full_shape_fused_equals_resident(X):
+    import torch
+
+    from paper_2604_02715_b200.exponent_codec import CompressedModel
+
+    spec = X.ModelSpec(2, 8, 4096, 14336)
+    T = 256
+    fwd = X.ForwardSpec(T, 2, 7)
+    container = X.generate_fast_model(spec, 7)
+    backends = [X.Backend(1, X.BackendKind.COMPRESSED_DEVICE, 300e9, 1 << 50),
+                X.Backend(2, X.BackendKind.HOST_OFFLOAD, 30e9, 1 << 50)]
+    hier = X.StorageHierarchy(container, CompressedModel.from_container(container),
+                              X.plan_placement(spec, backends, alpha=1.0), backends)
+    x = torch.from_numpy(np.random.default_rng(3).standard_normal((T, 4096), dtype=np.float32)).cuda()
+    runner = X.StreamedRunner(spec, hier, fwd, fused_decode=True, device_format="fx4")
+    rep = runner.run(2, acts=x.clone())
+    assert rep.page_fault is None and rep.violations == [] and rep.decoded_bytes == 0
+    paged = rep.final_activations.cpu().numpy()
+    del runner
+    torch.cuda.empty_cache()
+    model = X.ResidentModel(spec, container, max_tokens=T)
+    y, _ = model.run(2, fwd, x.clone())
+    assert paged.tobytes() == y.cpu().numpy().tobytes()

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--tokens", type=int, default=256)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--modes", default="1,0")
+    ap.add_argument("--device-format", default="huffman", choices=["huffman", "fx4"])
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -41,7 +42,7 @@ def main():
     x = torch.from_numpy(np.random.default_rng(3).standard_normal((args.tokens, H), dtype=np.float32)).cuda()
     outs = {}
     for mode in (int(m) for m in args.modes.split(",")):
-        runner = X.StreamedRunner(spec, hier, fwd, fused_decode=bool(mode))
+        runner = X.StreamedRunner(spec, hier, fwd, fused_decode=bool(mode), device_format=args.device_format)
         runner.run(1, acts=x.clone())
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -53,6 +54,7 @@ def main():
         ms = e0.elapsed_time(e1) / args.steps
         outs[mode] = rep.final_activations.cpu().numpy().tobytes()
         print(json.dumps({"config": args.config, "layers": args.layers, "T": args.tokens, "fused": mode,
+                          "device_format": args.device_format, "device_tier_bytes": runner.ctx.hbm_bytes()["device_tier"],
                           "ms_per_step": ms, "raw_GBps": spec.total_bytes / ms / 1e6,
                           "tok_s": args.tokens / ms * 1e3, "decoded_bytes_per_step": rep.decoded_bytes / args.steps,
                           "kernels": rep.kernels}), flush=True)

@@ -44,6 +44,8 @@ def main():
     ap.add_argument("--depth", type=int, default=None, help="budget: windows in flight on the planned ring (default: the planner picks 1 or 2)")
     ap.add_argument("--window", type=int, default=None, help="budget: experts per ring window")
     ap.add_argument("--b-dec", type=float, default=None, help="budget: the planner's decoder GB/s (model input)")
+    ap.add_argument("--device-format", default="auto", choices=["auto", "huffman", "fx4"],
+                    help="budget: device-tier records (auto: the planner picks by its step model)")
     ap.add_argument("--stage-bufs", type=int, default=None, help="staging buffers per kind (host codec)")
     ap.add_argument("--rings", default="6,8,12", help="sub-layer ring sizes (expert blocks per kind) for budget")
     args = ap.parse_args()
@@ -92,14 +94,16 @@ def main():
                                   **run_kw)
         plan = None
         if what in ("plan", "tokens"):
-            from paper_2604_02715_b200.budget import plan_residency
+            from paper_2604_02715_b200.budget import fx4_expert_bytes, plan_tiers
 
             Lc = cspec.experts_per_layer
             ceb = runner.device_tier_bytes(Lc) / (N * Lc) * 1.002
             b = p if what == "plan" else args.budget
-            plan = plan_residency(N, Lc, spec.expert_bytes, ceb, b * budget_base, shared_bytes=shared_b,
-                                  overhead_bytes=runner.ctx.hbm_bytes()["staging"], depth=args.depth, window=args.window,
-                                  **({"b_dec": args.b_dec * 1e9} if args.b_dec else {}))
+            plan = plan_tiers(N, Lc, spec.expert_bytes, ceb, b * budget_base, shared_bytes=shared_b,
+                              fx4_ceb=fx4_expert_bytes(spec.hidden_dim, spec.intermediate_dim) * 1.002,
+                              device_format=args.device_format,
+                              overhead_bytes=runner.ctx.hbm_bytes()["staging"], depth=args.depth, window=args.window,
+                              **({"b_dec": args.b_dec * 1e9} if args.b_dec else {}))
             runner.apply_plan(plan)
         runner.run(args.warmup, acts=x)
         secs, rep = timed(torch, lambda s: runner.run(s, acts=x), args.steps)
@@ -108,6 +112,9 @@ def main():
                "budget": p if what == "plan" else None,
                "pinned_per_layer": (plan.pinned_experts / N if plan else (p if what == "pinned" else 0)),
                "device_tier_per_layer": plan.device_experts / N if plan else 0,
+               "device_format": getattr(plan, "device_format", "huffman") if plan else None,
+               "fused_decode": bool(getattr(plan, "fused", False)) if plan else False,
+               "planned_tok_s": T / plan.est_step_s if plan else None,
                "ring_depth": plan.depth if plan else 2, "stage_buffers": args.stage_bufs or 4,
                "ring_experts": (plan.ring if plan else (p if what == "ring" else 2 * (L - (p if what == "pinned" else 0)))),
                "hbm_fraction": (hbm["ring"] + hbm["device_tier"]) / budget_base,
