@@ -184,10 +184,11 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
 
 # Raw-equivalent rates the format choice is made with (B200 measurements, Mixtral T = 256,
 # profiles/r2_fx4_*.jsonl): the Huffman decoder expanding into the ring beside the GEMMs, and
-# the decode-into-GEMM kernel reading FX4 records (GEMM included).  Resident GEMMs stream raw
+# the decode-into-GEMM kernel reading FX4 records through TMA-staged compressed stages (GEMM
+# included, profiles/r2_fused_fx4_mixtral_v3.jsonl).  Resident GEMMs stream raw
 # weights at about 5.2 TB/s.
 B_DEC_HUFFMAN = 1.1e12
-B_FUSED_FX4 = 2.3e12
+B_FUSED_FX4 = 3.2e12
 B_RESIDENT = 5.2e12
 
 

@@ -16,10 +16,11 @@
 // enters its row's stream once per unit (one chunk-index read) and then decodes the row
 // continuously across stages and chunks -- the stream of one tensor row is contiguous.
 //
-// Warps (448 threads, one CTA per SM):
+// Warps (480 threads, one CTA per SM):
 //   0      TMA producer of the activation tiles (hi and lo planes, moe_kernels.cuh)
 //   1      TMEM allocator + MMA issuer
 //   2..5   epilogue (TMEM lanes 32*(w%4)..)
+//   14     FX4 only: TMA producer of the compressed stages (sign/mantissa + nibble rows)
 //   6..13  decoders: thread d owns weight row d of the unit (tile d>>7, tile row d&127);
 //          per 64-value stage it decodes 32 exponent pairs through the 12-bit pair table
 //          (codec_dev.cuh) and writes 8 x 16 B into its swizzled smem row, then
@@ -42,21 +43,30 @@ namespace xpgb {
 namespace {
 
 constexpr int kDecWarps = 8;
-constexpr int kDecThreads = 192 + 32 * kDecWarps;  // 448
+constexpr int kDecThreads = 192 + 32 * kDecWarps + 32;  // 480: + the FX4 compressed-stage producer warp
 constexpr int kDecRows = 256;                      // weight rows per unit (two 128-row A tiles)
 constexpr int kDecThreads_dec = 32 * kDecWarps;    // decoder threads
 constexpr int kRingBytes = 256;                    // per decoder thread: four 64-byte stream blocks
 
-template <int BN, int STAGES>
+// FMT 0 (exponent-Huffman): decoded stages + the pair table and per-thread stream rings.
+// FMT 1 (FX4): decoded stages + CST compressed stages the TMA fills -- per stage the unit's
+// 2 x 128 rows of 64 sign/mantissa bytes (64-B swizzle) and 32 nibble bytes (32-B swizzle).
+constexpr int kFxSmTile = 128 * 64, kFxNibTile = 128 * 32;
+constexpr int kFxCStage = 2 * kFxSmTile + 2 * kFxNibTile;  // 24 KB
+
+template <int BN, int STAGES, int FMT = 0>
 struct DecCfg {
   static constexpr int A_BYTES = kBM * kBK * 2;             // one 128 x 64 bf16 tile
   static constexpr int B_BYTES = BN * kBK * 2;              // one activation plane
   static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;   // two A tiles + hi/lo activations
   static constexpr int TMEM_COLS = 512;                     // 2 accumulator stages x 256 columns
   static constexpr int TAB_BYTES = (3 * kMaxExperts + 8) * 4;
-  static constexpr int DEC_TAB = ((1 << kPairBits) * 4 + 3 * (kCodecMaxLen + 1) * 4 + kCodecSymbols + 15) & ~15;
-  static constexpr int RING = kDecThreads_dec * kRingBytes;  // per-decoder-thread bitstream rings
-  static constexpr int SMEM = STAGES * STAGE + 1024 + 256 + TAB_BYTES + DEC_TAB + RING;
+  static constexpr int DEC_TAB =
+      FMT ? 0 : (((1 << kPairBits) * 4 + 3 * (kCodecMaxLen + 1) * 4 + kCodecSymbols + 15) & ~15);
+  static constexpr int RING = FMT ? 0 : kDecThreads_dec * kRingBytes;  // per-decoder-thread bitstream rings
+  static constexpr int CST = FMT ? ((STAGES >= 3 || STAGE >= 60 * 1024) ? 3 : 4) : 0;  // compressed stages (FX4)
+  static constexpr int BAR_OFF = STAGES * STAGE + CST * kFxCStage;       // barriers, then the tables
+  static constexpr int SMEM = BAR_OFF + 1024 + 256 + TAB_BYTES + DEC_TAB + RING;
   static_assert(SMEM <= 227 * 1024, "decode-GEMM stages exceed 227 KB");
 };
 
@@ -202,18 +212,21 @@ __device__ __forceinline__ DUnit dec_unit(int u, const int* s_up, const int* s_o
 }  // namespace
 
 template <bool GU, int BN, int STAGES, int FMT>
-__global__ void __maxnreg__(128)  // 448 threads x 128 registers (144 was refused at launch)
+__global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was refused at launch)
     k_moe_gemm_dec(const __grid_constant__ CUtensorMap map_b, GemmParams p, const DecTables* __restrict__ tabs,
                    int chunk) {
-  using C = DecCfg<BN, STAGES>;
+  using C = DecCfg<BN, STAGES, FMT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_1k(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE);
+  uint8_t* cstage = smem + STAGES * C::STAGE;  // FX4 compressed stages (CST of them)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  int* s_off = reinterpret_cast<int*>(smem + STAGES * C::STAGE + 256);
+  uint64_t* cfull = tempty + 2;  // FX4: compressed stage filled (TMA bytes)
+  uint64_t* cempty = cfull + 4;  // FX4: compressed stage read by all decoder warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 4);
+  int* s_off = reinterpret_cast<int*>(smem + C::BAR_OFF + 256);
   int* s_up = s_off + kMaxExperts + 1;
   int* s_flag = s_up + kMaxExperts + 1;
   uint32_t* s_pair = reinterpret_cast<uint32_t*>(s_off + 3 * kMaxExperts + 8);
@@ -221,7 +234,7 @@ __global__ void __maxnreg__(128)  // 448 threads x 128 registers (144 was refuse
   int* s_count = reinterpret_cast<int*>(s_first + kCodecMaxLen + 1);
   int* s_rank = s_count + kCodecMaxLen + 1;
   uint8_t* s_sym = reinterpret_cast<uint8_t*>(s_rank + kCodecMaxLen + 1);
-  uint8_t* s_ring = smem + STAGES * C::STAGE + 256 + C::TAB_BYTES + C::DEC_TAB;  // 16-byte aligned
+  uint8_t* s_ring = smem + C::BAR_OFF + 256 + C::TAB_BYTES + C::DEC_TAB;  // 16-byte aligned
 
   const int E = p.E;
   const int MT = GU ? (p.F + kBM - 1) / kBM : (p.H + kDecRows - 1) / kDecRows;
@@ -275,10 +288,11 @@ __global__ void __maxnreg__(128)  // 448 threads x 128 registers (144 was refuse
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
+    for (int c = 0; c < 4; ++c) { mbar_init(&cfull[c], 1); mbar_init(&cempty[c], kDecWarps); }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
-  if (warp >= 6) {  // decoder tables -> smem
+  if (FMT == 0 && warp >= 6 && warp < 6 + kDecWarps) {  // decoder tables -> smem
     const int t = threadIdx.x - 192;
     const uint4* src = reinterpret_cast<const uint4*>(tabs->pair);
     for (int i = t; i < (1 << kPairBits) / 4; i += 32 * kDecWarps) reinterpret_cast<uint4*>(s_pair)[i] = src[i];
@@ -413,14 +427,43 @@ __global__ void __maxnreg__(128)  // 448 threads x 128 registers (144 was refuse
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
+  } else if (warp == 6 + kDecWarps) {
+    // ---- FX4 compressed stages by TMA, on their own warp so they run CST stages ahead of the
+    // decoders instead of queueing behind the activation loads' wait for a free decoded stage
+    if (FMT == 1 && lane == 0) {
+      const uint64_t pol_w = policy_evict_first();  // compressed weights: streamed once
+      int cs = 0;
+      uint32_t cph = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const DUnit un = dec_unit(u, s_up, s_off, E, BN, S);
+        int kb0 = 0, kb1 = KB;
+        if (!GU) split_kb(un.split, S, KB, &kb0, &kb1);
+        const CUtensorMap* fxm = p.dec[un.e].maps;  // [sign/mantissa, nibbles]
+        const int r0 = GU ? un.m0 : 2 * un.m0, r1 = GU ? p.F + un.m0 : 2 * un.m0 + kBM;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          // the stage's compressed rows of both A tiles: 2 x 128 x 64 B of sign/mantissa bytes,
+          // 2 x 128 x 32 B of nibbles (swizzled 64 / 32 B so the decoders' row reads spread banks)
+          mbar_wait_backoff(&cempty[cs], cph ^ 1);
+          uint8_t* cb = cstage + cs * kFxCStage;
+          mbar_arrive_expect_tx(&cfull[cs], kFxCStage);
+          tma_load_2d(cb, fxm, &cfull[cs], kb * kBK, r0, pol_w);
+          tma_load_2d(cb + kFxSmTile, fxm, &cfull[cs], kb * kBK, r1, pol_w);
+          tma_load_2d(cb + 2 * kFxSmTile, fxm + 1, &cfull[cs], kb * (kBK / 2), r0, pol_w);
+          tma_load_2d(cb + 2 * kFxSmTile + kFxNibTile, fxm + 1, &cfull[cs], kb * (kBK / 2), r1, pol_w);
+          if (++cs == C::CST) { cs = 0; cph ^= 1; }
+        }
+      }
+    }
   } else {
     // ---- decoders: thread d owns weight row d of the unit
     const int d = threadIdx.x - 192;
     const int a = d >> 7, lr = d & 127;
     const uint32_t sw = (uint32_t)(lr & 7);
-    const CanonTabs ct{s_count, s_first, s_rank, s_sym, tabs->maxlen};
+    const CanonTabs ct{s_count, s_first, s_rank, s_sym, FMT == 0 ? tabs->maxlen : 0};
     int stage = 0;
     uint32_t phase = 0;
+    int fcs = 0;        // FX4: compressed stage
+    uint32_t fcph = 0;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
       const DUnit un = dec_unit(u, s_up, s_off, E, BN, S);
       int kb0 = 0, kb1 = KB;
@@ -499,35 +542,48 @@ __global__ void __maxnreg__(128)  // 448 threads x 128 registers (144 was refuse
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
       } else {
-      // FX4 records (fx4.cuh): nibble codes at fixed positions, so every pair decodes
-      // independently -- no window, no table chain; the stage's 64 sign/mantissa bytes and 32
-      // nibble bytes are loaded one stage ahead into registers that are reused in place
-      const uint8_t* smp = R.sm + v0;
-      const uint8_t* nbp = reinterpret_cast<const uint8_t*>(R.bits) + v0 / 2;
-      const uint8_t* smend = R.sm + (uint64_t)wrow * K + (uint64_t)kb1 * kBK;
+      // FX4 records (fx4.cuh): the TMA warp stages each stage's sign/mantissa and nibble rows
+      // in shared memory; a decoder thread reads its row there (6 x LDS.128), releases the
+      // compressed stage, and expands 8 quads -- nibble codes sit at fixed positions, so the
+      // pairs decode independently (no window, no table chain, no global load on the path)
       const uint8_t* escp = R.esc;
       const uint32_t bb = R.bit_base * 0x01010101u;
-      uint4 sv[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
-      uint4 nv[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
-      if (valid) {
-        const uint4* q4 = reinterpret_cast<const uint4*>(smp);
-#pragma unroll
-        for (int g = 0; g < 4; ++g) ldg_v4(sv[g], q4 + g);
-        ldg_v4(nv[0], reinterpret_cast<const uint4*>(nbp));
-        ldg_v4(nv[1], reinterpret_cast<const uint4*>(nbp) + 1);
-        escp = R.esc + R.index[v0 / kFxSeg];
-        smp += kBK;
-        nbp += kBK / 2;
-      }
+      if (valid) escp = R.esc + R.index[v0 / kFxSeg];
+      const uint32_t sm_row = (uint32_t)(a * kFxSmTile + lr * 64), sm_sw = (uint32_t)((lr >> 1) & 3);
+      const uint32_t nb_row = (uint32_t)(2 * kFxSmTile + a * kFxNibTile + lr * 32), nb_sw = (uint32_t)((lr >> 2) & 1);
       for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&cfull[fcs], fcph);
+        uint4 sv[4], nv[2];
+        const uint32_t cb = smem_u32(cstage + fcs * kFxCStage);
+        if (valid) {
+#pragma unroll
+          for (uint32_t g = 0; g < 4; ++g)
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(sv[g].x), "=r"(sv[g].y), "=r"(sv[g].z), "=r"(sv[g].w)
+                         : "r"(cb + sm_row + ((g ^ sm_sw) << 4))
+                         : "memory");
+#pragma unroll
+          for (uint32_t g = 0; g < 2; ++g)
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(nv[g].x), "=r"(nv[g].y), "=r"(nv[g].z), "=r"(nv[g].w)
+                         : "r"(cb + nb_row + ((g ^ nb_sw) << 4))
+                         : "memory");
+          // the slot may be refilled by the TMA as soon as every warp arrives: make this thread's
+          // reads complete (a use of every loaded register) and order them before the async proxy's
+          // next write (without this the producer warp, running CST stages ahead, overwrote rows
+          // still being read: wrong results at T = 256)
+          const uint32_t all = sv[0].x ^ sv[0].y ^ sv[0].z ^ sv[0].w ^ sv[1].x ^ sv[1].y ^ sv[1].z ^ sv[1].w ^ sv[2].x ^
+                               sv[2].y ^ sv[2].z ^ sv[2].w ^ sv[3].x ^ sv[3].y ^ sv[3].z ^ sv[3].w ^ nv[0].x ^ nv[0].y ^
+                               nv[0].z ^ nv[0].w ^ nv[1].x ^ nv[1].y ^ nv[1].z ^ nv[1].w;
+          asm volatile("" ::"r"(all));
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&cempty[fcs]);
+        if (++fcs == C::CST) { fcs = 0; fcph ^= 1; }
         mbar_wait_backoff(&empty[stage], phase ^ 1);
         if (valid) {
-          if (smp + 128 < smend) {
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(smp + 128));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(nbp + 64));
-          }
           const uint32_t row = smem_u32(smem + stage * C::STAGE + a * C::A_BYTES + lr * 128);
-          const bool more = smp < smend;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const uint4& nq = nv[q >> 2];
@@ -555,11 +611,7 @@ __global__ void __maxnreg__(128)  // 448 threads x 128 registers (144 was refuse
                 }
             }
             st_smem_v4(row + ((((uint32_t)q) ^ sw) << 4), o[0], o[1], o[2], o[3]);
-            if ((q & 1) && more) ldg_v4(sv[q >> 1], reinterpret_cast<const uint4*>(smp) + (q >> 1));
-            if ((q & 3) == 3 && more) ldg_v4(nv[q >> 2], reinterpret_cast<const uint4*>(nbp) + (q >> 2));
           }
-          smp += kBK;
-          nbp += kBK / 2;
           fence_async_smem();
         }
         __syncwarp();
@@ -585,7 +637,8 @@ using DecKernel = void (*)(const CUtensorMap, GemmParams, const DecTables*, int)
 template <bool GU, int BN, int ST>
 static void set_dec_attr() {
   cudaFuncSetAttribute(k_moe_gemm_dec<GU, BN, ST, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, DecCfg<BN, ST>::SMEM);
-  cudaFuncSetAttribute(k_moe_gemm_dec<GU, BN, ST, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, DecCfg<BN, ST>::SMEM);
+  cudaFuncSetAttribute(k_moe_gemm_dec<GU, BN, ST, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       DecCfg<BN, ST, 1>::SMEM);
 }
 
 void set_gemm_dec_attrs() {
@@ -609,14 +662,14 @@ void launch_gemm_dec(bool gate_up, const CUtensorMap& map_b, const GemmParams& p
   if (bn == BN) {                                                                                        \
     kern = fx4 ? (gate_up ? k_moe_gemm_dec<true, BN, ST, 1> : k_moe_gemm_dec<false, BN, ST, 1>)           \
                : (gate_up ? k_moe_gemm_dec<true, BN, ST, 0> : k_moe_gemm_dec<false, BN, ST, 0>);          \
-    smem = DecCfg<BN, ST>::SMEM;                                                                         \
+    smem = fx4 ? DecCfg<BN, ST, 1>::SMEM : DecCfg<BN, ST>::SMEM;                                         \
   }
   XPGB_DEC_TILES(XPGB_PICK_DEC)
 #undef XPGB_PICK_DEC
   if (!kern) {
     kern = fx4 ? (gate_up ? k_moe_gemm_dec<true, 128, 2, 1> : k_moe_gemm_dec<false, 128, 2, 1>)
                : (gate_up ? k_moe_gemm_dec<true, 128, 2, 0> : k_moe_gemm_dec<false, 128, 2, 0>);
-    smem = DecCfg<128, 2>::SMEM;
+    smem = fx4 ? DecCfg<128, 2, 1>::SMEM : DecCfg<128, 2>::SMEM;
   }
   kern<<<grid, kDecThreads, smem, s>>>(map_b, p, tabs, chunk);
   note_launch();

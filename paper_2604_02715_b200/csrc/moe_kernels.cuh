@@ -69,6 +69,7 @@ struct DecRec {
   uint32_t bit_base;
   uint32_t fmt;  // 0 exponent-Huffman, 1 FX4
   const uint8_t* esc;
+  const CUtensorMap* maps;  // FX4: 2-D maps of the sign/mantissa plane [rows][K] and nibbles [rows][K/2]
 };
 
 // Arguments of one grouped-GEMM launch (gate/up or down) of one layer.

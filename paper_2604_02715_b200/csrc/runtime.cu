@@ -105,6 +105,22 @@ static CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint
   return m;
 }
 
+// Row-major bytes [rows][cols] -> box {box_cols, 128 rows} (FX4 planes of the device tier).
+static CUtensorMap make_map_u8(const void* base, uint64_t rows, uint64_t cols, uint32_t box_cols,
+                               CUtensorMapSwizzle swz) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols};
+  cuuint32_t box[2] = {box_cols, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) XFAIL(XPGB_ERR_CUDA, "cuTensorMapEncodeTiled (u8) failed (%d) rows=%llu cols=%llu", (int)r,
+                               (unsigned long long)rows, (unsigned long long)cols);
+  return m;
+}
+
 // --------------------------------------------------------------------------- small kernels
 
 struct PtOp {
@@ -283,6 +299,7 @@ struct Ctx {
   bool poison = false;
   int war_sab_it = 0, war_sab_layer = 0;
   DecRec* d_decrec = nullptr;  // [N][2][E]: record of each device-tier tensor (sm == nullptr: not device tier)
+  CUtensorMap* d_fxmaps = nullptr;  // [N*E*2][2]: FX4 sign/mantissa and nibble planes as TMA maps
   // device-tier record format: 0 exponent-Huffman (the host pool's records, staged as they are),
   // 1 FX4 (fx4.cuh: encoded on the GPU from the raw pool at staging, for decode-into-GEMM)
   int dev_fmt = 0;
@@ -344,6 +361,8 @@ static void free_pools(Ctx* c) {
   if (c->dev_tier) cudaFree(c->dev_tier);
   if (c->d_decrec) cudaFree(c->d_decrec);
   c->d_decrec = nullptr;
+  if (c->d_fxmaps) cudaFree(c->d_fxmaps);
+  c->d_fxmaps = nullptr;
   c->arena = nullptr;
   c->d_pt = nullptr;
   c->dev_tier = nullptr;
@@ -1504,6 +1523,19 @@ static void stage_device_tier_fx4(Ctx* c) {
   CK(cudaStreamSynchronize(s));
   cudaFree(raw);
   cudaFree(scratch);
+  // TMA maps of every FX4 tensor's planes: the decode-into-GEMM kernel stages a stage's rows of
+  // sign/mantissa bytes and nibbles with them (64-B / 32-B swizzles, decoder reads spread banks)
+  std::vector<CUtensorMap> maps(nt * 2);
+  for (size_t ti = 0; ti < nt; ++ti) {
+    if (!c->backend[ti]) continue;
+    const uint64_t rows = (ti & 1) ? (uint64_t)c->H : 2ull * c->F, K = (ti & 1) ? (uint64_t)c->F : (uint64_t)c->H;
+    const uint8_t* rec = c->dev_tier + c->dev_off[ti];
+    const FxLayout L = fx_layout(rows * K, 0);
+    maps[2 * ti] = make_map_u8(rec, rows, K, 64, CU_TENSOR_MAP_SWIZZLE_64B);
+    maps[2 * ti + 1] = make_map_u8(rec + L.nib, rows, K / 2, 32, CU_TENSOR_MAP_SWIZZLE_32B);
+  }
+  CK(cudaMalloc(&c->d_fxmaps, maps.size() * sizeof(CUtensorMap)));
+  CK(cudaMemcpy(c->d_fxmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
   std::vector<DecRec> recs(nt / 2 * 2);
   memset(recs.data(), 0, recs.size() * sizeof(DecRec));
   for (size_t ti = 0; ti < nt; ++ti) {
@@ -1514,7 +1546,7 @@ static void stage_device_tier_fx4(Ctx* c) {
     const size_t layer0 = ti / 2 / c->E, e = ti / 2 % c->E, k = ti & 1;
     recs[(layer0 * 2 + k) * c->E + e] =
         DecRec{rec, reinterpret_cast<const uint32_t*>(rec + L.nib), reinterpret_cast<const uint32_t*>(rec + L.idx),
-               (uint32_t)c->fx_base[ti], 1u, rec + L.esc};
+               (uint32_t)c->fx_base[ti], 1u, rec + L.esc, c->d_fxmaps + 2 * ti};
   }
   CK(cudaMalloc(&c->d_decrec, recs.size() * sizeof(DecRec)));
   CK(cudaMemcpy(c->d_decrec, recs.data(), recs.size() * sizeof(DecRec), cudaMemcpyHostToDevice));
@@ -1528,6 +1560,10 @@ static void stage_device_tier(Ctx* c) {
   if (c->d_decrec) {
     cudaFree(c->d_decrec);
     c->d_decrec = nullptr;
+  }
+  if (c->d_fxmaps) {
+    cudaFree(c->d_fxmaps);
+    c->d_fxmaps = nullptr;
   }
   const size_t pages = (size_t)c->N * c->E;
   auto tensor_bytes = [&](size_t ti) -> uint64_t {
@@ -1568,7 +1604,7 @@ static void stage_device_tier(Ctx* c) {
       const size_t layer0 = ti / 2 / c->E, e = ti / 2 % c->E, k = ti & 1;
       recs[(layer0 * 2 + k) * c->E + e] = DecRec{rec, reinterpret_cast<const uint32_t*>(rec + sm16),
                                                  reinterpret_cast<const uint32_t*>(rec + sm16 + bits16), 0u, 0u,
-                                                 nullptr};
+                                                 nullptr, nullptr};
     }
     if (c->d_decrec) cudaFree(c->d_decrec);
     CK(cudaMalloc(&c->d_decrec, recs.size() * sizeof(DecRec)));
