@@ -599,7 +599,8 @@ def main():
             ceb = runner.device_tier_bytes(Lc) / (Nl * Lc) * 1.002  # compressed expert (+ margin)
             plan = plan_tiers(Nl, Lc, eb, ceb, cap + shared_b + overhead, shared_bytes=shared_b,
                               overhead_bytes=overhead, device_format=args.device_format,
-                              fx4_ceb=fx4_expert_bytes(cspec.hidden_dim, cspec.intermediate_dim) * 1.002)
+                              fx4_ceb=fx4_expert_bytes(cspec.hidden_dim, cspec.intermediate_dim) * 1.002,
+                              units_per_expert=cspec.intermediate_dim // 128)
             if plan.device_experts or plan.pinned_experts:
                 runner.apply_plan(plan)
                 ring_blocks = min(plan.ring, ring_blocks) if plan.ring else ring_blocks

@@ -144,6 +144,11 @@ def cmd_calibrate(args) -> int:
     runner.set_device_experts([spec.experts_per_layer] * spec.num_layers)
     runner.run(1, acts=x)
     rep_dev = runner.run(3, acts=x)
+    # the FX4 device tier read in place by the decode-into-GEMM kernel (GEMM included)
+    runner.set_device_format("fx4", fused_decode=True)
+    runner.run(1, acts=x)
+    rep_fx4 = runner.run(3, acts=x)
+    runner.set_device_format("huffman", fused_decode=False)
     runner.set_device_experts([0] * spec.num_layers)
     del runner
     model = ResidentModel(spec, container, max_tokens=args.tokens)
@@ -156,17 +161,20 @@ def cmd_calibrate(args) -> int:
     tau_resident = e0.elapsed_time(e1) * 1e-3 / 3
     sm_time = rep_dev.elapsed_seconds / 3 - tau_resident
     b_dec_pipeline = spec.total_bytes / sm_time if sm_time > 0 else float("inf")
+    b_fx4_fused = 3 * spec.total_bytes / rep_fx4.elapsed_seconds if rep_fx4.elapsed_seconds > 0 else float("inf")
     n, p_layer = spec.num_layers, spec.layer_bytes
     knee = min(1.0, max(0.0, 1.0 - tau_resident * b_host / (n * p_layer)))
     from .exponent_codec import CompressedModel
 
     ratio = CompressedModel.from_container(container, pin=False).ratio
     doc = {"model": args.model, "tokens": args.tokens, "top_k": args.top_k,
-           "b_host": b_host, "b_dev": b_dev, "b_dec_pipeline": b_dec_pipeline, "tau_comp_theory": tau_resident,
+           "b_host": b_host, "b_dev": b_dev, "b_dec_pipeline": b_dec_pipeline, "b_fx4_fused": b_fx4_fused,
+           "tau_comp_theory": tau_resident,
            "tau_comp_paged_run": tau_comp / 2, "tau_load_paged_run": tau_load / 2,
            "compression_ratio": ratio, "knee_alpha": knee,
            "note": "b_host/b_dev in raw-equivalent B/s (b_dev: the decoder alone; b_dec_pipeline: device-tier-only "
-                   "paged stack, raw bytes over the step time beyond resident compute); tau per decode iteration "
+                   "paged stack, raw bytes over the step time beyond resident compute; b_fx4_fused: the FX4 device tier read in "
+                   "place by the decode-into-GEMM kernel, raw bytes per second of step); tau per decode iteration "
                    "(N layers); knee per simulate.knee_alpha with the measured b_host and resident tau"}
     text = json.dumps(doc, indent=2)
     if getattr(args, "out", None):

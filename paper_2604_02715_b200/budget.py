@@ -204,7 +204,8 @@ def fx4_expert_bytes(H: int, F: int) -> float:
 def plan_tiers(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *, fx4_ceb: float | None = None,
                shared_bytes: float = 0.0, overhead_bytes: float = 0.0, b_link: float = 54e9,
                b_dec: float = B_DEC_HUFFMAN, b_fx4: float = B_FUSED_FX4, b_resident: float = B_RESIDENT,
-               device_format: str = "auto", **kw) -> ResidencyPlan:
+               device_format: str = "auto", units_per_expert: int = 0, num_sms: int = 148,
+               **kw) -> ResidencyPlan:
     """Plan the budget with the device tier in exponent-Huffman records (decoded into the ring)
     and, when fx4_ceb is given, in FX4 records read in place by the decode-into-GEMM kernel;
     return the plan whose modelled step is shorter, tagged with ``device_format`` and ``fused``.
@@ -222,11 +223,24 @@ def plan_tiers(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *, fx
         p.device_format, p.fused = "huffman", False
         cands.append(p)
     if fx4_ceb and device_format in ("auto", "fx4"):
-        p = plan_residency(N, L, eb, ceb, budget_bytes, shared_bytes=shared_bytes, overhead_bytes=overhead_bytes,
-                           b_link=b_link, b_dec=b_dec, t_compute=t_res, dev_ceb=fx4_ceb, b_dev=b_fx4,
-                           dev_fused=True, **kw)
-        p.device_format, p.fused = "fx4", True
-        cands.append(p)
+        # the fused GEMM of a window has (experts per window) x units_per_expert units of work
+        # (gate/up: F / 128 weight-row tiles); a window of fewer units than SMs leaves SMs idle
+        # (DSv3's 2-expert windows: 32 units -> 8.6 K tok/s at 80% instead of the planned 33 K),
+        # so FX4 plans also try windows wide enough to fill the GPU, at the rate the width allows
+        widths = [kw.get("window")]
+        if units_per_expert and not kw.get("window"):
+            widths.append(max(1, min(L, -(-num_sms // units_per_expert))))
+        for w in widths:
+            fill = min(1.0, (w or 1) * units_per_expert / num_sms) if units_per_expert else 1.0
+            kww = dict(kw, window=w)
+            try:
+                p = plan_residency(N, L, eb, ceb, budget_bytes, shared_bytes=shared_bytes,
+                                   overhead_bytes=overhead_bytes, b_link=b_link, b_dec=b_dec, t_compute=t_res,
+                                   dev_ceb=fx4_ceb, b_dev=b_fx4 * fill, dev_fused=True, **kww)
+            except ValueError:
+                continue
+            p.device_format, p.fused, p.fx4_rate = "fx4", True, b_fx4 * fill
+            cands.append(p)
 
     def score(p):
         total = N * L
@@ -234,7 +248,7 @@ def plan_tiers(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *, fx
         host = total - d - pin
         link = p.link_bytes / b_link
         if p.fused:
-            sm = host * eb / b_dec + d * eb / b_fx4 + t_res * (total - d) / total
+            sm = host * eb / b_dec + d * eb / p.fx4_rate + t_res * (total - d) / total
         else:
             sm = (host + d) * eb / b_dec + t_res
         return max(link, sm)

@@ -40,10 +40,12 @@ def main():
         dev, pin = float(p.get("device_tier_per_layer", 0)), float(p.get("pinned_per_layer", 0))
         ref = S.predict_tiered(c, dev, pin)
         b_dec = args.b_dec * 1e9 if args.b_dec else cal.get("b_dec_pipeline")
-        ours = S.predict_sm_shared(c, dev, pin, b_dec=b_dec,
-                                   b_fused=args.b_fused * 1e9 if args.b_fused else None)
+        fused = p.get("device_format") == "fx4" and p.get("fused_decode")
+        b_fused = (args.b_fused * 1e9 if args.b_fused else cal.get("b_fx4_fused")) if fused else None
+        ours = S.predict_sm_shared(c, dev, pin, b_dec=b_dec, b_fused=b_fused)
         meas = float(p["tok_s"])
-        row = {"budget": p.get("budget"), "device_per_layer": dev, "pinned_per_layer": pin, "measured_tok_s": meas,
+        row = {"budget": p.get("budget"), "device_format": p.get("device_format", "huffman"),
+               "device_per_layer": dev, "pinned_per_layer": pin, "measured_tok_s": meas,
                "reference_model_tok_s": ref["tok_s"], "reference_model_err": ref["tok_s"] / meas - 1,
                "sm_shared_model_tok_s": ours["tok_s"], "sm_shared_model_err": ours["tok_s"] / meas - 1,
                "sm_shared_bound": ours["bound"]}
@@ -51,7 +53,8 @@ def main():
         worst["sm_shared_model"] = max(worst["sm_shared_model"], abs(row["sm_shared_model_err"]))
         print(json.dumps(row))
     print(json.dumps({"summary": "max |relative error| over the sweep", **worst,
-                      "inputs": {k: cal[k] for k in ("b_host", "b_dev", "b_dec_pipeline", "tau_comp_theory") if k in cal}}))
+                      "inputs": {k: cal[k] for k in ("b_host", "b_dev", "b_dec_pipeline", "b_fx4_fused", "tau_comp_theory")
+                                 if k in cal}}))
 
 
 if __name__ == "__main__":

@@ -101,6 +101,7 @@ def main():
             b = p if what == "plan" else args.budget
             plan = plan_tiers(N, Lc, spec.expert_bytes, ceb, b * budget_base, shared_bytes=shared_b,
                               fx4_ceb=fx4_expert_bytes(spec.hidden_dim, spec.intermediate_dim) * 1.002,
+                              units_per_expert=spec.intermediate_dim // 128,
                               device_format=args.device_format,
                               overhead_bytes=runner.ctx.hbm_bytes()["staging"], depth=args.depth, window=args.window,
                               **({"b_dec": args.b_dec * 1e9} if args.b_dec else {}))
