@@ -568,19 +568,7 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
                          : "=r"(nv[g].x), "=r"(nv[g].y), "=r"(nv[g].z), "=r"(nv[g].w)
                          : "r"(cb + nb_row + ((g ^ nb_sw) << 4))
                          : "memory");
-          // the slot may be refilled by the TMA as soon as every warp arrives: make this thread's
-          // reads complete (a use of every loaded register) and order them before the async proxy's
-          // next write (without this the producer warp, running CST stages ahead, overwrote rows
-          // still being read: wrong results at T = 256)
-          const uint32_t all = sv[0].x ^ sv[0].y ^ sv[0].z ^ sv[0].w ^ sv[1].x ^ sv[1].y ^ sv[1].z ^ sv[1].w ^ sv[2].x ^
-                               sv[2].y ^ sv[2].z ^ sv[2].w ^ sv[3].x ^ sv[3].y ^ sv[3].z ^ sv[3].w ^ nv[0].x ^ nv[0].y ^
-                               nv[0].z ^ nv[0].w ^ nv[1].x ^ nv[1].y ^ nv[1].z ^ nv[1].w;
-          asm volatile("" ::"r"(all));
         }
-        fence_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&cempty[fcs]);
-        if (++fcs == C::CST) { fcs = 0; fcph ^= 1; }
         mbar_wait_backoff(&empty[stage], phase ^ 1);
         if (valid) {
           const uint32_t row = smem_u32(smem + stage * C::STAGE + a * C::A_BYTES + lr * 128);
@@ -601,21 +589,31 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
               const uint32_t dup = __byte_perm(j < 2 ? sa : sb, 0, (j & 1) ? 0x3322u : 0x1100u);
               o[j] = (dup & 0x807F807Fu) | (ex & 0x7F807F80u);
             }
-            if (__builtin_expect(escf != 0u, 0)) {  // exponents outside the window, in value order
-#pragma unroll
-              for (int v = 0; v < 8; ++v)
+            const uint32_t qa = row + ((((uint32_t)q) ^ sw) << 4);
+            st_smem_v4(qa, o[0], o[1], o[2], o[3]);
+            if (__builtin_expect(escf != 0u, 0)) {
+              // exponents outside the window, in value order: rewrite those values in place
+#pragma unroll 1
+              for (uint32_t v = 0; v < 8; ++v)
                 if (((nw >> (4 * v)) & 15u) == 15u) {
-                  const uint32_t ex = (uint32_t)*escp++;
-                  const int sh = 16 * (v & 1) + 7;
-                  o[v >> 1] = (o[v >> 1] & ~(0xFFu << sh)) | (ex << sh);
+                  const uint32_t sbyte = ((v < 4 ? sa : sb) >> (8 * (v & 3))) & 0xFFu;
+                  const uint32_t bf = ((sbyte & 0x80u) << 8) | ((uint32_t)*escp++ << 7) | (sbyte & 0x7Fu);
+                  asm volatile("st.shared.u16 [%0], %1;" ::"r"(qa + 2 * v), "h"((unsigned short)bf) : "memory");
                 }
             }
-            st_smem_v4(row + ((((uint32_t)q) ^ sw) << 4), o[0], o[1], o[2], o[3]);
           }
-          fence_async_smem();
         }
+        // one fence for both hand-offs: the A tile's generic stores before the tensor cores'
+        // reads, and this stage's compressed-row reads (consumed above, so complete) before the
+        // producer's next TMA write into the slot (releasing the slot before the decode let the
+        // producer, CST stages ahead, overwrite rows still being read: wrong results at T = 256)
+        fence_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&full[stage]);
+        if (lane == 0) {
+          mbar_arrive(&full[stage]);
+          mbar_arrive(&cempty[fcs]);
+        }
+        if (++fcs == C::CST) { fcs = 0; fcph ^= 1; }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
       }
