@@ -278,6 +278,11 @@ int xpgb_set_fused_decode(xpgb_ctx* ctx, int32_t mode);
  * bandwidth of its compressed bytes.  Lossless either way.  Re-stages the device tier; no
  * session may be active. */
 int xpgb_set_device_format(xpgb_ctx* ctx, int32_t fmt);
+/* Staging ring and device-resident chunk index of the compressed host tier: 1 allocates them
+ * (the default once xpgb_set_codec(host_compressed = 1) ran), 0 releases them when the placement
+ * leaves no tensor on the host tier (a budget plan that keeps every streamed expert on the device
+ * tier gives that HBM back); a host-tier record streamed without them fails loudly. */
+int xpgb_set_host_staging(xpgb_ctx* ctx, int32_t on);
 /* Race hardening (debug; no reference counterpart -- the reference's sabotage control,
  * pipeline.py:369-370, covers RAW only).  poison != 0: every ring block a window maps is filled
  * with 0xFF bytes (bf16 NaN) on the copy stream before its load, so a GEMM that reads a block

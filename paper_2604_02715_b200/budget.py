@@ -46,6 +46,10 @@ class ResidencyPlan:
     def pinned_experts(self) -> int:
         return int(self.pinned_mask.sum())
 
+    @property
+    def host_experts(self) -> int:
+        return int(self.device_mask.size - self.device_mask.sum() - self.pinned_mask.sum())
+
 
 def _fill(total: int, caps) -> list:
     """`total` items over slots of capacity `caps`, as even as the capacities allow."""
@@ -97,9 +101,10 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
     """Choose (ring, device tier, pinned) for N layers x L experts under `budget_bytes`.
 
     eb: raw bytes of one expert (both tensors); ceb: its compressed record bytes.
-    overhead_bytes: HBM the codec holds whatever the plan (staging buffers, the device-resident
-    chunk index of the host records): counted inside ``budget_bytes`` like the shared experts,
-    so the plan's whole expert footprint stays within the budget.
+    overhead_bytes: HBM the codec holds for host-tier records (staging buffers, the device-resident
+    chunk index): counted inside ``budget_bytes`` like the shared experts, so the plan's whole
+    expert footprint stays within the budget -- unless the plan leaves no expert on the host
+    tier, which releases them (``ResidencyPlan.host_experts == 0``).
     Step model: max(link_bytes / b_link, decoded_raw_bytes / b_dec + t_compute).
     dev_ceb / b_dev: HBM bytes and raw-equivalent rate of a device-tier expert when the device
     tier uses another record format than the host tier (FX4: larger records, faster decode);
@@ -143,6 +148,10 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
         else:
             ring = depth * min(w_min, streamed_max)
         room = cap - ring * eb - p * eb
+        # with every streamed expert on the device tier nothing crosses the link, and the
+        # codec's staging buffers and host chunk index (overhead_bytes) are released
+        if (total - p) * dceb <= room + overhead_bytes:
+            room = max(room, (total - p) * dceb)
         if room < 0:
             continue
         d = int(min(total - p, room // dceb))
@@ -178,7 +187,7 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
     for l in range(N):
         streamed = L - p_layer[l]
         device[l, :streamed] = _spread_row(streamed, d_layer[l], w)
-    hbm = ring * eb + p * eb + device.sum() * dceb + shared_bytes + overhead_bytes
+    hbm = ring * eb + p * eb + device.sum() * dceb + shared_bytes + (overhead_bytes if total - p - d else 0.0)
     return ResidencyPlan(ring, device, pinned, float(hbm), float(est), float(link), depth, float((total - p) * eb))
 
 

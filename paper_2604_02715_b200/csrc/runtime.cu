@@ -1612,43 +1612,11 @@ static void stage_device_tier(Ctx* c) {
   }
 }
 
-static void set_codec(Ctx* c, const void* pool, uint64_t pool_bytes, const uint64_t* rec_offsets,
-                      const uint64_t* bits_lens, const uint8_t* lengths, int chunk, bool host_compressed) {
-  if (chunk <= 0 || chunk % 8) XFAIL(XPGB_ERR_CONFIG, "codec chunk must be a positive multiple of 8");
-  uint32_t codes[kCodecSymbols];
-  if (!codec_canonical_codes(lengths, codes)) XFAIL(XPGB_ERR_CONFIG, "invalid code lengths");
+// Staging ring and device-resident chunk index of the compressed host tier (on), or neither
+// (off: a plan that leaves no expert on the host tier gives their HBM back to the budget).
+static void alloc_host_staging(Ctx* c, bool host_compressed) {
   const size_t nt = (size_t)c->N * c->E * 2;
-  CK(cudaDeviceSynchronize());
-  c->cpool = static_cast<const uint8_t*>(pool);
-  c->cpool_bytes = pool_bytes;
-  c->rec_off.assign(rec_offsets, rec_offsets + nt);
-  c->rec_bits.assign(bits_lens, bits_lens + nt);
-  memcpy(c->ctab.len, lengths, kCodecSymbols);
-  prepare_decode_tables(c->ctab, nullptr);  // decoder tables built once, before any decode stream uses them
-  CKLAUNCH();
-  c->cchunk = chunk;
-  c->codec = true;
-  c->host_codec = host_compressed;
-  for (size_t ti = 0; ti < nt; ++ti) {
-    const uint64_t rb = xpgb_codec_record_bytes(((ti & 1) ? c->s2 : c->s1) / 2, c->rec_bits[ti], chunk);
-    if (c->rec_off[ti] + rb > pool_bytes) XFAIL(XPGB_ERR_CONTAINER_FORMAT, "record %zu outside the packed pool", ti);
-  }
-  if (!c->codec_events) {
-    for (int k = 0; k < 2; ++k) {
-      CK(cudaStreamCreateWithFlags(&c->s_dec[k], cudaStreamNonBlocking));
-      CK(cudaStreamCreateWithFlags(&c->s_alt[k], cudaStreamNonBlocking));
-      CK(cudaStreamCreateWithFlags(&c->s_cp[k], cudaStreamNonBlocking));
-      CK(cudaStreamCreateWithFlags(&c->s_devdec[k], cudaStreamNonBlocking));
-      CK(cudaEventCreateWithFlags(&c->ev_devdec[k], cudaEventDisableTiming));
-      for (int b = 0; b < kMaxStageBufs; ++b) {
-        CK(cudaEventCreateWithFlags(&c->ev_copied[k][b], cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&c->ev_decoded[k][b], cudaEventDisableTiming));
-      }
-      CK(cudaEventCreateWithFlags(&c->ev_mapped[k], cudaEventDisableTiming));
-      CK(cudaEventCreateWithFlags(&c->ev_raw[k], cudaEventDisableTiming));
-    }
-    c->codec_events = true;
-  }
+  const int chunk = c->cchunk;
   // staging: n_stage buffers per kind, each min(largest record, kStagePieceBytes) + alignment slack
   if (const char* env = getenv("XPGB_STAGE_BUFS")) c->n_stage = std::max(2, std::min(kMaxStageBufs, atoi(env)));
   for (int k = 0; k < 2; ++k) {
@@ -1695,6 +1663,46 @@ static void set_codec(Ctx* c, const void* pool, uint64_t pool_bytes, const uint6
                     ((n + chunk - 1) / chunk) * 4, cudaMemcpyHostToDevice));
     }
   }
+}
+
+static void set_codec(Ctx* c, const void* pool, uint64_t pool_bytes, const uint64_t* rec_offsets,
+                      const uint64_t* bits_lens, const uint8_t* lengths, int chunk, bool host_compressed) {
+  if (chunk <= 0 || chunk % 8) XFAIL(XPGB_ERR_CONFIG, "codec chunk must be a positive multiple of 8");
+  uint32_t codes[kCodecSymbols];
+  if (!codec_canonical_codes(lengths, codes)) XFAIL(XPGB_ERR_CONFIG, "invalid code lengths");
+  const size_t nt = (size_t)c->N * c->E * 2;
+  CK(cudaDeviceSynchronize());
+  c->cpool = static_cast<const uint8_t*>(pool);
+  c->cpool_bytes = pool_bytes;
+  c->rec_off.assign(rec_offsets, rec_offsets + nt);
+  c->rec_bits.assign(bits_lens, bits_lens + nt);
+  memcpy(c->ctab.len, lengths, kCodecSymbols);
+  prepare_decode_tables(c->ctab, nullptr);  // decoder tables built once, before any decode stream uses them
+  CKLAUNCH();
+  c->cchunk = chunk;
+  c->codec = true;
+  c->host_codec = host_compressed;
+  for (size_t ti = 0; ti < nt; ++ti) {
+    const uint64_t rb = xpgb_codec_record_bytes(((ti & 1) ? c->s2 : c->s1) / 2, c->rec_bits[ti], chunk);
+    if (c->rec_off[ti] + rb > pool_bytes) XFAIL(XPGB_ERR_CONTAINER_FORMAT, "record %zu outside the packed pool", ti);
+  }
+  if (!c->codec_events) {
+    for (int k = 0; k < 2; ++k) {
+      CK(cudaStreamCreateWithFlags(&c->s_dec[k], cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&c->s_alt[k], cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&c->s_cp[k], cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&c->s_devdec[k], cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&c->ev_devdec[k], cudaEventDisableTiming));
+      for (int b = 0; b < kMaxStageBufs; ++b) {
+        CK(cudaEventCreateWithFlags(&c->ev_copied[k][b], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_decoded[k][b], cudaEventDisableTiming));
+      }
+      CK(cudaEventCreateWithFlags(&c->ev_mapped[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_raw[k], cudaEventDisableTiming));
+    }
+    c->codec_events = true;
+  }
+  alloc_host_staging(c, host_compressed);
   stage_device_tier(c);
 }
 
@@ -2363,6 +2371,21 @@ int xpgb_set_hazard_checks(xpgb_ctx* h, int32_t poison, int32_t skip_war_iterati
     c->poison = poison != 0;
     c->war_sab_it = skip_war_iteration;
     c->war_sab_layer = skip_war_layer;
+  });
+}
+
+int xpgb_set_host_staging(xpgb_ctx* h, int32_t on) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    if (c->sess && c->sess->active) XFAIL(XPGB_ERR, "cannot change the host staging during a session");
+    if (!c->codec || !c->host_codec) XFAIL(XPGB_ERR_CONFIG, "no compressed host tier");
+    const size_t nt = (size_t)c->N * c->E * 2;
+    if (!on)
+      for (size_t ti = 0; ti < nt; ++ti)
+        if (!c->backend[ti] && !c->pinned[ti / 2])
+          XFAIL(XPGB_ERR_CONFIG, "tensor %zu is on the host tier: its records need the staging ring", ti);
+    CK(cudaDeviceSynchronize());
+    alloc_host_staging(c, on != 0);  // released: a host-tier record would fail loudly in materialize
   });
 }
 

@@ -163,6 +163,10 @@ class Context:
         call("xpgb_set_device_format", self._h, 1 if fmt == "fx4" else 0)
         self._dev_fmt = fmt
 
+    def set_host_staging(self, on: bool) -> None:
+        """Allocate / release the compressed host tier's staging ring and chunk index."""
+        call("xpgb_set_host_staging", self._h, 1 if on else 0)
+
     def set_fused_decode(self, on: bool) -> None:
         """Decode-into-GEMM for the builtin compute: device-tier experts read in place."""
         call("xpgb_set_fused_decode", self._h, 1 if on else 0)

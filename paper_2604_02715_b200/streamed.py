@@ -347,6 +347,10 @@ class StreamedRunner:
         sub = 0 < plan.ring and (plan.ring < 2 * streamed or depth != 2)
         self.ctx.apply_residency(full, int(plan.ring) if sub else 0, depth)
         self.set_device_mask(plan.device_mask)
+        if self.host_codec:
+            # no expert left on the host tier: the staging ring and chunk index go back to the budget
+            host = int(plan.device_mask.size - plan.device_mask.sum() - plan.pinned_mask.sum())
+            self.ctx.set_host_staging(host > 0)
 
     def set_device_experts(self, m_layers) -> None:
         """Placement: experts 1..m_l of layer l on the compressed device tier, the rest on the

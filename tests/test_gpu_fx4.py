@@ -103,3 +103,37 @@ def test_fx4_full_shape_fused_equals_resident(X):
     model = X.ResidentModel(spec, container, max_tokens=T)
     y, _ = model.run(2, fwd, x.clone())
     assert paged.tobytes() == y.cpu().numpy().tobytes()
+
+
+def test_host_staging_released_when_no_host_tier(X):
+    """A plan that leaves no expert on the host tier gives the staging ring and the chunk index
+    back (xpgb_set_host_staging); streaming a host record without them fails loudly."""
+    from paper_2604_02715_b200.budget import fx4_expert_bytes, plan_tiers
+    from paper_2604_02715_b200.errors import XpgError
+
+    spec = X.ModelSpec(4, 8, 256, 512)
+    fwd = X.ForwardSpec(16, 2, 7)
+    container = X.generate_synthetic_model(spec, 7)
+    backends = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 30e9, 1 << 40)]
+    hier = X.StorageHierarchy(container, None, X.plan_placement(spec, backends), backends)
+    runner = X.StreamedRunner(spec, hier, fwd, host_codec=True)
+    overhead = runner.ctx.hbm_bytes()["staging"]
+    assert overhead > 0
+    L, N = spec.experts_per_layer, spec.num_layers
+    ceb = runner.device_tier_bytes(L) / (N * L) * 1.002
+    plan = plan_tiers(N, L, spec.expert_bytes, ceb, 0.95 * spec.total_bytes, overhead_bytes=overhead,
+                      fx4_ceb=fx4_expert_bytes(spec.hidden_dim, spec.intermediate_dim) * 1.002,
+                      units_per_expert=spec.intermediate_dim // 128)
+    assert plan.host_experts == 0
+    runner.apply_plan(plan)
+    assert runner.ctx.hbm_bytes()["staging"] == 0
+    x = X.initial_activations(spec, fwd, 7)
+    rep = runner.run(2, acts=x.copy())
+    base = X.resident_baseline(2, spec, container, fwd, acts=x.copy())
+    assert rep.page_fault is None and rep.violations == []
+    assert np.asarray(rep.final_activations).tobytes() == np.asarray(base).tobytes()
+    # experts back on the host tier need the staging ring: refused while it is released
+    runner.set_device_mask(np.zeros((N, L), dtype=bool))
+    runner.ctx.set_pinned(np.zeros((N, L), dtype=np.uint8))
+    with pytest.raises(XpgError):
+        runner.ctx.set_host_staging(False)
