@@ -77,7 +77,7 @@ def load_tensor_peak():
 def ncu_traffic(config: str, tokens: int):
     """DRAM bytes (read + write) of one gate/up launch from the committed ncu --set full
     capture of this workload (profiles/), or None when none was taken for it."""
-    path = {("mixtral", 256): os.path.join(ROOT, "profiles", "r1_ncu_gemm_T256_v4.jsonl")}.get((config, tokens))
+    path = {("mixtral", 256): os.path.join(ROOT, "profiles", "r2_ncu_gemm_T256_final.jsonl")}.get((config, tokens))
     try:
         for line in open(path):
             rec = json.loads(line)
@@ -91,13 +91,13 @@ def ncu_traffic(config: str, tokens: int):
 def ncu_decoder_capture():
     """DRAM traffic vs algorithmic bytes of one decoder launch (Mixtral gate/up tensor) from
     the committed ncu --set full capture."""
-    path = os.path.join(ROOT, "profiles", "r1_ncu_exp_decode_v7.jsonl")
+    path = os.path.join(ROOT, "profiles", "r2_ncu_dec2_final.jsonl")
     try:
         rec = json.loads(open(path).readline())
         n = 117_440_512  # values of the captured tensor (tools/profile_codec.py default)
         algo = n + n * 2.591 / 8 + n / 256 * 4 + 2 * n
         return {"dram_bytes": rec["dram_read"] + rec["dram_write"], "algorithmic_bytes": algo,
-                "source": "profiles/r1_ncu_exp_decode_v7.jsonl (one 117.4M-value tensor, chunk 256)"}
+                "source": "profiles/r2_ncu_dec2_final.jsonl (k_exp_decode2, one 117.4M-value tensor, chunk 256)"}
     except Exception:
         return None
 
@@ -135,13 +135,13 @@ def decoder_roofline(stats, steps, step_s, hbm_peak, hbm_src):
     ns = stats["kernel_ns"] / n
     ach = per_launch / ns  # bytes/ns == GB/s
     return {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
-            "peak_source": hbm_src, "kernel": "k_exp_decode (exponent-Huffman -> bf16 into the ring, paged run)",
+            "peak_source": hbm_src, "kernel": "k_exp_decode2 (exponent-Huffman -> bf16 into the ring, paged run; 65% of kernel time, profiles/r2_launches_bench_mixtral.json)",
             "algorithmic_bytes_per_launch": per_launch, "avg_launch_us": ns / 1e3,
             "launches_per_step": n / steps, "kernel_time_per_step_ms": stats["kernel_ns"] / steps / 1e6,
             "step_ms": step_s * 1e3 / steps,
             "note": "launches overlap each other (two kinds, host and device tiers) and the GEMMs, so a launch's "
-                    "time includes sharing the SMs; standalone the kernel reaches ~1,450-1,600 GB/s of bf16 output "
-                    "on a 117M-value tensor (profiles/r1_decoder_experiments.md)",
+                    "time includes sharing the SMs; standalone the kernel reaches ~1,450-1,540 GB/s of bf16 output "
+                    "on a 117M-value tensor, bound by the per-stream decode chain (profiles/r2_decoder_experiments.md)",
             "traffic": None, "traffic_capture": ncu_decoder_capture()}
 
 
@@ -716,7 +716,7 @@ def main():
                  "down": {k: roof_dn[k] for k in ("bound", "achieved", "peak", "unit", "frac", "avg_launch_us")}})
     roof["down"]["splits"] = kern.get("down_splits")
     # the dominant kernel of the paged step is the decoder when the codec tiers are on (ncu
-    # launch list: profiles/r1_launches_bench_mixtral_codec.json); the GEMM roofline rides along
+    # launch list: profiles/r2_launches_bench_mixtral.json); the GEMM roofline rides along
     dec_roof = decoder_roofline(dec_stats, args.steps, elapsed, hbm_peak, peak_src)
     if dec_roof is not None:
         if roof.get("achieved"):  # EP runs have no resident comparator to time the GEMMs on
