@@ -145,6 +145,12 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
         streamed_max = L - min(p_layer)
         if streamed_max == 0:
             ring = 0
+        elif dev_fused:
+            # device-tier experts read in place hold no ring block: the ring serves the host
+            # tier only (one window of it in flight when nothing else is on the host)
+            d_max = int(min(total - p, max(0.0, cap - depth * eb - p * eb) // dceb))
+            host_layer = -(-(total - p - d_max) // N)
+            ring = depth * max(1, min(w_min, host_layer))
         else:
             ring = depth * min(w_min, streamed_max)
         room = cap - ring * eb - p * eb

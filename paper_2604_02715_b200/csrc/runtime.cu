@@ -672,6 +672,28 @@ static void enqueue_layer(Ctx* c, int layer, const float* x, float* y, int T, in
 
 // --------------------------------------------------------------------------- page table ops
 
+// A device-tier expert read in place by the decode-into-GEMM kernel is mapped without an arena
+// block: its slot-table entry goes LOADING -> RESIDENT in stream order like any page (the GEMM
+// prologue's residency check and the ordering log are unchanged), but it holds no ring memory,
+// so a window may carry any number of them beside its ring-backed experts.
+constexpr int kVirtualBlock = 0x3FFFFFFF;
+
+static int pt_map_virtual(Ctx* c, int layer, int expert, int kind) {
+  const int pi = page_index(c, layer, expert, kind);
+  const int k = kind - 1;
+  if (c->st[k][pi] != XPGB_PAGE_UNMAPPED || c->blk[k][pi] != 0)
+    XFAIL(XPGB_ERR_DOUBLE_MAP, "%s is already mapped (%s)", tid_str(layer, expert, kind).c_str(),
+          state_name(c->st[k][pi]));
+  c->blk[k][pi] = kVirtualBlock;
+  c->st[k][pi] = XPGB_PAGE_LOADING;
+  c->step += 1;
+  emit(c, "map", layer, expert, kind, 0, "in place (device tier, decode-into-GEMM)");
+  return kVirtualBlock;
+}
+
+// device slot-table block field of a host block id (virtual maps point at block 0: unused)
+static int32_t dev_block0(int b) { return b == kVirtualBlock ? 0 : b - 1; }
+
 static int pt_map(Ctx* c, int layer, int expert, int kind) {
   const int pi = page_index(c, layer, expert, kind);
   const int k = kind - 1;
@@ -715,10 +737,12 @@ static void pt_unmap(Ctx* c, int layer, int expert, int kind) {
   c->step += 1;
   emit(c, "state", layer, expert, kind, b, "state=evicting");
   c->blk[k][pi] = 0;
-  c->owner[k][b] = -1;
-  c->free_ids[k].insert(b);
   c->st[k][pi] = XPGB_PAGE_UNMAPPED;
-  c->bound -= sigma_of(c, kind);
+  if (b != kVirtualBlock) {
+    c->owner[k][b] = -1;
+    c->free_ids[k].insert(b);
+    c->bound -= sigma_of(c, kind);
+  }
   c->step += 1;
   emit(c, "unmap", layer, expert, kind, b, "");
 }
@@ -876,7 +900,7 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
         ou.set_n = std::min(chunk, thi - e0);
         for (int i = 0; i < ou.set_n; ++i) {
           const size_t pi = (size_t)(tgt - 1) * E + e0 + i;
-          ou.vals[i] = c->st[k][pi] == XPGB_PAGE_UNMAPPED ? -1 : pt_entry(c->blk[k][pi] - 1, c->st[k][pi]);
+          ou.vals[i] = c->st[k][pi] == XPGB_PAGE_UNMAPPED ? -1 : pt_entry(dev_block0(c->blk[k][pi]), c->st[k][pi]);
         }
         launch_op(ou, s);
       }
@@ -887,8 +911,9 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
   // map every streamed expert of the window (lowest free block first) -> LOADING entries
   std::vector<int> blocks(E, 0);
   for (int e = wlo; e < whi; ++e)
-    blocks[e] = is_pinned(layer, e) ? c->blk[k][(size_t)(layer - 1) * E + e]
-                                    : pt_map(c, layer, c->e_first + e + 1, kind);
+    blocks[e] = is_pinned(layer, e)              ? c->blk[k][(size_t)(layer - 1) * E + e]
+                : fused_tensor(c, layer, e, kind) ? pt_map_virtual(c, layer, c->e_first + e + 1, kind)
+                                                  : pt_map(c, layer, c->e_first + e + 1, kind);
   if (rs.log) set_rec(op, nrec++, XPGB_EV_LOAD_START, it, layer, kind, -1, -1, st.w);
   int32_t* row = c->d_pt + (size_t)k * N * E + (size_t)(layer - 1) * E;
   for (int e0 = wlo; e0 < whi; e0 += chunk) {
@@ -897,14 +922,15 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
     o2.set_row = row + e0;
     o2.set_n = std::min(chunk, whi - e0);
     for (int i = 0; i < o2.set_n; ++i)
-      o2.vals[i] = pt_entry(blocks[e0 + i] - 1, is_pinned(layer, e0 + i) ? XPGB_PAGE_RESIDENT : XPGB_PAGE_LOADING);
+      o2.vals[i] = pt_entry(dev_block0(blocks[e0 + i]), is_pinned(layer, e0 + i) ? XPGB_PAGE_RESIDENT : XPGB_PAGE_LOADING);
     launch_op(o2, s);
   }
   if (whi <= wlo && (op.n_rec > 0 || op.unmap_n > 0)) launch_op(op, s);  // window without routed experts
   static const bool env_poison = getenv("XPGB_POISON") && atoi(getenv("XPGB_POISON")) != 0;
   if (c->poison || env_poison)
     for (int e = wlo; e < whi; ++e)
-      if (!is_pinned(layer, e)) CK(cudaMemsetAsync(block_ptr(c, kind, blocks[e]), 0xFF, sigma_of(c, kind), s));
+      if (!is_pinned(layer, e) && blocks[e] != kVirtualBlock)
+        CK(cudaMemsetAsync(block_ptr(c, kind, blocks[e]), 0xFF, sigma_of(c, kind), s));
   const float* delays = rs.o->fetch_delay_s;
   auto delay_of = [&](int e) -> float {
     return delays ? delays[((size_t)(layer - 1) * c->L + (c->e_first + e)) * 2 + k] : 0.f;
@@ -1101,7 +1127,7 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
     PtOp o3 = blank_op(c, rs.log && e0 + chunk >= whi);
     o3.set_row = row + e0;
     o3.set_n = std::max(0, std::min(chunk, whi - e0));
-    for (int i = 0; i < o3.set_n; ++i) o3.vals[i] = pt_entry(blocks[e0 + i] - 1, XPGB_PAGE_RESIDENT);
+    for (int i = 0; i < o3.set_n; ++i) o3.vals[i] = pt_entry(dev_block0(blocks[e0 + i]), XPGB_PAGE_RESIDENT);
     if (o3.log) set_rec(o3, 0, XPGB_EV_LOAD_DONE, it, layer, kind, -1, -1, st.w);
     launch_op(o3, done_stream);
   }
@@ -1136,8 +1162,12 @@ static Session& session_of(Ctx* c) {
 // layer when the ring holds two whole layers (the reference geometry).
 static std::vector<std::pair<int, int>> layer_windows(Ctx* c, int layer) {
   const int E = c->E, G = groups_of(c);
+  // experts that need a ring block: streamed and not read in place by the decode-into-GEMM kernel
+  auto ring_backed = [&](int e) {
+    return !c->pinned[(size_t)(layer - 1) * E + e] && !(fused_tensor(c, layer, e, 1) && fused_tensor(c, layer, e, 2));
+  };
   int streamed = 0;
-  for (int e = 0; e < E; ++e) streamed += !c->pinned[(size_t)(layer - 1) * E + e];
+  for (int e = 0; e < E; ++e) streamed += ring_backed(e);
   const int gs = std::max(1, c->ring_blocks / depth_of(c));
   std::vector<std::pair<int, int>> w;
   if (c->pool != XPGB_POOL_RING || gs >= streamed) {
@@ -1146,7 +1176,7 @@ static std::vector<std::pair<int, int>> layer_windows(Ctx* c, int layer) {
   }
   int lo = 0, n = 0;
   for (int e = 0; e < E; ++e) {
-    n += !c->pinned[(size_t)(layer - 1) * E + e];
+    n += ring_backed(e);
     if (n == gs) {
       w.push_back({lo, e + 1});
       lo = e + 1;
@@ -1183,6 +1213,7 @@ static void session_begin(Ctx* c, const xpgb_run_opts* o, float* acts) {
     XFAIL(XPGB_ERR_OUT_OF_RANGE, "bad ForwardSpec (T=%d, top_k=%d)", o->tokens, o->top_k);
   const int N = c->N;
   ss.o = *o;
+  c->fused_now = fused_for(c, o->tokens, o->top_k);  // the schedule's windows depend on it
   build_schedule(c, ss, o->iterations);
   ss.mat_next = 0;
   ss.builtin_compute = false;
