@@ -145,6 +145,25 @@ def decoder_roofline(stats, steps, step_s, hbm_peak, hbm_src):
             "traffic": None, "traffic_capture": ncu_decoder_capture()}
 
 
+def fused_roofline(stats, steps, hbm_peak, hbm_src):
+    """Roofline of the decode-into-GEMM kernel: the compressed record bytes each launch reads in
+    place (its DRAM traffic is those bytes + the activation rows, ncu: profiles/r2_ncu_fused_fx4_final.jsonl)
+    over its mean launch time."""
+    n = stats.get("launches", 0)
+    if not n:
+        return None
+    per_launch = stats["record_bytes"] / n
+    ns = stats["kernel_ns"] / n
+    ach = per_launch / ns
+    return {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+            "peak_source": hbm_src,
+            "kernel": "k_moe_gemm_dec (decode-into-GEMM: device-tier records expanded into the UMMA tiles in smem)",
+            "algorithmic_bytes_per_launch": per_launch, "avg_launch_us": ns / 1e3, "launches_per_step": n / steps,
+            "kernel_time_per_step_ms": stats["kernel_ns"] / steps / 1e6,
+            "note": "algorithmic bytes = the compressed records read in place (activation rows excluded)",
+            "traffic": None}
+
+
 def gemm_roofline(kind, bytes_, ns, rows, H, F, hbm_peak, hbm_src, tc_peak, tc_src):
     """Roofline of one grouped-GEMM launch: HBM-bound (weights dominate) at decode sizes,
     tensor-bound once the rows per expert make the contraction compute-heavy."""
@@ -643,6 +662,7 @@ def main():
     page_in_gbps = rep.h2d_bytes / rep.elapsed_seconds / 1e9
     exposed = rep.stall_seconds / rep.elapsed_seconds
     dec_stats = runner.ctx.decode_stats()  # every decoder launch of the timed run, events on its own stream
+    fz_stats = runner.ctx.fused_stats()    # every decode-into-GEMM launch of the timed run
 
     log(f"timed paged run: {elapsed:.3f}s")
     # ---- e2e: the same metric through the public API with host buffers every step: a
@@ -718,6 +738,17 @@ def main():
     # the dominant kernel of the paged step is the decoder when the codec tiers are on (ncu
     # launch list: profiles/r2_launches_bench_mixtral.json); the GEMM roofline rides along
     dec_roof = decoder_roofline(dec_stats, args.steps, elapsed, hbm_peak, peak_src)
+    fz_roof = fused_roofline(fz_stats, args.steps, hbm_peak, peak_src)
+    # the dominant kernel of the paged step: the decoder or the decode-into-GEMM kernel,
+    # whichever took more device time in the timed run
+    if fz_roof is not None and (dec_roof is None or fz_stats["kernel_ns"] > dec_stats.get("kernel_ns", 0)):
+        if dec_roof is not None:
+            fz_roof["decoder"] = {k: dec_roof[k] for k in ("achieved", "frac", "avg_launch_us", "launches_per_step",
+                                                          "kernel_time_per_step_ms")}
+        dec_roof = fz_roof
+    elif dec_roof is not None and fz_roof is not None:
+        dec_roof["decode_into_gemm"] = {k: fz_roof[k] for k in ("achieved", "frac", "avg_launch_us",
+                                                               "launches_per_step", "kernel_time_per_step_ms")}
     if dec_roof is not None:
         if roof.get("achieved"):  # EP runs have no resident comparator to time the GEMMs on
             dec_roof["gemm"] = roof

@@ -301,6 +301,10 @@ int xpgb_set_stage_buffers(xpgb_ctx* ctx, int32_t n_buffers);
  * device time (events on each launch's own decode stream) and their algorithmic bytes
  * (sign/mantissa + bitstream + chunk index read, bf16 written).  Zeros without profile. */
 int xpgb_decode_stats(xpgb_ctx* ctx, int64_t* launches, double* kernel_ns, int64_t* algo_bytes);
+/* Decode-into-GEMM launches of the last run with opts.profile set: how many, their summed device
+ * time (events on the compute stream around each launch) and the compressed record bytes they
+ * read in place.  Zeros without profile or without fused launches. */
+int xpgb_fused_stats(xpgb_ctx* ctx, int64_t* launches, double* kernel_ns, int64_t* record_bytes);
 /* Shared experts (DeepSeek-V3 style; absent from the reference, our convention): n_shared
  * always-on experts per layer that every token passes through after its routed experts,
  * weight 1.0 (the routed sum keeps its f32(1/top_k) scale).  host = N*n_shared*(sigma1+sigma2)

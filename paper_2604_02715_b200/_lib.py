@@ -126,6 +126,7 @@ _SIGS = {
     "xpgb_set_hazard_checks": [_P, _I, _I, _I],
     "xpgb_set_stage_buffers": [_P, _I],
     "xpgb_decode_stats": [_P, _P, _P, _P],
+    "xpgb_fused_stats": [_P, _P, _P, _P],
     "xpgb_ep_window_alloc": [C.c_uint64, _P, _P],
     "xpgb_ep_window_open": [_P, _P],
     "xpgb_ep_window_close": [_P],

@@ -315,6 +315,13 @@ struct Ctx {
   // stream, with its algorithmic bytes (records read + bf16 written) -- xpgb_decode_stats
   std::vector<cudaEvent_t> dec_ev;
   std::vector<uint64_t> dec_bytes;
+  // decode-into-GEMM launches of a profiled run: events around each launch (compute stream),
+  // the record bytes of the experts it read in place
+  std::vector<cudaEvent_t> fz_ev;
+  std::vector<uint64_t> fz_bytes;
+  size_t fz_n = 0;
+  double fz_total_ns = 0;
+  uint64_t fz_total_bytes = 0, fz_launches = 0;
   size_t dec_n = 0;
   double dec_total_ns = 0;
   uint64_t dec_total_bytes = 0, dec_launches = 0;
@@ -546,6 +553,36 @@ static bool fused_tensor(const Ctx* c, int layer, int e, int kind) {
   return c->backend[ti] == 1 && c->pinned[(size_t)(layer - 1) * c->E + e] == 0;
 }
 
+// Profiled runs (c->cur_ev set by session_compute): events around each decode-into-GEMM launch.
+static void fz_mark(Ctx* c, cudaStream_t s, uint64_t bytes, bool begin) {
+  if (!c->cur_ev) return;
+  if (begin) {
+    while (c->fz_ev.size() < 2 * (c->fz_n + 1)) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      c->fz_ev.push_back(e);
+    }
+    if (c->fz_bytes.size() < c->fz_n + 1) c->fz_bytes.resize(c->fz_n + 1);
+    c->fz_bytes[c->fz_n] = bytes;
+    CK(cudaEventRecord(c->fz_ev[2 * c->fz_n], s));
+  } else {
+    CK(cudaEventRecord(c->fz_ev[2 * c->fz_n + 1], s));
+    ++c->fz_n;
+  }
+}
+
+// Record bytes the decode-into-GEMM launch of window [e0, e1), kind, reads in place.
+static uint64_t fused_bytes(Ctx* c, int layer, int e0, int e1, int kind) {
+  uint64_t b = 0;
+  for (int e = e0; e < std::min(e1, c->E); ++e) {
+    if (!fused_tensor(c, layer, e, kind)) continue;
+    const size_t ti = ((size_t)(layer - 1) * c->E + e) * 2 + (kind - 1);
+    const uint64_t n = ((kind == 2) ? c->s2 : c->s1) / 2;
+    b += c->dev_fmt == 1 ? c->fx_bytes[ti] : xpgb_codec_record_bytes(n, c->rec_bits[ti], c->cchunk);
+  }
+  return b;
+}
+
 static GemmParams gemm_params(Ctx* c, int layer, int kind, const int32_t* offsets, int splits,
                               bool with_shared = true) {
   GemmParams p;
@@ -628,8 +665,11 @@ static void enqueue_window(Ctx* c, int layer, const float* x, float* y, int T, i
     launch_gemm_pair(true, c->map_xp_pair, c->map_gu, c->S ? c->map_gu_sh : c->map_gu, pg, c->num_sms, s,
                      c->pair_split);
   else {
-    if (fused[0])
+    if (fused[0]) {
+      fz_mark(c, s, fused_bytes(c, layer, e0, e1, 1), true);
       launch_gemm_dec(true, c->map_xp, pg, c->ctab, c->cchunk, pick_bn_dec(c, T, kk), c->num_sms, s, c->dev_fmt == 1);
+      fz_mark(c, s, 0, false);
+    }
     if (rest[0])
       launch_gate_up(c->map_gu, c->map_xp, c->S ? c->map_gu_sh : c->map_gu, pg, bn, c->num_sms, s, lean_gemm(c));
   }
@@ -639,8 +679,11 @@ static void enqueue_window(Ctx* c, int layer, const float* x, float* y, int T, i
     launch_gemm_pair(false, c->map_h_pair, c->map_dn, c->S ? c->map_dn_sh : c->map_dn, pd, c->num_sms, s,
                      c->pair_split);
   else {
-    if (fused[1])
+    if (fused[1]) {
+      fz_mark(c, s, fused_bytes(c, layer, e0, e1, 2), true);
       launch_gemm_dec(false, c->map_h, pd, c->ctab, c->cchunk, pick_bn_dec(c, T, kk), c->num_sms, s, c->dev_fmt == 1);
+      fz_mark(c, s, 0, false);
+    }
     if (rest[1])
       launch_down(c->map_dn, c->map_h, c->S ? c->map_dn_sh : c->map_dn, pd, bn_dn, c->num_sms, s, lean_gemm(c));
   }
@@ -1218,6 +1261,7 @@ static void session_begin(Ctx* c, const xpgb_run_opts* o, float* acts) {
   ss.mat_next = 0;
   ss.builtin_compute = false;
   c->dec_n = 0;
+  c->fz_n = 0;
   ss.fetch_delay.clear();
   ss.compute_delay.clear();
   if (o->fetch_delay_s) ss.fetch_delay.assign(o->fetch_delay_s, o->fetch_delay_s + (size_t)N * c->L * 2);
@@ -1434,6 +1478,15 @@ static void session_end(Ctx* c, xpgb_report* rep) {
     rep->kern_gate_up_ns = gu * 1e6 / steps;
     rep->kern_down_ns = dn * 1e6 / steps;
     rep->kern_aux_ns = aux * 1e6 / steps;
+  }
+  c->fz_total_ns = 0;
+  c->fz_total_bytes = 0;
+  c->fz_launches = c->fz_n;
+  for (size_t i = 0; i < c->fz_n; ++i) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, c->fz_ev[2 * i], c->fz_ev[2 * i + 1]));
+    c->fz_total_ns += ms * 1e6;
+    c->fz_total_bytes += c->fz_bytes[i];
   }
   c->dec_total_ns = 0;
   c->dec_total_bytes = 0;
@@ -2450,6 +2503,15 @@ int xpgb_set_ring_depth(xpgb_ctx* h, int32_t depth) {
       XFAIL(XPGB_ERR_OUT_OF_RANGE, "ring depth %d exceeds the ring of %d experts", depth, c->ring_limit);
     c->ring_depth = depth;
     if (c->ring_limit > 0) apply_residency(c, c->pinned);
+  });
+}
+
+int xpgb_fused_stats(xpgb_ctx* h, int64_t* launches, double* kernel_ns, int64_t* record_bytes) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    *launches = (int64_t)c->fz_launches;
+    *kernel_ns = c->fz_total_ns;
+    *record_bytes = (int64_t)c->fz_total_bytes;
   });
 }
 

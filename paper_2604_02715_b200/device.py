@@ -190,6 +190,12 @@ class Context:
         call("xpgb_decode_stats", self._h, C.byref(n), C.byref(ns), C.byref(b))
         return {"launches": int(n.value), "kernel_ns": float(ns.value), "algo_bytes": int(b.value)}
 
+    def fused_stats(self) -> dict:
+        """Decode-into-GEMM launches of the last profiled run (xpgb_fused_stats)."""
+        n, ns, b = C.c_int64(), C.c_double(), C.c_int64()
+        call("xpgb_fused_stats", self._h, C.byref(n), C.byref(ns), C.byref(b))
+        return {"launches": int(n.value), "kernel_ns": float(ns.value), "record_bytes": int(b.value)}
+
     def make_resident(self) -> None:
         call("xpgb_make_resident", self._h)
 
