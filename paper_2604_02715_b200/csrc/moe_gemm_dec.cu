@@ -60,11 +60,14 @@ struct DecCfg {
   static constexpr int B_BYTES = BN * kBK * 2;              // one activation plane
   static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;   // two A tiles + hi/lo activations
   static constexpr int TMEM_COLS = 512;                     // 2 accumulator stages x 256 columns
-  static constexpr int TAB_BYTES = (3 * kMaxExperts + 8) * 4;
+  static constexpr int TAB_BYTES = FMT ? (2 * kMaxExperts + 4) * 4 : (3 * kMaxExperts + 8) * 4;  // s_off, s_up (+ flag)
   static constexpr int DEC_TAB =
       FMT ? 0 : (((1 << kPairBits) * 4 + 3 * (kCodecMaxLen + 1) * 4 + kCodecSymbols + 15) & ~15);
   static constexpr int RING = FMT ? 0 : kDecThreads_dec * kRingBytes;  // per-decoder-thread bitstream rings
-  static constexpr int CST = FMT ? ((STAGES >= 3 || STAGE >= 60 * 1024) ? 3 : 4) : 0;  // compressed stages (FX4)
+  // compressed stages (FX4): as many as fit beside the decoded stages, 2..4
+  static constexpr int CST_FIT = (227 * 1024 - 1024 - 256 - TAB_BYTES - STAGES * STAGE) / kFxCStage;
+  static constexpr int CST = FMT ? (CST_FIT > 4 ? 4 : CST_FIT) : 0;
+  static_assert(!FMT || CST >= 2, "FX4 decode-GEMM needs two compressed stages");
   static constexpr int BAR_OFF = STAGES * STAGE + CST * kFxCStage;       // barriers, then the tables
   static constexpr int SMEM = BAR_OFF + 1024 + 256 + TAB_BYTES + DEC_TAB + RING;
   static_assert(SMEM <= 227 * 1024, "decode-GEMM stages exceed 227 KB");
@@ -229,7 +232,7 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
   int* s_off = reinterpret_cast<int*>(smem + C::BAR_OFF + 256);
   int* s_up = s_off + kMaxExperts + 1;
   int* s_flag = s_up + kMaxExperts + 1;
-  uint32_t* s_pair = reinterpret_cast<uint32_t*>(s_off + 3 * kMaxExperts + 8);
+  uint32_t* s_pair = reinterpret_cast<uint32_t*>(s_off + 3 * kMaxExperts + 8);  // Huffman only (FMT 0)
   uint32_t* s_first = s_pair + (1 << kPairBits);
   int* s_count = reinterpret_cast<int*>(s_first + kCodecMaxLen + 1);
   int* s_rank = s_count + kCodecMaxLen + 1;
@@ -631,18 +634,25 @@ using DecKernel = void (*)(const CUtensorMap, GemmParams, const DecTables*, int)
 
 // stage counts: the A tiles are produced on-chip, so a few stages cover the decoder/MMA overlap
 #define XPGB_DEC_TILES(X) X(32, 3) X(48, 2) X(64, 2) X(80, 2) X(96, 2) X(128, 2)
+// FX4: 2 decoded stages and up to 4 compressed ones (default), or 3 decoded stages and fewer
+// compressed ones (XPGB_FX_STAGES=3, A/B)
+#define XPGB_FX_TILES(X) X(32, 3) X(48, 2) X(64, 2) X(80, 2) X(96, 2) X(128, 2)
+#define XPGB_FX_TILES3(X) X(32, 4) X(48, 3) X(64, 3) X(80, 3) X(96, 3) X(128, 2)
 
-template <bool GU, int BN, int ST>
+template <bool GU, int BN, int ST, int FMT>
 static void set_dec_attr() {
-  cudaFuncSetAttribute(k_moe_gemm_dec<GU, BN, ST, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, DecCfg<BN, ST>::SMEM);
-  cudaFuncSetAttribute(k_moe_gemm_dec<GU, BN, ST, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       DecCfg<BN, ST, 1>::SMEM);
+  cudaFuncSetAttribute(k_moe_gemm_dec<GU, BN, ST, FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       DecCfg<BN, ST, FMT>::SMEM);
 }
 
 void set_gemm_dec_attrs() {
-#define XPGB_SET_DEC(BN, ST) set_dec_attr<true, BN, ST>(); set_dec_attr<false, BN, ST>();
+#define XPGB_SET_DEC(BN, ST) set_dec_attr<true, BN, ST, 0>(); set_dec_attr<false, BN, ST, 0>();
+#define XPGB_SET_FX(BN, ST) set_dec_attr<true, BN, ST, 1>(); set_dec_attr<false, BN, ST, 1>();
   XPGB_DEC_TILES(XPGB_SET_DEC)
+  XPGB_FX_TILES(XPGB_SET_FX)
+  XPGB_FX_TILES3(XPGB_SET_FX)
 #undef XPGB_SET_DEC
+#undef XPGB_SET_FX
 }
 
 // A unit's K range (a split_kb range: multiples of 256 values) must start on a chunk boundary.
@@ -654,16 +664,28 @@ void launch_gemm_dec(bool gate_up, const CUtensorMap& map_b, const GemmParams& p
                      int bn, int grid, cudaStream_t s, bool fx4) {
   const DecTables* tabs = codec_device_tables(table, s);
   if (!tabs) return;
+  static const bool fx3 = getenv("XPGB_FX_STAGES") && atoi(getenv("XPGB_FX_STAGES")) == 3;
   DecKernel kern = nullptr;
   int smem = 0;
-#define XPGB_PICK_DEC(BN, ST)                                                                            \
-  if (bn == BN) {                                                                                        \
-    kern = fx4 ? (gate_up ? k_moe_gemm_dec<true, BN, ST, 1> : k_moe_gemm_dec<false, BN, ST, 1>)           \
-               : (gate_up ? k_moe_gemm_dec<true, BN, ST, 0> : k_moe_gemm_dec<false, BN, ST, 0>);          \
-    smem = fx4 ? DecCfg<BN, ST, 1>::SMEM : DecCfg<BN, ST>::SMEM;                                         \
+#define XPGB_PICK_DEC(BN, ST)                                                            \
+  if (bn == BN) {                                                                        \
+    kern = gate_up ? k_moe_gemm_dec<true, BN, ST, 0> : k_moe_gemm_dec<false, BN, ST, 0>;  \
+    smem = DecCfg<BN, ST>::SMEM;                                                         \
   }
-  XPGB_DEC_TILES(XPGB_PICK_DEC)
+#define XPGB_PICK_FX(BN, ST)                                                             \
+  if (bn == BN) {                                                                        \
+    kern = gate_up ? k_moe_gemm_dec<true, BN, ST, 1> : k_moe_gemm_dec<false, BN, ST, 1>;  \
+    smem = DecCfg<BN, ST, 1>::SMEM;                                                      \
+  }
+  if (!fx4) {
+    XPGB_DEC_TILES(XPGB_PICK_DEC)
+  } else if (fx3) {
+    XPGB_FX_TILES3(XPGB_PICK_FX)
+  } else {
+    XPGB_FX_TILES(XPGB_PICK_FX)
+  }
 #undef XPGB_PICK_DEC
+#undef XPGB_PICK_FX
   if (!kern) {
     kern = fx4 ? (gate_up ? k_moe_gemm_dec<true, 128, 2, 1> : k_moe_gemm_dec<false, 128, 2, 1>)
                : (gate_up ? k_moe_gemm_dec<true, 128, 2, 0> : k_moe_gemm_dec<false, 128, 2, 0>);
