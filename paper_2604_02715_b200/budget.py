@@ -164,7 +164,10 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
         link = (total - p - d) * ceb
         decode = (total - p) * eb
         sm = (total - p - d) * eb / b_dec + d * eb / bdev + t_compute * (1.0 - (d / total if dev_fused else 0.0))
-        est = max(link / b_link, sm)
+        # a host record's transfer is only partly hidden when the SMs are the bottleneck: the
+        # staging ring holds ~1 record ahead and a record is released when its window decodes
+        # (measured: an SM-bound step exposes about half its link time, DESIGN §5 calibration)
+        est = max(link / b_link, sm + HOST_EXPOSED * link / b_link)
         key = (est, -ring)
         if best is None or key < best[0]:
             best = (key, p, d, ring, link)
@@ -198,13 +201,15 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
 
 
 # Raw-equivalent rates the format choice is made with (B200 measurements, Mixtral T = 256,
-# profiles/r2_fx4_*.jsonl): the Huffman decoder expanding into the ring beside the GEMMs, and
+# `calibrate`, profiles/r2_calibrate_mixtral_v2.json): the Huffman decoder expanding into the ring
+# beside the GEMMs (raw bytes over the step time beyond resident compute), and
 # the decode-into-GEMM kernel reading FX4 records through TMA-staged compressed stages (GEMM
 # included, profiles/r2_fused_fx4_mixtral_v3.jsonl).  Resident GEMMs stream raw
 # weights at about 5.2 TB/s.
-B_DEC_HUFFMAN = 1.1e12
+B_DEC_HUFFMAN = 1.8e12
 B_FUSED_FX4 = 3.2e12
 B_RESIDENT = 5.2e12
+HOST_EXPOSED = 0.5  # share of the host link time an SM-bound step cannot hide
 
 
 def fx4_expert_bytes(H: int, F: int) -> float:
@@ -234,7 +239,7 @@ def plan_tiers(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *, fx
     cands = []
     if device_format in ("auto", "huffman"):
         p = plan_residency(N, L, eb, ceb, budget_bytes, shared_bytes=shared_bytes, overhead_bytes=overhead_bytes,
-                           b_link=b_link, b_dec=b_dec, **kw)
+                           b_link=b_link, b_dec=b_dec, t_compute=t_res, **kw)
         p.device_format, p.fused = "huffman", False
         cands.append(p)
     if fx4_ceb and device_format in ("auto", "fx4"):
@@ -266,7 +271,7 @@ def plan_tiers(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *, fx
             sm = host * eb / b_dec + d * eb / p.fx4_rate + t_res * (total - d) / total
         else:
             sm = (host + d) * eb / b_dec + t_res
-        return max(link, sm)
+        return max(link, sm + HOST_EXPOSED * link)
 
     best = min(cands, key=score)
     best.est_step_s = score(best)
