@@ -52,6 +52,8 @@ constexpr int kRingBytes = 256;                    // per decoder thread: four 6
 // FMT 1 (FX4): decoded stages + CST compressed stages the TMA fills -- per stage the unit's
 // 2 x 128 rows of 64 sign/mantissa bytes (64-B swizzle) and 32 nibble bytes (32-B swizzle).
 constexpr int kFxSmTile = 128 * 64, kFxNibTile = 128 * 32;
+constexpr int kFxFenceFlag = 1 << 30;  // FX4 launches: bit in `chunk` -> proxy fence before a slot release
+
 constexpr int kFxCStage = 2 * kFxSmTile + 2 * kFxNibTile;  // 24 KB
 
 template <int BN, int STAGES, int FMT = 0>
@@ -571,7 +573,19 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
                          : "=r"(nv[g].x), "=r"(nv[g].y), "=r"(nv[g].z), "=r"(nv[g].w)
                          : "r"(cb + nb_row + ((g ^ nb_sw) << 4))
                          : "memory");
+          // release the slot as soon as this warp holds its rows, so the producer runs a full
+          // CST stages ahead (releasing after the decode cost 6%); a use of every loaded register
+          // makes the reads complete first -- releasing before they completed let the producer
+          // overwrite rows still being read (wrong results at T = 256)
+          const uint32_t all = sv[0].x ^ sv[0].y ^ sv[0].z ^ sv[0].w ^ sv[1].x ^ sv[1].y ^ sv[1].z ^ sv[1].w ^ sv[2].x ^
+                               sv[2].y ^ sv[2].z ^ sv[2].w ^ sv[3].x ^ sv[3].y ^ sv[3].z ^ sv[3].w ^ nv[0].x ^ nv[0].y ^
+                               nv[0].z ^ nv[0].w ^ nv[1].x ^ nv[1].y ^ nv[1].z ^ nv[1].w;
+          asm volatile("" ::"r"(all));
         }
+        if (chunk & kFxFenceFlag) fence_async_smem();  // A/B knob: the reads are already complete
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&cempty[fcs]);
+        if (++fcs == C::CST) { fcs = 0; fcph ^= 1; }
         mbar_wait_backoff(&empty[stage], phase ^ 1);
         if (valid) {
           const uint32_t row = smem_u32(smem + stage * C::STAGE + a * C::A_BYTES + lr * 128);
@@ -606,17 +620,9 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
             }
           }
         }
-        // one fence for both hand-offs: the A tile's generic stores before the tensor cores'
-        // reads, and this stage's compressed-row reads (consumed above, so complete) before the
-        // producer's next TMA write into the slot (releasing the slot before the decode let the
-        // producer, CST stages ahead, overwrite rows still being read: wrong results at T = 256)
-        fence_async_smem();
+        fence_async_smem();  // the A tile's generic stores before the tensor cores' reads
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&full[stage]);
-          mbar_arrive(&cempty[fcs]);
-        }
-        if (++fcs == C::CST) { fcs = 0; fcph ^= 1; }
+        if (lane == 0) mbar_arrive(&full[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
       }
@@ -691,7 +697,10 @@ void launch_gemm_dec(bool gate_up, const CUtensorMap& map_b, const GemmParams& p
                : (gate_up ? k_moe_gemm_dec<true, 128, 2, 0> : k_moe_gemm_dec<false, 128, 2, 0>);
     smem = fx4 ? DecCfg<128, 2, 1>::SMEM : DecCfg<128, 2>::SMEM;
   }
-  kern<<<grid, kDecThreads, smem, s>>>(map_b, p, tabs, chunk);
+  // FX4 ignores the Huffman chunk; its top bit carries the release-fence A/B (XPGB_FX_FENCE=0 drops it)
+  static const bool fx_fence = !(getenv("XPGB_FX_FENCE") && atoi(getenv("XPGB_FX_FENCE")) == 0);
+  const int arg = fx4 ? (fx_fence ? kFxFenceFlag : 0) : chunk;
+  kern<<<grid, kDecThreads, smem, s>>>(map_b, p, tabs, arg);
   note_launch();
 }
 
