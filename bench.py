@@ -455,6 +455,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="mixtral", choices=sorted(CONFIGS))
     ap.add_argument("--tokens", type=int, default=None)
+    ap.add_argument("--layers", type=int, default=None,
+                    help="override the config's layer count (Qwen3-30B-A3B has 48; the default stack is 8)")
     ap.add_argument("--device-format", default="auto", choices=["auto", "huffman", "fx4"],
                     help="device-tier records: exponent-Huffman decoded into the ring, or FX4 read in place by "
                          "the decode-into-GEMM kernel (auto: the planner's step model picks)")
@@ -490,6 +492,14 @@ def main():
         args.tokens = 8192
     if args.tokens:
         cfg["T"] = args.tokens
+    if args.layers:
+        cfg["N"] = args.layers
+        cfg["name"] = cfg["name"].replace("8 layers", f"{args.layers} layers").replace(
+            "8 of 48 layers", f"{args.layers} of 48 layers")
+    if args.prefill and args.device_format == "auto":
+        # prefill-sized groups run on the CTA-pair GEMMs, which read ring blocks: a device tier
+        # is decoded into the ring there, where exponent-Huffman (smaller) is the better format
+        args.device_format = "huffman"
     if args.impl == "reference":
         run_reference_arm(args, cfg)
         return
