@@ -494,8 +494,9 @@ def main():
         cfg["T"] = args.tokens
     if args.layers:
         cfg["N"] = args.layers
-        cfg["name"] = cfg["name"].replace("8 layers", f"{args.layers} layers").replace(
-            "8 of 48 layers", f"{args.layers} of 48 layers")
+        name = cfg["name"]
+        cfg["name"] = (name.replace("8 of 48 layers", f"{args.layers} of 48 layers") if "8 of 48 layers" in name
+                       else name.replace("8 layers", f"{args.layers} layers"))
     if args.prefill and args.device_format == "auto":
         # prefill-sized groups run on the CTA-pair GEMMs, which read ring blocks: a device tier
         # is decoded into the ring there, where exponent-Huffman (smaller) is the better format
