@@ -457,9 +457,10 @@ def main():
     ap.add_argument("--tokens", type=int, default=None)
     ap.add_argument("--layers", type=int, default=None,
                     help="override the config's layer count (Qwen3-30B-A3B has 48; the default stack is 8)")
-    ap.add_argument("--device-format", default="auto", choices=["auto", "huffman", "fx4"],
-                    help="device-tier records: exponent-Huffman decoded into the ring, or FX4 read in place by "
-                         "the decode-into-GEMM kernel (auto: the planner's step model picks)")
+    ap.add_argument("--device-format", default="auto", choices=["auto", "huffman", "fx4", "mixed"],
+                    help="device-tier records: exponent-Huffman decoded into the ring, FX4 read in place by "
+                         "the decode-into-GEMM kernel, or mixed (every expert on the device tier, as many FX4 as "
+                         "fit; auto: the planner's step model picks)")
     ap.add_argument("--budget", type=float, default=0.25,
                     help="expert-HBM budget as a fraction of the expert bytes (ring + codec buffers + shared)")
     ap.add_argument("--tiering", default="device", choices=["device", "ring"],
@@ -621,7 +622,7 @@ def main():
         cap = args.budget * expert_bytes * 0.998 - shared_b - overhead  # margin: record sizes vary per expert
         m_dev = 0
         pinned_per_layer = 0
-        dev_format, dev_fused = "huffman", False
+        dev_format, dev_fused, fx4_per_layer = "huffman", False, 0.0
         if args.tiering == "device" and args.host_codec:
             from paper_2604_02715_b200.budget import fx4_expert_bytes, plan_tiers
 
@@ -637,6 +638,7 @@ def main():
                 m_dev = plan.device_experts / Nl
                 pinned_per_layer = plan.pinned_experts / Nl
                 dev_format, dev_fused = plan.device_format, plan.fused
+                fx4_per_layer = plan.fx4_experts / Nl
         if not (m_dev or pinned_per_layer):
             ring_fit = int((cap + 1) // eb) & ~1
             if 2 <= ring_fit < ring_blocks:
@@ -784,6 +786,7 @@ def main():
                    "pinned_experts_per_layer": round(pinned_per_layer, 3),
                    "device_tier_format": dev_format if not use_ep else "huffman",
                    "decode_into_gemm": bool(dev_fused) if not use_ep else False,
+                   "fx4_experts_per_layer": round(fx4_per_layer, 3) if not use_ep else 0.0,
                    "placement": ("2-layer ring" if use_ep or ring_blocks >= 2 * cspec.experts_per_layer else
                                  f"sub-layer ring of {ring_blocks} expert blocks per kind ({ring_depth} window(s) "
                                  f"in flight of {max(1, ring_blocks // ring_depth)} expert(s))") + (
@@ -793,7 +796,10 @@ def main():
                        ", host-only (alpha=0)") + (
                        ", exponent-Huffman records over PCIe decoded on-GPU into the ring (lossless)"
                        if args.host_codec else "") + (
-                       "; device tier in FX4 records read in place by the decode-into-GEMM kernel"
+                       (f"; device tier mixed: {fx4_per_layer:.2f} experts per layer in FX4 records read in place "
+                        f"by the decode-into-GEMM kernel, the rest exponent-Huffman decoded into the ring"
+                        if dev_format == "mixed" else
+                        "; device tier in FX4 records read in place by the decode-into-GEMM kernel")
                        if (not use_ep and dev_fused) else ""),
                    "l2": ("inputs larger than L2 (126 MB): each step reads %.1f GB of expert weights -- %.2f GB of "
                           "records over PCIe, %.2f GB of bf16 decoded on-GPU from HBM records, the rest pinned/ring"

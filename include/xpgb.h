@@ -269,7 +269,10 @@ int xpgb_set_ring_depth(xpgb_ctx* ctx, int32_t depth);
  * ordering log and the results are unchanged (bit-identical).  Applies to decode-sized expert
  * groups (the 1-CTA GEMMs) when K of both projections is a multiple of the codec chunk.  Mode 0
  * (default) keeps every expert in the ring, as callers with their own compute need
- * (xpgb_experts_forward_range).  No session may be active. */
+ * (xpgb_experts_forward_range).  Mode 2 reads only FX4 records in place and decodes
+ * exponent-Huffman device-tier records into the ring (a mixed device tier, where the Huffman
+ * decoder's serial chain makes in-place decoding slower than decode-into-ring).  No session may
+ * be active. */
 int xpgb_set_fused_decode(xpgb_ctx* ctx, int32_t mode);
 /* Record format of the compressed device tier: 0 = exponent-Huffman (default; the host pool's
  * records staged as they are, the reference's device tier, storage.py:143-168), 1 = FX4
@@ -278,6 +281,13 @@ int xpgb_set_fused_decode(xpgb_ctx* ctx, int32_t mode);
  * bandwidth of its compressed bytes.  Lossless either way.  Re-stages the device tier; no
  * session may be active. */
 int xpgb_set_device_format(xpgb_ctx* ctx, int32_t fmt);
+/* Per-tensor record format of the compressed device tier: formats[(layer * E + expert) * 2 +
+ * kind] (kind 0 = gate/up, 1 = down), each 0 or 1 as in xpgb_set_device_format.  A mixed tier
+ * lets a budget keep every streamed expert on the device tier -- FX4 for as many as fit, the
+ * denser Huffman records for the rest -- instead of pushing the remainder to the host tier.
+ * Entries of tensors not on the device tier are kept for when they are placed there.  Re-stages
+ * the device tier; no session may be active. */
+int xpgb_set_device_formats(xpgb_ctx* ctx, const uint8_t* formats);
 /* Staging ring and device-resident chunk index of the compressed host tier: 1 allocates them
  * (the default once xpgb_set_codec(host_compressed = 1) ran), 0 releases them when the placement
  * leaves no tensor on the host tier (a budget plan that keeps every streamed expert on the device

@@ -47,6 +47,14 @@ class ResidencyPlan:
         return int(self.pinned_mask.sum())
 
     @property
+    def fx4_experts(self) -> int:
+        """Device-tier experts in FX4 records (mixed plans; all device-tier experts of FX4 plans)."""
+        m = getattr(self, "fx4_mask", None)
+        if m is not None:
+            return int(m.sum())
+        return self.device_experts if getattr(self, "device_format", None) == "fx4" else 0
+
+    @property
     def host_experts(self) -> int:
         return int(self.device_mask.size - self.device_mask.sum() - self.pinned_mask.sum())
 
@@ -262,12 +270,21 @@ def plan_tiers(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *, fx
             p.device_format, p.fused, p.fx4_rate = "fx4", True, b_fx4 * fill
             cands.append(p)
 
+    if fx4_ceb and device_format in ("auto", "mixed"):
+        p = _plan_mixed(N, L, eb, ceb, fx4_ceb, budget_bytes, shared_bytes=shared_bytes, b_dec=b_dec, b_fx4=b_fx4,
+                        t_res=t_res, window=kw.get("window"), allow_pinned=kw.get("allow_pinned", True))
+        if p is not None:
+            cands.append(p)
+
     def score(p):
         total = N * L
         d, pin = p.device_experts, p.pinned_experts
         host = total - d - pin
         link = p.link_bytes / b_link
-        if p.fused:
+        if p.fused == 2:
+            x = p.fx4_experts
+            sm = (d - x) * eb / b_dec + x * eb / p.fx4_rate + t_res * (total - x) / total
+        elif p.fused:
             sm = host * eb / b_dec + d * eb / p.fx4_rate + t_res * (total - d) / total
         else:
             sm = (host + d) * eb / b_dec + t_res
@@ -276,3 +293,66 @@ def plan_tiers(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *, fx
     best = min(cands, key=score)
     best.est_step_s = score(best)
     return best
+
+
+def _plan_mixed(N: int, L: int, eb: float, ceb: float, fx4_ceb: float, budget_bytes: float, *, shared_bytes: float,
+                b_dec: float, b_fx4: float, t_res: float, window: int | None = None, allow_pinned: bool = True,
+                min_window_bytes: float = 128 * 2**20):
+    """A mixed device tier: every streamed expert on the device tier, as many as fit in FX4
+    records (read in place by the decode-into-GEMM kernel, no ring block) and the rest in the
+    denser exponent-Huffman records (decoded into a two-window ring).  Nothing crosses the link,
+    so the host staging is released.  Fills the budgets between "all Huffman on the device tier"
+    and "all FX4 on the device tier", where the single-format plans leave experts on the host
+    tier (Mixtral 75%: 3 host experts in FX4 plans, all 256 on the device tier here).  None when
+    the budget cannot hold every streamed expert in Huffman records."""
+    total = N * L
+    cap = budget_bytes - shared_bytes
+    w = int(window or max(1, -(-min_window_bytes // eb)))
+    step = fx4_ceb - ceb
+    if step <= 0:
+        return None
+    best = None
+    for p in (range(0, total + 1) if allow_pinned else [0]):
+        p_layer = _balanced(p, N)
+        S = total - p
+        if S == 0:
+            break
+        # x FX4 experts; the ring holds two windows of the busiest layer's Huffman experts
+        room0 = cap - p * eb - S * ceb
+        x = int(min(S, (room0 - 2 * min(w, L) * eb) // step))
+        if x < 0:
+            continue
+        h_layer = _spaced(S - x, N)
+        ring = 2 * min(w, max(h_layer))
+        if ring < 2 * min(w, L):  # few Huffman experts per layer: a smaller ring, more FX4
+            x = int(min(S, (room0 - ring * eb) // step))
+            h_layer = _spaced(S - x, N)
+            ring = 2 * min(w, max(h_layer))
+        if S - x <= 0:
+            continue  # all FX4: the FX4 plan covers it
+        sm = (S - x) * eb / b_dec + x * eb / b_fx4 + t_res * (total - x) / total
+        key = (sm, -x)
+        if best is None or key < best[0]:
+            best = (key, p, x, ring, h_layer)
+    if best is None:
+        return None
+    (est, _), p, x, ring, h_layer = best
+    p_layer = _balanced(p, N)
+    pinned = np.zeros((N, L), dtype=bool)
+    device = np.zeros((N, L), dtype=bool)
+    fx4 = np.zeros((N, L), dtype=bool)
+    for l in range(N):
+        streamed = L - p_layer[l]
+        if p_layer[l]:
+            pinned[l, streamed:] = True
+        device[l, :streamed] = True
+        # Huffman experts spaced over the layer, so every ring window has FX4 experts fused beside it
+        h = min(h_layer[l], streamed)
+        fx4[l, :streamed] = True
+        for i in range(h):
+            fx4[l, int((i + 0.5) * streamed / h)] = False
+    x = int(fx4.sum())
+    hbm = ring * eb + p * eb + x * fx4_ceb + (device.sum() - x) * ceb + shared_bytes
+    plan = ResidencyPlan(ring, device, pinned, float(hbm), float(est), 0.0, 2, float((total - p) * eb))
+    plan.device_format, plan.fused, plan.fx4_rate, plan.fx4_mask = "mixed", 2, b_fx4, fx4
+    return plan

@@ -261,7 +261,7 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
       int u = 0;
       if (e < E) {
         const int n = s_off[e + 1] - s_off[e];
-        if (n > 0 && e < p.E_routed && p.dec[e].sm) {
+        if (n > 0 && e < p.E_routed && p.dec[e].sm && p.dec[e].fmt == (uint32_t)FMT && ((p.dec_fmt_mask >> FMT) & 1u)) {
           u = ((n + BN - 1) / BN) * MT * S;
           const int32_t ent = p.pt[e];
           if (pt_state(ent) != 2) {

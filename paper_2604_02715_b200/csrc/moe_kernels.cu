@@ -569,7 +569,8 @@ __global__ void __launch_bounds__(192, 1)
       int u = 0;
       if (e < E) {
         const int n = s_off[e + 1] - s_off[e];
-        if (n > 0 && !(p.dec && e < p.E_routed && p.dec[e].sm)) {  // fused groups: k_moe_gemm_dec
+        // groups read in place run in k_moe_gemm_dec
+        if (n > 0 && !(p.dec && e < p.E_routed && p.dec[e].sm && ((p.dec_fmt_mask >> p.dec[e].fmt) & 1u))) {
           u = ((n + BN - 1) / BN) * MT * S;
           if (e < p.E_routed) {
             const int32_t ent = p.pt[e];

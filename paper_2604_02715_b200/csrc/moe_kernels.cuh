@@ -88,6 +88,7 @@ struct GemmParams {
   // per group of the launch: groups whose record pointer is set run in the decode-into-GEMM
   // kernel and are skipped by k_moe_gemm (nullptr: no fused groups)
   const DecRec* dec;
+  uint32_t dec_fmt_mask;  // bit f: records of format f are read in place by k_moe_gemm_dec in this layer
 };
 
 // ---- launchers (moe_kernels.cu)

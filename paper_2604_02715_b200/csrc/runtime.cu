@@ -291,7 +291,7 @@ struct Ctx {
   // instead of being expanded into their ring block.  fused_mode: 0 off (default; external
   // compute such as the EP runner reads ring blocks), 1 on for the builtin compute;
   // fused_now: on for the current run/session (decode-sized groups, supported shape).
-  int fused_mode = 0;
+  int fused_mode = 0;  // 2: FX4 tensors in place, Huffman device-tier tensors expanded into the ring
   bool fused_now = false;
   // race hardening (xpgb_set_hazard_checks): poison every block a window maps with 0xFF
   // bytes (bf16 NaN) before its load, and optionally skip one step's WAR wait, so a WAR
@@ -300,9 +300,9 @@ struct Ctx {
   int war_sab_it = 0, war_sab_layer = 0;
   DecRec* d_decrec = nullptr;  // [N][2][E]: record of each device-tier tensor (sm == nullptr: not device tier)
   CUtensorMap* d_fxmaps = nullptr;  // [N*E*2][2]: FX4 sign/mantissa and nibble planes as TMA maps
-  // device-tier record format: 0 exponent-Huffman (the host pool's records, staged as they are),
-  // 1 FX4 (fx4.cuh: encoded on the GPU from the raw pool at staging, for decode-into-GEMM)
-  int dev_fmt = 0;
+  // device-tier record format per tensor [N*E*2]: 0 exponent-Huffman (the host pool's records,
+  // staged as they are), 1 FX4 (fx4.cuh: encoded on the GPU from the raw pool at staging)
+  std::vector<uint8_t> tfmt;
   std::vector<int> fx_base;         // [N*E*2] FX4 base exponent of each device-tier tensor
   std::vector<uint64_t> fx_bytes;   // [N*E*2] FX4 record bytes
 
@@ -542,15 +542,24 @@ static bool use_pair(Ctx* c, int T, int kk) {
 // Decode-into-GEMM for this run: builtin compute asked for it, a compressed device tier
 // exists, the shape is supported and the groups are decode-sized (1-CTA kernels).
 static bool fused_for(Ctx* c, int T, int top_k) {
-  return c->fused_mode == 1 && c->codec && c->d_decrec && c->pool == XPGB_POOL_RING &&
+  return c->fused_mode != 0 && c->codec && c->d_decrec && c->pool == XPGB_POOL_RING &&
          gemm_dec_supported(c->H, c->F, c->cchunk) && !use_pair(c, T, std::min(top_k, c->L));
+}
+
+static int fmt_of(const Ctx* c, size_t ti) { return c->tfmt.empty() ? 0 : c->tfmt[ti]; }
+
+// Device-tier formats read in place by this run's decode-into-GEMM launches (bit f: format f).
+static uint32_t fused_fmt_mask(const Ctx* c) {
+  if (!c->fused_now) return 0;
+  return c->fused_mode == 2 ? 2u : 3u;
 }
 
 // Is tensor (layer, local expert e, kind) read in place by the decode-into-GEMM kernel?
 static bool fused_tensor(const Ctx* c, int layer, int e, int kind) {
   if (!c->fused_now || e >= c->E) return false;
   const size_t ti = ((size_t)(layer - 1) * c->E + e) * 2 + (kind - 1);
-  return c->backend[ti] == 1 && c->pinned[(size_t)(layer - 1) * c->E + e] == 0;
+  return c->backend[ti] == 1 && c->pinned[(size_t)(layer - 1) * c->E + e] == 0 &&
+         ((fused_fmt_mask(c) >> fmt_of(c, ti)) & 1u);
 }
 
 // Profiled runs (c->cur_ev set by session_compute): events around each decode-into-GEMM launch.
@@ -572,13 +581,14 @@ static void fz_mark(Ctx* c, cudaStream_t s, uint64_t bytes, bool begin) {
 }
 
 // Record bytes the decode-into-GEMM launch of window [e0, e1), kind, reads in place.
-static uint64_t fused_bytes(Ctx* c, int layer, int e0, int e1, int kind) {
+static uint64_t fused_bytes(Ctx* c, int layer, int e0, int e1, int kind, int fmt) {
   uint64_t b = 0;
   for (int e = e0; e < std::min(e1, c->E); ++e) {
     if (!fused_tensor(c, layer, e, kind)) continue;
     const size_t ti = ((size_t)(layer - 1) * c->E + e) * 2 + (kind - 1);
+    if (fmt_of(c, ti) != fmt) continue;
     const uint64_t n = ((kind == 2) ? c->s2 : c->s1) / 2;
-    b += c->dev_fmt == 1 ? c->fx_bytes[ti] : xpgb_codec_record_bytes(n, c->rec_bits[ti], c->cchunk);
+    b += fmt_of(c, ti) == 1 ? c->fx_bytes[ti] : xpgb_codec_record_bytes(n, c->rec_bits[ti], c->cchunk);
   }
   return b;
 }
@@ -603,6 +613,7 @@ static GemmParams gemm_params(Ctx* c, int layer, int kind, const int32_t* offset
   p.H = c->H;
   p.splits = splits;
   p.dec = nullptr;
+  p.dec_fmt_mask = 0;
   return p;
 }
 
@@ -651,25 +662,35 @@ static void enqueue_window(Ctx* c, int layer, const float* x, float* y, int T, i
   }
   // decode-into-GEMM: the window's device-tier groups run in k_moe_gemm_dec, the rest
   // (ring blocks, pinned and shared experts) in k_moe_gemm, which skips the fused groups
-  bool fused[2] = {false, false}, rest[2] = {e1 > c->E, e1 > c->E};
+  // (one decode-into-GEMM launch per record format present in the window)
+  bool fused[2][2] = {{false, false}, {false, false}}, rest[2] = {e1 > c->E, e1 > c->E};  // [kind][fmt]
   if (!pair && c->fused_now) {
     for (int kind = 1; kind <= 2; ++kind)
-      for (int e = e0; e < std::min(e1, c->E); ++e) (fused_tensor(c, layer, e, kind) ? fused : rest)[kind - 1] = true;
+      for (int e = e0; e < std::min(e1, c->E); ++e) {
+        const size_t ti = ((size_t)(layer - 1) * c->E + e) * 2 + (kind - 1);
+        if (fused_tensor(c, layer, e, kind)) fused[kind - 1][fmt_of(c, ti)] = true;
+        else rest[kind - 1] = true;
+      }
     const DecRec* base = c->d_decrec + (size_t)(layer - 1) * 2 * c->E + e0;
-    if (fused[0]) pg.dec = base;
-    if (fused[1]) pd.dec = base + c->E;
+    pg.dec = base;
+    pd.dec = base + c->E;
+    pg.dec_fmt_mask = pd.dec_fmt_mask = fused_fmt_mask(c);
   } else {
     rest[0] = rest[1] = true;
   }
+  auto fused_launch = [&](bool gate_up, GemmParams& gp, const CUtensorMap& map, int kind) {
+    for (int f = 0; f < 2; ++f) {
+      if (!fused[kind - 1][f]) continue;
+      fz_mark(c, s, fused_bytes(c, layer, e0, e1, kind, f), true);
+      launch_gemm_dec(gate_up, map, gp, c->ctab, c->cchunk, pick_bn_dec(c, T, kk), c->num_sms, s, f == 1);
+      fz_mark(c, s, 0, false);
+    }
+  };
   if (pair)
     launch_gemm_pair(true, c->map_xp_pair, c->map_gu, c->S ? c->map_gu_sh : c->map_gu, pg, c->num_sms, s,
                      c->pair_split);
   else {
-    if (fused[0]) {
-      fz_mark(c, s, fused_bytes(c, layer, e0, e1, 1), true);
-      launch_gemm_dec(true, c->map_xp, pg, c->ctab, c->cchunk, pick_bn_dec(c, T, kk), c->num_sms, s, c->dev_fmt == 1);
-      fz_mark(c, s, 0, false);
-    }
+    fused_launch(true, pg, c->map_xp, 1);
     if (rest[0])
       launch_gate_up(c->map_gu, c->map_xp, c->S ? c->map_gu_sh : c->map_gu, pg, bn, c->num_sms, s, lean_gemm(c));
   }
@@ -679,11 +700,7 @@ static void enqueue_window(Ctx* c, int layer, const float* x, float* y, int T, i
     launch_gemm_pair(false, c->map_h_pair, c->map_dn, c->S ? c->map_dn_sh : c->map_dn, pd, c->num_sms, s,
                      c->pair_split);
   else {
-    if (fused[1]) {
-      fz_mark(c, s, fused_bytes(c, layer, e0, e1, 2), true);
-      launch_gemm_dec(false, c->map_h, pd, c->ctab, c->cchunk, pick_bn_dec(c, T, kk), c->num_sms, s, c->dev_fmt == 1);
-      fz_mark(c, s, 0, false);
-    }
+    fused_launch(false, pd, c->map_h, 2);
     if (rest[1])
       launch_down(c->map_dn, c->map_h, c->S ? c->map_dn_sh : c->map_dn, pd, bn_dn, c->num_sms, s, lean_gemm(c));
   }
@@ -1013,6 +1030,7 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
     // a staged run may take expert e' after e when its record follows e's in the pool
     auto joins_run = [&](int e, int e2, int tier) {
       return e2 < whi && !is_pinned(layer, e2) && c->backend[tix(e2)] == tier && delay_of(e2) <= 0.f &&
+             !(tier == 1 && fmt_of(c, tix(e2)) != 0) && !fused_tensor(c, layer, e2, kind) &&
              (tier == 1 || c->rec_off[tix(e2)] == c->rec_off[tix(e)] + rec_bytes(e));
     };
     DecodeTensor dt[kMaxDecodeTensors];
@@ -1026,7 +1044,7 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
       const size_t ti = tix(e);
       uint8_t* dst = block_ptr(c, kind, blocks[e]);
       const float dl = delay_of(e);
-      if (c->backend[ti] == 1 && c->dev_fmt == 1) {
+      if (c->backend[ti] == 1 && fmt_of(c, ti) == 1) {
         // FX4 device tier, expanded into the ring (groups the fused GEMM does not take)
         if (!dev_on_dv) CK(cudaStreamWaitEvent(dv, c->ev_mapped[k], 0));
         dev_on_dv = true;
@@ -1561,81 +1579,13 @@ static void run_impl(Ctx* c, const xpgb_run_opts* o, const float* x, float* y, x
   session_end(c, rep);
 }
 
-// FX4 device tier: every device-tier tensor is copied raw from the pinned pool into a scratch
-// buffer and encoded there by the GPU (histogram -> base, escape counts -> size, then the
-// record), straight into its slot of the device tier.  Two passes (sizes, then records), so the
-// allocation is exact.  Setup work: it synchronises.
-static void stage_device_tier_fx4(Ctx* c) {
-  if (!c->host) XFAIL(XPGB_ERR_BACKEND_MISS, "the FX4 device tier is encoded from the raw host pool");
-  const size_t nt = (size_t)c->N * c->E * 2;
-  c->fx_base.assign(nt, 0);
-  c->fx_bytes.assign(nt, 0);
-  bool any = false;
-  for (size_t ti = 0; ti < nt; ++ti) any |= c->backend[ti] != 0;
-  if (!any) return;
-  const uint64_t maxraw = std::max(c->s1, c->s2);
-  uint8_t* raw = nullptr;
-  uint32_t* scratch = nullptr;
-  CK(cudaMalloc(&raw, maxraw));
-  CK(cudaMalloc(&scratch, xpgb_fx4_scratch_bytes(maxraw / 2)));
-  cudaStream_t s = c->s_copy[0];
-  auto src_of = [&](size_t ti) { return c->host + (ti / 2) * (c->s1 + c->s2) + ((ti & 1) ? c->s1 : 0); };
-  uint64_t total = 0;
-  for (size_t ti = 0; ti < nt; ++ti) {
-    if (!c->backend[ti]) continue;
-    const uint64_t sz = (ti & 1) ? c->s2 : c->s1;
-    CK(cudaMemcpyAsync(raw, src_of(ti), sz, cudaMemcpyHostToDevice, s));
-    int base = 0;
-    uint64_t esc = 0;
-    fx4_count(reinterpret_cast<const uint16_t*>(raw), sz / 2, scratch, &base, &esc, s);
-    CKLAUNCH();
-    c->fx_base[ti] = base;
-    c->fx_bytes[ti] = fx_layout(sz / 2, esc).total;
-    total += (c->fx_bytes[ti] + 255) & ~255ull;
-  }
-  CK(cudaMalloc(&c->dev_tier, total + 256));
-  uint64_t at = 0;
-  for (size_t ti = 0; ti < nt; ++ti) {
-    if (!c->backend[ti]) continue;
-    const uint64_t sz = (ti & 1) ? c->s2 : c->s1;
-    CK(cudaMemcpyAsync(raw, src_of(ti), sz, cudaMemcpyHostToDevice, s));
-    c->dev_off[ti] = (int64_t)at;
-    fx4_encode(reinterpret_cast<const uint16_t*>(raw), sz / 2, c->fx_base[ti], scratch, c->dev_tier + at, s);
-    CKLAUNCH();
-    at += (c->fx_bytes[ti] + 255) & ~255ull;
-  }
-  CK(cudaStreamSynchronize(s));
-  cudaFree(raw);
-  cudaFree(scratch);
-  // TMA maps of every FX4 tensor's planes: the decode-into-GEMM kernel stages a stage's rows of
-  // sign/mantissa bytes and nibbles with them (64-B / 32-B swizzles, decoder reads spread banks)
-  std::vector<CUtensorMap> maps(nt * 2);
-  for (size_t ti = 0; ti < nt; ++ti) {
-    if (!c->backend[ti]) continue;
-    const uint64_t rows = (ti & 1) ? (uint64_t)c->H : 2ull * c->F, K = (ti & 1) ? (uint64_t)c->F : (uint64_t)c->H;
-    const uint8_t* rec = c->dev_tier + c->dev_off[ti];
-    const FxLayout L = fx_layout(rows * K, 0);
-    maps[2 * ti] = make_map_u8(rec, rows, K, 64, CU_TENSOR_MAP_SWIZZLE_64B);
-    maps[2 * ti + 1] = make_map_u8(rec + L.nib, rows, K / 2, 32, CU_TENSOR_MAP_SWIZZLE_32B);
-  }
-  CK(cudaMalloc(&c->d_fxmaps, maps.size() * sizeof(CUtensorMap)));
-  CK(cudaMemcpy(c->d_fxmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
-  std::vector<DecRec> recs(nt / 2 * 2);
-  memset(recs.data(), 0, recs.size() * sizeof(DecRec));
-  for (size_t ti = 0; ti < nt; ++ti) {
-    if (!c->backend[ti]) continue;
-    const uint64_t n = ((ti & 1) ? c->s2 : c->s1) / 2;
-    const FxLayout L = fx_layout(n, 0);
-    const uint8_t* rec = c->dev_tier + c->dev_off[ti];
-    const size_t layer0 = ti / 2 / c->E, e = ti / 2 % c->E, k = ti & 1;
-    recs[(layer0 * 2 + k) * c->E + e] =
-        DecRec{rec, reinterpret_cast<const uint32_t*>(rec + L.nib), reinterpret_cast<const uint32_t*>(rec + L.idx),
-               (uint32_t)c->fx_base[ti], 1u, rec + L.esc, c->d_fxmaps + 2 * ti};
-  }
-  CK(cudaMalloc(&c->d_decrec, recs.size() * sizeof(DecRec)));
-  CK(cudaMemcpy(c->d_decrec, recs.data(), recs.size() * sizeof(DecRec), cudaMemcpyHostToDevice));
-}
-
+// The compressed device tier: every device-tier tensor in the record format tfmt[ti] names --
+// exponent-Huffman records copied from the host pool as they are (the reference's device tier),
+// or FX4 records encoded by the GPU from the raw pool (copied raw into a scratch buffer; histogram
+// -> base, escape counts -> size, then the record, straight into its slot).  Two passes over the
+// FX4 tensors (sizes, then records), so the allocation is exact.  Setup work: it synchronises.
+// Also builds the decode-into-GEMM kernel's record table and, for FX4 tensors, the TMA maps of
+// their sign/mantissa and nibble planes.
 static void stage_device_tier(Ctx* c) {
   if (c->dev_tier) {
     cudaFree(c->dev_tier);
@@ -1649,51 +1599,108 @@ static void stage_device_tier(Ctx* c) {
     cudaFree(c->d_fxmaps);
     c->d_fxmaps = nullptr;
   }
-  const size_t pages = (size_t)c->N * c->E;
-  auto tensor_bytes = [&](size_t ti) -> uint64_t {
+  const size_t pages = (size_t)c->N * c->E, nt = pages * 2;
+  if (c->tfmt.size() != nt) c->tfmt.assign(nt, 0);
+  c->fx_base.assign(nt, 0);
+  c->fx_bytes.assign(nt, 0);
+  std::fill(c->dev_off.begin(), c->dev_off.end(), -1);
+  auto huff_bytes = [&](size_t ti) -> uint64_t {
     const uint64_t raw = (ti & 1) ? c->s2 : c->s1;
     if (!c->codec) return raw;
     return xpgb_codec_record_bytes(raw / 2, c->rec_bits[ti], c->cchunk);
   };
-  std::fill(c->dev_off.begin(), c->dev_off.end(), -1);
-  if (c->dev_fmt == 1) {
-    stage_device_tier_fx4(c);
-    return;
+  auto is_fx = [&](size_t ti) { return c->backend[ti] && c->codec && c->tfmt[ti] == 1; };
+  auto raw_src = [&](size_t ti) { return c->host + (ti / 2) * (c->s1 + c->s2) + ((ti & 1) ? c->s1 : 0); };
+  bool any = false, any_fx = false;
+  for (size_t ti = 0; ti < nt; ++ti) {
+    any |= c->backend[ti] != 0;
+    any_fx |= is_fx(ti);
+  }
+  if (!any) return;
+  if (!c->codec && !c->host) XFAIL(XPGB_ERR_BACKEND_MISS, "device-tier staging needs the host pool");
+  if (any_fx && !c->host) XFAIL(XPGB_ERR_BACKEND_MISS, "the FX4 device tier is encoded from the raw host pool");
+  const uint64_t maxraw = std::max(c->s1, c->s2);
+  uint8_t* raw = nullptr;
+  uint32_t* scratch = nullptr;
+  cudaStream_t s = c->s_copy[0];
+  if (any_fx) {
+    CK(cudaMalloc(&raw, maxraw));
+    CK(cudaMalloc(&scratch, xpgb_fx4_scratch_bytes(maxraw / 2)));
   }
   uint64_t total = 0;
-  for (size_t ti = 0; ti < pages * 2; ++ti)
-    if (c->backend[ti]) total += (tensor_bytes(ti) + 255) & ~255ull;
-  if (total == 0) return;
-  if (!c->codec && !c->host) XFAIL(XPGB_ERR_BACKEND_MISS, "device-tier staging needs the host pool");
+  for (size_t ti = 0; ti < nt; ++ti) {
+    if (!c->backend[ti]) continue;
+    if (is_fx(ti)) {
+      const uint64_t sz = (ti & 1) ? c->s2 : c->s1;
+      CK(cudaMemcpyAsync(raw, raw_src(ti), sz, cudaMemcpyHostToDevice, s));
+      int base = 0;
+      uint64_t esc = 0;
+      fx4_count(reinterpret_cast<const uint16_t*>(raw), sz / 2, scratch, &base, &esc, s);
+      CKLAUNCH();
+      c->fx_base[ti] = base;
+      c->fx_bytes[ti] = fx_layout(sz / 2, esc).total;
+      total += (c->fx_bytes[ti] + 255) & ~255ull;
+    } else {
+      total += (huff_bytes(ti) + 255) & ~255ull;
+    }
+  }
   CK(cudaMalloc(&c->dev_tier, total + 256));  // slack: stream readers fetch 16-byte blocks ahead
   uint64_t at = 0;
-  for (size_t ti = 0; ti < pages * 2; ++ti) {
+  for (size_t ti = 0; ti < nt; ++ti) {
     if (!c->backend[ti]) continue;
-    const uint64_t sz = tensor_bytes(ti);
-    const uint8_t* src = c->codec ? c->cpool + c->rec_off[ti]
-                                  : c->host + (ti / 2) * (c->s1 + c->s2) + ((ti & 1) ? c->s1 : 0);
     c->dev_off[ti] = (int64_t)at;
-    CK(cudaMemcpy(c->dev_tier + at, src, sz, cudaMemcpyHostToDevice));
-    at += (sz + 255) & ~255ull;
-  }
-  if (c->codec) {
-    // records of the device tier as the decode-into-GEMM kernel reads them, [layer][kind][expert]
-    std::vector<DecRec> recs((size_t)c->N * 2 * c->E);
-    memset(recs.data(), 0, recs.size() * sizeof(DecRec));
-    for (size_t ti = 0; ti < pages * 2; ++ti) {
-      if (!c->backend[ti]) continue;
-      const uint64_t n = ((ti & 1) ? c->s2 : c->s1) / 2;
-      const uint64_t sm16 = (n + 15) & ~15ull, bits16 = (c->rec_bits[ti] + 8 + 15) & ~15ull;
-      const uint8_t* rec = c->dev_tier + c->dev_off[ti];
-      const size_t layer0 = ti / 2 / c->E, e = ti / 2 % c->E, k = ti & 1;
-      recs[(layer0 * 2 + k) * c->E + e] = DecRec{rec, reinterpret_cast<const uint32_t*>(rec + sm16),
-                                                 reinterpret_cast<const uint32_t*>(rec + sm16 + bits16), 0u, 0u,
-                                                 nullptr, nullptr};
+    if (is_fx(ti)) {
+      const uint64_t sz = (ti & 1) ? c->s2 : c->s1;
+      CK(cudaMemcpyAsync(raw, raw_src(ti), sz, cudaMemcpyHostToDevice, s));
+      fx4_encode(reinterpret_cast<const uint16_t*>(raw), sz / 2, c->fx_base[ti], scratch, c->dev_tier + at, s);
+      CKLAUNCH();
+      at += (c->fx_bytes[ti] + 255) & ~255ull;
+    } else {
+      const uint64_t sz = huff_bytes(ti);
+      const uint8_t* src = c->codec ? c->cpool + c->rec_off[ti] : raw_src(ti);
+      CK(cudaMemcpyAsync(c->dev_tier + at, src, sz, cudaMemcpyHostToDevice, s));
+      at += (sz + 255) & ~255ull;
     }
-    if (c->d_decrec) cudaFree(c->d_decrec);
-    CK(cudaMalloc(&c->d_decrec, recs.size() * sizeof(DecRec)));
-    CK(cudaMemcpy(c->d_decrec, recs.data(), recs.size() * sizeof(DecRec), cudaMemcpyHostToDevice));
   }
+  CK(cudaStreamSynchronize(s));
+  if (raw) cudaFree(raw);
+  if (scratch) cudaFree(scratch);
+  if (!c->codec) return;
+  // records as the decode-into-GEMM kernel reads them, [layer][kind][expert]; TMA maps of every
+  // FX4 tensor's planes (64-B / 32-B swizzles so the decoders' row reads spread banks)
+  std::vector<CUtensorMap> maps(nt * 2);
+  if (any_fx) {
+    for (size_t ti = 0; ti < nt; ++ti) {
+      if (!is_fx(ti)) continue;
+      const uint64_t rows = (ti & 1) ? (uint64_t)c->H : 2ull * c->F, K = (ti & 1) ? (uint64_t)c->F : (uint64_t)c->H;
+      const uint8_t* rec = c->dev_tier + c->dev_off[ti];
+      const FxLayout L = fx_layout(rows * K, 0);
+      maps[2 * ti] = make_map_u8(rec, rows, K, 64, CU_TENSOR_MAP_SWIZZLE_64B);
+      maps[2 * ti + 1] = make_map_u8(rec + L.nib, rows, K / 2, 32, CU_TENSOR_MAP_SWIZZLE_32B);
+    }
+    CK(cudaMalloc(&c->d_fxmaps, maps.size() * sizeof(CUtensorMap)));
+    CK(cudaMemcpy(c->d_fxmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+  }
+  std::vector<DecRec> recs(nt);
+  memset(recs.data(), 0, recs.size() * sizeof(DecRec));
+  for (size_t ti = 0; ti < nt; ++ti) {
+    if (!c->backend[ti]) continue;
+    const uint64_t n = ((ti & 1) ? c->s2 : c->s1) / 2;
+    const uint8_t* rec = c->dev_tier + c->dev_off[ti];
+    const size_t layer0 = ti / 2 / c->E, e = ti / 2 % c->E, k = ti & 1;
+    DecRec& r = recs[(layer0 * 2 + k) * c->E + e];
+    if (is_fx(ti)) {
+      const FxLayout L = fx_layout(n, 0);
+      r = DecRec{rec, reinterpret_cast<const uint32_t*>(rec + L.nib), reinterpret_cast<const uint32_t*>(rec + L.idx),
+                 (uint32_t)c->fx_base[ti], 1u, rec + L.esc, c->d_fxmaps + 2 * ti};
+    } else {
+      const uint64_t sm16 = (n + 15) & ~15ull, bits16 = (c->rec_bits[ti] + 8 + 15) & ~15ull;
+      r = DecRec{rec, reinterpret_cast<const uint32_t*>(rec + sm16),
+                 reinterpret_cast<const uint32_t*>(rec + sm16 + bits16), 0u, 0u, nullptr, nullptr};
+    }
+  }
+  CK(cudaMalloc(&c->d_decrec, recs.size() * sizeof(DecRec)));
+  CK(cudaMemcpy(c->d_decrec, recs.data(), recs.size() * sizeof(DecRec), cudaMemcpyHostToDevice));
 }
 
 // Staging ring and device-resident chunk index of the compressed host tier (on), or neither
@@ -2366,7 +2373,7 @@ int xpgb_hbm_bytes(xpgb_ctx* h, uint64_t* ring, uint64_t* staging, uint64_t* dev
     for (size_t ti = 0; ti < nt && c->dev_tier; ++ti)
       if (c->backend[ti]) {
         const uint64_t raw = (ti & 1) ? c->s2 : c->s1;
-        dt += c->dev_fmt == 1 ? c->fx_bytes[ti]
+        dt += (c->codec && fmt_of(c, ti) == 1) ? c->fx_bytes[ti]
               : c->codec      ? xpgb_codec_record_bytes(raw / 2, c->rec_bits[ti], c->cchunk)
                               : raw;
       }
@@ -2478,10 +2485,27 @@ int xpgb_set_device_format(xpgb_ctx* h, int32_t format) {
     Ctx* c = &h->c;
     if (c->sess && c->sess->active) XFAIL(XPGB_ERR, "cannot change the device-tier format during a session");
     if (format < 0 || format > 1) XFAIL(XPGB_ERR_OUT_OF_RANGE, "device-tier format %d: need 0 (Huffman) or 1 (FX4)", format);
-    if (format == c->dev_fmt) return;
+    const size_t nt = (size_t)c->N * c->E * 2;
+    if (c->tfmt.size() == nt && std::all_of(c->tfmt.begin(), c->tfmt.end(), [&](uint8_t f) { return f == format; }))
+      return;
     CK(cudaDeviceSynchronize());
-    c->dev_fmt = format;
+    c->tfmt.assign(nt, (uint8_t)format);
     if (c->codec) stage_device_tier(c);  // re-stage whatever is placed on the device tier
+  });
+}
+
+int xpgb_set_device_formats(xpgb_ctx* h, const uint8_t* formats) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    if (c->sess && c->sess->active) XFAIL(XPGB_ERR, "cannot change the device-tier format during a session");
+    if (!formats) XFAIL(XPGB_ERR_CONFIG, "formats is null");
+    const size_t nt = (size_t)c->N * c->E * 2;
+    for (size_t ti = 0; ti < nt; ++ti)
+      if (formats[ti] > 1) XFAIL(XPGB_ERR_OUT_OF_RANGE, "tensor %zu: device-tier format %d: need 0 or 1", ti, (int)formats[ti]);
+    if (c->tfmt.size() == nt && std::equal(c->tfmt.begin(), c->tfmt.end(), formats)) return;
+    CK(cudaDeviceSynchronize());
+    c->tfmt.assign(formats, formats + nt);
+    if (c->codec) stage_device_tier(c);
   });
 }
 
@@ -2489,7 +2513,7 @@ int xpgb_set_fused_decode(xpgb_ctx* h, int32_t mode) {
   return guard([&] {
     Ctx* c = &h->c;
     if (c->sess && c->sess->active) XFAIL(XPGB_ERR, "cannot switch decode-into-GEMM during a session");
-    if (mode < 0 || mode > 1) XFAIL(XPGB_ERR_OUT_OF_RANGE, "fused decode mode %d: need 0 or 1", mode);
+    if (mode < 0 || mode > 2) XFAIL(XPGB_ERR_OUT_OF_RANGE, "fused decode mode %d: need 0, 1 or 2", mode);
     c->fused_mode = mode;
   });
 }

@@ -163,13 +163,21 @@ class Context:
         call("xpgb_set_device_format", self._h, 1 if fmt == "fx4" else 0)
         self._dev_fmt = fmt
 
+    def set_device_formats(self, fx4_mask: np.ndarray) -> None:
+        """Per-tensor device-tier format: ``fx4_mask`` [layers, experts, 2] (gate/up, down) true
+        where the record is FX4, false for exponent-Huffman (xpgb_set_device_formats)."""
+        arr = np.ascontiguousarray(fx4_mask, dtype=np.uint8)
+        call("xpgb_set_device_formats", self._h, arr.ctypes.data_as(C.POINTER(C.c_uint8)))
+        self._dev_fmt = "mixed" if 0 < arr.sum() < arr.size else ("fx4" if arr.size and arr.all() else "huffman")
+
     def set_host_staging(self, on: bool) -> None:
         """Allocate / release the compressed host tier's staging ring and chunk index."""
         call("xpgb_set_host_staging", self._h, 1 if on else 0)
 
-    def set_fused_decode(self, on: bool) -> None:
-        """Decode-into-GEMM for the builtin compute: device-tier experts read in place."""
-        call("xpgb_set_fused_decode", self._h, 1 if on else 0)
+    def set_fused_decode(self, on) -> None:
+        """Decode-into-GEMM for the builtin compute: device-tier experts read in place
+        (True / 1); 2 = only FX4 records in place, Huffman records decoded into the ring."""
+        call("xpgb_set_fused_decode", self._h, int(on))
 
     def set_stage_buffers(self, n: int) -> None:
         """Staging ring of the compressed host tier: ``n`` buffers per kind (link run-ahead)."""

@@ -333,12 +333,19 @@ class StreamedRunner:
         """Apply a budget.ResidencyPlan -- pinned experts, ring size and depth, device-tier
         experts (and, for budget.plan_tiers plans, the device tier's record format and
         decode-into-GEMM) -- replacing whatever residency state an earlier plan left."""
-        if getattr(plan, "device_format", None) and plan.device_format != self.device_format:
-            self.set_device_format(plan.device_format)
-        if getattr(plan, "fused", None) is not None:
-            self.ctx.set_fused_decode(bool(plan.fused))
         spec = self.hierarchy.container.spec
         first, count = self._shard
+        fmt = getattr(plan, "device_format", None)
+        if fmt == "mixed":
+            # per-expert record format (both tensors of an expert alike), FX4 read in place
+            fx4 = np.zeros((self.spec.num_layers, self.spec.experts_per_layer), dtype=bool)
+            fx4[:, first:first + count] = np.asarray(plan.fx4_mask).reshape(spec.num_layers, spec.experts_per_layer)
+            self.ctx.set_device_formats(np.repeat(fx4[:, :, None], 2, axis=2))
+            self.device_format = "mixed"
+        elif fmt and fmt != self.device_format:
+            self.set_device_format(fmt)
+        if getattr(plan, "fused", None) is not None:
+            self.ctx.set_fused_decode(int(plan.fused))
         full = np.zeros((self.spec.num_layers, self.spec.experts_per_layer), dtype=np.uint8)
         full[:, first:first + count] = plan.pinned_mask.reshape(spec.num_layers, spec.experts_per_layer)
         streamed = spec.experts_per_layer - plan.pinned_mask.sum(axis=1).min()

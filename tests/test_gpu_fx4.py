@@ -137,3 +137,72 @@ def test_host_staging_released_when_no_host_tier(X):
     runner.ctx.set_pinned(np.zeros((N, L), dtype=np.uint8))
     with pytest.raises(XpgError):
         runner.ctx.set_host_staging(False)
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("T,host_codec", [(16, False), (40, True), (100, True)])
+def test_mixed_device_tier_stack_equals_resident(X, mode, T, host_codec):
+    """Per-tensor formats (xpgb_set_device_formats): FX4 and Huffman records side by side on the
+    device tier -- gate/up and down of one expert may differ -- decoded into the ring (mode 0),
+    all read in place (1), or FX4 in place and Huffman into the ring (2): byte-identical."""
+    spec = X.ModelSpec(4, 8, 256, 512)
+    fwd = X.ForwardSpec(T, 2, 7)
+    container = X.generate_synthetic_model(spec, 7)
+    backends = [X.Backend(1, X.BackendKind.COMPRESSED_DEVICE, 300e9, 1 << 50),
+                X.Backend(2, X.BackendKind.HOST_OFFLOAD, 30e9, 1 << 50)]
+    hier = X.StorageHierarchy(container, None, X.plan_placement(spec, backends, alpha=0.75 if host_codec else 1.0),
+                              backends)
+    x = np.random.default_rng(T).standard_normal((T, spec.hidden_dim), dtype=np.float32)
+    runner = X.StreamedRunner(spec, hier, fwd, host_codec=host_codec)
+    fmts = np.random.default_rng(T + mode).random((spec.num_layers, spec.experts_per_layer, 2)) < 0.5
+    runner.ctx.set_device_formats(fmts)
+    runner.ctx.set_fused_decode(mode)
+    rep = runner.run(2, acts=x.copy())
+    assert rep.page_fault is None and rep.violations == []
+    base = X.resident_baseline(2, spec, container, fwd, acts=x.copy())
+    assert np.asarray(rep.final_activations).tobytes() == np.asarray(base).tobytes()
+    # both formats staged: bigger than all-Huffman, smaller than all-FX4
+    mixed = runner.ctx.hbm_bytes()["device_tier"]
+    runner.ctx.set_device_format("huffman")
+    huff = runner.ctx.hbm_bytes()["device_tier"]
+    runner.ctx.set_device_format("fx4")
+    assert huff < mixed < runner.ctx.hbm_bytes()["device_tier"]
+    rep = runner.run(2, acts=x.copy())
+    assert np.asarray(rep.final_activations).tobytes() == np.asarray(base).tobytes()
+
+
+def test_mixed_plan_full_shape_equals_resident(X):
+    """The planner's mixed device tier (budget.plan_tiers) applied to two Mixtral-shaped layers at
+    T = 256: every expert on the device tier, FX4 in place beside Huffman into the ring, no host
+    record streamed, byte-identical to the resident model."""
+    import torch
+
+    from paper_2604_02715_b200.budget import fx4_expert_bytes, plan_tiers
+    from paper_2604_02715_b200.exponent_codec import CompressedModel
+
+    spec = X.ModelSpec(2, 8, 4096, 14336)
+    T = 256
+    fwd = X.ForwardSpec(T, 2, 7)
+    container = X.generate_fast_model(spec, 7)
+    backends = [X.Backend(1, X.BackendKind.HOST_OFFLOAD, 30e9, 1 << 50)]
+    hier = X.StorageHierarchy(container, CompressedModel.from_container(container),
+                              X.plan_placement(spec, backends), backends)
+    runner = X.StreamedRunner(spec, hier, fwd, host_codec=True)
+    N, L, eb = 2, 8, spec.expert_bytes
+    ceb = runner.device_tier_bytes(L) / (N * L) * 1.002
+    fx = fx4_expert_bytes(4096, 14336) * 1.002
+    budget = (N * L * ceb + 2 * eb + 5 * (fx - ceb)) * 1.001  # room for 5 FX4 conversions
+    plan = plan_tiers(N, L, eb, ceb, budget, fx4_ceb=fx, device_format="mixed", units_per_expert=112)
+    assert plan.device_format == "mixed" and plan.host_experts == 0 and 0 < plan.fx4_experts < N * L
+    runner.apply_plan(plan)
+    assert runner.ctx.hbm_bytes()["staging"] == 0
+    x = torch.from_numpy(np.random.default_rng(3).standard_normal((T, 4096), dtype=np.float32)).cuda()
+    rep = runner.run(2, acts=x.clone(), profile=True)
+    assert rep.page_fault is None and rep.violations == [] and rep.h2d_bytes == 0
+    assert runner.ctx.fused_stats()["launches"] > 0 and rep.decoded_bytes > 0
+    paged = rep.final_activations.cpu().numpy()
+    del runner
+    torch.cuda.empty_cache()
+    model = X.ResidentModel(spec, container, max_tokens=T)
+    y, _ = model.run(2, fwd, x.clone())
+    assert paged.tobytes() == y.cpu().numpy().tobytes()

@@ -301,3 +301,37 @@ def test_residency_plan_spaces_host_experts_and_picks_depth():
               plan_residency(8, 8, eb, ceb, 0.8 * 64 * eb).pinned_mask)).sum() == 0
     assert plan_residency(8, 8, eb, ceb, 0.25 * 64 * eb).depth == 1
     assert plan_residency(8, 8, eb, ceb, 0.8 * 64 * eb).depth == 2
+
+
+def test_tier_plan_mixed_device_tier_between_the_formats():
+    """budget.plan_tiers: between the budget that holds every streamed expert in Huffman records
+    and the one that holds them all in FX4, the mixed plan keeps every expert on the device tier
+    (no host record crosses the link), spends the budget on FX4 conversions, and stays within it."""
+    import numpy as np
+
+    from paper_2604_02715_b200.budget import fx4_expert_bytes, plan_tiers
+
+    H, F, N, L = 4096, 14336, 32, 8
+    eb = 3 * H * F * 2
+    ceb, fx = 0.6655 * 1.012 * eb, fx4_expert_bytes(H, F)
+    seen = []
+    prev = None
+    for b in (0.65, 0.7, 0.72, 0.75, 0.78, 0.8):
+        pl = plan_tiers(N, L, eb, ceb, b * N * L * eb, fx4_ceb=fx, overhead_bytes=0.8e9, units_per_expert=F // 128)
+        assert pl.hbm_bytes <= b * N * L * eb + 1
+        if prev is not None:
+            assert pl.est_step_s <= prev + 1e-12
+        prev = pl.est_step_s
+        seen.append(pl.device_format)
+        if pl.device_format == "mixed":
+            assert pl.host_experts == 0 and pl.link_bytes == 0 and pl.fused == 2
+            assert 0 < pl.fx4_experts < pl.device_experts
+            assert not (pl.fx4_mask & ~pl.device_mask).any()
+            # every layer keeps its Huffman experts spread out: no two adjacent in a layer
+            huff = pl.device_mask & ~pl.fx4_mask
+            for l in range(N):
+                idx = np.flatnonzero(huff[l])
+                assert len(idx) < 2 or np.diff(idx).min() >= 2 or len(idx) > L // 2
+    assert "mixed" in seen and seen[-1] == "fx4"
+    pl = plan_tiers(N, L, eb, ceb, 0.72 * N * L * eb, fx4_ceb=fx, device_format="mixed", units_per_expert=F // 128)
+    assert pl.device_format == "mixed"
