@@ -125,6 +125,9 @@ def parity_summary():
             "per_config": out, "source": "profiles/r2_parity_fullshape.jsonl"}
 
 
+PROFILE_EVERY = 7  # odd: gate/up and down decoder launches alternate
+
+
 def decoder_roofline(stats, steps, step_s, hbm_peak, hbm_src):
     """Roofline of the exponent decoder (the dominant kernel of a paged decode step): its
     algorithmic bytes per launch over its mean launch time, both over the timed run."""
@@ -471,6 +474,8 @@ def main():
     ap.add_argument("--ref-sample-tokens", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-resident", action="store_true")
+    ap.add_argument("--no-timed-profile", action="store_true",
+                    help="A/B only: time the paged run without its per-launch events (no kernel rooflines)")
     ap.add_argument("--ep", action="store_true", help="use the expert-parallel runner even at N=1")
     ap.add_argument("--transport", default="auto", choices=["auto", "p2p", "nccl"],
                     help="EP dispatch/combine: peer-memory scatter kernels (p2p), NCCL all_to_all, or p2p when "
@@ -663,7 +668,9 @@ def main():
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         ev0.record()
-        rep = runner.run(args.steps, acts=x_dev, profile=True)
+        # light profile: events around 1 in 7 decoder / decode-into-GEMM launches (the kernel
+        # rooflines below); per-launch events on every launch cost 1-18% of the step
+        rep = runner.run(args.steps, acts=x_dev, profile=0 if args.no_timed_profile else PROFILE_EVERY)
         ev1.record()
         torch.cuda.synchronize()
         launches = kernel_launches() - launches0
@@ -828,8 +835,8 @@ def main():
         "clocks": clocks.summary(),
         "model_gen_s": gen_s,
     }
-    if not args.no_resident and not use_ep:
-        line["paged_kernels"] = paged_kern
+    if not args.no_resident and not use_ep and any(paged_kern.get(k) for k in ("gate_up_ns", "down_ns")):
+        line["paged_kernels"] = paged_kern  # per-step events: only when the timed run profiles every launch
     if not use_ep and raw_path is not None:
         line["raw_host_tier"] = raw_path
     if use_ep:

@@ -106,7 +106,11 @@ typedef struct xpgb_run_opts {
   const float* fetch_delay_s;   /* optional [N][L][2] seconds per tensor (delay_fn hook), host memory */
   const float* compute_delay_s; /* optional [iterations][N] seconds (compute_delay_fn hook), host memory */
   int32_t log_enable;        /* record the ordering log (default on) */
-  int32_t profile;           /* time every MoE kernel launch with CUDA events (report.kern_*) */
+  int32_t profile;           /* 1: time every MoE kernel launch with CUDA events (report.kern_*,
+                              * decoder / decode-into-GEMM stats); n >= 2: events around 1 in n
+                              * decoder and decode-into-GEMM launches only (stats scaled to every
+                              * launch; a light profile for timed runs -- use an odd n so both kinds
+                              * are sampled) */
   int32_t fresh_inputs;      /* 1: every iteration starts from activations the caller wrote into acts_dev
                                 (a serving session: step(acts) per decode step); 0: iteration i+1 consumes
                                 iteration i's output, as run() does */

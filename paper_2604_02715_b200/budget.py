@@ -22,6 +22,7 @@ stay contiguous in the pool).
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -346,11 +347,17 @@ def _plan_mixed(N: int, L: int, eb: float, ceb: float, fx4_ceb: float, budget_by
         if p_layer[l]:
             pinned[l, streamed:] = True
         device[l, :streamed] = True
-        # Huffman experts spaced over the layer, so every ring window has FX4 experts fused beside it
+        # Huffman experts first, FX4 after: the layer's last window is one wide decode-into-GEMM
+        # launch over every FX4 expert, beside which the next layer's first Huffman decodes run
+        # (Mixtral 75%: 17.4 K tok/s; Huffman experts spread one per window, each window then
+        # a 1-expert fused launch: 14.5 K -- profiles/r2_mixed_layout_ab.jsonl)
         h = min(h_layer[l], streamed)
         fx4[l, :streamed] = True
-        for i in range(h):
-            fx4[l, int((i + 0.5) * streamed / h)] = False
+        if os.environ.get("XPGB_MIXED_LAYOUT") == "spread":  # A/B only
+            for i in range(h):
+                fx4[l, int((i + 0.5) * streamed / h)] = False
+        else:
+            fx4[l, :h] = False
     x = int(fx4.sum())
     hbm = ring * eb + p * eb + x * fx4_ceb + (device.sum() - x) * ceb + shared_bytes
     plan = ResidencyPlan(ring, device, pinned, float(hbm), float(est), 0.0, 2, float((total - p) * eb))

@@ -132,7 +132,7 @@ struct PtOp {
   int32_t* log_count;
   int32_t log_cap;
   int32_t n_rec;
-  int32_t rec[2][7];  // event, it, layer, kind, target_it, target_layer, group word
+  int32_t rec[3][7];  // event, it, layer, kind, target_it, target_layer, group word
   int32_t vals[448];
 };
 static_assert(sizeof(PtOp) < 4000, "kernel parameter block too large");
@@ -163,7 +163,8 @@ __global__ void k_pt_op(PtOp op) {
   for (int i = threadIdx.x; i < op.set_n; i += blockDim.x) op.set_row[i] = op.vals[i];
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0 && op.log && op.n_rec > 1) write_record(op.log, op.log_count, op.log_cap, op.rec[1]);
+  if (threadIdx.x == 0 && op.log)
+    for (int i = 1; i < op.n_rec; ++i) write_record(op.log, op.log_count, op.log_cap, op.rec[i]);
 }
 
 __global__ void k_sleep(uint64_t ns) {
@@ -320,6 +321,10 @@ struct Ctx {
   std::vector<cudaEvent_t> fz_ev;
   std::vector<uint64_t> fz_bytes;
   size_t fz_n = 0;
+  // sampled profiling (opts.profile >= 2): events bracket 1 in prof_every decoder / fused launches
+  int prof_every = 1, prof_mode = 0;
+  size_t dec_seen = 0, fz_seen = 0;
+  bool dec_skip = false, fz_skip = false;
   double fz_total_ns = 0;
   uint64_t fz_total_bytes = 0, fz_launches = 0;
   size_t dec_n = 0;
@@ -564,8 +569,10 @@ static bool fused_tensor(const Ctx* c, int layer, int e, int kind) {
 
 // Profiled runs (c->cur_ev set by session_compute): events around each decode-into-GEMM launch.
 static void fz_mark(Ctx* c, cudaStream_t s, uint64_t bytes, bool begin) {
-  if (!c->cur_ev) return;
+  if (!c->prof_mode) return;
   if (begin) {
+    c->fz_skip = (c->fz_seen++ % (size_t)c->prof_every) != 0;
+    if (c->fz_skip) return;
     while (c->fz_ev.size() < 2 * (c->fz_n + 1)) {
       cudaEvent_t e;
       CK(cudaEventCreate(&e));
@@ -575,6 +582,7 @@ static void fz_mark(Ctx* c, cudaStream_t s, uint64_t bytes, bool begin) {
     c->fz_bytes[c->fz_n] = bytes;
     CK(cudaEventRecord(c->fz_ev[2 * c->fz_n], s));
   } else {
+    if (c->fz_skip) return;
     CK(cudaEventRecord(c->fz_ev[2 * c->fz_n + 1], s));
     ++c->fz_n;
   }
@@ -911,6 +919,8 @@ static void dec_mark(RunState& rs, cudaStream_t s, uint64_t bytes, bool begin) {
   Ctx* c = rs.c;
   if (!rs.o->profile) return;
   if (begin) {
+    c->dec_skip = (c->dec_seen++ % (size_t)c->prof_every) != 0;
+    if (c->dec_skip) return;
     while (c->dec_ev.size() < 2 * (c->dec_n + 1)) {
       cudaEvent_t e;
       CK(cudaEventCreate(&e));
@@ -920,6 +930,7 @@ static void dec_mark(RunState& rs, cudaStream_t s, uint64_t bytes, bool begin) {
     c->dec_bytes[c->dec_n] = bytes;
     CK(cudaEventRecord(c->dec_ev[2 * c->dec_n], s));
   } else {
+    if (c->dec_skip) return;
     CK(cudaEventRecord(c->dec_ev[2 * c->dec_n + 1], s));
     ++c->dec_n;
   }
@@ -968,6 +979,16 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
       nrec = 0;
     }
   }
+  const float* delays = rs.o->fetch_delay_s;
+  auto delay_of = [&](int e) -> float {
+    return delays ? delays[((size_t)(layer - 1) * c->L + (c->e_first + e)) * 2 + k] : 0.f;
+  };
+  // a window whose streamed experts are all read in place (or pinned) has nothing to load: one
+  // slot-table launch takes it straight to RESIDENT (its LOAD_START and LOAD_DONE records in
+  // order inside it) instead of a LOADING launch and a RESIDENT launch on the decode stream
+  bool no_load = whi > wlo && whi - wlo <= chunk;
+  for (int e = wlo; e < whi && no_load; ++e)
+    no_load = is_pinned(layer, e) || (fused_tensor(c, layer, e, kind) && delay_of(e) <= 0.f);
   // map every streamed expert of the window (lowest free block first) -> LOADING entries
   std::vector<int> blocks(E, 0);
   for (int e = wlo; e < whi; ++e)
@@ -982,8 +1003,17 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
     o2.set_row = row + e0;
     o2.set_n = std::min(chunk, whi - e0);
     for (int i = 0; i < o2.set_n; ++i)
-      o2.vals[i] = pt_entry(dev_block0(blocks[e0 + i]), is_pinned(layer, e0 + i) ? XPGB_PAGE_RESIDENT : XPGB_PAGE_LOADING);
+      o2.vals[i] = pt_entry(dev_block0(blocks[e0 + i]),
+                            (no_load || is_pinned(layer, e0 + i)) ? XPGB_PAGE_RESIDENT : XPGB_PAGE_LOADING);
+    if (no_load && rs.log) set_rec(o2, nrec++, XPGB_EV_LOAD_DONE, it, layer, kind, -1, -1, st.w);
     launch_op(o2, s);
+  }
+  if (no_load) {
+    for (int e = wlo; e < whi; ++e)
+      if (!is_pinned(layer, e)) pt_mark_resident(c, layer, c->e_first + e + 1, kind);
+    CK(cudaEventRecord(c->ev_load[k][g % kEvRing], s));
+    if (seq) CK(cudaStreamSynchronize(s));
+    return;
   }
   if (whi <= wlo && (op.n_rec > 0 || op.unmap_n > 0)) launch_op(op, s);  // window without routed experts
   static const bool env_poison = getenv("XPGB_POISON") && atoi(getenv("XPGB_POISON")) != 0;
@@ -991,10 +1021,6 @@ static void materialize(RunState& rs, int g, const Step& st, const Step* tg, int
     for (int e = wlo; e < whi; ++e)
       if (!is_pinned(layer, e) && blocks[e] != kVirtualBlock)
         CK(cudaMemsetAsync(block_ptr(c, kind, blocks[e]), 0xFF, sigma_of(c, kind), s));
-  const float* delays = rs.o->fetch_delay_s;
-  auto delay_of = [&](int e) -> float {
-    return delays ? delays[((size_t)(layer - 1) * c->L + (c->e_first + e)) * 2 + k] : 0.f;
-  };
   auto sleep_on = [&](cudaStream_t st, float d) {
     k_sleep<<<1, 1, 0, st>>>((uint64_t)(d * 1e9));
     note_launch();
@@ -1280,6 +1306,9 @@ static void session_begin(Ctx* c, const xpgb_run_opts* o, float* acts) {
   ss.builtin_compute = false;
   c->dec_n = 0;
   c->fz_n = 0;
+  c->dec_seen = c->fz_seen = 0;
+  c->prof_mode = o->profile;
+  c->prof_every = o->profile >= 2 ? o->profile : 1;
   ss.fetch_delay.clear();
   ss.compute_delay.clear();
   if (o->fetch_delay_s) ss.fetch_delay.assign(o->fetch_delay_s, o->fetch_delay_s + (size_t)N * c->L * 2);
@@ -1377,7 +1406,7 @@ static void session_compute(Ctx* c, int g) {
   cudaStream_t s = c->s_comp;
   const int kt = slots_of(c, o->top_k);
   const int T = o->tokens;
-  c->cur_ev = (o->profile && T > 0) ? &c->run_ev[(size_t)g * 7] : nullptr;
+  c->cur_ev = (o->profile == 1 && T > 0) ? &c->run_ev[(size_t)g * 7] : nullptr;
   prof_rec(c, 0, s);
   if (layer == 1 && st.first && T > 0) {
     // one route+plan launch per decode step covers all N layers; plans alternate between
@@ -1484,7 +1513,7 @@ static void session_end(Ctx* c, xpgb_report* rep) {
     rep->gate_up_bytes = (long long)(a * c->s1 + r * c->H * 2 + r * c->F * 2);
     rep->down_bytes = (long long)(a * c->s2 + r * c->F * 2 + r * (double)c->H * 4 * std::max(1, rep->down_splits));
   }
-  if (o->profile && ss.builtin_compute && steps > 0 && o->tokens > 0) {
+  if (o->profile == 1 && ss.builtin_compute && steps > 0 && o->tokens > 0) {
     double gu = 0, dn = 0, aux = 0;
     for (int g = 0; g < steps; ++g) {
       float ms[6];
@@ -1515,6 +1544,20 @@ static void session_end(Ctx* c, xpgb_report* rep) {
     c->dec_total_ns += ms * 1e6;
     c->dec_total_bytes += c->dec_bytes[i];
   }
+  // sampled runs: the sampled launches' means, scaled to every launch of the run
+  if (c->dec_n && c->dec_seen > c->dec_n) {
+    const double f = (double)c->dec_seen / (double)c->dec_n;
+    c->dec_total_ns *= f;
+    c->dec_total_bytes = (decltype(c->dec_total_bytes))(c->dec_total_bytes * f);
+    c->dec_launches = c->dec_seen;
+  }
+  if (c->fz_n && c->fz_seen > c->fz_n) {
+    const double f = (double)c->fz_seen / (double)c->fz_n;
+    c->fz_total_ns *= f;
+    c->fz_total_bytes = (decltype(c->fz_total_bytes))(c->fz_total_bytes * f);
+    c->fz_launches = c->fz_seen;
+  }
+  c->prof_mode = 0;
 
   if (paged) {
     // drain: the last two layers are still bound; release them like a finished

@@ -305,7 +305,8 @@ def predict_tiered(config: SimConfig, device_per_layer: float, pinned_per_layer:
 
 
 def predict_sm_shared(config: SimConfig, device_per_layer: float, pinned_per_layer: float = 0.0, *,
-                      b_dec: float | None = None, b_fused: float | None = None) -> dict:
+                      b_dec: float | None = None, b_fused: float | None = None, fx4_per_layer: float | None = None,
+                      host_exposed: float = 0.0) -> dict:
     """Step time of this implementation's tiered decode step (our model, not the reference's).
 
     The reference overlaps every page-in with compute (``max(tau_comp, N * tau_layer)``,
@@ -315,9 +316,12 @@ def predict_sm_shared(config: SimConfig, device_per_layer: float, pinned_per_lay
       SMs   = tau_comp + streamed-compressed share x model bytes / b_dec
     where the streamed-compressed share is every non-pinned expert (device-tier records and
     host records are both expanded on the SMs).  With decode-into-GEMM (``b_fused``), the
-    device-tier experts instead cost model bytes / b_fused each *in place of* their share of
-    tau_comp (their GEMM reads the record directly), and only host records pay b_dec.
-    Rates are raw-equivalent B/s; ``b_dec`` defaults to the calibrated b_dev."""
+    FX4 device-tier experts -- all of them, or ``fx4_per_layer`` of them in a mixed device tier
+    whose other records are Huffman -- instead cost model bytes / b_fused each *in place of*
+    their share of tau_comp (their GEMM reads the record directly); every other streamed expert
+    pays b_dec.  ``host_exposed``: share of the link time an SM-bound step cannot hide (the
+    staging ring holds about one record ahead; budget.HOST_EXPOSED).  Rates are raw-equivalent
+    B/s; ``b_dec`` defaults to the calibrated b_dev."""
     spec = config.spec
     L = spec.experts_per_layer
     total = spec.num_layers * spec.layer_bytes
@@ -327,9 +331,10 @@ def predict_sm_shared(config: SimConfig, device_per_layer: float, pinned_per_lay
     b_dec = config.b_dev if b_dec is None else b_dec
     link = host * total / config.b_host
     if b_fused:
-        sm = config.tau_comp_theory * (1.0 - dev) + dev * total / b_fused + host * total / b_dec
+        fx = dev if fx4_per_layer is None else fx4_per_layer / L
+        sm = config.tau_comp_theory * (1.0 - fx) + fx * total / b_fused + (host + dev - fx) * total / b_dec
     else:
         sm = config.tau_comp_theory + (dev + host) * total / b_dec
-    t = max(link, sm)
+    t = max(link, sm + host_exposed * link)
     return {"link_s": link, "sm_s": sm, "iteration_time": t, "tok_s": config.batch_size / t,
             "bound": "link" if link >= sm else "sm"}

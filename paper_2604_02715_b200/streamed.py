@@ -201,7 +201,7 @@ def _run_context(ctx: Context, spec: ModelSpec, fwd: ForwardSpec, iterations: in
         keep.append(cd)
         opts.compute_delay_s = cd.ctypes.data_as(C.POINTER(C.c_float))
     opts.log_enable = 1 if log else 0
-    opts.profile = 1 if profile else 0
+    opts.profile = int(profile) if not isinstance(profile, bool) else (1 if profile else 0)
     rep = _lib.Report()
     torch.cuda.current_stream(ctx.device).synchronize()
     call("xpgb_run", ctx.handle, C.byref(opts), C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), C.byref(rep))

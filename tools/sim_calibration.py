@@ -26,9 +26,12 @@ def main():
     ap.add_argument("--config", default="mixtral")
     ap.add_argument("--b-fused", type=float, default=None, help="decode-into-GEMM raw-equivalent GB/s")
     ap.add_argument("--b-dec", type=float, default=None, help="in-pipeline decoder raw-equivalent GB/s")
+    ap.add_argument("--host-exposed", type=float, default=None,
+                    help="share of the link time an SM-bound step exposes (default budget.HOST_EXPOSED)")
     args = ap.parse_args()
     from paper_2604_02715_b200 import ModelSpec
     from paper_2604_02715_b200 import simulate as S
+    from paper_2604_02715_b200.budget import HOST_EXPOSED
 
     cal = json.load(open(args.calibration))
     spec = ModelSpec(*SHAPES[args.config])
@@ -40,11 +43,13 @@ def main():
         dev, pin = float(p.get("device_tier_per_layer", 0)), float(p.get("pinned_per_layer", 0))
         ref = S.predict_tiered(c, dev, pin)
         b_dec = args.b_dec * 1e9 if args.b_dec else cal.get("b_dec_pipeline")
-        fused = p.get("device_format") == "fx4" and p.get("fused_decode")
+        fused = p.get("device_format") in ("fx4", "mixed") and p.get("fused_decode")
         b_fused = (args.b_fused * 1e9 if args.b_fused else cal.get("b_fx4_fused")) if fused else None
-        ours = S.predict_sm_shared(c, dev, pin, b_dec=b_dec, b_fused=b_fused)
+        fx = p.get("fx4_per_layer") if p.get("device_format") == "mixed" else None
+        ours = S.predict_sm_shared(c, dev, pin, b_dec=b_dec, b_fused=b_fused, fx4_per_layer=fx,
+                                   host_exposed=HOST_EXPOSED if args.host_exposed is None else args.host_exposed)
         meas = float(p["tok_s"])
-        row = {"budget": p.get("budget"), "device_format": p.get("device_format", "huffman"),
+        row = {"budget": p.get("budget"), "device_format": p.get("device_format", "huffman"), "fx4_per_layer": fx,
                "device_per_layer": dev, "pinned_per_layer": pin, "measured_tok_s": meas,
                "reference_model_tok_s": ref["tok_s"], "reference_model_err": ref["tok_s"] / meas - 1,
                "sm_shared_model_tok_s": ours["tok_s"], "sm_shared_model_err": ours["tok_s"] / meas - 1,
