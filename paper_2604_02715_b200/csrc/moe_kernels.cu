@@ -337,6 +337,7 @@ __device__ __forceinline__ void pack_split4(float4 v, uint2* hi, uint2* lo) {
 __global__ void k_gather(const float* __restrict__ x, const int32_t* __restrict__ pos,
                          const long long* __restrict__ fault, __nv_bfloat16* __restrict__ xp, long long lo_rows,
                          int kk, int H) {
+  if (threadIdx.x == 0) griddep_launch_dependents();
   if (*fault) return;
   const int t = blockIdx.x;
   const float4* xr = reinterpret_cast<const float4*>(x + (size_t)t * H);
@@ -387,6 +388,7 @@ __global__ void k_combine(const float* __restrict__ part, const int32_t* __restr
                           const long long* __restrict__ fault, float* __restrict__ y, int kk, int kr, int H,
                           int splits, long long split_stride, float inv_k, const int32_t* __restrict__ next_pos,
                           __nv_bfloat16* __restrict__ xp, long long lo_rows, int accumulate) {
+  if (threadIdx.x == 0) griddep_launch_dependents();  // the next layer's GEMM may stage its prologue
   if (*fault) return;
   const int t = blockIdx.x;
   int p[kMaxTopK], q[kMaxTopK];
@@ -616,6 +618,23 @@ __global__ void __launch_bounds__(192, 1)
   const int K = GU ? p.H : p.F;
   const int KB = (K + kBK - 1) / kBK;
   const int rows_per_block = GU ? 2 * p.F : p.H;
+  // Programmatic dependent launch (launch_gate_up / launch_down with pdl): everything above --
+  // unit prefix, residency check, barriers, TMEM -- and an L2 prefetch of this CTA's first unit
+  // of weights (resident before the previous kernel started: loads are ordered by events) overlap
+  // the previous kernel's tail; activations are read and outputs written only after the wait.
+  if (threadIdx.x == 0) griddep_launch_dependents();
+  if (warp == 0 && lane == 0) {
+    const Unit un = decode_unit(blockIdx.x, s_up, s_off, E, BN, S, GU, C::UNIT_ROWS);
+    int kb0 = 0, kb1 = KB;
+    if (!GU) split_kb(un.split, S, KB, &kb0, &kb1);
+    const int wrow = s_slot[un.e] * rows_per_block + un.m0;
+    const CUtensorMap* mw = un.e < p.E_routed ? &map_w : &map_ws;
+    for (int kb = kb0; kb < kb1; ++kb) {
+      tma_prefetch_l2_2d(mw, kb * kBK, wrow);
+      if (C::NA == 2) tma_prefetch_l2_2d(mw, kb * kBK, wrow + (GU ? p.F : kBM));
+    }
+  }
+  griddep_wait();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -778,6 +797,31 @@ void set_gemm_attrs() {
 #undef XPGB_SET_DN
 }
 
+// Grouped-GEMM launch with programmatic stream serialization (PDL): the CTAs may start
+// during the tail of the previous kernel in the stream and wait (griddep_wait) before touching
+// its outputs.  XPGB_PDL=0 launches them plainly (A/B).
+static void launch_gemm_pdl(GemmKernel kern, int grid, int smem, cudaStream_t s, const CUtensorMap& a,
+                            const CUtensorMap& b, const CUtensorMap& c, const GemmParams& p) {
+  static const bool pdl = !(getenv("XPGB_PDL") && atoi(getenv("XPGB_PDL")) == 0);
+  if (!pdl) {
+    kern<<<grid, 192, smem, s>>>(a, b, c, p);
+    note_launch();
+    return;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, a, b, c, p);
+  note_launch();
+}
+
 void launch_gate_up(const CUtensorMap& map_w, const CUtensorMap& map_x, const CUtensorMap& map_ws,
                     const GemmParams& p, int bn, int grid, cudaStream_t s, bool lean) {
   GemmKernel kern = nullptr;
@@ -791,8 +835,7 @@ void launch_gate_up(const CUtensorMap& map_w, const CUtensorMap& map_x, const CU
   }
 #undef XPGB_PICK_GU
   if (!kern) { kern = k_moe_gemm<true, 128, 3>; smem = GemmCfg<true, 128, 3>::SMEM; }
-  kern<<<grid, 192, smem, s>>>(map_w, map_x, map_ws, p);
-  note_launch();
+  launch_gemm_pdl(kern, grid, smem, s, map_w, map_x, map_ws, p);
 }
 
 void launch_down(const CUtensorMap& map_w, const CUtensorMap& map_h, const CUtensorMap& map_ws,
@@ -808,8 +851,7 @@ void launch_down(const CUtensorMap& map_w, const CUtensorMap& map_h, const CUten
   }
 #undef XPGB_PICK_DN
   if (!kern) { kern = k_moe_gemm<false, 128, 3>; smem = GemmCfg<false, 128, 3>::SMEM; }
-  kern<<<grid, 192, smem, s>>>(map_w, map_h, map_ws, p);
-  note_launch();
+  launch_gemm_pdl(kern, grid, smem, s, map_w, map_h, map_ws, p);
 }
 
 }  // namespace xpgb

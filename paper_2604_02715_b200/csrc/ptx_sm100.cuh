@@ -63,6 +63,19 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// 2-D tile prefetch into L2 (no smem, no barrier): warms a tile a later tma_load_2d reads.
+__device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* map, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+
+// Programmatic dependent launch: wait for the preceding grid in the stream (its writes visible;
+// a no-op when this grid was not launched with programmatic stream serialization), and let the
+// next grid's CTAs launch once every CTA of this one has executed launch_dependents or exited.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 // 1-D bulk copy global -> shared (TMA engine, no tensor map): 16-byte aligned src/dst/size,
 // completion as transaction bytes on `bar`.
 __device__ __forceinline__ void bulk_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {

@@ -44,7 +44,7 @@ def main():
     ap.add_argument("--depth", type=int, default=None, help="budget: windows in flight on the planned ring (default: the planner picks 1 or 2)")
     ap.add_argument("--window", type=int, default=None, help="budget: experts per ring window")
     ap.add_argument("--b-dec", type=float, default=None, help="budget: the planner's decoder GB/s (model input)")
-    ap.add_argument("--device-format", default="auto", choices=["auto", "huffman", "fx4"],
+    ap.add_argument("--device-format", default="auto", choices=["auto", "huffman", "fx4", "mixed"],
                     help="budget: device-tier records (auto: the planner picks by its step model)")
     ap.add_argument("--stage-bufs", type=int, default=None, help="staging buffers per kind (host codec)")
     ap.add_argument("--rings", default="6,8,12", help="sub-layer ring sizes (expert blocks per kind) for budget")
@@ -115,6 +115,7 @@ def main():
                "device_tier_per_layer": plan.device_experts / N if plan else 0,
                "device_format": getattr(plan, "device_format", "huffman") if plan else None,
                "fused_decode": bool(getattr(plan, "fused", False)) if plan else False,
+               "fx4_per_layer": plan.fx4_experts / N if plan else 0,
                "planned_tok_s": T / plan.est_step_s if plan else None,
                "ring_depth": plan.depth if plan else 2, "stage_buffers": args.stage_bufs or 4,
                "ring_experts": (plan.ring if plan else (p if what == "ring" else 2 * (L - (p if what == "pinned" else 0)))),
