@@ -53,6 +53,7 @@ constexpr int kRingBytes = 256;                    // per decoder thread: four 6
 // 2 x 128 rows of 64 sign/mantissa bytes (64-B swizzle) and 32 nibble bytes (32-B swizzle).
 constexpr int kFxSmTile = 128 * 64, kFxNibTile = 128 * 32;
 constexpr int kFxFenceFlag = 1 << 30;  // FX4 launches: bit in `chunk` -> proxy fence before a slot release
+constexpr int kFxSpinFlag = 1 << 29;   // FX4 launches: bit in `chunk` -> MMA and decoders spin (no backoff)
 
 constexpr int kFxCStage = 2 * kFxSmTile + 2 * kFxNibTile;  // 24 KB
 
@@ -109,6 +110,13 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity
     if (ok) return;
     __nanosleep(64);
   }
+}
+
+// The handoffs on the per-stage critical path (decoders -> MMA -> decoders) poll without a
+// backoff when `spin` is set: a sleeping waiter adds up to ~2 x 64 ns per stage.
+__device__ __forceinline__ void mbar_wait_role(uint64_t* bar, uint32_t parity, bool spin) {
+  if (spin) mbar_wait(bar, parity);
+  else mbar_wait_backoff(bar, parity);
 }
 
 // Branch-free stream window over a per-thread shared-memory ring of four 64-byte blocks
@@ -357,7 +365,7 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
       tc_fence_after();
       const uint32_t d0 = tmem + acc * 256;
       for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait_backoff(&full[stage], phase);
+        mbar_wait_role(&full[stage], phase, FMT == 1 && (chunk & kFxSpinFlag));
         tc_fence_after();
         if (lane == 0) {
           const uint32_t base = smem_u32(smem + stage * C::STAGE);
@@ -586,7 +594,7 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
         __syncwarp();
         if (lane == 0) mbar_arrive(&cempty[fcs]);
         if (++fcs == C::CST) { fcs = 0; fcph ^= 1; }
-        mbar_wait_backoff(&empty[stage], phase ^ 1);
+        mbar_wait_role(&empty[stage], phase ^ 1, chunk & kFxSpinFlag);
         if (valid) {
           const uint32_t row = smem_u32(smem + stage * C::STAGE + a * C::A_BYTES + lr * 128);
 #pragma unroll
@@ -699,7 +707,8 @@ void launch_gemm_dec(bool gate_up, const CUtensorMap& map_b, const GemmParams& p
   }
   // FX4 ignores the Huffman chunk; its top bit carries the release-fence A/B (XPGB_FX_FENCE=0 drops it)
   static const bool fx_fence = !(getenv("XPGB_FX_FENCE") && atoi(getenv("XPGB_FX_FENCE")) == 0);
-  const int arg = fx4 ? (fx_fence ? kFxFenceFlag : 0) : chunk;
+  static const bool fx_spin = getenv("XPGB_FX_SPIN") && atoi(getenv("XPGB_FX_SPIN")) != 0;
+  const int arg = fx4 ? ((fx_fence ? kFxFenceFlag : 0) | (fx_spin ? kFxSpinFlag : 0)) : chunk;
   kern<<<grid, kDecThreads, smem, s>>>(map_b, p, tabs, arg);
   note_launch();
 }
