@@ -54,15 +54,28 @@ constexpr int kRingBytes = 256;                    // per decoder thread: four 6
 constexpr int kFxSmTile = 128 * 64, kFxNibTile = 128 * 32;
 constexpr int kFxFenceFlag = 1 << 30;  // FX4 launches: bit in `chunk` -> proxy fence before a slot release
 constexpr int kFxSpinFlag = 1 << 29;   // FX4 launches: bit in `chunk` -> MMA and decoders spin (no backoff)
+constexpr int kFxNoDecFlag = 1 << 28;  // FX4 launches, timing A/B only: skip the decode math (wrong results)
 
 constexpr int kFxCStage = 2 * kFxSmTile + 2 * kFxNibTile;  // 24 KB
 
+// FMT 2: FX4 records, the decoded A tiles written to tensor memory (tcgen05.st) instead of
+// shared memory, and the MMAs read A from there: shared memory then carries only the compressed
+// stages and the activations (the smem path moves ~216 KB per 64-K stage -- the MMAs alone read
+// each A tile twice, hi and lo planes -- and bounds the kernel, r2_t47: 405 us per Mixtral gate/up
+// launch with the decode math switched off, 553 us with it).
 template <int BN, int STAGES, int FMT = 0>
 struct DecCfg {
   static constexpr int A_BYTES = kBM * kBK * 2;             // one 128 x 64 bf16 tile
   static constexpr int B_BYTES = BN * kBK * 2;              // one activation plane
-  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;   // two A tiles + hi/lo activations
+  static constexpr int B_OFF = FMT == 2 ? 0 : 2 * A_BYTES;  // activations after the A tiles (smem A)
+  static constexpr int STAGE = B_OFF + 2 * B_BYTES;         // [two A tiles +] hi/lo activations
   static constexpr int TMEM_COLS = 512;                     // 2 accumulator stages x 256 columns
+  // accumulator columns per stage and the second accumulator's offset (up / W_down rows 128..255);
+  // FMT 2 packs them at BN and keeps columns 384..511 for 2 stages x 2 decoded A tiles x 32
+  static constexpr int ACC_W = FMT == 2 ? 2 * BN : 256;
+  static constexpr int UP_OFF = FMT == 2 ? BN : 128;
+  static constexpr int A_COL = 384;
+  static_assert(FMT != 2 || (4 * BN <= A_COL && STAGES == 2), "TMEM-A tiles: BN <= 96, two stages");
   static constexpr int TAB_BYTES = FMT ? (2 * kMaxExperts + 4) * 4 : (3 * kMaxExperts + 8) * 4;  // s_off, s_up (+ flag)
   static constexpr int DEC_TAB =
       FMT ? 0 : (((1 << kPairBits) * 4 + 3 * (kCodecMaxLen + 1) * 4 + kCodecSymbols + 15) & ~15);
@@ -229,6 +242,7 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
     k_moe_gemm_dec(const __grid_constant__ CUtensorMap map_b, GemmParams p, const DecTables* __restrict__ tabs,
                    int chunk) {
   using C = DecCfg<BN, STAGES, FMT>;
+  constexpr int RFMT = FMT == 2 ? 1 : FMT;  // record format
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_1k(smem_raw);
   uint8_t* cstage = smem + STAGES * C::STAGE;  // FX4 compressed stages (CST of them)
@@ -269,7 +283,7 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
       int u = 0;
       if (e < E) {
         const int n = s_off[e + 1] - s_off[e];
-        if (n > 0 && e < p.E_routed && p.dec[e].sm && p.dec[e].fmt == (uint32_t)FMT && ((p.dec_fmt_mask >> FMT) & 1u)) {
+        if (n > 0 && e < p.E_routed && p.dec[e].sm && p.dec[e].fmt == (uint32_t)RFMT && ((p.dec_fmt_mask >> RFMT) & 1u)) {
           u = ((n + BN - 1) / BN) * MT * S;
           const int32_t ent = p.pt[e];
           if (pt_state(ent) != 2) {
@@ -337,7 +351,7 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
         const uint32_t bytes = 2 * nb * kBoxRowsB * kBK * 2;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait_backoff(&empty[stage], phase ^ 1);
-          uint8_t* sb = smem + stage * C::STAGE + 2 * C::A_BYTES;
+          uint8_t* sb = smem + stage * C::STAGE + C::B_OFF;
           mbar_arrive_expect_tx(&full[stage], bytes);
           for (int i = 0; i < nb; ++i) {
             tma_load_2d(sb + i * kBoxRowsB * kBK * 2, &map_b, &full[stage], kb * kBK, un.row_begin + i * kBoxRowsB,
@@ -363,24 +377,32 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
       const uint32_t acc_par = (it >> 1) & 1;
       mbar_wait_backoff(&tempty[acc], acc_par ^ 1);
       tc_fence_after();
-      const uint32_t d0 = tmem + acc * 256;
+      const uint32_t d0 = tmem + acc * C::ACC_W;
       for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait_role(&full[stage], phase, FMT == 1 && (chunk & kFxSpinFlag));
+        mbar_wait_role(&full[stage], phase, FMT >= 1 && (chunk & kFxSpinFlag));
         tc_fence_after();
         if (lane == 0) {
           const uint32_t base = smem_u32(smem + stage * C::STAGE);
-          const uint32_t bbase = base + 2 * C::A_BYTES;
+          const uint32_t bbase = base + C::B_OFF;
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
             const uint64_t bdesc = sdesc_k_sw128(bbase + 32 * k);
             const uint64_t bdesc_lo = sdesc_k_sw128(bbase + C::B_BYTES + 32 * k);
             const uint32_t accum = (kb > kb0 || k > 0) ? 1u : 0u;
-            const uint64_t a0 = sdesc_k_sw128(base + 32 * k);
-            const uint64_t a1 = sdesc_k_sw128(base + C::A_BYTES + 32 * k);
-            umma_bf16(d0, a0, bdesc, idesc, accum);
-            umma_bf16(d0, a0, bdesc_lo, idesc, 1u);
-            umma_bf16(d0 + 128, a1, bdesc, idesc, accum);
-            umma_bf16(d0 + 128, a1, bdesc_lo, idesc, 1u);
+            if constexpr (FMT == 2) {
+              const uint32_t a0 = tmem + C::A_COL + stage * 64 + 8 * k, a1 = a0 + 32;
+              umma_bf16_ts(d0, a0, bdesc, idesc, accum);
+              umma_bf16_ts(d0, a0, bdesc_lo, idesc, 1u);
+              umma_bf16_ts(d0 + C::UP_OFF, a1, bdesc, idesc, accum);
+              umma_bf16_ts(d0 + C::UP_OFF, a1, bdesc_lo, idesc, 1u);
+            } else {
+              const uint64_t a0 = sdesc_k_sw128(base + 32 * k);
+              const uint64_t a1 = sdesc_k_sw128(base + C::A_BYTES + 32 * k);
+              umma_bf16(d0, a0, bdesc, idesc, accum);
+              umma_bf16(d0, a0, bdesc_lo, idesc, 1u);
+              umma_bf16(d0 + 128, a1, bdesc, idesc, accum);
+              umma_bf16(d0 + 128, a1, bdesc_lo, idesc, 1u);
+            }
           }
           umma_commit(&empty[stage]);
         }
@@ -400,7 +422,7 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
       const uint32_t acc_par = (it >> 1) & 1;
       mbar_wait_backoff(&tfull[acc], acc_par);
       tc_fence_after();
-      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * 256;
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * C::ACC_W;
       if (GU) {
         const int r = un.m0 + q * 32 + lane;
         __nv_bfloat16* hcol = p.hbuf + (size_t)un.row_begin * p.F + r;
@@ -408,7 +430,7 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
         for (int c0 = 0; c0 < un.n_rows; c0 += 16) {
           float g[16], v[16];
           tmem_ld16(tbase + c0, g);
-          tmem_ld16(tbase + 128 + c0, v);
+          tmem_ld16(tbase + C::UP_OFF + c0, v);
           if (r < p.F) {
 #pragma unroll
             for (int i = 0; i < 16; ++i)
@@ -428,7 +450,7 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
           float* out = p.part + un.split * p.split_stride + (size_t)un.row_begin * p.H + r;
           for (int c0 = 0; c0 < un.n_rows; c0 += 16) {
             float v[16];
-            tmem_ld16(tbase + half * 128 + c0, v);
+            tmem_ld16(tbase + half * C::UP_OFF + c0, v);
             if (r < p.H) {
 #pragma unroll
               for (int i = 0; i < 16; ++i)
@@ -443,7 +465,7 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
   } else if (warp == 6 + kDecWarps) {
     // ---- FX4 compressed stages by TMA, on their own warp so they run CST stages ahead of the
     // decoders instead of queueing behind the activation loads' wait for a free decoded stage
-    if (FMT == 1 && lane == 0) {
+    if (FMT >= 1 && lane == 0) {
       const uint64_t pol_w = policy_evict_first();  // compressed weights: streamed once
       int cs = 0;
       uint32_t cph = 0;
@@ -469,8 +491,12 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
     }
   } else {
     // ---- decoders: thread d owns weight row d of the unit
-    const int d = threadIdx.x - 192;
-    const int a = d >> 7, lr = d & 127;
+    // (FMT 2: a warp writes only its own TMEM lane quarter, warp id % 4, so its 32 rows are that
+    // quarter of A tile (decoder warp / 4))
+    const int dw = (threadIdx.x - 192) >> 5;
+    const int a = FMT == 2 ? dw >> 2 : (threadIdx.x - 192) >> 7;
+    const int lr = FMT == 2 ? (int)((warp & 3) * 32 + lane) : (threadIdx.x - 192) & 127;
+    const int d = a * 128 + lr;
     const uint32_t sw = (uint32_t)(lr & 7);
     const CanonTabs ct{s_count, s_first, s_rank, s_sym, FMT == 0 ? tabs->maxlen : 0};
     int stage = 0;
@@ -595,7 +621,48 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
         if (lane == 0) mbar_arrive(&cempty[fcs]);
         if (++fcs == C::CST) { fcs = 0; fcph ^= 1; }
         mbar_wait_role(&empty[stage], phase ^ 1, chunk & kFxSpinFlag);
-        if (valid) {
+        if constexpr (FMT == 2) {
+          // the stage's 64 values of this row -> 32 registers (bf16 pairs, K order) -> TMEM
+          // lane lr, columns A_COL + stage * 64 + a * 32 .. + 31; escapes patched in registers
+          tc_fence_after();  // after the empty wait: the MMAs that read this stage are complete
+          uint32_t o[32];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const uint4& nq = nv[q >> 2];
+            const uint32_t nw = (q & 3) == 0 ? nq.x : (q & 3) == 1 ? nq.y : (q & 3) == 2 ? nq.z : nq.w;
+            const uint4& sq = sv[q >> 1];
+            const uint32_t sa = (q & 1) ? sq.z : sq.x, sb = (q & 1) ? sq.w : sq.y;
+            const uint32_t lo = nw & 0x0F0F0F0Fu, hi = (nw >> 4) & 0x0F0F0F0Fu;
+            const uint32_t escf = ((lo + 0x01010101u) | (hi + 0x01010101u)) & 0x10101010u;
+            const uint32_t le = lo + bb, he = hi + bb;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint32_t x = __byte_perm(le, he, (uint32_t)(j | ((4 + j) << 4)));
+              const uint32_t ex = ((x & 0xFFu) << 7) | ((x >> 8) << 23);
+              const uint32_t dup = __byte_perm(j < 2 ? sa : sb, 0, (j & 1) ? 0x3322u : 0x1100u);
+              o[4 * q + j] = (dup & 0x807F807Fu) | (ex & 0x7F807F80u);
+            }
+            if (__builtin_expect(valid && escf != 0u, 0)) {
+              // exponents outside the window, in value order: value v is half (v & 1) of word v / 2
+#pragma unroll
+              for (int v = 0; v < 8; ++v)
+                if (((nw >> (4 * v)) & 15u) == 15u) {
+                  const uint32_t sh = 7u + 16u * (uint32_t)(v & 1);
+                  o[4 * q + (v >> 1)] = (o[4 * q + (v >> 1)] & ~(0xFFu << sh)) | ((uint32_t)*escp++ << sh);
+                }
+            }
+          }
+          if (!valid)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = 0u;
+          tmem_st32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(C::A_COL + stage * 64 + a * 32), o);
+          tc_fence_before();  // the stores before the MMA warp's barrier wait
+        } else if (valid && (chunk & kFxNoDecFlag)) {  // timing A/B: raw stores, no decode
+          const uint32_t row = smem_u32(smem + stage * C::STAGE + a * C::A_BYTES + lr * 128);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            st_smem_v4(row + ((((uint32_t)q) ^ sw) << 4), sv[q >> 1].x, sv[q >> 1].y, nv[q >> 2].x, nv[q >> 2].y);
+        } else if (valid) {
           const uint32_t row = smem_u32(smem + stage * C::STAGE + a * C::A_BYTES + lr * 128);
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
@@ -628,7 +695,7 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
             }
           }
         }
-        fence_async_smem();  // the A tile's generic stores before the tensor cores' reads
+        if constexpr (FMT != 2) fence_async_smem();  // the A tile's generic stores before the tensor cores' reads
         __syncwarp();
         if (lane == 0) mbar_arrive(&full[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -652,6 +719,8 @@ using DecKernel = void (*)(const CUtensorMap, GemmParams, const DecTables*, int)
 // compressed ones (XPGB_FX_STAGES=3, A/B)
 #define XPGB_FX_TILES(X) X(32, 3) X(48, 2) X(64, 2) X(80, 2) X(96, 2) X(128, 2)
 #define XPGB_FX_TILES3(X) X(32, 4) X(48, 3) X(64, 3) X(80, 3) X(96, 3) X(128, 2)
+// FX4 with the decoded A tiles in tensor memory (FMT 2, the default for BN <= 96)
+#define XPGB_FXT_TILES(X) X(32, 2) X(48, 2) X(64, 2) X(80, 2) X(96, 2)
 
 template <bool GU, int BN, int ST, int FMT>
 static void set_dec_attr() {
@@ -665,6 +734,9 @@ void set_gemm_dec_attrs() {
   XPGB_DEC_TILES(XPGB_SET_DEC)
   XPGB_FX_TILES(XPGB_SET_FX)
   XPGB_FX_TILES3(XPGB_SET_FX)
+#define XPGB_SET_FXT(BN, ST) set_dec_attr<true, BN, ST, 2>(); set_dec_attr<false, BN, ST, 2>();
+  XPGB_FXT_TILES(XPGB_SET_FXT)
+#undef XPGB_SET_FXT
 #undef XPGB_SET_DEC
 #undef XPGB_SET_FX
 }
@@ -691,8 +763,16 @@ void launch_gemm_dec(bool gate_up, const CUtensorMap& map_b, const GemmParams& p
     kern = gate_up ? k_moe_gemm_dec<true, BN, ST, 1> : k_moe_gemm_dec<false, BN, ST, 1>;  \
     smem = DecCfg<BN, ST, 1>::SMEM;                                                      \
   }
+#define XPGB_PICK_FXT(BN, ST)                                                            \
+  if (bn == BN) {                                                                        \
+    kern = gate_up ? k_moe_gemm_dec<true, BN, ST, 2> : k_moe_gemm_dec<false, BN, ST, 2>;  \
+    smem = DecCfg<BN, ST, 2>::SMEM;                                                      \
+  }
+  static const bool fx_tmem = !(getenv("XPGB_FX_TMEM") && atoi(getenv("XPGB_FX_TMEM")) == 0);
   if (!fx4) {
     XPGB_DEC_TILES(XPGB_PICK_DEC)
+  } else if (fx_tmem && !fx3 && bn <= 96) {
+    XPGB_FXT_TILES(XPGB_PICK_FXT)
   } else if (fx3) {
     XPGB_FX_TILES3(XPGB_PICK_FX)
   } else {
@@ -700,6 +780,7 @@ void launch_gemm_dec(bool gate_up, const CUtensorMap& map_b, const GemmParams& p
   }
 #undef XPGB_PICK_DEC
 #undef XPGB_PICK_FX
+#undef XPGB_PICK_FXT
   if (!kern) {
     kern = fx4 ? (gate_up ? k_moe_gemm_dec<true, 128, 2, 1> : k_moe_gemm_dec<false, 128, 2, 1>)
                : (gate_up ? k_moe_gemm_dec<true, 128, 2, 0> : k_moe_gemm_dec<false, 128, 2, 0>);
@@ -708,7 +789,9 @@ void launch_gemm_dec(bool gate_up, const CUtensorMap& map_b, const GemmParams& p
   // FX4 ignores the Huffman chunk; its top bit carries the release-fence A/B (XPGB_FX_FENCE=0 drops it)
   static const bool fx_fence = !(getenv("XPGB_FX_FENCE") && atoi(getenv("XPGB_FX_FENCE")) == 0);
   static const bool fx_spin = getenv("XPGB_FX_SPIN") && atoi(getenv("XPGB_FX_SPIN")) != 0;
-  const int arg = fx4 ? ((fx_fence ? kFxFenceFlag : 0) | (fx_spin ? kFxSpinFlag : 0)) : chunk;
+  static const bool fx_nodec = getenv("XPGB_FX_NODEC") && atoi(getenv("XPGB_FX_NODEC")) != 0;
+  const int arg =
+      fx4 ? ((fx_fence ? kFxFenceFlag : 0) | (fx_spin ? kFxSpinFlag : 0) | (fx_nodec ? kFxNoDecFlag : 0)) : chunk;
   kern<<<grid, kDecThreads, smem, s>>>(map_b, p, tabs, arg);
   note_launch();
 }

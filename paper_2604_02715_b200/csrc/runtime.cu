@@ -488,6 +488,8 @@ static int pick_bn(Ctx* c, int T, int kk) { return pick_bn_rows(avg_group_rows(c
 // Decode-into-GEMM tile: every extra token tile of an expert decodes its weights again, so
 // cover mean + 3 sd of the rows per expert (capped at the 128-column accumulators).
 static int pick_bn_dec(Ctx* c, int T, int kk) {
+  static const int force = getenv("XPGB_BN_DEC") ? atoi(getenv("XPGB_BN_DEC")) : 0;  // A/B
+  if (force == 32 || force == 48 || force == 64 || force == 80 || force == 96 || force == 128) return force;
   const double avg = avg_group_rows(c, T, kk);
   const double want = avg + 3.0 * std::sqrt(std::max(avg, 0.0));
   for (int bn : {32, 48, 64, 80, 96}) if (want <= bn) return bn;
