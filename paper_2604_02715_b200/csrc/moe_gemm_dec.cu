@@ -57,6 +57,10 @@ constexpr int kFxSpinFlag = 1 << 29;   // FX4 launches: bit in `chunk` -> MMA an
 constexpr int kFxNoDecFlag = 1 << 28;  // FX4 launches, timing A/B only: skip the decode math (wrong results)
 
 constexpr int kFxCStage = 2 * kFxSmTile + 2 * kFxNibTile;  // 24 KB
+#ifndef XPGB_FX_MAX_CST
+#define XPGB_FX_MAX_CST 4
+#endif
+constexpr int kFxMaxCst = XPGB_FX_MAX_CST;  // compressed stages with the A tiles in TMEM (the smem they free)
 
 // FMT 2: FX4 records, the decoded A tiles written to tensor memory (tcgen05.st) instead of
 // shared memory, and the MMAs read A from there: shared memory then carries only the compressed
@@ -82,7 +86,8 @@ struct DecCfg {
   static constexpr int RING = FMT ? 0 : kDecThreads_dec * kRingBytes;  // per-decoder-thread bitstream rings
   // compressed stages (FX4): as many as fit beside the decoded stages, 2..4
   static constexpr int CST_FIT = (227 * 1024 - 1024 - 256 - TAB_BYTES - STAGES * STAGE) / kFxCStage;
-  static constexpr int CST = FMT ? (CST_FIT > 4 ? 4 : CST_FIT) : 0;
+  static constexpr int CST_MAX = FMT == 2 ? kFxMaxCst : 4;
+  static constexpr int CST = FMT ? (CST_FIT > CST_MAX ? CST_MAX : CST_FIT) : 0;
   static_assert(!FMT || CST >= 2, "FX4 decode-GEMM needs two compressed stages");
   static constexpr int BAR_OFF = STAGES * STAGE + CST * kFxCStage;       // barriers, then the tables
   static constexpr int SMEM = BAR_OFF + 1024 + 256 + TAB_BYTES + DEC_TAB + RING;
@@ -251,8 +256,8 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* cfull = tempty + 2;  // FX4: compressed stage filled (TMA bytes)
-  uint64_t* cempty = cfull + 4;  // FX4: compressed stage read by all decoder warps
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 4);
+  uint64_t* cempty = cfull + kFxMaxCst;  // FX4: compressed stage read by all decoder warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + kFxMaxCst);
   int* s_off = reinterpret_cast<int*>(smem + C::BAR_OFF + 256);
   int* s_up = s_off + kMaxExperts + 1;
   int* s_flag = s_up + kMaxExperts + 1;
@@ -315,7 +320,7 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
-    for (int c = 0; c < 4; ++c) { mbar_init(&cfull[c], 1); mbar_init(&cempty[c], kDecWarps); }
+    for (int c = 0; c < kFxMaxCst; ++c) { mbar_init(&cfull[c], 1); mbar_init(&cempty[c], kDecWarps); }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
@@ -637,10 +642,11 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
             const uint32_t le = lo + bb, he = hi + bb;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              const uint32_t x = __byte_perm(le, he, (uint32_t)(j | ((4 + j) << 4)));
-              const uint32_t ex = ((x & 0xFFu) << 7) | ((x >> 8) << 23);
+              // y = [le_j, le_j, he_j, he_j]: << 7 puts the two exponents at bits 7..14 and 23..30,
+              // one bit-select merges them with the sign/mantissa bytes (4 ops per value pair)
+              const uint32_t y = __byte_perm(le, he, (uint32_t)(j | (j << 4) | ((4 + j) << 8) | ((4 + j) << 12)));
               const uint32_t dup = __byte_perm(j < 2 ? sa : sb, 0, (j & 1) ? 0x3322u : 0x1100u);
-              o[4 * q + j] = (dup & 0x807F807Fu) | (ex & 0x7F807F80u);
+              o[4 * q + j] = (dup & 0x807F807Fu) | ((y << 7) & 0x7F807F80u);
             }
             if (__builtin_expect(valid && escf != 0u, 0)) {
               // exponents outside the window, in value order: value v is half (v & 1) of word v / 2
