@@ -231,7 +231,8 @@ int xpgb_codec_decode(const void* record_dev, uint64_t n, uint64_t bits_len, int
  * like the exponent-Huffman record (codec.py:235-272), 12.1 bits per value instead of ~10.7.
  * n % 256 == 0.  measure: histogram -> base and escape count -> record bytes (synchronises
  * `stream`); encode: raw bf16 (device) -> record (device, record_bytes); decode: record ->
- * n bf16 words.  scratch: xpgb_fx4_scratch_bytes(n) bytes of device memory. */
+ * n bf16 words; base in [0, 240] (measure picks it).  scratch: xpgb_fx4_scratch_bytes(n) bytes of
+ * device memory. */
 uint64_t xpgb_fx4_scratch_bytes(uint64_t n);
 int xpgb_fx4_measure(const void* raw_dev, uint64_t n, void* scratch_dev, int32_t* base, uint64_t* n_escapes,
                      uint64_t* record_bytes, void* stream);

@@ -170,7 +170,9 @@ void fx4_count(const uint16_t* raw, uint64_t n, uint32_t* scratch, int* base, ui
   cudaStreamSynchronize(s);
   uint64_t best = 0;
   int b = 0;
-  for (int lo = 0; lo + 15 <= 256; ++lo) {  // 15-wide window with the most values
+  // 15-wide window with the most values; base <= 240 so base + 15 (an escape's code) still fits
+  // a byte -- the decoders add the base to four codes at once, and a carry would reach the next
+  for (int lo = 0; lo <= kFxMaxBase; ++lo) {
     uint64_t c = 0;
     for (int k = 0; k < 15; ++k) c += h[lo + k];
     if (c > best) {

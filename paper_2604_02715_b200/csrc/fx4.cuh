@@ -16,7 +16,8 @@
 //                           15 = escape (exponent outside [base, base + 14])
 //   idx   ns + 1 uint32     escapes before each 256-value segment (ns = n / 256), exclusive prefix
 //   esc   total bytes       exponent bytes of the escaped values, in value order (+16 slack)
-// The base is chosen per tensor to cover the most values (15-wide window of the histogram).
+// The base is chosen per tensor to cover the most values (15-wide window of the histogram),
+// at most kFxMaxBase: decoders add it to four codes in one 32-bit add, so base + 15 must fit a byte.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -24,6 +25,7 @@
 namespace xpgb {
 
 constexpr int kFxSeg = 256;  // values per escape-index segment
+constexpr int kFxMaxBase = 240;  // base + 15 <= 255
 
 struct FxLayout {
   uint64_t n, nib, idx, esc, total;  // byte offsets (sm at 0) and record size

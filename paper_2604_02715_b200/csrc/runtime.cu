@@ -2378,7 +2378,7 @@ int xpgb_fx4_measure(const void* raw_dev, uint64_t n, void* scratch_dev, int32_t
 int xpgb_fx4_encode(const void* raw_dev, uint64_t n, int32_t base, void* scratch_dev, void* record_dev, void* stream) {
   return guard([&] {
     if (n % kFxSeg) XFAIL(XPGB_ERR_CONFIG, "FX4 tensors hold a multiple of %d values", kFxSeg);
-    if (base < 0 || base > 241) XFAIL(XPGB_ERR_OUT_OF_RANGE, "FX4 base %d outside [0, 241]", base);
+    if (base < 0 || base > kFxMaxBase) XFAIL(XPGB_ERR_OUT_OF_RANGE, "FX4 base %d outside [0, %d]", base, kFxMaxBase);
     fx4_encode(static_cast<const uint16_t*>(raw_dev), n, base, static_cast<uint32_t*>(scratch_dev),
                static_cast<uint8_t*>(record_dev), (cudaStream_t)stream);
     CKLAUNCH();

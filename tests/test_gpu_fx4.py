@@ -61,6 +61,19 @@ def test_fx4_roundtrip_every_bf16_pattern_and_escapes():
     assert esc > words.size // 2
 
 
+def test_fx4_roundtrip_top_exponents():
+    """Exponents crowded at the top of the range: the base stops at 240 so base + 15 (an escape's
+    code) never carries into the next byte of the decoders' four-codes-at-once add."""
+    rng = np.random.default_rng(9)
+    n = 1 << 16
+    ex = rng.integers(236, 256, n).astype(np.uint32)
+    words = ((rng.integers(0, 2, n).astype(np.uint32) << 15) | (ex << 7) | rng.integers(0, 128, n).astype(np.uint32))
+    words = words.astype(np.uint16)
+    out, base, esc, _ = _roundtrip(words)
+    assert base <= 240
+    assert np.array_equal(out, words)
+
+
 @pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("T,host_codec", [(16, False), (40, True), (100, True)])
 def test_fx4_device_tier_stack_equals_resident(X, fused, T, host_codec):
