@@ -341,6 +341,8 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
   const uint32_t tmem = *tmem_slot;
   const int K = GU ? p.H : p.F;
   const int KB = K / kBK;
+  // gate/up -> down overlap: the down launch may start on SMs this grid's tail leaves idle
+  if (GU && p.unit_done && threadIdx.x == 0) griddep_launch_dependents();
 
   if (warp == 0) {
     // ---- activation tiles (hi, lo) by TMA
@@ -354,6 +356,19 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
         if (!GU) split_kb(un.split, S, KB, &kb0, &kb1);
         const int nb = (un.n_rows + kBoxRowsB - 1) / kBoxRowsB;
         const uint32_t bytes = 2 * nb * kBoxRowsB * kBK * 2;
+        if (!GU && p.unit_done) {
+          // this group's h rows: every gate/up unit of the group has stored them (release
+          // counter), then order those generic-proxy stores before this thread's TMA reads
+          const int n = s_off[un.e + 1] - s_off[un.e];
+          const int need = ((n + BN - 1) / BN) * (p.F / kBM);
+          for (;;) {
+            int v;
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p.unit_done + un.e) : "memory");
+            if (v >= need || *(volatile long long*)p.fault != 0) break;
+            __nanosleep(200);
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait_backoff(&empty[stage], phase ^ 1);
           uint8_t* sb = smem + stage * C::STAGE + C::B_OFF;
@@ -466,6 +481,16 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
+      if (GU && p.unit_done) {
+        // the unit's h rows are stored: count it for the down launch (all 128 epilogue threads'
+        // stores, then one fenced release increment)
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (q == 0 && lane == 0) {
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          __threadfence();
+          atomicAdd(p.unit_done + un.e, 1);
+        }
+      }
     }
   } else if (warp == 6 + kDecWarps) {
     // ---- FX4 compressed stages by TMA, on their own warp so they run CST stages ahead of the
@@ -800,7 +825,21 @@ void launch_gemm_dec(bool gate_up, const CUtensorMap& map_b, const GemmParams& p
   static const bool fx_nodec = getenv("XPGB_FX_NODEC") && atoi(getenv("XPGB_FX_NODEC")) != 0;
   const int arg =
       fx4 ? ((fx_fence ? kFxFenceFlag : 0) | (fx_spin ? kFxSpinFlag : 0) | (fx_nodec ? kFxNoDecFlag : 0)) : chunk;
-  kern<<<grid, kDecThreads, smem, s>>>(map_b, p, tabs, arg);
+  if (!gate_up && p.unit_done) {  // overlaps the gate/up launch's tail (programmatic dependent launch)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kDecThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, map_b, p, tabs, arg);
+  } else {
+    kern<<<grid, kDecThreads, smem, s>>>(map_b, p, tabs, arg);
+  }
   note_launch();
 }
 

@@ -89,6 +89,10 @@ struct GemmParams {
   // kernel and are skipped by k_moe_gemm (nullptr: no fused groups)
   const DecRec* dec;
   uint32_t dec_fmt_mask;  // bit f: records of format f are read in place by k_moe_gemm_dec in this layer
+  // gate/up -> down overlap of the decode-into-GEMM kernels (nullptr: off): the gate/up launch
+  // counts each group's finished units here and lets the down launch start early (programmatic
+  // dependent launch); the down launch waits per group for all of that group's gate/up units
+  int* unit_done;
 };
 
 // ---- launchers (moe_kernels.cu)

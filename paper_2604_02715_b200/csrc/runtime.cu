@@ -323,6 +323,7 @@ struct Ctx {
   size_t fz_n = 0;
   // sampled profiling (opts.profile >= 2): events bracket 1 in prof_every decoder / fused launches
   int prof_every = 1, prof_mode = 0;
+  int* d_unit_done = nullptr;  // per-group gate/up unit counters of the fused gate/up -> down overlap
   size_t dec_seen = 0, fz_seen = 0;
   bool dec_skip = false, fz_skip = false;
   double fz_total_ns = 0;
@@ -375,6 +376,8 @@ static void free_pools(Ctx* c) {
   c->d_decrec = nullptr;
   if (c->d_fxmaps) cudaFree(c->d_fxmaps);
   c->d_fxmaps = nullptr;
+  if (c->d_unit_done) cudaFree(c->d_unit_done);
+  c->d_unit_done = nullptr;
   c->arena = nullptr;
   c->d_pt = nullptr;
   c->dev_tier = nullptr;
@@ -624,6 +627,7 @@ static GemmParams gemm_params(Ctx* c, int layer, int kind, const int32_t* offset
   p.splits = splits;
   p.dec = nullptr;
   p.dec_fmt_mask = 0;
+  p.unit_done = nullptr;
   return p;
 }
 
@@ -688,6 +692,15 @@ static void enqueue_window(Ctx* c, int layer, const float* x, float* y, int T, i
   } else {
     rest[0] = rest[1] = true;
   }
+  // gate/up -> down overlap (FX4 windows read wholly in place): the fused down launch starts in
+  // the fused gate/up launch's tail and waits per group on the gate/up units' counters
+  static const bool overlap_env = !(getenv("XPGB_FUSED_OVERLAP") && atoi(getenv("XPGB_FUSED_OVERLAP")) == 0);
+  const bool overlap = overlap_env && !pair && fused[0][1] && !fused[0][0] && !rest[0] && fused[1][1] && !fused[1][0];
+  if (overlap) {
+    if (!c->d_unit_done) CK(cudaMalloc(&c->d_unit_done, sizeof(int) * (kMaxExperts + 1)));
+    CK(cudaMemsetAsync(c->d_unit_done, 0, sizeof(int) * (e1 - e0), s));
+    pg.unit_done = pd.unit_done = c->d_unit_done;
+  }
   auto fused_launch = [&](bool gate_up, GemmParams& gp, const CUtensorMap& map, int kind) {
     for (int f = 0; f < 2; ++f) {
       if (!fused[kind - 1][f]) continue;
@@ -711,8 +724,10 @@ static void enqueue_window(Ctx* c, int layer, const float* x, float* y, int T, i
                      c->pair_split);
   else {
     fused_launch(false, pd, c->map_h, 2);
-    if (rest[1])
+    if (rest[1]) {
+      pd.unit_done = nullptr;  // the regular down runs after the fused one (stream order)
       launch_down(c->map_dn, c->map_h, c->S ? c->map_dn_sh : c->map_dn, pd, bn_dn, c->num_sms, s, lean_gemm(c));
+    }
   }
   CKLAUNCH();
   prof_rec(c, 5, s);

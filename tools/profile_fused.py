@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--tokens", type=int, default=256)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--modes", default="1,0")
+    ap.add_argument("--no-profile", action="store_true", help="no per-launch events (they serialise the launches)")
     ap.add_argument("--device-format", default="huffman", choices=["huffman", "fx4"])
     args = ap.parse_args()
     import numpy as np
@@ -47,7 +48,7 @@ def main():
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        rep = runner.run(args.steps, acts=x.clone(), profile=True)
+        rep = runner.run(args.steps, acts=x.clone(), profile=not args.no_profile)
         e1.record()
         torch.cuda.synchronize()
         assert rep.page_fault is None and rep.violations == []
