@@ -634,7 +634,10 @@ __global__ void __launch_bounds__(192, 1)
       if (C::NA == 2) tma_prefetch_l2_2d(mw, kb * kBK, wrow + (GU ? p.F : kBM));
     }
   }
-  griddep_wait();
+  // a down launch paired with counting gate/up launch waits per group on the counters instead
+  // (before its h loads); its outputs are written only after its group's gate/up units counted,
+  // which happens after that gate/up grid's own wait, so nothing it writes is still being read
+  if (GU || !p.unit_done) griddep_wait();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -650,6 +653,17 @@ __global__ void __launch_bounds__(192, 1)
         const int wrow = s_slot[un.e] * rows_per_block + un.m0;
         const CUtensorMap* mw = un.e < p.E_routed ? &map_w : &map_ws;
         const uint32_t bytes = C::NA * C::A_BYTES + 2 * nb * kBoxRowsB * kBK * 2;
+        if (!GU && p.unit_done) {
+          const int n = s_off[un.e + 1] - s_off[un.e];
+          const int need = ((n + p.unit_bn - 1) / p.unit_bn) * ((p.F + kBM - 1) / kBM);
+          for (;;) {
+            int v;
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p.unit_done + un.e) : "memory");
+            if (v >= need || *(volatile long long*)p.fault != 0) break;
+            __nanosleep(200);
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE;
@@ -756,6 +770,16 @@ __global__ void __launch_bounds__(192, 1)
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
+      if (GU && p.unit_done) {
+        // the unit's h rows are stored: count it for the down launch (all 128 epilogue threads'
+        // stores, then one fenced release increment)
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (q == 0 && lane == 0) {
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          __threadfence();
+          atomicAdd(p.unit_done + un.e, 1);
+        }
+      }
     }
   }
   tc_fence_before();

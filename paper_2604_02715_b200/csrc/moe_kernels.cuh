@@ -93,6 +93,7 @@ struct GemmParams {
   // counts each group's finished units here and lets the down launch start early (programmatic
   // dependent launch); the down launch waits per group for all of that group's gate/up units
   int* unit_done;
+  int unit_bn;  // token-tile width of the gate/up launch whose units unit_done counts (k_moe_gemm)
 };
 
 // ---- launchers (moe_kernels.cu)

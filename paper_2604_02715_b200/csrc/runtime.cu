@@ -628,6 +628,7 @@ static GemmParams gemm_params(Ctx* c, int layer, int kind, const int32_t* offset
   p.dec = nullptr;
   p.dec_fmt_mask = 0;
   p.unit_done = nullptr;
+  p.unit_bn = 0;
   return p;
 }
 
@@ -701,6 +702,15 @@ static void enqueue_window(Ctx* c, int layer, const float* x, float* y, int T, i
     CK(cudaMemsetAsync(c->d_unit_done, 0, sizeof(int) * (e1 - e0), s));
     pg.unit_done = pd.unit_done = c->d_unit_done;
   }
+  // the same overlap for the regular grouped GEMMs when they carry the whole window
+  const bool overlap_reg = overlap_env && !pair && !overlap && rest[0] && rest[1] && !fused[0][0] && !fused[0][1] &&
+                           !fused[1][0] && !fused[1][1];
+  if (overlap_reg) {
+    if (!c->d_unit_done) CK(cudaMalloc(&c->d_unit_done, sizeof(int) * (kMaxExperts + 1)));
+    CK(cudaMemsetAsync(c->d_unit_done, 0, sizeof(int) * (e1 - e0), s));
+    pg.unit_done = pd.unit_done = c->d_unit_done;
+    pg.unit_bn = pd.unit_bn = bn;
+  }
   auto fused_launch = [&](bool gate_up, GemmParams& gp, const CUtensorMap& map, int kind) {
     for (int f = 0; f < 2; ++f) {
       if (!fused[kind - 1][f]) continue;
@@ -725,7 +735,7 @@ static void enqueue_window(Ctx* c, int layer, const float* x, float* y, int T, i
   else {
     fused_launch(false, pd, c->map_h, 2);
     if (rest[1]) {
-      pd.unit_done = nullptr;  // the regular down runs after the fused one (stream order)
+      if (!overlap_reg) pd.unit_done = nullptr;  // the regular down runs after the fused one (stream order)
       launch_down(c->map_dn, c->map_h, c->S ? c->map_dn_sh : c->map_dn, pd, bn_dn, c->num_sms, s, lean_gemm(c));
     }
   }
