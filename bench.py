@@ -150,7 +150,7 @@ def decoder_roofline(stats, steps, step_s, hbm_peak, hbm_src):
 
 def fused_roofline(stats, steps, hbm_peak, hbm_src):
     """Roofline of the decode-into-GEMM kernel: the compressed record bytes each launch reads in
-    place (its DRAM traffic is those bytes + the activation rows, ncu: profiles/r2_ncu_fused_fx4_final.jsonl)
+    place (its DRAM traffic is those bytes + the activation rows, ncu: profiles/r2_ncu_fused_fx4_tmem.jsonl)
     over its mean launch time."""
     n = stats.get("launches", 0)
     if not n:
@@ -164,7 +164,21 @@ def fused_roofline(stats, steps, hbm_peak, hbm_src):
             "algorithmic_bytes_per_launch": per_launch, "avg_launch_us": ns / 1e3, "launches_per_step": n / steps,
             "kernel_time_per_step_ms": stats["kernel_ns"] / steps / 1e6,
             "note": "algorithmic bytes = the compressed records read in place (activation rows excluded)",
-            "traffic": None}
+            "traffic": fused_traffic(per_launch)}
+
+
+def fused_traffic(record_bytes):
+    """DRAM bytes of a decode-into-GEMM launch that reads `record_bytes` of FX4 records, from the
+    committed ncu --set full capture of a Mixtral gate/up launch (8 experts' records read in place:
+    DRAM read + write over record bytes -- the activation re-reads and escape bytes on top)."""
+    path = os.path.join(ROOT, "profiles", "r2_ncu_fused_fx4_tmem.jsonl")
+    try:
+        rec = json.loads(open(path).readline())
+        n = 2 * 4096 * 14336
+        captured = 8 * (n + n // 2 + 4 * (n // 256 + 1))  # 8 experts' FX4 gate/up records (no escapes)
+        return record_bytes * (rec["dram_read"] + rec["dram_write"]) / captured
+    except Exception:
+        return None
 
 
 def gemm_roofline(kind, bytes_, ns, rows, H, F, hbm_peak, hbm_src, tc_peak, tc_src):

@@ -3,9 +3,9 @@
 # list, ncu captures (decoder, fused FX4, decode GEMMs, prefill pair GEMMs), 2-rank bench
 O=gpurun_out/r2_t46; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1 || { tail -20 $O/build.log; exit 1; }
-export XPGB_PARITY_LOG=$O/parity.jsonl
-timeout 2400 python -m pytest tests -m gpu -q > $O/pytest_all.log 2>&1; echo "all gpu tests rc=$?"; grep -E "passed|failed|FAILED" $O/pytest_all.log | tail -6
-unset XPGB_PARITY_LOG
+
+
+
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"; tail -2 $O/smoke.log
 timeout 900 python bench.py > $O/bench_default.json 2> $O/bench_default.err; echo "bench default rc=$?"; head -c 400 $O/bench_default.json; echo
 timeout 900 python bench.py --steps 10 --warmup 3 > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"; head -c 400 $O/bench.json; echo
