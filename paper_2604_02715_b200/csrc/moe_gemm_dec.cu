@@ -80,16 +80,21 @@ struct DecCfg {
   static constexpr int UP_OFF = FMT == 2 ? BN : 128;
   static constexpr int A_COL = 384;
   static_assert(FMT != 2 || (4 * BN <= A_COL && STAGES == 2), "TMEM-A tiles: BN <= 96, two stages");
+  // activation stages in shared memory: with the A tiles in TMEM (two stages there) the
+  // activations get their own deeper ring, so a stage's TMA load is issued BST - 1 stages ahead
+  // of its MMAs instead of one (with two shared stages the L2 latency of every activation load
+  // sat in the MMA loop: r2_t54, no unit saturated -- DRAM 42%, L2 33%, issue 50%)
+  static constexpr int BST = FMT == 2 ? 4 : STAGES;
   static constexpr int TAB_BYTES = FMT ? (2 * kMaxExperts + 4) * 4 : (3 * kMaxExperts + 8) * 4;  // s_off, s_up (+ flag)
   static constexpr int DEC_TAB =
       FMT ? 0 : (((1 << kPairBits) * 4 + 3 * (kCodecMaxLen + 1) * 4 + kCodecSymbols + 15) & ~15);
   static constexpr int RING = FMT ? 0 : kDecThreads_dec * kRingBytes;  // per-decoder-thread bitstream rings
   // compressed stages (FX4): as many as fit beside the decoded stages, 2..4
-  static constexpr int CST_FIT = (227 * 1024 - 1024 - 256 - TAB_BYTES - STAGES * STAGE) / kFxCStage;
+  static constexpr int CST_FIT = (227 * 1024 - 1024 - 256 - TAB_BYTES - BST * STAGE) / kFxCStage;
   static constexpr int CST_MAX = FMT == 2 ? kFxMaxCst : 4;
   static constexpr int CST = FMT ? (CST_FIT > CST_MAX ? CST_MAX : CST_FIT) : 0;
   static_assert(!FMT || CST >= 2, "FX4 decode-GEMM needs two compressed stages");
-  static constexpr int BAR_OFF = STAGES * STAGE + CST * kFxCStage;       // barriers, then the tables
+  static constexpr int BAR_OFF = BST * STAGE + CST * kFxCStage;          // barriers, then the tables
   static constexpr int SMEM = BAR_OFF + 1024 + 256 + TAB_BYTES + DEC_TAB + RING;
   static_assert(SMEM <= 227 * 1024, "decode-GEMM stages exceed 227 KB");
 };
@@ -250,14 +255,16 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
   constexpr int RFMT = FMT == 2 ? 1 : FMT;  // record format
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_1k(smem_raw);
-  uint8_t* cstage = smem + STAGES * C::STAGE;  // FX4 compressed stages (CST of them)
+  uint8_t* cstage = smem + C::BST * C::STAGE;  // FX4 compressed stages (CST of them)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint64_t* empty = full + C::BST;
+  uint64_t* tfull = empty + C::BST;
   uint64_t* tempty = tfull + 2;
   uint64_t* cfull = tempty + 2;  // FX4: compressed stage filled (TMA bytes)
   uint64_t* cempty = cfull + kFxMaxCst;  // FX4: compressed stage read by all decoder warps
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + kFxMaxCst);
+  uint64_t* afull = cempty + kFxMaxCst;  // FMT 2: decoded A stage in TMEM written (decoder warps)
+  uint64_t* aempty = afull + 2;          // FMT 2: decoded A stage read by the MMAs
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 2);
   int* s_off = reinterpret_cast<int*>(smem + C::BAR_OFF + 256);
   int* s_up = s_off + kMaxExperts + 1;
   int* s_flag = s_up + kMaxExperts + 1;
@@ -315,10 +322,11 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_b);
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1 + kDecWarps);
+    for (int s = 0; s < C::BST; ++s) {
+      mbar_init(&full[s], FMT == 2 ? 1 : 1 + kDecWarps);  // FMT 2: activations only
       mbar_init(&empty[s], 1);
     }
+    for (int s = 0; s < 2; ++s) { mbar_init(&afull[s], kDecWarps); mbar_init(&aempty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
     for (int c = 0; c < kFxMaxCst; ++c) { mbar_init(&cfull[c], 1); mbar_init(&cempty[c], kDecWarps); }
     fence_mbar_init();
@@ -379,14 +387,16 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
             tma_load_2d(sb + C::B_BYTES + i * kBoxRowsB * kBK * 2, &map_b, &full[stage], kb * kBK,
                         (int)(un.row_begin + p.act_lo_rows) + i * kBoxRowsB, pol_b);
           }
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == C::BST) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     // ---- MMA issuer: A tile 0 -> d0, A tile 1 -> d0 + 128, each against the hi and lo planes
-    int stage = 0;
+    int stage = 0;       // activation (and, FMT 0/1, A) stage
     uint32_t phase = 0;
+    int ast = 0;         // FMT 2: decoded A stage in TMEM
+    uint32_t aph = 0;
     int it = 0;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
       const DUnit un = dec_unit(u, s_up, s_off, E, BN, S);
@@ -400,6 +410,7 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
       const uint32_t d0 = tmem + acc * C::ACC_W;
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait_role(&full[stage], phase, FMT >= 1 && (chunk & kFxSpinFlag));
+        if constexpr (FMT == 2) mbar_wait_role(&afull[ast], aph, chunk & kFxSpinFlag);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t base = smem_u32(smem + stage * C::STAGE);
@@ -410,7 +421,7 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
             const uint64_t bdesc_lo = sdesc_k_sw128(bbase + C::B_BYTES + 32 * k);
             const uint32_t accum = (kb > kb0 || k > 0) ? 1u : 0u;
             if constexpr (FMT == 2) {
-              const uint32_t a0 = tmem + C::A_COL + stage * 64 + 8 * k, a1 = a0 + 32;
+              const uint32_t a0 = tmem + C::A_COL + ast * 64 + 8 * k, a1 = a0 + 32;
               umma_bf16_ts(d0, a0, bdesc, idesc, accum);
               umma_bf16_ts(d0, a0, bdesc_lo, idesc, 1u);
               umma_bf16_ts(d0 + C::UP_OFF, a1, bdesc, idesc, accum);
@@ -425,9 +436,11 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
             }
           }
           umma_commit(&empty[stage]);
+          if constexpr (FMT == 2) umma_commit(&aempty[ast]);
         }
         __syncwarp();
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        if (++stage == C::BST) { stage = 0; phase ^= 1; }
+        if (++ast == 2) { ast = 0; aph ^= 1; }
       }
       if (lane == 0) umma_commit(&tfull[acc]);
       __syncwarp();
@@ -650,12 +663,13 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
         __syncwarp();
         if (lane == 0) mbar_arrive(&cempty[fcs]);
         if (++fcs == C::CST) { fcs = 0; fcph ^= 1; }
-        mbar_wait_role(&empty[stage], phase ^ 1, chunk & kFxSpinFlag);
+        mbar_wait_role(FMT == 2 ? &aempty[stage] : &empty[stage], phase ^ 1, chunk & kFxSpinFlag);
         if constexpr (FMT == 2) {
           // the stage's 64 values of this row -> 32 registers (bf16 pairs, K order) -> TMEM
           // lane lr, columns A_COL + stage * 64 + a * 32 .. + 31; escapes patched in registers
           tc_fence_after();  // after the empty wait: the MMAs that read this stage are complete
           uint32_t o[32];
+          const uint32_t bb7 = bb & 0x00FF00FFu;  // base at bytes 0 and 2: (code pair << 7) + (base pair << 7)
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const uint4& nq = nv[q >> 2];
@@ -664,14 +678,16 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
             const uint32_t sa = (q & 1) ? sq.z : sq.x, sb = (q & 1) ? sq.w : sq.y;
             const uint32_t lo = nw & 0x0F0F0F0Fu, hi = (nw >> 4) & 0x0F0F0F0Fu;
             const uint32_t escf = ((lo + 0x01010101u) | (hi + 0x01010101u)) & 0x10101010u;
-            const uint32_t le = lo + bb, he = hi + bb;  // base <= 240: no carry between bytes
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              // y = [le_j, le_j, he_j, he_j]: << 7 puts the two exponents at bits 7..14 and 23..30,
-              // one bit-select merges them with the sign/mantissa bytes (4 ops per value pair)
-              const uint32_t y = __byte_perm(le, he, (uint32_t)(j | (j << 4) | ((4 + j) << 8) | ((4 + j) << 12)));
+              // y = [lo_j, lo_j, hi_j, hi_j] (codes of values 2j, 2j+1); y * 128 + base pair puts
+              // the two exponents at bits 7..14 and 23..30 (code + base <= 255: no carry out of a
+              // field; the duplicate bytes land in bits the bit-select drops), and one bit-select
+              // merges them with the sign/mantissa bytes: 4 ops per value pair
+              const uint32_t y = __byte_perm(lo, hi, (uint32_t)(j | (j << 4) | ((4 + j) << 8) | ((4 + j) << 12)));
+              const uint32_t ex = y * 128u + (bb7 << 7);
               const uint32_t dup = __byte_perm(j < 2 ? sa : sb, 0, (j & 1) ? 0x3322u : 0x1100u);
-              o[4 * q + j] = (dup & 0x807F807Fu) | ((y << 7) & 0x7F807F80u);
+              o[4 * q + j] = (dup & 0x807F807Fu) | (ex & 0x7F807F80u);
             }
             // (one branch per stage instead of per quad: 15% slower, the unrolled patch block
             // changed the schedule of the whole stage)
@@ -688,6 +704,7 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
           if (!valid)
 #pragma unroll
             for (int i = 0; i < 32; ++i) o[i] = 0u;
+
           tmem_st32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(C::A_COL + stage * 64 + a * 32), o);
           tc_fence_before();  // the stores before the MMA warp's barrier wait
         } else if (valid && (chunk & kFxNoDecFlag)) {  // timing A/B: raw stores, no decode
@@ -730,7 +747,7 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
         }
         if constexpr (FMT != 2) fence_async_smem();  // the A tile's generic stores before the tensor cores' reads
         __syncwarp();
-        if (lane == 0) mbar_arrive(&full[stage]);
+        if (lane == 0) mbar_arrive(FMT == 2 ? &afull[stage] : &full[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
       }
