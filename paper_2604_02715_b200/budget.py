@@ -148,9 +148,18 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
         window = int(max(1, -(-min_window_bytes // eb)))
     w_min = int(min(L, window))
     best = None
-    p_grid = range(0, total + 1) if allow_pinned else [0]
+    # with the device tier read in place, pinned experts run in a second GEMM launch beside the
+    # layer's decode-into-GEMM launch (two half-empty waves, no gate/up -> down overlap): measured
+    # slower per expert than the FX4 experts they replace (Mixtral 90%, 27 pinned: 42.2 K tok/s vs
+    # 45.3 K at 80% with 2, r2_t58), so fused plans pin whole layers only
+    whole = dev_fused
+    p_grid = (range(0, total + 1, L) if whole else range(0, total + 1)) if allow_pinned else [0]
+
+    def layers_of(p):
+        return [L * c for c in _spaced(p // L, N)] if whole else _balanced(p, N)
+
     for p in p_grid:
-        p_layer = _balanced(p, N)
+        p_layer = layers_of(p)
         streamed_max = L - min(p_layer)
         if streamed_max == 0:
             ring = 0
@@ -187,7 +196,7 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
                                   allow_pinned=allow_pinned, depth=depth, window=max(1, w_min // 2), **kw)
         raise ValueError(f"budget {budget_bytes:.3g} B cannot hold a ring")
     (est, _), p, d, ring, link = best
-    p_layer = _balanced(p, N)
+    p_layer = layers_of(p)
     # host-tier experts spaced evenly over the layers: each host record then has the
     # layers since the previous one to cross the link (the staging ring holds about one
     # record ahead), instead of queueing behind a neighbour (Mixtral 80%: 3 host experts
@@ -213,10 +222,10 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
 # `calibrate`, profiles/r2_calibrate_mixtral_v2.json): the Huffman decoder expanding into the ring
 # beside the GEMMs (raw bytes over the step time beyond resident compute), and
 # the decode-into-GEMM kernel reading FX4 records through TMA-staged compressed stages (GEMM
-# included, profiles/r2_fused_fx4_mixtral_v3.jsonl).  Resident GEMMs stream raw
+# included: 4.28 TB/s raw-equivalent with the A tiles in TMEM, `calibrate` in r2_t58).  Resident GEMMs stream raw
 # weights at about 5.2 TB/s.
 B_DEC_HUFFMAN = 1.8e12
-B_FUSED_FX4 = 3.2e12
+B_FUSED_FX4 = 4.2e12
 B_RESIDENT = 5.2e12
 HOST_EXPOSED = 0.5  # share of the host link time an SM-bound step cannot hide
 
