@@ -337,3 +337,23 @@ def test_tier_plan_mixed_device_tier_between_the_formats():
     assert "mixed" in seen and seen[-1] == "fx4"
     pl = plan_tiers(N, L, eb, ceb, 0.72 * N * L * eb, fx4_ceb=fx, device_format="mixed", units_per_expert=F // 128)
     assert pl.device_format == "mixed"
+
+
+def test_fused_plans_pin_whole_layers():
+    """Decode-into-GEMM plans pin whole layers (a layer's pinned experts would otherwise run in a
+    second, mostly idle GEMM launch beside its FX4 launch), spaced over the stack."""
+    from paper_2604_02715_b200.budget import fx4_expert_bytes, plan_tiers
+
+    H, F, N, L = 4096, 14336, 8, 8
+    eb = 3 * H * F * 2
+    ceb, fx = 0.6655 * 1.012 * eb, fx4_expert_bytes(H, F)
+    for b in (0.8, 0.85, 0.9, 0.95):
+        pl = plan_tiers(N, L, eb, ceb, b * N * L * eb, fx4_ceb=fx, units_per_expert=F // 128)
+        assert pl.hbm_bytes <= b * N * L * eb + 1
+        if pl.fused is True:
+            per_layer = pl.pinned_mask.sum(axis=1)
+            assert set(per_layer.tolist()) <= {0, L}
+    pl = plan_tiers(N, L, eb, ceb, 0.9 * N * L * eb, fx4_ceb=fx, units_per_expert=F // 128)
+    assert pl.device_format == "fx4" and pl.pinned_experts > 0
+    pinned_layers = [l for l in range(N) if pl.pinned_mask[l].all()]
+    assert len(pinned_layers) < 2 or min(b - a for a, b in zip(pinned_layers, pinned_layers[1:])) >= 2
