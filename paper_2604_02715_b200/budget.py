@@ -322,8 +322,10 @@ def _plan_mixed(N: int, L: int, eb: float, ceb: float, fx4_ceb: float, budget_by
     if step <= 0:
         return None
     best = None
-    for p in (range(0, total + 1) if allow_pinned else [0]):
-        p_layer = _balanced(p, N)
+    # pinned experts in whole layers only, as in the fused plans (plan_residency)
+    whole_layers = lambda p: [L * c for c in _spaced(p // L, N)]
+    for p in (range(0, total + 1, L) if allow_pinned else [0]):
+        p_layer = whole_layers(p)
         S = total - p
         if S == 0:
             break
@@ -347,7 +349,7 @@ def _plan_mixed(N: int, L: int, eb: float, ceb: float, fx4_ceb: float, budget_by
     if best is None:
         return None
     (est, _), p, x, ring, h_layer = best
-    p_layer = _balanced(p, N)
+    p_layer = whole_layers(p)
     pinned = np.zeros((N, L), dtype=bool)
     device = np.zeros((N, L), dtype=bool)
     fx4 = np.zeros((N, L), dtype=bool)
