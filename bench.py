@@ -145,7 +145,18 @@ def decoder_roofline(stats, steps, step_s, hbm_peak, hbm_src):
             "note": "launches overlap each other (two kinds, host and device tiers) and the GEMMs, so a launch's "
                     "time includes sharing the SMs; standalone the kernel reaches ~1,450-1,540 GB/s of bf16 output "
                     "on a 117M-value tensor, bound by the per-stream decode chain (profiles/r2_decoder_experiments.md)",
-            "traffic": None, "traffic_capture": ncu_decoder_capture()}
+            "traffic": decoder_traffic(per_launch), "traffic_capture": ncu_decoder_capture()}
+
+
+def decoder_traffic(algo_bytes):
+    """DRAM bytes of a decoder launch with `algo_bytes` algorithmic bytes, scaled from the
+    committed ncu --set full capture of one launch (DRAM / algorithmic = 0.89 there: the
+    bitstream words a thread reads twice at chunk edges hit L2, and part of the output is still
+    in L2 when the capture ends)."""
+    cap = ncu_decoder_capture()
+    if not cap:
+        return None
+    return algo_bytes * cap["dram_bytes"] / cap["algorithmic_bytes"]
 
 
 def fused_roofline(stats, steps, hbm_peak, hbm_src):
