@@ -359,6 +359,10 @@ int xpgb_session_materialize(xpgb_ctx* ctx, int32_t step);  /* _materialize, pip
 int xpgb_session_acquire(xpgb_ctx* ctx, int32_t step, void* stream); /* RAW wait + compute-start */
 int xpgb_session_compute(xpgb_ctx* ctx, int32_t step);      /* built-in layer_forward of the step */
 int xpgb_session_release(xpgb_ctx* ctx, int32_t step, void* stream); /* compute-done + WAR event */
+/* Steps first .. first+count-1 with the built-in compute, each as acquire(g, s); compute(g);
+ * release(g, s); materialize(g+2) -- one call per served iteration instead of four per step
+ * (the host enqueue sits between a step's output readback and the next step's first kernels). */
+int xpgb_session_run_steps(xpgb_ctx* ctx, int32_t first, int32_t count, void* stream);
 int xpgb_session_end(xpgb_ctx* ctx, xpgb_report* rep);
 int xpgb_session_abort(xpgb_ctx* ctx);
 /* Shape of the active session's schedule and the stream the built-in compute runs on (the

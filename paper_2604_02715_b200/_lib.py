@@ -109,6 +109,7 @@ _SIGS = {
     "xpgb_session_materialize": [_P, _I],
     "xpgb_session_acquire": [_P, _I, _P],
     "xpgb_session_compute": [_P, _I],
+    "xpgb_session_run_steps": [_P, _I, _I, _P],
     "xpgb_session_release": [_P, _I, _P],
     "xpgb_session_end": [_P, C.POINTER(Report)],
     "xpgb_session_abort": [_P],

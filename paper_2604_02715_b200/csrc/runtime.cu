@@ -2765,6 +2765,24 @@ int xpgb_session_compute(xpgb_ctx* h, int32_t step) {
 int xpgb_session_release(xpgb_ctx* h, int32_t step, void* stream) {
   return guard([&] { session_release(&h->c, step, (cudaStream_t)stream); });
 }
+int xpgb_session_run_steps(xpgb_ctx* h, int32_t first, int32_t count, void* stream) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    if (!session_of(c).rs.acts) XFAIL(XPGB_ERR, "session has no activation buffer for built-in compute");
+    if (count < 0) XFAIL(XPGB_ERR_OUT_OF_RANGE, "step count %d", count);
+    try {
+      for (int32_t g = first; g < first + count; ++g) {
+        session_acquire(c, g, (cudaStream_t)stream);
+        session_compute(c, g);
+        session_release(c, g, (cudaStream_t)stream);
+        session_materialize(c, g + 2);
+      }
+    } catch (...) {
+      session_abort(c);
+      throw;
+    }
+  });
+}
 int xpgb_session_end(xpgb_ctx* h, xpgb_report* rep) {
   return guard([&] {
     if (!rep) XFAIL(XPGB_ERR, "null argument");

@@ -477,16 +477,11 @@ class DecodeSession:
         ev = torch.cuda.Event()
         ev.record(cur)
         self.stream.wait_event(ev)
-        try:
-            for _ in range(self.steps_per_iteration):
-                call("xpgb_session_acquire", h, self.g, C.c_void_p(self._stream_ptr))
-                call("xpgb_session_compute", h, self.g)
-                call("xpgb_session_release", h, self.g, C.c_void_p(self._stream_ptr))
-                call("xpgb_session_materialize", h, self.g + 2)
-                self.g += 1
+        try:  # the iteration's steps in one call (acquire / compute / release / materialize(g+2))
+            call("xpgb_session_run_steps", h, self.g, self.steps_per_iteration, C.c_void_p(self._stream_ptr))
+            self.g += self.steps_per_iteration
         except Exception:
-            _lib.lib().xpgb_session_abort(h)
-            self.closed = True
+            self.closed = True  # the library aborted the session
             raise
         self.iteration += 1
         dst = out if out is not None else torch.empty(self.acts.shape, dtype=torch.float32,
