@@ -219,3 +219,25 @@ def test_mixed_plan_full_shape_equals_resident(X):
     model = X.ResidentModel(spec, container, max_tokens=T)
     y, _ = model.run(2, fwd, x.clone())
     assert paged.tobytes() == y.cpu().numpy().tobytes()
+
+
+def test_device_formats_rejects_bad_entries(X):
+    """xpgb_set_device_formats: entries other than 0 / 1 fail loudly, the tier is left as it was."""
+    from paper_2604_02715_b200.errors import XpgError
+
+    spec = X.ModelSpec(2, 4, 256, 512)
+    fwd = X.ForwardSpec(8, 2, 7)
+    container = X.generate_synthetic_model(spec, 7)
+    backends = [X.Backend(1, X.BackendKind.COMPRESSED_DEVICE, 300e9, 1 << 50)]
+    hier = X.StorageHierarchy(container, None, X.plan_placement(spec, backends, alpha=1.0), backends)
+    runner = X.StreamedRunner(spec, hier, fwd)
+    before = runner.ctx.hbm_bytes()["device_tier"]
+    bad = np.zeros((spec.num_layers, spec.experts_per_layer, 2), dtype=np.uint8)
+    bad[1, 2, 0] = 2
+    with pytest.raises(XpgError):
+        runner.ctx.set_device_formats(bad)
+    assert runner.ctx.hbm_bytes()["device_tier"] == before
+    x = X.initial_activations(spec, fwd, 7)
+    rep = runner.run(1, acts=x.copy())
+    base = X.resident_baseline(1, spec, container, fwd, acts=x.copy())
+    assert rep.page_fault is None and np.asarray(rep.final_activations).tobytes() == np.asarray(base).tobytes()
