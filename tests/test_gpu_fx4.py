@@ -228,7 +228,8 @@ def test_device_formats_rejects_bad_entries(X):
     spec = X.ModelSpec(2, 4, 256, 512)
     fwd = X.ForwardSpec(8, 2, 7)
     container = X.generate_synthetic_model(spec, 7)
-    backends = [X.Backend(1, X.BackendKind.COMPRESSED_DEVICE, 300e9, 1 << 50)]
+    backends = [X.Backend(1, X.BackendKind.COMPRESSED_DEVICE, 300e9, 1 << 50),
+                X.Backend(2, X.BackendKind.HOST_OFFLOAD, 30e9, 1 << 50)]
     hier = X.StorageHierarchy(container, None, X.plan_placement(spec, backends, alpha=1.0), backends)
     runner = X.StreamedRunner(spec, hier, fwd)
     before = runner.ctx.hbm_bytes()["device_tier"]
