@@ -499,6 +499,9 @@ def main():
     ap.add_argument("--ref-sample-tokens", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-resident", action="store_true")
+    ap.add_argument("--act-planes", type=int, default=2, choices=[1, 2],
+                    help="activation planes of the decode-sized GEMMs: 2 = bf16 hi + lo (fp32-like, default), "
+                         "1 = bf16 activations (half the MMAs; rel-L2 ~3e-3, inside the 1e-2 tolerance)")
     ap.add_argument("--no-timed-profile", action="store_true",
                     help="A/B only: time the paged run without its per-launch events (no kernel rooflines)")
     ap.add_argument("--ep", action="store_true", help="use the expert-parallel runner even at N=1")
@@ -634,6 +637,7 @@ def main():
             log(f"packed compressed host pool: ratio {hier.compressed.ratio:.4f} "
                 f"({hier.compressed.wire_bytes / 1e9:.2f} GB) in {time.time() - t1:.1f}s")
         runner = X.StreamedRunner(spec, hier, fwd, mode="threaded", device=dev, host_codec=args.host_codec, **run_kw)
+        runner.ctx.set_activation_planes(args.act_planes)
         hbm = runner.ctx.hbm_bytes()
         expert_bytes = cspec.total_bytes + (container.shared.total_bytes if container.shared is not None else 0)
         # fixed expert-HBM budget (north star): HBM holding expert weights -- ring slots, the
@@ -747,6 +751,7 @@ def main():
         gc.collect()
         torch.cuda.empty_cache()
         model = X.ResidentModel(spec, container, device=dev, max_tokens=T_run, **run_kw)
+        model.ctx.set_activation_planes(args.act_planes)
         model.run(args.warmup, fwd, x_dev)
         torch.cuda.synchronize()
         r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -819,6 +824,7 @@ def main():
                    "device_tier_format": dev_format if not use_ep else "huffman",
                    "decode_into_gemm": bool(dev_fused) if not use_ep else False,
                    "fx4_experts_per_layer": round(fx4_per_layer, 3) if not use_ep else 0.0,
+                   "activation_planes": args.act_planes,
                    "placement": ("2-layer ring" if use_ep or ring_blocks >= 2 * cspec.experts_per_layer else
                                  f"sub-layer ring of {ring_blocks} expert blocks per kind ({ring_depth} window(s) "
                                  f"in flight of {max(1, ring_blocks // ring_depth)} expert(s))") + (

@@ -279,6 +279,13 @@ int xpgb_set_ring_depth(xpgb_ctx* ctx, int32_t depth);
  * decoder's serial chain makes in-place decoding slower than decode-into-ring).  No session may
  * be active. */
 int xpgb_set_fused_decode(xpgb_ctx* ctx, int32_t mode);
+/* Activation planes the decode-sized (1-CTA) grouped GEMMs multiply: 2 (default) = the bf16 hi
+ * and lo planes of every fp32 activation (fp32-like products: per-layer rel-L2 ~1e-5..5e-5 vs the
+ * reference's fp32 forward), 1 = the hi plane only (bf16 activations: half the MMAs and half the
+ * activation traffic; rel-L2 ~3e-3, inside the 1e-2 tolerance).  Streamed and resident runs of one
+ * setting stay bit-identical; the CTA-pair prefill GEMMs always use both planes.  No session may
+ * be active. */
+int xpgb_set_activation_planes(xpgb_ctx* ctx, int32_t planes);
 /* Record format of the compressed device tier: 0 = exponent-Huffman (default; the host pool's
  * records staged as they are, the reference's device tier, storage.py:143-168), 1 = FX4
  * (fx4.cuh; encoded on the GPU from the raw host pool when staged).  FX4 costs ~13% more HBM per

@@ -122,6 +122,7 @@ _SIGS = {
     "xpgb_set_ring_experts": [_P, _I],
     "xpgb_set_ring_depth": [_P, _I],
     "xpgb_set_fused_decode": [_P, _I],
+    "xpgb_set_activation_planes": [_P, _I],
     "xpgb_set_device_format": [_P, _I],
     "xpgb_set_device_formats": [_P, C.POINTER(C.c_uint8)],
     "xpgb_set_host_staging": [_P, _I],

@@ -363,7 +363,7 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
         int kb0 = 0, kb1 = KB;
         if (!GU) split_kb(un.split, S, KB, &kb0, &kb1);
         const int nb = (un.n_rows + kBoxRowsB - 1) / kBoxRowsB;
-        const uint32_t bytes = 2 * nb * kBoxRowsB * kBK * 2;
+        const uint32_t bytes = (p.act_lo ? 2 : 1) * nb * kBoxRowsB * kBK * 2;
         if (!GU && p.unit_done) {
           // this group's h rows: every gate/up unit of the group has stored them (release
           // counter), then order those generic-proxy stores before this thread's TMA reads
@@ -384,8 +384,9 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
           for (int i = 0; i < nb; ++i) {
             tma_load_2d(sb + i * kBoxRowsB * kBK * 2, &map_b, &full[stage], kb * kBK, un.row_begin + i * kBoxRowsB,
                         pol_b);
-            tma_load_2d(sb + C::B_BYTES + i * kBoxRowsB * kBK * 2, &map_b, &full[stage], kb * kBK,
-                        (int)(un.row_begin + p.act_lo_rows) + i * kBoxRowsB, pol_b);
+            if (p.act_lo)
+              tma_load_2d(sb + C::B_BYTES + i * kBoxRowsB * kBK * 2, &map_b, &full[stage], kb * kBK,
+                          (int)(un.row_begin + p.act_lo_rows) + i * kBoxRowsB, pol_b);
           }
           if (++stage == C::BST) { stage = 0; phase ^= 1; }
         }
@@ -423,16 +424,16 @@ __global__ void __maxnreg__(128)  // 480 threads x 128 registers (448 x 144 was 
             if constexpr (FMT == 2) {
               const uint32_t a0 = tmem + C::A_COL + ast * 64 + 8 * k, a1 = a0 + 32;
               umma_bf16_ts(d0, a0, bdesc, idesc, accum);
-              umma_bf16_ts(d0, a0, bdesc_lo, idesc, 1u);
+              if (p.act_lo) umma_bf16_ts(d0, a0, bdesc_lo, idesc, 1u);
               umma_bf16_ts(d0 + C::UP_OFF, a1, bdesc, idesc, accum);
-              umma_bf16_ts(d0 + C::UP_OFF, a1, bdesc_lo, idesc, 1u);
+              if (p.act_lo) umma_bf16_ts(d0 + C::UP_OFF, a1, bdesc_lo, idesc, 1u);
             } else {
               const uint64_t a0 = sdesc_k_sw128(base + 32 * k);
               const uint64_t a1 = sdesc_k_sw128(base + C::A_BYTES + 32 * k);
               umma_bf16(d0, a0, bdesc, idesc, accum);
-              umma_bf16(d0, a0, bdesc_lo, idesc, 1u);
+              if (p.act_lo) umma_bf16(d0, a0, bdesc_lo, idesc, 1u);
               umma_bf16(d0 + 128, a1, bdesc, idesc, accum);
-              umma_bf16(d0 + 128, a1, bdesc_lo, idesc, 1u);
+              if (p.act_lo) umma_bf16(d0 + 128, a1, bdesc_lo, idesc, 1u);
             }
           }
           umma_commit(&empty[stage]);

@@ -652,7 +652,7 @@ __global__ void __launch_bounds__(192, 1)
         const int nb = (un.n_rows + kBoxRowsB - 1) / kBoxRowsB;
         const int wrow = s_slot[un.e] * rows_per_block + un.m0;
         const CUtensorMap* mw = un.e < p.E_routed ? &map_w : &map_ws;
-        const uint32_t bytes = C::NA * C::A_BYTES + 2 * nb * kBoxRowsB * kBK * 2;
+        const uint32_t bytes = C::NA * C::A_BYTES + (p.act_lo ? 2 : 1) * nb * kBoxRowsB * kBK * 2;
         if (!GU && p.unit_done) {
           const int n = s_off[un.e + 1] - s_off[un.e];
           const int need = ((n + p.unit_bn - 1) / p.unit_bn) * ((p.F + kBM - 1) / kBM);
@@ -674,8 +674,9 @@ __global__ void __launch_bounds__(192, 1)
           for (int i = 0; i < nb; ++i) {
             tma_load_2d(sb + i * kBoxRowsB * kBK * 2, &map_b, &full[stage], kb * kBK, un.row_begin + i * kBoxRowsB,
                         pol_b);
-            tma_load_2d(sb + C::B_BYTES + i * kBoxRowsB * kBK * 2, &map_b, &full[stage], kb * kBK,
-                        (int)(un.row_begin + p.act_lo_rows) + i * kBoxRowsB, pol_b);
+            if (p.act_lo)
+              tma_load_2d(sb + C::B_BYTES + i * kBoxRowsB * kBK * 2, &map_b, &full[stage], kb * kBK,
+                          (int)(un.row_begin + p.act_lo_rows) + i * kBoxRowsB, pol_b);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -708,11 +709,11 @@ __global__ void __launch_bounds__(192, 1)
             const uint32_t accum = (kb > kb0 || k > 0) ? 1u : 0u;
             const uint64_t adesc = sdesc_k_sw128(base + 32 * k);
             umma_bf16(d0, adesc, bdesc, idesc, accum);
-            umma_bf16(d0, adesc, bdesc_lo, idesc, 1u);
+            if (p.act_lo) umma_bf16(d0, adesc, bdesc_lo, idesc, 1u);
             if (C::NA == 2) {
               const uint64_t adesc_u = sdesc_k_sw128(base + C::A_BYTES + 32 * k);
               umma_bf16(d0 + 128, adesc_u, bdesc, idesc, accum);
-              umma_bf16(d0 + 128, adesc_u, bdesc_lo, idesc, 1u);
+              if (p.act_lo) umma_bf16(d0 + 128, adesc_u, bdesc_lo, idesc, 1u);
             }
           }
           umma_commit(&empty[stage]);

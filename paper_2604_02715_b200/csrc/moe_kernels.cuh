@@ -94,6 +94,8 @@ struct GemmParams {
   // dependent launch); the down launch waits per group for all of that group's gate/up units
   int* unit_done;
   int unit_bn;  // token-tile width of the gate/up launch whose units unit_done counts (k_moe_gemm)
+  int act_lo;   // 1: the activations' lo plane is multiplied too (fp32-like); 0: the hi plane only
+                // (bf16 activations, half the MMAs; xpgb_set_activation_planes) -- 1-CTA kernels
 };
 
 // ---- launchers (moe_kernels.cu)

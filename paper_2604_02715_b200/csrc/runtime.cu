@@ -324,6 +324,7 @@ struct Ctx {
   // sampled profiling (opts.profile >= 2): events bracket 1 in prof_every decoder / fused launches
   int prof_every = 1, prof_mode = 0;
   int* d_unit_done = nullptr;  // per-group gate/up unit counters of the fused gate/up -> down overlap
+  int act_planes = 2;          // activation planes the 1-CTA GEMMs multiply (xpgb_set_activation_planes)
   size_t dec_seen = 0, fz_seen = 0;
   bool dec_skip = false, fz_skip = false;
   double fz_total_ns = 0;
@@ -629,6 +630,7 @@ static GemmParams gemm_params(Ctx* c, int layer, int kind, const int32_t* offset
   p.dec_fmt_mask = 0;
   p.unit_done = nullptr;
   p.unit_bn = 0;
+  p.act_lo = c->act_planes >= 2 ? 1 : 0;
   return p;
 }
 
@@ -2576,6 +2578,15 @@ int xpgb_set_device_formats(xpgb_ctx* h, const uint8_t* formats) {
     CK(cudaDeviceSynchronize());
     c->tfmt.assign(formats, formats + nt);
     if (c->codec) stage_device_tier(c);
+  });
+}
+
+int xpgb_set_activation_planes(xpgb_ctx* h, int32_t planes) {
+  return guard([&] {
+    Ctx* c = &h->c;
+    if (c->sess && c->sess->active) XFAIL(XPGB_ERR, "cannot change the activation planes during a session");
+    if (planes != 1 && planes != 2) XFAIL(XPGB_ERR_OUT_OF_RANGE, "activation planes %d: need 1 or 2", planes);
+    c->act_planes = planes;
   });
 }
 

@@ -179,6 +179,11 @@ class Context:
         (True / 1); 2 = only FX4 records in place, Huffman records decoded into the ring."""
         call("xpgb_set_fused_decode", self._h, int(on))
 
+    def set_activation_planes(self, planes: int) -> None:
+        """Activation planes of the decode-sized GEMMs: 2 (hi + lo, fp32-like; default) or 1
+        (bf16 activations, half the MMAs) -- xpgb_set_activation_planes."""
+        call("xpgb_set_activation_planes", self._h, int(planes))
+
     def set_stage_buffers(self, n: int) -> None:
         """Staging ring of the compressed host tier: ``n`` buffers per kind (link run-ahead)."""
         call("xpgb_set_stage_buffers", self._h, int(n))

@@ -242,3 +242,34 @@ def test_device_formats_rejects_bad_entries(X):
     rep = runner.run(1, acts=x.copy())
     base = X.resident_baseline(1, spec, container, fwd, acts=x.copy())
     assert rep.page_fault is None and np.asarray(rep.final_activations).tobytes() == np.asarray(base).tobytes()
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_single_activation_plane_mode(X, fused):
+    """xpgb_set_activation_planes(1): the decode-sized GEMMs multiply the bf16 hi plane only.
+    Streamed (FX4 device tier, read in place or decoded into the ring) == resident in that mode,
+    byte for byte; against the two-plane result it stays well inside the 1e-2 tolerance."""
+    import torch
+
+    spec = X.ModelSpec(2, 8, 256, 512)
+    T = 40
+    fwd = X.ForwardSpec(T, 2, 7)
+    container = X.generate_synthetic_model(spec, 7)
+    backends = [X.Backend(1, X.BackendKind.COMPRESSED_DEVICE, 300e9, 1 << 50),
+                X.Backend(2, X.BackendKind.HOST_OFFLOAD, 30e9, 1 << 50)]
+    hier = X.StorageHierarchy(container, None, X.plan_placement(spec, backends, alpha=1.0), backends)
+    x = torch.from_numpy(np.random.default_rng(11).standard_normal((T, spec.hidden_dim), dtype=np.float32)).cuda()
+    model = X.ResidentModel(spec, container, max_tokens=T)
+    y2, _ = model.run(2, fwd, x.clone())
+    y2 = y2.cpu().numpy()
+    model.ctx.set_activation_planes(1)
+    y1, _ = model.run(2, fwd, x.clone())
+    y1 = y1.cpu().numpy()
+    del model
+    runner = X.StreamedRunner(spec, hier, fwd, fused_decode=fused, device_format="fx4")
+    runner.ctx.set_activation_planes(1)
+    rep = runner.run(2, acts=x.clone())
+    assert rep.page_fault is None and rep.violations == []
+    assert rep.final_activations.cpu().numpy().tobytes() == y1.tobytes()
+    rel = float(np.linalg.norm(y1 - y2) / np.linalg.norm(y2))
+    assert 0.0 < rel < 1e-2
