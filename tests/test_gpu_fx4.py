@@ -258,18 +258,20 @@ def test_single_activation_plane_mode(X, fused):
     backends = [X.Backend(1, X.BackendKind.COMPRESSED_DEVICE, 300e9, 1 << 50),
                 X.Backend(2, X.BackendKind.HOST_OFFLOAD, 30e9, 1 << 50)]
     hier = X.StorageHierarchy(container, None, X.plan_placement(spec, backends, alpha=1.0), backends)
+    # one pass over the 2-layer stack (deep synthetic stacks overflow by design)
     x = torch.from_numpy(np.random.default_rng(11).standard_normal((T, spec.hidden_dim), dtype=np.float32)).cuda()
     model = X.ResidentModel(spec, container, max_tokens=T)
-    y2, _ = model.run(2, fwd, x.clone())
+    y2, _ = model.run(1, fwd, x.clone())
     y2 = y2.cpu().numpy()
     model.ctx.set_activation_planes(1)
-    y1, _ = model.run(2, fwd, x.clone())
+    y1, _ = model.run(1, fwd, x.clone())
     y1 = y1.cpu().numpy()
     del model
     runner = X.StreamedRunner(spec, hier, fwd, fused_decode=fused, device_format="fx4")
     runner.ctx.set_activation_planes(1)
-    rep = runner.run(2, acts=x.clone())
+    rep = runner.run(1, acts=x.clone())
     assert rep.page_fault is None and rep.violations == []
     assert rep.final_activations.cpu().numpy().tobytes() == y1.tobytes()
+    assert np.isfinite(y1).all() and np.isfinite(y2).all()
     rel = float(np.linalg.norm(y1 - y2) / np.linalg.norm(y2))
     assert 0.0 < rel < 1e-2
