@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--modes", default="1,0")
     ap.add_argument("--no-profile", action="store_true", help="no per-launch events (they serialise the launches)")
+    ap.add_argument("--act-planes", type=int, default=2, choices=[1, 2])
     ap.add_argument("--device-format", default="huffman", choices=["huffman", "fx4"])
     args = ap.parse_args()
     import numpy as np
@@ -44,6 +45,7 @@ def main():
     outs = {}
     for mode in (int(m) for m in args.modes.split(",")):
         runner = X.StreamedRunner(spec, hier, fwd, fused_decode=bool(mode), device_format=args.device_format)
+        runner.ctx.set_activation_planes(args.act_planes)
         runner.run(1, acts=x.clone())
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
