@@ -174,11 +174,15 @@ def plan_residency(N: int, L: int, eb: float, ceb: float, budget_bytes: float, *
         room = cap - ring * eb - p * eb
         # with every streamed expert on the device tier nothing crosses the link, and the
         # codec's staging buffers and host chunk index (overhead_bytes) are released
-        if (total - p) * dceb <= room + overhead_bytes:
+        all_device = (total - p) * dceb <= room + overhead_bytes
+        if all_device:
             room = max(room, (total - p) * dceb)
         if room < 0:
             continue
-        d = int(min(total - p, room // dceb))
+        # all_device: place every streamed expert (room // dceb can round (total - p) * dceb / dceb
+        # down to total - p - 1, leaving one host expert whose overhead the room did not charge:
+        # Qwen3 x 48 layers at 80% ran at a 0.819 footprint)
+        d = total - p if all_device else int(min(total - p, room // dceb))
         link = (total - p - d) * ceb
         decode = (total - p) * eb
         sm = (total - p - d) * eb / b_dec + d * eb / bdev + t_compute * (1.0 - (d / total if dev_fused else 0.0))
